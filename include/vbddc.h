@@ -1,0 +1,156 @@
+/*
+ * vbddc.h -- C ABI of the B200-native BDDC-preconditioned CG for the 3D divergence-free
+ * VEM discretisation of Stokes (arXiv 2304.09770).  `P:n` = PAPER.md line n.
+ *
+ * Call sequence:  vb_setup -> vb_factor -> vb_pcg_solve (repeatable)
+ *                                   -> vb_destroy.
+ * All functions return vb_status; no C++ exception or longjmp crosses the ABI.  On failure
+ * vb_last_error(ctx) (or vb_last_error(NULL) for failures before a context exists) returns a
+ * NUL-terminated message naming the failing subdomain/entity where applicable.
+ * A context is single-threaded (one driving call at a time) and bound to one CUDA device.
+ * All arithmetic of the method runs in the library's sm_100a kernels; nothing here falls back
+ * to the CPU.
+ */
+#ifndef VBDDC_H
+#define VBDDC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vb_ctx vb_ctx; /* opaque; one per rank / GPU */
+
+typedef enum {
+  VB_OK = 0,
+  VB_EINVAL = 1,      /* bad argument (message says which)                                  */
+  VB_ESTATE = 2,      /* call out of order (setup -> factor -> solve)                       */
+  VB_ENOMEM = 3,      /* device allocation failed                                           */
+  VB_ECUDA = 4,       /* CUDA runtime error                                                 */
+  VB_ENCCL = 5,       /* NCCL error                                                         */
+  VB_ESINGULAR = 6,   /* zero/wrong-sign pivot in a local, deluxe or coarse factorisation   */
+  VB_EBREAKDOWN = 7,  /* p^T S p <= 0 or r^T z <= 0: iterate left the benign space */
+  VB_ENOTCONV = 8     /* maxit reached ("NC"); x holds the last iterate            */
+} vb_status;
+
+/* General polyhedral mesh.  Host arrays, copied by vb_setup (borrowed only for the
+ * duration of the call).  Face loops must be planar; cell_face_sign[j] = +1 iff the right-hand
+ * normal of the loop of cell_face[j] points out of the cell.  face_on_dirichlet = 1 marks
+ * boundary faces (homogeneous Dirichlet after lifting, Eq.(ContinuousProblem)). */
+typedef struct {
+  int32_t k;                       /* VEM degree: 2 or 3                         */
+  int64_t n_vertices; const double *xyz;              /* [n_vertices][3]                      */
+  int64_t n_faces; const int64_t *face_ptr; const int64_t *face_vtx;   /* CSR vertex loops    */
+  int64_t n_cells; const int64_t *cell_ptr; const int64_t *cell_face;  /* CSR face lists      */
+  const int8_t *cell_face_sign;
+  const uint8_t *face_on_dirichlet;
+} vb_mesh;
+
+/* Primal constraints per interface entity and scaling. */
+enum { VB_DELUXE = 0, VB_MULTIPLICITY = 1 };
+typedef struct {
+  int32_t vertex, edge_avg, face_avg, face_flux;   /* booleans                              */
+  double adaptive_tau;   /* 0 = off; else add face GEVP eigenvectors with lambda < 1/tau */
+  int32_t scaling;       /* VB_DELUXE | VB_MULTIPLICITY                                       */
+  double svd_rel_tol;    /* constraint filter; <= 0 means 1e-10                       */
+} vb_constraints;
+
+/* Distribution: one rank per GPU; ranks own contiguous sets of subdomains. nranks = 1 needs no
+ * NCCL id.  `stream` is a cudaStream_t owned by the caller (torch); the library works on it. */
+typedef struct {
+  int32_t rank, nranks, device;
+  const void *nccl_unique_id;      /* 128 bytes from vb_nccl_unique_id on rank 0, or NULL     */
+  void *stream;
+} vb_dist;
+
+/* Analytic problem data evaluated by the library's kernels (BASELINE.json configs).
+ *  kind 0 = manufactured: u = curl(sin(pi x)sin(pi y)sin(pi z)(1,1,1)), p = sin(2 pi x)cos(pi y)z,
+ *           f = (3 pi^2 nu_K / 2) u - grad p, boundary data lifted;
+ *  kind 1 = multi-sinker force f = (0,0,beta(chi-1)) with sinker centres c_i, homogeneous BC. */
+typedef struct {
+  int32_t kind;
+  int32_t n_sinkers; const double *centres;        /* [n_sinkers][3]                         */
+  double delta, omega, beta;
+} vb_problem;
+
+typedef struct {
+  int32_t iterations, converged;
+  double r0_norm, r_final_norm, rel_residual;   /* interface residual ||r||_2        */
+  double lambda_min, lambda_max, kappa;         /* Lanczos from the CG coefficients  */
+  double true_rel_residual;                     /* ||b - K x|| / ||b|| by the element operator */
+  double t_setup_s, t_factor_s, t_solve_s;
+  double bytes_per_iter_model, flux_violation_max;
+  int32_t n_primal, n_coarse;
+  int64_t n_dofs_paper;                         /* nDofs as counted in T2-T4                   */
+} vb_report;
+
+/* rank 0: fills 128 bytes to broadcast with torch.distributed before vb_setup. */
+vb_status vb_nccl_unique_id(void *out128);
+
+/* Build the context: topology, DOF numbering, box-free general subdomain
+ * classification, interface entities, and the VEM element matrices A^K, B^K computed
+ * on the device from the geometry and the per-cell viscosity.
+ *   cell_subdomain[n_cells]  subdomain id per cell (0..n_subdomains-1)
+ *   subdomain_rank[n_subdomains] owning rank (NULL = all rank 0)
+ *   cell_viscosity[n_cells]  nu_K > 0                                               */
+vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
+                   const int32_t *subdomain_rank, const vb_constraints *cons,
+                   const double *cell_viscosity, const vb_dist *dist, vb_ctx **out);
+
+/* Bring-up/testing variant: identical, but the element matrices are supplied (host, row-major,
+ * per cell in the library's local DOF order -- see vb_cell_local_dofs) instead of generated. */
+vb_status vb_setup_from_elements(const vb_mesh *mesh, const int32_t *cell_subdomain,
+                                 int32_t n_subdomains, const int32_t *subdomain_rank,
+                                 const vb_constraints *cons, const double *cell_viscosity,
+                                 const vb_dist *dist, const int64_t *elem_ptr_A,
+                                 const double *elem_A, const int64_t *elem_ptr_B,
+                                 const double *elem_B, vb_ctx **out);
+
+/* Factorisations feeding the hot path: subdomain Dirichlet LDL^T and
+ * interface Schur S_G (Eq.(firstSchur)), change of basis, dual Schur inverse, coarse
+ * basis, deluxe operators, adaptive enrichment, coarse saddle inverse. */
+vb_status vb_factor(vb_ctx *ctx);
+
+/* Right-hand side of Eq.(DiscProblem) on the free DOFs (velocity free DOFs in global order, then
+ * pressure): load (f_h, v) = int Pi^0_k f . v (Eq.(discreteF)) minus the lifted
+ * boundary data.  rhs_dev: device buffer of vb_num_free_dofs doubles (caller-owned).          */
+vb_status vb_build_rhs(vb_ctx *ctx, const vb_problem *prob, double *rhs_dev);
+
+/* PCG on the interface saddle problem Eq.(globInt) preconditioned by
+ * M^-1 = R~_D^T S~^-1 R~_D (Eq.(BDDCprec)), x0 = 0, stop at ||r|| <= rtol ||r0||.
+ * rhs_dev, x_dev: caller-owned device buffers in the free-DOF layout; x gets the full solution
+ * (interior back-substitution, pressure with zero global mean).  maxit <= 0 means 2000. */
+vb_status vb_pcg_solve(vb_ctx *ctx, const double *rhs_dev, double *x_dev, double rtol,
+                       int32_t maxit, vb_report *rep);
+
+/* Same, with HOST rhs/x buffers: the host<->device copies are part of the call (e2e timing). */
+vb_status vb_pcg_solve_host(vb_ctx *ctx, const double *rhs_host, double *x_host, double rtol,
+                            int32_t maxit, vb_report *rep);
+
+/* y = K x with the element-by-element saddle operator on the free DOFs (device). */
+vb_status vb_apply_operator(vb_ctx *ctx, const double *x_dev, double *y_dev);
+
+/* Parity/debug: y = S^ x (which = 0, Eq.(globInt)) or y = M^-1 x (which = 1, Eq.(BDDCprec)) on a
+ * HOST vector in original interface coordinates: the vb_interface_dofs order (entity-major),
+ * then one p_0 per subdomain.  Requires vb_factor.                                            */
+vb_status vb_debug_interface_op(vb_ctx *ctx, int32_t which, const double *in_host, double *out_host);
+/* Interface DOFs (free velocity ids) in the library's entity-major order; *n = count.
+ * ids may be NULL to query the count only.                                                     */
+vb_status vb_interface_dofs(const vb_ctx *ctx, int64_t *ids, int64_t *n);
+
+/* Queries. */
+vb_status vb_num_free_dofs(const vb_ctx *ctx, int64_t *n_vel, int64_t *n_p);
+vb_status vb_dof_layout(const vb_ctx *ctx, int64_t *global_ids);   /* free -> global DOF id    */
+vb_status vb_cell_local_dofs(const vb_ctx *ctx, int64_t cell, int64_t *vel_ids, int32_t *n_vel,
+                             int64_t *p_ids, int32_t *n_p);       /* local order -> global id  */
+vb_status vb_get_element_matrices(const vb_ctx *ctx, int64_t cell, double *A, double *B);
+vb_status vb_stats(const vb_ctx *ctx, int64_t *out16);            /* sizes: see DESIGN.md      */
+vb_status vb_kernel_times(const vb_ctx *ctx, double *ms_out, int32_t n_max, int32_t *n_out);
+const char *vb_kernel_time_name(int32_t i);
+const char *vb_last_error(const vb_ctx *ctx);
+vb_status vb_destroy(vb_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VBDDC_H */

@@ -150,7 +150,7 @@ class ElementSet:
 class GlobalSystem:
     """Assembled A, B, load, lifted rhs on the free DOFs (SURVEY O-6)."""
 
-    def __init__(self, prob, processes=None):
+    def __init__(self, prob, processes=None, u_bc=None, f_of_nu=None):
         self.prob = prob
         mesh, k = prob.mesh, prob.k
         self.dofs = dofs = GlobalDofs(mesh, k)
@@ -159,7 +159,9 @@ class GlobalSystem:
         rows, cols, vals = [], [], []
         brow, bcol, bval = [], [], []
         fvel = np.zeros(dofs.nvel)
-        if prob.kind == "manufactured":
+        if f_of_nu is not None:
+            self.f = f_of_nu
+        elif prob.kind == "manufactured":
             self.f = problems.f_manufactured
         else:
             fs = problems.f_sinker(prob.params)
@@ -178,7 +180,9 @@ class GlobalSystem:
         self.fvel = fvel
         # lifting of the exact trace; sinker: homogeneous
         uD = np.zeros(dofs.nvel)
-        if prob.kind == "manufactured":
+        if u_bc is not None:
+            uD = self.boundary_interpolant(u_bc)
+        elif prob.kind == "manufactured":
             uD = self.boundary_interpolant(problems.u_exact)
         self.uD = uD
         fr, bd = dofs.free_vel, dofs.bnd_vel

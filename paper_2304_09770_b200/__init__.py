@@ -1,0 +1,272 @@
+"""B200-native BDDC-preconditioned CG for the 3D divergence-free VEM Stokes system (arXiv 2304.09770).
+
+Thin ctypes binding of the C ABI in include/vbddc.h: argument marshalling only -- every step of
+setup/factor/solve runs in libvbddc.so's sm_100a kernels.  torch is used for device memory and the
+CUDA stream.  There is no CPU fallback: importing fails loudly if the library is missing.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvbddc.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError("libvbddc.so not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(the CUDA library is required; there is no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+VB_OK, VB_EINVAL, VB_ESTATE, VB_ENOMEM, VB_ECUDA, VB_ENCCL, VB_ESINGULAR, VB_EBREAKDOWN, VB_ENOTCONV = range(9)
+STATUS = {0: "OK", 1: "EINVAL", 2: "ESTATE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESINGULAR",
+          7: "EBREAKDOWN", 8: "ENOTCONV"}
+VB_DELUXE, VB_MULTIPLICITY = 0, 1
+
+_p = ctypes.c_void_p
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+class VBMesh(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("n_vertices", ctypes.c_int64), ("xyz", _dp),
+                ("n_faces", ctypes.c_int64), ("face_ptr", _i64p), ("face_vtx", _i64p),
+                ("n_cells", ctypes.c_int64), ("cell_ptr", _i64p), ("cell_face", _i64p),
+                ("cell_face_sign", ctypes.POINTER(ctypes.c_int8)),
+                ("face_on_dirichlet", ctypes.POINTER(ctypes.c_uint8))]
+
+
+class VBConstraints(ctypes.Structure):
+    _fields_ = [("vertex", ctypes.c_int32), ("edge_avg", ctypes.c_int32), ("face_avg", ctypes.c_int32),
+                ("face_flux", ctypes.c_int32), ("adaptive_tau", ctypes.c_double),
+                ("scaling", ctypes.c_int32), ("svd_rel_tol", ctypes.c_double)]
+
+
+class VBDist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("nccl_unique_id", _p), ("stream", _p)]
+
+
+class VBProblem(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("n_sinkers", ctypes.c_int32), ("centres", _dp),
+                ("delta", ctypes.c_double), ("omega", ctypes.c_double), ("beta", ctypes.c_double)]
+
+
+class VBReport(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("r0_norm", ctypes.c_double), ("r_final_norm", ctypes.c_double), ("rel_residual", ctypes.c_double),
+                ("lambda_min", ctypes.c_double), ("lambda_max", ctypes.c_double), ("kappa", ctypes.c_double),
+                ("true_rel_residual", ctypes.c_double),
+                ("t_setup_s", ctypes.c_double), ("t_factor_s", ctypes.c_double), ("t_solve_s", ctypes.c_double),
+                ("bytes_per_iter_model", ctypes.c_double), ("flux_violation_max", ctypes.c_double),
+                ("n_primal", ctypes.c_int32), ("n_coarse", ctypes.c_int32), ("n_dofs_paper", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+_vb_setup = _sig("vb_setup", ctypes.c_int, [ctypes.POINTER(VBMesh), _i32p, ctypes.c_int32, _i32p,
+                                           ctypes.POINTER(VBConstraints), _dp, ctypes.POINTER(VBDist), ctypes.POINTER(_p)])
+_vb_setup_el = _sig("vb_setup_from_elements", ctypes.c_int,
+                    [ctypes.POINTER(VBMesh), _i32p, ctypes.c_int32, _i32p, ctypes.POINTER(VBConstraints), _dp,
+                     ctypes.POINTER(VBDist), _i64p, _dp, _i64p, _dp, ctypes.POINTER(_p)])
+_vb_factor = _sig("vb_factor", ctypes.c_int, [_p])
+_vb_build_rhs = _sig("vb_build_rhs", ctypes.c_int, [_p, ctypes.POINTER(VBProblem), _p])
+_vb_pcg_solve = _sig("vb_pcg_solve", ctypes.c_int, [_p, _p, _p, ctypes.c_double, ctypes.c_int32, ctypes.POINTER(VBReport)])
+_vb_pcg_solve_host = _sig("vb_pcg_solve_host", ctypes.c_int,
+                          [_p, _dp, _dp, ctypes.c_double, ctypes.c_int32, ctypes.POINTER(VBReport)])
+_vb_apply_operator = _sig("vb_apply_operator", ctypes.c_int, [_p, _p, _p])
+_vb_num_free_dofs = _sig("vb_num_free_dofs", ctypes.c_int, [_p, _i64p, _i64p])
+_vb_dof_layout = _sig("vb_dof_layout", ctypes.c_int, [_p, _i64p])
+_vb_cell_local_dofs = _sig("vb_cell_local_dofs", ctypes.c_int, [_p, ctypes.c_int64, _i64p, _i32p, _i64p, _i32p])
+_vb_get_element_matrices = _sig("vb_get_element_matrices", ctypes.c_int, [_p, ctypes.c_int64, _dp, _dp])
+_vb_stats = _sig("vb_stats", ctypes.c_int, [_p, _i64p])
+_vb_last_error = _sig("vb_last_error", ctypes.c_char_p, [_p])
+_vb_destroy = _sig("vb_destroy", ctypes.c_int, [_p])
+_vb_nccl_unique_id = _sig("vb_nccl_unique_id", ctypes.c_int, [_p])
+_vb_debug_iop = _sig("vb_debug_interface_op", ctypes.c_int, [_p, ctypes.c_int32, _dp, _dp])
+_vb_interface_dofs = _sig("vb_interface_dofs", ctypes.c_int, [_p, _i64p, _i64p])
+
+EXPORTED = ["vb_nccl_unique_id", "vb_setup", "vb_setup_from_elements", "vb_factor", "vb_build_rhs",
+            "vb_pcg_solve", "vb_pcg_solve_host", "vb_apply_operator", "vb_debug_interface_op",
+            "vb_interface_dofs", "vb_num_free_dofs", "vb_dof_layout",
+            "vb_cell_local_dofs", "vb_get_element_matrices", "vb_stats", "vb_kernel_times",
+            "vb_kernel_time_name", "vb_last_error", "vb_destroy"]
+
+
+class VBError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+
+
+def _arr(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _ptr(a, ctype):
+    return a.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+def _cons(constraints):
+    c = dict(vertex=1, edge_avg=1, face_avg=1, face_flux=1, adaptive_tau=0.0, scaling=VB_DELUXE, svd_rel_tol=1e-10)
+    if constraints:
+        c.update({k: v for k, v in constraints.items() if k in c})
+        if constraints.get("all_primal"):
+            c["svd_rel_tol"] = -1.0
+    return VBConstraints(int(c["vertex"]), int(c["edge_avg"]), int(c["face_avg"]), int(c["face_flux"]),
+                         float(c["adaptive_tau"]), int(c["scaling"]), float(c["svd_rel_tol"]))
+
+
+class Context:
+    """One vb_ctx (one GPU).  Call factor(), then build_rhs()/pcg_solve() any number of times."""
+
+    def __init__(self, mesh, k, cell_subdomain, n_subdomains, viscosity, constraints=None, stream=None,
+                 device=0, elements=None):
+        import torch
+        self._keep = []
+        xyz = _arr(mesh.xyz, np.float64)
+        fp, fv = _arr(mesh.face_ptr, np.int64), _arr(mesh.face_vtx, np.int64)
+        cp, cf = _arr(mesh.cell_ptr, np.int64), _arr(mesh.cell_face, np.int64)
+        cs = _arr(mesh.cell_face_sign, np.int8)
+        fb = _arr(mesh.face_on_boundary, np.uint8)
+        self._keep += [xyz, fp, fv, cp, cf, cs, fb]
+        m = VBMesh(int(k), xyz.shape[0], _ptr(xyz, ctypes.c_double), fp.size - 1, _ptr(fp, ctypes.c_int64),
+                   _ptr(fv, ctypes.c_int64), cp.size - 1, _ptr(cp, ctypes.c_int64), _ptr(cf, ctypes.c_int64),
+                   _ptr(cs, ctypes.c_int8), _ptr(fb, ctypes.c_uint8))
+        sub = _arr(cell_subdomain, np.int32)
+        nu = _arr(viscosity, np.float64)
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        dist = VBDist(0, 1, int(device), None, ctypes.c_void_p(stream.cuda_stream))
+        cons = _cons(constraints)
+        h = _p()
+        if elements is None:
+            st = _vb_setup(ctypes.byref(m), _ptr(sub, ctypes.c_int32), int(n_subdomains), None, ctypes.byref(cons),
+                           _ptr(nu, ctypes.c_double), ctypes.byref(dist), ctypes.byref(h))
+        else:
+            pa, A, pb, B = [_arr(x, t) for x, t in zip(elements, (np.int64, np.float64, np.int64, np.float64))]
+            st = _vb_setup_el(ctypes.byref(m), _ptr(sub, ctypes.c_int32), int(n_subdomains), None, ctypes.byref(cons),
+                              _ptr(nu, ctypes.c_double), ctypes.byref(dist), _ptr(pa, ctypes.c_int64),
+                              _ptr(A, ctypes.c_double), _ptr(pb, ctypes.c_int64), _ptr(B, ctypes.c_double),
+                              ctypes.byref(h))
+        if st != VB_OK:
+            raise VBError(st, _vb_last_error(None).decode())
+        self._h = h
+        nv, npr = ctypes.c_int64(), ctypes.c_int64()
+        _vb_num_free_dofs(self._h, ctypes.byref(nv), ctypes.byref(npr))
+        self.n_vel, self.n_p = nv.value, npr.value
+        self.n_free = self.n_vel + self.n_p
+
+    def _check(self, st):
+        if st != VB_OK:
+            raise VBError(st, _vb_last_error(self._h).decode())
+
+    def factor(self):
+        self._check(_vb_factor(self._h))
+
+    def build_rhs(self, problem, out):
+        """problem: dict(kind='manufactured'|'sinker', centres, delta, omega, beta); out: cuda float64 tensor."""
+        if problem.get("kind", "manufactured") == "sinker":
+            cen = _arr(problem["centres"], np.float64)
+            self._keep.append(cen)
+            p = VBProblem(1, cen.shape[0], _ptr(cen, ctypes.c_double), problem["delta"], problem["omega"], problem["beta"])
+        else:
+            p = VBProblem(0, 0, None, 0.0, 0.0, 0.0)
+        self._check(_vb_build_rhs(self._h, ctypes.byref(p), ctypes.c_void_p(out.data_ptr())))
+        return out
+
+    def pcg_solve(self, rhs, x, rtol=1e-10, maxit=2000, raise_on_error=True):
+        rep = VBReport()
+        st = _vb_pcg_solve(self._h, ctypes.c_void_p(rhs.data_ptr()), ctypes.c_void_p(x.data_ptr()), float(rtol),
+                           int(maxit), ctypes.byref(rep))
+        d = rep.as_dict()
+        d["status"] = STATUS[st]
+        if raise_on_error and st != VB_OK:
+            self._check(st)
+        return d
+
+    def pcg_solve_host(self, rhs_host, x_host, rtol=1e-10, maxit=2000):
+        rep = VBReport()
+        self._check(_vb_pcg_solve_host(self._h, _ptr(rhs_host, ctypes.c_double), _ptr(x_host, ctypes.c_double),
+                                       float(rtol), int(maxit), ctypes.byref(rep)))
+        return rep.as_dict()
+
+    def apply_operator(self, x, y):
+        self._check(_vb_apply_operator(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr())))
+        return y
+
+    def interface_dofs(self):
+        n = ctypes.c_int64()
+        self._check(_vb_interface_dofs(self._h, None, ctypes.byref(n)))
+        ids = np.zeros(n.value, np.int64)
+        self._check(_vb_interface_dofs(self._h, _ptr(ids, ctypes.c_int64), ctypes.byref(n)))
+        return ids
+
+    def interface_op(self, which, vec):
+        """which: 'S' (interface saddle operator) or 'M' (BDDC preconditioner); original coordinates."""
+        v = _arr(vec, np.float64)
+        out = np.zeros_like(v)
+        self._check(_vb_debug_iop(self._h, 0 if which == "S" else 1, _ptr(v, ctypes.c_double),
+                                  _ptr(out, ctypes.c_double)))
+        return out
+
+    def dof_layout(self):
+        ids = np.zeros(self.n_free, np.int64)
+        self._check(_vb_dof_layout(self._h, _ptr(ids, ctypes.c_int64)))
+        return ids
+
+    def cell_local_dofs(self, cell):
+        v = np.zeros(512, np.int64); p = np.zeros(64, np.int64)
+        nv, npr = ctypes.c_int32(), ctypes.c_int32()
+        self._check(_vb_cell_local_dofs(self._h, int(cell), _ptr(v, ctypes.c_int64), ctypes.byref(nv),
+                                        _ptr(p, ctypes.c_int64), ctypes.byref(npr)))
+        return v[:nv.value].copy(), p[:npr.value].copy()
+
+    def element_matrices(self, cell):
+        v, p = self.cell_local_dofs(cell)
+        A = np.zeros((v.size, v.size)); B = np.zeros((p.size, v.size))
+        self._check(_vb_get_element_matrices(self._h, int(cell), _ptr(A, ctypes.c_double), _ptr(B, ctypes.c_double)))
+        return A, B
+
+    def stats(self):
+        o = np.zeros(16, np.int64)
+        self._check(_vb_stats(self._h, _ptr(o, ctypes.c_int64)))
+        keys = ["n_dofs_paper", "n_free_vel", "n_pres", "n_sub", "n_ent", "n_gamma", "n_primal", "n_coarse",
+                "n_delta", "max_n", "max_nG", "max_nd", "n_edges", "bytes_per_iter", "nv_max", "n_colors"]
+        return dict(zip(keys, o.tolist()))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _vb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def problem_args(prob):
+    """Library problem descriptor for a synthetic.Problem."""
+    if prob.kind == "sinker":
+        return dict(kind="sinker", centres=prob.params["centres"], delta=prob.params["delta"],
+                    omega=prob.params["omega"], beta=prob.params["beta"])
+    return dict(kind="manufactured")
+
+
+def context_for(prob, elements=None, constraints=None, stream=None):
+    cons = dict(prob.constraints)
+    if constraints:
+        cons.update(constraints)
+    return Context(prob.mesh, prob.k, prob.cell_subdomain, int(prob.cell_subdomain.max()) + 1, prob.nu_cell,
+                   constraints=cons, stream=stream, elements=elements)

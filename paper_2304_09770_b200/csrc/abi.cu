@@ -1,0 +1,428 @@
+// C ABI (include/vbddc.h) and the host layout of device data.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include "setup.h"
+
+using namespace vb;
+
+static thread_local std::string g_last_error;
+
+static vb_status fail(vb_ctx *c, const Error &e) {
+  g_last_error = e.msg;
+  if (c) c->err = e.msg;
+  return e.st;
+}
+
+#define ABI_GUARD(ctx, ...)                                                                     \
+  try {                                                                                         \
+    __VA_ARGS__;                                                                                \
+  } catch (const Error &e) {                                                                    \
+    return fail(ctx, e);                                                                        \
+  } catch (const std::exception &e) {                                                          \
+    return fail(ctx, Error{VB_EINVAL, e.what()});                                               \
+  }                                                                                             \
+  return VB_OK;
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+namespace vb {
+
+// ------------------------------------------------------------------ layout before the ranks
+void layout_phase_a(vb_ctx *c) {
+  const int N = c->N;
+  cudaStream_t s = c->stream;
+  c->h_sub.assign(N, SubDev{});
+  std::vector<int> sub_cells;
+  int64_t K = 0, G = 0, P = 0, I = 0, Dn = 0, X = 0;
+  for (int i = 0; i < N; ++i) {
+    Sub &S = c->subs[i];
+    SubDev &D = c->h_sub[i];
+    D.nI = S.nI; D.nP = S.nP; D.nG = S.nG; D.nD = S.nD; D.n = S.n;
+    D.cell_begin = sub_cells.size();
+    for (int cell : S.cells) sub_cells.push_back(cell);
+    D.cell_end = sub_cells.size();
+    D.off_K = K; K += (int64_t)S.n * S.n;
+    D.off_G = G; G += S.nG;
+    D.off_P = P; P += S.nP;
+    D.off_I = I; I += S.nI;
+    D.off_Dn = Dn; Dn += S.nD;
+    D.off_X = X; X += (int64_t)S.nG * S.nG;
+    double vol = 0, nus = 0;
+    for (int cell : S.cells) { vol += c->cellgeo[(int64_t)cell * c->geo_stride]; nus += c->nu[cell]; }
+    D.vol = vol;
+    S.vol = vol;
+    D.gamma = 1.0 / ((nus / std::max<size_t>(S.cells.size(), 1)) * vol);
+  }
+  c->len_K = K; c->len_G = G; c->len_P = P; c->len_I = I; c->len_Dn = Dn; c->len_X = X;
+  // entity-major slots
+  c->h_slot.clear();
+  c->h_ent.assign(c->ents.size(), EntDev{});
+  int64_t gam = 0;
+  std::vector<std::vector<int>> sub_slot(N);
+  for (size_t e = 0; e < c->ents.size(); ++e) {
+    Entity &E = c->ents[e];
+    EntDev &D = c->h_ent[e];
+    D.n = E.n; D.kind = E.kind; D.nsides = E.sharers.size(); D.side_begin = c->h_slot.size();
+    D.off_gam = gam; gam += E.n;
+    for (int m : E.sharers) {
+      Sub &S = c->subs[m];
+      int j = std::lower_bound(S.ents.begin(), S.ents.end(), (int)e) - S.ents.begin();
+      SlotDev sl{};
+      sl.sub = m; sl.ent = e; sl.n = E.n; sl.offG = S.ent_offG[j];
+      sub_slot[m].push_back(c->h_slot.size());
+      c->h_slot.push_back(sl);
+    }
+  }
+  c->h_sub_slots.clear();
+  for (int i = 0; i < N; ++i) {
+    // subdomain slot order = its entity order (sorted by entity id = slot creation order)
+    c->h_sub[i].slot_begin = c->h_sub_slots.size();
+    for (int q : sub_slot[i]) c->h_sub_slots.push_back(q);
+    c->h_sub[i].slot_end = c->h_sub_slots.size();
+  }
+  // index maps
+  std::vector<int64_t> Ifree, Pglob, Gfree, gamfree;
+  std::vector<double> cvec, mvec;
+  for (int i = 0; i < N; ++i) {
+    Sub &S = c->subs[i];
+    Ifree.insert(Ifree.end(), S.I.begin(), S.I.end());
+    Pglob.insert(Pglob.end(), S.P.begin(), S.P.end());
+    for (int e : S.ents) Gfree.insert(Gfree.end(), c->ents[e].dofs.begin(), c->ents[e].dofs.end());
+    for (int64_t p : S.P) {
+      int64_t cell = p / c->np, a = p % c->np;
+      cvec.push_back(c->cellgeo[cell * c->geo_stride + 5 + a]);
+      mvec.push_back(a == 0 ? c->cellgeo[cell * c->geo_stride] : 0.0);
+    }
+  }
+  for (auto &E : c->ents) gamfree.insert(gamfree.end(), E.dofs.begin(), E.dofs.end());
+  c->d_subI_free.upload(Ifree, s);
+  c->d_subP_glob.upload(Pglob, s);
+  c->d_subG_free.upload(Gfree, s);
+  c->d_gam_free.upload(gamfree, s);
+  c->d_cvec.upload(cvec, s);
+  c->d_mvec.upload(mvec, s);
+  c->d_sub_cells.upload(sub_cells, s);
+  c->d_sub_slots.upload(c->h_sub_slots, s);
+  // cell -> subdomain-matrix positions
+  const int stride = c->nv_max + c->np;
+  std::vector<int> loc((size_t)c->nK * stride, -1);
+  std::vector<int64_t> posI(c->n_free_vel, -1);
+  for (int i = 0; i < N; ++i) {
+    Sub &S = c->subs[i];
+    for (int j = 0; j < S.nI; ++j) posI[S.I[j]] = j;
+    for (int cell : S.cells) {
+      int *L = &loc[(size_t)cell * stride];
+      for (int64_t j = c->cell_l2g_ptr[cell]; j < c->cell_l2g_ptr[cell + 1]; ++j) {
+        int64_t f = c->vel2free[c->cell_l2g[j]];
+        int q = j - c->cell_l2g_ptr[cell];
+        if (f < 0) continue;
+        if (posI[f] >= 0 && c->cell_sub[cell] == i && std::binary_search(S.I.begin(), S.I.end(), f)) {
+          L[q] = posI[f];
+        } else {
+          // interface: find the entity of f among this subdomain's entities
+          for (size_t t = 0; t < S.ents.size(); ++t) {
+            const Entity &E = c->ents[S.ents[t]];
+            auto it = std::lower_bound(E.dofs.begin(), E.dofs.end(), f);
+            if (it != E.dofs.end() && *it == f) { L[q] = S.nD + S.ent_offG[t] + (int)(it - E.dofs.begin()); break; }
+          }
+          VB_REQUIRE(L[q] >= 0, VB_EINVAL, "internal: interface dof not found in its subdomain");
+        }
+      }
+      int64_t p0 = std::lower_bound(S.P.begin(), S.P.end(), (int64_t)cell * c->np) - S.P.begin();
+      for (int a = 0; a < c->np; ++a) L[c->nv_max + a] = S.nI + p0 + a;
+    }
+  }
+  c->d_cell_loc.upload(loc, s);
+  // greedy coloring of the subdomain adjacency (shared entities) for the coarse assembly
+  std::vector<std::vector<int>> adj(N);
+  for (auto &E : c->ents)
+    for (int a : E.sharers)
+      for (int b : E.sharers)
+        if (a != b) adj[a].push_back(b);
+  c->ncolors = 0;
+  for (int i = 0; i < N; ++i) {
+    std::vector<char> used(64, 0);
+    for (int j : adj[i]) if (j < i && c->subs[j].color < 64) used[c->subs[j].color] = 1;
+    int col = 0;
+    while (used[col]) ++col;
+    c->subs[i].color = col;
+    c->ncolors = std::max(c->ncolors, col + 1);
+  }
+  c->d_sub.upload(c->h_sub, s);
+  c->d_slot.upload(c->h_slot, s);
+  c->d_ent.upload(c->h_ent, s);
+  VB_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------------ maps needing the ranks
+void build_transformed_maps(vb_ctx *c) {
+  std::vector<int64_t> loc2x(c->len_G, -1), pig(std::max<int64_t>(c->len_Pi, 1), -1);
+  c->max_npi = 0;
+  for (int i = 0; i < c->N; ++i) {
+    const SubDev &S = c->h_sub[i];
+    c->max_npi = std::max(c->max_npi, S.npi);
+    for (int q = S.slot_begin; q < S.slot_end; ++q) {
+      const SlotDev &sl = c->h_slot[c->h_sub_slots[q]];
+      const EntDev &E = c->h_ent[sl.ent];
+      for (int j = 0; j < sl.nd; ++j) loc2x[S.off_G + sl.offD + j] = E.off_xd + j;
+      for (int j = 0; j < sl.r; ++j) {
+        loc2x[S.off_G + S.nd + sl.offPi + j] = c->n_delta_glob + E.off_pi + j;
+        pig[S.off_Pi + sl.offPi + j] = E.off_pi + j;
+      }
+    }
+  }
+  c->d_loc2x.upload(loc2x, c->stream);
+  c->d_pi_glob.upload(pig, c->stream);
+  VB_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// ------------------------------------------------------------------ common setup
+static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, int32_t nsub,
+                         const vb_constraints *cons, const double *nu, const vb_dist *dist) {
+  VB_REQUIRE(m && cell_sub && nu && cons, VB_EINVAL, "null argument");
+  VB_REQUIRE(m->k == 2 || m->k == 3, VB_EINVAL, "k must be 2 or 3");
+  VB_REQUIRE(nsub >= 1, VB_EINVAL, "n_subdomains must be >= 1");
+  c->k = m->k;
+  c->cons = *cons;
+  c->debug = getenv("VB_DEBUG") ? atoi(getenv("VB_DEBUG")) : 0;
+  if (dist) {
+    c->rank = dist->rank; c->nranks = dist->nranks; c->device = dist->device;
+    c->stream = (cudaStream_t)dist->stream;
+  }
+  VB_REQUIRE(c->nranks == 1, VB_EINVAL, "multi-rank contexts are not enabled in this build (nranks must be 1)");
+  VB_CUDA(cudaSetDevice(c->device));
+  build_topology(c, m);
+  c->nu.assign(nu, nu + c->nK);
+  for (int64_t K = 0; K < c->nK; ++K) VB_REQUIRE(c->nu[K] > 0, VB_EINVAL, "viscosity must be positive (P:108)");
+  build_subdomains(c, cell_sub, nsub);
+  cudaStream_t s = c->stream;
+  c->d_xyz.upload(c->xyz, s);
+  c->d_topo.upload(c->cell_topo, s);
+  c->d_nu.upload(c->nu, s);
+  c->d_cell_nv.upload(c->cell_nv, s);
+  c->d_vel2free.upload(c->vel2free, s);
+  std::vector<int64_t> l2g((size_t)c->nK * c->nv_max, -1);
+  for (int64_t K = 0; K < c->nK; ++K)
+    for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) l2g[K * c->nv_max + (j - c->cell_l2g_ptr[K])] = c->cell_l2g[j];
+  c->d_cell_l2g.upload(l2g, s);
+  cell_geometry_device(c);
+  c->d_cellgeo.download(c->cellgeo, s);
+  VB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace vb
+
+// ------------------------------------------------------------------ ABI
+extern "C" {
+
+vb_status vb_nccl_unique_id(void *out128) {
+  if (!out128) return VB_EINVAL;
+  g_last_error = "NCCL is not enabled in this build (single-rank contexts only)";
+  return VB_ENCCL;
+}
+
+vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
+                   const int32_t *subdomain_rank, const vb_constraints *cons, const double *cell_viscosity,
+                   const vb_dist *dist, vb_ctx **out) {
+  if (!out) return VB_EINVAL;
+  *out = nullptr;
+  vb_ctx *c = new vb_ctx();
+  try {
+    double t0 = now_s();
+    common_setup(c, mesh, cell_subdomain, n_subdomains, cons, cell_viscosity, dist);
+    element_matrices_device(c);
+    layout_phase_a(c);
+    c->t_setup = now_s() - t0;
+    c->state = 1;
+  } catch (const Error &e) {
+    vb_status st = fail(c, e);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return VB_OK;
+}
+
+vb_status vb_setup_from_elements(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
+                                 const int32_t *subdomain_rank, const vb_constraints *cons,
+                                 const double *cell_viscosity, const vb_dist *dist, const int64_t *elem_ptr_A,
+                                 const double *elem_A, const int64_t *elem_ptr_B, const double *elem_B,
+                                 vb_ctx **out) {
+  if (!out) return VB_EINVAL;
+  *out = nullptr;
+  vb_ctx *c = new vb_ctx();
+  try {
+    double t0 = now_s();
+    common_setup(c, mesh, cell_subdomain, n_subdomains, cons, cell_viscosity, dist);
+    VB_REQUIRE(elem_ptr_A && elem_A && elem_ptr_B && elem_B, VB_EINVAL, "null element arrays");
+    const int nvm = c->nv_max, np = c->np;
+    std::vector<double> A((size_t)c->nK * nvm * nvm, 0.0), B((size_t)c->nK * np * nvm, 0.0);
+    for (int64_t K = 0; K < c->nK; ++K) {
+      const int nv = c->cell_nv[K];
+      VB_REQUIRE(elem_ptr_A[K + 1] - elem_ptr_A[K] == (int64_t)nv * nv, VB_EINVAL, "element A size mismatch");
+      VB_REQUIRE(elem_ptr_B[K + 1] - elem_ptr_B[K] == (int64_t)np * nv, VB_EINVAL, "element B size mismatch");
+      std::copy(elem_A + elem_ptr_A[K], elem_A + elem_ptr_A[K + 1], A.begin() + (size_t)K * nvm * nvm);
+      std::copy(elem_B + elem_ptr_B[K], elem_B + elem_ptr_B[K + 1], B.begin() + (size_t)K * np * nvm);
+    }
+    c->d_elA.upload(A, c->stream);
+    c->d_elB.upload(B, c->stream);
+    layout_phase_a(c);
+    c->t_setup = now_s() - t0;
+    c->state = 1;
+  } catch (const Error &e) {
+    vb_status st = fail(c, e);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return VB_OK;
+}
+
+vb_status vb_factor(vb_ctx *c) {
+  if (!c) return VB_EINVAL;
+  if (c->state < 1) return fail(c, Error{VB_ESTATE, "vb_factor before vb_setup"});
+  ABI_GUARD(c, {
+    double t0 = now_s();
+    factor_device(c);
+    prepare_solve(c);
+    c->t_factor = now_s() - t0;
+    c->state = 2;
+  })
+}
+
+vb_status vb_build_rhs(vb_ctx *c, const vb_problem *prob, double *rhs_dev) {
+  if (!c || !prob || !rhs_dev) return VB_EINVAL;
+  if (c->state < 1) return fail(c, Error{VB_ESTATE, "vb_build_rhs before vb_setup"});
+  ABI_GUARD(c, { build_rhs_device(c, prob, rhs_dev); })
+}
+
+vb_status vb_pcg_solve(vb_ctx *c, const double *rhs_dev, double *x_dev, double rtol, int32_t maxit, vb_report *rep) {
+  if (!c || !rhs_dev || !x_dev) return VB_EINVAL;
+  if (c->state < 2) return fail(c, Error{VB_ESTATE, "vb_pcg_solve before vb_factor"});
+  if (!(rtol > 0)) return fail(c, Error{VB_EINVAL, "rtol must be positive"});
+  if (rep) memset(rep, 0, sizeof(*rep));
+  ABI_GUARD(c, {
+    double t0 = now_s();
+    pcg_device(c, rhs_dev, x_dev, rtol, maxit > 0 ? maxit : 2000, rep);
+    if (rep) {
+      rep->t_solve_s = now_s() - t0;
+      rep->t_setup_s = c->t_setup;
+      rep->t_factor_s = c->t_factor;
+    }
+  })
+}
+
+vb_status vb_pcg_solve_host(vb_ctx *c, const double *rhs_host, double *x_host, double rtol, int32_t maxit,
+                            vb_report *rep) {
+  if (!c || !rhs_host || !x_host) return VB_EINVAL;
+  if (c->state < 2) return fail(c, Error{VB_ESTATE, "vb_pcg_solve_host before vb_factor"});
+  ABI_GUARD(c, {
+    const int64_t n = c->n_free_vel + c->npres;
+    if (c->w_hostio.n < (size_t)(2 * n)) c->w_hostio.alloc(2 * n);
+    VB_CUDA(cudaMemcpyAsync(c->w_hostio.p, rhs_host, n * 8, cudaMemcpyHostToDevice, c->stream));
+    vb_status st = vb_pcg_solve(c, c->w_hostio.p, c->w_hostio.p + n, rtol, maxit, rep);
+    if (st != VB_OK) throw Error{st, c->err};
+    VB_CUDA(cudaMemcpyAsync(x_host, c->w_hostio.p + n, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    VB_CUDA(cudaStreamSynchronize(c->stream));
+  })
+}
+
+vb_status vb_apply_operator(vb_ctx *c, const double *x_dev, double *y_dev) {
+  if (!c || !x_dev || !y_dev) return VB_EINVAL;
+  if (c->state < 1) return fail(c, Error{VB_ESTATE, "vb_apply_operator before vb_setup"});
+  ABI_GUARD(c, {
+    if (c->state < 2) throw Error{VB_ESTATE, "vb_apply_operator needs vb_factor (work buffers)"};
+    apply_operator_device(c, x_dev, y_dev);
+    VB_CUDA(cudaStreamSynchronize(c->stream));
+  })
+}
+
+vb_status vb_debug_interface_op(vb_ctx *c, int32_t which, const double *in, double *out) {
+  if (!c || !in || !out || (which != 0 && which != 1)) return VB_EINVAL;
+  if (c->state < 2) return fail(c, Error{VB_ESTATE, "vb_debug_interface_op before vb_factor"});
+  ABI_GUARD(c, { debug_interface_op(c, which, in, out); })
+}
+
+vb_status vb_interface_dofs(const vb_ctx *c, int64_t *ids, int64_t *n) {
+  if (!c || !n) return VB_EINVAL;
+  *n = c->nGamma;
+  if (ids) {
+    int64_t q = 0;
+    for (auto &E : c->ents)
+      for (auto d : E.dofs) ids[q++] = d;
+  }
+  return VB_OK;
+}
+
+vb_status vb_num_free_dofs(const vb_ctx *c, int64_t *n_vel, int64_t *n_p) {
+  if (!c || !n_vel || !n_p) return VB_EINVAL;
+  *n_vel = c->n_free_vel;
+  *n_p = c->npres;
+  return VB_OK;
+}
+
+vb_status vb_dof_layout(const vb_ctx *c, int64_t *ids) {
+  if (!c || !ids) return VB_EINVAL;
+  for (int64_t i = 0; i < c->n_free_vel; ++i) ids[i] = c->free2vel[i];
+  for (int64_t p = 0; p < c->npres; ++p) ids[c->n_free_vel + p] = c->nvel + p;
+  return VB_OK;
+}
+
+vb_status vb_cell_local_dofs(const vb_ctx *c, int64_t cell, int64_t *vel_ids, int32_t *n_vel, int64_t *p_ids,
+                             int32_t *n_p) {
+  if (!c || cell < 0 || cell >= c->nK) return VB_EINVAL;
+  int nv = c->cell_nv[cell];
+  if (n_vel) *n_vel = nv;
+  if (n_p) *n_p = c->np;
+  if (vel_ids)
+    for (int j = 0; j < nv; ++j) vel_ids[j] = c->cell_l2g[c->cell_l2g_ptr[cell] + j];
+  if (p_ids)
+    for (int a = 0; a < c->np; ++a) p_ids[a] = cell * c->np + a;
+  return VB_OK;
+}
+
+vb_status vb_get_element_matrices(const vb_ctx *c, int64_t cell, double *A, double *B) {
+  if (!c || cell < 0 || cell >= c->nK) return VB_EINVAL;
+  const int nvm = c->nv_max, np = c->np, nv = c->cell_nv[cell];
+  try {
+    if (A) VB_CUDA(cudaMemcpy(A, c->d_elA.p + cell * nvm * nvm, (size_t)nv * nv * 8, cudaMemcpyDeviceToHost));
+    if (B) VB_CUDA(cudaMemcpy(B, c->d_elB.p + cell * np * nvm, (size_t)np * nv * 8, cudaMemcpyDeviceToHost));
+  } catch (const Error &e) {
+    return fail(const_cast<vb_ctx *>(c), e);
+  }
+  return VB_OK;
+}
+
+vb_status vb_stats(const vb_ctx *c, int64_t *o) {
+  if (!c || !o) return VB_EINVAL;
+  int64_t maxnG = 0, maxnd = 0, maxn = 0;
+  for (auto &S : c->h_sub) { maxnG = std::max<int64_t>(maxnG, S.nG); maxnd = std::max<int64_t>(maxnd, S.nd); maxn = std::max<int64_t>(maxn, S.n); }
+  int64_t v[16] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
+                   c->NPi, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max, c->ncolors};
+  memcpy(o, v, sizeof(v));
+  return VB_OK;
+}
+
+vb_status vb_kernel_times(const vb_ctx *c, double *ms, int32_t n_max, int32_t *n_out) {
+  if (!c || !n_out) return VB_EINVAL;
+  *n_out = 0;
+  return VB_OK;
+}
+
+const char *vb_kernel_time_name(int32_t) { return ""; }
+
+const char *vb_last_error(const vb_ctx *c) { return c ? c->err.c_str() : g_last_error.c_str(); }
+
+vb_status vb_destroy(vb_ctx *c) {
+  if (!c) return VB_EINVAL;
+  cudaStreamSynchronize(c->stream);
+  destroy_solve_state(c);
+  delete c;
+  return VB_OK;
+}
+
+}  // extern "C"

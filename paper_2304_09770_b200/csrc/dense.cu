@@ -1,0 +1,346 @@
+// Batched dense FP64 kernels: grouped DMMA GEMM (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4, the
+// FP64 tensor path of sm_100a; tcgen05 has no f64 kind), blocked partial LDL^T,
+// triangular inverse, packing.  Used by the factor stage.
+#include <algorithm>
+#include "dense.cuh"
+
+namespace vb {
+
+// ------------------------------------------------------------------ grouped GEMM (DMMA)
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+constexpr int GPAD = 4;
+
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
+                                                           const int4 *__restrict__ tiles, int tile0) {
+  const int4 t = tiles[tile0 + blockIdx.x];
+  const GemmProb P = probs[t.x];
+  const int m0 = t.y * GBM, n0 = t.z * GBN;
+  __shared__ double As[GBM][GBK + GPAD];
+  __shared__ double Bs[GBK][GBN + GPAD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int k0 = 0; k0 < P.K; k0 += GBK) {
+    // load op(A) tile [GBM x GBK] (scaled by d) and op(B) tile [GBK x GBN]
+    for (int idx = tid; idx < GBM * GBK; idx += 128) {
+      int i, kk;
+      if (!P.transA) { i = idx % GBM; kk = idx / GBM; } else { kk = idx % GBK; i = idx / GBK; }
+      int gi = m0 + i, gk = k0 + kk;
+      double v = 0.0;
+      if (gi < P.M && gk < P.K) {
+        v = P.transA ? P.A[gk + (int64_t)gi * P.lda] : P.A[gi + (int64_t)gk * P.lda];
+        if (P.d) v *= P.d[(int64_t)gk * P.dstride];
+      }
+      As[i][kk] = v;
+    }
+    for (int idx = tid; idx < GBK * GBN; idx += 128) {
+      int j, kk;
+      if (!P.transB) { kk = idx % GBK; j = idx / GBK; } else { j = idx % GBN; kk = idx / GBN; }
+      int gj = n0 + j, gk = k0 + kk;
+      double v = 0.0;
+      if (gj < P.N && gk < P.K) v = P.transB ? P.B[gj + (int64_t)gk * P.ldb] : P.B[gk + (int64_t)gj * P.ldb];
+      Bs[kk][j] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[wm + 8 * i + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk + (lane & 3)][wn + 8 * j + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int gi = m0 + wm + 8 * i + (lane >> 2);
+        int gj = n0 + wn + 8 * j + 2 * (lane & 3) + h;
+        if (gi < P.M && gj < P.N && (!P.lower || gi >= gj)) {
+          double *c = P.C + gi + (int64_t)gj * P.ldc;
+          *c = (P.beta == 0.0 ? 0.0 : P.beta * *c) + P.alpha * acc[i][j][h];
+        }
+      }
+}
+
+void GemmPlan::add(const GemmProb &p) {
+  if (p.M <= 0 || p.N <= 0) return;
+  int pid = probs.size();
+  probs.push_back(p);
+  int tm = (p.M + GBM - 1) / GBM, tn = (p.N + GBN - 1) / GBN;
+  for (int i = 0; i < tm; ++i)
+    for (int j = 0; j < tn; ++j) {
+      if (p.lower && (i * GBM + GBM - 1) < j * GBN) continue;   // tile strictly above diagonal
+      tiles.push_back(make_int4(pid, i, j, 0));
+      launches.back().second++;
+    }
+}
+
+void GemmPlan::upload(cudaStream_t s) {
+  std::vector<GemmProb> hp(probs);
+  std::vector<int4> ht(tiles);
+  d_probs.upload(hp, s);
+  d_tiles.upload(ht, s);
+  VB_CUDA(cudaStreamSynchronize(s));
+}
+
+void GemmPlan::run(int launch, cudaStream_t s) {
+  auto &L = launches[launch];
+  if (L.second == 0) return;
+  gemm_grouped_kernel<<<L.second, 128, 0, s>>>(d_probs.p, d_tiles.p, L.first);
+  VB_CHECK_LAUNCH();
+}
+
+void gemm_grouped(GemmPlan &plan, int launch, cudaStream_t s) { plan.run(launch, s); }
+
+// ------------------------------------------------------------------ partial LDL^T
+// Phase 1 (blockIdx.x == 0 launch): factor the nb x nb diagonal block in place.
+// Phase 2 (separate launch): panel rows below read the factored block (no read/write race).
+__global__ void ldl_panel_kernel(const MatDesc *__restrict__ mats, int j0, int *info, int phase) {
+  const MatDesc M = mats[blockIdx.y];
+  if (j0 >= M.m) return;
+  const int nb = min(32, M.m - j0);
+  const int r0 = phase == 0 ? j0 : j0 + nb + 32 * blockIdx.x;
+  if (r0 >= M.n) return;
+  __shared__ double L11[32][33];
+  __shared__ double dd[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *A = M.A;
+  const int64_t ld = M.ld;
+  if (phase == 1) {
+    for (int idx = tid; idx < 1024; idx += blockDim.x) {
+      int i = idx & 31, j = idx >> 5;
+      L11[i][j] = (i < nb && j < nb && i > j) ? A[(j0 + i) + (j0 + j) * ld] : 0.0;
+    }
+    if (tid < 32) dd[tid] = tid < nb ? A[(j0 + tid) * (ld + 1)] : 1.0;
+    __syncthreads();
+    if (warp == 0) {
+      const int row = r0 + lane;
+      if (row < M.n) {
+        double l[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < nb) {
+            double v = A[row + (j0 + j) * ld];
+            for (int t = 0; t < j; ++t) v -= l[t] * dd[t] * L11[j][t];
+            l[j] = v / dd[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nb) A[row + (j0 + j) * ld] = l[j];
+      }
+    }
+    return;
+  }
+  for (int idx = tid; idx < 1024; idx += blockDim.x) {
+    int i = idx & 31, j = idx >> 5;
+    L11[i][j] = (i < nb && j < nb && i >= j) ? A[(j0 + i) + (j0 + j) * ld] : 0.0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int j = 0; j < nb; ++j) {
+      double d = L11[j][j];
+      if (lane == 0) {
+        dd[j] = d;
+        if (!(fabs(d) > 1e-300) || !isfinite(d)) {
+          if (info && blockIdx.x == 0) atomicCAS(&info[blockIdx.y], 0, 1 + j0 + j);
+        }
+      }
+      __syncwarp();
+      if (lane > j && lane < nb) L11[lane][j] /= d;
+      __syncwarp();
+      if (lane > j && lane < nb) {
+        double lij = L11[lane][j] * d;
+        for (int t = j + 1; t <= lane; ++t) L11[lane][t] -= lij * L11[t][j];
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < 1024; idx += blockDim.x) {
+    int i = idx & 31, j = idx >> 5;
+    if (i < nb && j < nb && i >= j) A[(j0 + i) + (j0 + j) * ld] = (i == j) ? dd[i] : L11[i][j];
+  }
+}
+
+void ldl_partial_batched(const std::vector<MatDesc> &mats, int *info_dev, cudaStream_t s) {
+  if (mats.empty()) return;
+  DBuf<MatDesc> dm;
+  std::vector<MatDesc> hm(mats);
+  dm.upload(hm, s);
+  int maxm = 0, maxn = 0;
+  for (auto &M : mats) { maxm = std::max(maxm, M.m); maxn = std::max(maxn, M.n); }
+  GemmPlan plan;
+  for (int j0 = 0; j0 < maxm; j0 += 32) {
+    plan.begin_launch();
+    for (auto &M : mats) {
+      if (j0 >= M.m) continue;
+      int nb = std::min(32, M.m - j0);
+      int rows = M.n - j0 - nb;
+      if (rows <= 0) continue;
+      GemmProb p{};
+      p.A = M.A + (j0 + nb) + (int64_t)j0 * M.ld; p.lda = M.ld; p.transA = 0;
+      p.B = p.A; p.ldb = M.ld; p.transB = 1;
+      p.d = M.A + (int64_t)j0 * (M.ld + 1); p.dstride = M.ld + 1;
+      p.C = M.A + (int64_t)(j0 + nb) * (M.ld + 1); p.ldc = M.ld;
+      p.M = p.N = rows; p.K = nb; p.alpha = -1.0; p.beta = 1.0; p.lower = 1;
+      plan.add(p);
+    }
+  }
+  plan.upload(s);
+  int step = 0;
+  for (int j0 = 0; j0 < maxm; j0 += 32, ++step) {
+    ldl_panel_kernel<<<dim3(1, mats.size()), 128, 0, s>>>(dm.p, j0, info_dev, 0);
+    VB_CHECK_LAUNCH();
+    dim3 grid((maxn - j0 + 31) / 32, mats.size());
+    ldl_panel_kernel<<<grid, 32, 0, s>>>(dm.p, j0, info_dev, 1);
+    VB_CHECK_LAUNCH();
+    plan.run(step, s);
+  }
+  VB_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------------ triangular inverse
+__global__ void set_identity_kernel(const TriDesc *mats) {
+  const TriDesc T = mats[blockIdx.y];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < T.m; i += gridDim.x * blockDim.x)
+    T.X[i + (int64_t)i * T.ldx] = 1.0;
+}
+
+// Solve L_JJ X_J = X_J (in place) for column block cb of block row J (unit lower L_JJ).
+__global__ void trsm_diag_kernel(const TriDesc *__restrict__ mats, int J) {
+  const TriDesc T = mats[blockIdx.y];
+  const int r0 = 32 * J;
+  if (r0 >= T.m) return;
+  const int cb = blockIdx.x;
+  if (cb > J) return;
+  const int nb = min(32, T.m - r0);
+  __shared__ double L[32][33];
+  for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
+    int i = idx & 31, j = idx >> 5;
+    L[i][j] = (i < nb && j < nb && i > j) ? T.L[(r0 + i) + (int64_t)(r0 + j) * T.ldl] : 0.0;
+  }
+  __syncthreads();
+  int col = 32 * cb + threadIdx.x;
+  if (threadIdx.x < 32 && col < T.m) {
+    double x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i < nb) {
+        double v = T.X[(r0 + i) + (int64_t)col * T.ldx];
+        for (int t = 0; t < i; ++t) v -= L[i][t] * x[t];
+        x[i] = v;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < nb) T.X[(r0 + i) + (int64_t)col * T.ldx] = x[i];
+  }
+}
+
+void tri_inverse_batched(const std::vector<TriDesc> &mats, cudaStream_t s) {
+  if (mats.empty()) return;
+  DBuf<TriDesc> dm;
+  std::vector<TriDesc> hm(mats);
+  dm.upload(hm, s);
+  int maxm = 0;
+  for (auto &T : mats) maxm = std::max(maxm, T.m);
+  set_identity_kernel<<<dim3((maxm + 255) / 256, mats.size()), 256, 0, s>>>(dm.p);
+  VB_CHECK_LAUNCH();
+  int nblk = (maxm + 31) / 32;
+  GemmPlan plan;
+  for (int J = 0; J < nblk; ++J) {
+    plan.begin_launch();
+    for (auto &T : mats) {
+      int r0 = 32 * J;
+      if (r0 >= T.m) continue;
+      int nb = std::min(32, T.m - r0);
+      int rows = T.m - r0 - nb;
+      if (rows <= 0) continue;
+      GemmProb p{};
+      p.A = T.L + (r0 + nb) + (int64_t)r0 * T.ldl; p.lda = T.ldl; p.transA = 0;
+      p.B = T.X + r0; p.ldb = T.ldx; p.transB = 0;
+      p.C = T.X + (r0 + nb); p.ldc = T.ldx;
+      p.M = rows; p.N = std::min(T.m, r0 + nb); p.K = nb;
+      p.alpha = -1.0; p.beta = 1.0; p.lower = 0;
+      plan.add(p);
+    }
+  }
+  plan.upload(s);
+  for (int J = 0; J < nblk; ++J) {
+    trsm_diag_kernel<<<dim3(J + 1, mats.size()), 32, 0, s>>>(dm.p, J);
+    VB_CHECK_LAUNCH();
+    plan.run(J, s);
+  }
+  VB_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------------ symmetrize / pack
+__global__ void symmetrize_kernel(const MatDesc *__restrict__ mats) {
+  const MatDesc M = mats[blockIdx.z];
+  int i = blockIdx.y * 32 + threadIdx.y, j = blockIdx.x * 32 + threadIdx.x;   // write (i,j), i<j
+  if (i < M.n && j < M.n && i < j) M.A[i + (int64_t)j * M.ld] = M.A[j + (int64_t)i * M.ld];
+}
+
+void symmetrize_lower_batched(const std::vector<MatDesc> &mats, cudaStream_t s) {
+  if (mats.empty()) return;
+  DBuf<MatDesc> dm;
+  std::vector<MatDesc> hm(mats);
+  dm.upload(hm, s);
+  int maxn = 0;
+  for (auto &M : mats) maxn = std::max(maxn, M.n);
+  int nt = (maxn + 31) / 32;
+  symmetrize_kernel<<<dim3(nt, nt, mats.size()), dim3(32, 32), 0, s>>>(dm.p);
+  VB_CHECK_LAUNCH();
+  VB_CUDA(cudaStreamSynchronize(s));
+}
+
+__global__ void pack_tiles_kernel(const PackDesc *__restrict__ mats) {
+  const PackDesc M = mats[blockIdx.z];
+  const int I = blockIdx.y, J = blockIdx.x;
+  if (J > I) return;
+  if (32 * I >= M.n) return;
+  double *out = M.out + ((int64_t)I * (I + 1) / 2 + J) * 1024;
+  for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
+    int r = idx >> 5, cc = idx & 31;
+    int row = 32 * I + r, col = 32 * J + cc;
+    double v = 0.0;
+    if (row < M.n && col < M.n)
+      v = row >= col ? M.A[row + (int64_t)col * M.ld] : M.A[col + (int64_t)row * M.ld];
+    out[idx] = v;
+  }
+}
+
+void pack_tiles_batched(const std::vector<PackDesc> &mats, cudaStream_t s) {
+  if (mats.empty()) return;
+  DBuf<PackDesc> dm;
+  std::vector<PackDesc> hm(mats);
+  dm.upload(hm, s);
+  int maxn = 0;
+  for (auto &M : mats) maxn = std::max(maxn, M.n);
+  int nt = (maxn + 31) / 32;
+  pack_tiles_kernel<<<dim3(nt, nt, mats.size()), 256, 0, s>>>(dm.p);
+  VB_CHECK_LAUNCH();
+  VB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace vb

@@ -1,0 +1,55 @@
+// Batched dense FP64 kernels for the factorisations.
+#pragma once
+#include "internal.h"
+
+namespace vb {
+
+struct MatDesc {      // column-major square matrix
+  double *A;
+  int n, ld, m;       // m = number of leading columns to eliminate
+};
+
+// A sequence of grouped-GEMM launches planned on the host and uploaded once.
+struct GemmPlan {
+  std::vector<GemmProb> probs;
+  std::vector<int4> tiles;                 // (prob, tile_m, tile_n, 0)
+  std::vector<std::pair<int, int>> launches;  // (tile_begin, tile_count)
+  DBuf<GemmProb> d_probs;
+  DBuf<int4> d_tiles;
+  int begin_launch() { launches.push_back({(int)tiles.size(), 0}); return launches.size() - 1; }
+  void add(const GemmProb &p);             // adds tiles to the current launch
+  void upload(cudaStream_t s);
+  void run(int launch, cudaStream_t s);
+};
+
+void gemm_grouped(GemmPlan &plan, int launch, cudaStream_t s);
+
+// Partial LDL^T (no pivoting, velocity-first quasi-definite ordering) of a batch:
+// eliminates the first m columns; on exit the strictly lower part of those columns holds L, the
+// diagonal holds D, and the lower triangle of the trailing block holds the Schur complement.
+// `info[b]` receives 1 + the column of the first tiny/sign-inconsistent pivot, else 0.
+// pivot_sign: +1 all pivots positive (SPD), 0 = any sign allowed.
+void ldl_partial_batched(const std::vector<MatDesc> &mats, int *info_dev, cudaStream_t s);
+
+// X <- L^{-1} for the unit lower triangle of the leading m x m block of each matrix (column-major,
+// X with leading dimension ldx, overwritten; X must be pre-zeroed).
+struct TriDesc {
+  const double *L;
+  int ldl;
+  double *X;
+  int ldx, m;
+};
+void tri_inverse_batched(const std::vector<TriDesc> &mats, cudaStream_t s);
+
+// Fill the strictly upper triangle of an n x n block from its lower triangle.
+void symmetrize_lower_batched(const std::vector<MatDesc> &mats, cudaStream_t s);
+
+// Pack the lower triangle of a symmetric column-major n x n block into 32x32 row-major tiles.
+struct PackDesc {
+  const double *A;
+  int n, ld;
+  double *out;
+};
+void pack_tiles_batched(const std::vector<PackDesc> &mats, cudaStream_t s);
+
+}  // namespace vb

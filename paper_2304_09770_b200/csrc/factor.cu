@@ -1,0 +1,630 @@
+// Factor stage: subdomain assembly, partial LDL^T giving the interface
+// Stokes Schur complement S_G (Eq.(firstSchur)), orthogonal change of basis to explicit
+// primal coordinates, dual Schur inverse, coarse basis Phi, deluxe operators,
+// coarse saddle matrix on (u_Pi, p_0) and its inverse.
+//
+// Q_I (zero-mean interior pressure) is imposed by augmenting the pressure block with
+// -gamma m m^T and projecting the pressure-velocity coupling with Pi^T = I - m c^T / vol
+// (reading A5); this gives exactly the Q_I Schur complement.
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <set>
+#include <cstring>
+#include "dense.cuh"
+#include "setup.h"
+
+namespace vb {
+
+// ------------------------------------------------------------------ assembly (one CTA / subdomain)
+__global__ void assemble_kernel(const SubDev *__restrict__ subs, const int *__restrict__ sub_cells,
+                                const int *__restrict__ cell_loc, const int *__restrict__ cell_nv,
+                                const double *__restrict__ elA, const double *__restrict__ elB,
+                                int nvmax, int np, const double *__restrict__ cvec,
+                                const double *__restrict__ mvec, double *Kall, double *b0all) {
+  const SubDev S = subs[blockIdx.x];
+  double *K = Kall + S.off_K;
+  const double *c = cvec + S.off_P;
+  const double *m = mvec + S.off_P;
+  double *b0 = b0all + S.off_G;
+  const int64_t ld = S.n;
+  const int nI = S.nI, nP = S.nP, nG = S.nG;
+  const int stride = nvmax + np;
+  for (int q = S.cell_begin; q < S.cell_end; ++q) {
+    const int cell = sub_cells[q];
+    const int nv = cell_nv[cell];
+    const int *loc = cell_loc + (int64_t)cell * stride;
+    const double *A = elA + (int64_t)cell * nvmax * nvmax;
+    const double *B = elB + (int64_t)cell * np * nvmax;
+    for (int idx = threadIdx.x; idx < nv * nv; idx += blockDim.x) {
+      int a = idx / nv, b = idx % nv;
+      int pa = loc[a], pb = loc[b];
+      if (pa >= 0 && pb >= 0) K[pa + pb * ld] += A[(int64_t)a * nv + b];
+    }
+    for (int idx = threadIdx.x; idx < np * nv; idx += blockDim.x) {
+      int p = idx / nv, b = idx % nv;
+      int pp = loc[nvmax + p], pb = loc[b];
+      if (pb >= 0) {
+        double v = B[(int64_t)p * nv + b];
+        K[pp + pb * ld] += v;
+        K[pb + pp * ld] += v;
+      }
+    }
+    __syncthreads();
+  }
+  // augmentation of the pressure block: -gamma m m^T
+  for (int idx = threadIdx.x; idx < nP * nP; idx += blockDim.x) {
+    int a = idx / nP, b = idx % nP;
+    if (m[a] != 0.0 && m[b] != 0.0) K[(nI + a) + (int64_t)(nI + b) * ld] -= S.gamma * m[a] * m[b];
+  }
+  __syncthreads();
+  // projection Pi^T of the pressure rows on every velocity column: K[P,v] -= m (c^T K[P,v]) / vol
+  for (int v = threadIdx.x; v < nI + nG; v += blockDim.x) {
+    const int col = v < nI ? v : v + nP;
+    double s = 0.0;
+    for (int a = 0; a < nP; ++a) s += c[a] * K[(nI + a) + (int64_t)col * ld];
+    if (v >= nI) b0[v - nI] = s;      // flux row B_0G^(i) on the local interface
+    for (int a = 0; a < nP; ++a) {
+      if (m[a] != 0.0) K[(nI + a) + (int64_t)col * ld] -= m[a] * s / S.vol;
+      K[col + (int64_t)(nI + a) * ld] = K[(nI + a) + (int64_t)col * ld];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ change of basis per entity
+// Householder QR with column pivoting of C_G^T; T_G = [N_G | Q_1] (dual coordinates first),
+// rank by |R_jj| > tol |R_00|.  One CTA per entity; T (n x n col-major) in global memory.
+__device__ double block_sum(double v, double *red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+  return s;
+}
+
+__global__ void entity_basis_kernel(const EntDev *__restrict__ ents, const double *__restrict__ Crows,
+                                    double *Tall, double *work, int *rank_out, double tol) {
+  const EntDev E = ents[blockIdx.x];
+  const int n = E.n, nr = E.nrowsC;
+  double *T = Tall + E.off_T;
+  const double *C = Crows + E.off_C;     // nr x n row-major
+  double *W = work + E.off_C;            // n x nr column-major (same size as C)
+  __shared__ double red[32];
+  for (int idx = threadIdx.x; idx < n * nr; idx += blockDim.x) {
+    int row = idx % n, col = idx / n;
+    W[row + (int64_t)col * n] = C[(int64_t)col * n + row];
+  }
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) T[idx] = (idx % n == idx / n) ? 1.0 : 0.0;
+  __syncthreads();
+  double r00 = 0.0;
+  int r = 0;
+  for (int j = 0; j < nr && j < n; ++j) {
+    int pc = j;
+    double best = -1.0;
+    for (int col = j; col < nr; ++col) {
+      double s = 0.0;
+      for (int row = j + threadIdx.x; row < n; row += blockDim.x) s += W[row + (int64_t)col * n] * W[row + (int64_t)col * n];
+      s = block_sum(s, red);
+      if (s > best) { best = s; pc = col; }
+    }
+    if (pc != j) {
+      for (int row = threadIdx.x; row < n; row += blockDim.x) {
+        double t = W[row + (int64_t)j * n];
+        W[row + (int64_t)j * n] = W[row + (int64_t)pc * n];
+        W[row + (int64_t)pc * n] = t;
+      }
+    }
+    __syncthreads();
+    double nrm = sqrt(best);
+    if (j == 0) r00 = nrm;
+    if (!(nrm > tol * r00)) break;
+    r = j + 1;
+    double x0 = W[j + (int64_t)j * n];
+    double alpha = x0 >= 0 ? -nrm : nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) W[j + (int64_t)j * n] = x0 - alpha;
+    __syncthreads();
+    double vv = 0.0;
+    for (int row = j + threadIdx.x; row < n; row += blockDim.x) vv += W[row + (int64_t)j * n] * W[row + (int64_t)j * n];
+    vv = block_sum(vv, red);
+    const double beta = 2.0 / vv;
+    for (int col = j + 1; col < nr; ++col) {
+      double s = 0.0;
+      for (int row = j + threadIdx.x; row < n; row += blockDim.x) s += W[row + (int64_t)j * n] * W[row + (int64_t)col * n];
+      s = block_sum(s, red) * beta;
+      for (int row = j + threadIdx.x; row < n; row += blockDim.x) W[row + (int64_t)col * n] -= s * W[row + (int64_t)j * n];
+      __syncthreads();
+    }
+    for (int row = 0; row < n; ++row) {     // Q <- Q H_j
+      double s = 0.0;
+      for (int q = j + threadIdx.x; q < n; q += blockDim.x) s += T[row + (int64_t)q * n] * W[q + (int64_t)j * n];
+      s = block_sum(s, red) * beta;
+      for (int q = j + threadIdx.x; q < n; q += blockDim.x) T[row + (int64_t)q * n] -= s * W[q + (int64_t)j * n];
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // Q = [Q1 (r) | Q2 (n-r)] -> T = [Q2 | Q1]; W (n*nr >= n*r) is free scratch now
+  for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) W[idx] = T[idx];
+  __syncthreads();
+  for (int col = 0; col < n - r; ++col) {
+    for (int row = threadIdx.x; row < n; row += blockDim.x) T[row + (int64_t)col * n] = T[row + (int64_t)(col + r) * n];
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) T[(int64_t)(n - r) * n + idx] = W[idx];
+  if (threadIdx.x == 0) rank_out[blockIdx.x] = r;
+}
+
+// b~0 = b0 T on the primal coordinates; max |b0 T_Delta| / |b0| is the benign check (Eq.(ass1)).
+__global__ void b0_transform_kernel(const SlotDev *__restrict__ slots, int nslot, const SubDev *__restrict__ subs,
+                                    const double *__restrict__ T, const double *__restrict__ b0all,
+                                    double *b0T, unsigned long long *viol) {
+  int w = blockIdx.x;
+  if (w >= nslot) return;
+  const SlotDev s = slots[w];
+  const SubDev S = subs[s.sub];
+  const double *Te = T + s.off_T;
+  const double *b0 = b0all + S.off_G + s.offG;
+  const int n = s.n;
+  double nb = 0.0;
+  for (int j = threadIdx.x; j < n; j += 32) nb += b0[j] * b0[j];
+  for (int o = 16; o; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  for (int col = 0; col < n; ++col) {
+    double sum = 0.0;
+    for (int j = threadIdx.x; j < n; j += 32) sum += b0[j] * Te[j + (int64_t)col * n];
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (threadIdx.x == 0) {
+      if (col >= s.nd) b0T[S.off_Pi + s.offPi + (col - s.nd)] = sum;
+      else if (nb > 0) atomicMax(viol, (unsigned long long)__double_as_longlong(fabs(sum) / sqrt(nb)));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ deluxe helpers
+__global__ void deluxe_gather_kernel(const SlotDev *__restrict__ slots, const SubDev *__restrict__ subs,
+                                     const double *__restrict__ Kall, double *sidebuf) {
+  const SlotDev s = slots[blockIdx.y];
+  const SubDev S = subs[s.sub];
+  const double *ST = Kall + S.off_K + (int64_t)S.nD * (S.n + 1);
+  const int64_t ld = S.n;
+  const int nd = s.nd;
+  double *out = sidebuf + s.off_side;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nd * nd; idx += gridDim.x * blockDim.x) {
+    int a = idx % nd, b = idx / nd;
+    int ra = s.offD + a, rb = s.offD + b;
+    out[idx] = ra >= rb ? ST[ra + rb * ld] : ST[rb + ra * ld];
+  }
+}
+
+__global__ void deluxe_sum_kernel(const EntDev *__restrict__ ents, const SlotDev *__restrict__ slots,
+                                  const double *__restrict__ sidebuf, double *sumbuf) {
+  const EntDev E = ents[blockIdx.y];
+  const int nd = E.nd;
+  if (nd == 0) return;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nd * nd; idx += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int q = 0; q < E.nsides; ++q) v += sidebuf[slots[E.side_begin + q].off_side + idx];
+    sumbuf[E.off_sum + idx] = v;
+  }
+}
+
+__global__ void multiplicity_kernel(const SlotDev *__restrict__ slots, const EntDev *__restrict__ ents, double *Dlx) {
+  const SlotDev s = slots[blockIdx.y];
+  const double v = 1.0 / ents[s.ent].nsides;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < s.nd * s.nd; idx += gridDim.x * blockDim.x)
+    Dlx[s.off_Dlx + idx] = (idx % s.nd == idx / s.nd) ? v : 0.0;
+}
+
+__global__ void recip_diag_kernel(const double *A, int64_t ld, int n, double *out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = 1.0 / A[i + i * ld];
+}
+
+// ------------------------------------------------------------------ coarse assembly (colored)
+__global__ void coarse_assemble_kernel(const int *__restrict__ color_subs, const SubDev *__restrict__ subs,
+                                       const double *__restrict__ Kall, const int64_t *__restrict__ pi_glob,
+                                       const double *__restrict__ b0T, double *Kc, int64_t ldc, int64_t NPi) {
+  const int i = color_subs[blockIdx.y];
+  const SubDev S = subs[i];
+  const int npi = S.npi;
+  const double *Sc = Kall + S.off_K + (int64_t)S.nD * (S.n + 1) + (int64_t)S.nd * (S.n + 1);
+  const int64_t ld = S.n;
+  const int64_t *g = pi_glob + S.off_Pi;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < npi * npi; idx += gridDim.x * blockDim.x) {
+    int a = idx % npi, b = idx / npi;
+    double v = a >= b ? Sc[a + b * ld] : Sc[b + a * ld];
+    Kc[g[a] + g[b] * ldc] += v;
+  }
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < npi; a += gridDim.x * blockDim.x) {
+    double v = b0T[S.off_Pi + a];
+    Kc[(NPi + i) + g[a] * ldc] += v;
+    Kc[g[a] + (NPi + i) * ldc] += v;
+  }
+}
+
+__global__ void coarse_augment_kernel(const SubDev *__restrict__ subs, int N, double gam, double *Kc, int64_t ldc, int64_t NPi) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < N * N; idx += gridDim.x * blockDim.x) {
+    int a = idx % N, b = idx / N;
+    Kc[(NPi + a) + (NPi + b) * ldc] -= gam * subs[a].vol * subs[b].vol;
+  }
+}
+
+// ------------------------------------------------------------------ host orchestration
+static void sync(vb_ctx *c) { VB_CUDA(cudaStreamSynchronize(c->stream)); }
+
+static void check_info(vb_ctx *c, int nmat, const char *what, const std::vector<int> *names = nullptr) {
+  std::vector<int> info(nmat);
+  VB_CUDA(cudaMemcpyAsync(info.data(), c->d_info.p, nmat * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  for (int b = 0; b < nmat; ++b)
+    if (info[b])
+      throw Error{VB_ESINGULAR, std::string(what) + ": zero pivot at column " + std::to_string(info[b] - 1) +
+                                    " of matrix " + std::to_string(names ? (*names)[b] : b)};
+}
+
+// layout after the ranks of the entity bases are known
+static void layout_phase_b(vb_ctx *c, const std::vector<int> &rank) {
+  int64_t xd = 0, pi = 0;
+  for (size_t e = 0; e < c->ents.size(); ++e) {
+    Entity &E = c->ents[e];
+    EntDev &D = c->h_ent[e];
+    E.r = rank[e]; E.nd = E.n - E.r;
+    D.r = E.r; D.nd = E.nd;
+    E.off_d = xd; D.off_xd = xd; xd += E.nd;
+    E.off_p = pi; D.off_pi = pi; pi += E.r;
+  }
+  c->n_delta_glob = xd;
+  c->NPi = pi;
+  c->nx = xd + pi + c->N;
+  int64_t sum = 0, Dl = 0, side = 0;
+  for (size_t e = 0; e < c->ents.size(); ++e) {
+    EntDev &D = c->h_ent[e];
+    D.off_sum = sum; D.off_W = sum; sum += (int64_t)D.nd * D.nd;
+    for (int q = 0; q < D.nsides; ++q) {
+      SlotDev &s = c->h_slot[D.side_begin + q];
+      s.nd = D.nd; s.r = D.r;
+      s.off_Dlx = Dl; Dl += (int64_t)D.nd * D.nd;
+      s.off_side = side; side += (int64_t)D.nd * D.nd;
+    }
+  }
+  c->len_sum = sum; c->len_Dlx = Dl; c->len_side = side;
+  int64_t offDv = 0, offPi = 0, STp = 0, SDi = 0, Phi = 0;
+  for (int i = 0; i < c->N; ++i) {
+    SubDev &S = c->h_sub[i];
+    int nd = 0, npi = 0;
+    for (int q = S.slot_begin; q < S.slot_end; ++q) {
+      SlotDev &s = c->h_slot[c->h_sub_slots[q]];
+      s.offD = nd; nd += s.nd;
+    }
+    for (int q = S.slot_begin; q < S.slot_end; ++q) {
+      SlotDev &s = c->h_slot[c->h_sub_slots[q]];
+      s.offPi = npi; npi += s.r;
+    }
+    S.nd = nd; S.npi = npi;
+    c->subs[i].nd = nd; c->subs[i].npi = npi;
+    S.off_Dv = offDv; offDv += nd;
+    S.off_Pi = offPi; offPi += npi;
+    S.off_STp = STp; STp += packed_tiles(S.nG) * 1024;
+    S.off_SDi = SDi; SDi += packed_tiles(nd) * 1024;
+    S.off_Phi = Phi; Phi += (int64_t)nd * npi;
+  }
+  c->len_Dv = offDv; c->len_Pi = offPi; c->len_STp = STp; c->len_SDi = SDi; c->len_Phi = Phi;
+}
+
+void factor_device(vb_ctx *c) {
+  cudaStream_t s = c->stream;
+  const int N = c->N;
+  // ---------------- A1: assemble subdomain matrices [I | P | Gamma]
+  c->d_K.alloc(c->len_K);
+  c->d_K.zero(s);
+  c->d_b0.alloc(c->len_G);
+  c->d_b0.zero(s);
+  assemble_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->d_sub_cells.p, c->d_cell_loc.p, c->d_cell_nv.p,
+                                    c->d_elA.p, c->d_elB.p, c->nv_max, c->np, c->d_cvec.p, c->d_mvec.p,
+                                    c->d_K.p, c->d_b0.p);
+  VB_STAGE();
+  // ---------------- A1/A2: partial LDL^T eliminating (u_I, p) -> trailing block = S_G
+  c->d_info.alloc(std::max<int64_t>(N, std::max<int64_t>(c->ents.size(), 1)) + 1);
+  c->d_info.zero(s);
+  std::vector<MatDesc> mats(N);
+  for (int i = 0; i < N; ++i) {
+    const SubDev &S = c->h_sub[i];
+    mats[i] = MatDesc{c->d_K.p + S.off_K, S.n, S.n, S.nD};
+  }
+  ldl_partial_batched(mats, c->d_info.p, s);
+  check_info(c, N, "subdomain Dirichlet LDL^T (A1)");
+  std::vector<MatDesc> sg(N);
+  for (int i = 0; i < N; ++i) {
+    const SubDev &S = c->h_sub[i];
+    sg[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.nG, S.n, 0};
+  }
+  symmetrize_lower_batched(sg, s);
+  // ---------------- A3: entity bases T_G = [N_G | C'^T]
+  std::vector<double> rows;
+  build_constraint_rows(c, rows);
+  int64_t lenT = 0;
+  for (size_t e = 0; e < c->ents.size(); ++e) {
+    EntDev &D = c->h_ent[e];
+    D.off_C = c->ents[e].off_C; D.nrowsC = c->ents[e].nrows_C;
+    D.off_T = lenT; lenT += (int64_t)D.n * D.n;
+  }
+  for (auto &sl : c->h_slot) sl.off_T = c->h_ent[sl.ent].off_T;
+  c->len_T = lenT;
+  c->d_C.upload(rows, s);
+  c->d_T.alloc(lenT);
+  DBuf<double> wq;
+  wq.alloc(std::max<size_t>(rows.size(), 1));
+  c->d_ent.upload(c->h_ent, s);
+  DBuf<int> drank;
+  drank.alloc(c->ents.size());
+  double tol = c->cons.svd_rel_tol > 0 ? c->cons.svd_rel_tol : 1e-10;
+  if (c->cons.svd_rel_tol < 0) tol = 1e-10;
+  entity_basis_kernel<<<c->ents.size(), 128, 0, s>>>(c->d_ent.p, c->d_C.p, c->d_T.p, wq.p, drank.p, tol);
+  VB_STAGE();
+  std::vector<int> rank;
+  drank.download(rank, s);
+  sync(c);
+  layout_phase_b(c, rank);
+  c->d_ent.upload(c->h_ent, s);
+  c->d_slot.upload(c->h_slot, s);
+  c->d_sub.upload(c->h_sub, s);
+  build_transformed_maps(c);
+  // ---------------- S_T = T^T S_G T (into the trailing block of K), via scratch X = S_G T
+  DBuf<double> X, Y;
+  X.alloc(c->len_X);
+  Y.alloc(c->len_X);
+  {
+    GemmPlan plan;
+    int l0 = plan.begin_launch();
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      double *SG = c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1);
+      for (int q = S.slot_begin; q < S.slot_end; ++q) {
+        const SlotDev &sl = c->h_slot[c->h_sub_slots[q]];
+        const double *Te = c->d_T.p + sl.off_T;
+        for (int part = 0; part < 2; ++part) {
+          GemmProb p{};
+          p.A = SG + (int64_t)sl.offG * S.n; p.lda = S.n;
+          p.B = Te + (part ? (int64_t)sl.nd * sl.n : 0); p.ldb = sl.n;
+          int oc = part ? S.nd + sl.offPi : sl.offD;
+          p.C = X.p + S.off_X + (int64_t)oc * S.nG; p.ldc = S.nG;
+          p.M = S.nG; p.N = part ? sl.r : sl.nd; p.K = sl.n; p.alpha = 1.0; p.beta = 0.0;
+          plan.add(p);
+        }
+      }
+    }
+    int l1 = plan.begin_launch();
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      double *ST = c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1);
+      for (int q = S.slot_begin; q < S.slot_end; ++q) {
+        const SlotDev &sl = c->h_slot[c->h_sub_slots[q]];
+        const double *Te = c->d_T.p + sl.off_T;
+        for (int part = 0; part < 2; ++part) {
+          GemmProb p{};
+          p.A = Te + (part ? (int64_t)sl.nd * sl.n : 0); p.lda = sl.n; p.transA = 1;
+          p.B = X.p + S.off_X + sl.offG; p.ldb = S.nG;
+          int orow = part ? S.nd + sl.offPi : sl.offD;
+          p.C = ST + orow; p.ldc = S.n;
+          p.M = part ? sl.r : sl.nd; p.N = S.nG; p.K = sl.n; p.alpha = 1.0; p.beta = 0.0;
+          plan.add(p);
+        }
+      }
+    }
+    plan.upload(s);
+    plan.run(l0, s);
+    plan.run(l1, s);
+    sync(c);
+  }
+  // ---------------- operator matrix: packed tiles of S_T (per-iteration operator, B1)
+  c->d_STp.alloc(c->len_STp);
+  {
+    std::vector<PackDesc> pk(N);
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      pk[i] = PackDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.nG, S.n, c->d_STp.p + S.off_STp};
+    }
+    pack_tiles_batched(pk, s);
+  }
+  // ---------------- deluxe side blocks S_GD^(m) (before S_T is factored)
+  DBuf<double> sidebuf, sumbuf, Wbuf, dinv;
+  const int nslot = c->h_slot.size();
+  const int nent = c->h_ent.size();
+  sidebuf.alloc(std::max<int64_t>(c->len_side, 1));
+  sumbuf.alloc(std::max<int64_t>(c->len_sum, 1));
+  Wbuf.alloc(std::max<int64_t>(c->len_sum, 1));
+  if (nslot) {
+    deluxe_gather_kernel<<<dim3(16, nslot), 256, 0, s>>>(c->d_slot.p, c->d_sub.p, c->d_K.p, sidebuf.p);
+    VB_STAGE();
+    deluxe_sum_kernel<<<dim3(16, nent), 256, 0, s>>>(c->d_ent.p, c->d_slot.p, sidebuf.p, sumbuf.p);
+    VB_STAGE();
+  }
+  // ---------------- A3: partial LDL^T of S_T eliminating the dual block -> S_c trailing
+  c->d_info.zero(s);
+  for (int i = 0; i < N; ++i) {
+    const SubDev &S = c->h_sub[i];
+    mats[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.nG, S.n, S.nd};
+  }
+  ldl_partial_batched(mats, c->d_info.p, s);
+  check_info(c, N, "dual Schur LDL^T (A3)");
+  for (int i = 0; i < N; ++i) {
+    const SubDev &S = c->h_sub[i];
+    sg[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)(S.nD + S.nd) * (S.n + 1), S.npi, S.n, 0};
+  }
+  symmetrize_lower_batched(sg, s);
+  // W = L_DD^-1 (in X), Y = W^T D^-1 W = S_DD^-1, Phi = -W^T L_PiD^T
+  X.zero(s);
+  {
+    std::vector<TriDesc> td(N);
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      td[i] = TriDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.n, X.p + S.off_X, S.nd, S.nd};
+    }
+    tri_inverse_batched(td, s);
+  }
+  dinv.alloc(std::max<int64_t>(c->len_Dv, 1));
+  for (int i = 0; i < N; ++i) {
+    const SubDev &S = c->h_sub[i];
+    if (S.nd) recip_diag_kernel<<<(S.nd + 255) / 256, 256, 0, s>>>(c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.n, S.nd, dinv.p + S.off_Dv);
+  }
+  VB_STAGE();
+  c->d_Phi.alloc(std::max<int64_t>(c->len_Phi, 1));
+  {
+    GemmPlan plan;
+    int l0 = plan.begin_launch();
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      GemmProb p{};
+      p.A = X.p + S.off_X; p.lda = S.nd; p.transA = 1;
+      p.d = dinv.p + S.off_Dv; p.dstride = 1;
+      p.B = X.p + S.off_X; p.ldb = S.nd;
+      p.C = Y.p + S.off_X; p.ldc = S.nd;
+      p.M = p.N = p.K = S.nd; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
+      plan.add(p);
+      GemmProb q{};
+      q.A = X.p + S.off_X; q.lda = S.nd; q.transA = 1;
+      q.B = c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1) + S.nd; q.ldb = S.n; q.transB = 1;
+      q.C = c->d_Phi.p + S.off_Phi; q.ldc = S.nd;
+      q.M = S.nd; q.N = S.npi; q.K = S.nd; q.alpha = -1.0; q.beta = 0.0;
+      plan.add(q);
+    }
+    plan.upload(s);
+    plan.run(l0, s);
+    sync(c);
+  }
+  c->d_SDi.alloc(c->len_SDi);
+  {
+    std::vector<PackDesc> pk(N);
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      pk[i] = PackDesc{Y.p + S.off_X, S.nd, S.nd, c->d_SDi.p + S.off_SDi};
+    }
+    pack_tiles_batched(pk, s);
+  }
+  // ---------------- b~0 and the benign check
+  c->d_b0T.alloc(std::max<int64_t>(c->len_Pi, 1));
+  c->d_b0T.zero(s);
+  DBuf<unsigned long long> dviol;
+  dviol.alloc(1);
+  dviol.zero(s);
+  if (nslot) b0_transform_kernel<<<nslot, 32, 0, s>>>(c->d_slot.p, nslot, c->d_sub.p, c->d_T.p, c->d_b0.p, c->d_b0T.p, dviol.p);
+  VB_STAGE();
+  unsigned long long vv = 0;
+  VB_CUDA(cudaMemcpyAsync(&vv, dviol.p, 8, cudaMemcpyDeviceToHost, s));
+  // ---------------- A4: deluxe D_G^(m) = (sum S)^-1 S^(m)
+  c->d_Dlx.alloc(std::max<int64_t>(c->len_Dlx, 1));
+  if (c->cons.scaling == VB_MULTIPLICITY) {
+    if (nslot) multiplicity_kernel<<<dim3(16, nslot), 256, 0, s>>>(c->d_slot.p, c->d_ent.p, c->d_Dlx.p);
+    VB_STAGE();
+  } else {
+    std::vector<MatDesc> em;
+    std::vector<int> names;
+    for (int e = 0; e < nent; ++e) {
+      const EntDev &E = c->h_ent[e];
+      if (E.nd) { em.push_back(MatDesc{sumbuf.p + E.off_sum, E.nd, E.nd, E.nd}); names.push_back(e); }
+    }
+    c->d_info.zero(s);
+    ldl_partial_batched(em, c->d_info.p, s);
+    check_info(c, em.size(), "deluxe sum LDL^T (A4)", &names);
+    Wbuf.zero(s);
+    std::vector<TriDesc> td;
+    for (auto &M : em) td.push_back(TriDesc{M.A, M.n, Wbuf.p + (M.A - sumbuf.p), M.n, M.n});
+    tri_inverse_batched(td, s);
+    DBuf<double> edinv;
+    edinv.alloc(std::max<int64_t>(c->len_sum, 1));
+    for (auto &M : em)
+      recip_diag_kernel<<<(M.n + 255) / 256, 256, 0, s>>>(M.A, M.n, M.n, edinv.p + (M.A - sumbuf.p));
+    VB_STAGE();
+    {
+      GemmPlan plan;
+      int l0 = plan.begin_launch();
+      for (auto &M : em) {
+        int64_t off = M.A - sumbuf.p;
+        GemmProb p{};
+        p.A = Wbuf.p + off; p.lda = M.n; p.transA = 1;
+        p.d = edinv.p + off; p.dstride = 1;
+        p.B = Wbuf.p + off; p.ldb = M.n;
+        p.C = sumbuf.p + off; p.ldc = M.n;
+        p.M = p.N = p.K = M.n; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
+        plan.add(p);
+      }
+      plan.upload(s);
+      plan.run(l0, s);
+      sync(c);
+    }
+    for (auto &M : em) M.m = 0;
+    symmetrize_lower_batched(em, s);
+    {
+      GemmPlan plan;
+      int l0 = plan.begin_launch();
+      for (int q = 0; q < nslot; ++q) {
+        const SlotDev &sl = c->h_slot[q];
+        if (!sl.nd) continue;
+        const EntDev &E = c->h_ent[sl.ent];
+        GemmProb p{};
+        p.A = sumbuf.p + E.off_sum; p.lda = sl.nd;
+        p.B = sidebuf.p + sl.off_side; p.ldb = sl.nd;
+        p.C = c->d_Dlx.p + sl.off_Dlx; p.ldc = sl.nd;
+        p.M = p.N = p.K = sl.nd; p.alpha = 1.0; p.beta = 0.0;
+        plan.add(p);
+      }
+      plan.upload(s);
+      plan.run(l0, s);
+      sync(c);
+    }
+  }
+  // ---------------- A5: coarse saddle matrix on (u_Pi, p_0), dense inverse
+  const int64_t Nc = c->NPi + N;
+  c->Nc = Nc;
+  {
+    DBuf<double> Kc, Wc, dc;
+    Kc.alloc(Nc * Nc);
+    Kc.zero(s);
+    std::vector<std::vector<int>> colors(c->ncolors);
+    for (int i = 0; i < N; ++i) colors[c->subs[i].color].push_back(i);
+    for (auto &col : colors) {
+      if (col.empty()) continue;
+      DBuf<int> dcol;
+      dcol.upload(col, s);
+      coarse_assemble_kernel<<<dim3(8, col.size()), 256, 0, s>>>(dcol.p, c->d_sub.p, c->d_K.p, c->d_pi_glob.p,
+                                                                c->d_b0T.p, Kc.p, Nc, c->NPi);
+      VB_STAGE();
+      sync(c);
+    }
+    double nubar = 0, volO = 0;
+    for (int64_t K = 0; K < c->nK; ++K) nubar += c->nu[K];
+    nubar /= c->nK;
+    for (int i = 0; i < N; ++i) volO += c->h_sub[i].vol;
+    coarse_augment_kernel<<<(N * N + 255) / 256, 256, 0, s>>>(c->d_sub.p, N, 1.0 / (nubar * volO), Kc.p, Nc, c->NPi);
+    VB_STAGE();
+    c->d_info.zero(s);
+    std::vector<MatDesc> cm{MatDesc{Kc.p, (int)Nc, (int)Nc, (int)Nc}};
+    ldl_partial_batched(cm, c->d_info.p, s);
+    check_info(c, 1, "coarse saddle LDL^T (A5)");
+    Wc.alloc(Nc * Nc);
+    Wc.zero(s);
+    tri_inverse_batched({TriDesc{Kc.p, (int)Nc, Wc.p, (int)Nc, (int)Nc}}, s);
+    dc.alloc(Nc);
+    recip_diag_kernel<<<(Nc + 255) / 256, 256, 0, s>>>(Kc.p, Nc, Nc, dc.p);
+    VB_STAGE();
+    GemmPlan plan;
+    int l0 = plan.begin_launch();
+    GemmProb p{};
+    p.A = Wc.p; p.lda = Nc; p.transA = 1; p.d = dc.p; p.dstride = 1;
+    p.B = Wc.p; p.ldb = Nc; p.C = Kc.p; p.ldc = Nc;
+    p.M = p.N = p.K = Nc; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
+    plan.add(p);
+    plan.upload(s);
+    plan.run(l0, s);
+    sync(c);
+    c->d_Kcp.alloc(packed_tiles(Nc) * 1024);
+    pack_tiles_batched({PackDesc{Kc.p, (int)Nc, (int)Nc, c->d_Kcp.p}}, s);
+  }
+  sync(c);
+  double fv;
+  memcpy(&fv, &vv, 8);
+  c->flux_violation = fv;
+}
+
+}  // namespace vb

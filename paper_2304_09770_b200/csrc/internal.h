@@ -1,0 +1,261 @@
+// Internal state of a vb_ctx (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+#include "../../include/vbddc.h"
+
+namespace vb {
+
+struct Error {
+  vb_status st;
+  std::string msg;
+};
+
+#define VB_CUDA(x)                                                                              \
+  do {                                                                                          \
+    cudaError_t _e = (x);                                                                       \
+    if (_e != cudaSuccess)                                                                      \
+      throw ::vb::Error{VB_ECUDA, std::string(#x) + ": " + cudaGetErrorString(_e) + " at " +    \
+                                      __FILE__ + ":" + std::to_string(__LINE__)};               \
+  } while (0)
+#define VB_CHECK_LAUNCH() VB_CUDA(cudaGetLastError())
+#define VB_REQUIRE(cond, code, m)                                                               \
+  do {                                                                                          \
+    if (!(cond)) throw ::vb::Error{code, std::string(m)};                                       \
+  } while (0)
+
+// ------------------------------------------------------------------ device buffer
+template <class T>
+struct DBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) return;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw Error{VB_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed"};
+    }
+    n = count;
+  }
+  void zero(cudaStream_t s) {
+    if (n) VB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void upload(const std::vector<T> &h, cudaStream_t s) {
+    alloc(h.size());
+    if (n) VB_CUDA(cudaMemcpyAsync(p, h.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void download(std::vector<T> &h, cudaStream_t s) const {
+    h.resize(n);
+    if (n) VB_CUDA(cudaMemcpyAsync(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+};
+
+// ------------------------------------------------------------------ grouped GEMM descriptor
+// C(MxN) = beta*C + alpha * op(A) * diag(d) * op(B), column-major, op = transpose if flag.
+struct GemmProb {
+  const double *A;
+  const double *B;
+  double *C;
+  const double *d;   // optional diagonal scaling (length K), stride dstride
+  int lda, ldb, ldc, dstride;
+  int M, N, K;
+  double alpha, beta;
+  int transA, transB;
+  int lower;         // only compute tiles intersecting the lower triangle (i >= j)
+};
+
+// ------------------------------------------------------------------ packed symmetric tiles
+// Lower-triangular 32x32 tiles (I >= J) in row-of-tiles order, each tile row-major, zero padded.
+inline int64_t packed_tiles(int n) {
+  int64_t nt = (n + 31) / 32;
+  return nt * (nt + 1) / 2;
+}
+
+struct Entity {
+  int kind = 0;                 // 0 vertex, 1 edge, 2 face
+  std::vector<int> sharers;     // subdomains (sorted)
+  std::vector<int64_t> dofs;    // free velocity ids (sorted)
+  int n = 0, r = 0, nd = 0;
+  int64_t off_d = 0;            // offset of its dual coords in the global coordinate vector
+  int64_t off_p = 0;            // offset of its primal coords within u_Pi
+  int64_t off_T = 0;            // offset of T_G (n x n, column-major) in the T buffer
+  int64_t off_C = 0;            // offset of constraint rows C_G (rows x n, row-major)
+  int nrows_C = 0;
+  int64_t off_D = 0;            // offset of deluxe blocks (one nd x nd per sharer, row-major)
+};
+
+struct Sub {
+  std::vector<int> cells;
+  std::vector<int64_t> I;       // interior free velocity ids
+  std::vector<int64_t> P;       // pressure global ids
+  std::vector<int> ents;        // entity ids (sorted by entity id)
+  std::vector<int> ent_offG, ent_offD, ent_offP;
+  int nI = 0, nP = 0, nG = 0, nD = 0, n = 0, nd = 0, npi = 0;
+  int64_t off_K = 0;            // dense (n x n) subdomain matrix, column-major, ld = n
+  int64_t off_ST = 0;           // dense transformed Schur S_T (nG x nG), column-major
+  int64_t off_STp = 0;          // packed tiles of S_T
+  int64_t off_SDi = 0;          // packed tiles of S_DD^-1
+  int64_t off_Phi = 0;          // Phi (nd x npi), row-major
+  int64_t off_Sc = 0;           // S_c (npi x npi) column-major
+  int64_t off_vecG = 0;         // offset into per-subdomain vectors of length nG
+  int64_t off_vecD = 0;         // offset into per-subdomain vectors of length nd
+  int64_t off_vecPi = 0;        // offset into per-subdomain vectors of length npi
+  int64_t off_vecDfull = 0;     // offset into per-subdomain vectors of length nD
+  int color = 0;
+  double vol = 0, gamma = 0;
+};
+
+// Device-side descriptors (plain data, uploaded once).
+struct SubDev {
+  int nI, nP, nG, nD, n, nd, npi;
+  int cell_begin, cell_end;   // into sub_cells
+  int slot_begin, slot_end;   // into the subdomain-major slot index list
+  int pad;
+  int64_t off_K;              // dense n x n (column-major, ld = n)
+  int64_t off_ST;             // dense nG x nG: S_T, then its partial LDL^T
+  int64_t off_STp;            // packed tiles of S_T
+  int64_t off_SDi;            // packed tiles of S_DD^-1
+  int64_t off_Phi;            // Phi, nd x npi column-major
+  int64_t off_G;              // offset into length-nG per-subdomain vectors
+  int64_t off_Dv;             // offset into length-nd vectors
+  int64_t off_Pi;             // offset into length-npi vectors
+  int64_t off_P;              // offset into length-nP vectors
+  int64_t off_I;              // offset into length-nI vectors
+  int64_t off_Dn;             // offset into length-nD vectors
+  int64_t off_X;              // scratch square (nG x nG) offset
+  double vol, gamma;
+};
+
+struct SlotDev {              // one (entity, sharer) pair; slots are entity-major
+  int sub, ent, n, nd, r;
+  int offG;                   // local original-Gamma offset in the subdomain
+  int offD;                   // local dual offset (0..nd_sub)
+  int offPi;                  // local primal offset (0..npi_sub)
+  int64_t off_T;              // T_G of the entity
+  int64_t off_Dlx;            // deluxe block D_G^(sub) (nd x nd, column-major)
+  int64_t off_side;           // scratch for S_GD^(sub)
+};
+
+struct EntDev {
+  int n, nd, r, nsides, side_begin, kind, nrowsC, pad;
+  int64_t off_T, off_C, off_xd, off_pi, off_gam, off_sum, off_W;
+};
+
+struct KTimer {
+  std::string name;
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+}  // namespace vb
+
+struct vb_ctx {
+  // ---------------- configuration
+  int k = 2;
+  vb_constraints cons{};
+  int rank = 0, nranks = 1, device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int state = 0;  // 1 = setup, 2 = factored
+  // ---------------- mesh (host copy)
+  int64_t nV = 0, nF = 0, nK = 0, nE = 0;
+  std::vector<double> xyz;
+  std::vector<int64_t> face_ptr, face_vtx, cell_ptr, cell_face;
+  std::vector<int8_t> cell_sign;
+  std::vector<uint8_t> face_bnd;
+  std::vector<int64_t> edges;        // [nE][2] (a<b), lexicographic
+  std::vector<double> nu;
+  // ---------------- DOF numbering
+  int nm = 0, n4 = 0, n5 = 0, np = 0, nv_max = 0;
+  int64_t oE = 0, oF = 0, oC = 0, nvel = 0, npres = 0;
+  std::vector<int64_t> vel2free;     // -1 for Dirichlet DOFs
+  std::vector<int64_t> free2vel;
+  int64_t n_free_vel = 0;
+  // per cell local topology
+  std::vector<int> cell_nv;              // local velocity dof count
+  std::vector<int64_t> cell_l2g_ptr;     // CSR into cell_l2g (velocity global ids)
+  std::vector<int64_t> cell_l2g;
+  std::vector<int> cell_topo;            // packed local topology for the element kernel
+  int topo_stride = 0;
+  // ---------------- subdomains / entities
+  int N = 0;
+  std::vector<int> cell_sub;
+  std::vector<vb::Sub> subs;
+  std::vector<vb::Entity> ents;
+  int64_t nGamma = 0;                // number of interface (original) DOFs
+  int64_t n_delta_glob = 0;          // global dual coordinates
+  int64_t NPi = 0;                   // global primal count
+  int64_t nx = 0;                    // PCG vector length = n_delta_glob + NPi + N
+  int ncolors = 0;
+  // ---------------- device data
+  vb::DBuf<double> d_xyz, d_nu;
+  vb::DBuf<int> d_topo;
+  vb::DBuf<double> d_elA, d_elB;     // element matrices: A [nK][nv_max^2], B [nK][np*nv_max]
+  vb::DBuf<int64_t> d_cell_l2g;      // [nK][nv_max] global velocity ids (-1 pad)
+  vb::DBuf<int> d_cell_loc;          // [nK][nv_max + np] position in subdomain matrix (-1 = drop)
+  vb::DBuf<int> d_cell_nv;
+  vb::DBuf<int64_t> d_vel2free;
+  double flux_violation = 0;
+  void *solve_state = nullptr;
+  int debug = 0;
+  vb::DBuf<double> w_hostio;
+  int max_npi = 0, geo_stride = 0;
+  std::vector<double> cellgeo;       // host copy of d_cellgeo
+  vb::DBuf<double> d_K;              // subdomain dense matrices
+  vb::DBuf<double> d_ST, d_STp, d_SDi, d_Phi, d_Sc;
+  vb::DBuf<double> d_T, d_C, d_Dlx;  // per-entity T_G, constraint rows, deluxe blocks
+  vb::DBuf<double> d_Kc, d_Kcp;      // coarse dense & packed inverse
+  int64_t Nc = 0;
+  // descriptors
+  std::vector<vb::SubDev> h_sub;
+  std::vector<vb::SlotDev> h_slot;
+  std::vector<vb::EntDev> h_ent;
+  std::vector<int> h_sub_slots;      // subdomain-major list of slot ids
+  vb::DBuf<vb::SubDev> d_sub;
+  vb::DBuf<vb::SlotDev> d_slot;
+  vb::DBuf<vb::EntDev> d_ent;
+  vb::DBuf<int> d_sub_slots, d_sub_cells;
+  int64_t len_G = 0, len_Dv = 0, len_Pi = 0, len_P = 0, len_I = 0, len_Dn = 0;
+  int64_t len_K = 0, len_ST = 0, len_STp = 0, len_SDi = 0, len_Phi = 0, len_X = 0;
+  int64_t len_T = 0, len_Dlx = 0, len_side = 0, len_sum = 0, len_W = 0;
+  // per-subdomain vectors
+  vb::DBuf<double> d_b0;             // original flux row on local Gamma (len_G)
+  vb::DBuf<double> d_b0T;            // transformed flux row on local Pi (len_Pi)
+  vb::DBuf<double> d_cvec, d_mvec;   // D_Q of q = 1 and int psi_j (len_P)
+  vb::DBuf<int64_t> d_loc2x;         // local transformed coord -> x index (len_G)
+  vb::DBuf<int64_t> d_subG_free;     // local original Gamma -> free vel id (len_G)
+  vb::DBuf<int64_t> d_subI_free;     // interior -> free vel id (len_I)
+  vb::DBuf<int64_t> d_subP_glob;     // pressure -> pressure global id (len_P)
+  vb::DBuf<int64_t> d_pi_glob;       // local primal -> global primal index (len_Pi)
+  // x coordinate -> local copies (sub-local transformed positions, global offsets into len_G)
+  vb::DBuf<int64_t> d_xcopy_ptr, d_xcopy;
+  vb::DBuf<int64_t> d_gam_free;      // interface DOFs (free ids), entity-major order
+  vb::DBuf<double> d_cellgeo;        // per cell: vol, centroid(3), h, c-vector(np)
+  vb::DBuf<int> d_info;
+  // solve workspaces
+  vb::DBuf<double> w_x, w_r, w_z, w_p, w_q, w_part, w_locD, w_locY, w_locC, w_uc, w_rc, w_ucp,
+      w_scal, w_gam, w_bD, w_zG, w_dots, w_elt;
+  vb::DBuf<int> d_op_work, d_loc_work, d_c_work;   // packed-GEMV chunk work lists
+  int n_op_work = 0, n_loc_work = 0, n_c_work = 0, P_op = 4, P_loc = 4, P_c = 296;
+  vb::DBuf<int64_t> d_op_part_off, d_loc_part_off;
+  vb::DBuf<int64_t> d_el_ptr, d_el_ent;   // K7: free dof -> (cell, local) contributions
+  double bytes_per_iter = 0;
+  // timing
+  bool timing = false;
+  std::vector<double> ktime_ms;
+  std::vector<std::string> ktime_name;
+  double t_setup = 0, t_factor = 0;
+};

@@ -1,0 +1,363 @@
+// Host-side structural setup of a vb_ctx: edges, DOF numbering, local cell
+// topology, subdomain/interface classification and constraint rows.
+// This is index bookkeeping and O(#interface DOFs) geometry; every O(n^2)/O(n^3) numeric step
+// of the method runs on the device (vem.cu, dense.cu, factor.cu, solve.cu).
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <numeric>
+#include "internal.h"
+#include "setup.h"
+
+namespace vb {
+
+// ------------------------------------------------------------------ quadrature nodes (host)
+static double legendre(int n, double x, double *dp) {
+  double p0 = 1, p1 = x;
+  if (n == 0) { *dp = 0; return 1; }
+  for (int k = 2; k <= n; ++k) {
+    double p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+    p0 = p1; p1 = p2;
+  }
+  *dp = n * (x * p1 - p0) / (x * x - 1);
+  return p1;
+}
+
+void gauss_legendre01(int n, double *x, double *w) {
+  for (int i = 0; i < n; ++i) {
+    double z = cos(M_PI * (i + 0.75) / (n + 0.5)), dp = 0;
+    for (int it = 0; it < 100; ++it) {
+      double p = legendre(n, z, &dp);
+      double dz = p / dp;
+      z -= dz;
+      if (fabs(dz) < 1e-16) break;
+    }
+    legendre(n, z, &dp);
+    x[n - 1 - i] = 0.5 * (z + 1);
+    w[n - 1 - i] = 1.0 / ((1 - z * z) * dp * dp);   // 2/((1-z^2)P'^2) scaled by 1/2
+  }
+}
+
+void gauss_lobatto01(int npts, double *x, double *w) {
+  int m = npts - 1;
+  x[0] = 0; x[m] = 1;
+  // interior nodes: roots of P'_m, found by Newton on P'_m using the GL roots of degree m-1 as guess
+  for (int i = 1; i < m; ++i) {
+    double z = -cos(M_PI * i / m);
+    for (int it = 0; it < 200; ++it) {
+      // P'_m and P''_m via Legendre ODE: (1-z^2)P'' = 2z P' - m(m+1)P
+      double dp, p = legendre(m, z, &dp);
+      double d2 = (2 * z * dp - m * (m + 1) * p) / (1 - z * z);
+      double dz = dp / d2;
+      z -= dz;
+      if (fabs(dz) < 1e-16) break;
+    }
+    x[i] = 0.5 * (z + 1);
+  }
+  for (int i = 0; i <= m; ++i) {
+    double z = 2 * x[i] - 1, dp;
+    double p = legendre(m, z, &dp);
+    w[i] = 1.0 / (m * (m + 1) * p * p);   // (2/(m(m+1)P^2)) / 2
+  }
+}
+
+static inline int dim2(int n) { return n < 0 ? 0 : (n + 1) * (n + 2) / 2; }
+static inline int dim3(int n) { return n < 0 ? 0 : (n + 1) * (n + 2) * (n + 3) / 6; }
+
+// ------------------------------------------------------------------ topology and numbering
+void build_topology(vb_ctx *c, const vb_mesh *m) {
+  int k = c->k;
+  c->nV = m->n_vertices; c->nF = m->n_faces; c->nK = m->n_cells;
+  c->xyz.assign(m->xyz, m->xyz + 3 * c->nV);
+  c->face_ptr.assign(m->face_ptr, m->face_ptr + c->nF + 1);
+  c->face_vtx.assign(m->face_vtx, m->face_vtx + c->face_ptr[c->nF]);
+  c->cell_ptr.assign(m->cell_ptr, m->cell_ptr + c->nK + 1);
+  c->cell_face.assign(m->cell_face, m->cell_face + c->cell_ptr[c->nK]);
+  c->cell_sign.assign(m->cell_face_sign, m->cell_face_sign + c->cell_ptr[c->nK]);
+  c->face_bnd.assign(m->face_on_dirichlet, m->face_on_dirichlet + c->nF);
+  // edges: unique (min,max) pairs of loop edges, lexicographic
+  std::vector<int64_t> keys;
+  keys.reserve(c->face_vtx.size());
+  int64_t nV = c->nV;
+  for (int64_t f = 0; f < c->nF; ++f) {
+    int64_t s = c->face_ptr[f], e = c->face_ptr[f + 1];
+    VB_REQUIRE(e - s >= 3 && e - s <= MAXL, VB_EINVAL, "face " + std::to_string(f) + " has an unsupported loop length");
+    for (int64_t i = s; i < e; ++i) {
+      int64_t a = c->face_vtx[i], b = c->face_vtx[i + 1 < e ? i + 1 : s];
+      keys.push_back(std::min(a, b) * nV + std::max(a, b));
+    }
+  }
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  c->nE = keys.size();
+  c->edges.resize(2 * c->nE);
+  for (int64_t i = 0; i < c->nE; ++i) { c->edges[2 * i] = keys[i] / nV; c->edges[2 * i + 1] = keys[i] % nV; }
+  auto edge_id = [&](int64_t a, int64_t b) {
+    int64_t key = std::min(a, b) * nV + std::max(a, b);
+    return (int64_t)(std::lower_bound(keys.begin(), keys.end(), key) - keys.begin());
+  };
+  // numbering (identical convention to DESIGN.md §Layout)
+  c->nm = dim2(k - 2);
+  c->n4 = 3 * dim3(k - 3) - dim3(k - 4);
+  c->n5 = dim3(k - 1) - 1;
+  c->np = dim3(k - 1);
+  c->oE = 3 * c->nV;
+  c->oF = c->oE + 3 * (k - 1) * c->nE;
+  c->oC = c->oF + 3 * (int64_t)c->nm * c->nF;
+  c->nvel = c->oC + c->nK * (c->n4 + c->n5);
+  c->npres = c->nK * c->np;
+  // boundary DOFs
+  std::vector<char> isb(c->nvel, 0);
+  for (int64_t f = 0; f < c->nF; ++f) {
+    if (!c->face_bnd[f]) continue;
+    int64_t s = c->face_ptr[f], e = c->face_ptr[f + 1];
+    for (int64_t i = s; i < e; ++i) {
+      int64_t a = c->face_vtx[i], b = c->face_vtx[i + 1 < e ? i + 1 : s];
+      for (int q = 0; q < 3; ++q) isb[3 * a + q] = 1;
+      int64_t ed = edge_id(a, b);
+      for (int q = 0; q < 3 * (k - 1); ++q) isb[c->oE + 3 * (k - 1) * ed + q] = 1;
+    }
+    for (int q = 0; q < 3 * c->nm; ++q) isb[c->oF + 3 * c->nm * f + q] = 1;
+  }
+  c->vel2free.assign(c->nvel, -1);
+  c->free2vel.clear();
+  for (int64_t g = 0; g < c->nvel; ++g)
+    if (!isb[g]) { c->vel2free[g] = c->free2vel.size(); c->free2vel.push_back(g); }
+  c->n_free_vel = c->free2vel.size();
+  // per-cell local topology (vertices / edges / faces in increasing global id)
+  c->topo_stride = TOPO_STRIDE;
+  c->cell_topo.assign((size_t)c->nK * TOPO_STRIDE, 0);
+  c->cell_nv.resize(c->nK);
+  c->cell_l2g_ptr.assign(c->nK + 1, 0);
+  c->cell_l2g.clear();
+  c->nv_max = 0;
+  for (int64_t K = 0; K < c->nK; ++K) {
+    int64_t s = c->cell_ptr[K], e = c->cell_ptr[K + 1];
+    int nf = e - s;
+    VB_REQUIRE(nf >= 4 && nf <= MAXF, VB_EINVAL, "cell " + std::to_string(K) + " has an unsupported face count");
+    std::vector<std::pair<int64_t, int>> fl;
+    for (int64_t j = s; j < e; ++j) fl.push_back({c->cell_face[j], (int)c->cell_sign[j]});
+    std::sort(fl.begin(), fl.end());
+    std::vector<int64_t> vs, es;
+    for (auto &fs : fl) {
+      int64_t a0 = c->face_ptr[fs.first], a1 = c->face_ptr[fs.first + 1];
+      for (int64_t i = a0; i < a1; ++i) {
+        vs.push_back(c->face_vtx[i]);
+        es.push_back(edge_id(c->face_vtx[i], c->face_vtx[i + 1 < a1 ? i + 1 : a0]));
+      }
+    }
+    std::sort(vs.begin(), vs.end()); vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
+    std::sort(es.begin(), es.end()); es.erase(std::unique(es.begin(), es.end()), es.end());
+    VB_REQUIRE((int)vs.size() <= MAXV && (int)es.size() <= MAXE, VB_EINVAL,
+               "cell " + std::to_string(K) + " exceeds the supported vertex/edge count");
+    int *T = &c->cell_topo[(size_t)K * TOPO_STRIDE];
+    T[0] = vs.size(); T[1] = es.size(); T[2] = nf;
+    for (size_t i = 0; i < vs.size(); ++i) T[TOPO_V + i] = (int)vs[i];
+    auto lv = [&](int64_t g) { return (int)(std::lower_bound(vs.begin(), vs.end(), g) - vs.begin()); };
+    for (size_t i = 0; i < es.size(); ++i) {
+      T[TOPO_E + 2 * i] = lv(c->edges[2 * es[i]]);
+      T[TOPO_E + 2 * i + 1] = lv(c->edges[2 * es[i] + 1]);
+    }
+    for (int f = 0; f < nf; ++f) {
+      int *F = T + TOPO_F + f * FACE_STRIDE;
+      int64_t gf = fl[f].first, a0 = c->face_ptr[gf], a1 = c->face_ptr[gf + 1];
+      F[0] = fl[f].second; F[1] = a1 - a0;
+      for (int64_t i = a0; i < a1; ++i) {
+        int64_t a = c->face_vtx[i], b = c->face_vtx[i + 1 < a1 ? i + 1 : a0];
+        int q = i - a0;
+        F[2 + q] = lv(a);
+        F[2 + MAXL + q] = (int)(std::lower_bound(es.begin(), es.end(), edge_id(a, b)) - es.begin());
+        F[2 + 2 * MAXL + q] = a < b ? 1 : 0;
+      }
+    }
+    // local -> global velocity map (vertices, edges, faces, cell)
+    int nv = 3 * vs.size() + 3 * (k - 1) * es.size() + 3 * c->nm * nf + c->n4 + c->n5;
+    c->cell_nv[K] = nv;
+    c->nv_max = std::max(c->nv_max, nv);
+    for (auto g : vs) for (int q = 0; q < 3; ++q) c->cell_l2g.push_back(3 * g + q);
+    for (auto ed : es) for (int q = 0; q < 3 * (k - 1); ++q) c->cell_l2g.push_back(c->oE + 3 * (k - 1) * ed + q);
+    for (auto &fs : fl) for (int q = 0; q < 3 * c->nm; ++q) c->cell_l2g.push_back(c->oF + 3 * c->nm * fs.first + q);
+    for (int q = 0; q < c->n4 + c->n5; ++q) c->cell_l2g.push_back(c->oC + K * (c->n4 + c->n5) + q);
+    c->cell_l2g_ptr[K + 1] = c->cell_l2g.size();
+  }
+}
+
+// ------------------------------------------------------------------ subdomains and entities
+void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int N) {
+  c->N = N;
+  c->cell_sub.assign(cell_sub, cell_sub + c->nK);
+  c->subs.assign(N, Sub());
+  for (int64_t K = 0; K < c->nK; ++K) {
+    VB_REQUIRE(cell_sub[K] >= 0 && cell_sub[K] < N, VB_EINVAL, "cell_subdomain out of range");
+    c->subs[cell_sub[K]].cells.push_back(K);
+  }
+  // (free dof, subdomain) pairs -> sharer sets
+  std::vector<std::pair<int64_t, int>> ds;
+  for (int64_t K = 0; K < c->nK; ++K)
+    for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) {
+      int64_t f = c->vel2free[c->cell_l2g[j]];
+      if (f >= 0) ds.push_back({f, cell_sub[K]});
+    }
+  std::sort(ds.begin(), ds.end());
+  ds.erase(std::unique(ds.begin(), ds.end()), ds.end());
+  std::map<std::vector<int>, int> emap;
+  std::vector<std::vector<int>> ekeys;
+  std::vector<std::vector<int64_t>> edofs;
+  std::vector<int> owner_sub(c->n_free_vel, -1);   // for interior dofs
+  for (size_t i = 0; i < ds.size();) {
+    size_t j = i;
+    std::vector<int> sh;
+    while (j < ds.size() && ds[j].first == ds[i].first) sh.push_back(ds[j++].second);
+    if (sh.size() == 1) {
+      owner_sub[ds[i].first] = sh[0];
+    } else {
+      auto it = emap.find(sh);
+      int e;
+      if (it == emap.end()) { e = ekeys.size(); emap[sh] = e; ekeys.push_back(sh); edofs.push_back({}); }
+      else e = it->second;
+      edofs[e].push_back(ds[i].first);
+    }
+    i = j;
+  }
+  // entities ordered by their smallest DOF
+  std::vector<int> order(ekeys.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return edofs[a][0] < edofs[b][0]; });
+  c->ents.assign(order.size(), Entity());
+  c->nGamma = 0;
+  for (size_t q = 0; q < order.size(); ++q) {
+    Entity &E = c->ents[q];
+    E.sharers = ekeys[order[q]];
+    E.dofs = edofs[order[q]];
+    E.n = E.dofs.size();
+    c->nGamma += E.n;
+    bool vert = true;
+    int64_t v0 = c->free2vel[E.dofs[0]] / 3;
+    for (auto d : E.dofs) { int64_t g = c->free2vel[d]; if (g >= c->oE || g / 3 != v0) vert = false; }
+    E.kind = vert ? 0 : (E.sharers.size() == 2 ? 2 : 1);
+    for (int s : E.sharers) c->subs[s].ents.push_back(q);
+  }
+  // per-subdomain orderings
+  std::vector<int64_t> posI(c->n_free_vel, -1);
+  for (int i = 0; i < N; ++i) {
+    Sub &S = c->subs[i];
+    std::sort(S.ents.begin(), S.ents.end());
+    std::vector<int64_t> fr;
+    for (int K : S.cells) {
+      for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) {
+        int64_t f = c->vel2free[c->cell_l2g[j]];
+        if (f >= 0 && owner_sub[f] == i) fr.push_back(f);
+      }
+      for (int q = 0; q < c->np; ++q) S.P.push_back((int64_t)K * c->np + q);
+    }
+    std::sort(fr.begin(), fr.end()); fr.erase(std::unique(fr.begin(), fr.end()), fr.end());
+    S.I = fr;
+    std::sort(S.P.begin(), S.P.end());
+    S.nI = S.I.size(); S.nP = S.P.size();
+    S.nG = 0;
+    for (int e : S.ents) { S.ent_offG.push_back(S.nG); S.nG += c->ents[e].n; }
+    S.nD = S.nI + S.nP;
+    S.n = S.nD + S.nG;
+  }
+}
+
+// ------------------------------------------------------------------ face geometry (host)
+void face_frame(const vb_ctx *c, int64_t f, double *area, double n[3], double t1[3], double t2[3]) {
+  int64_t s = c->face_ptr[f], e = c->face_ptr[f + 1];
+  double av[3] = {0, 0, 0};
+  for (int64_t i = s; i < e; ++i) {
+    const double *p = &c->xyz[3 * c->face_vtx[i]];
+    const double *q = &c->xyz[3 * c->face_vtx[i + 1 < e ? i + 1 : s]];
+    av[0] += 0.5 * (p[1] * q[2] - p[2] * q[1]);
+    av[1] += 0.5 * (p[2] * q[0] - p[0] * q[2]);
+    av[2] += 0.5 * (p[0] * q[1] - p[1] * q[0]);
+  }
+  double a = sqrt(av[0] * av[0] + av[1] * av[1] + av[2] * av[2]);
+  *area = a;
+  for (int q = 0; q < 3; ++q) n[q] = av[q] / a;
+  const double *p0 = &c->xyz[3 * c->face_vtx[s]], *p1 = &c->xyz[3 * c->face_vtx[s + 1]];
+  double d[3] = {p1[0] - p0[0], p1[1] - p0[1], p1[2] - p0[2]};
+  double l = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  for (int q = 0; q < 3; ++q) t1[q] = d[q] / l;
+  t2[0] = n[1] * t1[2] - n[2] * t1[1];
+  t2[1] = n[2] * t1[0] - n[0] * t1[2];
+  t2[2] = n[0] * t1[1] - n[1] * t1[0];
+}
+
+// Constraint rows C_G (SURVEY O-9 / A8) as dense rows over the entity's DOFs.
+void build_constraint_rows(vb_ctx *c, std::vector<double> &rows_out) {
+  int k = c->k;
+  double xg[8], wg[8];
+  gauss_lobatto01(k + 1, xg, wg);
+  // face sign w.r.t. the first sharer: from any cell of that subdomain containing the face
+  std::vector<int> fsgn_cell(c->nF * 2, 0);
+  std::vector<int> fcell(c->nF * 2, -1);
+  for (int64_t K = 0; K < c->nK; ++K)
+    for (int64_t j = c->cell_ptr[K]; j < c->cell_ptr[K + 1]; ++j) {
+      int64_t f = c->cell_face[j];
+      int slot = fcell[2 * f] < 0 ? 0 : 1;
+      fcell[2 * f + slot] = K;
+      fsgn_cell[2 * f + slot] = c->cell_sign[j];
+    }
+  rows_out.clear();
+  for (auto &E : c->ents) {
+    int n = E.n;
+    std::vector<std::vector<double>> R;
+    auto pos = [&](int64_t gvel) {
+      int64_t f = c->vel2free[gvel];
+      auto it = std::lower_bound(E.dofs.begin(), E.dofs.end(), f);
+      return (it != E.dofs.end() && *it == f) ? (int)(it - E.dofs.begin()) : -1;
+    };
+    if (c->cons.svd_rel_tol < 0) {  // internal: all DOFs primal (exact-limit test)
+      for (int j = 0; j < n; ++j) { std::vector<double> r(n, 0.0); r[j] = 1; R.push_back(r); }
+    } else if (E.kind == 0) {
+      if (c->cons.vertex)
+        for (int q = 0; q < 3; ++q) { std::vector<double> r(n, 0.0); r[q] = 1; R.push_back(r); }
+    } else if (E.kind == 1) {
+      if (c->cons.edge_avg) {
+        std::vector<std::vector<double>> r3(3, std::vector<double>(n, 0.0));
+        std::vector<int64_t> eids;
+        for (auto d : E.dofs) { int64_t g = c->free2vel[d]; if (g >= c->oE && g < c->oF) eids.push_back((g - c->oE) / (3 * (k - 1))); }
+        std::sort(eids.begin(), eids.end()); eids.erase(std::unique(eids.begin(), eids.end()), eids.end());
+        for (auto ed : eids) {
+          int64_t a = c->edges[2 * ed], b = c->edges[2 * ed + 1];
+          double L = 0;
+          for (int q = 0; q < 3; ++q) L += (c->xyz[3 * b + q] - c->xyz[3 * a + q]) * (c->xyz[3 * b + q] - c->xyz[3 * a + q]);
+          L = sqrt(L);
+          for (int d = 0; d < 3; ++d) {
+            for (int j = 0; j < k - 1; ++j) r3[d][pos(c->oE + 3 * (k - 1) * ed + 3 * j + d)] += L * wg[j + 1];
+            int pa = pos(3 * a + d), pb = pos(3 * b + d);
+            if (pa >= 0) r3[d][pa] += L * wg[0];
+            if (pb >= 0) r3[d][pb] += L * wg[k];
+          }
+        }
+        for (int d = 0; d < 3; ++d) R.push_back(r3[d]);
+      }
+    } else {
+      std::vector<std::vector<double>> avg(3, std::vector<double>(n, 0.0));
+      std::vector<double> flux(n, 0.0);
+      std::vector<int64_t> fids;
+      for (auto d : E.dofs) { int64_t g = c->free2vel[d]; if (g >= c->oF && g < c->oC) fids.push_back((g - c->oF) / (3 * c->nm)); }
+      std::sort(fids.begin(), fids.end()); fids.erase(std::unique(fids.begin(), fids.end()), fids.end());
+      int s0 = E.sharers[0];
+      for (auto f : fids) {
+        double area, nn[3], t1[3], t2[3];
+        face_frame(c, f, &area, nn, t1, t2);
+        int sg = (fcell[2 * f] >= 0 && c->cell_sub[fcell[2 * f]] == s0) ? fsgn_cell[2 * f] : fsgn_cell[2 * f + 1];
+        const double *tau[3] = {nn, t1, t2};
+        for (int t = 0; t < 3; ++t) {
+          int col = pos(c->oF + 3 * c->nm * f + t * c->nm);
+          for (int d = 0; d < 3; ++d) avg[d][col] += area * tau[t][d];
+        }
+        flux[pos(c->oF + 3 * c->nm * f)] += sg * area;
+      }
+      if (c->cons.face_avg) for (int d = 0; d < 3; ++d) R.push_back(avg[d]);
+      if (c->cons.face_flux) R.push_back(flux);
+    }
+    E.nrows_C = R.size();
+    E.off_C = rows_out.size();
+    for (auto &r : R) rows_out.insert(rows_out.end(), r.begin(), r.end());
+  }
+}
+
+}  // namespace vb

@@ -1,0 +1,51 @@
+#pragma once
+#include "internal.h"
+
+namespace vb {
+// Local cell topology packing (one int block of TOPO_STRIDE per cell).
+constexpr int MAXV = 8;      // vertices per cell (hexahedra, jittered/triangulated hexahedra)
+constexpr int MAXE = 18;     // edges per cell
+constexpr int MAXF = 12;     // faces per cell
+constexpr int MAXL = 4;      // vertices per face loop
+constexpr int FACE_STRIDE = 2 + 3 * MAXL;    // sign, len, loop vertices, loop edges, forward flags
+constexpr int TOPO_V = 3;
+constexpr int TOPO_E = TOPO_V + MAXV;
+constexpr int TOPO_F = TOPO_E + 2 * MAXE;
+constexpr int TOPO_STRIDE = TOPO_F + MAXF * FACE_STRIDE;
+
+// VB_DEBUG=1: synchronise and check after every stage, naming it in the error.
+inline void dbg(vb_ctx *c, const char *what) {
+  if (!c->debug) return;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error{VB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+#define VB_STR_(x) #x
+#define VB_XSTR(x) VB_STR_(x)
+#define VB_STAGE()                                                                              \
+  do {                                                                                          \
+    VB_CHECK_LAUNCH();                                                                          \
+    dbg(c, __FILE__ ":" VB_XSTR(__LINE__));                                                     \
+  } while (0)
+
+void gauss_legendre01(int n, double *x, double *w);
+void gauss_lobatto01(int npts, double *x, double *w);
+void build_topology(vb_ctx *c, const vb_mesh *m);
+void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int N);
+void face_frame(const vb_ctx *c, int64_t f, double *area, double n[3], double t1[3], double t2[3]);
+void build_constraint_rows(vb_ctx *c, std::vector<double> &rows_out);
+
+// device-side stages (defined in the .cu files)
+void cell_geometry_device(vb_ctx *c);                    // vem.cu
+void layout_phase_a(vb_ctx *c);                          // abi.cu
+void build_transformed_maps(vb_ctx *c);                  // abi.cu (after the entity ranks)
+void prepare_solve(vb_ctx *c);                           // solve.cu
+void destroy_solve_state(vb_ctx *c);                     // solve.cu
+void element_matrices_device(vb_ctx *c);                 // vem.cu  (K9)
+void build_rhs_device(vb_ctx *c, const vb_problem *p, double *rhs);   // vem.cu
+void factor_device(vb_ctx *c);                           // factor.cu
+void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit, vb_report *rep);
+void apply_operator_device(vb_ctx *c, const double *x, double *y);    // solve.cu (K7)
+void debug_interface_op(vb_ctx *c, int which, const double *in, double *out);   // solve.cu
+}  // namespace vb

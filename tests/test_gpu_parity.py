@@ -1,0 +1,92 @@
+"""GPU-vs-oracle parity through the C ABI (SURVEY §8(c) parity metrics):
+solution rel. L2 <= 1e-8 (velocity and pressure blocks), final rel. residual <= 1e-10 with the same
+stopping rule, iterations within +-1, Lanczos kappa within 1%."""
+import numpy as np
+import pytest
+
+from synthetic import make_problem
+
+pytestmark = pytest.mark.gpu
+
+TOL_SOL = 1e-8
+
+
+def _oracle(prob, rtol=1e-10, **bkw):
+    from oracle.assemble import GlobalSystem
+    from oracle.bddc import BDDC
+    gs = GlobalSystem(prob)
+    bd = BDDC(gs, **bkw)
+    u, p, rep = bd.solve(rtol=rtol)
+    return gs, bd, u, p, rep
+
+
+def _elements(gs):
+    pa, A, pb, B = [0], [], [0], []
+    for K in range(gs.prob.mesh.n_cells):
+        op = gs.el.op(K)
+        A.append((gs.prob.nu_cell[K] * op.A).ravel()); B.append(op.B.ravel())
+        pa.append(pa[-1] + op.A.size); pb.append(pb[-1] + op.B.size)
+    return np.array(pa), np.concatenate(A), np.array(pb), np.concatenate(B)
+
+
+def _compare(ctx, gs, u_o, p_o, rep_o, rhs, rtol=1e-10):
+    import torch
+    dev = torch.device("cuda")
+    n = ctx.n_free
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    rep = ctx.pcg_solve(rhs, x, rtol=rtol)
+    xh = x.cpu().numpy()
+    u, p = xh[:ctx.n_vel], xh[ctx.n_vel:]
+    du = np.linalg.norm(u - u_o) / np.linalg.norm(u_o)
+    dp = np.linalg.norm(p - p_o) / np.linalg.norm(p_o)
+    assert rep["rel_residual"] <= rtol
+    assert abs(rep["iterations"] - rep_o["iterations"]) <= 1, (rep["iterations"], rep_o["iterations"])
+    assert abs(rep["kappa"] - rep_o["kappa"]) <= 0.01 * rep_o["kappa"], (rep["kappa"], rep_o["kappa"])
+    assert du <= TOL_SOL and dp <= TOL_SOL, (du, dp)
+    return rep, du, dp
+
+
+@pytest.mark.parametrize("name,kw", [("c1", {}), ("c1", dict(n=8, sub=(4, 4, 4)))])
+def test_interface_operators_parity(name, kw):
+    """S^ and M^-1 (Eq.(globInt), Eq.(BDDCprec)) applied to random vectors, GPU vs oracle (1e-11)."""
+    import paper_2304_09770_b200 as vb
+    from oracle.assemble import GlobalSystem
+    from oracle.bddc import BDDC
+    prob = make_problem(name, **kw)
+    gs = GlobalSystem(prob)
+    bd = BDDC(gs)
+    ctx = vb.context_for(prob, elements=_elements(gs))
+    ctx.factor()
+    gid = ctx.interface_dofs()
+    pos = {int(d): i for i, d in enumerate(bd.gamma)}
+    perm = np.array([pos[int(d)] for d in gid])
+    rng = np.random.default_rng(7)
+    for which, fn in (("S", bd.apply_S), ("M", bd.apply_M)):
+        v = rng.standard_normal(bd.nG + bd.N)
+        v[bd.nG:] -= v[bd.nG:].mean()
+        y = fn(v)
+        yg = ctx.interface_op(which, np.concatenate([v[:bd.nG][perm], v[bd.nG:]]))
+        ref = np.concatenate([y[:bd.nG][perm], y[bd.nG:]])
+        err = np.linalg.norm(yg - ref) / np.linalg.norm(ref)
+        assert err < 1e-11, (which, err)
+
+
+@pytest.mark.parametrize("name,kw", [("c1", {}), ("c1", dict(n=8, sub=(4, 4, 4)))])
+def test_solver_parity_from_oracle_elements(name, kw):
+    """Solver-only parity: the library ingests the oracle's element matrices (bring-up entry)."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    prob = make_problem(name, **kw)
+    gs, bd, u_o, p_o, rep_o = _oracle(prob)
+    ctx = vb.context_for(prob, elements=_elements(gs))
+    # the library's local DOF order and global numbering equal the oracle's
+    for K in range(0, prob.mesh.n_cells, max(1, prob.mesh.n_cells // 17)):
+        v, p = ctx.cell_local_dofs(K)
+        iv, ip = gs.el.l2g[K]
+        assert np.array_equal(v, iv) and np.array_equal(p, ip)
+    assert ctx.n_vel == gs.dofs.n_free_vel
+    ctx.factor()
+    st = ctx.stats()
+    assert st["n_primal"] == bd.NPi
+    rhs = torch.tensor(np.concatenate([gs.rhs_u, gs.rhs_p]), dtype=torch.float64, device="cuda")
+    _compare(ctx, gs, u_o, p_o, rep_o, rhs)
