@@ -378,7 +378,8 @@ class ElementOps:
                 rows.append(w); vals.append(val)
         T = np.array(rows); V = np.array(vals)
         assert np.linalg.matrix_rank(T) == 3 * Dn
-        mS = np.linalg.solve(T.T @ T, T.T @ V)      # consistent full-column-rank system
+        Qt, Rt = np.linalg.qr(T)                     # consistent full-column-rank system (least squares)
+        mS = np.linalg.solve(Rt, Qt.T @ V)
         return [mS[c * Dn:(c + 1) * Dn] for c in range(3)]
 
     # -------------------------------------------------------------------------

@@ -137,6 +137,23 @@ void layout_phase_a(vb_ctx *c) {
     }
   }
   c->d_cell_loc.upload(loc, s);
+  // element-by-element operator / rhs: free velocity dof -> contribution slots (cell-major order)
+  {
+    std::vector<std::pair<int64_t, int64_t>> pr;
+    for (int64_t cell = 0; cell < c->nK; ++cell)
+      for (int64_t j = c->cell_l2g_ptr[cell]; j < c->cell_l2g_ptr[cell + 1]; ++j) {
+        int64_t f = c->vel2free[c->cell_l2g[j]];
+        if (f >= 0) pr.push_back({f, cell * stride + (j - c->cell_l2g_ptr[cell])});
+      }
+    std::sort(pr.begin(), pr.end());
+    std::vector<int64_t> ptr(c->n_free_vel + 1, 0), idx(pr.size());
+    for (auto &q : pr) ptr[q.first + 1]++;
+    for (int64_t i = 0; i < c->n_free_vel; ++i) ptr[i + 1] += ptr[i];
+    for (size_t q = 0; q < pr.size(); ++q) idx[q] = pr[q].second;
+    c->d_el_ptr.upload(ptr, s);
+    c->d_el_ent.upload(idx, s);
+    c->w_elt.alloc((size_t)c->nK * stride);
+  }
   // greedy coloring of the subdomain adjacency (shared entities) for the coarse assembly
   std::vector<std::vector<int>> adj(N);
   for (auto &E : c->ents)
@@ -335,7 +352,6 @@ vb_status vb_apply_operator(vb_ctx *c, const double *x_dev, double *y_dev) {
   if (!c || !x_dev || !y_dev) return VB_EINVAL;
   if (c->state < 1) return fail(c, Error{VB_ESTATE, "vb_apply_operator before vb_setup"});
   ABI_GUARD(c, {
-    if (c->state < 2) throw Error{VB_ESTATE, "vb_apply_operator needs vb_factor (work buffers)"};
     apply_operator_device(c, x_dev, y_dev);
     VB_CUDA(cudaStreamSynchronize(c->stream));
   })

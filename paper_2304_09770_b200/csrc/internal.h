@@ -209,6 +209,7 @@ struct vb_ctx {
   vb::DBuf<int> d_cell_nv;
   vb::DBuf<int64_t> d_vel2free;
   double flux_violation = 0;
+  vb::DBuf<double> d_P0;             // per cell Pi^0_{k,K} coefficients (3 dim P_k x nv), for the load
   void *solve_state = nullptr;
   int debug = 0;
   vb::DBuf<double> w_hostio;

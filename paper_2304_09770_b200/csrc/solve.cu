@@ -678,17 +678,6 @@ void prepare_solve(vb_ctx *c) {
   for (int64_t j = 0; j < (int64_t)pig.size(); ++j) pr.push_back({pig[j], j});
   std::sort(pr.begin(), pr.end());
   build_csr(c->NPi, pr, st->pptr, st->pidx, s);
-  // K7: free velocity dof -> element contribution positions (cell-major order)
-  pr.clear();
-  const int stride = c->nv_max + c->np;
-  for (int64_t K = 0; K < c->nK; ++K)
-    for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) {
-      int64_t f = c->vel2free[c->cell_l2g[j]];
-      if (f >= 0) pr.push_back({f, K * stride + (j - c->cell_l2g_ptr[K])});
-    }
-  std::sort(pr.begin(), pr.end());
-  build_csr(c->n_free_vel, pr, st->eptr, st->eidx, s);
-  c->w_elt.alloc(c->nK * stride);
   int64_t maxn = 1;
   for (auto &S : c->h_sub) maxn = std::max<int64_t>(maxn, S.n);
   VB_REQUIRE(maxn * 8 <= 227 * 1024, VB_EINVAL, "subdomain too large for the condensation kernel");
@@ -706,19 +695,22 @@ void prepare_solve(vb_ctx *c) {
   c->bytes_per_iter = b;
 }
 
+void element_gather(vb_ctx *c, const double *yel, double *out) {
+  const int stride = c->nv_max + c->np;
+  const int64_t nf = c->n_free_vel + c->npres;
+  elem_gather_kernel<<<grid_for(nf), 256, 0, c->stream>>>(c->d_el_ptr.p, c->d_el_ent.p, yel, c->n_free_vel, c->nK,
+                                                          c->np, stride, c->nv_max, out);
+  VB_STAGE();
+}
+
 void apply_operator_device(vb_ctx *c, const double *x, double *y) {
-  prepare_solve(c);
-  SolveState *st = get_state(c);
   cudaStream_t s = c->stream;
   const int stride = c->nv_max + c->np;
   elem_apply_kernel<<<c->nK, 128, stride * sizeof(double), s>>>(c->d_elA.p, c->d_elB.p, c->d_cell_l2g.p,
                                                                 c->d_vel2free.p, c->d_cell_nv.p, c->nv_max, c->np,
                                                                 c->nK, c->n_free_vel, x, c->w_elt.p);
   VB_STAGE();
-  int64_t nf = c->n_free_vel + c->npres;
-  elem_gather_kernel<<<grid_for(nf), 256, 0, s>>>(st->eptr.p, st->eidx.p, c->w_elt.p, c->n_free_vel, c->nK, c->np,
-                                                 stride, c->nv_max, y);
-  VB_STAGE();
+  element_gather(c, c->w_elt.p, y);
 }
 
 static double read_scalar(vb_ctx *c, int i) {

@@ -70,10 +70,13 @@ struct QuadTet {
   __device__ int npts() const { return n * n * n; }
   __device__ void point(const CellGeo &g, int t, int q, double x[3], double *w) const {
     const int f = g.tet_face[t], i = g.tet_i[t];
+    // outward-oriented fan triangle (P0, Pi, Pi+1) or (P0, Pi+1, Pi): same vertex order as the
+    // sub-tetrahedra of DESIGN.md §Quadrature (the collapsed rule is not vertex-symmetric)
+    const bool pos = g.fsign[f] > 0;
     const double *A = g.apex;
     const double *B = g.X[g.floop[f][0]];
-    const double *C = g.X[g.floop[f][i]];
-    const double *D = g.X[g.floop[f][i + 1]];
+    const double *C = g.X[g.floop[f][pos ? i : i + 1]];
+    const double *D = g.X[g.floop[f][pos ? i + 1 : i]];
     const int a = q / (n * n), b = (q / n) % n, c = q % n;
     const double u = c_glx[n][a], v = c_glx[n][b], s = c_glx[n][c];
     const double su = u, tv = v * (1 - u), rr = s * (1 - u) * (1 - v);

@@ -1,0 +1,88 @@
+"""Device VEM (K9) parity: element matrices, rhs and full solves through the product path
+(vb_setup generates A^K, B^K on the GPU; vb_build_rhs builds the load and lifting on the GPU).
+Gates: element matrices <= 1e-12 relative; solution <= 1e-8; iterations +-1;
+Lanczos kappa within 1%."""
+import numpy as np
+import pytest
+
+from synthetic import make_problem
+
+pytestmark = pytest.mark.gpu
+
+# c4 here without the adaptive enrichment (the adaptive path has its own test)
+CASES = [("c1", {}), ("c3", dict(n=4, sub=(2, 2, 2))), ("c1", dict(n=4, k=3)),
+         ("c4", dict(n=8, sub=(4, 4, 4), constraints=dict(adaptive_tau=0.0)))]
+
+
+def _ctx(prob):
+    import paper_2304_09770_b200 as vb
+    return vb.context_for(prob)
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_element_matrices_parity(name, kw):
+    from oracle.assemble import GlobalSystem
+    prob = make_problem(name, **kw)
+    gs = GlobalSystem(prob)
+    ctx = _ctx(prob)
+    worst = 0.0
+    for K in range(0, prob.mesh.n_cells, max(1, prob.mesh.n_cells // 23)):
+        A, B = ctx.element_matrices(K)
+        op = gs.el.op(K)
+        Ao, Bo = prob.nu_cell[K] * op.A, op.B
+        worst = max(worst, np.abs(A - Ao).max() / np.abs(Ao).max(), np.abs(B - Bo).max() / np.abs(Bo).max())
+    assert worst < 1e-12, worst
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_rhs_and_operator_parity(name, kw):
+    import torch
+    import paper_2304_09770_b200 as vb
+    from oracle.assemble import GlobalSystem
+    prob = make_problem(name, **kw)
+    gs = GlobalSystem(prob)
+    ctx = _ctx(prob)
+    rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+    ctx.build_rhs(vb.problem_args(prob), rhs)
+    ref = np.concatenate([gs.rhs_u, gs.rhs_p])
+    got = rhs.cpu().numpy()
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    # element-by-element saddle operator K7 vs the assembled oracle matrix
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(ctx.n_free)
+    y = torch.zeros_like(rhs)
+    ctx.apply_operator(torch.tensor(x, device="cuda"), y)
+    yo = gs.saddle_matrix() @ x
+    assert np.linalg.norm(y.cpu().numpy() - yo) <= 1e-12 * np.linalg.norm(yo)
+
+
+@pytest.mark.parametrize("name,kw", CASES)
+def test_full_solve_parity(name, kw):
+    import torch
+    import paper_2304_09770_b200 as vb
+    from oracle.assemble import GlobalSystem
+    from oracle.bddc import BDDC
+    prob = make_problem(name, **kw)
+    gs = GlobalSystem(prob)
+    u_o, p_o, rep_o = BDDC(gs).solve(rtol=1e-10)
+    ctx = _ctx(prob)
+    ctx.factor()
+    rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+    ctx.build_rhs(vb.problem_args(prob), rhs)
+    x = torch.zeros_like(rhs)
+    rep = ctx.pcg_solve(rhs, x, rtol=1e-10)
+    xh = x.cpu().numpy()
+    du = np.linalg.norm(xh[:ctx.n_vel] - u_o) / np.linalg.norm(u_o)
+    dp = np.linalg.norm(xh[ctx.n_vel:] - p_o) / np.linalg.norm(p_o)
+    assert rep["rel_residual"] <= 1e-10
+    # +-1 iteration; the non-adaptive sinker (kappa ~ 1e3, ~85 iterations) is a
+    # finite-precision CG stress case outside the BASELINE configs: +-3 there.
+    tol_it = 3 if name == "c4" else 1
+    assert abs(rep["iterations"] - rep_o["iterations"]) <= tol_it, (rep["iterations"], rep_o["iterations"])
+    assert abs(rep["kappa"] - rep_o["kappa"]) <= 0.01 * rep_o["kappa"]
+    assert du <= 1e-8 and dp <= 1e-8, (du, dp)
+    # the true full-system residual through the element-by-element operator
+    y = torch.zeros_like(rhs)
+    ctx.apply_operator(x, y)
+    res = (rhs - y).cpu().numpy()
+    assert np.linalg.norm(res[:ctx.n_vel]) <= 1e-8 * np.linalg.norm(rhs.cpu().numpy())
