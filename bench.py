@@ -1,0 +1,262 @@
+#!/usr/bin/env python
+"""Benchmark: PCG+BDDC solve of the divergence-free VEM Stokes system (BASELINE.json metric).
+
+A step = one vb_pcg_solve (rhs condensation B0, the whole PCG loop B1-B7 with the BDDC
+preconditioner, back-substitution B8) on the config-5 workload: 32^3 hexahedra (k=2) in 8^3
+subdomains of 4^3 cells per GPU, manufactured solution, vertex+edge+face constraints, deluxe
+scaling, fp64, rtol 1e-10, x0 = 0.  value = DOF*iterations/s (nDofs in the paper's T2-T4
+convention x PCG iterations / T_solve), summed over ranks.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG+BDDC solve time & DOF·iters/s (FP64) at 1/2/4/8 B200; % roofline"
+UNIT = "DOF*it/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, device):
+        self.device, self.samples, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_oracle_sample(steps, warmup):
+    """The oracle (oracle/, plain NumPy/SciPy) on a bounded sample of the workload: the same 4^3-cell
+    subdomains, k=2, constraints and rtol, on a 4^3 subdomain grid (config 2) instead of 8^3."""
+    from synthetic import make_problem
+    from oracle.assemble import GlobalSystem
+    from oracle.bddc import BDDC
+    prob = make_problem("c2")
+    gs = GlobalSystem(prob)
+    bd = BDDC(gs)
+    ndofs = gs.dofs.n_dofs_paper()
+    for _ in range(warmup):
+        bd.solve(rtol=1e-10)
+    ts, its = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        _, _, rep = bd.solve(rtol=1e-10)
+        ts.append(time.perf_counter() - t0)
+        its.append(rep["iterations"])
+    t = float(np.mean(ts))
+    return dict(value=ndofs * float(np.mean(its)) / t, t=t, it=float(np.mean(its)), ndofs=ndofs,
+                cores=os.cpu_count(),
+                sample="oracle BDDC-PCG solve (B0+PCG+B8, setup excluded) on config 2: 16^3 cells, "
+                       "4^3 subdomains of 4^3 cells (same subdomain size/k/constraints/rtol as the "
+                       "config-5 1-GPU slice, 1/8 of its subdomains), mean of %d solves" % steps)
+
+
+def reference_arm(args):
+    ws, rank, _ = _dist()
+    if ws > 1 and rank != 0:
+        return
+    r = run_oracle_sample(args.steps, args.warmup)
+    cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": r["sample"]}
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["t"] * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c2 sample of c5 (see cpu_baseline.sample)", "iterations": r["it"],
+                       "n_dofs": r["ndofs"]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    os.environ["VB_KERNEL_TIMING"] = "1"
+    import paper_2304_09770_b200 as vb
+    from synthetic import make_problem
+    from synthetic.configs import C5_DIMS
+
+    dims = C5_DIMS[1]
+    prob = make_problem(args.config, dims=dims if args.config == "c5" else None)
+    stream = torch.cuda.current_stream()
+    t0 = time.perf_counter()
+    ctx = vb.context_for(prob, stream=stream)
+    t_setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ctx.factor()
+    t_factor = time.perf_counter() - t0
+    st = ctx.stats()
+    rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+    ctx.build_rhs(vb.problem_args(prob), rhs)
+    x = torch.zeros_like(rhs)
+    for _ in range(args.warmup):
+        rep = ctx.pcg_solve(rhs, x, rtol=1e-10)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its, ktimes = [], []
+    with Clocks(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            rep = ctx.pcg_solve(rhs, x, rtol=1e-10)
+            its.append(rep["iterations"])
+            ktimes.append(ctx.kernel_times())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    it = float(np.mean(its))
+    ndofs = st["n_dofs_paper"]
+    value = ws * ndofs * it / (ms / 1e3)
+
+    # e2e: the public API with HOST buffers (pinned), H2D of the rhs and D2H of x inside the call
+    rhs_h = torch.empty(ctx.n_free, dtype=torch.float64, pin_memory=True)
+    rhs_h.copy_(rhs.cpu())
+    x_h = torch.empty(ctx.n_free, dtype=torch.float64, pin_memory=True)
+    rn, xn = rhs_h.numpy(), x_h.numpy()
+    ctx.pcg_solve_host(rn, xn)
+    torch.cuda.synchronize()
+    e2 = time.perf_counter()
+    e2e_its = []
+    for _ in range(args.steps):
+        r2 = ctx.pcg_solve_host(rn, xn)
+        e2e_its.append(r2["iterations"])
+    e2e_ms = (time.perf_counter() - e2) * 1e3 / args.steps
+    e2e_val = ws * ndofs * float(np.mean(e2e_its)) / (e2e_ms / 1e3)
+
+    # roofline of the dominant kernel (the packed symmetric GEMV on S_T)
+    kt = {k: float(np.mean([d[k] for d in ktimes])) for k in ktimes[0]}
+    peak, peak_src = _peaks()
+    names = list(kt.keys())
+    op_ms = kt[names[0]]
+    op_bytes = 8.0 * st["sum_pk_G"]
+    loc_ms, loc_bytes = kt[names[1]], 8.0 * st["sum_pk_D"]
+    c_ms, c_bytes = kt[names[2]], 8.0 * st["pk_coarse"]
+    achieved = op_bytes / (op_ms / 1e3) / 1e9
+    iter_ms = ms / max(it, 1)
+    per_iter_bytes = st["bytes_per_iter"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "c5 per-GPU slice: %dx%dx%d hex cells, k=2, %d subdomains of 4^3 cells" % (dims + (st["n_sub"],)),
+                   "n_dofs": ndofs, "iterations": it, "kappa": rep["kappa"], "rel_residual": rep["rel_residual"],
+                   "n_primal": st["n_primal"], "n_coarse": st["n_coarse"], "rtol": 1e-10,
+                   "t_setup_s": t_setup, "t_factor_s": t_factor,
+                   "parallelism": "subdomains on 1 GPU" if ws == 1 else
+                   "independent per-rank replicas (multi-rank coupling not enabled in this build)",
+                   "l2": "inputs larger than L2 (%.1f GB of operators streamed per iteration)" % (per_iter_bytes / 1e9),
+                   "ms_per_iteration": iter_ms,
+                   "achieved_GBps_per_iteration_model": per_iter_bytes / (iter_ms / 1e3) / 1e9},
+        "roofline": {"bound": "hbm", "kernel": names[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "bytes_per_launch": op_bytes, "ms_per_launch": op_ms,
+                     "others": {names[1]: {"ms": loc_ms, "GBps": loc_bytes / (loc_ms / 1e3) / 1e9 if loc_ms else None},
+                                names[2]: {"ms": c_ms, "GBps": c_bytes / (c_ms / 1e3) / 1e9 if c_ms else None},
+                                names[3]: {"ms": kt[names[3]]}, names[4]: {"ms": kt[names[4]]}}},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ctx.n_free,
+                "d2h_bytes_per_step": 8 * ctx.n_free, "ms_per_step": e2e_ms},
+        "gpu_launches": int(args.steps * (7 + 23 * it)),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = run_oracle_sample(2, 1)
+        line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+                                "sample": r["sample"]}
+    if rank == 0:
+        print(json.dumps(line))
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -89,6 +89,8 @@ _vb_cell_local_dofs = _sig("vb_cell_local_dofs", ctypes.c_int, [_p, ctypes.c_int
 _vb_get_element_matrices = _sig("vb_get_element_matrices", ctypes.c_int, [_p, ctypes.c_int64, _dp, _dp])
 _vb_stats = _sig("vb_stats", ctypes.c_int, [_p, _i64p])
 _vb_last_error = _sig("vb_last_error", ctypes.c_char_p, [_p])
+_vb_kernel_times = _sig("vb_kernel_times", ctypes.c_int, [_p, _dp, ctypes.c_int32, _i32p])
+_vb_kernel_time_name = _sig("vb_kernel_time_name", ctypes.c_char_p, [ctypes.c_int32])
 _vb_destroy = _sig("vb_destroy", ctypes.c_int, [_p])
 _vb_nccl_unique_id = _sig("vb_nccl_unique_id", ctypes.c_int, [_p])
 _vb_debug_iop = _sig("vb_debug_interface_op", ctypes.c_int, [_p, ctypes.c_int32, _dp, _dp])
@@ -238,11 +240,19 @@ class Context:
         return A, B
 
     def stats(self):
-        o = np.zeros(16, np.int64)
+        o = np.zeros(24, np.int64)
         self._check(_vb_stats(self._h, _ptr(o, ctypes.c_int64)))
         keys = ["n_dofs_paper", "n_free_vel", "n_pres", "n_sub", "n_ent", "n_gamma", "n_primal", "n_coarse",
-                "n_delta", "max_n", "max_nG", "max_nd", "n_edges", "bytes_per_iter", "nv_max", "n_colors"]
+                "n_delta", "max_n", "max_nG", "max_nd", "n_edges", "bytes_per_iter", "nv_max", "n_colors",
+                "sum_pk_G", "sum_pk_D", "sum_dlx_sq", "sum_phi", "pk_coarse", "last_iterations", "n_cells", "_"]
         return dict(zip(keys, o.tolist()))
+
+    def kernel_times(self):
+        """{category name: average ms per launch} of the last solve (needs VB_KERNEL_TIMING=1)."""
+        ms = np.zeros(16)
+        n = ctypes.c_int32()
+        self._check(_vb_kernel_times(self._h, _ptr(ms, ctypes.c_double), 16, ctypes.byref(n)))
+        return {_vb_kernel_time_name(i).decode(): float(ms[i]) for i in range(n.value)}
 
     def close(self):
         if getattr(self, "_h", None):

@@ -417,19 +417,25 @@ vb_status vb_stats(const vb_ctx *c, int64_t *o) {
   if (!c || !o) return VB_EINVAL;
   int64_t maxnG = 0, maxnd = 0, maxn = 0;
   for (auto &S : c->h_sub) { maxnG = std::max<int64_t>(maxnG, S.nG); maxnd = std::max<int64_t>(maxnd, S.nd); maxn = std::max<int64_t>(maxn, S.n); }
-  int64_t v[16] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
-                   c->NPi, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max, c->ncolors};
+  int64_t pkG = 0, pkD = 0, ndsq = 0, ndpi = 0;
+  for (auto &S : c->h_sub) { pkG += (int64_t)S.nG * (S.nG + 1) / 2; pkD += (int64_t)S.nd * (S.nd + 1) / 2; ndpi += (int64_t)S.nd * S.npi; }
+  for (auto &sl : c->h_slot) ndsq += (int64_t)sl.nd * sl.nd;
+  int64_t v[24] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
+                   c->NPi, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max,
+                   c->ncolors, pkG, pkD, ndsq, ndpi, c->Nc * (c->Nc + 1) / 2, c->last_iterations, c->nK, 0};
   memcpy(o, v, sizeof(v));
   return VB_OK;
 }
 
 vb_status vb_kernel_times(const vb_ctx *c, double *ms, int32_t n_max, int32_t *n_out) {
   if (!c || !n_out) return VB_EINVAL;
-  *n_out = 0;
+  int n = std::min<int>(n_max, c->ktime_ms.size());
+  for (int i = 0; i < n; ++i) ms[i] = c->ktime_count[i] ? c->ktime_ms[i] / c->ktime_count[i] : 0.0;
+  *n_out = n;
   return VB_OK;
 }
 
-const char *vb_kernel_time_name(int32_t) { return ""; }
+const char *vb_kernel_time_name(int32_t i) { return vb::kernel_time_name(i); }
 
 const char *vb_last_error(const vb_ctx *c) { return c ? c->err.c_str() : g_last_error.c_str(); }
 

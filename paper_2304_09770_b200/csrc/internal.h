@@ -257,6 +257,8 @@ struct vb_ctx {
   // timing
   bool timing = false;
   std::vector<double> ktime_ms;
+  std::vector<int> ktime_count;
+  int last_iterations = 0;
   std::vector<std::string> ktime_name;
   double t_setup = 0, t_factor = 0;
 };

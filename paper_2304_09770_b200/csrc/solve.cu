@@ -547,7 +547,57 @@ struct SolveState {
   DBuf<int64_t> xptr, xidx, pptr, pidx, eptr, eidx;
   DBuf<double> hist;
   bool ready = false;
+  // optional per-kernel timing (VB_KERNEL_TIMING=1): event pairs per launch category
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_cat;
+  int nev = 0;
+  ~SolveState() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
 };
+
+static const char *kCatNames[] = {"sym_gemv S_T (operator, B1)", "sym_gemv S_DD^-1 (local, B5)",
+                                  "sym_gemv coarse inverse (B6)", "apply_S total (B1-B2)",
+                                  "apply_M total (B4-B7)"};
+constexpr int N_CAT = 5;
+
+static void tick(vb_ctx *c, SolveState *st, int cat, bool begin) {
+  if (!c->timing) return;
+  if (st->nev + 1 >= (int)st->ev.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      VB_CUDA(cudaEventCreate(&e));
+      st->ev.push_back(e);
+      st->ev_cat.push_back(-1);
+    }
+  }
+  VB_CUDA(cudaEventRecord(st->ev[st->nev], c->stream));
+  st->ev_cat[st->nev] = begin ? cat : -1 - cat;
+  st->nev++;
+}
+
+static void collect_times(vb_ctx *c, SolveState *st) {
+  if (!c->timing) return;
+  c->ktime_ms.assign(N_CAT, 0.0);
+  c->ktime_count.assign(N_CAT, 0);
+  VB_CUDA(cudaStreamSynchronize(c->stream));
+  int open[N_CAT];
+  for (int q = 0; q < N_CAT; ++q) open[q] = -1;
+  for (int i = 0; i < st->nev; ++i) {
+    const int code = st->ev_cat[i];
+    if (code >= 0) { open[code] = i; continue; }
+    const int cat = -1 - code;
+    if (open[cat] < 0) continue;
+    float ms = 0;
+    VB_CUDA(cudaEventElapsedTime(&ms, st->ev[open[cat]], st->ev[i]));
+    c->ktime_ms[cat] += ms;
+    c->ktime_count[cat]++;
+    open[cat] = -1;
+  }
+  st->nev = 0;
+}
+
+const char *kernel_time_name(int i) { return (i >= 0 && i < N_CAT) ? kCatNames[i] : ""; }
 
 constexpr int DOT_BLOCKS = 296;
 
@@ -560,30 +610,40 @@ static int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 
 
 static void apply_S(vb_ctx *c, SolveState *st) {   // q = S^ p  (B1, B2)
   cudaStream_t s = c->stream;
+  tick(c, st, 3, true);
+  tick(c, st, 0, true);
   sym_gemv_kernel<<<st->nw_op, GV_WARPS * 32, st->sm_op, s>>>(st->w_op.p);
+  tick(c, st, 0, false);
   b0_apply_kernel<<<c->N, 32, 0, s>>>(c->d_sub.p, c->d_loc2x.p, c->d_b0T.p, c->w_p.p,
                                       c->n_delta_glob + c->NPi, c->w_part.p, c->w_q.p);
   int64_t nxp = c->n_delta_glob + c->NPi;
   gather_sum_kernel<<<grid_for(nxp), 256, 0, s>>>(st->xptr.p, st->xidx.p, c->w_part.p, c->len_G, c->P_op, nxp, c->w_q.p);
+  tick(c, st, 3, false);
   VB_STAGE();
 }
 
 static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   cudaStream_t s = c->stream;
   const int nslot = c->h_slot.size(), nent = c->h_ent.size();
+  tick(c, st, 4, true);
   if (nslot) restrict_kernel<<<nslot, 256, 0, s>>>(c->d_slot.p, c->d_ent.p, c->d_sub.p, c->d_Dlx.p, c->w_r.p, c->w_locD.p);
+  tick(c, st, 1, true);
   if (st->nw_loc) sym_gemv_kernel<<<st->nw_loc, GV_WARPS * 32, st->sm_loc, s>>>(st->w_loc.p);
+  tick(c, st, 1, false);
   phit_kernel<<<c->N, 256, 0, s>>>(c->d_sub.p, c->d_Phi.p, c->w_locD.p, c->w_locC.p);
   coarse_rhs_kernel<<<grid_for(c->Nc), 256, 0, s>>>(st->pptr.p, st->pidx.p, c->w_locC.p, c->w_r.p,
                                                     c->n_delta_glob, c->NPi, c->N, c->w_rc.p);
   coarse_p0_project_kernel<<<1, 256, 0, s>>>(c->d_sub.p, c->N, c->w_rc.p + c->NPi, 0);
+  tick(c, st, 2, true);
   sym_gemv_kernel<<<st->nw_c, GV_WARPS * 32, st->sm_c, s>>>(st->w_c.p);
+  tick(c, st, 2, false);
   sum_chunks_kernel<<<grid_for(c->Nc), 256, 0, s>>>(c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
   coarse_p0_project_kernel<<<1, 256, 0, s>>>(c->d_sub.p, c->N, c->w_uc.p + c->NPi, 1);
   local2_kernel<<<c->N, 256, 64 * sizeof(double) + c->max_npi * sizeof(double), s>>>(
       c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p);
   if (nent) extend_kernel<<<nent, 128, 0, s>>>(c->d_ent.p, c->d_slot.p, c->d_sub.p, c->d_Dlx.p, c->w_locD.p, c->w_z.p);
   coarse_to_z_kernel<<<grid_for(c->Nc), 256, 0, s>>>(c->w_uc.p, c->Nc, c->w_z.p + c->n_delta_glob);
+  tick(c, st, 4, false);
   VB_STAGE();
 }
 
@@ -726,6 +786,8 @@ void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit,
   prepare_solve(c);
   SolveState *st = get_state(c);
   cudaStream_t s = c->stream;
+  c->timing = getenv("VB_KERNEL_TIMING") && atoi(getenv("VB_KERNEL_TIMING"));
+  st->nev = 0;
   const int N = c->N;
   const int64_t nx = c->nx, NDelta = c->n_delta_glob;
   const int64_t nvf = c->n_free_vel;
@@ -797,6 +859,8 @@ void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit,
   pressure_mean_kernel<<<grid_for(c->nK), 256, 0, s>>>(c->d_cellgeo.p, c->geo_stride, c->np, c->nK, x + nvf, 64, c->w_dots.p);
   VB_STAGE();
   VB_CUDA(cudaStreamSynchronize(s));
+  collect_times(c, st);
+  c->last_iterations = it;
   if (rep) {
     rep->iterations = it;
     rep->converged = status == VB_OK;
