@@ -217,6 +217,21 @@ __global__ void multiplicity_kernel(const SlotDev *__restrict__ slots, const Ent
     Dlx[s.off_Dlx + idx] = (idx % s.nd == idx / s.nd) ? v : 0.0;
 }
 
+// column-major nd x nd deluxe block -> row-major 32x32 tiles (tile (I,J) at (I nt + J) 1024)
+__global__ void tile_rect_kernel(const SlotDev *__restrict__ slots, const int *__restrict__ act,
+                                 const double *__restrict__ Dlx, double *Dt) {
+  const SlotDev s = slots[act[blockIdx.y]];
+  const int nd = s.nd, nt = (nd + 31) / 32;
+  const double *D = Dlx + s.off_Dlx;
+  double *out = Dt + s.off_Dt;
+  for (int64_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)nt * nt * 1024; idx += gridDim.x * blockDim.x) {
+    const int tile = idx / 1024, w = idx % 1024;
+    const int I = tile / nt, J = tile % nt, r = w / 32, cc = w % 32;
+    const int row = 32 * I + r, col = 32 * J + cc;
+    out[idx] = (row < nd && col < nd) ? D[row + (int64_t)col * nd] : 0.0;
+  }
+}
+
 __global__ void recip_diag_kernel(const double *A, int64_t ld, int n, double *out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = 1.0 / A[i + i * ld];
 }
@@ -340,6 +355,66 @@ void factor_device(vb_ctx *c) {
     sg[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.nG, S.n, 0};
   }
   symmetrize_lower_batched(sg, s);
+  // ---------------- Dirichlet operators for B0/B8 as dense GEMV operands:
+  //   Psi^T = K_GD K_DD^-1 = L_GD L_DD^-1  (nG x nD),  K_DD^-1 = L_DD^-T D^-1 L_DD^-1 (packed)
+  {
+    int64_t lenWD = 0, lenPsi = 0, lenKDi = 0;
+    std::vector<int64_t> offWD(N), offPsi(N), offKDi(N);
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      offWD[i] = lenWD; lenWD += (int64_t)S.nD * S.nD;
+      offPsi[i] = lenPsi; lenPsi += (int64_t)S.nG * S.nD;
+      offKDi[i] = lenKDi; lenKDi += packed_tiles(S.nD) * 1024;
+      c->h_sub[i].off_Psi = offPsi[i];
+      c->h_sub[i].off_KDi = offKDi[i];
+    }
+    DBuf<double> WD, WD2, dD;
+    WD.alloc(lenWD);
+    WD.zero(s);
+    std::vector<TriDesc> td(N);
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      td[i] = TriDesc{c->d_K.p + S.off_K, S.n, WD.p + offWD[i], S.nD, S.nD};
+    }
+    tri_inverse_batched(td, s);
+    dD.alloc(c->len_Dn);
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      recip_diag_kernel<<<(S.nD + 255) / 256, 256, 0, s>>>(c->d_K.p + S.off_K, S.n, S.nD, dD.p + S.off_Dn);
+    }
+    VB_STAGE();
+    c->d_Psi.alloc(std::max<int64_t>(lenPsi, 1));
+    WD2.alloc(lenWD);
+    GemmPlan plan;
+    int l0 = plan.begin_launch();
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      GemmProb p{};
+      p.A = c->d_K.p + S.off_K + S.nD; p.lda = S.n;                 // L_GD (nG x nD)
+      p.B = WD.p + offWD[i]; p.ldb = S.nD;                          // L_DD^-1
+      p.C = c->d_Psi.p + offPsi[i]; p.ldc = S.nG;
+      p.M = S.nG; p.N = S.nD; p.K = S.nD; p.alpha = 1.0; p.beta = 0.0;
+      plan.add(p);
+      GemmProb q{};
+      q.A = WD.p + offWD[i]; q.lda = S.nD; q.transA = 1;
+      q.d = dD.p + S.off_Dn; q.dstride = 1;
+      q.B = WD.p + offWD[i]; q.ldb = S.nD;
+      q.C = WD2.p + offWD[i]; q.ldc = S.nD;
+      q.M = q.N = q.K = S.nD; q.alpha = 1.0; q.beta = 0.0; q.lower = 1;
+      plan.add(q);
+    }
+    plan.upload(s);
+    plan.run(l0, s);
+    sync(c);
+    c->d_KDi.alloc(lenKDi);
+    std::vector<PackDesc> pk(N);
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      pk[i] = PackDesc{WD2.p + offWD[i], S.nD, S.nD, c->d_KDi.p + offKDi[i]};
+    }
+    pack_tiles_batched(pk, s);
+    c->len_KDi = lenKDi;
+  }
   // ---------------- A3: entity bases T_G = [N_G | C'^T]
   std::vector<double> rows;
   build_constraint_rows(c, rows);
@@ -572,6 +647,30 @@ void factor_device(vb_ctx *c) {
       plan.upload(s);
       plan.run(l0, s);
       sync(c);
+    }
+  }
+  // ---------------- deluxe blocks -> row-major 32x32 tiles for the per-iteration kernels
+  {
+    int64_t off = 0;
+    std::vector<int> act_s, act_e;
+    for (int q = 0; q < nslot; ++q) {
+      SlotDev &sl = c->h_slot[q];
+      const int nt = (sl.nd + 31) / 32;
+      sl.off_Dt = off;
+      off += (int64_t)nt * nt * 1024;
+      if (sl.nd) act_s.push_back(q);
+    }
+    for (int e = 0; e < nent; ++e)
+      if (c->h_ent[e].nd) act_e.push_back(e);
+    c->d_Dt.alloc(std::max<int64_t>(off, 1));
+    c->d_slot.upload(c->h_slot, s);
+    c->d_act_slots.upload(act_s, s);
+    c->d_act_ents.upload(act_e, s);
+    c->n_act_slots = act_s.size();
+    c->n_act_ents = act_e.size();
+    if (c->n_act_slots) {
+      tile_rect_kernel<<<dim3(64, c->n_act_slots), 256, 0, s>>>(c->d_slot.p, c->d_act_slots.p, c->d_Dlx.p, c->d_Dt.p);
+      VB_STAGE();
     }
   }
   // ---------------- A5: coarse saddle matrix on (u_Pi, p_0), dense inverse

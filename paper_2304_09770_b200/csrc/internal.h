@@ -137,6 +137,8 @@ struct SubDev {
   int64_t off_I;              // offset into length-nI vectors
   int64_t off_Dn;             // offset into length-nD vectors
   int64_t off_X;              // scratch square (nG x nG) offset
+  int64_t off_Psi;            // Psi^T = K_GD K_DD^-1 (nG x nD, column-major, ld = nG)
+  int64_t off_KDi;            // packed tiles of K_DD^-1 (Q_I-augmented, A5)
   double vol, gamma;
 };
 
@@ -148,6 +150,7 @@ struct SlotDev {              // one (entity, sharer) pair; slots are entity-maj
   int64_t off_T;              // T_G of the entity
   int64_t off_Dlx;            // deluxe block D_G^(sub) (nd x nd, column-major)
   int64_t off_side;           // scratch for S_GD^(sub)
+  int64_t off_Dt;             // D_G^(sub) as row-major 32x32 tiles (nt x nt, zero padded)
 };
 
 struct EntDev {
@@ -216,8 +219,12 @@ struct vb_ctx {
   int max_npi = 0, geo_stride = 0;
   std::vector<double> cellgeo;       // host copy of d_cellgeo
   vb::DBuf<double> d_K;              // subdomain dense matrices
-  vb::DBuf<double> d_ST, d_STp, d_SDi, d_Phi, d_Sc;
+  vb::DBuf<double> d_ST, d_STp, d_SDi, d_Phi, d_Sc, d_Psi, d_KDi;
+  int64_t len_KDi = 0;
   vb::DBuf<double> d_T, d_C, d_Dlx;  // per-entity T_G, constraint rows, deluxe blocks
+  vb::DBuf<double> d_Dt;             // deluxe blocks as row-major 32x32 tiles (per-iteration layout)
+  vb::DBuf<int> d_act_slots, d_act_ents;   // slots / entities with a dual part (nd > 0)
+  int n_act_slots = 0, n_act_ents = 0;
   vb::DBuf<double> d_Kc, d_Kcp;      // coarse dense & packed inverse
   int64_t Nc = 0;
   // descriptors
@@ -248,9 +255,10 @@ struct vb_ctx {
   vb::DBuf<int> d_info;
   // solve workspaces
   vb::DBuf<double> w_x, w_r, w_z, w_p, w_q, w_part, w_locD, w_locY, w_locC, w_uc, w_rc, w_ucp,
-      w_scal, w_gam, w_bD, w_zG, w_dots, w_elt;
+      w_scal, w_gam, w_bD, w_zG, w_dots, w_elt, w_yDp, w_xD;
+  int P_kd = 4;
   vb::DBuf<int> d_op_work, d_loc_work, d_c_work;   // packed-GEMV chunk work lists
-  int n_op_work = 0, n_loc_work = 0, n_c_work = 0, P_op = 4, P_loc = 4, P_c = 296;
+  int n_op_work = 0, n_loc_work = 0, n_c_work = 0, P_op = 4, P_loc = 4, P_c = 148;
   vb::DBuf<int64_t> d_op_part_off, d_loc_part_off;
   vb::DBuf<int64_t> d_el_ptr, d_el_ent;   // K7: free dof -> (cell, local) contributions
   double bytes_per_iter = 0;

@@ -32,8 +32,10 @@ struct GemvWork {
   int n, r0, r1, pad;
 };
 
-constexpr int GV_WARPS = 4;
+constexpr int GV_WARPS = 4;      // subdomain matrices (several CTAs per SM)
+constexpr int GV_WARPS_C = 8;    // the single coarse matrix (one CTA per SM)
 
+template <int GV_WARPS>
 __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork *__restrict__ work) {
   extern __shared__ double sm[];
   const GemvWork W = work[blockIdx.x];
@@ -94,7 +96,9 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
   for (int j = tid; j < n; j += blockDim.x) W.out[j] = ys[j];
 }
 
-static size_t gemv_smem(int nmax) { return (size_t)(2 * ((nmax + 31) / 32) * 32 + GV_WARPS * 32) * sizeof(double); }
+static size_t gemv_smem(int nmax, int warps = GV_WARPS) {
+  return (size_t)(2 * ((nmax + 31) / 32) * 32 + warps * 32) * sizeof(double);
+}
 
 // split a packed matrix of n into P chunks of tile rows balanced by tile count
 static void split_rows(int n, int P, std::vector<std::pair<int, int>> &out) {
@@ -190,36 +194,64 @@ __global__ void rotate_rz_kernel(double *scal, double *hist, int it) {
   scal[0] = scal[3];
 }
 
-// restriction with deluxe scaling: rD^(sub)[offD+j] = sum_i D^(sub)[i, j] r_x[off_xd + i]  (D^T r)
-__global__ void restrict_kernel(const SlotDev *__restrict__ slots, const EntDev *__restrict__ ents,
-                                const SubDev *__restrict__ subs, const double *__restrict__ Dlx,
+// restriction with deluxe scaling: rD^(sub)[offD+j] = sum_i D^(sub)[i, j] r_x[off_xd + i]  (D^T r).
+// D is stored as row-major 32x32 tiles (zero padded): a warp streams one contiguous 8 KB tile with
+// lane = tile column, so the column sums need no cross-lane reduction; per-warp partials are
+// summed in fixed order (deterministic).  One CTA per active (entity, sharer) slot.
+constexpr int DLX_WARPS = 4;
+__global__ void __launch_bounds__(DLX_WARPS * 32) restrict_kernel(const SlotDev *__restrict__ slots,
+                                const int *__restrict__ act, const EntDev *__restrict__ ents,
+                                const SubDev *__restrict__ subs, const double *__restrict__ Dt,
                                 const double *__restrict__ r, double *rD) {
-  const SlotDev s = slots[blockIdx.x];
+  extern __shared__ double sh[];
+  const SlotDev s = slots[act[blockIdx.x]];
   const int nd = s.nd;
-  if (!nd) return;
-  const double *D = Dlx + s.off_Dlx;
-  const double *re = r + ents[s.ent].off_xd;
-  double *out = rD + subs[s.sub].off_Dv + s.offD;
+  const int nt = (nd + 31) / 32, npad = nt * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = warp; j < nd; j += nw) {
+  double *xs = sh;                  // npad
+  double *part = sh + npad;         // nw * npad
+  const double *D = Dt + s.off_Dt;
+  const double *re = r + ents[s.ent].off_xd;
+  for (int i = threadIdx.x; i < npad; i += blockDim.x) xs[i] = i < nd ? re[i] : 0.0;
+  for (int i = threadIdx.x; i < nw * npad; i += blockDim.x) part[i] = 0.0;
+  __syncthreads();
+  for (int u = warp; u < nt * nt; u += nw) {
+    const int I = u / nt, J = u % nt;
+    const double *T = D + (int64_t)u * 1024;
+    double t[32];
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) t[rr] = __ldg(T + rr * 32 + lane);
+    double acc = 0.0;
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) acc += t[rr] * xs[32 * I + rr];
+    part[warp * npad + 32 * J + lane] += acc;
+  }
+  __syncthreads();
+  double *out = rD + subs[s.sub].off_Dv + s.offD;
+  for (int j = threadIdx.x; j < nd; j += blockDim.x) {
     double v = 0.0;
-    for (int i = lane; i < nd; i += 32) v += D[i + (int64_t)j * nd] * re[i];
-    v = warp_sum(v);
-    if (lane == 0) out[j] = v;
+    for (int w = 0; w < nw; ++w) v += part[w * npad + j];
+    out[j] = v;
   }
 }
 
-// c_i = Phi_i^T rD_i (coarse rhs pieces); warp per primal column
-__global__ void phit_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
+// c_i = Phi_i^T rD_i (coarse rhs pieces): PHIT_SPLIT CTAs per subdomain, warp per primal column
+constexpr int PHIT_SPLIT = 4;
+__global__ void __launch_bounds__(256) phit_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
                             const double *__restrict__ rD, double *cpart) {
-  const SubDev S = subs[blockIdx.x];
+  const SubDev S = subs[blockIdx.y];
   const double *F = Phi + S.off_Phi;
   const double *x = rD + S.off_Dv;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int a = warp; a < S.npi; a += nw) {
-    double v = 0.0;
-    for (int j = lane; j < S.nd; j += 32) v += F[j + (int64_t)a * S.nd] * x[j];
-    v = warp_sum(v);
+  for (int a = blockIdx.x * nw + warp; a < S.npi; a += gridDim.x * nw) {
+    const double *col = F + (int64_t)a * S.nd;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    int j = lane;
+    for (; j + 96 < S.nd; j += 128) {
+      v0 += col[j] * x[j]; v1 += col[j + 32] * x[j + 32]; v2 += col[j + 64] * x[j + 64]; v3 += col[j + 96] * x[j + 96];
+    }
+    for (; j < S.nd; j += 32) v0 += col[j] * x[j];
+    double v = warp_sum((v0 + v1) + (v2 + v3));
     if (lane == 0) cpart[S.off_Pi + a] = v;
   }
 }
@@ -260,38 +292,77 @@ __global__ void coarse_p0_project_kernel(const SubDev *__restrict__ subs, int N,
   for (int i = threadIdx.x; i < N; i += blockDim.x) v[i] -= mode == 0 ? subs[i].vol * mean : mean;
 }
 
-// w_i = sum_chunks y_i + Phi_i u_Pi^(i)   (lanes over rows of column-major Phi)
-__global__ void local2_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
+// w_i = sum_chunks y_i + Phi_i u_Pi^(i)   (thread per row of column-major Phi, 4 accumulators)
+__global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
                               const double *__restrict__ part, int64_t part_stride, int P,
                               const int64_t *__restrict__ pi_glob, const double *__restrict__ uc, double *w) {
-  const SubDev S = subs[blockIdx.x];
+  const SubDev S = subs[blockIdx.y];
   const double *F = Phi + S.off_Phi;
   extern __shared__ double us[];
   for (int a = threadIdx.x; a < S.npi; a += blockDim.x) us[a] = uc[pi_glob[S.off_Pi + a]];
   __syncthreads();
-  for (int j = threadIdx.x; j < S.nd; j += blockDim.x) {
-    double v = 0.0;
-    for (int c = 0; c < P; ++c) v += part[c * part_stride + S.off_Dv + j];
-    for (int a = 0; a < S.npi; ++a) v += F[j + (int64_t)a * S.nd] * us[a];
-    w[S.off_Dv + j] = v;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= S.nd) return;
+  double v = 0.0;
+  for (int c = 0; c < P; ++c) v += part[c * part_stride + S.off_Dv + j];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int a = 0;
+  for (; a + 3 < S.npi; a += 4) {
+    a0 += F[j + (int64_t)a * S.nd] * us[a];
+    a1 += F[j + (int64_t)(a + 1) * S.nd] * us[a + 1];
+    a2 += F[j + (int64_t)(a + 2) * S.nd] * us[a + 2];
+    a3 += F[j + (int64_t)(a + 3) * S.nd] * us[a + 3];
   }
+  for (; a < S.npi; ++a) a0 += F[j + (int64_t)a * S.nd] * us[a];
+  w[S.off_Dv + j] = v + ((a0 + a1) + (a2 + a3));
 }
 
 // extension with deluxe scaling: z_x[off_xd + i] = sum_m sum_j D^(m)[i, j] w^(m)[offD_m + j];
-// primal and p0 coordinates copied from the coarse solution.
-__global__ void extend_kernel(const EntDev *__restrict__ ents, const SlotDev *__restrict__ slots,
-                              const SubDev *__restrict__ subs, const double *__restrict__ Dlx,
+// warps stream (side, 32x32 row-major tile) units, lane = tile column; the row sums come from a
+// transpose-reduce; per-warp row partials are summed in fixed order.  One CTA per active entity.
+__global__ void __launch_bounds__(DLX_WARPS * 32) extend_kernel(const EntDev *__restrict__ ents,
+                              const int *__restrict__ act, const SlotDev *__restrict__ slots,
+                              const SubDev *__restrict__ subs, const double *__restrict__ Dt,
                               const double *__restrict__ w, double *z) {
-  const EntDev E = ents[blockIdx.x];
+  extern __shared__ double sh[];
+  const EntDev E = ents[act[blockIdx.x]];
   const int nd = E.nd;
+  const int nt = (nd + 31) / 32, npad = nt * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double *ws = sh;                        // nsides * npad
+  double *part = sh + E.nsides * npad;    // nw * npad
+  for (int q = 0; q < E.nsides; ++q) {
+    const SlotDev s = slots[E.side_begin + q];
+    const double *src = w + subs[s.sub].off_Dv + s.offD;
+    for (int i = threadIdx.x; i < npad; i += blockDim.x) ws[q * npad + i] = i < nd ? src[i] : 0.0;
+  }
+  for (int i = threadIdx.x; i < nw * npad; i += blockDim.x) part[i] = 0.0;
+  __syncthreads();
+  for (int u = warp; u < E.nsides * nt * nt; u += nw) {
+    const int q = u / (nt * nt), tile = u % (nt * nt), I = tile / nt, J = tile % nt;
+    const double *T = Dt + slots[E.side_begin + q].off_Dt + (int64_t)tile * 1024;
+    double p[32];
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) p[rr] = __ldg(T + rr * 32 + lane);
+    const double wc = ws[q * npad + 32 * J + lane];
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) p[rr] *= wc;
+#pragma unroll
+    for (int sft = 16; sft > 0; sft >>= 1) {
+      const bool up = (lane & sft) != 0;
+#pragma unroll
+      for (int k2 = 0; k2 < sft; ++k2) {
+        double send = up ? p[k2] : p[k2 + sft];
+        double keep = up ? p[k2 + sft] : p[k2];
+        p[k2] = keep + __shfl_xor_sync(FULL, send, sft);
+      }
+    }
+    part[warp * npad + 32 * I + lane] += p[0];
+  }
+  __syncthreads();
   for (int i = threadIdx.x; i < nd; i += blockDim.x) {
     double v = 0.0;
-    for (int q = 0; q < E.nsides; ++q) {
-      const SlotDev s = slots[E.side_begin + q];
-      const double *D = Dlx + s.off_Dlx;
-      const double *ws = w + subs[s.sub].off_Dv + s.offD;
-      for (int j = 0; j < nd; ++j) v += D[i + (int64_t)j * nd] * ws[j];
-    }
+    for (int w2 = 0; w2 < nw; ++w2) v += part[w2 * npad + i];
     z[E.off_xd + i] = v;
   }
 }
@@ -300,46 +371,96 @@ __global__ void copy_kernel(const double *a, double *b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
-// ------------------------------------------------------------------ B0: rhs condensation
-// v = [b_I ; Pi^T b_P ; 0]; forward substitution with the partial L -> z_G (= -K_GD K_DD^-1 b_D);
-// stores D^-1 z_D for the back-substitution and g0_i = c^T b_P (p0 rhs).
-__global__ void condense_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Kall,
-                                const int64_t *__restrict__ Ifree, const int64_t *__restrict__ Pglob,
-                                const double *__restrict__ cvec, const double *__restrict__ mvec,
-                                const double *__restrict__ rhs, int64_t nvf, double *zG, double *yD, double *g0) {
-  extern __shared__ double v[];
+// ------------------------------------------------------------------ B0 / B8
+// B0 (GEMV form): b_D = [b_I ; Pi^T b_P] and g0_i = c^T b_P (p0 rhs, A5)
+__global__ void rhs_D_kernel(const SubDev *__restrict__ subs, const int64_t *__restrict__ Ifree,
+                             const int64_t *__restrict__ Pglob, const double *__restrict__ cvec,
+                             const double *__restrict__ mvec, const double *__restrict__ rhs, int64_t nvf,
+                             double *bD, double *g0) {
   __shared__ double red[32];
   const SubDev S = subs[blockIdx.x];
-  const double *K = Kall + S.off_K;
-  const int64_t ld = S.n;
-  const int tid = threadIdx.x;
-  for (int j = tid; j < S.n; j += blockDim.x) {
-    double val = 0.0;
-    if (j < S.nI) val = rhs[Ifree[S.off_I + j]];
-    else if (j < S.nD) val = rhs[nvf + Pglob[S.off_P + j - S.nI]];
-    v[j] = val;
-  }
-  __syncthreads();
-  // g0 = c^T b_P ; b_P -= m g0 / vol
+  const int tid = threadIdx.x, nw = blockDim.x >> 5;
+  double *b = bD + S.off_Dn;
+  for (int j = tid; j < S.nI; j += blockDim.x) b[j] = rhs[Ifree[S.off_I + j]];
   double s = 0.0;
-  for (int a = tid; a < S.nP; a += blockDim.x) s += cvec[S.off_P + a] * v[S.nI + a];
+  for (int a = tid; a < S.nP; a += blockDim.x) s += cvec[S.off_P + a] * rhs[nvf + Pglob[S.off_P + a]];
   s = warp_sum(s);
   if ((tid & 31) == 0) red[tid >> 5] = s;
   __syncthreads();
   double g = 0.0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) g += red[w];
+  for (int w = 0; w < nw; ++w) g += red[w];
   if (tid == 0) g0[blockIdx.x] = g;
-  for (int a = tid; a < S.nP; a += blockDim.x) v[S.nI + a] -= mvec[S.off_P + a] * g / S.vol;
-  __syncthreads();
-  // forward substitution with unit lower L (columns 0..nD-1), rows j+1..n-1
-  for (int j = 0; j < S.nD; ++j) {
-    const double vj = v[j];
-    const double *col = K + (int64_t)j * ld;
-    for (int i = j + 1 + tid; i < S.n; i += blockDim.x) v[i] -= col[i] * vj;
-    __syncthreads();
+  for (int a = tid; a < S.nP; a += blockDim.x)
+    b[S.nI + a] = rhs[nvf + Pglob[S.off_P + a]] - mvec[S.off_P + a] * g / S.vol;
+}
+
+// B0: z_G = -Psi^T b_D = -K_GD K_DD^-1 b_D (thread per interface row, column-major Psi^T)
+__global__ void __launch_bounds__(128) zG_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Psi,
+                                                 const double *__restrict__ bD, double *zG) {
+  const SubDev S = subs[blockIdx.y];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S.nG) return;
+  const double *P = Psi + S.off_Psi;
+  const double *b = bD + S.off_Dn;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int j = 0;
+  for (; j + 3 < S.nD; j += 4) {
+    a0 += P[i + (int64_t)j * S.nG] * b[j];
+    a1 += P[i + (int64_t)(j + 1) * S.nG] * b[j + 1];
+    a2 += P[i + (int64_t)(j + 2) * S.nG] * b[j + 2];
+    a3 += P[i + (int64_t)(j + 3) * S.nG] * b[j + 3];
   }
-  for (int j = tid; j < S.nD; j += blockDim.x) yD[S.off_Dn + j] = v[j] / K[j + (int64_t)j * ld];
-  for (int j = tid; j < S.nG; j += blockDim.x) zG[S.off_G + j] = v[S.nD + j];
+  for (; j < S.nD; ++j) a0 += P[i + (int64_t)j * S.nG] * b[j];
+  zG[S.off_G + i] = -((a0 + a1) + (a2 + a3));
+}
+
+// B8: x_D[j] = y_D[j] - sum_i Psi^T[i, j] x_G[i]  (y_D = K_DD^-1 b_D from the packed GEMV partials);
+// warp per column j of Psi^T (contiguous), XD_SPLIT CTAs per subdomain.
+constexpr int XD_SPLIT = 4;
+__global__ void __launch_bounds__(256) xD_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Psi,
+                                                 const double *__restrict__ ypart, int64_t pstride, int P,
+                                                 const int64_t *__restrict__ Gfree, const double *__restrict__ x_in,
+                                                 double *xD) {
+  extern __shared__ double xg[];
+  const SubDev S = subs[blockIdx.y];
+  for (int i = threadIdx.x; i < S.nG; i += blockDim.x) xg[i] = x_in[Gfree[S.off_G + i]];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double *Pm = Psi + S.off_Psi;
+  for (int j = blockIdx.x * nw + warp; j < S.nD; j += gridDim.x * nw) {
+    const double *col = Pm + (int64_t)j * S.nG;
+    double v0 = 0.0, v1 = 0.0;
+    int i = lane;
+    for (; i + 32 < S.nG; i += 64) { v0 += col[i] * xg[i]; v1 += col[i + 32] * xg[i + 32]; }
+    for (; i < S.nG; i += 32) v0 += col[i] * xg[i];
+    const double v = warp_sum(v0 + v1);
+    if (lane == 0) {
+      double y = 0.0;
+      for (int c = 0; c < P; ++c) y += ypart[c * pstride + S.off_Dn + j];
+      xD[S.off_Dn + j] = y - v;
+    }
+  }
+}
+
+// B8: pressure p = p_aug - c (m^T p_aug)/vol + p0 c (Q_I projection + Q_0 part); scatter to x
+__global__ void xout_kernel(const SubDev *__restrict__ subs, const double *__restrict__ xD,
+                            const int64_t *__restrict__ Ifree, const int64_t *__restrict__ Pglob,
+                            const double *__restrict__ cvec, const double *__restrict__ mvec,
+                            const double *__restrict__ p0, int64_t nvf, double *xout) {
+  __shared__ double red[32];
+  const SubDev S = subs[blockIdx.x];
+  const int tid = threadIdx.x, nw = blockDim.x >> 5;
+  const double *t = xD + S.off_Dn;
+  double s = 0.0;
+  for (int a = tid; a < S.nP; a += blockDim.x) s += mvec[S.off_P + a] * t[S.nI + a];
+  s = warp_sum(s);
+  if ((tid & 31) == 0) red[tid >> 5] = s;
+  __syncthreads();
+  double mp = 0.0;
+  for (int w = 0; w < nw; ++w) mp += red[w];
+  const double shift = p0[blockIdx.x] - mp / S.vol;
+  for (int j = tid; j < S.nI; j += blockDim.x) xout[Ifree[S.off_I + j]] = t[j];
+  for (int a = tid; a < S.nP; a += blockDim.x) xout[nvf + Pglob[S.off_P + a]] = t[S.nI + a] + shift * cvec[S.off_P + a];
 }
 
 // per entity: ghat_e = b_e + sum_m zG^(m)[e]; r_x = T_e^T ghat_e
@@ -388,59 +509,6 @@ __global__ void gamma_back_kernel(const EntDev *__restrict__ ents, const int64_t
     gam[E.off_gam + j] = v;
     xout[gam_free[E.off_gam + j]] = v;
   }
-}
-
-// B8: x_D = L_DD^-T (D^-1 z_D - L_GD^T x_G); pressure projection, + p0 c; interior to x
-__global__ void backsub_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Kall,
-                               const int64_t *__restrict__ Ifree, const int64_t *__restrict__ Pglob,
-                               const int64_t *__restrict__ Gfree, const double *__restrict__ cvec,
-                               const double *__restrict__ mvec, const double *__restrict__ yD,
-                               const double *__restrict__ x_in, const double *__restrict__ p0, int64_t nvf,
-                               double *xout) {
-  extern __shared__ double t[];
-  __shared__ double red[32];
-  const SubDev S = subs[blockIdx.x];
-  const double *K = Kall + S.off_K;
-  const int64_t ld = S.n;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  double *xG = t + S.nD;
-  for (int j = tid; j < S.nG; j += blockDim.x) xG[j] = x_in[Gfree[S.off_G + j]];
-  __syncthreads();
-  // t_j = yD_j - sum_{i in G} L[nD+i, j] xG_i   (warp per column j)
-  for (int j = warp; j < S.nD; j += nw) {
-    const double *col = K + (int64_t)j * ld + S.nD;
-    double v = 0.0;
-    for (int i = lane; i < S.nG; i += 32) v += col[i] * xG[i];
-    v = warp_sum(v);
-    if (lane == 0) t[j] = yD[S.off_Dn + j] - v;
-  }
-  __syncthreads();
-  // backward substitution: x_j = t_j - sum_{i>j, i<nD} L[i, j] x_i   (j descending)
-  for (int j = S.nD - 1; j >= 0; --j) {
-    const double *col = K + (int64_t)j * ld;
-    double v = 0.0;
-    for (int i = j + 1 + tid; i < S.nD; i += blockDim.x) v += col[i] * t[i];
-    v = warp_sum(v);
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    if (tid == 0) {
-      double sacc = 0.0;
-      for (int w = 0; w < nw; ++w) sacc += red[w];
-      t[j] -= sacc;
-    }
-    __syncthreads();
-  }
-  // pressure: p = p_aug - c (m^T p_aug)/vol + p0 c
-  double s = 0.0;
-  for (int a = tid; a < S.nP; a += blockDim.x) s += mvec[S.off_P + a] * t[S.nI + a];
-  s = warp_sum(s);
-  if (lane == 0) red[warp] = s;
-  __syncthreads();
-  double mp = 0.0;
-  for (int w = 0; w < nw; ++w) mp += red[w];
-  const double shift = p0[blockIdx.x] - mp / S.vol;
-  for (int j = tid; j < S.nI; j += blockDim.x) xout[Ifree[S.off_I + j]] = t[j];
-  for (int a = tid; a < S.nP; a += blockDim.x) xout[nvf + Pglob[S.off_P + a]] = t[S.nI + a] + shift * cvec[S.off_P + a];
 }
 
 // global zero-mean pressure (Q_{h,0}): p -= c_K * (sum_K vol_K p_K0) / vol_Omega
@@ -527,11 +595,22 @@ __global__ void axpby_kernel(const double *a, const double *b, double *out, int6
 }
 
 // ------------------------------------------------------------------ host side
-__global__ void sum_chunks_kernel(const double *__restrict__ part, int64_t stride, int P, int64_t n, double *out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double v = 0.0;
-    for (int c = 0; c < P; ++c) v += part[c * stride + i];
-    out[i] = v;
+// out[i] = sum_c part[c][i]: block = 32 outputs x 8 warps (warp w sums chunks w, w+8, ...), then
+// the 8 warp partials are added in fixed order.
+__global__ void __launch_bounds__(256) sum_chunks_kernel(const double *__restrict__ part, int64_t stride, int P,
+                                                         int64_t n, double *out) {
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i = blockIdx.x * 32 + lane;
+  double v = 0.0;
+  if (i < n)
+    for (int c = warp; c < P; c += 8) v += part[c * stride + i];
+  red[warp][lane] = v;
+  __syncthreads();
+  if (warp == 0 && i < n) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w][lane];
+    out[i] = s;
   }
 }
 
@@ -542,8 +621,9 @@ __global__ void coarse_to_z_kernel(const double *uc, int64_t n, double *z) {
 
 struct SolveState {
   DBuf<GemvWork> w_op, w_loc, w_c;
-  int nw_op = 0, nw_loc = 0, nw_c = 0;
-  size_t sm_op = 0, sm_loc = 0, sm_c = 0;
+  DBuf<GemvWork> w_kd;
+  int nw_op = 0, nw_loc = 0, nw_c = 0, nw_kd = 0, max_nd = 1;
+  size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_rx = 0, sm_ex = 0, sm_kd = 0;
   DBuf<int64_t> xptr, xidx, pptr, pidx, eptr, eidx;
   DBuf<double> hist;
   bool ready = false;
@@ -612,7 +692,7 @@ static void apply_S(vb_ctx *c, SolveState *st) {   // q = S^ p  (B1, B2)
   cudaStream_t s = c->stream;
   tick(c, st, 3, true);
   tick(c, st, 0, true);
-  sym_gemv_kernel<<<st->nw_op, GV_WARPS * 32, st->sm_op, s>>>(st->w_op.p);
+  sym_gemv_kernel<GV_WARPS><<<st->nw_op, GV_WARPS * 32, st->sm_op, s>>>(st->w_op.p);
   tick(c, st, 0, false);
   b0_apply_kernel<<<c->N, 32, 0, s>>>(c->d_sub.p, c->d_loc2x.p, c->d_b0T.p, c->w_p.p,
                                       c->n_delta_glob + c->NPi, c->w_part.p, c->w_q.p);
@@ -626,22 +706,26 @@ static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   cudaStream_t s = c->stream;
   const int nslot = c->h_slot.size(), nent = c->h_ent.size();
   tick(c, st, 4, true);
-  if (nslot) restrict_kernel<<<nslot, 256, 0, s>>>(c->d_slot.p, c->d_ent.p, c->d_sub.p, c->d_Dlx.p, c->w_r.p, c->w_locD.p);
+  if (c->n_act_slots)
+    restrict_kernel<<<c->n_act_slots, DLX_WARPS * 32, st->sm_rx, s>>>(c->d_slot.p, c->d_act_slots.p, c->d_ent.p,
+                                                                     c->d_sub.p, c->d_Dt.p, c->w_r.p, c->w_locD.p);
   tick(c, st, 1, true);
-  if (st->nw_loc) sym_gemv_kernel<<<st->nw_loc, GV_WARPS * 32, st->sm_loc, s>>>(st->w_loc.p);
+  if (st->nw_loc) sym_gemv_kernel<GV_WARPS><<<st->nw_loc, GV_WARPS * 32, st->sm_loc, s>>>(st->w_loc.p);
   tick(c, st, 1, false);
-  phit_kernel<<<c->N, 256, 0, s>>>(c->d_sub.p, c->d_Phi.p, c->w_locD.p, c->w_locC.p);
+  phit_kernel<<<dim3(PHIT_SPLIT, c->N), 256, 0, s>>>(c->d_sub.p, c->d_Phi.p, c->w_locD.p, c->w_locC.p);
   coarse_rhs_kernel<<<grid_for(c->Nc), 256, 0, s>>>(st->pptr.p, st->pidx.p, c->w_locC.p, c->w_r.p,
                                                     c->n_delta_glob, c->NPi, c->N, c->w_rc.p);
   coarse_p0_project_kernel<<<1, 256, 0, s>>>(c->d_sub.p, c->N, c->w_rc.p + c->NPi, 0);
   tick(c, st, 2, true);
-  sym_gemv_kernel<<<st->nw_c, GV_WARPS * 32, st->sm_c, s>>>(st->w_c.p);
+  sym_gemv_kernel<GV_WARPS_C><<<st->nw_c, GV_WARPS_C * 32, st->sm_c, s>>>(st->w_c.p);
   tick(c, st, 2, false);
-  sum_chunks_kernel<<<grid_for(c->Nc), 256, 0, s>>>(c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
+  sum_chunks_kernel<<<(c->Nc + 31) / 32, 256, 0, s>>>(c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
   coarse_p0_project_kernel<<<1, 256, 0, s>>>(c->d_sub.p, c->N, c->w_uc.p + c->NPi, 1);
-  local2_kernel<<<c->N, 256, 64 * sizeof(double) + c->max_npi * sizeof(double), s>>>(
+  local2_kernel<<<dim3((st->max_nd + 127) / 128, c->N), 128, c->max_npi * sizeof(double), s>>>(
       c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p);
-  if (nent) extend_kernel<<<nent, 128, 0, s>>>(c->d_ent.p, c->d_slot.p, c->d_sub.p, c->d_Dlx.p, c->w_locD.p, c->w_z.p);
+  if (c->n_act_ents)
+    extend_kernel<<<c->n_act_ents, DLX_WARPS * 32, st->sm_ex, s>>>(c->d_ent.p, c->d_act_ents.p, c->d_slot.p, c->d_sub.p,
+                                                                   c->d_Dt.p, c->w_locD.p, c->w_z.p);
   coarse_to_z_kernel<<<grid_for(c->Nc), 256, 0, s>>>(c->w_uc.p, c->Nc, c->w_z.p + c->n_delta_glob);
   tick(c, st, 4, false);
   VB_STAGE();
@@ -718,10 +802,23 @@ void prepare_solve(vb_ctx *c) {
   split_rows(c->Nc, Pc, rows);
   for (int q = 0; q < Pc; ++q)
     wl.push_back(GemvWork{c->d_Kcp.p, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, rows[q].first, rows[q].second, 0});
-  st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = gemv_smem(c->Nc);
-  size_t smmax = std::max(st->sm_op, std::max(st->sm_loc, st->sm_c));
-  VB_REQUIRE(smmax <= 227 * 1024, VB_EINVAL, "packed GEMV vector exceeds shared memory (coarse too large)");
-  VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smmax));
+  st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = gemv_smem(c->Nc, GV_WARPS_C);
+  size_t smmax = std::max(st->sm_op, st->sm_loc);
+  VB_REQUIRE(smmax <= 227 * 1024 && st->sm_c <= 227 * 1024, VB_EINVAL,
+             "packed GEMV vector exceeds shared memory (coarse too large)");
+  VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smmax));
+  VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS_C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_c));
+  // deluxe restriction / extension shared memory (vectors + per-warp partials)
+  int maxnd_e = 1, maxs = 1;
+  for (auto &E : c->h_ent)
+    if (E.nd) { maxnd_e = std::max(maxnd_e, E.nd); maxs = std::max(maxs, E.nsides); }
+  const int npad = (maxnd_e + 31) / 32 * 32;
+  st->sm_rx = (size_t)(1 + DLX_WARPS) * npad * sizeof(double);
+  st->sm_ex = (size_t)(maxs + DLX_WARPS) * npad * sizeof(double);
+  VB_REQUIRE(st->sm_ex <= 227 * 1024, VB_EINVAL, "deluxe entity too large for the extension kernel");
+  VB_CUDA(cudaFuncSetAttribute(restrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_rx));
+  VB_CUDA(cudaFuncSetAttribute(extend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_ex));
+  st->max_nd = nmaxD;
   // x coordinate -> local copies (ordered by subdomain), primal -> local Pi copies
   std::vector<int64_t> loc2x;
   c->d_loc2x.download(loc2x, s);
@@ -738,11 +835,30 @@ void prepare_solve(vb_ctx *c) {
   for (int64_t j = 0; j < (int64_t)pig.size(); ++j) pr.push_back({pig[j], j});
   std::sort(pr.begin(), pr.end());
   build_csr(c->NPi, pr, st->pptr, st->pidx, s);
-  int64_t maxn = 1;
-  for (auto &S : c->h_sub) maxn = std::max<int64_t>(maxn, S.n);
-  VB_REQUIRE(maxn * 8 <= 227 * 1024, VB_EINVAL, "subdomain too large for the condensation kernel");
-  VB_CUDA(cudaFuncSetAttribute(condense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(maxn * 8)));
-  VB_CUDA(cudaFuncSetAttribute(backsub_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(maxn * 8)));
+  // B0/B8: packed K_DD^-1 GEMV work list (y_D = K_DD^-1 b_D) and buffers
+  c->w_yDp.alloc((int64_t)c->P_kd * std::max<int64_t>(c->len_Dn, 1));
+  c->w_xD.alloc(std::max<int64_t>(c->len_Dn, 1));
+  {
+    std::vector<GemvWork> wk;
+    size_t nmaxDn = 1;
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      nmaxDn = std::max<size_t>(nmaxDn, S.nD);
+      split_rows(S.nD, c->P_kd, rows);
+      for (int q = 0; q < c->P_kd; ++q)
+        wk.push_back(GemvWork{c->d_KDi.p + S.off_KDi, nullptr, c->w_bD.p + S.off_Dn,
+                              c->w_yDp.p + (int64_t)q * c->len_Dn + S.off_Dn, S.nD, rows[q].first, rows[q].second, 0});
+    }
+    st->w_kd.upload(wk, s);
+    st->nw_kd = wk.size();
+    st->sm_kd = gemv_smem(nmaxDn);
+    VB_REQUIRE(st->sm_kd <= 227 * 1024, VB_EINVAL, "Dirichlet block too large for the packed GEMV");
+    size_t smg = std::max(std::max(st->sm_op, st->sm_loc), st->sm_kd);
+    VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smg));
+    int64_t mg = 1;
+    for (auto &S : c->h_sub) mg = std::max<int64_t>(mg, S.nG);
+    VB_CUDA(cudaFuncSetAttribute(xD_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(mg * 8)));
+  }
   VB_CUDA(cudaStreamSynchronize(s));
   st->ready = true;
   // bytes per PCG iteration (model of the streamed operators)
@@ -792,11 +908,13 @@ void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit,
   const int64_t nx = c->nx, NDelta = c->n_delta_glob;
   const int64_t nvf = c->n_free_vel;
   // ---------------- B0: condensed rhs in transformed coordinates
-  int64_t maxn = 1;
-  for (auto &S : c->h_sub) maxn = std::max<int64_t>(maxn, S.n);
+  int64_t maxnG = 1, maxnD = 1;
+  for (auto &S : c->h_sub) { maxnG = std::max<int64_t>(maxnG, S.nG); maxnD = std::max<int64_t>(maxnD, S.nD); }
   c->w_r.zero(s);
-  condense_kernel<<<N, 256, maxn * 8, s>>>(c->d_sub.p, c->d_K.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p,
-                                           c->d_mvec.p, rhs, nvf, c->w_zG.p, c->w_bD.p, c->w_r.p + NDelta + c->NPi);
+  rhs_D_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p, c->d_mvec.p, rhs, nvf,
+                                 c->w_bD.p, c->w_r.p + NDelta + c->NPi);
+  sym_gemv_kernel<GV_WARPS><<<st->nw_kd, GV_WARPS * 32, st->sm_kd, s>>>(st->w_kd.p);   // y_D = K_DD^-1 b_D
+  zG_kernel<<<dim3((maxnG + 127) / 128, N), 128, 0, s>>>(c->d_sub.p, c->d_Psi.p, c->w_bD.p, c->w_zG.p);
   VB_STAGE();
   gamma_rhs_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_slot.p, c->d_sub.p, c->d_gam_free.p, rhs,
                                                    c->w_zG.p, c->d_T.p, NDelta, c->w_gam.p, c->w_r.p);
@@ -851,9 +969,10 @@ void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit,
   gamma_back_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_gam_free.p, c->d_T.p, c->w_x.p, NDelta,
                                                     c->w_gam.p, x);
   VB_STAGE();
-  backsub_kernel<<<N, 256, maxn * 8, s>>>(c->d_sub.p, c->d_K.p, c->d_subI_free.p, c->d_subP_glob.p,
-                                          c->d_subG_free.p, c->d_cvec.p, c->d_mvec.p, c->w_bD.p, x,
-                                          c->w_x.p + NDelta + c->NPi, nvf, x);
+  xD_kernel<<<dim3(XD_SPLIT, N), 256, maxnG * 8, s>>>(c->d_sub.p, c->d_Psi.p, c->w_yDp.p, c->len_Dn, c->P_kd,
+                                                      c->d_subG_free.p, x, c->w_xD.p);
+  xout_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->w_xD.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p, c->d_mvec.p,
+                                c->w_x.p + NDelta + c->NPi, nvf, x);
   VB_STAGE();
   pressure_mean_kernel<<<64, 256, 0, s>>>(c->d_cellgeo.p, c->geo_stride, c->np, c->nK, x + nvf, 0, c->w_dots.p);
   pressure_mean_kernel<<<grid_for(c->nK), 256, 0, s>>>(c->d_cellgeo.p, c->geo_stride, c->np, c->nK, x + nvf, 64, c->w_dots.p);
