@@ -55,12 +55,17 @@ typedef struct {
   double svd_rel_tol;    /* constraint filter; <= 0 means 1e-10                       */
 } vb_constraints;
 
-/* Distribution: one rank per GPU; ranks own contiguous sets of subdomains. nranks = 1 needs no
- * NCCL id.  `stream` is a cudaStream_t owned by the caller (torch); the library works on it. */
+/* Distribution: one rank per GPU; each rank owns the subdomains with
+ * subdomain_rank == rank and exchanges interface sums, coarse pieces and dot partials with the
+ * others over NCCL (NVLink).  nranks = 1 needs no NCCL id.  `stream` is a cudaStream_t owned by
+ * the caller (torch); the library works on it.  loopback_world (test infrastructure): when set,
+ * the ranks are threads of one process sharing one GPU (vb_loopback_world_create) and exchange by
+ * host-synchronised device copies instead of NCCL. */
 typedef struct {
   int32_t rank, nranks, device;
   const void *nccl_unique_id;      /* 128 bytes from vb_nccl_unique_id on rank 0, or NULL     */
   void *stream;
+  void *loopback_world;            /* NULL = NCCL                                              */
 } vb_dist;
 
 /* Analytic problem data evaluated by the library's kernels (BASELINE.json configs).
@@ -82,10 +87,16 @@ typedef struct {
   double bytes_per_iter_model, flux_violation_max;
   int32_t n_primal, n_coarse;
   int64_t n_dofs_paper;                         /* nDofs as counted in T2-T4                   */
+  int32_t n_adaptive;                           /* primal rows added by the face GEVPs */
+  double adaptive_margin;                       /* min |lambda - 1/tau| over all face pencils  */
 } vb_report;
 
 /* rank 0: fills 128 bytes to broadcast with torch.distributed before vb_setup. */
 vb_status vb_nccl_unique_id(void *out128);
+/* Test transport: a world of nranks in-process ranks (threads) on one GPU; destroy after every
+ * context using it is destroyed. */
+vb_status vb_loopback_world_create(int32_t nranks, void **world);
+vb_status vb_loopback_world_destroy(void *world);
 
 /* Build the context: topology, DOF numbering, box-free general subdomain
  * classification, interface entities, and the VEM element matrices A^K, B^K computed
@@ -118,8 +129,11 @@ vb_status vb_build_rhs(vb_ctx *ctx, const vb_problem *prob, double *rhs_dev);
 
 /* PCG on the interface saddle problem Eq.(globInt) preconditioned by
  * M^-1 = R~_D^T S~^-1 R~_D (Eq.(BDDCprec)), x0 = 0, stop at ||r|| <= rtol ||r0||.
- * rhs_dev, x_dev: caller-owned device buffers in the free-DOF layout; x gets the full solution
- * (interior back-substitution, pressure with zero global mean).  maxit <= 0 means 2000. */
+ * rhs_dev, x_dev: caller-owned device buffers in the rank's free-DOF layout (vb_dof_layout: the
+ * velocity DOFs whose lowest sharing subdomain is on this rank, then the pressure DOFs of its
+ * cells; for one rank, all free DOFs in global order); x gets the full solution (interior
+ * back-substitution, pressure with zero global mean).  maxit <= 0 means 2000.
+ * Collective: every rank calls it with the same rtol/maxit. */
 vb_status vb_pcg_solve(vb_ctx *ctx, const double *rhs_dev, double *x_dev, double rtol,
                        int32_t maxit, vb_report *rep);
 

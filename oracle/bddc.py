@@ -395,6 +395,7 @@ class BDDC:
         A = S~i:S~j, B = Si:Sj, GEVP A psi = lam B psi, keep lam < 1/tau, add rows (B Psi)^T N_F^T
         to C_F (SURVEY O-12)."""
         extra = {}
+        self.adaptive_spectra = {}
         self.adaptive_margin = np.inf
         self.adaptive_count = 0
         for e, E in enumerate(self.ents):
@@ -416,6 +417,7 @@ class BDDC:
             par = lambda X, Y: _sym(X @ np.linalg.solve(X + Y, Y))
             Aop = par(St[0], St[1]); Bop = par(Sf[0], Sf[1])
             lam, Psi = sla.eigh(Aop, Bop)
+            self.adaptive_spectra[e] = lam
             sel = lam < 1.0 / tau
             self.adaptive_margin = min(self.adaptive_margin, float(np.min(np.abs(lam - 1.0 / tau))))
             if np.any(sel):

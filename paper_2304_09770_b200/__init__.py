@@ -44,7 +44,7 @@ class VBConstraints(ctypes.Structure):
 
 class VBDist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("nccl_unique_id", _p), ("stream", _p)]
+                ("nccl_unique_id", _p), ("stream", _p), ("loopback_world", _p)]
 
 
 class VBProblem(ctypes.Structure):
@@ -59,7 +59,8 @@ class VBReport(ctypes.Structure):
                 ("true_rel_residual", ctypes.c_double),
                 ("t_setup_s", ctypes.c_double), ("t_factor_s", ctypes.c_double), ("t_solve_s", ctypes.c_double),
                 ("bytes_per_iter_model", ctypes.c_double), ("flux_violation_max", ctypes.c_double),
-                ("n_primal", ctypes.c_int32), ("n_coarse", ctypes.c_int32), ("n_dofs_paper", ctypes.c_int64)]
+                ("n_primal", ctypes.c_int32), ("n_coarse", ctypes.c_int32), ("n_dofs_paper", ctypes.c_int64),
+                ("n_adaptive", ctypes.c_int32), ("adaptive_margin", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -96,7 +97,7 @@ _vb_nccl_unique_id = _sig("vb_nccl_unique_id", ctypes.c_int, [_p])
 _vb_debug_iop = _sig("vb_debug_interface_op", ctypes.c_int, [_p, ctypes.c_int32, _dp, _dp])
 _vb_interface_dofs = _sig("vb_interface_dofs", ctypes.c_int, [_p, _i64p, _i64p])
 
-EXPORTED = ["vb_nccl_unique_id", "vb_setup", "vb_setup_from_elements", "vb_factor", "vb_build_rhs",
+EXPORTED = ["vb_nccl_unique_id", "vb_loopback_world_create", "vb_loopback_world_destroy", "vb_setup", "vb_setup_from_elements", "vb_factor", "vb_build_rhs",
             "vb_pcg_solve", "vb_pcg_solve_host", "vb_apply_operator", "vb_debug_interface_op",
             "vb_interface_dofs", "vb_num_free_dofs", "vb_dof_layout",
             "vb_cell_local_dofs", "vb_get_element_matrices", "vb_stats", "vb_kernel_times",
@@ -131,7 +132,10 @@ class Context:
     """One vb_ctx (one GPU).  Call factor(), then build_rhs()/pcg_solve() any number of times."""
 
     def __init__(self, mesh, k, cell_subdomain, n_subdomains, viscosity, constraints=None, stream=None,
-                 device=0, elements=None):
+                 device=0, elements=None, rank=0, nranks=1, subdomain_rank=None, nccl_id=None, world=None):
+        """Multi-rank (one rank per GPU): pass rank, nranks, subdomain_rank and either
+        nccl_id (128 bytes from nccl_unique_id() on rank 0, broadcast by the caller) or world (a
+        LoopbackWorld: ranks as threads of one process on one GPU, test transport)."""
         import torch
         self._keep = []
         xyz = _arr(mesh.xyz, np.float64)
@@ -148,15 +152,25 @@ class Context:
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
-        dist = VBDist(0, 1, int(device), None, ctypes.c_void_p(stream.cuda_stream))
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            self._keep.append(idbuf)
+        dist = VBDist(int(rank), int(nranks), int(device), ctypes.cast(idbuf, _p) if idbuf is not None else None,
+                      ctypes.c_void_p(stream.cuda_stream), world.handle if world is not None else None)
+        srank = None
+        if subdomain_rank is not None:
+            sr = _arr(subdomain_rank, np.int32)
+            self._keep.append(sr)
+            srank = _ptr(sr, ctypes.c_int32)
         cons = _cons(constraints)
         h = _p()
         if elements is None:
-            st = _vb_setup(ctypes.byref(m), _ptr(sub, ctypes.c_int32), int(n_subdomains), None, ctypes.byref(cons),
+            st = _vb_setup(ctypes.byref(m), _ptr(sub, ctypes.c_int32), int(n_subdomains), srank, ctypes.byref(cons),
                            _ptr(nu, ctypes.c_double), ctypes.byref(dist), ctypes.byref(h))
         else:
             pa, A, pb, B = [_arr(x, t) for x, t in zip(elements, (np.int64, np.float64, np.int64, np.float64))]
-            st = _vb_setup_el(ctypes.byref(m), _ptr(sub, ctypes.c_int32), int(n_subdomains), None, ctypes.byref(cons),
+            st = _vb_setup_el(ctypes.byref(m), _ptr(sub, ctypes.c_int32), int(n_subdomains), srank, ctypes.byref(cons),
                               _ptr(nu, ctypes.c_double), ctypes.byref(dist), _ptr(pa, ctypes.c_int64),
                               _ptr(A, ctypes.c_double), _ptr(pb, ctypes.c_int64), _ptr(B, ctypes.c_double),
                               ctypes.byref(h))
@@ -266,6 +280,50 @@ class Context:
             pass
 
 
+_vb_nccl_uid = _sig("vb_nccl_unique_id", ctypes.c_int, [_p])
+_vb_lw_create = _sig("vb_loopback_world_create", ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(_p)])
+_vb_lw_destroy = _sig("vb_loopback_world_destroy", ctypes.c_int, [_p])
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id (rank 0), to broadcast with torch.distributed before Context()."""
+    buf = ctypes.create_string_buffer(128)
+    st = _vb_nccl_uid(ctypes.cast(buf, _p))
+    if st != VB_OK:
+        raise VBError(st, _vb_last_error(None).decode())
+    return bytes(buf.raw)
+
+
+class LoopbackWorld:
+    """Test transport: nranks library ranks as threads of this process sharing one GPU."""
+
+    def __init__(self, nranks):
+        self.handle = _p()
+        st = _vb_lw_create(int(nranks), ctypes.byref(self.handle))
+        if st != VB_OK:
+            raise VBError(st, "loopback world")
+        self.nranks = nranks
+
+    def close(self):
+        if self.handle:
+            _vb_lw_destroy(self.handle)
+            self.handle = None
+
+
+def box_ranks(sub_grid, rank_grid):
+    """Subdomain -> rank for a box partition: sub_grid (sx, sy, sz) subdomains (x fastest),
+    rank_grid (rx, ry, rz) ranks, each owning a contiguous box of subdomains."""
+    sx, sy, sz = sub_grid
+    rx, ry, rz = rank_grid
+    assert sx % rx == 0 and sy % ry == 0 and sz % rz == 0
+    out = np.zeros(sx * sy * sz, np.int32)
+    for k in range(sz):
+        for j in range(sy):
+            for i in range(sx):
+                out[i + sx * (j + sy * k)] = (i // (sx // rx)) + rx * ((j // (sy // ry)) + ry * (k // (sz // rz)))
+    return out
+
+
 def problem_args(prob):
     """Library problem descriptor for a synthetic.Problem."""
     if prob.kind == "sinker":
@@ -274,9 +332,9 @@ def problem_args(prob):
     return dict(kind="manufactured")
 
 
-def context_for(prob, elements=None, constraints=None, stream=None):
+def context_for(prob, elements=None, constraints=None, stream=None, **dist):
     cons = dict(prob.constraints)
     if constraints:
         cons.update(constraints)
     return Context(prob.mesh, prob.k, prob.cell_subdomain, int(prob.cell_subdomain.max()) + 1, prob.nu_cell,
-                   constraints=cons, stream=stream, elements=elements)
+                   constraints=cons, stream=stream, elements=elements, **dist)

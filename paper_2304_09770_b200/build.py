@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libvbddc.so")
-SOURCES = ["setup.cu", "dense.cu", "factor.cu", "solve.cu", "vem.cu", "abi.cu"]
+SOURCES = ["setup.cu", "dense.cu", "factor.cu", "solve.cu", "vem.cu", "adaptive.cu", "comm.cu", "exchange.cu", "abi.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 

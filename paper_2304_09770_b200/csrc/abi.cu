@@ -12,6 +12,7 @@ static thread_local std::string g_last_error;
 static vb_status fail(vb_ctx *c, const Error &e) {
   g_last_error = e.msg;
   if (c) c->err = e.msg;
+  if (c && c->comm) c->comm->abort();   // release peers waiting in an exchange (loopback)
   return e.st;
 }
 
@@ -37,6 +38,7 @@ void layout_phase_a(vb_ctx *c) {
   cudaStream_t s = c->stream;
   c->h_sub.assign(N, SubDev{});
   std::vector<int> sub_cells;
+  std::vector<double> lvol(N);
   int64_t K = 0, G = 0, P = 0, I = 0, Dn = 0, X = 0;
   for (int i = 0; i < N; ++i) {
     Sub &S = c->subs[i];
@@ -52,13 +54,35 @@ void layout_phase_a(vb_ctx *c) {
     D.off_Dn = Dn; Dn += S.nD;
     D.off_X = X; X += (int64_t)S.nG * S.nG;
     double vol = 0, nus = 0;
-    for (int cell : S.cells) { vol += c->cellgeo[(int64_t)cell * c->geo_stride]; nus += c->nu[cell]; }
+    for (int cell : S.cells) { vol += c->cellgeo[(int64_t)cell * c->geo_stride]; nus += c->nu[c->cell_gid[cell]]; }
     D.vol = vol;
     S.vol = vol;
+    lvol[i] = vol;
     D.gamma = 1.0 / ((nus / std::max<size_t>(S.cells.size(), 1)) * vol);
   }
   c->len_K = K; c->len_G = G; c->len_P = P; c->len_I = I; c->len_Dn = Dn; c->len_X = X;
-  // entity-major slots
+  // volumes of all subdomains (C0: gathered once; every rank owns a set of subdomains)
+  c->gsub_vol.assign(c->Ng, 0.0);
+  if (c->nranks == 1) {
+    c->gsub_vol = lvol;
+  } else {
+    int maxN = 0;
+    std::vector<int> cnt(c->nranks, 0);
+    for (int g = 0; g < c->Ng; ++g) cnt[c->sub_rank[g]]++;
+    for (int r = 0; r < c->nranks; ++r) maxN = std::max(maxN, cnt[r]);
+    std::vector<double> mine(maxN, 0.0);
+    for (int i = 0; i < N; ++i) mine[i] = lvol[i];
+    DBuf<double> dm, dg;
+    dm.upload(mine, s);
+    dg.alloc((size_t)maxN * c->nranks);
+    c->comm->allgather(dm.p, dg.p, maxN, s);
+    std::vector<double> all;
+    dg.download(all, s);
+    VB_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> seen(c->nranks, 0);
+    for (int g = 0; g < c->Ng; ++g) { const int r = c->sub_rank[g]; c->gsub_vol[g] = all[(size_t)r * maxN + seen[r]++]; }
+  }
+  // entity-major slots: one per (local entity, LOCAL sharer)
   c->h_slot.clear();
   c->h_ent.assign(c->ents.size(), EntDev{});
   int64_t gam = 0;
@@ -66,9 +90,11 @@ void layout_phase_a(vb_ctx *c) {
   for (size_t e = 0; e < c->ents.size(); ++e) {
     Entity &E = c->ents[e];
     EntDev &D = c->h_ent[e];
-    D.n = E.n; D.kind = E.kind; D.nsides = E.sharers.size(); D.side_begin = c->h_slot.size();
+    D.n = E.n; D.kind = E.kind; D.nsh = E.sharers.size(); D.side_begin = c->h_slot.size();
     D.off_gam = gam; gam += E.n;
-    for (int m : E.sharers) {
+    for (int mg : E.sharers) {
+      const int m = c->sub_lid[mg];
+      if (m < 0) continue;
       Sub &S = c->subs[m];
       int j = std::lower_bound(S.ents.begin(), S.ents.end(), (int)e) - S.ents.begin();
       SlotDev sl{};
@@ -76,6 +102,7 @@ void layout_phase_a(vb_ctx *c) {
       sub_slot[m].push_back(c->h_slot.size());
       c->h_slot.push_back(sl);
     }
+    D.nsides = c->h_slot.size() - D.side_begin;
   }
   c->h_sub_slots.clear();
   for (int i = 0; i < N; ++i) {
@@ -93,7 +120,7 @@ void layout_phase_a(vb_ctx *c) {
     Pglob.insert(Pglob.end(), S.P.begin(), S.P.end());
     for (int e : S.ents) Gfree.insert(Gfree.end(), c->ents[e].dofs.begin(), c->ents[e].dofs.end());
     for (int64_t p : S.P) {
-      int64_t cell = p / c->np, a = p % c->np;
+      int64_t cell = c->cell_lid[p / c->np], a = p % c->np;
       cvec.push_back(c->cellgeo[cell * c->geo_stride + 5 + a]);
       mvec.push_back(a == 0 ? c->cellgeo[cell * c->geo_stride] : 0.0);
     }
@@ -107,20 +134,21 @@ void layout_phase_a(vb_ctx *c) {
   c->d_mvec.upload(mvec, s);
   c->d_sub_cells.upload(sub_cells, s);
   c->d_sub_slots.upload(c->h_sub_slots, s);
-  // cell -> subdomain-matrix positions
+  // local cell -> subdomain-matrix positions
   const int stride = c->nv_max + c->np;
-  std::vector<int> loc((size_t)c->nK * stride, -1);
+  std::vector<int> loc((size_t)c->nKl * stride, -1);
   std::vector<int64_t> posI(c->n_free_vel, -1);
   for (int i = 0; i < N; ++i) {
     Sub &S = c->subs[i];
     for (int j = 0; j < S.nI; ++j) posI[S.I[j]] = j;
     for (int cell : S.cells) {
+      const int64_t Kg = c->cell_gid[cell];
       int *L = &loc[(size_t)cell * stride];
-      for (int64_t j = c->cell_l2g_ptr[cell]; j < c->cell_l2g_ptr[cell + 1]; ++j) {
+      for (int64_t j = c->cell_l2g_ptr[Kg]; j < c->cell_l2g_ptr[Kg + 1]; ++j) {
         int64_t f = c->vel2free[c->cell_l2g[j]];
-        int q = j - c->cell_l2g_ptr[cell];
+        int q = j - c->cell_l2g_ptr[Kg];
         if (f < 0) continue;
-        if (posI[f] >= 0 && c->cell_sub[cell] == i && std::binary_search(S.I.begin(), S.I.end(), f)) {
+        if (posI[f] >= 0 && std::binary_search(S.I.begin(), S.I.end(), f)) {
           L[q] = posI[f];
         } else {
           // interface: find the entity of f among this subdomain's entities
@@ -132,19 +160,21 @@ void layout_phase_a(vb_ctx *c) {
           VB_REQUIRE(L[q] >= 0, VB_EINVAL, "internal: interface dof not found in its subdomain");
         }
       }
-      int64_t p0 = std::lower_bound(S.P.begin(), S.P.end(), (int64_t)cell * c->np) - S.P.begin();
+      int64_t p0 = std::lower_bound(S.P.begin(), S.P.end(), Kg * c->np) - S.P.begin();
       for (int a = 0; a < c->np; ++a) L[c->nv_max + a] = S.nI + p0 + a;
     }
   }
   c->d_cell_loc.upload(loc, s);
-  // element-by-element operator / rhs: free velocity dof -> contribution slots (cell-major order)
+  // element-by-element operator / rhs: free velocity dof -> contribution slots (local cells, in order)
   {
     std::vector<std::pair<int64_t, int64_t>> pr;
-    for (int64_t cell = 0; cell < c->nK; ++cell)
-      for (int64_t j = c->cell_l2g_ptr[cell]; j < c->cell_l2g_ptr[cell + 1]; ++j) {
+    for (int64_t cell = 0; cell < c->nKl; ++cell) {
+      const int64_t Kg = c->cell_gid[cell];
+      for (int64_t j = c->cell_l2g_ptr[Kg]; j < c->cell_l2g_ptr[Kg + 1]; ++j) {
         int64_t f = c->vel2free[c->cell_l2g[j]];
-        if (f >= 0) pr.push_back({f, cell * stride + (j - c->cell_l2g_ptr[cell])});
+        if (f >= 0) pr.push_back({f, cell * stride + (j - c->cell_l2g_ptr[Kg])});
       }
+    }
     std::sort(pr.begin(), pr.end());
     std::vector<int64_t> ptr(c->n_free_vel + 1, 0), idx(pr.size());
     for (auto &q : pr) ptr[q.first + 1]++;
@@ -152,23 +182,39 @@ void layout_phase_a(vb_ctx *c) {
     for (size_t q = 0; q < pr.size(); ++q) idx[q] = pr[q].second;
     c->d_el_ptr.upload(ptr, s);
     c->d_el_ent.upload(idx, s);
-    c->w_elt.alloc((size_t)c->nK * stride);
+    c->w_elt.alloc((size_t)c->nKl * stride);
   }
-  // greedy coloring of the subdomain adjacency (shared entities) for the coarse assembly
-  std::vector<std::vector<int>> adj(N);
-  for (auto &E : c->ents)
-    for (int a : E.sharers)
-      for (int b : E.sharers)
-        if (a != b) adj[a].push_back(b);
-  c->ncolors = 0;
-  for (int i = 0; i < N; ++i) {
-    std::vector<char> used(64, 0);
-    for (int j : adj[i]) if (j < i && c->subs[j].color < 64) used[c->subs[j].color] = 1;
-    int col = 0;
-    while (used[col]) ++col;
-    c->subs[i].color = col;
-    c->ncolors = std::max(c->ncolors, col + 1);
+  // greedy colouring of the GLOBAL subdomain adjacency (shared entities) for the coarse assembly
+  {
+    std::vector<std::vector<int>> adj(c->Ng);
+    for (auto &E : c->gents)
+      for (int a : E.sharers)
+        for (int b : E.sharers)
+          if (a != b) adj[a].push_back(b);
+    c->gsub_color.assign(c->Ng, 0);
+    c->ncolors = 0;
+    for (int i = 0; i < c->Ng; ++i) {
+      std::vector<char> used(128, 0);
+      for (int j : adj[i]) if (j < i && c->gsub_color[j] < 128) used[c->gsub_color[j]] = 1;
+      int col = 0;
+      while (used[col]) ++col;
+      c->gsub_color[i] = col;
+      c->ncolors = std::max(c->ncolors, col + 1);
+    }
   }
+  // ABI layout of the free vectors: owned velocity DOFs (lowest sharer on this rank), then the
+  // pressure DOFs of the local cells; identical to the global free numbering for one rank
+  c->owned_free.clear();
+  for (int64_t f = 0; f < c->n_free_vel; ++f)
+    if (c->dof_owner_sub[f] >= 0 && c->sub_rank[c->dof_owner_sub[f]] == c->rank) c->owned_free.push_back(f);
+  {
+    std::vector<int64_t> pl;
+    for (int64_t l = 0; l < c->nKl; ++l)
+      for (int a = 0; a < c->np; ++a) pl.push_back(c->n_free_vel + c->cell_gid[l] * c->np + a);
+    std::sort(pl.begin(), pl.end());
+    c->owned_free.insert(c->owned_free.end(), pl.begin(), pl.end());
+  }
+  c->d_owned_free.upload(c->owned_free, s);
   c->d_sub.upload(c->h_sub, s);
   c->d_slot.upload(c->h_slot, s);
   c->d_ent.upload(c->h_ent, s);
@@ -187,7 +233,7 @@ void build_transformed_maps(vb_ctx *c) {
       const EntDev &E = c->h_ent[sl.ent];
       for (int j = 0; j < sl.nd; ++j) loc2x[S.off_G + sl.offD + j] = E.off_xd + j;
       for (int j = 0; j < sl.r; ++j) {
-        loc2x[S.off_G + S.nd + sl.offPi + j] = c->n_delta_glob + E.off_pi + j;
+        loc2x[S.off_G + S.nd + sl.offPi + j] = c->n_delta_glob + E.off_pl + j;
         pig[S.off_Pi + sl.offPi + j] = E.off_pi + j;
       }
     }
@@ -199,7 +245,8 @@ void build_transformed_maps(vb_ctx *c) {
 
 // ------------------------------------------------------------------ common setup
 static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, int32_t nsub,
-                         const vb_constraints *cons, const double *nu, const vb_dist *dist) {
+                         const int32_t *sub_rank, const vb_constraints *cons, const double *nu,
+                         const vb_dist *dist) {
   VB_REQUIRE(m && cell_sub && nu && cons, VB_EINVAL, "null argument");
   VB_REQUIRE(m->k == 2 || m->k == 3, VB_EINVAL, "k must be 2 or 3");
   VB_REQUIRE(nsub >= 1, VB_EINVAL, "n_subdomains must be >= 1");
@@ -210,22 +257,38 @@ static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, i
     c->rank = dist->rank; c->nranks = dist->nranks; c->device = dist->device;
     c->stream = (cudaStream_t)dist->stream;
   }
-  VB_REQUIRE(c->nranks == 1, VB_EINVAL, "multi-rank contexts are not enabled in this build (nranks must be 1)");
+  VB_REQUIRE(c->nranks >= 1 && c->rank >= 0 && c->rank < c->nranks, VB_EINVAL, "bad rank / nranks");
   VB_CUDA(cudaSetDevice(c->device));
+  if (c->nranks > 1) {
+    VB_REQUIRE(sub_rank, VB_EINVAL, "nranks > 1 needs subdomain_rank");
+    if (dist->loopback_world) c->comm = make_loopback_comm(dist->loopback_world, c->rank);
+    else c->comm = make_nccl_comm(c->rank, c->nranks, dist->nccl_unique_id, c->device);
+    VB_REQUIRE(c->comm->nranks == c->nranks, VB_EINVAL, "communicator size differs from nranks");
+  }
   build_topology(c, m);
   c->nu.assign(nu, nu + c->nK);
   for (int64_t K = 0; K < c->nK; ++K) VB_REQUIRE(c->nu[K] > 0, VB_EINVAL, "viscosity must be positive (P:108)");
-  build_subdomains(c, cell_sub, nsub);
+  build_subdomains(c, cell_sub, nsub, c->nranks > 1 ? sub_rank : nullptr);
   cudaStream_t s = c->stream;
+  // device copies of the LOCAL cells (topology, viscosity, dof maps); vertices and the dof status are global
+  std::vector<int> topo((size_t)c->nKl * TOPO_STRIDE);
+  std::vector<double> nul(c->nKl);
+  std::vector<int> nvl(c->nKl);
+  std::vector<int64_t> l2g((size_t)c->nKl * c->nv_max, -1);
+  for (int64_t l = 0; l < c->nKl; ++l) {
+    const int64_t K = c->cell_gid[l];
+    std::copy(c->cell_topo.begin() + K * TOPO_STRIDE, c->cell_topo.begin() + (K + 1) * TOPO_STRIDE, topo.begin() + l * TOPO_STRIDE);
+    nul[l] = c->nu[K];
+    nvl[l] = c->cell_nv[K];
+    for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) l2g[l * c->nv_max + (j - c->cell_l2g_ptr[K])] = c->cell_l2g[j];
+  }
   c->d_xyz.upload(c->xyz, s);
-  c->d_topo.upload(c->cell_topo, s);
-  c->d_nu.upload(c->nu, s);
-  c->d_cell_nv.upload(c->cell_nv, s);
+  c->d_topo.upload(topo, s);
+  c->d_nu.upload(nul, s);
+  c->d_cell_nv.upload(nvl, s);
   c->d_vel2free.upload(c->vel2free, s);
-  std::vector<int64_t> l2g((size_t)c->nK * c->nv_max, -1);
-  for (int64_t K = 0; K < c->nK; ++K)
-    for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) l2g[K * c->nv_max + (j - c->cell_l2g_ptr[K])] = c->cell_l2g[j];
   c->d_cell_l2g.upload(l2g, s);
+  c->d_cell_gid.upload(c->cell_gid, s);
   cell_geometry_device(c);
   c->d_cellgeo.download(c->cellgeo, s);
   VB_CUDA(cudaStreamSynchronize(s));
@@ -238,8 +301,19 @@ extern "C" {
 
 vb_status vb_nccl_unique_id(void *out128) {
   if (!out128) return VB_EINVAL;
-  g_last_error = "NCCL is not enabled in this build (single-rank contexts only)";
-  return VB_ENCCL;
+  ABI_GUARD(nullptr, { vb::nccl_unique_id(out128); })
+}
+
+vb_status vb_loopback_world_create(int32_t nranks, void **world) {
+  if (!world || nranks < 1) return VB_EINVAL;
+  *world = vb::loopback_world_create(nranks);
+  return VB_OK;
+}
+
+vb_status vb_loopback_world_destroy(void *world) {
+  if (!world) return VB_EINVAL;
+  vb::loopback_world_destroy(world);
+  return VB_OK;
 }
 
 vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
@@ -250,7 +324,7 @@ vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n
   vb_ctx *c = new vb_ctx();
   try {
     double t0 = now_s();
-    common_setup(c, mesh, cell_subdomain, n_subdomains, cons, cell_viscosity, dist);
+    common_setup(c, mesh, cell_subdomain, n_subdomains, subdomain_rank, cons, cell_viscosity, dist);
     element_matrices_device(c);
     layout_phase_a(c);
     c->t_setup = now_s() - t0;
@@ -274,16 +348,17 @@ vb_status vb_setup_from_elements(const vb_mesh *mesh, const int32_t *cell_subdom
   vb_ctx *c = new vb_ctx();
   try {
     double t0 = now_s();
-    common_setup(c, mesh, cell_subdomain, n_subdomains, cons, cell_viscosity, dist);
+    common_setup(c, mesh, cell_subdomain, n_subdomains, subdomain_rank, cons, cell_viscosity, dist);
     VB_REQUIRE(elem_ptr_A && elem_A && elem_ptr_B && elem_B, VB_EINVAL, "null element arrays");
     const int nvm = c->nv_max, np = c->np;
-    std::vector<double> A((size_t)c->nK * nvm * nvm, 0.0), B((size_t)c->nK * np * nvm, 0.0);
-    for (int64_t K = 0; K < c->nK; ++K) {
+    std::vector<double> A((size_t)c->nKl * nvm * nvm, 0.0), B((size_t)c->nKl * np * nvm, 0.0);
+    for (int64_t l = 0; l < c->nKl; ++l) {
+      const int64_t K = c->cell_gid[l];
       const int nv = c->cell_nv[K];
       VB_REQUIRE(elem_ptr_A[K + 1] - elem_ptr_A[K] == (int64_t)nv * nv, VB_EINVAL, "element A size mismatch");
       VB_REQUIRE(elem_ptr_B[K + 1] - elem_ptr_B[K] == (int64_t)np * nv, VB_EINVAL, "element B size mismatch");
-      std::copy(elem_A + elem_ptr_A[K], elem_A + elem_ptr_A[K + 1], A.begin() + (size_t)K * nvm * nvm);
-      std::copy(elem_B + elem_ptr_B[K], elem_B + elem_ptr_B[K + 1], B.begin() + (size_t)K * np * nvm);
+      std::copy(elem_A + elem_ptr_A[K], elem_A + elem_ptr_A[K + 1], A.begin() + (size_t)l * nvm * nvm);
+      std::copy(elem_B + elem_ptr_B[K], elem_B + elem_ptr_B[K + 1], B.begin() + (size_t)l * np * nvm);
     }
     c->d_elA.upload(A, c->stream);
     c->d_elB.upload(B, c->stream);
@@ -360,6 +435,7 @@ vb_status vb_apply_operator(vb_ctx *c, const double *x_dev, double *y_dev) {
 vb_status vb_debug_interface_op(vb_ctx *c, int32_t which, const double *in, double *out) {
   if (!c || !in || !out || (which != 0 && which != 1)) return VB_EINVAL;
   if (c->state < 2) return fail(c, Error{VB_ESTATE, "vb_debug_interface_op before vb_factor"});
+  if (c->nranks != 1) return fail(c, Error{VB_EINVAL, "vb_debug_interface_op is single-rank only"});
   ABI_GUARD(c, { debug_interface_op(c, which, in, out); })
 }
 
@@ -376,15 +452,17 @@ vb_status vb_interface_dofs(const vb_ctx *c, int64_t *ids, int64_t *n) {
 
 vb_status vb_num_free_dofs(const vb_ctx *c, int64_t *n_vel, int64_t *n_p) {
   if (!c || !n_vel || !n_p) return VB_EINVAL;
-  *n_vel = c->n_free_vel;
-  *n_p = c->npres;
+  *n_p = c->nKl * c->np;
+  *n_vel = (int64_t)c->owned_free.size() - *n_p;
   return VB_OK;
 }
 
 vb_status vb_dof_layout(const vb_ctx *c, int64_t *ids) {
   if (!c || !ids) return VB_EINVAL;
-  for (int64_t i = 0; i < c->n_free_vel; ++i) ids[i] = c->free2vel[i];
-  for (int64_t p = 0; p < c->npres; ++p) ids[c->n_free_vel + p] = c->nvel + p;
+  for (size_t i = 0; i < c->owned_free.size(); ++i) {
+    const int64_t f = c->owned_free[i];
+    ids[i] = f < c->n_free_vel ? c->free2vel[f] : c->nvel + (f - c->n_free_vel);
+  }
   return VB_OK;
 }
 
@@ -401,9 +479,10 @@ vb_status vb_cell_local_dofs(const vb_ctx *c, int64_t cell, int64_t *vel_ids, in
   return VB_OK;
 }
 
-vb_status vb_get_element_matrices(const vb_ctx *c, int64_t cell, double *A, double *B) {
-  if (!c || cell < 0 || cell >= c->nK) return VB_EINVAL;
-  const int nvm = c->nv_max, np = c->np, nv = c->cell_nv[cell];
+vb_status vb_get_element_matrices(const vb_ctx *c, int64_t gcell, double *A, double *B) {
+  if (!c || gcell < 0 || gcell >= c->nK || c->cell_lid[gcell] < 0) return VB_EINVAL;
+  const int nvm = c->nv_max, np = c->np, nv = c->cell_nv[gcell];
+  const int64_t cell = c->cell_lid[gcell];
   try {
     if (A) VB_CUDA(cudaMemcpy(A, c->d_elA.p + cell * nvm * nvm, (size_t)nv * nv * 8, cudaMemcpyDeviceToHost));
     if (B) VB_CUDA(cudaMemcpy(B, c->d_elB.p + cell * np * nvm, (size_t)np * nv * 8, cudaMemcpyDeviceToHost));
@@ -421,7 +500,7 @@ vb_status vb_stats(const vb_ctx *c, int64_t *o) {
   for (auto &S : c->h_sub) { pkG += (int64_t)S.nG * (S.nG + 1) / 2; pkD += (int64_t)S.nd * (S.nd + 1) / 2; ndpi += (int64_t)S.nd * S.npi; }
   for (auto &sl : c->h_slot) ndsq += (int64_t)sl.nd * sl.nd;
   int64_t v[24] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
-                   c->NPi, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max,
+                   c->NPi_g, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max,
                    c->ncolors, pkG, pkD, ndsq, ndpi, c->Nc * (c->Nc + 1) / 2, c->last_iterations, c->nK, 0};
   memcpy(o, v, sizeof(v));
   return VB_OK;
@@ -443,6 +522,7 @@ vb_status vb_destroy(vb_ctx *c) {
   if (!c) return VB_EINVAL;
   cudaStreamSynchronize(c->stream);
   destroy_solve_state(c);
+  delete c->comm;
   delete c;
   return VB_OK;
 }

@@ -13,6 +13,7 @@
 #include <cstring>
 #include "dense.cuh"
 #include "setup.h"
+#include "exchange.h"
 
 namespace vb {
 
@@ -198,21 +199,9 @@ __global__ void deluxe_gather_kernel(const SlotDev *__restrict__ slots, const Su
   }
 }
 
-__global__ void deluxe_sum_kernel(const EntDev *__restrict__ ents, const SlotDev *__restrict__ slots,
-                                  const double *__restrict__ sidebuf, double *sumbuf) {
-  const EntDev E = ents[blockIdx.y];
-  const int nd = E.nd;
-  if (nd == 0) return;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nd * nd; idx += gridDim.x * blockDim.x) {
-    double v = 0.0;
-    for (int q = 0; q < E.nsides; ++q) v += sidebuf[slots[E.side_begin + q].off_side + idx];
-    sumbuf[E.off_sum + idx] = v;
-  }
-}
-
 __global__ void multiplicity_kernel(const SlotDev *__restrict__ slots, const EntDev *__restrict__ ents, double *Dlx) {
   const SlotDev s = slots[blockIdx.y];
-  const double v = 1.0 / ents[s.ent].nsides;
+  const double v = 1.0 / ents[s.ent].nsh;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < s.nd * s.nd; idx += gridDim.x * blockDim.x)
     Dlx[s.off_Dlx + idx] = (idx % s.nd == idx / s.nd) ? v : 0.0;
 }
@@ -237,31 +226,47 @@ __global__ void recip_diag_kernel(const double *A, int64_t ld, int n, double *ou
 }
 
 // ------------------------------------------------------------------ coarse assembly (colored)
-__global__ void coarse_assemble_kernel(const int *__restrict__ color_subs, const SubDev *__restrict__ subs,
-                                       const double *__restrict__ Kall, const int64_t *__restrict__ pi_glob,
-                                       const double *__restrict__ b0T, double *Kc, int64_t ldc, int64_t NPi) {
-  const int i = color_subs[blockIdx.y];
-  const SubDev S = subs[i];
-  const int npi = S.npi;
-  const double *Sc = Kall + S.off_K + (int64_t)S.nD * (S.n + 1) + (int64_t)S.nd * (S.n + 1);
-  const int64_t ld = S.n;
-  const int64_t *g = pi_glob + S.off_Pi;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < npi * npi; idx += gridDim.x * blockDim.x) {
-    int a = idx % npi, b = idx / npi;
-    double v = a >= b ? Sc[a + b * ld] : Sc[b + a * ld];
-    Kc[g[a] + g[b] * ldc] += v;
-  }
-  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < npi; a += gridDim.x * blockDim.x) {
-    double v = b0T[S.off_Pi + a];
-    Kc[(NPi + i) + g[a] * ldc] += v;
-    Kc[g[a] + (NPi + i) * ldc] += v;
+__global__ void coarse_augment_kernel(const double *__restrict__ vol, int N, double gam, double *Kc, int64_t ldc, int64_t NPi) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)N * N; idx += (int64_t)gridDim.x * blockDim.x) {
+    int a = idx % N, b = idx / N;
+    Kc[(NPi + a) + (NPi + b) * ldc] -= gam * vol[a] * vol[b];
   }
 }
 
-__global__ void coarse_augment_kernel(const SubDev *__restrict__ subs, int N, double gam, double *Kc, int64_t ldc, int64_t NPi) {
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < N * N; idx += gridDim.x * blockDim.x) {
-    int a = idx % N, b = idx / N;
-    Kc[(NPi + a) + (NPi + b) * ldc] -= gam * subs[a].vol * subs[b].vol;
+// C4 pieces: [S_c (npi x npi, full) | b~0 on Pi (npi)] per local subdomain, concatenated
+__global__ void coarse_piece_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Kall,
+                                    const double *__restrict__ b0T, const int64_t *__restrict__ poff, double *buf) {
+  const SubDev S = subs[blockIdx.y];
+  const int npi = S.npi;
+  const double *Sc = Kall + S.off_K + (int64_t)(S.nD + S.nd) * (S.n + 1);
+  double *o = buf + poff[blockIdx.y];
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < npi * npi + npi; idx += gridDim.x * blockDim.x) {
+    if (idx < npi * npi) {
+      const int a = idx % npi, b = idx / npi;
+      o[idx] = a >= b ? Sc[a + (int64_t)b * S.n] : Sc[b + (int64_t)a * S.n];
+    } else {
+      o[idx] = b0T[S.off_Pi + (idx - npi * npi)];
+    }
+  }
+}
+
+// coarse assembly from the gathered pieces of one colour class of GLOBAL subdomains
+__global__ void coarse_assemble_kernel2(const int *__restrict__ color_subs, const int64_t *__restrict__ poff,
+                                        const int *__restrict__ pnpi, const int64_t *__restrict__ pimoff,
+                                        const int64_t *__restrict__ pimap, const double *__restrict__ buf,
+                                        double *Kc, int64_t ldc, int64_t NPi) {
+  const int i = color_subs[blockIdx.y];
+  const int npi = pnpi[i];
+  const double *Sc = buf + poff[i];
+  const double *b0 = Sc + (int64_t)npi * npi;
+  const int64_t *g = pimap + pimoff[i];
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < npi * npi; idx += gridDim.x * blockDim.x) {
+    const int a = idx % npi, b = idx / npi;
+    Kc[g[a] + g[b] * ldc] += Sc[idx];
+  }
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < npi; a += gridDim.x * blockDim.x) {
+    Kc[(NPi + i) + g[a] * ldc] += b0[a];
+    Kc[g[a] + (NPi + i) * ldc] += b0[a];
   }
 }
 
@@ -278,20 +283,57 @@ static void check_info(vb_ctx *c, int nmat, const char *what, const std::vector<
                                     " of matrix " + std::to_string(names ? (*names)[b] : b)};
 }
 
+// primal ranks of ALL entities (each provided by the entity's owner rank = rank of its lowest
+// sharer) and the global primal numbering (entity order)
+static void global_entity_ranks(vb_ctx *c, const std::vector<int> &rank) {
+  const int nge = c->gents.size();
+  std::vector<double> mine(nge, 0.0), all;
+  for (size_t e = 0; e < c->ents.size(); ++e) {
+    const Entity &E = c->ents[e];
+    if (c->sub_rank[E.sharers[0]] == c->rank) mine[E.gid] = rank[e];
+  }
+  if (c->nranks == 1) {
+    all = mine;
+  } else {
+    DBuf<double> dm, dg;
+    dm.upload(mine, c->stream);
+    dg.alloc((size_t)nge * c->nranks);
+    c->comm->allgather(dm.p, dg.p, nge, c->stream);
+    std::vector<double> g;
+    dg.download(g, c->stream);
+    sync(c);
+    all.assign(nge, 0.0);
+    for (int r = 0; r < c->nranks; ++r)
+      for (int e = 0; e < nge; ++e) all[e] += g[(size_t)r * nge + e];
+  }
+  int64_t off = 0;
+  for (int e = 0; e < nge; ++e) {
+    c->gents[e].r = (int)all[e];
+    c->gents[e].off_pi = off;
+    off += c->gents[e].r;
+  }
+  c->NPi_g = off;
+  for (size_t e = 0; e < c->ents.size(); ++e)
+    VB_REQUIRE(c->gents[c->ents[e].gid].r == rank[e], VB_EINVAL,
+               "primal rank of entity " + std::to_string(c->ents[e].gid) + " differs between ranks");
+}
+
 // layout after the ranks of the entity bases are known
 static void layout_phase_b(vb_ctx *c, const std::vector<int> &rank) {
-  int64_t xd = 0, pi = 0;
+  global_entity_ranks(c, rank);
+  int64_t xd = 0, pl = 0;
   for (size_t e = 0; e < c->ents.size(); ++e) {
     Entity &E = c->ents[e];
     EntDev &D = c->h_ent[e];
     E.r = rank[e]; E.nd = E.n - E.r;
     D.r = E.r; D.nd = E.nd;
     E.off_d = xd; D.off_xd = xd; xd += E.nd;
-    E.off_p = pi; D.off_pi = pi; pi += E.r;
+    E.off_p = c->gents[E.gid].off_pi; D.off_pi = E.off_p;
+    E.off_pl = pl; D.off_pl = pl; pl += E.r;
   }
   c->n_delta_glob = xd;
-  c->NPi = pi;
-  c->nx = xd + pi + c->N;
+  c->NPi = pl;
+  c->nx = xd + pl + c->N;
   int64_t sum = 0, Dl = 0, side = 0;
   for (size_t e = 0; e < c->ents.size(); ++e) {
     EntDev &D = c->h_ent[e];
@@ -327,7 +369,8 @@ static void layout_phase_b(vb_ctx *c, const std::vector<int> &rank) {
   c->len_Dv = offDv; c->len_Pi = offPi; c->len_STp = STp; c->len_SDi = SDi; c->len_Phi = Phi;
 }
 
-void factor_device(vb_ctx *c) {
+// A1/A2: assembly, Dirichlet LDL^T, S_G in the trailing block of K, B0/B8 operators.
+static void stage_dirichlet(vb_ctx *c) {
   cudaStream_t s = c->stream;
   const int N = c->N;
   // ---------------- A1: assemble subdomain matrices [I | P | Gamma]
@@ -415,6 +458,13 @@ void factor_device(vb_ctx *c) {
     pack_tiles_batched(pk, s);
     c->len_KDi = lenKDi;
   }
+}
+
+// A3 (first half): entity bases, layout, S_T = T^T S_G T over the trailing block of K, packed S_T,
+// deluxe side blocks S_GD^(m) (sidebuf) and their sums (sumbuf).
+static void stage_interface(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
+  cudaStream_t s = c->stream;
+  const int N = c->N;
   // ---------------- A3: entity bases T_G = [N_G | C'^T]
   std::vector<double> rows;
   build_constraint_rows(c, rows);
@@ -503,18 +553,40 @@ void factor_device(vb_ctx *c) {
     pack_tiles_batched(pk, s);
   }
   // ---------------- deluxe side blocks S_GD^(m) (before S_T is factored)
-  DBuf<double> sidebuf, sumbuf, Wbuf, dinv;
   const int nslot = c->h_slot.size();
-  const int nent = c->h_ent.size();
-  sidebuf.alloc(std::max<int64_t>(c->len_side, 1));
+  // sums over ALL sharers: blocks of sharers on other ranks arrive by a C1 exchange
+  SlotExchange XD;
+  auto L2 = [&](int e) { return (int64_t)c->h_ent[e].nd * c->h_ent[e].nd; };
+  build_slot_exchange(c, XD, L2, [&](int sl, std::vector<int64_t> &out) {
+    const int64_t b = c->h_slot[sl].off_side, n = L2(c->h_slot[sl].ent);
+    for (int64_t q = 0; q < n; ++q) out.push_back(b + q);
+  });
+  sidebuf.alloc(std::max<int64_t>(c->len_side + XD.recv_len, 1));
   sumbuf.alloc(std::max<int64_t>(c->len_sum, 1));
-  Wbuf.alloc(std::max<int64_t>(c->len_sum, 1));
   if (nslot) {
     deluxe_gather_kernel<<<dim3(16, nslot), 256, 0, s>>>(c->d_slot.p, c->d_sub.p, c->d_K.p, sidebuf.p);
     VB_STAGE();
-    deluxe_sum_kernel<<<dim3(16, nent), 256, 0, s>>>(c->d_ent.p, c->d_slot.p, sidebuf.p, sumbuf.p);
-    VB_STAGE();
   }
+  run_slot_exchange(c, XD, sidebuf.p, sidebuf.p + c->len_side);
+  EntitySum ES;
+  build_entity_sum(c, ES, XD, L2, [&](int sl) { return c->h_slot[sl].off_side; }, c->len_side,
+                   [&](int e) { return c->h_ent[e].off_sum; });
+  run_entity_sum(c, ES, sidebuf.p, sumbuf.p);
+  VB_STAGE();
+  sync(c);
+}
+
+// A3 (second half) .. A5: dual Schur inverse, Phi, S_c, b~0, deluxe D_G^(m), coarse inverse.
+static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
+  cudaStream_t s = c->stream;
+  const int N = c->N;
+  const int nslot = c->h_slot.size();
+  const int nent = c->h_ent.size();
+  std::vector<MatDesc> mats(N), sg(N);
+  DBuf<double> X, Y, Wbuf, dinv;
+  X.alloc(c->len_X);
+  Y.alloc(c->len_X);
+  Wbuf.alloc(std::max<int64_t>(c->len_sum, 1));
   // ---------------- A3: partial LDL^T of S_T eliminating the dual block -> S_c trailing
   c->d_info.zero(s);
   for (int i = 0; i < N; ++i) {
@@ -673,29 +745,76 @@ void factor_device(vb_ctx *c) {
       VB_STAGE();
     }
   }
-  // ---------------- A5: coarse saddle matrix on (u_Pi, p_0), dense inverse
-  const int64_t Nc = c->NPi + N;
+  // ---------------- A5: coarse saddle matrix on (u_Pi, p_0) of ALL subdomains, dense inverse
+  //   C4: every rank gathers every subdomain's (S_c, b~0) and assembles/factors the same matrix
+  const int Ng = c->Ng;
+  const int64_t Nc = c->NPi_g + Ng;
   c->Nc = Nc;
   {
-    DBuf<double> Kc, Wc, dc;
+    // global piece layout: rank-major, subdomains in order within a rank
+    std::vector<int> gnpi(Ng, 0);
+    std::vector<int64_t> pimoff(Ng + 1, 0), pimap;
+    for (int g = 0; g < Ng; ++g) {
+      for (int e : c->gsub_ents[g])
+        for (int t = 0; t < c->gents[e].r; ++t) pimap.push_back(c->gents[e].off_pi + t);
+      gnpi[g] = pimap.size() - pimoff[g];
+      pimoff[g + 1] = pimap.size();
+    }
+    std::vector<int64_t> rlen(c->nranks, 0), poff(Ng, 0), lpoff(N, 0);
+    for (int g = 0; g < Ng; ++g) {
+      const int r = c->sub_rank[g];
+      poff[g] = rlen[r];
+      rlen[r] += (int64_t)gnpi[g] * gnpi[g] + gnpi[g];
+    }
+    int64_t maxlen = 1;
+    for (int r = 0; r < c->nranks; ++r) maxlen = std::max(maxlen, rlen[r]);
+    for (int g = 0; g < Ng; ++g) poff[g] += (int64_t)c->sub_rank[g] * maxlen;
+    for (int i = 0; i < N; ++i) {
+      VB_REQUIRE(gnpi[c->sub_gid[i]] == c->h_sub[i].npi, VB_EINVAL, "internal: coarse piece size mismatch");
+      lpoff[i] = poff[c->sub_gid[i]] - (int64_t)c->rank * maxlen;
+    }
+    DBuf<double> mine, gathered;
+    DBuf<int64_t> dlpoff, dpoff, dpimoff, dpimap;
+    DBuf<int> dgnpi;
+    mine.alloc(maxlen);
+    mine.zero(s);
+    dlpoff.upload(lpoff, s);
+    coarse_piece_kernel<<<dim3(8, N), 256, 0, s>>>(c->d_sub.p, c->d_K.p, c->d_b0T.p, dlpoff.p, mine.p);
+    VB_STAGE();
+    sync(c);
+    c->d_K.release();   // the dense subdomain matrices are not needed by the solve (frees ~48 MB per subdomain)
+    const double *pieces = mine.p;
+    if (c->nranks > 1) {
+      gathered.alloc((size_t)maxlen * c->nranks);
+      c->comm->allgather(mine.p, gathered.p, maxlen, s);
+      pieces = gathered.p;
+    }
+    dpoff.upload(poff, s);
+    dgnpi.upload(gnpi, s);
+    dpimoff.upload(pimoff, s);
+    if (pimap.empty()) pimap.push_back(0);
+    dpimap.upload(pimap, s);
+    DBuf<double> Kc, Wc, dc, gvol;
     Kc.alloc(Nc * Nc);
     Kc.zero(s);
     std::vector<std::vector<int>> colors(c->ncolors);
-    for (int i = 0; i < N; ++i) colors[c->subs[i].color].push_back(i);
+    for (int g = 0; g < Ng; ++g) colors[c->gsub_color[g]].push_back(g);
     for (auto &col : colors) {
       if (col.empty()) continue;
       DBuf<int> dcol;
       dcol.upload(col, s);
-      coarse_assemble_kernel<<<dim3(8, col.size()), 256, 0, s>>>(dcol.p, c->d_sub.p, c->d_K.p, c->d_pi_glob.p,
-                                                                c->d_b0T.p, Kc.p, Nc, c->NPi);
+      coarse_assemble_kernel2<<<dim3(8, col.size()), 256, 0, s>>>(dcol.p, dpoff.p, dgnpi.p, dpimoff.p, dpimap.p,
+                                                                 pieces, Kc.p, Nc, c->NPi_g);
       VB_STAGE();
       sync(c);
     }
     double nubar = 0, volO = 0;
     for (int64_t K = 0; K < c->nK; ++K) nubar += c->nu[K];
     nubar /= c->nK;
-    for (int i = 0; i < N; ++i) volO += c->h_sub[i].vol;
-    coarse_augment_kernel<<<(N * N + 255) / 256, 256, 0, s>>>(c->d_sub.p, N, 1.0 / (nubar * volO), Kc.p, Nc, c->NPi);
+    for (int g = 0; g < Ng; ++g) volO += c->gsub_vol[g];
+    gvol.upload(c->gsub_vol, s);
+    coarse_augment_kernel<<<(int)std::min<int64_t>(((int64_t)Ng * Ng + 255) / 256, 4096), 256, 0, s>>>(
+        gvol.p, Ng, 1.0 / (nubar * volO), Kc.p, Nc, c->NPi_g);
     VB_STAGE();
     c->d_info.zero(s);
     std::vector<MatDesc> cm{MatDesc{Kc.p, (int)Nc, (int)Nc, (int)Nc}};
@@ -724,6 +843,36 @@ void factor_device(vb_ctx *c) {
   double fv;
   memcpy(&fv, &vv, 8);
   c->flux_violation = fv;
+}
+
+void factor_device(vb_ctx *c) {
+  cudaStream_t s = c->stream;
+  stage_dirichlet(c);
+  DBuf<double> sidebuf, sumbuf;
+  const double tau = c->cons.adaptive_tau;
+  c->extra_rows.assign(c->ents.size(), std::vector<double>());
+  c->n_adaptive = 0;
+  c->adaptive_margin = INFINITY;
+  if (tau > 0) {
+    // keep S_G: the interface stage overwrites it with S_T, and the enriched pass starts again from S_G
+    DBuf<double> SG;
+    SG.alloc(c->len_X);
+    for (int i = 0; i < c->N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      VB_CUDA(cudaMemcpy2DAsync(SG.p + S.off_X, S.nG * 8, c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), (size_t)S.n * 8,
+                                S.nG * 8, S.nG, cudaMemcpyDeviceToDevice, s));
+    }
+    stage_interface(c, sidebuf, sumbuf);
+    adaptive_enrich(c, tau, sidebuf);           // A6: face GEVPs -> c->extra_rows
+    for (int i = 0; i < c->N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      VB_CUDA(cudaMemcpy2DAsync(c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), (size_t)S.n * 8, SG.p + S.off_X, S.nG * 8,
+                                S.nG * 8, S.nG, cudaMemcpyDeviceToDevice, s));
+    }
+    sync(c);
+  }
+  stage_interface(c, sidebuf, sumbuf);
+  stage_dual(c, sidebuf, sumbuf);
 }
 
 }  // namespace vb

@@ -6,6 +6,7 @@
 #include <vector>
 #include <cuda_runtime.h>
 #include "../../include/vbddc.h"
+#include "comm.h"
 
 namespace vb {
 
@@ -85,13 +86,21 @@ inline int64_t packed_tiles(int n) {
   return nt * (nt + 1) / 2;
 }
 
-struct Entity {
+struct GEnt {                  // global interface entity (every rank holds the whole list)
+  std::vector<int> sharers;     // global subdomain ids (sorted)
+  int n = 0, kind = 0, r = -1;  // DOFs, kind, primal rank (after the constraint filter)
+  int64_t off_pi = 0;           // offset of its primal coordinates in the global u_Pi
+};
+
+struct Entity {                 // interface entity touched by a local subdomain
+  int gid = -1;                 // global entity id
   int kind = 0;                 // 0 vertex, 1 edge, 2 face
-  std::vector<int> sharers;     // subdomains (sorted)
+  std::vector<int> sharers;     // GLOBAL subdomain ids (sorted), local or not
   std::vector<int64_t> dofs;    // free velocity ids (sorted)
   int n = 0, r = 0, nd = 0;
-  int64_t off_d = 0;            // offset of its dual coords in the global coordinate vector
-  int64_t off_p = 0;            // offset of its primal coords within u_Pi
+  int64_t off_d = 0;            // offset of its dual coords in the (rank-local) PCG vector
+  int64_t off_p = 0;            // offset of its primal coords within the GLOBAL u_Pi
+  int64_t off_pl = 0;           // offset of its primal coords within the rank-local primal block
   int64_t off_T = 0;            // offset of T_G (n x n, column-major) in the T buffer
   int64_t off_C = 0;            // offset of constraint rows C_G (rows x n, row-major)
   int nrows_C = 0;
@@ -154,8 +163,9 @@ struct SlotDev {              // one (entity, sharer) pair; slots are entity-maj
 };
 
 struct EntDev {
-  int n, nd, r, nsides, side_begin, kind, nrowsC, pad;
+  int n, nd, r, nsides, side_begin, kind, nrowsC, nsh;   // nsides: local sharers; nsh: all sharers
   int64_t off_T, off_C, off_xd, off_pi, off_gam, off_sum, off_W;
+  int64_t off_pl;             // rank-local primal offset (x = [dual | local primal | p0])
 };
 
 struct KTimer {
@@ -170,6 +180,7 @@ struct vb_ctx {
   int k = 2;
   vb_constraints cons{};
   int rank = 0, nranks = 1, device = 0;
+  vb::Comm *comm = nullptr;          // null for nranks = 1
   cudaStream_t stream = nullptr;
   std::string err;
   int state = 0;  // 1 = setup, 2 = factored
@@ -193,15 +204,26 @@ struct vb_ctx {
   std::vector<int64_t> cell_l2g;
   std::vector<int> cell_topo;            // packed local topology for the element kernel
   int topo_stride = 0;
-  // ---------------- subdomains / entities
-  int N = 0;
+  // ---------------- subdomains / entities (global view + the local part of this rank)
+  int Ng = 0;                        // global subdomain count
+  std::vector<int> sub_rank, sub_gid, sub_lid;     // rank of each global sub; local<->global ids
+  std::vector<int64_t> cell_gid, cell_lid;         // local<->global cell ids
+  int64_t nKl = 0;                   // local cells
+  std::vector<int> gsub_ncell;
+  std::vector<int> dof_owner_sub, dof_nsh;         // per free velocity DOF: lowest sharer, #sharers
+  std::vector<vb::GEnt> gents;
+  std::vector<std::vector<int>> gsub_ents;         // global sub -> global entities (sorted)
+  std::vector<int> gent_lid;                       // global entity -> local entity (-1)
+  std::vector<double> gsub_vol;                    // volumes of all subdomains
+  int64_t NPi_g = 0;                 // global primal count (coarse = NPi_g + Ng)
+  int N = 0;                         // local subdomains
   std::vector<int> cell_sub;
   std::vector<vb::Sub> subs;
   std::vector<vb::Entity> ents;
   int64_t nGamma = 0;                // number of interface (original) DOFs
-  int64_t n_delta_glob = 0;          // global dual coordinates
-  int64_t NPi = 0;                   // global primal count
-  int64_t nx = 0;                    // PCG vector length = n_delta_glob + NPi + N
+  int64_t n_delta_glob = 0;          // dual coordinates of the local entities
+  int64_t NPi = 0;                   // primal coordinates of the local entities
+  int64_t nx = 0;                    // rank-local PCG vector length = n_delta_glob + NPi + N
   int ncolors = 0;
   // ---------------- device data
   vb::DBuf<double> d_xyz, d_nu;
@@ -269,4 +291,15 @@ struct vb_ctx {
   int last_iterations = 0;
   std::vector<std::string> ktime_name;
   double t_setup = 0, t_factor = 0;
+  // adaptive coarse space (A6): extra constraint rows per entity (rows x n, row-major)
+  std::vector<std::vector<double>> extra_rows;
+  int n_adaptive = 0;
+  double adaptive_margin = 0;
+  // multi-rank
+  vb::DBuf<double> w_red;            // C3 scratch (nranks x k)
+  vb::DBuf<int64_t> d_cell_gid;      // local cell -> global cell (pressure indexing)
+  std::vector<int> gsub_color;       // colouring of the global subdomain adjacency (coarse assembly)
+  std::vector<int64_t> owned_free;   // ABI layout: owned free DOF ids (global free numbering)
+  vb::DBuf<int64_t> d_owned_free;
+  vb::DBuf<double> w_rhsg, w_xg;     // global-layout free vectors (nranks > 1)
 };

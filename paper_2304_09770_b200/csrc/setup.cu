@@ -183,15 +183,36 @@ void build_topology(vb_ctx *c, const vb_mesh *m) {
 }
 
 // ------------------------------------------------------------------ subdomains and entities
-void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int N) {
-  c->N = N;
+// Interface entities are classified GLOBALLY (every rank sees the whole mesh): classes
+// of interface DOFs with equal sharer sets.  The context then keeps only its LOCAL subdomains
+// (subdomain_rank == rank, renumbered 0..N-1 in global order), the cells of those subdomains
+// (renumbered in global order) and the entities they touch (renumbered in global order).
+void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t *sub_rank) {
+  c->Ng = Ng;
   c->cell_sub.assign(cell_sub, cell_sub + c->nK);
-  c->subs.assign(N, Sub());
+  c->sub_rank.assign(Ng, 0);
+  if (sub_rank) c->sub_rank.assign(sub_rank, sub_rank + Ng);
+  for (int i = 0; i < Ng; ++i)
+    VB_REQUIRE(c->sub_rank[i] >= 0 && c->sub_rank[i] < c->nranks, VB_EINVAL, "subdomain_rank out of range");
+  c->sub_gid.clear();
+  c->sub_lid.assign(Ng, -1);
+  for (int i = 0; i < Ng; ++i)
+    if (c->sub_rank[i] == c->rank) { c->sub_lid[i] = c->sub_gid.size(); c->sub_gid.push_back(i); }
+  const int N = c->N = c->sub_gid.size();
+  VB_REQUIRE(N >= 1, VB_EINVAL, "rank " + std::to_string(c->rank) + " owns no subdomain");
+  c->cell_lid.assign(c->nK, -1);
+  c->cell_gid.clear();
+  c->gsub_ncell.assign(Ng, 0);
   for (int64_t K = 0; K < c->nK; ++K) {
-    VB_REQUIRE(cell_sub[K] >= 0 && cell_sub[K] < N, VB_EINVAL, "cell_subdomain out of range");
-    c->subs[cell_sub[K]].cells.push_back(K);
+    VB_REQUIRE(cell_sub[K] >= 0 && cell_sub[K] < Ng, VB_EINVAL, "cell_subdomain out of range");
+    c->gsub_ncell[cell_sub[K]]++;
+    if (c->sub_lid[cell_sub[K]] >= 0) { c->cell_lid[K] = c->cell_gid.size(); c->cell_gid.push_back(K); }
   }
-  // (free dof, subdomain) pairs -> sharer sets
+  for (int i = 0; i < Ng; ++i) VB_REQUIRE(c->gsub_ncell[i] > 0, VB_EINVAL, "empty subdomain " + std::to_string(i));
+  c->nKl = c->cell_gid.size();
+  c->subs.assign(N, Sub());
+  for (int64_t l = 0; l < c->nKl; ++l) c->subs[c->sub_lid[cell_sub[c->cell_gid[l]]]].cells.push_back(l);
+  // (free dof, subdomain) pairs -> sharer sets (global)
   std::vector<std::pair<int64_t, int>> ds;
   for (int64_t K = 0; K < c->nK; ++K)
     for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) {
@@ -203,14 +224,15 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int N) {
   std::map<std::vector<int>, int> emap;
   std::vector<std::vector<int>> ekeys;
   std::vector<std::vector<int64_t>> edofs;
-  std::vector<int> owner_sub(c->n_free_vel, -1);   // for interior dofs
+  c->dof_owner_sub.assign(c->n_free_vel, -1);
+  c->dof_nsh.assign(c->n_free_vel, 0);
   for (size_t i = 0; i < ds.size();) {
     size_t j = i;
     std::vector<int> sh;
     while (j < ds.size() && ds[j].first == ds[i].first) sh.push_back(ds[j++].second);
-    if (sh.size() == 1) {
-      owner_sub[ds[i].first] = sh[0];
-    } else {
+    c->dof_owner_sub[ds[i].first] = sh[0];
+    c->dof_nsh[ds[i].first] = sh.size();
+    if (sh.size() > 1) {
       auto it = emap.find(sh);
       int e;
       if (it == emap.end()) { e = ekeys.size(); emap[sh] = e; ekeys.push_back(sh); edofs.push_back({}); }
@@ -219,36 +241,53 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int N) {
     }
     i = j;
   }
-  // entities ordered by their smallest DOF
+  // global entities ordered by their smallest DOF
   std::vector<int> order(ekeys.size());
   std::iota(order.begin(), order.end(), 0);
   std::sort(order.begin(), order.end(), [&](int a, int b) { return edofs[a][0] < edofs[b][0]; });
-  c->ents.assign(order.size(), Entity());
+  const int nge = order.size();
+  c->gents.assign(nge, GEnt());
+  c->gsub_ents.assign(Ng, std::vector<int>());
+  c->gent_lid.assign(nge, -1);
+  c->ents.clear();
   c->nGamma = 0;
-  for (size_t q = 0; q < order.size(); ++q) {
-    Entity &E = c->ents[q];
-    E.sharers = ekeys[order[q]];
-    E.dofs = edofs[order[q]];
-    E.n = E.dofs.size();
-    c->nGamma += E.n;
+  for (int q = 0; q < nge; ++q) {
+    GEnt &G = c->gents[q];
+    G.sharers = ekeys[order[q]];
+    G.n = edofs[order[q]].size();
     bool vert = true;
-    int64_t v0 = c->free2vel[E.dofs[0]] / 3;
-    for (auto d : E.dofs) { int64_t g = c->free2vel[d]; if (g >= c->oE || g / 3 != v0) vert = false; }
-    E.kind = vert ? 0 : (E.sharers.size() == 2 ? 2 : 1);
-    for (int s : E.sharers) c->subs[s].ents.push_back(q);
+    int64_t v0 = c->free2vel[edofs[order[q]][0]] / 3;
+    for (auto d : edofs[order[q]]) { int64_t g = c->free2vel[d]; if (g >= c->oE || g / 3 != v0) vert = false; }
+    G.kind = vert ? 0 : (G.sharers.size() == 2 ? 2 : 1);
+    for (int s : G.sharers) c->gsub_ents[s].push_back(q);
+    bool local = false;
+    for (int s : G.sharers) local |= c->sub_lid[s] >= 0;
+    if (!local) continue;
+    c->gent_lid[q] = c->ents.size();
+    Entity E;
+    E.gid = q;
+    E.sharers = G.sharers;
+    E.dofs = edofs[order[q]];
+    E.n = G.n;
+    E.kind = G.kind;
+    c->nGamma += E.n;
+    for (int s : E.sharers)
+      if (c->sub_lid[s] >= 0) c->subs[c->sub_lid[s]].ents.push_back(c->ents.size());
+    c->ents.push_back(std::move(E));
   }
-  // per-subdomain orderings
-  std::vector<int64_t> posI(c->n_free_vel, -1);
+  // per-subdomain orderings (local subdomains)
   for (int i = 0; i < N; ++i) {
     Sub &S = c->subs[i];
+    const int gi = c->sub_gid[i];
     std::sort(S.ents.begin(), S.ents.end());
     std::vector<int64_t> fr;
-    for (int K : S.cells) {
+    for (int l : S.cells) {
+      const int64_t K = c->cell_gid[l];
       for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) {
         int64_t f = c->vel2free[c->cell_l2g[j]];
-        if (f >= 0 && owner_sub[f] == i) fr.push_back(f);
+        if (f >= 0 && c->dof_nsh[f] == 1 && c->dof_owner_sub[f] == gi) fr.push_back(f);
       }
-      for (int q = 0; q < c->np; ++q) S.P.push_back((int64_t)K * c->np + q);
+      for (int q = 0; q < c->np; ++q) S.P.push_back(K * c->np + q);
     }
     std::sort(fr.begin(), fr.end()); fr.erase(std::unique(fr.begin(), fr.end()), fr.end());
     S.I = fr;
@@ -353,6 +392,12 @@ void build_constraint_rows(vb_ctx *c, std::vector<double> &rows_out) {
       }
       if (c->cons.face_avg) for (int d = 0; d < 3; ++d) R.push_back(avg[d]);
       if (c->cons.face_flux) R.push_back(flux);
+    }
+    // adaptive rows (SURVEY O-12 step 5), appended after the standard constraints
+    size_t eid = &E - &c->ents[0];
+    if (eid < c->extra_rows.size() && !c->extra_rows[eid].empty()) {
+      const std::vector<double> &X = c->extra_rows[eid];
+      for (size_t q = 0; q + n <= X.size(); q += n) R.push_back(std::vector<double>(X.begin() + q, X.begin() + q + n));
     }
     E.nrows_C = R.size();
     E.off_C = rows_out.size();

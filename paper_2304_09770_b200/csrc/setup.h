@@ -32,7 +32,7 @@ inline void dbg(vb_ctx *c, const char *what) {
 void gauss_legendre01(int n, double *x, double *w);
 void gauss_lobatto01(int npts, double *x, double *w);
 void build_topology(vb_ctx *c, const vb_mesh *m);
-void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int N);
+void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t *sub_rank);
 void face_frame(const vb_ctx *c, int64_t f, double *area, double n[3], double t1[3], double t2[3]);
 void build_constraint_rows(vb_ctx *c, std::vector<double> &rows_out);
 
@@ -45,6 +45,7 @@ void destroy_solve_state(vb_ctx *c);                     // solve.cu
 void element_matrices_device(vb_ctx *c);                 // vem.cu  (K9)
 void build_rhs_device(vb_ctx *c, const vb_problem *p, double *rhs);   // vem.cu
 void factor_device(vb_ctx *c);                           // factor.cu
+void adaptive_enrich(vb_ctx *c, double tau, const DBuf<double> &sidebuf);   // adaptive.cu (A6)
 void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit, vb_report *rep);
 void apply_operator_device(vb_ctx *c, const double *x, double *y);    // solve.cu (K7)
 void debug_interface_op(vb_ctx *c, int which, const double *in, double *out);   // solve.cu

@@ -9,6 +9,7 @@
 #include <cmath>
 #include "dense.cuh"
 #include "setup.h"
+#include "exchange.h"
 
 namespace vb {
 
@@ -35,21 +36,32 @@ struct GemvWork {
 constexpr int GV_WARPS = 4;      // subdomain matrices (several CTAs per SM)
 constexpr int GV_WARPS_C = 8;    // the single coarse matrix (one CTA per SM)
 
-template <int GV_WARPS>
+// BIG: vectors too long for shared memory (large coarse problems): x is read through the L2 (it is
+// small next to the streamed matrix) and the partial output accumulates in the CTA's own global
+// partial vector (each column J is owned by one warp, so there are no races).
+template <int GV_WARPS, bool BIG = false>
 __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork *__restrict__ work) {
   extern __shared__ double sm[];
   const GemvWork W = work[blockIdx.x];
   const int n = W.n, nt = (n + 31) / 32;
   const int npad = nt * 32;
-  double *xs = sm;              // npad
-  double *ys = sm + npad;       // npad
-  double *rowred = ys + npad;   // GV_WARPS * 32
+  double *xs = BIG ? nullptr : sm;              // npad
+  double *ys = BIG ? W.out : sm + npad;         // npad (BIG: n, guarded)
+  double *rowred = BIG ? sm : sm + 2 * npad;    // GV_WARPS * 32
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int j = tid; j < npad; j += blockDim.x) {
-    double v = 0.0;
-    if (j < n) v = W.map ? W.xsrc[W.map[j]] : W.xsrc[j];
-    xs[j] = v;
-    ys[j] = 0.0;
+  auto X = [&](int j) -> double {
+    if (BIG) return j < n ? __ldg(W.xsrc + j) : 0.0;
+    return xs[j];
+  };
+  if (BIG) {
+    for (int j = tid; j < n; j += blockDim.x) ys[j] = 0.0;
+  } else {
+    for (int j = tid; j < npad; j += blockDim.x) {
+      double v = 0.0;
+      if (j < n) v = W.map ? W.xsrc[W.map[j]] : W.xsrc[j];
+      xs[j] = v;
+      ys[j] = 0.0;
+    }
   }
   __syncthreads();
   for (int I = W.r0; I < W.r1; ++I) {
@@ -57,20 +69,20 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
     double rsum[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) rsum[r] = 0.0;
-    const double xI_lane = xs[32 * I + lane];
+    const double xI_lane = X(32 * I + lane);
     for (int J = warp; J <= I; J += GV_WARPS) {
       const double *T = rowbase + (int64_t)J * 1024;
       double t[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) t[r] = __ldg(T + r * 32 + lane);
-      const double xJ = xs[32 * J + lane];
+      const double xJ = X(32 * J + lane);
       double csum = 0.0;
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         rsum[r] += t[r] * xJ;
         csum += t[r] * __shfl_sync(FULL, xI_lane, r);
       }
-      if (J < I) ys[32 * J + lane] += csum;   // transpose contribution, one warp per J
+      if (J < I && (!BIG || 32 * J + lane < n)) ys[32 * J + lane] += csum;   // transpose part, one warp per J
     }
     // transpose-reduce rsum across lanes: lane l ends with sum over lanes of rsum[l]
 #pragma unroll
@@ -89,11 +101,12 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
       double v = 0.0;
 #pragma unroll
       for (int w = 0; w < GV_WARPS; ++w) v += rowred[w * 32 + lane];
-      ys[32 * I + lane] += v;
+      if (!BIG || 32 * I + lane < n) ys[32 * I + lane] += v;
     }
     __syncthreads();
   }
-  for (int j = tid; j < n; j += blockDim.x) W.out[j] = ys[j];
+  if (!BIG)
+    for (int j = tid; j < n; j += blockDim.x) W.out[j] = ys[j];
 }
 
 static size_t gemv_smem(int nmax, int warps = GV_WARPS) {
@@ -119,42 +132,51 @@ static void split_rows(int n, int P, std::vector<std::pair<int, int>> &out) {
 }
 
 // ------------------------------------------------------------------ small kernels of the loop
-// q_x[g] = sum over local copies and over the P partial chunks (deterministic order)
-__global__ void gather_sum_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ idx,
-                                  const double *__restrict__ part, int64_t part_stride, int P, int64_t n,
-                                  double *out) {
+// per local subdomain: s_j = sum over the P partial chunks of the packed GEMV (fixed order), plus
+// the b0 coupling on the primal coordinates: s_Pi += b~0 p0_i (Eq.(globInt) row 1); and
+// q0_i = b~0 . u_Pi^(i) (row 2), written to the rank-local p0 position of q.
+__global__ void chunk_sum_b0_kernel(const SubDev *__restrict__ subs, const double *__restrict__ part, int64_t stride,
+                                    int P, const double *__restrict__ b0T, const int64_t *__restrict__ loc2x,
+                                    const double *__restrict__ p, int64_t p0off, double *sbuf, double *q) {
+  const SubDev S = subs[blockIdx.y];
+  const double p0 = p[p0off + blockIdx.y];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S.nG; j += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int c = 0; c < P; ++c) v += part[c * stride + S.off_G + j];
+    if (j >= S.nd) v += b0T[S.off_Pi + (j - S.nd)] * p0;
+    sbuf[S.off_G + j] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    double acc = 0.0;
+    for (int a = threadIdx.x; a < S.npi; a += 32) acc += b0T[S.off_Pi + a] * p[loc2x[S.off_G + S.nd + a]];
+    acc = warp_sum(acc);
+    if (threadIdx.x == 0) q[p0off + blockIdx.y] = acc;
+  }
+}
+
+// out[g] = sum over the CSR sources of g (fixed order: sharers in global subdomain order)
+__global__ void gather_src_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ idx,
+                                  const double *__restrict__ src, int64_t n, double *out) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
     double v = 0.0;
-    for (int64_t q = ptr[g]; q < ptr[g + 1]; ++q) {
-      const int64_t j = idx[q];
-      for (int c = 0; c < P; ++c) v += part[c * part_stride + j];
-    }
+    for (int64_t q = ptr[g]; q < ptr[g + 1]; ++q) v += src[idx[q]];
     out[g] = v;
   }
 }
 
-// b0 coupling: q_Pi += sum_i b0T_i p0_i  (into the partial of chunk 0), q0_i = b0T_i . u_Pi^(i)
-__global__ void b0_apply_kernel(const SubDev *__restrict__ subs, const int64_t *__restrict__ loc2x,
-                                const double *__restrict__ b0T, const double *__restrict__ p,
-                                int64_t p0off, double *part0, double *q) {
-  const SubDev S = subs[blockIdx.x];
-  const double p0 = p[p0off + blockIdx.x];
-  double acc = 0.0;
-  for (int a = threadIdx.x; a < S.npi; a += 32) {
-    const int64_t j = S.off_G + S.nd + a;
-    const double b = b0T[S.off_Pi + a];
-    part0[j] += b * p0;
-    acc += b * p[loc2x[j]];
-  }
-  acc = warp_sum(acc);
-  if (threadIdx.x == 0) q[p0off + blockIdx.x] = acc;
-}
-
 // block partial dot products (fixed grid) -> part[blockIdx]
-__global__ void dot_partial_kernel(const double *__restrict__ a, const double *__restrict__ b, int64_t n, double *part) {
+// mask (multi-rank): 1 on the coordinates this rank owns, 0 on ghost copies
+__global__ void dot_partial_kernel(const double *__restrict__ a, const double *__restrict__ b,
+                                   const double *__restrict__ mask, int64_t n, double *part) {
   __shared__ double red[32];
   double v = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v += a[i] * b[i];
+  if (mask) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      v += mask[i] * (a[i] * b[i]);
+  } else {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      v += a[i] * b[i];
+  }
   v = warp_sum(v);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
@@ -256,27 +278,14 @@ __global__ void __launch_bounds__(256) phit_kernel(const SubDev *__restrict__ su
   }
 }
 
-// rc[pi] = r_Pi[pi] + sum over copies c_i; rc[NPi + i] = r0_i
-__global__ void coarse_rhs_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ idx,
-                                  const double *__restrict__ cpart, const double *__restrict__ r,
-                                  int64_t NDelta, int64_t NPi, int N, double *rc) {
-  const int64_t n = NPi + N;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
-    double v = r[NDelta + g];
-    if (g < NPi)
-      for (int64_t q = ptr[g]; q < ptr[g + 1]; ++q) v += cpart[idx[q]];
-    rc[g] = v;
-  }
-}
-
 // p0 projections of the coarse problem (gauge sum vol_i p0_i = 0, A5):
 // mode 0 (input):  rc_p0 -= vol * (sum rc_p0) / sum vol ;  mode 1 (output): uc_p0 -= (vol . uc_p0)/sum vol
-__global__ void coarse_p0_project_kernel(const SubDev *__restrict__ subs, int N, double *v, int mode) {
+__global__ void coarse_p0_project_kernel(const double *__restrict__ vol, int N, double *v, int mode) {
   __shared__ double red[32];
   double a = 0.0, w = 0.0;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    a += mode == 0 ? v[i] : subs[i].vol * v[i];
-    w += subs[i].vol;
+    a += mode == 0 ? v[i] : vol[i] * v[i];
+    w += vol[i];
   }
   a = warp_sum(a); w = warp_sum(w);
   __shared__ double ra[32], rw[32];
@@ -289,7 +298,7 @@ __global__ void coarse_p0_project_kernel(const SubDev *__restrict__ subs, int N,
   }
   __syncthreads();
   const double mean = red[0];
-  for (int i = threadIdx.x; i < N; i += blockDim.x) v[i] -= mode == 0 ? subs[i].vol * mean : mean;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) v[i] -= mode == 0 ? vol[i] * mean : mean;
 }
 
 // w_i = sum_chunks y_i + Phi_i u_Pi^(i)   (thread per row of column-major Phi, 4 accumulators)
@@ -317,34 +326,32 @@ __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ 
   w[S.off_Dv + j] = v + ((a0 + a1) + (a2 + a3));
 }
 
-// extension with deluxe scaling: z_x[off_xd + i] = sum_m sum_j D^(m)[i, j] w^(m)[offD_m + j];
-// warps stream (side, 32x32 row-major tile) units, lane = tile column; the row sums come from a
-// transpose-reduce; per-warp row partials are summed in fixed order.  One CTA per active entity.
-__global__ void __launch_bounds__(DLX_WARPS * 32) extend_kernel(const EntDev *__restrict__ ents,
-                              const int *__restrict__ act, const SlotDev *__restrict__ slots,
-                              const SubDev *__restrict__ subs, const double *__restrict__ Dt,
-                              const double *__restrict__ w, double *z) {
+// extension with deluxe scaling, per local slot: t^(m) = D^(m) w^(m) (the entity sum over all sharers
+// follows in fixed order).  Warps stream 32x32 row-major tiles, lane = tile column; row sums by a
+// transpose-reduce; per-warp row partials summed in fixed order.  One CTA per active slot.
+__global__ void __launch_bounds__(DLX_WARPS * 32) slot_extend_kernel(const SlotDev *__restrict__ slots,
+                              const int *__restrict__ act, const SubDev *__restrict__ subs,
+                              const double *__restrict__ Dt, const int64_t *__restrict__ toff,
+                              const double *__restrict__ w, double *t) {
   extern __shared__ double sh[];
-  const EntDev E = ents[act[blockIdx.x]];
-  const int nd = E.nd;
+  const int slot = act[blockIdx.x];
+  const SlotDev s = slots[slot];
+  const int nd = s.nd;
   const int nt = (nd + 31) / 32, npad = nt * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double *ws = sh;                        // nsides * npad
-  double *part = sh + E.nsides * npad;    // nw * npad
-  for (int q = 0; q < E.nsides; ++q) {
-    const SlotDev s = slots[E.side_begin + q];
-    const double *src = w + subs[s.sub].off_Dv + s.offD;
-    for (int i = threadIdx.x; i < npad; i += blockDim.x) ws[q * npad + i] = i < nd ? src[i] : 0.0;
-  }
+  double *ws = sh;                 // npad
+  double *part = sh + npad;        // nw * npad
+  const double *src = w + subs[s.sub].off_Dv + s.offD;
+  for (int i = threadIdx.x; i < npad; i += blockDim.x) ws[i] = i < nd ? src[i] : 0.0;
   for (int i = threadIdx.x; i < nw * npad; i += blockDim.x) part[i] = 0.0;
   __syncthreads();
-  for (int u = warp; u < E.nsides * nt * nt; u += nw) {
-    const int q = u / (nt * nt), tile = u % (nt * nt), I = tile / nt, J = tile % nt;
-    const double *T = Dt + slots[E.side_begin + q].off_Dt + (int64_t)tile * 1024;
+  for (int u = warp; u < nt * nt; u += nw) {
+    const int I = u / nt, J = u % nt;
+    const double *T = Dt + s.off_Dt + (int64_t)u * 1024;
     double p[32];
 #pragma unroll
     for (int rr = 0; rr < 32; ++rr) p[rr] = __ldg(T + rr * 32 + lane);
-    const double wc = ws[q * npad + 32 * J + lane];
+    const double wc = ws[32 * J + lane];
 #pragma unroll
     for (int rr = 0; rr < 32; ++rr) p[rr] *= wc;
 #pragma unroll
@@ -360,10 +367,11 @@ __global__ void __launch_bounds__(DLX_WARPS * 32) extend_kernel(const EntDev *__
     part[warp * npad + 32 * I + lane] += p[0];
   }
   __syncthreads();
+  double *out = t + toff[slot];
   for (int i = threadIdx.x; i < nd; i += blockDim.x) {
     double v = 0.0;
     for (int w2 = 0; w2 < nw; ++w2) v += part[w2 * npad + i];
-    z[E.off_xd + i] = v;
+    out[i] = v;
   }
 }
 
@@ -463,23 +471,12 @@ __global__ void xout_kernel(const SubDev *__restrict__ subs, const double *__res
   for (int a = tid; a < S.nP; a += blockDim.x) xout[nvf + Pglob[S.off_P + a]] = t[S.nI + a] + shift * cvec[S.off_P + a];
 }
 
-// per entity: ghat_e = b_e + sum_m zG^(m)[e]; r_x = T_e^T ghat_e
-__global__ void gamma_rhs_kernel(const EntDev *__restrict__ ents, const SlotDev *__restrict__ slots,
-                                 const SubDev *__restrict__ subs, const int64_t *__restrict__ gam_free,
-                                 const double *__restrict__ rhs, const double *__restrict__ zG,
-                                 const double *__restrict__ T, int64_t NDelta, double *gtmp, double *r) {
+// per entity: r_x = T_e^T ghat_e, ghat_e = b_e + sum_m zG^(m)[e] (entity-major, gathered before)
+__global__ void gamma_rhs_kernel(const EntDev *__restrict__ ents, const double *__restrict__ T,
+                                 const double *__restrict__ ghat, int64_t NDelta, double *r) {
   const EntDev E = ents[blockIdx.x];
   const int n = E.n;
-  double *gh = gtmp + E.off_gam;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    double v = rhs[gam_free[E.off_gam + j]];
-    for (int q = 0; q < E.nsides; ++q) {
-      const SlotDev s = slots[E.side_begin + q];
-      v += zG[subs[s.sub].off_G + s.offG + j];
-    }
-    gh[j] = v;
-  }
-  __syncthreads();
+  const double *gh = ghat + E.off_gam;
   const double *Te = T + E.off_T;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int i = warp; i < n; i += nw) {
@@ -488,7 +485,7 @@ __global__ void gamma_rhs_kernel(const EntDev *__restrict__ ents, const SlotDev 
     v = warp_sum(v);
     if (lane == 0) {
       if (i < E.nd) r[E.off_xd + i] = v;
-      else r[NDelta + E.off_pi + (i - E.nd)] = v;
+      else r[NDelta + E.off_pl + (i - E.nd)] = v;
     }
   }
 }
@@ -503,7 +500,7 @@ __global__ void gamma_back_kernel(const EntDev *__restrict__ ents, const int64_t
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     double v = 0.0;
     for (int i = 0; i < n; ++i) {
-      const double xi = i < E.nd ? x[E.off_xd + i] : x[NDelta + E.off_pi + (i - E.nd)];
+      const double xi = i < E.nd ? x[E.off_xd + i] : x[NDelta + E.off_pl + (i - E.nd)];
       v += Te[j + (int64_t)i * n] * xi;
     }
     gam[E.off_gam + j] = v;
@@ -512,14 +509,14 @@ __global__ void gamma_back_kernel(const EntDev *__restrict__ ents, const int64_t
 }
 
 // global zero-mean pressure (Q_{h,0}): p -= c_K * (sum_K vol_K p_K0) / vol_Omega
-__global__ void pressure_mean_kernel(const double *__restrict__ cellgeo, int geo_stride, int np, int64_t nK,
-                                     double *p, int phase, double *acc) {
+__global__ void pressure_mean_kernel(const double *__restrict__ cellgeo, const int64_t *__restrict__ gid,
+                                     int geo_stride, int np, int64_t nK, double *p, int phase, double *acc) {
   if (phase == 0) {
     __shared__ double red[2][32];
     double a = 0.0, w = 0.0;
     for (int64_t K = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; K < nK; K += (int64_t)gridDim.x * blockDim.x) {
       const double vol = cellgeo[K * geo_stride];
-      a += vol * p[K * np];
+      a += vol * p[gid[K] * np];
       w += vol;
     }
     a = warp_sum(a); w = warp_sum(w);
@@ -530,12 +527,16 @@ __global__ void pressure_mean_kernel(const double *__restrict__ cellgeo, int geo
       for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { A += red[0][q]; Wt += red[1][q]; }
       acc[2 * blockIdx.x] = A; acc[2 * blockIdx.x + 1] = Wt;
     }
+  } else if (phase == 1) {   // fold the block partials: acc[200], acc[201]
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      double A = 0, Wt = 0;
+      for (int b = 0; b < 64; ++b) { A += acc[2 * b]; Wt += acc[2 * b + 1]; }
+      acc[200] = A; acc[201] = Wt;
+    }
   } else {
-    double A = 0, Wt = 0;
-    for (int b = 0; b < phase; ++b) { A += acc[2 * b]; Wt += acc[2 * b + 1]; }
-    const double mean = A / Wt;
+    const double mean = acc[200] / acc[201];
     for (int64_t K = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; K < nK; K += (int64_t)gridDim.x * blockDim.x)
-      for (int a = 0; a < np; ++a) p[K * np + a] -= mean * cellgeo[K * geo_stride + 5 + a];
+      for (int a = 0; a < np; ++a) p[gid[K] * np + a] -= mean * cellgeo[K * geo_stride + 5 + a];
   }
 }
 
@@ -543,8 +544,8 @@ __global__ void pressure_mean_kernel(const double *__restrict__ cellgeo, int geo
 // y_K = [A_K B_K^T; B_K 0] x_K per element, then a deterministic per-DOF gather-sum.
 __global__ void elem_apply_kernel(const double *__restrict__ elA, const double *__restrict__ elB,
                                   const int64_t *__restrict__ l2g, const int64_t *__restrict__ vel2free,
-                                  const int *__restrict__ cell_nv, int nvmax, int np, int64_t nK, int64_t nvf,
-                                  const double *__restrict__ x, double *yel) {
+                                  const int *__restrict__ cell_nv, const int64_t *__restrict__ gid, int nvmax,
+                                  int np, int64_t nK, int64_t nvf, const double *__restrict__ x, double *yel) {
   const int64_t K = blockIdx.x;
   if (K >= nK) return;
   extern __shared__ double xs[];
@@ -554,7 +555,7 @@ __global__ void elem_apply_kernel(const double *__restrict__ elA, const double *
     const int64_t f = vel2free[l2g[K * nvmax + j]];
     xs[j] = f >= 0 ? x[f] : 0.0;
   }
-  for (int a = threadIdx.x; a < np; a += blockDim.x) xs[nvmax + a] = x[nvf + K * np + a];
+  for (int a = threadIdx.x; a < np; a += blockDim.x) xs[nvmax + a] = x[nvf + gid[K] * np + a];
   __syncthreads();
   const double *A = elA + K * nvmax * nvmax;
   const double *B = elB + K * np * nvmax;
@@ -573,19 +574,20 @@ __global__ void elem_apply_kernel(const double *__restrict__ elA, const double *
   }
 }
 
+// per free DOF: sum of its local cells' contributions (cell order); pressure rows of local cells
 __global__ void elem_gather_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ idx,
-                                   const double *__restrict__ yel, int64_t nvf, int64_t nK, int np, int stride,
-                                   int nvmax, double *y) {
+                                   const int64_t *__restrict__ gid, const double *__restrict__ yel, int64_t nvf,
+                                   int64_t nK, int np, int stride, int nvmax, double *y) {
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nvf + nK * np;
        f += (int64_t)gridDim.x * blockDim.x) {
-    double v = 0.0;
     if (f < nvf) {
+      double v = 0.0;
       for (int64_t q = ptr[f]; q < ptr[f + 1]; ++q) v += yel[idx[q]];
+      y[f] = v;
     } else {
       const int64_t pidx = f - nvf, K = pidx / np, a = pidx % np;
-      v = yel[K * stride + nvmax + a];
+      y[nvf + gid[K] * np + a] = yel[K * stride + nvmax + a];
     }
-    y[f] = v;
   }
 }
 
@@ -614,18 +616,26 @@ __global__ void __launch_bounds__(256) sum_chunks_kernel(const double *__restric
   }
 }
 
-// z_Pi = u_Pi, z_p0 = p0 (copy of the coarse solution into the tail of z)
-__global__ void coarse_to_z_kernel(const double *uc, int64_t n, double *z) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) z[i] = uc[i];
-}
-
 struct SolveState {
   DBuf<GemvWork> w_op, w_loc, w_c;
   DBuf<GemvWork> w_kd;
   int nw_op = 0, nw_loc = 0, nw_c = 0, nw_kd = 0, max_nd = 1;
+  bool big_c = false;                // coarse vectors exceed shared memory: BIG GEMV variant
   size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_rx = 0, sm_ex = 0, sm_kd = 0;
-  DBuf<int64_t> xptr, xidx, pptr, pidx, eptr, eidx;
-  DBuf<double> hist;
+  DBuf<int64_t> xptr, xidx;          // B2: x coordinate <- copies (local s or received), sharer order
+  DBuf<int64_t> pptr, pidx;          // B6: global coarse index <- coarse pieces, fixed order
+  DBuf<int64_t> cpack, zmap;         // coarse piece packing (r0, owned r_Pi); z tail <- u_c
+  DBuf<int64_t> toff;                // per slot: offset of its extension product
+  DBuf<double> hist, mask, gvol;
+  DBuf<double> sx;                   // [s (len_G) | received copies]
+  DBuf<double> tx;                   // [slot products | received]
+  DBuf<double> cbuf, cgath;          // coarse pieces (local), gathered (nranks x cmax)
+  DBuf<double> gam2, gbuf, hbuf;     // B0: entity-major b_e; [zG | received]; DOF halo receive
+  int64_t cmax = 0, len_t = 0;
+  SlotExchange XS, XE, XB, XH, XR;   // apply_S copies, extension products, B0 zG, DOF halo, rank partials
+  EntitySum ESE, ESB, ESR;
+  DBuf<int64_t> gh_dst;              // DOF halo: destination free ids of received owner values
+  int64_t n_gh = 0;
   bool ready = false;
   // optional per-kernel timing (VB_KERNEL_TIMING=1): event pairs per launch category
   std::vector<cudaEvent_t> ev;
@@ -681,9 +691,17 @@ const char *kernel_time_name(int i) { return (i >= 0 && i < N_CAT) ? kCatNames[i
 
 constexpr int DOT_BLOCKS = 296;
 
+static SolveState *get_state(vb_ctx *c) {
+  if (!c->solve_state) c->solve_state = new SolveState();
+  return (SolveState *)c->solve_state;
+}
+
+// C3: block partials -> rank partial -> fixed-order sum over ranks
 static void dot(vb_ctx *c, const double *a, const double *b, int64_t n, double *dst) {
-  dot_partial_kernel<<<DOT_BLOCKS, 256, 0, c->stream>>>(a, b, n, c->w_dots.p);
+  SolveState *st = get_state(c);
+  dot_partial_kernel<<<DOT_BLOCKS, 256, 0, c->stream>>>(a, b, c->nranks > 1 ? st->mask.p : nullptr, n, c->w_dots.p);
   dot_final_kernel<<<1, 32, 0, c->stream>>>(c->w_dots.p, DOT_BLOCKS, dst);
+  allreduce_sum_fixed(c, dst, 1);
 }
 
 static int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 8); }
@@ -694,46 +712,76 @@ static void apply_S(vb_ctx *c, SolveState *st) {   // q = S^ p  (B1, B2)
   tick(c, st, 0, true);
   sym_gemv_kernel<GV_WARPS><<<st->nw_op, GV_WARPS * 32, st->sm_op, s>>>(st->w_op.p);
   tick(c, st, 0, false);
-  b0_apply_kernel<<<c->N, 32, 0, s>>>(c->d_sub.p, c->d_loc2x.p, c->d_b0T.p, c->w_p.p,
-                                      c->n_delta_glob + c->NPi, c->w_part.p, c->w_q.p);
+  int maxnG = 1;
+  for (auto &S : c->h_sub) maxnG = std::max(maxnG, S.nG);
+  chunk_sum_b0_kernel<<<dim3((maxnG + 255) / 256, c->N), 256, 0, s>>>(c->d_sub.p, c->w_part.p, c->len_G, c->P_op,
+                                                                     c->d_b0T.p, c->d_loc2x.p, c->w_p.p,
+                                                                     c->n_delta_glob + c->NPi, st->sx.p, c->w_q.p);
+  run_slot_exchange(c, st->XS, st->sx.p, st->sx.p + c->len_G);      // C1 (cross-rank copies)
   int64_t nxp = c->n_delta_glob + c->NPi;
-  gather_sum_kernel<<<grid_for(nxp), 256, 0, s>>>(st->xptr.p, st->xidx.p, c->w_part.p, c->len_G, c->P_op, nxp, c->w_q.p);
+  gather_src_kernel<<<grid_for(nxp), 256, 0, s>>>(st->xptr.p, st->xidx.p, st->sx.p, nxp, c->w_q.p);
   tick(c, st, 3, false);
   VB_STAGE();
 }
 
+// debugging aid (VB_PCG_TRACE=2): squared norm of a vector, summed over ranks unless replicated
+static void trace_norm(vb_ctx *c, const char *name, const double *v, int64_t n, bool replicated) {
+  static const bool on = getenv("VB_PCG_TRACE") && atoi(getenv("VB_PCG_TRACE")) >= 2;
+  if (!on) return;
+  double *d = c->w_dots.p + DOT_BLOCKS + 16;
+  dot_partial_kernel<<<DOT_BLOCKS, 256, 0, c->stream>>>(v, v, nullptr, n, c->w_dots.p);
+  dot_final_kernel<<<1, 32, 0, c->stream>>>(c->w_dots.p, DOT_BLOCKS, d);
+  if (!replicated) allreduce_sum_fixed(c, d, 1);
+  double h;
+  VB_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c->stream));
+  VB_CUDA(cudaStreamSynchronize(c->stream));
+  fprintf(stderr, "[vb rank %d] %s %.17g\n", c->rank, name, h);
+}
+
 static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   cudaStream_t s = c->stream;
-  const int nslot = c->h_slot.size(), nent = c->h_ent.size();
   tick(c, st, 4, true);
   if (c->n_act_slots)
     restrict_kernel<<<c->n_act_slots, DLX_WARPS * 32, st->sm_rx, s>>>(c->d_slot.p, c->d_act_slots.p, c->d_ent.p,
                                                                      c->d_sub.p, c->d_Dt.p, c->w_r.p, c->w_locD.p);
+  trace_norm(c, "rD", c->w_locD.p, c->len_Dv, false);
   tick(c, st, 1, true);
   if (st->nw_loc) sym_gemv_kernel<GV_WARPS><<<st->nw_loc, GV_WARPS * 32, st->sm_loc, s>>>(st->w_loc.p);
   tick(c, st, 1, false);
-  phit_kernel<<<dim3(PHIT_SPLIT, c->N), 256, 0, s>>>(c->d_sub.p, c->d_Phi.p, c->w_locD.p, c->w_locC.p);
-  coarse_rhs_kernel<<<grid_for(c->Nc), 256, 0, s>>>(st->pptr.p, st->pidx.p, c->w_locC.p, c->w_r.p,
-                                                    c->n_delta_glob, c->NPi, c->N, c->w_rc.p);
-  coarse_p0_project_kernel<<<1, 256, 0, s>>>(c->d_sub.p, c->N, c->w_rc.p + c->NPi, 0);
+  // coarse pieces (C2): [Phi_i^T rD_i per local subdomain | r0_i | r_Pi of the owned entities]
+  phit_kernel<<<dim3(PHIT_SPLIT, c->N), 256, 0, s>>>(c->d_sub.p, c->d_Phi.p, c->w_locD.p, st->cbuf.p);
+  dev_gather(c->w_r.p, st->cpack.p, (int64_t)st->cpack.n, st->cbuf.p + c->len_Pi, s);
+  const double *pieces = st->cbuf.p;
+  if (c->nranks > 1) {
+    c->comm->allgather(st->cbuf.p, st->cgath.p, st->cmax, s);
+    pieces = st->cgath.p;
+  }
+  trace_norm(c, "cpart", st->cbuf.p, c->len_Pi, false);
+  gather_src_kernel<<<grid_for(c->Nc), 256, 0, s>>>(st->pptr.p, st->pidx.p, pieces, c->Nc, c->w_rc.p);
+  trace_norm(c, "rc", c->w_rc.p, c->Nc, true);
+  coarse_p0_project_kernel<<<1, 256, 0, s>>>(st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
   tick(c, st, 2, true);
-  sym_gemv_kernel<GV_WARPS_C><<<st->nw_c, GV_WARPS_C * 32, st->sm_c, s>>>(st->w_c.p);
+  if (st->big_c)
+    sym_gemv_kernel<GV_WARPS_C, true><<<st->nw_c, GV_WARPS_C * 32, GV_WARPS_C * 32 * sizeof(double), s>>>(st->w_c.p);
+  else
+    sym_gemv_kernel<GV_WARPS_C><<<st->nw_c, GV_WARPS_C * 32, st->sm_c, s>>>(st->w_c.p);
   tick(c, st, 2, false);
   sum_chunks_kernel<<<(c->Nc + 31) / 32, 256, 0, s>>>(c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
-  coarse_p0_project_kernel<<<1, 256, 0, s>>>(c->d_sub.p, c->N, c->w_uc.p + c->NPi, 1);
+  coarse_p0_project_kernel<<<1, 256, 0, s>>>(st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
+  trace_norm(c, "uc", c->w_uc.p, c->Nc, true);
   local2_kernel<<<dim3((st->max_nd + 127) / 128, c->N), 128, c->max_npi * sizeof(double), s>>>(
       c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p);
-  if (c->n_act_ents)
-    extend_kernel<<<c->n_act_ents, DLX_WARPS * 32, st->sm_ex, s>>>(c->d_ent.p, c->d_act_ents.p, c->d_slot.p, c->d_sub.p,
-                                                                   c->d_Dt.p, c->w_locD.p, c->w_z.p);
-  coarse_to_z_kernel<<<grid_for(c->Nc), 256, 0, s>>>(c->w_uc.p, c->Nc, c->w_z.p + c->n_delta_glob);
+  trace_norm(c, "w", c->w_locD.p, c->len_Dv, false);
+  if (c->n_act_slots)
+    slot_extend_kernel<<<c->n_act_slots, DLX_WARPS * 32, st->sm_ex, s>>>(c->d_slot.p, c->d_act_slots.p, c->d_sub.p,
+                                                                        c->d_Dt.p, st->toff.p, c->w_locD.p, st->tx.p);
+  run_slot_exchange(c, st->XE, st->tx.p, st->tx.p + st->len_t);    // C1 (cross-rank products)
+  trace_norm(c, "t", st->tx.p, st->len_t, false);
+  run_entity_sum(c, st->ESE, st->tx.p, c->w_z.p);
+  trace_norm(c, "zdual", c->w_z.p, c->n_delta_glob, false);
+  dev_gather(c->w_uc.p, st->zmap.p, c->NPi + c->N, c->w_z.p + c->n_delta_glob, s);
   tick(c, st, 4, false);
   VB_STAGE();
-}
-
-static SolveState *get_state(vb_ctx *c) {
-  if (!c->solve_state) c->solve_state = new SolveState();
-  return (SolveState *)c->solve_state;
 }
 
 void destroy_solve_state(vb_ctx *c) {
@@ -743,11 +791,11 @@ void destroy_solve_state(vb_ctx *c) {
 
 static void build_csr(int64_t nrows, const std::vector<std::pair<int64_t, int64_t>> &pairs, DBuf<int64_t> &ptr,
                       DBuf<int64_t> &idx, cudaStream_t s) {
-  std::vector<int64_t> p(nrows + 1, 0), ix(pairs.size());
+  std::vector<int64_t> p(nrows + 1, 0), ix(std::max<size_t>(pairs.size(), 1));
   for (auto &q : pairs) p[q.first + 1]++;
   for (int64_t i = 0; i < nrows; ++i) p[i + 1] += p[i];
   std::vector<int64_t> fill(p.begin(), p.end() - 1);
-  for (auto &q : pairs) ix[fill[q.first]++] = q.second;   // pairs are pre-sorted by (row, sub)
+  for (auto &q : pairs) ix[fill[q.first]++] = q.second;   // pairs arrive in the required order per row
   ptr.upload(p, s);
   idx.upload(ix, s);
 }
@@ -762,10 +810,9 @@ void prepare_solve(vb_ctx *c) {
   c->w_part.alloc((int64_t)c->P_op * std::max<int64_t>(c->len_G, 1));
   c->w_locD.alloc(std::max<int64_t>(c->len_Dv, 1));
   c->w_locY.alloc((int64_t)c->P_loc * std::max<int64_t>(c->len_Dv, 1));
-  c->w_locC.alloc(std::max<int64_t>(c->len_Pi, 1));
   c->w_uc.alloc(c->Nc); c->w_rc.alloc(c->Nc);
   c->w_scal.alloc(16); c->w_scal.zero(s);
-  c->w_dots.alloc(DOT_BLOCKS * 2);
+  c->w_dots.alloc(DOT_BLOCKS * 2 + 256);
   c->w_gam.alloc(std::max<int64_t>(c->nGamma, 1));
   c->w_bD.alloc(std::max<int64_t>(c->len_Dn, 1));
   c->w_zG.alloc(std::max<int64_t>(c->len_G, 1));
@@ -803,38 +850,193 @@ void prepare_solve(vb_ctx *c) {
   for (int q = 0; q < Pc; ++q)
     wl.push_back(GemvWork{c->d_Kcp.p, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, rows[q].first, rows[q].second, 0});
   st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = gemv_smem(c->Nc, GV_WARPS_C);
+  st->big_c = st->sm_c > 200 * 1024;
   size_t smmax = std::max(st->sm_op, st->sm_loc);
-  VB_REQUIRE(smmax <= 227 * 1024 && st->sm_c <= 227 * 1024, VB_EINVAL,
-             "packed GEMV vector exceeds shared memory (coarse too large)");
+  VB_REQUIRE(smmax <= 227 * 1024, VB_EINVAL, "packed GEMV vector exceeds shared memory (subdomain interface too large)");
   VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smmax));
-  VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS_C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_c));
-  // deluxe restriction / extension shared memory (vectors + per-warp partials)
-  int maxnd_e = 1, maxs = 1;
+  if (!st->big_c)
+    VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS_C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_c));
+  // deluxe restriction / extension shared memory (vector + per-warp partials)
+  int maxnd_e = 1;
   for (auto &E : c->h_ent)
-    if (E.nd) { maxnd_e = std::max(maxnd_e, E.nd); maxs = std::max(maxs, E.nsides); }
+    if (E.nd) maxnd_e = std::max(maxnd_e, E.nd);
   const int npad = (maxnd_e + 31) / 32 * 32;
   st->sm_rx = (size_t)(1 + DLX_WARPS) * npad * sizeof(double);
-  st->sm_ex = (size_t)(maxs + DLX_WARPS) * npad * sizeof(double);
+  st->sm_ex = st->sm_rx;
   VB_REQUIRE(st->sm_ex <= 227 * 1024, VB_EINVAL, "deluxe entity too large for the extension kernel");
   VB_CUDA(cudaFuncSetAttribute(restrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_rx));
-  VB_CUDA(cudaFuncSetAttribute(extend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_ex));
+  VB_CUDA(cudaFuncSetAttribute(slot_extend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_ex));
   st->max_nd = nmaxD;
-  // x coordinate -> local copies (ordered by subdomain), primal -> local Pi copies
-  std::vector<int64_t> loc2x;
-  c->d_loc2x.download(loc2x, s);
-  VB_CUDA(cudaStreamSynchronize(s));
-  std::vector<std::pair<int64_t, int64_t>> pr;
-  pr.reserve(loc2x.size());
-  for (int64_t j = 0; j < (int64_t)loc2x.size(); ++j) pr.push_back({loc2x[j], j});
-  std::sort(pr.begin(), pr.end());
-  build_csr(c->n_delta_glob + c->NPi, pr, st->xptr, st->xidx, s);
-  std::vector<int64_t> pig;
-  c->d_pi_glob.download(pig, s);
-  VB_CUDA(cudaStreamSynchronize(s));
-  pr.clear();
-  for (int64_t j = 0; j < (int64_t)pig.size(); ++j) pr.push_back({pig[j], j});
-  std::sort(pr.begin(), pr.end());
-  build_csr(c->NPi, pr, st->pptr, st->pidx, s);
+  const int ne = c->ents.size();
+  // ---------------- B2 (apply_S): copies of each x coordinate, local and received, in sharer order
+  {
+    auto L = [&](int e) { return (int64_t)c->h_ent[e].n; };
+    auto pos = [&](int sl, std::vector<int64_t> &out) {
+      const SlotDev &q = c->h_slot[sl];
+      const SubDev &S = c->h_sub[q.sub];
+      for (int t = 0; t < q.nd; ++t) out.push_back(S.off_G + q.offD + t);
+      for (int t = 0; t < q.r; ++t) out.push_back(S.off_G + S.nd + q.offPi + t);
+    };
+    build_slot_exchange(c, st->XS, L, pos);
+    st->sx.alloc(std::max<int64_t>(c->len_G + st->XS.recv_len, 1));
+    std::vector<std::pair<int64_t, int64_t>> pr;
+    for (int e = 0; e < ne; ++e) {
+      const Entity &E = c->ents[e];
+      const EntDev &D = c->h_ent[e];
+      int li = 0;
+      for (size_t k = 0; k < E.sharers.size(); ++k) {
+        std::vector<int64_t> src;
+        if (c->sub_lid[E.sharers[k]] >= 0) {
+          pos(D.side_begin + li, src);
+          ++li;
+        } else {
+          const int64_t ro = st->XS.recv_off[st->XS.ent_ptr[e] + k];
+          for (int t = 0; t < D.n; ++t) src.push_back(c->len_G + ro + t);
+        }
+        for (int t = 0; t < D.nd; ++t) pr.push_back({D.off_xd + t, src[t]});
+        for (int t = 0; t < D.r; ++t) pr.push_back({c->n_delta_glob + D.off_pl + t, src[D.nd + t]});
+      }
+    }
+    std::stable_sort(pr.begin(), pr.end(), [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) {
+      return a.first < b.first;
+    });
+    build_csr(c->n_delta_glob + c->NPi, pr, st->xptr, st->xidx, s);
+  }
+  // ---------------- B7 (extension): per-slot products and their sums over all sharers
+  {
+    std::vector<int64_t> toff(c->h_slot.size(), 0);
+    int64_t o = 0;
+    for (size_t q = 0; q < c->h_slot.size(); ++q) { toff[q] = o; o += c->h_slot[q].nd; }
+    st->len_t = o;
+    st->toff.upload(toff, s);
+    auto L = [&](int e) { return (int64_t)c->h_ent[e].nd; };
+    build_slot_exchange(c, st->XE, L, [&](int sl, std::vector<int64_t> &out) {
+      for (int t = 0; t < c->h_slot[sl].nd; ++t) out.push_back(toff[sl] + t);
+    });
+    st->tx.alloc(std::max<int64_t>(st->len_t + st->XE.recv_len, 1));
+    build_entity_sum(c, st->ESE, st->XE, L, [&](int sl) { return toff[sl]; }, st->len_t,
+                     [&](int e) { return c->h_ent[e].off_xd; });
+  }
+  // ---------------- B0: zG copies of each entity DOF, summed over all sharers after b_e
+  {
+    auto L = [&](int e) { return (int64_t)c->h_ent[e].n; };
+    auto sb = [&](int sl) { return c->h_sub[c->h_slot[sl].sub].off_G + c->h_slot[sl].offG; };
+    build_slot_exchange(c, st->XB, L, [&](int sl, std::vector<int64_t> &out) {
+      const int64_t b = sb(sl);
+      for (int t = 0; t < c->h_slot[sl].n; ++t) out.push_back(b + t);
+    });
+    st->gbuf.alloc(std::max<int64_t>(c->len_G + st->XB.recv_len, 1));
+    st->gam2.alloc(std::max<int64_t>(c->nGamma, 1));
+    std::function<int64_t(int)> gb = [&](int e) { return c->h_ent[e].off_gam; };
+    build_entity_sum(c, st->ESB, st->XB, L, sb, c->len_G, gb, &gb);
+  }
+  // ---------------- free-DOF halo (owner -> holders) and rank partial sums (holders -> all)
+  {
+    auto L = [&](int e) { return (int64_t)c->h_ent[e].n; };
+    auto pos = [&](int sl, std::vector<int64_t> &out) {
+      const EntDev &D = c->h_ent[c->h_slot[sl].ent];
+      for (int t = 0; t < D.n; ++t) out.push_back(D.off_gam + t);
+    };
+    build_slot_exchange(c, st->XH, L, pos, XCH_OWNER);
+    build_slot_exchange(c, st->XR, L, pos, XCH_RANK);
+    std::function<int64_t(int)> gb = [&](int e) { return c->h_ent[e].off_gam; };
+    build_entity_sum(c, st->ESR, st->XR, L, [&](int sl) { return c->h_ent[c->h_slot[sl].ent].off_gam; }, c->nGamma,
+                     gb, nullptr, XCH_RANK);
+    // received owner values: destination positions (entity-major) of the ghost entity DOFs
+    // (indexed by receive position: the receive area is peer-major, not entity-major)
+    std::vector<int64_t> dst(st->XH.recv_len, -1);
+    for (int e = 0; e < ne; ++e) {
+      const int64_t ro = st->XH.recv_off.empty() ? -1 : st->XH.recv_off[st->XH.ent_ptr[e]];
+      if (ro < 0) continue;
+      for (int t = 0; t < c->h_ent[e].n; ++t) dst[ro + t] = c->h_ent[e].off_gam + t;
+    }
+    st->n_gh = dst.size();
+    st->hbuf.alloc(std::max<int64_t>(st->XH.recv_len, 1));
+    for (int64_t d : dst) VB_REQUIRE(d >= 0, VB_EINVAL, "internal: halo receive position without destination");
+    if (dst.empty()) dst.push_back(0);
+    st->gh_dst.upload(dst, s);
+  }
+  // ---------------- B6: coarse pieces, their global layout and the coarse rhs sources
+  {
+    const int R = c->nranks, me = c->rank;
+    std::vector<int> gnpi(c->Ng, 0);
+    for (int g = 0; g < c->Ng; ++g)
+      for (int e : c->gsub_ents[g]) gnpi[g] += c->gents[e].r;
+    // per rank: [cpart of its subdomains (in order) | r0 of its subdomains | r_Pi of its owned entities]
+    std::vector<int64_t> lenPi(R, 0), nsub(R, 0), nown(R, 0), sub_cpos(c->Ng, 0), sub_r0(c->Ng, 0);
+    for (int g = 0; g < c->Ng; ++g) {
+      const int r = c->sub_rank[g];
+      sub_cpos[g] = lenPi[r];
+      lenPi[r] += gnpi[g];
+      sub_r0[g] = nsub[r]++;
+    }
+    std::vector<int64_t> ent_own(c->gents.size(), 0);
+    for (size_t e = 0; e < c->gents.size(); ++e) {
+      const int r = c->sub_rank[c->gents[e].sharers[0]];
+      ent_own[e] = nown[r];
+      nown[r] += c->gents[e].r;
+    }
+    int64_t cmax = 1;
+    for (int r = 0; r < R; ++r) cmax = std::max(cmax, lenPi[r] + nsub[r] + nown[r]);
+    st->cmax = cmax;
+    VB_REQUIRE(lenPi[me] == c->len_Pi, VB_EINVAL, "internal: coarse piece layout mismatch");
+    st->cbuf.alloc(cmax);
+    st->cbuf.zero(s);
+    if (R > 1) st->cgath.alloc((size_t)cmax * R);
+    auto base = [&](int r) { return (int64_t)r * (R > 1 ? cmax : 0); };
+    // local packing: r0 of local subs, then r_Pi of owned local entities
+    std::vector<int64_t> cpack;
+    for (int i = 0; i < N; ++i) cpack.push_back(c->n_delta_glob + c->NPi + i);
+    for (int e = 0; e < ne; ++e) {
+      const Entity &E = c->ents[e];
+      if (c->sub_rank[E.sharers[0]] != me) continue;
+      for (int t = 0; t < E.r; ++t) cpack.push_back(c->n_delta_glob + E.off_pl + t);
+    }
+    st->cpack.upload(cpack, s);
+    // sources of every global coarse index: owner's r_Pi, then each sharer's Phi^T r piece
+    std::vector<std::pair<int64_t, int64_t>> pr;
+    for (size_t e = 0; e < c->gents.size(); ++e) {
+      const GEnt &G = c->gents[e];
+      const int ro = c->sub_rank[G.sharers[0]];
+      for (int t = 0; t < G.r; ++t) pr.push_back({G.off_pi + t, base(ro) + lenPi[ro] + nsub[ro] + ent_own[e] + t});
+      for (int m : G.sharers) {
+        const int rm = c->sub_rank[m];
+        int64_t within = 0;   // position of e in m's primal layout (entities in id order)
+        for (int e2 : c->gsub_ents[m]) { if (e2 == (int)e) break; within += c->gents[e2].r; }
+        for (int t = 0; t < G.r; ++t) pr.push_back({G.off_pi + t, base(rm) + sub_cpos[m] + within + t});
+      }
+    }
+    for (int g = 0; g < c->Ng; ++g) {
+      const int r = c->sub_rank[g];
+      pr.push_back({c->NPi_g + g, base(r) + lenPi[r] + sub_r0[g]});
+    }
+    std::stable_sort(pr.begin(), pr.end(), [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) {
+      return a.first < b.first;
+    });
+    build_csr(c->Nc, pr, st->pptr, st->pidx, s);
+    // z tail <- u_c: local primal coordinates, then the local p0
+    std::vector<int64_t> zm(c->NPi + N, 0);
+    for (int e = 0; e < ne; ++e)
+      for (int t = 0; t < c->h_ent[e].r; ++t) zm[c->h_ent[e].off_pl + t] = c->h_ent[e].off_pi + t;
+    for (int i = 0; i < N; ++i) zm[c->NPi + i] = c->NPi_g + c->sub_gid[i];
+    st->zmap.upload(zm, s);
+    st->gvol.upload(c->gsub_vol, s);
+  }
+  // ---------------- C3 mask: coordinates owned by this rank (entities whose lowest sharer is here)
+  if (c->nranks > 1) {
+    std::vector<double> mk(nx, 0.0);
+    for (int e = 0; e < ne; ++e) {
+      if (c->sub_rank[c->ents[e].sharers[0]] != c->rank) continue;
+      const EntDev &D = c->h_ent[e];
+      for (int t = 0; t < D.nd; ++t) mk[D.off_xd + t] = 1.0;
+      for (int t = 0; t < D.r; ++t) mk[c->n_delta_glob + D.off_pl + t] = 1.0;
+    }
+    for (int i = 0; i < N; ++i) mk[c->n_delta_glob + c->NPi + i] = 1.0;
+    st->mask.upload(mk, s);
+    const int64_t nfg = c->n_free_vel + c->npres;
+    c->w_rhsg.alloc(nfg);
+    c->w_xg.alloc(nfg);
+  }
   // B0/B8: packed K_DD^-1 GEMV work list (y_D = K_DD^-1 b_D) and buffers
   c->w_yDp.alloc((int64_t)c->P_kd * std::max<int64_t>(c->len_Dn, 1));
   c->w_xD.alloc(std::max<int64_t>(c->len_Dn, 1));
@@ -871,20 +1073,64 @@ void prepare_solve(vb_ctx *c) {
   c->bytes_per_iter = b;
 }
 
+// owner values of the ghost interface DOFs (global free layout vector v, entity DOFs)
+static void dof_halo(vb_ctx *c, SolveState *st, double *v) {
+  if (c->nranks == 1) return;
+  cudaStream_t s = c->stream;
+  dev_gather(v, c->d_gam_free.p, c->nGamma, c->w_gam.p, s);
+  run_slot_exchange(c, st->XH, c->w_gam.p, st->hbuf.p);
+  if (st->n_gh) {
+    // w_gam[dst[k]] = received[k], then back to the free layout
+    dev_scatter(st->hbuf.p, st->gh_dst.p, st->n_gh, c->w_gam.p, s);
+    dev_scatter(c->w_gam.p, c->d_gam_free.p, c->nGamma, v, s);
+  }
+}
+
+// interface DOF sums across ranks of per-rank partial sums (global free layout vector v)
+static void dof_rank_sum(vb_ctx *c, SolveState *st, double *v) {
+  if (c->nranks == 1) return;
+  cudaStream_t s = c->stream;
+  dev_gather(v, c->d_gam_free.p, c->nGamma, c->w_gam.p, s);
+  DBuf<double> comb;
+  comb.alloc(std::max<int64_t>(c->nGamma + st->XR.recv_len, 1));
+  VB_CUDA(cudaMemcpyAsync(comb.p, c->w_gam.p, c->nGamma * 8, cudaMemcpyDeviceToDevice, s));
+  run_slot_exchange(c, st->XR, comb.p, comb.p + c->nGamma);
+  run_entity_sum(c, st->ESR, comb.p, c->w_gam.p);
+  dev_scatter(c->w_gam.p, c->d_gam_free.p, c->nGamma, v, s);
+  VB_CUDA(cudaStreamSynchronize(s));
+}
+
+// element contributions -> free vector in the ABI layout (owned DOFs; all free DOFs for one rank)
 void element_gather(vb_ctx *c, const double *yel, double *out) {
   const int stride = c->nv_max + c->np;
-  const int64_t nf = c->n_free_vel + c->npres;
-  elem_gather_kernel<<<grid_for(nf), 256, 0, c->stream>>>(c->d_el_ptr.p, c->d_el_ent.p, yel, c->n_free_vel, c->nK,
-                                                          c->np, stride, c->nv_max, out);
+  const int64_t nf = c->n_free_vel + c->nKl * c->np;
+  if (c->nranks > 1)
+    VB_REQUIRE(get_state(c)->ready, VB_ESTATE, "multi-rank assembly needs vb_factor first (exchange plans)");
+  double *dst = c->nranks > 1 ? c->w_rhsg.p : out;
+  elem_gather_kernel<<<grid_for(nf), 256, 0, c->stream>>>(c->d_el_ptr.p, c->d_el_ent.p, c->d_cell_gid.p, yel,
+                                                          c->n_free_vel, c->nKl, c->np, stride, c->nv_max, dst);
   VB_STAGE();
+  if (c->nranks > 1) {
+    dof_rank_sum(c, get_state(c), dst);
+    dev_gather(dst, c->d_owned_free.p, (int64_t)c->owned_free.size(), out, c->stream);
+  }
 }
 
 void apply_operator_device(vb_ctx *c, const double *x, double *y) {
   cudaStream_t s = c->stream;
   const int stride = c->nv_max + c->np;
-  elem_apply_kernel<<<c->nK, 128, stride * sizeof(double), s>>>(c->d_elA.p, c->d_elB.p, c->d_cell_l2g.p,
-                                                                c->d_vel2free.p, c->d_cell_nv.p, c->nv_max, c->np,
-                                                                c->nK, c->n_free_vel, x, c->w_elt.p);
+  const double *xin = x;
+  if (c->nranks > 1) {
+    SolveState *st = get_state(c);
+    VB_REQUIRE(st->ready, VB_ESTATE, "multi-rank operator needs vb_factor first (exchange plans)");
+    dev_scatter(x, c->d_owned_free.p, (int64_t)c->owned_free.size(), c->w_xg.p, s);
+    dof_halo(c, st, c->w_xg.p);
+    xin = c->w_xg.p;
+  }
+  elem_apply_kernel<<<c->nKl, 128, stride * sizeof(double), s>>>(c->d_elA.p, c->d_elB.p, c->d_cell_l2g.p,
+                                                                 c->d_vel2free.p, c->d_cell_nv.p, c->d_cell_gid.p,
+                                                                 c->nv_max, c->np, c->nKl, c->n_free_vel, xin,
+                                                                 c->w_elt.p);
   VB_STAGE();
   element_gather(c, c->w_elt.p, y);
 }
@@ -898,15 +1144,25 @@ static double read_scalar(vb_ctx *c, int i) {
 
 void lanczos_extremes(const std::vector<double> &al, const std::vector<double> &be, double *lmin, double *lmax);
 
-void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit, vb_report *rep) {
+void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int maxit, vb_report *rep) {
   prepare_solve(c);
   SolveState *st = get_state(c);
   cudaStream_t s = c->stream;
   c->timing = getenv("VB_KERNEL_TIMING") && atoi(getenv("VB_KERNEL_TIMING"));
+  const bool trace = getenv("VB_PCG_TRACE") && atoi(getenv("VB_PCG_TRACE"));
   st->nev = 0;
   const int N = c->N;
   const int64_t nx = c->nx, NDelta = c->n_delta_glob;
   const int64_t nvf = c->n_free_vel;
+  // multi-rank: work on global-layout free vectors (owned values + ghost interface values)
+  const double *rhs = rhs_in;
+  double *x = x_out;
+  if (c->nranks > 1) {
+    dev_scatter(rhs_in, c->d_owned_free.p, (int64_t)c->owned_free.size(), c->w_rhsg.p, s);
+    dof_halo(c, st, c->w_rhsg.p);
+    rhs = c->w_rhsg.p;
+    x = c->w_xg.p;
+  }
   // ---------------- B0: condensed rhs in transformed coordinates
   int64_t maxnG = 1, maxnD = 1;
   for (auto &S : c->h_sub) { maxnG = std::max<int64_t>(maxnG, S.nG); maxnD = std::max<int64_t>(maxnD, S.nD); }
@@ -914,10 +1170,12 @@ void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit,
   rhs_D_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p, c->d_mvec.p, rhs, nvf,
                                  c->w_bD.p, c->w_r.p + NDelta + c->NPi);
   sym_gemv_kernel<GV_WARPS><<<st->nw_kd, GV_WARPS * 32, st->sm_kd, s>>>(st->w_kd.p);   // y_D = K_DD^-1 b_D
-  zG_kernel<<<dim3((maxnG + 127) / 128, N), 128, 0, s>>>(c->d_sub.p, c->d_Psi.p, c->w_bD.p, c->w_zG.p);
+  zG_kernel<<<dim3((maxnG + 127) / 128, N), 128, 0, s>>>(c->d_sub.p, c->d_Psi.p, c->w_bD.p, st->gbuf.p);
   VB_STAGE();
-  gamma_rhs_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_slot.p, c->d_sub.p, c->d_gam_free.p, rhs,
-                                                   c->w_zG.p, c->d_T.p, NDelta, c->w_gam.p, c->w_r.p);
+  dev_gather(rhs, c->d_gam_free.p, c->nGamma, st->gam2.p, s);                // b_e (entity-major)
+  run_slot_exchange(c, st->XB, st->gbuf.p, st->gbuf.p + c->len_G);          // C1 (cross-rank zG)
+  run_entity_sum(c, st->ESB, st->gbuf.p, c->w_gam.p, st->gam2.p);             // ghat = b + sum_m zG^(m)
+  gamma_rhs_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_T.p, c->w_gam.p, NDelta, c->w_r.p);
   VB_STAGE();
   // ---------------- PCG (SURVEY O-15)
   c->w_x.zero(s);
@@ -925,6 +1183,7 @@ void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit,
   dot(c, c->w_r.p, c->w_r.p, nx, sc + 2);
   const double rr0 = read_scalar(c, 2);
   const double r0n = sqrt(rr0);
+  if (trace) fprintf(stderr, "[vb rank %d] rr0 %.17g\n", c->rank, rr0);
   apply_M(c, st);
   dot(c, c->w_r.p, c->w_z.p, nx, sc + 0);
   update_p_kernel<<<grid_for(nx), 256, 0, s>>>(c->w_p.p, c->w_z.p, nx, sc, 1);
@@ -944,6 +1203,8 @@ void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit,
     VB_CUDA(cudaMemcpyAsync(h, sc, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
     VB_CUDA(cudaStreamSynchronize(s));
     const double rz = h[0], pq = h[1];
+    if (trace)
+      fprintf(stderr, "[vb rank %d] it %d rz %.17g pq %.17g rr %.17g\n", c->rank, it, rz, pq, h[2]);
     if (!(pq > 0) || !(rz > 0)) { status = VB_EBREAKDOWN; break; }
     alphas.push_back(rz / pq);
     rn = sqrt(h[2]);
@@ -974,9 +1235,15 @@ void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit,
   xout_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->w_xD.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p, c->d_mvec.p,
                                 c->w_x.p + NDelta + c->NPi, nvf, x);
   VB_STAGE();
-  pressure_mean_kernel<<<64, 256, 0, s>>>(c->d_cellgeo.p, c->geo_stride, c->np, c->nK, x + nvf, 0, c->w_dots.p);
-  pressure_mean_kernel<<<grid_for(c->nK), 256, 0, s>>>(c->d_cellgeo.p, c->geo_stride, c->np, c->nK, x + nvf, 64, c->w_dots.p);
+  pressure_mean_kernel<<<64, 256, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np, c->nKl, x + nvf, 0,
+                                          c->w_dots.p);
+  pressure_mean_kernel<<<1, 32, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np, c->nKl, x + nvf, 1,
+                                        c->w_dots.p);
+  allreduce_sum_fixed(c, c->w_dots.p + 200, 2);
+  pressure_mean_kernel<<<grid_for(c->nKl), 256, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np,
+                                                        c->nKl, x + nvf, 2, c->w_dots.p);
   VB_STAGE();
+  if (c->nranks > 1) dev_gather(x, c->d_owned_free.p, (int64_t)c->owned_free.size(), x_out, s);
   VB_CUDA(cudaStreamSynchronize(s));
   collect_times(c, st);
   c->last_iterations = it;
@@ -993,31 +1260,14 @@ void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit,
     rep->lambda_min = lmin; rep->lambda_max = lmax; rep->kappa = lmin > 0 ? lmax / lmin : INFINITY;
     rep->bytes_per_iter_model = c->bytes_per_iter;
     rep->flux_violation_max = c->flux_violation;
-    rep->n_primal = c->NPi; rep->n_coarse = c->Nc;
+    rep->n_primal = c->NPi_g; rep->n_coarse = c->Nc;
     rep->n_dofs_paper = c->nvel + c->npres;
+    rep->n_adaptive = c->n_adaptive;
+    rep->adaptive_margin = c->adaptive_margin;
   }
   if (status != VB_OK)
     throw Error{(vb_status)status, status == VB_ENOTCONV ? "PCG reached maxit without converging"
                                                           : "PCG breakdown: p^T S p <= 0 or r^T z <= 0"};
-}
-
-// original interface coordinates (entity-major) -> transformed x (T_e^T per entity)
-__global__ void to_transformed_kernel(const EntDev *__restrict__ ents, const double *__restrict__ T,
-                                      const double *__restrict__ g, int64_t NDelta, double *x) {
-  const EntDev E = ents[blockIdx.x];
-  const int n = E.n;
-  const double *Te = T + E.off_T;
-  const double *gh = g + E.off_gam;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = warp; i < n; i += nw) {
-    double v = 0.0;
-    for (int j = lane; j < n; j += 32) v += Te[j + (int64_t)i * n] * gh[j];
-    v = warp_sum(v);
-    if (lane == 0) {
-      if (i < E.nd) x[E.off_xd + i] = v;
-      else x[NDelta + E.off_pi + (i - E.nd)] = v;
-    }
-  }
 }
 
 // Debug/parity entry: y = S^ x (which = 0) or y = M^-1 x (which = 1) in ORIGINAL interface
@@ -1033,7 +1283,7 @@ void debug_interface_op(vb_ctx *c, int which, const double *in, double *out) {
   dummy.alloc(c->n_free_vel + 1);
   VB_CUDA(cudaMemcpyAsync(gin.p, in, (ng + N) * 8, cudaMemcpyHostToDevice, s));
   double *dst = which == 0 ? c->w_p.p : c->w_r.p;
-  to_transformed_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_T.p, gin.p, NDelta, dst);
+  gamma_rhs_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_T.p, gin.p, NDelta, dst);
   VB_CUDA(cudaMemcpyAsync(dst + NDelta + c->NPi, gin.p + ng, N * 8, cudaMemcpyDeviceToDevice, s));
   VB_STAGE();
   const double *res;

@@ -45,9 +45,9 @@ void init_quadrature_constants(int k) {
 void cell_geometry_device(vb_ctx *c) {
   init_quadrature_constants(c->k);
   c->geo_stride = 5 + c->np;
-  c->d_cellgeo.alloc(c->nK * c->geo_stride);
-  cell_geometry_kernel<<<(c->nK + 127) / 128, 128, 0, c->stream>>>(c->d_topo.p, c->d_xyz.p, c->nK, c->k, c->np,
-                                                                    c->geo_stride, c->d_cellgeo.p);
+  c->d_cellgeo.alloc(std::max<int64_t>(c->nKl, 1) * c->geo_stride);
+  cell_geometry_kernel<<<(c->nKl + 127) / 128, 128, 0, c->stream>>>(c->d_topo.p, c->d_xyz.p, c->nKl, c->k, c->np,
+                                                                     c->geo_stride, c->d_cellgeo.p);
   VB_CHECK_LAUNCH();
   VB_CUDA(cudaStreamSynchronize(c->stream));
 }
@@ -526,16 +526,16 @@ void element_matrices_device(vb_ctx *c) {
   cudaStream_t s = c->stream;
   const int nvm = c->nv_max;
   const int S3 = 3 * (c->k == 2 ? 10 : 20);
-  c->d_elA.alloc((size_t)c->nK * nvm * nvm);
-  c->d_elB.alloc((size_t)c->nK * c->np * nvm);
-  c->d_P0.alloc((size_t)c->nK * S3 * nvm);
+  c->d_elA.alloc((size_t)c->nKl * nvm * nvm);
+  c->d_elB.alloc((size_t)c->nKl * c->np * nvm);
+  c->d_P0.alloc((size_t)c->nKl * S3 * nvm);
   const int64_t per = c->k == 2 ? Arena<2>(nvm).total : Arena<3>(nvm).total;
-  int64_t NE = std::max<int64_t>(128, std::min<int64_t>(c->nK, (int64_t)(3.0e9 / 8 / per)));
+  int64_t NE = std::max<int64_t>(128, std::min<int64_t>(c->nKl, (int64_t)(3.0e9 / 8 / per)));
   NE = (NE + 127) / 128 * 128;
   DBuf<double> scratch;
   scratch.alloc((size_t)per * NE);
-  for (int64_t K0 = 0; K0 < c->nK; K0 += NE) {
-    const int64_t n = std::min<int64_t>(NE, c->nK - K0);
+  for (int64_t K0 = 0; K0 < c->nKl; K0 += NE) {
+    const int64_t n = std::min<int64_t>(NE, c->nKl - K0);
     const int blocks = (n + 127) / 128;
     if (c->k == 2)
       vem_element_kernel<2><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, K0, n, nvm, scratch.p, NE,
@@ -694,15 +694,15 @@ void build_rhs_device(vb_ctx *c, const vb_problem *p, double *rhs) {
     for (int i = 0; i < P.ns; ++i) for (int q = 0; q < 3; ++q) P.cen[i][q] = p->centres[3 * i + q];
   }
   cudaStream_t s = c->stream;
-  const int blocks = (c->nK + 127) / 128;
+  const int blocks = (c->nKl + 127) / 128;
   if (c->k == 2)
     rhs_element_kernel<2><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, c->d_cell_l2g.p, c->d_vel2free.p,
-                                                 c->d_elA.p, c->d_elB.p, c->d_P0.p, c->nK, c->nv_max, P, c->w_elt.p);
+                                                 c->d_elA.p, c->d_elB.p, c->d_P0.p, c->nKl, c->nv_max, P, c->w_elt.p);
   else
     rhs_element_kernel<3><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, c->d_cell_l2g.p, c->d_vel2free.p,
-                                                 c->d_elA.p, c->d_elB.p, c->d_P0.p, c->nK, c->nv_max, P, c->w_elt.p);
+                                                 c->d_elA.p, c->d_elB.p, c->d_P0.p, c->nKl, c->nv_max, P, c->w_elt.p);
   VB_STAGE();
-  element_gather(c, c->w_elt.p, rhs);
+  element_gather(c, c->w_elt.p, rhs);   // owned layout (multi-rank: interface sums exchanged)
   VB_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -1,0 +1,126 @@
+"""Multi-rank data path on ONE GPU through the loopback transport: R library ranks
+run as R threads of this process, each owning a box of subdomains, exchanging interface sums (C1),
+coarse pieces (C2), dot partials (C3) and local coarse matrices (C4) by host-synchronised device
+copies -- the same exchange plans the NCCL transport runs over NVLink.  Gates: the R-rank solve
+equals the oracle (SURVEY §8(c) parity gates) and the 1-rank solve (decomposition invariance:
+iterations equal, solution to 1e-12)."""
+import concurrent.futures as cf
+
+import numpy as np
+import pytest
+
+from synthetic import make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True):
+    import torch
+    import paper_2304_09770_b200 as vb
+    R = int(np.prod(rank_grid))
+    srank = vb.box_ranks(prob.sub_grid, rank_grid)
+    world = vb.LoopbackWorld(R)
+    streams = [torch.cuda.Stream() for _ in range(R)]
+
+    def rank_main(r):
+        ctx = vb.context_for(prob, stream=streams[r], rank=r, nranks=R, subdomain_rank=srank, world=world)
+        ctx.factor()
+        rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+        x = torch.zeros_like(rhs)
+        torch.cuda.synchronize()
+        ctx.build_rhs(vb.problem_args(prob), rhs)
+        rep = ctx.pcg_solve(rhs, x, rtol=rtol)
+        res = None
+        if check_operator:
+            y = torch.zeros_like(rhs)
+            ctx.apply_operator(x, y)
+            res = (rhs - y).cpu().numpy()
+        out = dict(rep=rep, ids=ctx.dof_layout(), x=x.cpu().numpy(), rhs=rhs.cpu().numpy(), res=res)
+        ctx.close()
+        return out
+
+    with cf.ThreadPoolExecutor(R) as ex:
+        outs = list(ex.map(rank_main, range(R)))
+    world.close()
+    return outs
+
+
+def _assemble(outs, n_total):
+    x = np.full(n_total, np.nan)
+    b = np.full(n_total, np.nan)
+    for o in outs:
+        x[o["ids"]] = o["x"]
+        b[o["ids"]] = o["rhs"]
+    return x, b
+
+
+def _global_free_ids(gs):
+    return np.concatenate([gs.dofs.free_vel, gs.dofs.nvel + np.arange(gs.dofs.npres)])
+
+
+@pytest.mark.parametrize("name,kw,rank_grid", [
+    ("c1", {}, (1, 1, 2)),
+    ("c1", {}, (2, 2, 2)),
+    ("c1", dict(n=8), (1, 2, 2)),
+    ("c4", dict(n=8, constraints=dict(adaptive_tau=0.0)), (2, 1, 1)),
+])
+def test_multirank_matches_oracle_and_single_rank(name, kw, rank_grid):
+    import torch
+    import paper_2304_09770_b200 as vb
+    from oracle.assemble import GlobalSystem
+    from oracle.bddc import BDDC
+    prob = make_problem(name, **kw)
+    gs = GlobalSystem(prob)
+    u_o, p_o, rep_o = BDDC(gs).solve(rtol=1e-10)
+    # single rank reference
+    ctx = vb.context_for(prob)
+    ctx.factor()
+    rhs1 = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+    ctx.build_rhs(vb.problem_args(prob), rhs1)
+    x1 = torch.zeros_like(rhs1)
+    rep1 = ctx.pcg_solve(rhs1, x1, rtol=1e-10)
+    ids1 = ctx.dof_layout()
+    x1 = x1.cpu().numpy()
+    outs = _run_ranks(prob, rank_grid)
+    gid = _global_free_ids(gs)
+    assert np.array_equal(np.sort(np.concatenate([o["ids"] for o in outs])), np.sort(gid))   # a partition
+    pos = {int(g): i for i, g in enumerate(gid)}
+    n = gid.size
+    xR, bR = _assemble([dict(o, ids=np.array([pos[int(g)] for g in o["ids"]])) for o in outs], n)
+    assert np.array_equal(ids1, gid)
+    # the distributed rhs assembly equals the single-rank one
+    assert np.abs(bR - rhs1.cpu().numpy()).max() <= 1e-13 * np.abs(bR).max()
+    for o in outs:
+        assert o["rep"]["iterations"] == rep1["iterations"]
+        # reductions run in a different order than on one rank: kappa to rounding of the Lanczos
+        # coefficients (the sinker case without enrichment has kappa ~ 270)
+        assert abs(o["rep"]["kappa"] - rep1["kappa"]) <= 1e-4 * rep1["kappa"]
+        assert o["rep"]["n_primal"] == rep1["n_primal"]
+    # not bitwise (dot partials are summed per rank): both are rtol-1e-10 solutions
+    assert np.linalg.norm(xR - x1) <= 1e-10 * np.linalg.norm(x1)
+    nv = gs.dofs.n_free_vel
+    assert np.linalg.norm(xR[:nv] - u_o) <= 1e-8 * np.linalg.norm(u_o)
+    assert np.linalg.norm(xR[nv:] - p_o) <= 1e-8 * np.linalg.norm(p_o)
+    assert abs(outs[0]["rep"]["iterations"] - rep_o["iterations"]) <= 1
+    # true residual of the distributed element-by-element operator
+    rR = np.concatenate([o["res"] for o in outs])
+    assert np.linalg.norm(rR) <= 1e-8 * np.linalg.norm(bR)
+
+
+def test_multirank_adaptive():
+    """Adaptive enrichment across a rank boundary: faces shared by two ranks are solved redundantly
+    (bitwise-identical inputs), so the primal space and the iterates match the single-rank run."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    prob = make_problem("c4", n=8)
+    ctx = vb.context_for(prob)
+    ctx.factor()
+    rhs1 = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+    ctx.build_rhs(vb.problem_args(prob), rhs1)
+    x1 = torch.zeros_like(rhs1)
+    rep1 = ctx.pcg_solve(rhs1, x1, rtol=1e-10)
+    outs = _run_ranks(prob, (2, 1, 1), check_operator=False)
+    for o in outs:
+        assert o["rep"]["n_adaptive"] == rep1["n_adaptive"]
+        assert o["rep"]["n_primal"] == rep1["n_primal"]
+        assert o["rep"]["iterations"] == rep1["iterations"]
