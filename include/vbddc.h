@@ -98,6 +98,15 @@ vb_status vb_nccl_unique_id(void *out128);
 vb_status vb_loopback_world_create(int32_t nranks, void **world);
 vb_status vb_loopback_world_destroy(void *world);
 
+/* Host-only planning, no GPU needed (tests of the multi-rank bookkeeping): for one double per
+ * interface DOF per sending sharer, the doubles this rank would send to (send_counts[p]) and
+ * receive from (recv_counts[p]) every rank p under exchange `mode` (0: every sharer sends,
+ * 1: only the entity's lowest sharer, 2: the lowest sharer on each rank), and the number of free
+ * DOFs this rank owns in the vb_dof_layout sense.  Arrays have nranks entries. */
+vb_status vb_plan_exchange(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
+                           const int32_t *subdomain_rank, int32_t rank, int32_t nranks, int32_t mode,
+                           int64_t *send_counts, int64_t *recv_counts, int64_t *n_owned_free);
+
 /* Build the context: topology, DOF numbering, box-free general subdomain
  * classification, interface entities, and the VEM element matrices A^K, B^K computed
  * on the device from the geometry and the per-cell viscosity.

@@ -97,7 +97,7 @@ _vb_nccl_unique_id = _sig("vb_nccl_unique_id", ctypes.c_int, [_p])
 _vb_debug_iop = _sig("vb_debug_interface_op", ctypes.c_int, [_p, ctypes.c_int32, _dp, _dp])
 _vb_interface_dofs = _sig("vb_interface_dofs", ctypes.c_int, [_p, _i64p, _i64p])
 
-EXPORTED = ["vb_nccl_unique_id", "vb_loopback_world_create", "vb_loopback_world_destroy", "vb_setup", "vb_setup_from_elements", "vb_factor", "vb_build_rhs",
+EXPORTED = ["vb_plan_exchange", "vb_nccl_unique_id", "vb_loopback_world_create", "vb_loopback_world_destroy", "vb_setup", "vb_setup_from_elements", "vb_factor", "vb_build_rhs",
             "vb_pcg_solve", "vb_pcg_solve_host", "vb_apply_operator", "vb_debug_interface_op",
             "vb_interface_dofs", "vb_num_free_dofs", "vb_dof_layout",
             "vb_cell_local_dofs", "vb_get_element_matrices", "vb_stats", "vb_kernel_times",
@@ -322,6 +322,39 @@ def box_ranks(sub_grid, rank_grid):
             for i in range(sx):
                 out[i + sx * (j + sy * k)] = (i // (sx // rx)) + rx * ((j // (sy // ry)) + ry * (k // (sz // rz)))
     return out
+
+
+_vb_plan = _sig("vb_plan_exchange", ctypes.c_int, [ctypes.POINTER(VBMesh), _i32p, ctypes.c_int32, _i32p,
+                                                    ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _i64p, _i64p,
+                                                    _i64p])
+
+
+def plan_exchange(mesh, k, cell_subdomain, subdomain_rank, rank, nranks, mode=0):
+    """Host-only (no GPU): (send_counts[nranks], recv_counts[nranks], n_owned_free) of this rank's
+    interface exchange plan (vb_plan_exchange)."""
+    keep = []
+    m = _mesh_struct(mesh, k, keep)
+    sub = _arr(cell_subdomain, np.int32)
+    sr = _arr(subdomain_rank, np.int32)
+    snd = np.zeros(nranks, np.int64); rcv = np.zeros(nranks, np.int64)
+    own = ctypes.c_int64()
+    st = _vb_plan(ctypes.byref(m), _ptr(sub, ctypes.c_int32), int(sub.max()) + 1, _ptr(sr, ctypes.c_int32), int(rank),
+                  int(nranks), int(mode), _ptr(snd, ctypes.c_int64), _ptr(rcv, ctypes.c_int64), ctypes.byref(own))
+    if st != VB_OK:
+        raise VBError(st, _vb_last_error(None).decode())
+    return snd, rcv, own.value
+
+
+def _mesh_struct(mesh, k, keep):
+    xyz = _arr(mesh.xyz, np.float64)
+    fp, fv = _arr(mesh.face_ptr, np.int64), _arr(mesh.face_vtx, np.int64)
+    cp, cf = _arr(mesh.cell_ptr, np.int64), _arr(mesh.cell_face, np.int64)
+    cs = _arr(mesh.cell_face_sign, np.int8)
+    fb = _arr(mesh.face_on_boundary, np.uint8)
+    keep += [xyz, fp, fv, cp, cf, cs, fb]
+    return VBMesh(int(k), xyz.shape[0], _ptr(xyz, ctypes.c_double), fp.size - 1, _ptr(fp, ctypes.c_int64),
+                  _ptr(fv, ctypes.c_int64), cp.size - 1, _ptr(cp, ctypes.c_int64), _ptr(cf, ctypes.c_int64),
+                  _ptr(cs, ctypes.c_int8), _ptr(fb, ctypes.c_uint8))
 
 
 def problem_args(prob):

@@ -4,6 +4,7 @@
 #include <cstring>
 #include <map>
 #include "setup.h"
+#include "exchange.h"
 
 using namespace vb;
 
@@ -313,6 +314,33 @@ vb_status vb_loopback_world_create(int32_t nranks, void **world) {
 vb_status vb_loopback_world_destroy(void *world) {
   if (!world) return VB_EINVAL;
   vb::loopback_world_destroy(world);
+  return VB_OK;
+}
+
+vb_status vb_plan_exchange(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
+                           const int32_t *subdomain_rank, int32_t rank, int32_t nranks, int32_t mode,
+                           int64_t *send_counts, int64_t *recv_counts, int64_t *n_owned_free) {
+  if (!mesh || !cell_subdomain || !send_counts || !recv_counts || !n_owned_free || nranks < 1 || rank < 0 ||
+      rank >= nranks || mode < XCH_ALL || mode > XCH_RANK || (nranks > 1 && !subdomain_rank))
+    return VB_EINVAL;
+  vb_ctx c;   // host bookkeeping only: no device work
+  try {
+    VB_REQUIRE(mesh->k == 2 || mesh->k == 3, VB_EINVAL, "k must be 2 or 3");
+    c.k = mesh->k;
+    c.rank = rank;
+    c.nranks = nranks;
+    build_topology(&c, mesh);
+    build_subdomains(&c, cell_subdomain, n_subdomains, nranks > 1 ? subdomain_rank : nullptr);
+    std::vector<int64_t> snd, rcv;
+    plan_slot_counts(&c, [&](int e) { return (int64_t)c.ents[e].n; }, mode, snd, rcv);
+    for (int p = 0; p < nranks; ++p) { send_counts[p] = snd[p]; recv_counts[p] = rcv[p]; }
+    int64_t own = c.nKl * c.np;
+    for (int64_t f = 0; f < c.n_free_vel; ++f)
+      if (c.dof_owner_sub[f] >= 0 && c.sub_rank[c.dof_owner_sub[f]] == rank) ++own;
+    *n_owned_free = own;
+  } catch (const Error &e) {
+    return fail(nullptr, e);
+  }
   return VB_OK;
 }
 

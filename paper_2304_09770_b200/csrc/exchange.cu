@@ -45,6 +45,27 @@ bool xch_sends(const vb_ctx *c, int e, int k, int mode) {
   return true;
 }
 
+void plan_slot_counts(const vb_ctx *c, const std::function<int64_t(int)> &L, int mode, std::vector<int64_t> &send,
+                      std::vector<int64_t> &recv) {
+  send.assign(c->nranks, 0);
+  recv.assign(c->nranks, 0);
+  for (size_t e = 0; e < c->ents.size(); ++e) {
+    const std::vector<int> &sh = c->ents[e].sharers;
+    const int64_t Le = L(e);
+    for (int p = 0; p < c->nranks; ++p) {
+      if (p == c->rank) continue;
+      bool shared = false;
+      for (int m : sh) shared |= c->sub_rank[m] == p;
+      if (!shared) continue;
+      for (size_t k = 0; k < sh.size(); ++k) {
+        if (!xch_sends(c, e, k, mode)) continue;
+        if (c->sub_rank[sh[k]] == c->rank) send[p] += Le;
+        if (c->sub_rank[sh[k]] == p) recv[p] += Le;
+      }
+    }
+  }
+}
+
 void build_slot_exchange(vb_ctx *c, SlotExchange &X, const std::function<int64_t(int)> &L,
                          const std::function<void(int, std::vector<int64_t> &)> &pos, int mode) {
   const int R = c->nranks, me = c->rank;
@@ -90,6 +111,10 @@ void build_slot_exchange(vb_ctx *c, SlotExchange &X, const std::function<int64_t
   }
   X.send_len = sidx.size();
   X.recv_len = roff;
+  std::vector<int64_t> ps, pr;
+  plan_slot_counts(c, L, mode, ps, pr);
+  for (const PeerXfer &x : X.xfers)
+    VB_REQUIRE(x.scount == ps[x.peer] && x.rcount == pr[x.peer], VB_EINVAL, "internal: exchange differs from its plan");
   X.send_idx.upload(sidx, c->stream);
   X.sendbuf.alloc(std::max<int64_t>(X.send_len, 1));
   VB_CUDA(cudaStreamSynchronize(c->stream));

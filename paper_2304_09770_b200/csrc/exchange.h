@@ -28,6 +28,10 @@ struct SlotExchange {
 enum { XCH_ALL = 0, XCH_OWNER = 1, XCH_RANK = 2 };
 void build_slot_exchange(vb_ctx *c, SlotExchange &X, const std::function<int64_t(int)> &L,
                          const std::function<void(int, std::vector<int64_t> &)> &pos, int mode = XCH_ALL);
+// Host-only plan of the same exchange: doubles sent to / received from every rank (size nranks).
+// build_slot_exchange checks its transfers against this plan.
+void plan_slot_counts(const vb_ctx *c, const std::function<int64_t(int)> &L, int mode, std::vector<int64_t> &send,
+                      std::vector<int64_t> &recv);
 // does sharer k of local entity e send under `mode`?
 bool xch_sends(const vb_ctx *c, int e, int k, int mode);
 // pack from `local`, exchange, receive into `recv` (recv_len doubles).  No-op for one rank.

@@ -1,0 +1,75 @@
+"""Multi-rank bookkeeping on the CPU (no GPU): world-size 2 and 4 process groups over gloo.
+
+Each process plays one rank of the weak-scaling box layouts of SURVEY §8(e) and asks the library's
+host planner (vb_plan_exchange, the same counting that every multi-rank context checks its NCCL
+transfers against) what it would send to and receive from every other rank.  The ranks exchange
+those plans over gloo and check that they agree pairwise (what r sends p is what p expects from
+r) for the three exchange modes, and that the owned free DOFs partition the global free vector."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, name, kw, rank_grid, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2304_09770_b200 as vb
+        from synthetic import make_problem
+        prob = make_problem(name, **kw)
+        srank = vb.box_ranks(prob.sub_grid, rank_grid)
+        ok = True
+        owned = None
+        for mode in (0, 1, 2):
+            snd, rcv, own = vb.plan_exchange(prob.mesh, prob.k, prob.cell_subdomain, srank, rank, world, mode)
+            owned = own
+            S = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
+            Rv = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(S, torch.tensor(snd))
+            dist.all_gather(Rv, torch.tensor(rcv))
+            S = torch.stack(S).numpy(); Rv = torch.stack(Rv).numpy()
+            ok &= bool(np.array_equal(S, Rv.T))                      # send[r][p] == recv[p][r]
+            ok &= bool(np.all(np.diag(S) == 0) and S.sum() > 0)
+        O = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(O, torch.tensor([owned]))
+        total = int(sum(int(o.item()) for o in O))
+        if rank == 0:
+            from oracle.assemble import GlobalDofs   # the free DOF count of the oracle's numbering
+            d = GlobalDofs(prob.mesh, prob.k)
+            nfree = d.n_free_vel + d.npres
+            q.put((ok, total, nfree))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,kw,rank_grid", [("c1", dict(n=8), (1, 1, 2)), ("c1", dict(n=8), (2, 2, 1)),
+                                              ("c3", dict(n=8), (1, 2, 1))])
+def test_exchange_plans_agree_across_ranks(name, kw, rank_grid):
+    world = int(np.prod(rank_grid))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, kw, rank_grid, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    ok, total, nfree = q.get(timeout=10)
+    assert ok
+    assert total == nfree
+
