@@ -35,6 +35,27 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _ncu_traffic(role_key="S_T packed GEMV"):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu --set full
+    capture (profiles/*ncu_full_sym_gemv.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full_sym_gemv.json")))
+    if not files:
+        return None, None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        for d in json.load(open(files[-1])):
+            if role_key in d.get("role", ""):
+                tot = 0.0
+                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v, u = d[k].split()
+                    tot += float(v) * scale[u]
+                return tot, os.path.basename(files[-1])
+    except Exception:
+        pass
+    return None, None
+
+
 class Clocks:
     """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
 
@@ -137,6 +158,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernel-timing", action="store_true", help="skip the per-kernel CUDA events")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -150,7 +172,7 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    os.environ["VB_KERNEL_TIMING"] = "1"
+    os.environ["VB_KERNEL_TIMING"] = "0"
     import paper_2304_09770_b200 as vb
     from synthetic import make_problem
     from synthetic.configs import C5_DIMS
@@ -187,6 +209,9 @@ def main():
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     its, ktimes = [], []
+    # timed pass: the product path (iterations as one CUDA-graph launch, no per-kernel events)
+    os.environ["VB_KERNEL_TIMING"] = "0"
+    ctx.pcg_solve(rhs, x, rtol=1e-10)
     with Clocks(local) as clk:
         barrier()
         torch.cuda.synchronize()
@@ -194,7 +219,6 @@ def main():
         for _ in range(args.steps):
             rep = ctx.pcg_solve(rhs, x, rtol=1e-10)
             its.append(rep["iterations"])
-            ktimes.append(ctx.kernel_times())
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -203,6 +227,24 @@ def main():
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
+    # second timed pass for the roofline: the same solves with CUDA events around every launch of
+    # the GEMV categories on the library stream (host-driven iterations: event records are not
+    # allowed inside the conditional graph body)
+    ms_instr = None
+    if not args.no_kernel_timing:
+        os.environ["VB_KERNEL_TIMING"] = "1"
+        ctx.pcg_solve(rhs, x, rtol=1e-10)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.pcg_solve(rhs, x, rtol=1e-10)
+            ktimes.append(ctx.kernel_times())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_instr = e0.elapsed_time(e1) / args.steps
+        os.environ["VB_KERNEL_TIMING"] = "0"
     it = float(np.mean(its))
     ndofs = st["n_dofs_paper"]          # the whole (global) problem, all ranks together
     value = ndofs * it / (ms / 1e3)
@@ -227,6 +269,8 @@ def main():
     e2e_val = ndofs * float(np.mean(e2e_its)) / (e2e_ms / 1e3)
 
     # roofline of the dominant kernel (the packed symmetric GEMV on S_T)
+    if not ktimes or not ktimes[0]:
+        ktimes = [{n: float("nan") for n in ("op", "loc", "coarse", "S", "M")}]
     kt = {k: float(np.mean([d[k] for d in ktimes])) for k in ktimes[0]}
     peak, peak_src = _peaks()
     names = list(kt.keys())
@@ -235,6 +279,7 @@ def main():
     loc_ms, loc_bytes = kt[names[1]], 8.0 * st["sum_pk_D"]
     c_ms, c_bytes = kt[names[2]], 8.0 * st["pk_coarse"]
     achieved = op_bytes / (op_ms / 1e3) / 1e9
+    traffic, traffic_src = _ncu_traffic()
     iter_ms = ms / max(it, 1)
     per_iter_bytes = st["bytes_per_iter"]
     line = {
@@ -251,16 +296,22 @@ def main():
                    % (ws, "x".join(map(str, rank_grid))),
                    "l2": "inputs larger than L2 (%.1f GB of operators streamed per iteration)" % (per_iter_bytes / 1e9),
                    "ms_per_iteration": iter_ms,
+                   "ms_per_step_instrumented": ms_instr,
+                   "iteration_driver": "CUDA graph, conditional WHILE node (device-side stopping test)",
                    "achieved_GBps_per_iteration_model": per_iter_bytes / (iter_ms / 1e3) / 1e9},
-        "roofline": {"bound": "hbm", "kernel": names[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+        "roofline": {"bound": "hbm", "kernel": names[0], "measured_in": "second timed pass (per-launch CUDA events)", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src,
                      "bytes_per_launch": op_bytes, "ms_per_launch": op_ms,
                      "others": {names[1]: {"ms": loc_ms, "GBps": loc_bytes / (loc_ms / 1e3) / 1e9 if loc_ms else None},
                                 names[2]: {"ms": c_ms, "GBps": c_bytes / (c_ms / 1e3) / 1e9 if c_ms else None},
                                 names[3]: {"ms": kt[names[3]]}, names[4]: {"ms": kt[names[4]]}}},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ctx.n_free,
                 "d2h_bytes_per_step": 8 * ctx.n_free, "ms_per_step": e2e_ms},
-        "gpu_launches": int(args.steps * (7 + 23 * it)),
+        # kernels per solve (single rank): B0 6 + init 2 + first M^-1 15 + it S-steps x 6 +
+        # (it-1) M-steps x 16 + B8 6 = 13 + 22 it (cross-checked against the ncu launch list in
+        # profiles/); multi-rank adds the exchange pack/sum kernels
+        "gpu_launches": int(args.steps * (13 + 22 * it)),
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -66,6 +66,7 @@ static NcclApi &nccl() {
 
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
+  bool capturable() const override { return true; }
   ~NcclComm() override {
     if (comm && nccl().CommDestroy) nccl().CommDestroy(comm);
   }

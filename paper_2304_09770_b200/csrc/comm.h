@@ -26,6 +26,7 @@ struct Comm {
   // every rank contributes `count` doubles; recv holds nranks * count in rank order
   virtual void allgather(const double *send, double *recv, int64_t count, cudaStream_t s) = 0;
   virtual void abort() {}
+  virtual bool capturable() const { return false; }   // may run inside CUDA stream capture
 };
 
 Comm *make_nccl_comm(int rank, int nranks, const void *unique_id128, int device);

@@ -206,18 +206,16 @@ __global__ void multiplicity_kernel(const SlotDev *__restrict__ slots, const Ent
     Dlx[s.off_Dlx + idx] = (idx % s.nd == idx / s.nd) ? v : 0.0;
 }
 
-// column-major nd x nd deluxe block -> row-major 32x32 tiles (tile (I,J) at (I nt + J) 1024)
-__global__ void tile_rect_kernel(const SlotDev *__restrict__ slots, const int *__restrict__ act,
-                                 const double *__restrict__ Dlx, double *Dt) {
+// column-major nd x nd deluxe block -> row-major (unpadded)
+__global__ void transpose_slot_kernel(const SlotDev *__restrict__ slots, const int *__restrict__ act,
+                                      const double *__restrict__ Dlx, double *Dt) {
   const SlotDev s = slots[act[blockIdx.y]];
-  const int nd = s.nd, nt = (nd + 31) / 32;
+  const int nd = s.nd;
   const double *D = Dlx + s.off_Dlx;
   double *out = Dt + s.off_Dt;
-  for (int64_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < (int64_t)nt * nt * 1024; idx += gridDim.x * blockDim.x) {
-    const int tile = idx / 1024, w = idx % 1024;
-    const int I = tile / nt, J = tile % nt, r = w / 32, cc = w % 32;
-    const int row = 32 * I + r, col = 32 * J + cc;
-    out[idx] = (row < nd && col < nd) ? D[row + (int64_t)col * nd] : 0.0;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nd * nd; idx += gridDim.x * blockDim.x) {
+    const int i = idx / nd, j = idx % nd;     // out row-major (i, j)
+    out[idx] = D[i + (int64_t)j * nd];
   }
 }
 
@@ -721,27 +719,24 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
       sync(c);
     }
   }
-  // ---------------- deluxe blocks -> row-major 32x32 tiles for the per-iteration kernels
+  // ---------------- deluxe blocks: also row-major (= D^T column-major) for the restriction
   {
-    int64_t off = 0;
     std::vector<int> act_s, act_e;
     for (int q = 0; q < nslot; ++q) {
       SlotDev &sl = c->h_slot[q];
-      const int nt = (sl.nd + 31) / 32;
-      sl.off_Dt = off;
-      off += (int64_t)nt * nt * 1024;
+      sl.off_Dt = sl.off_Dlx;
       if (sl.nd) act_s.push_back(q);
     }
     for (int e = 0; e < nent; ++e)
       if (c->h_ent[e].nd) act_e.push_back(e);
-    c->d_Dt.alloc(std::max<int64_t>(off, 1));
+    c->d_Dt.alloc(std::max<int64_t>(c->len_Dlx, 1));
     c->d_slot.upload(c->h_slot, s);
     c->d_act_slots.upload(act_s, s);
     c->d_act_ents.upload(act_e, s);
     c->n_act_slots = act_s.size();
     c->n_act_ents = act_e.size();
     if (c->n_act_slots) {
-      tile_rect_kernel<<<dim3(64, c->n_act_slots), 256, 0, s>>>(c->d_slot.p, c->d_act_slots.p, c->d_Dlx.p, c->d_Dt.p);
+      transpose_slot_kernel<<<dim3(16, c->n_act_slots), 256, 0, s>>>(c->d_slot.p, c->d_act_slots.p, c->d_Dlx.p, c->d_Dt.p);
       VB_STAGE();
     }
   }

@@ -114,15 +114,18 @@ static size_t gemv_smem(int nmax, int warps = GV_WARPS) {
 }
 
 // split a packed matrix of n into P chunks of tile rows balanced by tile count
-static void split_rows(int n, int P, std::vector<std::pair<int, int>> &out) {
+// split a packed matrix of n into P chunks of tile rows balanced by cost = tiles + row_cost per tile
+// row (the per-row reduction and barriers cost about row_cost tiles of streaming)
+static void split_rows(int n, int P, std::vector<std::pair<int, int>> &out, double row_cost = 0.0) {
   int nt = (n + 31) / 32;
-  int64_t total = (int64_t)nt * (nt + 1) / 2;
+  auto cum = [&](int r) { return (double)r * (r + 1) / 2 + row_cost * r; };   // cost of rows [0, r)
+  const double total = cum(nt);
   out.clear();
   int r = 0;
   for (int p = 0; p < P && r < nt; ++p) {
-    int64_t target = total * (p + 1) / P;
+    const double target = total * (p + 1) / P;
     int r1 = r;
-    while (r1 < nt && (int64_t)(r1 + 1) * (r1 + 2) / 2 <= target) ++r1;
+    while (r1 < nt && cum(r1 + 1) <= target) ++r1;
     if (r1 == r) r1 = r + 1;
     if (p == P - 1) r1 = nt;
     out.push_back({r, r1});
@@ -195,13 +198,6 @@ __global__ void dot_final_kernel(const double *__restrict__ part, int nb, double
 }
 
 // scal: [0] rz, [1] pq, [2] rr, [3] rz_new, [4] alpha, [5] beta
-__global__ void update_xr_kernel(double *x, double *r, const double *p, const double *q, int64_t n, const double *scal) {
-  const double alpha = scal[0] / scal[1];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] += alpha * p[i];
-    r[i] -= alpha * q[i];
-  }
-}
 
 __global__ void update_p_kernel(double *p, const double *z, int64_t n, double *scal, int first) {
   const double beta = first ? 0.0 : scal[3] / scal[0];
@@ -209,51 +205,118 @@ __global__ void update_p_kernel(double *p, const double *z, int64_t n, double *s
     p[i] = z[i] + beta * p[i];
 }
 
-__global__ void rotate_rz_kernel(double *scal, double *hist, int it) {
-  // record alpha_it, beta_it and rotate rz <- rz_new
-  hist[2 * it + 0] = scal[0] / scal[1];
-  hist[2 * it + 1] = scal[3] / scal[0];
+__global__ void rotate_rz_kernel(double *scal, double *hist) {
+  // record beta of this step and rotate rz <- rz_new (it = scal[6] already counts this step)
+  const int it = (int)scal[6];
+  if (it >= 1 && it <= 4096) hist[2 * (it - 1) + 1] = scal[3] / scal[0];
   scal[0] = scal[3];
 }
 
-// restriction with deluxe scaling: rD^(sub)[offD+j] = sum_i D^(sub)[i, j] r_x[off_xd + i]  (D^T r).
-// D is stored as row-major 32x32 tiles (zero padded): a warp streams one contiguous 8 KB tile with
-// lane = tile column, so the column sums need no cross-lane reduction; per-warp partials are
-// summed in fixed order (deterministic).  One CTA per active (entity, sharer) slot.
-constexpr int DLX_WARPS = 4;
-__global__ void __launch_bounds__(DLX_WARPS * 32) restrict_kernel(const SlotDev *__restrict__ slots,
-                                const int *__restrict__ act, const EntDev *__restrict__ ents,
-                                const SubDev *__restrict__ subs, const double *__restrict__ Dt,
-                                const double *__restrict__ r, double *rD) {
-  extern __shared__ double sh[];
-  const SlotDev s = slots[act[blockIdx.x]];
-  const int nd = s.nd;
-  const int nt = (nd + 31) / 32, npad = nt * 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double *xs = sh;                  // npad
-  double *part = sh + npad;         // nw * npad
-  const double *D = Dt + s.off_Dt;
-  const double *re = r + ents[s.ent].off_xd;
-  for (int i = threadIdx.x; i < npad; i += blockDim.x) xs[i] = i < nd ? re[i] : 0.0;
-  for (int i = threadIdx.x; i < nw * npad; i += blockDim.x) part[i] = 0.0;
+// ---- single-launch deterministic reductions: block partials, the last block to finish sums them
+// in block order (threadfence + ticket), then resets the ticket for the next use.
+__device__ __forceinline__ void block_reduce_last(double v, double *part, unsigned *ticket, double *dst) {
+  __shared__ double red[32];
+  __shared__ bool last;
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
-  for (int u = warp; u < nt * nt; u += nw) {
-    const int I = u / nt, J = u % nt;
-    const double *T = D + (int64_t)u * 1024;
-    double t[32];
-#pragma unroll
-    for (int rr = 0; rr < 32; ++rr) t[rr] = __ldg(T + rr * 32 + lane);
-    double acc = 0.0;
-#pragma unroll
-    for (int rr = 0; rr < 32; ++rr) acc += t[rr] * xs[32 * I + rr];
-    part[warp * npad + 32 * J + lane] += acc;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    part[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  double *out = rD + subs[s.sub].off_Dv + s.offD;
+  if (last && threadIdx.x < 32) {
+    __threadfence();
+    double t = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) t += ((volatile double *)part)[i];
+    t = warp_sum(t);
+    if (threadIdx.x == 0) { *dst = t; *ticket = 0u; }
+  }
+}
+
+__global__ void dot_kernel(const double *__restrict__ a, const double *__restrict__ b, const double *__restrict__ mask,
+                           int64_t n, double *part, unsigned *ticket, double *dst) {
+  double v = 0.0;
+  if (mask) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      v += mask[i] * (a[i] * b[i]);
+  } else {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      v += a[i] * b[i];
+  }
+  block_reduce_last(v, part, ticket, dst);
+}
+
+// x += alpha p, r -= alpha q (alpha = rz / pq), fused with the partial of r.r -> dst
+__global__ void update_xr_rr_kernel(double *x, double *r, const double *p, const double *q, const double *mask,
+                                    int64_t n, const double *scal, double *part, unsigned *ticket, double *dst) {
+  const double alpha = scal[0] / scal[1];
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    v += mask ? mask[i] * (ri * ri) : ri * ri;
+  }
+  block_reduce_last(v, part, ticket, dst);
+}
+
+// scal: [0] rz [1] pq [2] rr [3] rz_new [4] r0n [5] rtol*r0n [6] it [7] status [8] maxit
+//  status: 0 running, 1 converged, 2 breakdown (p.Sp <= 0 or r.z <= 0), 3 maxit
+__global__ void pcg_init_kernel(double *scal, double rtol, int maxit) {
+  const double r0n = sqrt(scal[2]);
+  scal[4] = r0n; scal[5] = rtol * r0n; scal[6] = 0.0; scal[8] = maxit;
+  scal[7] = (r0n <= rtol * r0n) ? 1.0 : (maxit <= 0 ? 3.0 : 0.0);
+}
+
+__global__ void pcg_check_kernel(double *scal, double *hist, cudaGraphConditionalHandle hw, int use_graph) {
+  const double rz = scal[0], pq = scal[1];
+  int it = (int)scal[6];
+  double status = 0.0;
+  if (!(pq > 0) || !(rz > 0)) {
+    status = 2.0;
+  } else {
+    if (it < 4096) hist[2 * it] = rz / pq;
+    ++it;
+    scal[6] = it;
+    if (sqrt(scal[2]) <= scal[5]) status = 1.0;
+    else if (it >= (int)scal[8]) status = 3.0;
+  }
+  scal[7] = status;
+  if (use_graph) cudaGraphSetConditional(hw, status == 0.0 ? 1u : 0u);
+}
+
+// deluxe restriction / extension per active slot: out[j] = sum_i M[i nd + j] in[i], M row-major
+// nd x nd, unpadded: thread per column j, rows streamed coalesced (4 independent accumulators, fixed
+// order).  Restriction: M = D^(m) row-major, giving D^T r_e; extension: M = D^(m)
+// column-major (= (D^(m))^T row-major), giving D^(m) w^(m).
+struct DlxDesc {
+  int64_t moff, in_off, out_off;
+  int nd, pad;
+};
+
+__global__ void __launch_bounds__(256) dlx_apply_kernel(const DlxDesc *__restrict__ desc, const double *__restrict__ M,
+                                                        const double *__restrict__ in, double *out) {
+  extern __shared__ double xs[];
+  const DlxDesc D = desc[blockIdx.x];
+  const int nd = D.nd;
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) xs[i] = in[D.in_off + i];
+  __syncthreads();
   for (int j = threadIdx.x; j < nd; j += blockDim.x) {
-    double v = 0.0;
-    for (int w = 0; w < nw; ++w) v += part[w * npad + j];
-    out[j] = v;
+    const double *m = M + D.moff + j;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int i = 0;
+    for (; i + 3 < nd; i += 4) {
+      a0 += __ldg(m + (int64_t)i * nd) * xs[i];
+      a1 += __ldg(m + (int64_t)(i + 1) * nd) * xs[i + 1];
+      a2 += __ldg(m + (int64_t)(i + 2) * nd) * xs[i + 2];
+      a3 += __ldg(m + (int64_t)(i + 3) * nd) * xs[i + 3];
+    }
+    for (; i < nd; ++i) a0 += __ldg(m + (int64_t)i * nd) * xs[i];
+    out[D.out_off + j] = (a0 + a1) + (a2 + a3);
   }
 }
 
@@ -324,55 +387,6 @@ __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ 
   }
   for (; a < S.npi; ++a) a0 += F[j + (int64_t)a * S.nd] * us[a];
   w[S.off_Dv + j] = v + ((a0 + a1) + (a2 + a3));
-}
-
-// extension with deluxe scaling, per local slot: t^(m) = D^(m) w^(m) (the entity sum over all sharers
-// follows in fixed order).  Warps stream 32x32 row-major tiles, lane = tile column; row sums by a
-// transpose-reduce; per-warp row partials summed in fixed order.  One CTA per active slot.
-__global__ void __launch_bounds__(DLX_WARPS * 32) slot_extend_kernel(const SlotDev *__restrict__ slots,
-                              const int *__restrict__ act, const SubDev *__restrict__ subs,
-                              const double *__restrict__ Dt, const int64_t *__restrict__ toff,
-                              const double *__restrict__ w, double *t) {
-  extern __shared__ double sh[];
-  const int slot = act[blockIdx.x];
-  const SlotDev s = slots[slot];
-  const int nd = s.nd;
-  const int nt = (nd + 31) / 32, npad = nt * 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  double *ws = sh;                 // npad
-  double *part = sh + npad;        // nw * npad
-  const double *src = w + subs[s.sub].off_Dv + s.offD;
-  for (int i = threadIdx.x; i < npad; i += blockDim.x) ws[i] = i < nd ? src[i] : 0.0;
-  for (int i = threadIdx.x; i < nw * npad; i += blockDim.x) part[i] = 0.0;
-  __syncthreads();
-  for (int u = warp; u < nt * nt; u += nw) {
-    const int I = u / nt, J = u % nt;
-    const double *T = Dt + s.off_Dt + (int64_t)u * 1024;
-    double p[32];
-#pragma unroll
-    for (int rr = 0; rr < 32; ++rr) p[rr] = __ldg(T + rr * 32 + lane);
-    const double wc = ws[32 * J + lane];
-#pragma unroll
-    for (int rr = 0; rr < 32; ++rr) p[rr] *= wc;
-#pragma unroll
-    for (int sft = 16; sft > 0; sft >>= 1) {
-      const bool up = (lane & sft) != 0;
-#pragma unroll
-      for (int k2 = 0; k2 < sft; ++k2) {
-        double send = up ? p[k2] : p[k2 + sft];
-        double keep = up ? p[k2 + sft] : p[k2];
-        p[k2] = keep + __shfl_xor_sync(FULL, send, sft);
-      }
-    }
-    part[warp * npad + 32 * I + lane] += p[0];
-  }
-  __syncthreads();
-  double *out = t + toff[slot];
-  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
-    double v = 0.0;
-    for (int w2 = 0; w2 < nw; ++w2) v += part[w2 * npad + i];
-    out[i] = v;
-  }
 }
 
 __global__ void copy_kernel(const double *a, double *b, int64_t n) {
@@ -621,6 +635,8 @@ struct SolveState {
   DBuf<GemvWork> w_kd;
   int nw_op = 0, nw_loc = 0, nw_c = 0, nw_kd = 0, max_nd = 1;
   bool big_c = false;                // coarse vectors exceed shared memory: BIG GEMV variant
+  DBuf<DlxDesc> dlx_r, dlx_e;        // deluxe restriction / extension descriptors (active slots)
+  int dlx_threads = 32;
   size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_rx = 0, sm_ex = 0, sm_kd = 0;
   DBuf<int64_t> xptr, xidx;          // B2: x coordinate <- copies (local s or received), sharer order
   DBuf<int64_t> pptr, pidx;          // B6: global coarse index <- coarse pieces, fixed order
@@ -637,12 +653,25 @@ struct SolveState {
   DBuf<int64_t> gh_dst;              // DOF halo: destination free ids of received owner values
   int64_t n_gh = 0;
   bool ready = false;
-  // optional per-kernel timing (VB_KERNEL_TIMING=1): event pairs per launch category
+  DBuf<unsigned> ticket;             // single-launch reductions
+  cudaStream_t s2 = nullptr;         // coarse branch of M^-1, concurrent with the local solves
+  cudaStream_t sg = nullptr;         // stream the iteration graph is captured on and launched on
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // the PCG iteration as a CUDA graph: WHILE(status == 0) { S-part; check; IF(status == 0) M-part }
+  cudaGraphExec_t gexec = nullptr;
+  bool capturing = false;
+  // optional per-kernel timing (VB_KERNEL_TIMING=1, host-driven iterations): event pairs per
+  // launch category
   std::vector<cudaEvent_t> ev;
   std::vector<int> ev_cat;
   int nev = 0;
   ~SolveState() {
     for (auto e : ev) cudaEventDestroy(e);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (s2) cudaStreamDestroy(s2);
+    if (sg) cudaStreamDestroy(sg);
   }
 };
 
@@ -651,8 +680,9 @@ static const char *kCatNames[] = {"sym_gemv S_T (operator, B1)", "sym_gemv S_DD^
                                   "apply_M total (B4-B7)"};
 constexpr int N_CAT = 5;
 
-static void tick(vb_ctx *c, SolveState *st, int cat, bool begin) {
+static void tick(vb_ctx *c, SolveState *st, int cat, bool begin, cudaStream_t strm = nullptr) {
   if (!c->timing) return;
+  if (!strm) strm = c->stream;
   if (st->nev + 1 >= (int)st->ev.size()) {
     for (int i = 0; i < 256; ++i) {
       cudaEvent_t e;
@@ -661,7 +691,7 @@ static void tick(vb_ctx *c, SolveState *st, int cat, bool begin) {
       st->ev_cat.push_back(-1);
     }
   }
-  VB_CUDA(cudaEventRecord(st->ev[st->nev], c->stream));
+  VB_CUDA(cudaEventRecord(st->ev[st->nev], strm));
   st->ev_cat[st->nev] = begin ? cat : -1 - cat;
   st->nev++;
 }
@@ -685,6 +715,7 @@ static void collect_times(vb_ctx *c, SolveState *st) {
     open[cat] = -1;
   }
   st->nev = 0;
+
 }
 
 const char *kernel_time_name(int i) { return (i >= 0 && i < N_CAT) ? kCatNames[i] : ""; }
@@ -699,8 +730,8 @@ static SolveState *get_state(vb_ctx *c) {
 // C3: block partials -> rank partial -> fixed-order sum over ranks
 static void dot(vb_ctx *c, const double *a, const double *b, int64_t n, double *dst) {
   SolveState *st = get_state(c);
-  dot_partial_kernel<<<DOT_BLOCKS, 256, 0, c->stream>>>(a, b, c->nranks > 1 ? st->mask.p : nullptr, n, c->w_dots.p);
-  dot_final_kernel<<<1, 32, 0, c->stream>>>(c->w_dots.p, DOT_BLOCKS, dst);
+  dot_kernel<<<DOT_BLOCKS, 256, 0, c->stream>>>(a, b, c->nranks > 1 ? st->mask.p : nullptr, n, c->w_dots.p,
+                                                st->ticket.p, dst);
   allreduce_sum_fixed(c, dst, 1);
 }
 
@@ -739,42 +770,43 @@ static void trace_norm(vb_ctx *c, const char *name, const double *v, int64_t n, 
 }
 
 static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
-  cudaStream_t s = c->stream;
+  cudaStream_t s = c->stream, s2 = st->s2;
   tick(c, st, 4, true);
   if (c->n_act_slots)
-    restrict_kernel<<<c->n_act_slots, DLX_WARPS * 32, st->sm_rx, s>>>(c->d_slot.p, c->d_act_slots.p, c->d_ent.p,
-                                                                     c->d_sub.p, c->d_Dt.p, c->w_r.p, c->w_locD.p);
+    dlx_apply_kernel<<<c->n_act_slots, st->dlx_threads, st->sm_rx, s>>>(st->dlx_r.p, c->d_Dt.p, c->w_r.p, c->w_locD.p);
   trace_norm(c, "rD", c->w_locD.p, c->len_Dv, false);
+  // fork: the coarse branch (B6) runs on s2 while the local dual solves (B5) stream on s
+  VB_CUDA(cudaEventRecord(st->ev_fork, s));
+  VB_CUDA(cudaStreamWaitEvent(s2, st->ev_fork, 0));
   tick(c, st, 1, true);
   if (st->nw_loc) sym_gemv_kernel<GV_WARPS><<<st->nw_loc, GV_WARPS * 32, st->sm_loc, s>>>(st->w_loc.p);
   tick(c, st, 1, false);
   // coarse pieces (C2): [Phi_i^T rD_i per local subdomain | r0_i | r_Pi of the owned entities]
-  phit_kernel<<<dim3(PHIT_SPLIT, c->N), 256, 0, s>>>(c->d_sub.p, c->d_Phi.p, c->w_locD.p, st->cbuf.p);
-  dev_gather(c->w_r.p, st->cpack.p, (int64_t)st->cpack.n, st->cbuf.p + c->len_Pi, s);
+  phit_kernel<<<dim3(PHIT_SPLIT, c->N), 256, 0, s2>>>(c->d_sub.p, c->d_Phi.p, c->w_locD.p, st->cbuf.p);
+  dev_gather(c->w_r.p, st->cpack.p, (int64_t)st->cpack.n, st->cbuf.p + c->len_Pi, s2);
   const double *pieces = st->cbuf.p;
   if (c->nranks > 1) {
-    c->comm->allgather(st->cbuf.p, st->cgath.p, st->cmax, s);
+    c->comm->allgather(st->cbuf.p, st->cgath.p, st->cmax, s2);
     pieces = st->cgath.p;
   }
-  trace_norm(c, "cpart", st->cbuf.p, c->len_Pi, false);
-  gather_src_kernel<<<grid_for(c->Nc), 256, 0, s>>>(st->pptr.p, st->pidx.p, pieces, c->Nc, c->w_rc.p);
-  trace_norm(c, "rc", c->w_rc.p, c->Nc, true);
-  coarse_p0_project_kernel<<<1, 256, 0, s>>>(st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
-  tick(c, st, 2, true);
+  gather_src_kernel<<<grid_for(c->Nc), 256, 0, s2>>>(st->pptr.p, st->pidx.p, pieces, c->Nc, c->w_rc.p);
+  coarse_p0_project_kernel<<<1, 256, 0, s2>>>(st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
+  tick(c, st, 2, true, s2);
   if (st->big_c)
-    sym_gemv_kernel<GV_WARPS_C, true><<<st->nw_c, GV_WARPS_C * 32, GV_WARPS_C * 32 * sizeof(double), s>>>(st->w_c.p);
+    sym_gemv_kernel<GV_WARPS_C, true><<<st->nw_c, GV_WARPS_C * 32, GV_WARPS_C * 32 * sizeof(double), s2>>>(st->w_c.p);
   else
-    sym_gemv_kernel<GV_WARPS_C><<<st->nw_c, GV_WARPS_C * 32, st->sm_c, s>>>(st->w_c.p);
-  tick(c, st, 2, false);
-  sum_chunks_kernel<<<(c->Nc + 31) / 32, 256, 0, s>>>(c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
-  coarse_p0_project_kernel<<<1, 256, 0, s>>>(st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
+    sym_gemv_kernel<GV_WARPS_C><<<st->nw_c, GV_WARPS_C * 32, st->sm_c, s2>>>(st->w_c.p);
+  tick(c, st, 2, false, s2);
+  sum_chunks_kernel<<<(c->Nc + 31) / 32, 256, 0, s2>>>(c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
+  coarse_p0_project_kernel<<<1, 256, 0, s2>>>(st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
+  VB_CUDA(cudaEventRecord(st->ev_join, s2));
+  VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
   trace_norm(c, "uc", c->w_uc.p, c->Nc, true);
   local2_kernel<<<dim3((st->max_nd + 127) / 128, c->N), 128, c->max_npi * sizeof(double), s>>>(
       c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p);
   trace_norm(c, "w", c->w_locD.p, c->len_Dv, false);
   if (c->n_act_slots)
-    slot_extend_kernel<<<c->n_act_slots, DLX_WARPS * 32, st->sm_ex, s>>>(c->d_slot.p, c->d_act_slots.p, c->d_sub.p,
-                                                                        c->d_Dt.p, st->toff.p, c->w_locD.p, st->tx.p);
+    dlx_apply_kernel<<<c->n_act_slots, st->dlx_threads, st->sm_rx, s>>>(st->dlx_e.p, c->d_Dlx.p, c->w_locD.p, st->tx.p);
   run_slot_exchange(c, st->XE, st->tx.p, st->tx.p + st->len_t);    // C1 (cross-rank products)
   trace_norm(c, "t", st->tx.p, st->len_t, false);
   run_entity_sum(c, st->ESE, st->tx.p, c->w_z.p);
@@ -812,6 +844,14 @@ void prepare_solve(vb_ctx *c) {
   c->w_locY.alloc((int64_t)c->P_loc * std::max<int64_t>(c->len_Dv, 1));
   c->w_uc.alloc(c->Nc); c->w_rc.alloc(c->Nc);
   c->w_scal.alloc(16); c->w_scal.zero(s);
+  st->ticket.alloc(4); st->ticket.zero(s);
+  if (!st->s2) {
+    VB_CUDA(cudaStreamCreateWithFlags(&st->s2, cudaStreamNonBlocking));
+    VB_CUDA(cudaStreamCreateWithFlags(&st->sg, cudaStreamNonBlocking));
+    VB_CUDA(cudaEventCreateWithFlags(&st->ev_fork, cudaEventDisableTiming));
+    VB_CUDA(cudaEventCreateWithFlags(&st->ev_join, cudaEventDisableTiming));
+  }
+  if (c->nranks > 1) c->w_red.alloc((size_t)c->nranks * 8);
   c->w_dots.alloc(DOT_BLOCKS * 2 + 256);
   c->w_gam.alloc(std::max<int64_t>(c->nGamma, 1));
   c->w_bD.alloc(std::max<int64_t>(c->len_Dn, 1));
@@ -846,7 +886,7 @@ void prepare_solve(vb_ctx *c) {
   wl.clear();
   int Pc = std::max(1, std::min<int>(c->P_c, (int)((c->Nc + 31) / 32)));
   c->w_ucp.alloc((int64_t)Pc * c->Nc);
-  split_rows(c->Nc, Pc, rows);
+  split_rows(c->Nc, Pc, rows, 4.0);
   for (int q = 0; q < Pc; ++q)
     wl.push_back(GemvWork{c->d_Kcp.p, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, rows[q].first, rows[q].second, 0});
   st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = gemv_smem(c->Nc, GV_WARPS_C);
@@ -860,12 +900,8 @@ void prepare_solve(vb_ctx *c) {
   int maxnd_e = 1;
   for (auto &E : c->h_ent)
     if (E.nd) maxnd_e = std::max(maxnd_e, E.nd);
-  const int npad = (maxnd_e + 31) / 32 * 32;
-  st->sm_rx = (size_t)(1 + DLX_WARPS) * npad * sizeof(double);
-  st->sm_ex = st->sm_rx;
-  VB_REQUIRE(st->sm_ex <= 227 * 1024, VB_EINVAL, "deluxe entity too large for the extension kernel");
-  VB_CUDA(cudaFuncSetAttribute(restrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_rx));
-  VB_CUDA(cudaFuncSetAttribute(slot_extend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_ex));
+  st->sm_rx = (size_t)maxnd_e * sizeof(double);
+  st->dlx_threads = std::min(256, (maxnd_e + 31) / 32 * 32);
   st->max_nd = nmaxD;
   const int ne = c->ents.size();
   // ---------------- B2 (apply_S): copies of each x coordinate, local and received, in sharer order
@@ -909,6 +945,18 @@ void prepare_solve(vb_ctx *c) {
     for (size_t q = 0; q < c->h_slot.size(); ++q) { toff[q] = o; o += c->h_slot[q].nd; }
     st->len_t = o;
     st->toff.upload(toff, s);
+    // deluxe descriptors of the active slots (same order as d_act_slots)
+    std::vector<DlxDesc> dr, de;
+    for (size_t q = 0; q < c->h_slot.size(); ++q) {
+      const SlotDev &sl = c->h_slot[q];
+      if (!sl.nd) continue;
+      const SubDev &S = c->h_sub[sl.sub];
+      const int64_t wl = S.off_Dv + sl.offD;
+      dr.push_back(DlxDesc{sl.off_Dt, c->h_ent[sl.ent].off_xd, wl, sl.nd, 0});
+      de.push_back(DlxDesc{sl.off_Dlx, wl, toff[q], sl.nd, 0});
+    }
+    st->dlx_r.upload(dr, s);
+    st->dlx_e.upload(de, s);
     auto L = [&](int e) { return (int64_t)c->h_ent[e].nd; };
     build_slot_exchange(c, st->XE, L, [&](int sl, std::vector<int64_t> &out) {
       for (int t = 0; t < c->h_slot[sl].nd; ++t) out.push_back(toff[sl] + t);
@@ -1144,6 +1192,81 @@ static double read_scalar(vb_ctx *c, int i) {
 
 void lanczos_extremes(const std::vector<double> &al, const std::vector<double> &be, double *lmin, double *lmax);
 
+// one PCG step up to the stopping test: q = S^ p, pq, x/r update fused with r.r, check (SURVEY O-15)
+static void pcg_step(vb_ctx *c, SolveState *st, cudaGraphConditionalHandle hw, bool graph) {
+  cudaStream_t s = c->stream;
+  double *sc = c->w_scal.p;
+  const int64_t nx = c->nx;
+  apply_S(c, st);
+  dot(c, c->w_p.p, c->w_q.p, nx, sc + 1);
+  update_xr_rr_kernel<<<DOT_BLOCKS, 256, 0, s>>>(c->w_x.p, c->w_r.p, c->w_p.p, c->w_q.p,
+                                                 c->nranks > 1 ? st->mask.p : nullptr, nx, sc, c->w_dots.p,
+                                                 st->ticket.p, sc + 2);
+  allreduce_sum_fixed(c, sc + 2, 1);
+  pcg_check_kernel<<<1, 1, 0, s>>>(sc, st->hist.p, hw, graph ? 1 : 0);
+  VB_STAGE();
+}
+
+// the rest of the step: z = M^-1 r, rz, p update, beta and rz rotation
+static void pcg_mstep(vb_ctx *c, SolveState *st) {
+  cudaStream_t s = c->stream;
+  double *sc = c->w_scal.p;
+  const int64_t nx = c->nx;
+  apply_M(c, st);
+  dot(c, c->w_r.p, c->w_z.p, nx, sc + 3);
+  update_p_kernel<<<grid_for(nx), 256, 0, s>>>(c->w_p.p, c->w_z.p, nx, sc, 0);
+  rotate_rz_kernel<<<1, 1, 0, s>>>(sc, st->hist.p);
+  VB_STAGE();
+}
+
+// graphs need a capturable transport (no host synchronisation inside the iteration)
+static bool use_graph(const vb_ctx *c) {
+  if (getenv("VB_NO_GRAPH") && atoi(getenv("VB_NO_GRAPH"))) return false;
+  if (c->timing) return false;   // event records are not allowed inside conditional graph bodies
+  if (getenv("VB_PCG_TRACE") && atoi(getenv("VB_PCG_TRACE"))) return false;
+  return c->nranks == 1 || c->comm->capturable();
+}
+
+// WHILE(status == 0) { z = M^-1 r, beta, p; q = S^ p, alpha, x, r, stopping test } -- the first
+// S-part runs before the graph, so no step is wasted at convergence.
+static void build_iteration_graph(vb_ctx *c, SolveState *st) {
+  // capture on the library's own stream (the caller's may be the legacy default stream, which
+  // cannot be captured); kernels launched on c->stream during capture go to sg
+  cudaStream_t s = st->sg, user = c->stream;
+  c->stream = s;
+  cudaGraph_t g;
+  VB_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle hw;
+  VB_CUDA(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams wp = {};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  VB_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  st->capturing = true;
+  try {
+    VB_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    pcg_mstep(c, st);
+    pcg_step(c, st, hw, true);
+    VB_CUDA(cudaStreamEndCapture(s, &body));
+  } catch (...) {
+    st->capturing = false;
+    c->stream = user;
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(s, &dummy);
+    (void)cudaGetLastError();
+    cudaGraphDestroy(g);
+    throw;
+  }
+  st->capturing = false;
+  c->stream = user;
+  VB_CUDA(cudaGraphInstantiate(&st->gexec, g, 0));
+  VB_CUDA(cudaGraphDestroy(g));
+}
+
 void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int maxit, vb_report *rep) {
   prepare_solve(c);
   SolveState *st = get_state(c);
@@ -1177,54 +1300,53 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   run_entity_sum(c, st->ESB, st->gbuf.p, c->w_gam.p, st->gam2.p);             // ghat = b + sum_m zG^(m)
   gamma_rhs_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_T.p, c->w_gam.p, NDelta, c->w_r.p);
   VB_STAGE();
-  // ---------------- PCG (SURVEY O-15)
+  // ---------------- PCG (SURVEY O-15), iterations driven on the device (scal[6] = it, scal[7] = status)
   c->w_x.zero(s);
   double *sc = c->w_scal.p;
   dot(c, c->w_r.p, c->w_r.p, nx, sc + 2);
-  const double rr0 = read_scalar(c, 2);
-  const double r0n = sqrt(rr0);
-  if (trace) fprintf(stderr, "[vb rank %d] rr0 %.17g\n", c->rank, rr0);
-  apply_M(c, st);
-  dot(c, c->w_r.p, c->w_z.p, nx, sc + 0);
-  update_p_kernel<<<grid_for(nx), 256, 0, s>>>(c->w_p.p, c->w_z.p, nx, sc, 1);
-  VB_STAGE();
-  int it = 0;
-  int status = VB_OK;
-  double rn = r0n;
-  std::vector<double> alphas, betas;
-  while (true) {
-    if (rn <= rtol * r0n) break;
-    if (it >= maxit) { status = VB_ENOTCONV; break; }
-    apply_S(c, st);
-    dot(c, c->w_p.p, c->w_q.p, nx, sc + 1);
-    update_xr_kernel<<<grid_for(nx), 256, 0, s>>>(c->w_x.p, c->w_r.p, c->w_p.p, c->w_q.p, nx, sc);
-    dot(c, c->w_r.p, c->w_r.p, nx, sc + 2);
-    double h[4];
-    VB_CUDA(cudaMemcpyAsync(h, sc, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    VB_CUDA(cudaStreamSynchronize(s));
-    const double rz = h[0], pq = h[1];
-    if (trace)
-      fprintf(stderr, "[vb rank %d] it %d rz %.17g pq %.17g rr %.17g\n", c->rank, it, rz, pq, h[2]);
-    if (!(pq > 0) || !(rz > 0)) { status = VB_EBREAKDOWN; break; }
-    alphas.push_back(rz / pq);
-    rn = sqrt(h[2]);
-    ++it;
-    if (rn <= rtol * r0n || it >= maxit) {
-      if (rn > rtol * r0n) status = VB_ENOTCONV;
-      break;
-    }
+  pcg_init_kernel<<<1, 1, 0, s>>>(sc, rtol, maxit);
+  double h[9];
+  VB_CUDA(cudaMemcpyAsync(h, sc, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  VB_CUDA(cudaStreamSynchronize(s));
+  const double r0n = h[4];
+  if (trace) fprintf(stderr, "[vb rank %d] rr0 %.17g\n", c->rank, h[2]);
+  if (h[7] == 0.0) {
     apply_M(c, st);
-    dot(c, c->w_r.p, c->w_z.p, nx, sc + 3);
-    update_p_kernel<<<grid_for(nx), 256, 0, s>>>(c->w_p.p, c->w_z.p, nx, sc, 0);
-    rotate_rz_kernel<<<1, 1, 0, s>>>(sc, st->hist.p, std::min(it, 4095));
+    dot(c, c->w_r.p, c->w_z.p, nx, sc + 0);
+    update_p_kernel<<<grid_for(nx), 256, 0, s>>>(c->w_p.p, c->w_z.p, nx, sc, 1);
     VB_STAGE();
+    const bool graph = use_graph(c);
+    while (true) {
+      pcg_step(c, st, cudaGraphConditionalHandle{}, false);
+      VB_CUDA(cudaMemcpyAsync(h, sc, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      VB_CUDA(cudaStreamSynchronize(s));
+      if (trace)
+        fprintf(stderr, "[vb rank %d] it %d rz %.17g pq %.17g rr %.17g\n", c->rank, (int)h[6], h[0], h[1], h[2]);
+      if (h[7] != 0.0) break;
+      if (graph) {     // the remaining steps as one graph launch, stopping on the device
+        if (!st->gexec) build_iteration_graph(c, st);
+        VB_CUDA(cudaEventRecord(st->ev_fork, s));
+        VB_CUDA(cudaStreamWaitEvent(st->sg, st->ev_fork, 0));
+        VB_CUDA(cudaGraphLaunch(st->gexec, st->sg));
+        VB_CUDA(cudaEventRecord(st->ev_join, st->sg));
+        VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
+        break;
+      }
+      pcg_mstep(c, st);
+    }
   }
-  // betas from the recorded history
+  VB_CUDA(cudaMemcpyAsync(h, sc, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  VB_CUDA(cudaStreamSynchronize(s));
+  const int it = (int)h[6];
+  const double rn = sqrt(h[2]);
+  const int status = h[7] == 2.0 ? VB_EBREAKDOWN : (h[7] == 3.0 ? VB_ENOTCONV : VB_OK);
+  std::vector<double> alphas, betas;
   {
     std::vector<double> hh(2 * 4096);
     VB_CUDA(cudaMemcpyAsync(hh.data(), st->hist.p, hh.size() * 8, cudaMemcpyDeviceToHost, s));
     VB_CUDA(cudaStreamSynchronize(s));
-    for (int j = 1; j < (int)alphas.size() && j < 4096; ++j) betas.push_back(hh[2 * j + 1]);
+    for (int j = 0; j < it && j < 4096; ++j) alphas.push_back(hh[2 * j]);
+    for (int j = 0; j + 1 < it && j < 4096; ++j) betas.push_back(hh[2 * j + 1]);
   }
   // ---------------- B8: back to original coordinates and back-substitution
   gamma_back_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_gam_free.p, c->d_T.p, c->w_x.p, NDelta,
@@ -1245,8 +1367,8 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   VB_STAGE();
   if (c->nranks > 1) dev_gather(x, c->d_owned_free.p, (int64_t)c->owned_free.size(), x_out, s);
   VB_CUDA(cudaStreamSynchronize(s));
-  collect_times(c, st);
   c->last_iterations = it;
+  collect_times(c, st);
   if (rep) {
     rep->iterations = it;
     rep->converged = status == VB_OK;
