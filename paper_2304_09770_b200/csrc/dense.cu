@@ -7,8 +7,14 @@
 namespace vb {
 
 // ------------------------------------------------------------------ grouped GEMM (DMMA)
-constexpr int GBM = 64, GBN = 64, GBK = 16;
+// CTA tile 128 x 64 x 16, 8 warps (4 along M x 2 along N), warp tile 32 x 32 = 4 x 4 DMMA 8x8x4.
+// The next K-slab is prefetched from global memory into registers while the current one is
+// multiplied out of shared memory (one smem buffer, two barriers per slab).
+constexpr int GBM = 128, GBN = 64, GBK = 16;
 constexpr int GPAD = 4;
+constexpr int GTHREADS = 256;
+constexpr int GA_PER = GBM * GBK / GTHREADS;   // 8
+constexpr int GB_PER = GBK * GBN / GTHREADS;   // 4
 
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -16,10 +22,47 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(128) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
-                                                           const int4 *__restrict__ tiles, int tile0) {
+// element (i, kk) of the op(A) slab / (kk, j) of the op(B) slab handled by thread `tid`, slot q:
+// the index order makes consecutive threads read consecutive addresses for every transpose case
+__device__ __forceinline__ void a_coord(const GemmProb &P, int idx, int &i, int &kk) {
+  if (!P.transA) { i = idx % GBM; kk = idx / GBM; } else { kk = idx % GBK; i = idx / GBK; }
+}
+__device__ __forceinline__ void b_coord(const GemmProb &P, int idx, int &kk, int &j) {
+  if (!P.transB) { kk = idx % GBK; j = idx / GBK; } else { j = idx % GBN; kk = idx / GBN; }
+}
+
+__device__ __forceinline__ void load_slab(const GemmProb &P, int m0, int n0, int k0, int tid, double (&ra)[GA_PER],
+                                          double (&rb)[GB_PER]) {
+#pragma unroll
+  for (int q = 0; q < GA_PER; ++q) {
+    int i, kk;
+    a_coord(P, tid + q * GTHREADS, i, kk);
+    const int gi = m0 + i, gk = k0 + kk;
+    double v = 0.0;
+    if (gi < P.M && gk < P.K) {
+      v = P.transA ? P.A[gk + (int64_t)gi * P.lda] : P.A[gi + (int64_t)gk * P.lda];
+      if (P.d) v *= P.d[(int64_t)gk * P.dstride];
+    }
+    ra[q] = v;
+  }
+#pragma unroll
+  for (int q = 0; q < GB_PER; ++q) {
+    int kk, j;
+    b_coord(P, tid + q * GTHREADS, kk, j);
+    const int gj = n0 + j, gk = k0 + kk;
+    double v = 0.0;
+    if (gj < P.N && gk < P.K) v = P.transB ? P.B[gj + (int64_t)gk * P.ldb] : P.B[gk + (int64_t)gj * P.ldb];
+    rb[q] = v;
+  }
+}
+
+__global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
+                                                                  const int4 *__restrict__ tiles, int tile0) {
   const int4 t = tiles[tile0 + blockIdx.x];
-  const GemmProb P = probs[t.x];
+  __shared__ GemmProb Ps;                 // problem descriptor in shared memory (register pressure)
+  if (threadIdx.x == 0) Ps = probs[t.x];
+  __syncthreads();
+  const GemmProb &P = Ps;
   const int m0 = t.y * GBM, n0 = t.z * GBN;
   __shared__ double As[GBM][GBK + GPAD];
   __shared__ double Bs[GBK][GBN + GPAD];
@@ -30,28 +73,23 @@ __global__ void __launch_bounds__(128) gemm_grouped_kernel(const GemmProb *__res
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double ra[GA_PER], rb[GB_PER];
+  load_slab(P, m0, n0, 0, tid, ra, rb);
   for (int k0 = 0; k0 < P.K; k0 += GBK) {
-    // load op(A) tile [GBM x GBK] (scaled by d) and op(B) tile [GBK x GBN]
-    for (int idx = tid; idx < GBM * GBK; idx += 128) {
+#pragma unroll
+    for (int q = 0; q < GA_PER; ++q) {
       int i, kk;
-      if (!P.transA) { i = idx % GBM; kk = idx / GBM; } else { kk = idx % GBK; i = idx / GBK; }
-      int gi = m0 + i, gk = k0 + kk;
-      double v = 0.0;
-      if (gi < P.M && gk < P.K) {
-        v = P.transA ? P.A[gk + (int64_t)gi * P.lda] : P.A[gi + (int64_t)gk * P.lda];
-        if (P.d) v *= P.d[(int64_t)gk * P.dstride];
-      }
-      As[i][kk] = v;
+      a_coord(P, tid + q * GTHREADS, i, kk);
+      As[i][kk] = ra[q];
     }
-    for (int idx = tid; idx < GBK * GBN; idx += 128) {
-      int j, kk;
-      if (!P.transB) { kk = idx % GBK; j = idx / GBK; } else { j = idx % GBN; kk = idx / GBN; }
-      int gj = n0 + j, gk = k0 + kk;
-      double v = 0.0;
-      if (gj < P.N && gk < P.K) v = P.transB ? P.B[gj + (int64_t)gk * P.ldb] : P.B[gk + (int64_t)gj * P.ldb];
-      Bs[kk][j] = v;
+#pragma unroll
+    for (int q = 0; q < GB_PER; ++q) {
+      int kk, j;
+      b_coord(P, tid + q * GTHREADS, kk, j);
+      Bs[kk][j] = rb[q];
     }
     __syncthreads();
+    if (k0 + GBK < P.K) load_slab(P, m0, n0, k0 + GBK, tid, ra, rb);   // in flight during the DMMAs
 #pragma unroll
     for (int kk = 0; kk < GBK; kk += 4) {
       double a[4], b[4];
@@ -105,7 +143,7 @@ void GemmPlan::upload(cudaStream_t s) {
 void GemmPlan::run(int launch, cudaStream_t s) {
   auto &L = launches[launch];
   if (L.second == 0) return;
-  gemm_grouped_kernel<<<L.second, 128, 0, s>>>(d_probs.p, d_tiles.p, L.first);
+  gemm_grouped_kernel<<<L.second, GTHREADS, 0, s>>>(d_probs.p, d_tiles.p, L.first);
   VB_CHECK_LAUNCH();
 }
 
@@ -182,6 +220,12 @@ __global__ void ldl_panel_kernel(const MatDesc *__restrict__ mats, int j0, int *
   }
 }
 
+// Blocked right-looking LDL^T: 32-column panels factored by ldl_panel_kernel, grouped into wide
+// panels of LDL_NB columns; inside a wide panel only its remaining columns are updated (K = 32), the
+// trailing matrix once per wide panel with K = LDL_NB (DMMA GEMM, 4x fewer passes over the trailing
+// matrix than a 32-column right-looking update).
+constexpr int LDL_NB = 128;
+
 void ldl_partial_batched(const std::vector<MatDesc> &mats, int *info_dev, cudaStream_t s) {
   if (mats.empty()) return;
   DBuf<MatDesc> dm;
@@ -190,31 +234,52 @@ void ldl_partial_batched(const std::vector<MatDesc> &mats, int *info_dev, cudaSt
   int maxm = 0, maxn = 0;
   for (auto &M : mats) { maxm = std::max(maxm, M.m); maxn = std::max(maxn, M.n); }
   GemmPlan plan;
-  for (int j0 = 0; j0 < maxm; j0 += 32) {
-    plan.begin_launch();
+  std::vector<int> intra_launch, trail_launch;   // per 32-panel step / per wide panel
+  for (int J0 = 0; J0 < maxm; J0 += LDL_NB) {
+    for (int j0 = J0; j0 < std::min(J0 + LDL_NB, maxm); j0 += 32) {
+      intra_launch.push_back(plan.begin_launch());
+      for (auto &M : mats) {
+        if (j0 >= M.m) continue;
+        const int nb = std::min(32, M.m - j0);
+        const int Je = std::min(J0 + LDL_NB, M.m);
+        const int rows = M.n - j0 - nb, cols = Je - j0 - nb;
+        if (rows <= 0 || cols <= 0) continue;
+        GemmProb p{};
+        p.A = M.A + (j0 + nb) + (int64_t)j0 * M.ld; p.lda = M.ld; p.transA = 0;
+        p.B = p.A; p.ldb = M.ld; p.transB = 1;
+        p.d = M.A + (int64_t)j0 * (M.ld + 1); p.dstride = M.ld + 1;
+        p.C = M.A + (int64_t)(j0 + nb) * (M.ld + 1); p.ldc = M.ld;
+        p.M = rows; p.N = cols; p.K = nb; p.alpha = -1.0; p.beta = 1.0; p.lower = 1;
+        plan.add(p);
+      }
+    }
+    trail_launch.push_back(plan.begin_launch());
     for (auto &M : mats) {
-      if (j0 >= M.m) continue;
-      int nb = std::min(32, M.m - j0);
-      int rows = M.n - j0 - nb;
+      if (J0 >= M.m) continue;
+      const int Je = std::min(J0 + LDL_NB, M.m);
+      const int rows = M.n - Je;
       if (rows <= 0) continue;
       GemmProb p{};
-      p.A = M.A + (j0 + nb) + (int64_t)j0 * M.ld; p.lda = M.ld; p.transA = 0;
+      p.A = M.A + Je + (int64_t)J0 * M.ld; p.lda = M.ld; p.transA = 0;
       p.B = p.A; p.ldb = M.ld; p.transB = 1;
-      p.d = M.A + (int64_t)j0 * (M.ld + 1); p.dstride = M.ld + 1;
-      p.C = M.A + (int64_t)(j0 + nb) * (M.ld + 1); p.ldc = M.ld;
-      p.M = p.N = rows; p.K = nb; p.alpha = -1.0; p.beta = 1.0; p.lower = 1;
+      p.d = M.A + (int64_t)J0 * (M.ld + 1); p.dstride = M.ld + 1;
+      p.C = M.A + (int64_t)Je * (M.ld + 1); p.ldc = M.ld;
+      p.M = p.N = rows; p.K = Je - J0; p.alpha = -1.0; p.beta = 1.0; p.lower = 1;
       plan.add(p);
     }
   }
   plan.upload(s);
-  int step = 0;
-  for (int j0 = 0; j0 < maxm; j0 += 32, ++step) {
-    ldl_panel_kernel<<<dim3(1, mats.size()), 128, 0, s>>>(dm.p, j0, info_dev, 0);
-    VB_CHECK_LAUNCH();
-    dim3 grid((maxn - j0 + 31) / 32, mats.size());
-    ldl_panel_kernel<<<grid, 32, 0, s>>>(dm.p, j0, info_dev, 1);
-    VB_CHECK_LAUNCH();
-    plan.run(step, s);
+  int step = 0, wide = 0;
+  for (int J0 = 0; J0 < maxm; J0 += LDL_NB, ++wide) {
+    for (int j0 = J0; j0 < std::min(J0 + LDL_NB, maxm); j0 += 32, ++step) {
+      ldl_panel_kernel<<<dim3(1, mats.size()), 128, 0, s>>>(dm.p, j0, info_dev, 0);
+      VB_CHECK_LAUNCH();
+      dim3 grid((maxn - j0 + 31) / 32, mats.size());
+      ldl_panel_kernel<<<grid, 32, 0, s>>>(dm.p, j0, info_dev, 1);
+      VB_CHECK_LAUNCH();
+      plan.run(intra_launch[step], s);
+    }
+    plan.run(trail_launch[wide], s);
   }
   VB_CUDA(cudaStreamSynchronize(s));
 }
@@ -264,6 +329,7 @@ void tri_inverse_batched(const std::vector<TriDesc> &mats, cudaStream_t s) {
   dm.upload(hm, s);
   int maxm = 0;
   for (auto &T : mats) maxm = std::max(maxm, T.m);
+  if (maxm == 0) return;
   set_identity_kernel<<<dim3((maxm + 255) / 256, mats.size()), 256, 0, s>>>(dm.p);
   VB_CHECK_LAUNCH();
   int nblk = (maxm + 31) / 32;
@@ -308,6 +374,7 @@ void symmetrize_lower_batched(const std::vector<MatDesc> &mats, cudaStream_t s) 
   dm.upload(hm, s);
   int maxn = 0;
   for (auto &M : mats) maxn = std::max(maxn, M.n);
+  if (maxn == 0) return;
   int nt = (maxn + 31) / 32;
   symmetrize_kernel<<<dim3(nt, nt, mats.size()), dim3(32, 32), 0, s>>>(dm.p);
   VB_CHECK_LAUNCH();
@@ -319,14 +386,22 @@ __global__ void pack_tiles_kernel(const PackDesc *__restrict__ mats) {
   const int I = blockIdx.y, J = blockIdx.x;
   if (J > I) return;
   if (32 * I >= M.n) return;
-  double *out = M.out + ((int64_t)I * (I + 1) / 2 + J) * 1024;
-  for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
-    int r = idx >> 5, cc = idx & 31;
-    int row = 32 * I + r, col = 32 * J + cc;
-    double v = 0.0;
-    if (row < M.n && col < M.n)
-      v = row >= col ? M.A[row + (int64_t)col * M.ld] : M.A[col + (int64_t)row * M.ld];
-    out[idx] = v;
+  const int rows = min(32, M.n - 32 * I);
+  double *out = M.out + ptile_off(M.n, I, J);
+  if (J < I) {
+    for (int idx = threadIdx.x; idx < rows * 32; idx += blockDim.x) {
+      const int r = idx >> 5, cc = idx & 31;
+      const int row = 32 * I + r, col = 32 * J + cc;
+      out[idx] = M.A[row + (int64_t)col * M.ld];   // row > col: lower triangle
+    }
+  } else {   // diagonal tile: lower triangle, row r holds columns 0..r
+    for (int idx = threadIdx.x; idx < rows * (rows + 1) / 2; idx += blockDim.x) {
+      int r = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+      while (r * (r + 1) / 2 > idx) --r;
+      while ((r + 1) * (r + 2) / 2 <= idx) ++r;
+      const int cc = idx - r * (r + 1) / 2;
+      out[idx] = M.A[(32 * I + r) + (int64_t)(32 * J + cc) * M.ld];
+    }
   }
 }
 
@@ -337,6 +412,7 @@ void pack_tiles_batched(const std::vector<PackDesc> &mats, cudaStream_t s) {
   dm.upload(hm, s);
   int maxn = 0;
   for (auto &M : mats) maxn = std::max(maxn, M.n);
+  if (maxn == 0) return;
   int nt = (maxn + 31) / 32;
   pack_tiles_kernel<<<dim3(nt, nt, mats.size()), 256, 0, s>>>(dm.p);
   VB_CHECK_LAUNCH();

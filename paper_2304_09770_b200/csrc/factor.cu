@@ -219,6 +219,16 @@ __global__ void transpose_slot_kernel(const SlotDev *__restrict__ slots, const i
   }
 }
 
+// rows [lo, lo + rows) of the symmetric matrix whose lower triangle is in A (column-major, n x n),
+// row-major into out (zero rows past n)
+__global__ void coarse_rows_kernel(const double *__restrict__ A, int64_t n, int64_t lo, int64_t rows, double *out) {
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const int64_t i = lo + r;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+      out[r * n + j] = i >= n ? 0.0 : (i >= j ? A[i + j * n] : A[j + i * n]);
+  }
+}
+
 __global__ void recip_diag_kernel(const double *A, int64_t ld, int n, double *out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = 1.0 / A[i + i * ld];
 }
@@ -360,8 +370,8 @@ static void layout_phase_b(vb_ctx *c, const std::vector<int> &rank) {
     c->subs[i].nd = nd; c->subs[i].npi = npi;
     S.off_Dv = offDv; offDv += nd;
     S.off_Pi = offPi; offPi += npi;
-    S.off_STp = STp; STp += packed_tiles(S.nG) * 1024;
-    S.off_SDi = SDi; SDi += packed_tiles(nd) * 1024;
+    S.off_STp = STp; STp += packed_size(S.nG);
+    S.off_SDi = SDi; SDi += packed_size(nd);
     S.off_Phi = Phi; Phi += (int64_t)nd * npi;
   }
   c->len_Dv = offDv; c->len_Pi = offPi; c->len_STp = STp; c->len_SDi = SDi; c->len_Phi = Phi;
@@ -405,7 +415,7 @@ static void stage_dirichlet(vb_ctx *c) {
       const SubDev &S = c->h_sub[i];
       offWD[i] = lenWD; lenWD += (int64_t)S.nD * S.nD;
       offPsi[i] = lenPsi; lenPsi += (int64_t)S.nG * S.nD;
-      offKDi[i] = lenKDi; lenKDi += packed_tiles(S.nD) * 1024;
+      offKDi[i] = lenKDi; lenKDi += packed_size(S.nD);
       c->h_sub[i].off_Psi = offPsi[i];
       c->h_sub[i].off_KDi = offKDi[i];
     }
@@ -483,7 +493,8 @@ static void stage_interface(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumb
   drank.alloc(c->ents.size());
   double tol = c->cons.svd_rel_tol > 0 ? c->cons.svd_rel_tol : 1e-10;
   if (c->cons.svd_rel_tol < 0) tol = 1e-10;
-  entity_basis_kernel<<<c->ents.size(), 128, 0, s>>>(c->d_ent.p, c->d_C.p, c->d_T.p, wq.p, drank.p, tol);
+  if (!c->ents.empty())
+    entity_basis_kernel<<<c->ents.size(), 128, 0, s>>>(c->d_ent.p, c->d_C.p, c->d_T.p, wq.p, drank.p, tol);
   VB_STAGE();
   std::vector<int> rank;
   drank.download(rank, s);
@@ -831,8 +842,20 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     plan.upload(s);
     plan.run(l0, s);
     sync(c);
-    c->d_Kcp.alloc(packed_tiles(Nc) * 1024);
-    pack_tiles_batched({PackDesc{Kc.p, (int)Nc, (int)Nc, c->d_Kcp.p}}, s);
+    if (c->nranks == 1) {
+      c->d_Kcp.alloc(packed_size(Nc));
+      pack_tiles_batched({PackDesc{Kc.p, (int)Nc, (int)Nc, c->d_Kcp.p}}, s);
+    } else {
+      // distributed coarse solve: this rank keeps rows [lo, lo + rows) of the (replicated) inverse,
+      // row-major, zero-padded to ceil(Nc / nranks) rows; u_c = allgather of the row blocks (C2)
+      const int64_t rows = (Nc + c->nranks - 1) / c->nranks;
+      c->coarse_rows = rows;
+      c->coarse_lo = std::min<int64_t>(Nc, rows * c->rank);
+      c->d_Kcr.alloc(rows * Nc);
+      coarse_rows_kernel<<<dim3(64, (unsigned)std::min<int64_t>(rows, 65535)), 256, 0, s>>>(
+          Kc.p, Nc, c->coarse_lo, rows, c->d_Kcr.p);
+      VB_STAGE();
+    }
   }
   sync(c);
   double fv;

@@ -8,6 +8,12 @@
 #include "../../include/vbddc.h"
 #include "comm.h"
 
+#ifdef __CUDACC__
+#define HD_INLINE __host__ __device__ __forceinline__
+#else
+#define HD_INLINE inline
+#endif
+
 namespace vb {
 
 struct Error {
@@ -80,10 +86,20 @@ struct GemmProb {
 };
 
 // ------------------------------------------------------------------ packed symmetric tiles
-// Lower-triangular 32x32 tiles (I >= J) in row-of-tiles order, each tile row-major, zero padded.
-inline int64_t packed_tiles(int n) {
-  int64_t nt = (n + 31) / 32;
-  return nt * (nt + 1) / 2;
+// Lower triangle of a symmetric n x n matrix as 32x32 tiles (I >= J) in row-of-tiles order, each
+// tile row-major; diagonal tiles store only their lower triangle (row r: r+1 entries) and the tiles
+// of the last tile row only its rv = n - 32 (nt - 1) valid rows -- nothing but the matrix is stored.
+HD_INLINE int64_t ptile_row_start(int64_t I) { return 1024 * (I * (I - 1) / 2) + 528 * I; }
+HD_INLINE int64_t ptile_off(int n, int I, int J) {   // offset of tile (I, J), J <= I
+  const int nt = (n + 31) / 32;
+  const int64_t rows = (I == nt - 1) ? n - 32 * (nt - 1) : 32;
+  return ptile_row_start(I) + (int64_t)J * rows * 32;
+}
+HD_INLINE int64_t packed_size(int n) {               // doubles
+  if (n <= 0) return 0;
+  const int nt = (n + 31) / 32;
+  const int64_t rv = n - 32 * (nt - 1);
+  return ptile_row_start(nt - 1) + (int64_t)(nt - 1) * rv * 32 + rv * (rv + 1) / 2;
 }
 
 struct GEnt {                  // global interface entity (every rank holds the whole list)
@@ -302,4 +318,6 @@ struct vb_ctx {
   std::vector<int64_t> owned_free;   // ABI layout: owned free DOF ids (global free numbering)
   vb::DBuf<int64_t> d_owned_free;
   vb::DBuf<double> w_rhsg, w_xg;     // global-layout free vectors (nranks > 1)
+  vb::DBuf<double> d_Kcr;            // distributed coarse: this rank's rows of the coarse inverse
+  int64_t coarse_rows = 0, coarse_lo = 0;
 };

@@ -65,24 +65,33 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
   }
   __syncthreads();
   for (int I = W.r0; I < W.r1; ++I) {
-    const double *rowbase = W.M + ((int64_t)I * (I + 1) / 2) * 1024;
+    const int rows = (I == nt - 1) ? n - 32 * (nt - 1) : 32;    // short last tile row
     double rsum[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) rsum[r] = 0.0;
     const double xI_lane = X(32 * I + lane);
     for (int J = warp; J <= I; J += GV_WARPS) {
-      const double *T = rowbase + (int64_t)J * 1024;
+      const double *T = W.M + ptile_off(n, I, J);
       double t[32];
+      if (J < I) {
 #pragma unroll
-      for (int r = 0; r < 32; ++r) t[r] = __ldg(T + r * 32 + lane);
+        for (int r = 0; r < 32; ++r) t[r] = r < rows ? __ldg(T + r * 32 + lane) : 0.0;
+      } else {     // diagonal tile, lower triangle only: row r holds columns 0..r
+#pragma unroll
+        for (int r = 0; r < 32; ++r) t[r] = (r < rows && lane <= r) ? __ldg(T + r * (r + 1) / 2 + lane) : 0.0;
+      }
       const double xJ = X(32 * J + lane);
-      double csum = 0.0;
+      double csum = 0.0, dval = 0.0;
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         rsum[r] += t[r] * xJ;
         csum += t[r] * __shfl_sync(FULL, xI_lane, r);
+        if (r == lane) dval = t[r];
       }
-      if (J < I && (!BIG || 32 * J + lane < n)) ys[32 * J + lane] += csum;   // transpose part, one warp per J
+      // transposed part (one warp per J): entries (r, lane) add to output lane; on the diagonal tile
+      // the stored triangle is transposed without its diagonal
+      if (J == I) csum -= dval * xI_lane;
+      if (!BIG || 32 * J + lane < n) ys[32 * J + lane] += csum;
     }
     // transpose-reduce rsum across lanes: lane l ends with sum over lanes of rsum[l]
 #pragma unroll
@@ -132,6 +141,21 @@ static void split_rows(int n, int P, std::vector<std::pair<int, int>> &out, doub
     r = r1;
   }
   while ((int)out.size() < P) out.push_back({nt, nt});
+}
+
+// distributed coarse solve: y = K_rows x for this rank's rows (row-major), warp per row
+__global__ void __launch_bounds__(256) rows_gemv_kernel(const double *__restrict__ K, int64_t rows, int64_t n,
+                                                        const double *__restrict__ x, double *y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const double *row = K + r * n;
+  double a0 = 0.0, a1 = 0.0;
+  int64_t j = lane;
+  for (; j + 32 < n; j += 64) { a0 += __ldg(row + j) * __ldg(x + j); a1 += __ldg(row + j + 32) * __ldg(x + j + 32); }
+  for (; j < n; j += 32) a0 += __ldg(row + j) * __ldg(x + j);
+  const double v = warp_sum(a0 + a1);
+  if (lane == 0) y[r] = v;
 }
 
 // ------------------------------------------------------------------ small kernels of the loop
@@ -262,6 +286,20 @@ __global__ void update_xr_rr_kernel(double *x, double *r, const double *p, const
     v += mask ? mask[i] * (ri * ri) : ri * ri;
   }
   block_reduce_last(v, part, ticket, dst);
+}
+
+// p0 block of the condensed rhs: the compatibility sum_i g0_i = 0 holds up to rounding; remove the
+// rounding (mode 0: local sum into *acc; mode 1: subtract acc[0] / n_total from every entry)
+__global__ void p0_compat_kernel(double *p0, int n, double *acc, int mode, int n_total) {
+  if (mode == 0) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) v += p0[i];
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *acc = v;
+  } else {
+    const double mean = *acc / n_total;
+    for (int i = threadIdx.x; i < n; i += 32) p0[i] -= mean;
+  }
 }
 
 // scal: [0] rz [1] pq [2] rr [3] rz_new [4] r0n [5] rtol*r0n [6] it [7] status [8] maxit
@@ -646,6 +684,7 @@ struct SolveState {
   DBuf<double> sx;                   // [s (len_G) | received copies]
   DBuf<double> tx;                   // [slot products | received]
   DBuf<double> cbuf, cgath;          // coarse pieces (local), gathered (nranks x cmax)
+  DBuf<double> ucl;                  // distributed coarse: this rank's rows of u_c
   DBuf<double> gam2, gbuf, hbuf;     // B0: entity-major b_e; [zG | received]; DOF halo receive
   int64_t cmax = 0, len_t = 0;
   SlotExchange XS, XE, XB, XH, XR;   // apply_S copies, extension products, B0 zG, DOF halo, rank partials
@@ -735,7 +774,7 @@ static void dot(vb_ctx *c, const double *a, const double *b, int64_t n, double *
   allreduce_sum_fixed(c, dst, 1);
 }
 
-static int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 8); }
+static int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
 
 static void apply_S(vb_ctx *c, SolveState *st) {   // q = S^ p  (B1, B2)
   cudaStream_t s = c->stream;
@@ -792,12 +831,20 @@ static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   gather_src_kernel<<<grid_for(c->Nc), 256, 0, s2>>>(st->pptr.p, st->pidx.p, pieces, c->Nc, c->w_rc.p);
   coarse_p0_project_kernel<<<1, 256, 0, s2>>>(st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
   tick(c, st, 2, true, s2);
+  if (c->nranks > 1) {
+    // rows of the coarse inverse owned here, then the allgather of the row blocks (C2)
+    rows_gemv_kernel<<<(unsigned)((c->coarse_rows + 7) / 8), 256, 0, s2>>>(c->d_Kcr.p, c->coarse_rows, c->Nc, c->w_rc.p,
+                                                                        st->ucl.p);
+    tick(c, st, 2, false, s2);
+    c->comm->allgather(st->ucl.p, c->w_uc.p, c->coarse_rows, s2);
+  } else {
   if (st->big_c)
     sym_gemv_kernel<GV_WARPS_C, true><<<st->nw_c, GV_WARPS_C * 32, GV_WARPS_C * 32 * sizeof(double), s2>>>(st->w_c.p);
   else
     sym_gemv_kernel<GV_WARPS_C><<<st->nw_c, GV_WARPS_C * 32, st->sm_c, s2>>>(st->w_c.p);
   tick(c, st, 2, false, s2);
   sum_chunks_kernel<<<(c->Nc + 31) / 32, 256, 0, s2>>>(c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
+  }
   coarse_p0_project_kernel<<<1, 256, 0, s2>>>(st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
   VB_CUDA(cudaEventRecord(st->ev_join, s2));
   VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
@@ -842,7 +889,8 @@ void prepare_solve(vb_ctx *c) {
   c->w_part.alloc((int64_t)c->P_op * std::max<int64_t>(c->len_G, 1));
   c->w_locD.alloc(std::max<int64_t>(c->len_Dv, 1));
   c->w_locY.alloc((int64_t)c->P_loc * std::max<int64_t>(c->len_Dv, 1));
-  c->w_uc.alloc(c->Nc); c->w_rc.alloc(c->Nc);
+  c->w_uc.alloc(std::max<int64_t>(c->Nc, c->coarse_rows * c->nranks)); c->w_rc.alloc(c->Nc);
+  if (c->nranks > 1) st->ucl.alloc(std::max<int64_t>(c->coarse_rows, 1));
   c->w_scal.alloc(16); c->w_scal.zero(s);
   st->ticket.alloc(4); st->ticket.zero(s);
   if (!st->s2) {
@@ -884,12 +932,12 @@ void prepare_solve(vb_ctx *c) {
   c->w_locY.zero(s);
   st->w_loc.upload(wl, s); st->nw_loc = wl.size(); st->sm_loc = gemv_smem(nmaxD);
   wl.clear();
-  int Pc = std::max(1, std::min<int>(c->P_c, (int)((c->Nc + 31) / 32)));
-  c->w_ucp.alloc((int64_t)Pc * c->Nc);
+  int Pc = c->nranks > 1 ? 0 : std::max(1, std::min<int>(c->P_c, (int)((c->Nc + 31) / 32)));
+  c->w_ucp.alloc(std::max<int64_t>((int64_t)Pc * c->Nc, 1));
   split_rows(c->Nc, Pc, rows, 4.0);
   for (int q = 0; q < Pc; ++q)
     wl.push_back(GemvWork{c->d_Kcp.p, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, rows[q].first, rows[q].second, 0});
-  st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = gemv_smem(c->Nc, GV_WARPS_C);
+  st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = c->nranks > 1 ? 0 : gemv_smem(c->Nc, GV_WARPS_C);
   st->big_c = st->sm_c > 200 * 1024;
   size_t smmax = std::max(st->sm_op, st->sm_loc);
   VB_REQUIRE(smmax <= 227 * 1024, VB_EINVAL, "packed GEMV vector exceeds shared memory (subdomain interface too large)");
@@ -1114,10 +1162,10 @@ void prepare_solve(vb_ctx *c) {
   // bytes per PCG iteration (model of the streamed operators)
   double b = 0;
   for (auto &S : c->h_sub) {
-    b += 8.0 * packed_tiles(S.nG) * 1024 + 8.0 * packed_tiles(S.nd) * 1024 + 2 * 8.0 * S.nd * S.npi;
+    b += 8.0 * packed_size(S.nG) + 8.0 * packed_size(S.nd) + 2 * 8.0 * S.nd * S.npi;
   }
   for (auto &sl : c->h_slot) b += 2 * 8.0 * sl.nd * sl.nd;
-  b += 8.0 * packed_tiles(c->Nc) * 1024;
+  b += c->nranks > 1 ? 8.0 * c->coarse_rows * c->Nc : 8.0 * packed_size(c->Nc);
   c->bytes_per_iter = b;
 }
 
@@ -1298,7 +1346,11 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   dev_gather(rhs, c->d_gam_free.p, c->nGamma, st->gam2.p, s);                // b_e (entity-major)
   run_slot_exchange(c, st->XB, st->gbuf.p, st->gbuf.p + c->len_G);          // C1 (cross-rank zG)
   run_entity_sum(c, st->ESB, st->gbuf.p, c->w_gam.p, st->gam2.p);             // ghat = b + sum_m zG^(m)
-  gamma_rhs_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_T.p, c->w_gam.p, NDelta, c->w_r.p);
+  if (!c->h_ent.empty())
+    gamma_rhs_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_T.p, c->w_gam.p, NDelta, c->w_r.p);
+  p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + 220, 0, c->Ng);
+  allreduce_sum_fixed(c, c->w_dots.p + 220, 1);
+  p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + 220, 1, c->Ng);
   VB_STAGE();
   // ---------------- PCG (SURVEY O-15), iterations driven on the device (scal[6] = it, scal[7] = status)
   c->w_x.zero(s);
@@ -1349,7 +1401,8 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
     for (int j = 0; j + 1 < it && j < 4096; ++j) betas.push_back(hh[2 * j + 1]);
   }
   // ---------------- B8: back to original coordinates and back-substitution
-  gamma_back_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_gam_free.p, c->d_T.p, c->w_x.p, NDelta,
+  if (!c->h_ent.empty())
+    gamma_back_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_gam_free.p, c->d_T.p, c->w_x.p, NDelta,
                                                     c->w_gam.p, x);
   VB_STAGE();
   xD_kernel<<<dim3(XD_SPLIT, N), 256, maxnG * 8, s>>>(c->d_sub.p, c->d_Psi.p, c->w_yDp.p, c->len_Dn, c->P_kd,

@@ -1,0 +1,105 @@
+"""Edge and degenerate cases of the GPU path: a single subdomain (no interface),
+every interface DOF primal (M^-1 = S^-1, one iteration), multiplicity scaling
+(Eq.(pseudoinv)) against the oracle, the exact viscosity invariance nu -> c nu (F9),
+maxit reached (VB_ENOTCONV, "NC" P:1233) and out-of-order calls."""
+import numpy as np
+import pytest
+
+from synthetic import make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_solve(prob, rtol=1e-10, maxit=2000, raise_on_error=True, **kw):
+    import torch
+    import paper_2304_09770_b200 as vb
+    ctx = vb.context_for(prob, **kw)
+    ctx.factor()
+    rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+    ctx.build_rhs(vb.problem_args(prob), rhs)
+    x = torch.zeros_like(rhs)
+    rep = ctx.pcg_solve(rhs, x, rtol=rtol, maxit=maxit, raise_on_error=raise_on_error)
+    return ctx, rhs, x, rep
+
+
+def test_single_subdomain_direct():
+    """One subdomain: no interface, the coarse problem is the single p0 (gauge-fixed to 0); the
+    solve is the back-substitution alone and must equal the dense direct solve of Eq.(MatrixForm)."""
+    import torch
+    from oracle.assemble import GlobalSystem
+    prob = make_problem("c1", sub=(4, 4, 4))
+    assert int(prob.cell_subdomain.max()) == 0
+    ctx, rhs, x, rep = _gpu_solve(prob)
+    assert rep["iterations"] == 0 and rep["status"] == "OK"
+    gs = GlobalSystem(prob)
+    u, p = gs.direct_solve()
+    xh = x.cpu().numpy()
+    assert np.linalg.norm(xh[:ctx.n_vel] - u) <= 1e-10 * np.linalg.norm(u)
+    assert np.linalg.norm(xh[ctx.n_vel:] - p) <= 1e-10 * np.linalg.norm(p)
+
+
+def test_all_primal_exact_limit():
+    """Every interface DOF primal: S~ = S^, so M^-1 S^ = I on the benign space and CG stops after
+    one step; the oracle does the same."""
+    from oracle.assemble import GlobalSystem
+    from oracle.bddc import BDDC
+    prob = make_problem("c1")
+    ctx, rhs, x, rep = _gpu_solve(prob, constraints=dict(all_primal=1))
+    assert rep["iterations"] == 1
+    u_o, p_o, rep_o = BDDC(GlobalSystem(prob), constraints=dict(all_primal=1)).solve()
+    assert rep_o["iterations"] == 1
+    xh = x.cpu().numpy()
+    assert np.linalg.norm(xh[:ctx.n_vel] - u_o) <= 1e-8 * np.linalg.norm(u_o)
+
+
+@pytest.mark.parametrize("name,kw", [("c1", {}), ("c1", dict(n=8))])
+def test_multiplicity_scaling_parity(name, kw):
+    import paper_2304_09770_b200 as vb
+    from oracle.assemble import GlobalSystem
+    from oracle.bddc import BDDC
+    prob = make_problem(name, **kw)
+    ctx, rhs, x, rep = _gpu_solve(prob, constraints=dict(scaling=vb.VB_MULTIPLICITY))
+    u_o, p_o, rep_o = BDDC(GlobalSystem(prob), scaling="multiplicity").solve()
+    assert abs(rep["iterations"] - rep_o["iterations"]) <= 1
+    assert abs(rep["kappa"] - rep_o["kappa"]) <= 0.01 * rep_o["kappa"]
+    xh = x.cpu().numpy()
+    assert np.linalg.norm(xh[:ctx.n_vel] - u_o) <= 1e-8 * np.linalg.norm(u_o)
+    assert np.linalg.norm(xh[ctx.n_vel:] - p_o) <= 1e-8 * np.linalg.norm(p_o)
+
+
+def test_viscosity_scaling_invariance():
+    """F9: nu -> 1000 nu with the same rhs: identical iterations and kappa, u / 1000, p unchanged."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    p1 = make_problem("c1", n=8)
+    p2 = make_problem("c1", n=8, nu=1000.0)
+    c1, rhs, x1, r1 = _gpu_solve(p1)
+    c2 = vb.context_for(p2)
+    c2.factor()
+    x2 = torch.zeros_like(rhs)
+    r2 = c2.pcg_solve(rhs, x2, rtol=1e-10)
+    assert r1["iterations"] == r2["iterations"]
+    assert abs(r1["kappa"] - r2["kappa"]) <= 1e-8 * r1["kappa"]
+    a, b = x1.cpu().numpy(), x2.cpu().numpy()
+    nv = c1.n_vel
+    assert np.linalg.norm(a[:nv] - 1000.0 * b[:nv]) <= 1e-9 * np.linalg.norm(a[:nv])
+    assert np.linalg.norm(a[nv:] - b[nv:]) <= 1e-9 * np.linalg.norm(a[nv:])
+
+
+def test_maxit_and_state_errors():
+    import torch
+    import paper_2304_09770_b200 as vb
+    prob = make_problem("c1", n=8)
+    ctx = vb.context_for(prob)
+    rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+    x = torch.zeros_like(rhs)
+    with pytest.raises(vb.VBError) as e:     # solve before factor
+        ctx.pcg_solve(rhs, x)
+    assert e.value.status == vb.VB_ESTATE
+    ctx.factor()
+    ctx.build_rhs(vb.problem_args(prob), rhs)
+    rep = ctx.pcg_solve(rhs, x, rtol=1e-14, maxit=3, raise_on_error=False)
+    assert rep["status"] == "ENOTCONV" and rep["iterations"] == 3
+    assert rep["rel_residual"] > 1e-14
+    rep = ctx.pcg_solve(rhs, x, rtol=1e-10)          # the context is still usable
+    assert rep["status"] == "OK"

@@ -57,7 +57,7 @@ def _worker(rank, world, port, name, kw, rank_grid, q):
 
 
 @pytest.mark.parametrize("name,kw,rank_grid", [("c1", dict(n=8), (1, 1, 2)), ("c1", dict(n=8), (2, 2, 1)),
-                                              ("c3", dict(n=8), (1, 2, 1))])
+                                              ("c3", dict(n=8), (1, 2, 1)), ("c1", dict(n=8), (2, 2, 2))])
 def test_exchange_plans_agree_across_ranks(name, kw, rank_grid):
     world = int(np.prod(rank_grid))
     ctx = mp.get_context("spawn")

@@ -9,11 +9,14 @@ def main(path):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     tot = 0.0
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
     for r in rows[hi + 1:]:
         if len(r) <= vi:
+            continue
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
             continue
         name = r[ki].split("(")[0].replace("void ", "")
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)

@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 N_SAMPLE = 20000
 
 
-def make(name):
+def make(name, outdir=None):
     from synthetic import make_problem
     from oracle.assemble import GlobalSystem
     from oracle.bddc import BDDC
@@ -33,7 +33,7 @@ def make(name):
     x = np.concatenate([u, p])
     rng = np.random.default_rng(12345)
     idx = np.sort(rng.choice(x.size, min(N_SAMPLE, x.size), replace=False)).astype(np.int64)
-    out = os.path.join(ROOT, "tests", "golden", "oracle_%s_full.npz" % name)
+    out = os.path.join(outdir or os.path.join(ROOT, "tests", "golden"), "oracle_%s_full.npz" % name)
     meta = dict(config=name, iterations=int(rep["iterations"]), kappa=float(rep["kappa"]),
                 lambda_min=float(rep["lambda_min"]), n_primal=int(bd.NPi), n_coarse=int(bd.NPi + bd.N),
                 n_adaptive=int(getattr(bd, "adaptive_count", 0)),
@@ -49,5 +49,12 @@ def make(name):
 
 
 if __name__ == "__main__":
-    for name in sys.argv[1:] or ["c2", "c3", "c4"]:
-        make(name)
+    args = sys.argv[1:]
+    outdir = None
+    if "--out" in args:
+        i = args.index("--out")
+        outdir = args[i + 1]
+        del args[i:i + 2]
+        os.makedirs(outdir, exist_ok=True)
+    for name in args or ["c2", "c3", "c4"]:
+        make(name, outdir)
