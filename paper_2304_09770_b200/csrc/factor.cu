@@ -219,16 +219,6 @@ __global__ void transpose_slot_kernel(const SlotDev *__restrict__ slots, const i
   }
 }
 
-// rows [lo, lo + rows) of the symmetric matrix whose lower triangle is in A (column-major, n x n),
-// row-major into out (zero rows past n)
-__global__ void coarse_rows_kernel(const double *__restrict__ A, int64_t n, int64_t lo, int64_t rows, double *out) {
-  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
-    const int64_t i = lo + r;
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-      out[r * n + j] = i >= n ? 0.0 : (i >= j ? A[i + j * n] : A[j + i * n]);
-  }
-}
-
 __global__ void recip_diag_kernel(const double *A, int64_t ld, int n, double *out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = 1.0 / A[i + i * ld];
 }
@@ -832,28 +822,41 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     dc.alloc(Nc);
     recip_diag_kernel<<<(Nc + 255) / 256, 256, 0, s>>>(Kc.p, Nc, Nc, dc.p);
     VB_STAGE();
-    GemmPlan plan;
-    int l0 = plan.begin_launch();
-    GemmProb p{};
-    p.A = Wc.p; p.lda = Nc; p.transA = 1; p.d = dc.p; p.dstride = 1;
-    p.B = Wc.p; p.ldb = Nc; p.C = Kc.p; p.ldc = Nc;
-    p.M = p.N = p.K = Nc; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
-    plan.add(p);
-    plan.upload(s);
-    plan.run(l0, s);
-    sync(c);
     if (c->nranks == 1) {
+      // (K_c)^-1 = W^T D^-1 W (lower), packed
+      GemmPlan plan;
+      int l0 = plan.begin_launch();
+      GemmProb p{};
+      p.A = Wc.p; p.lda = Nc; p.transA = 1; p.d = dc.p; p.dstride = 1;
+      p.B = Wc.p; p.ldb = Nc; p.C = Kc.p; p.ldc = Nc;
+      p.M = p.N = p.K = Nc; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
+      plan.add(p);
+      plan.upload(s);
+      plan.run(l0, s);
+      sync(c);
       c->d_Kcp.alloc(packed_size(Nc));
       pack_tiles_batched({PackDesc{Kc.p, (int)Nc, (int)Nc, c->d_Kcp.p}}, s);
     } else {
-      // distributed coarse solve: this rank keeps rows [lo, lo + rows) of the (replicated) inverse,
-      // row-major, zero-padded to ceil(Nc / nranks) rows; u_c = allgather of the row blocks (C2)
+      // distributed coarse solve: this rank computes and keeps only rows [lo, lo + rows) of the
+      // inverse, (W[:, lo:hi])^T D^-1 W, column-major rows x N_c (zero rows past N_c); the
+      // solve is a row-block GEMV and an allgather of the row blocks (C2)
       const int64_t rows = (Nc + c->nranks - 1) / c->nranks;
       c->coarse_rows = rows;
       c->coarse_lo = std::min<int64_t>(Nc, rows * c->rank);
       c->d_Kcr.alloc(rows * Nc);
-      coarse_rows_kernel<<<dim3(64, (unsigned)std::min<int64_t>(rows, 65535)), 256, 0, s>>>(
-          Kc.p, Nc, c->coarse_lo, rows, c->d_Kcr.p);
+      c->d_Kcr.zero(s);
+      const int64_t mine = std::min<int64_t>(rows, Nc - c->coarse_lo);
+      if (mine > 0) {
+        GemmPlan plan;
+        int l0 = plan.begin_launch();
+        GemmProb p{};
+        p.A = Wc.p + c->coarse_lo * Nc; p.lda = Nc; p.transA = 1; p.d = dc.p; p.dstride = 1;
+        p.B = Wc.p; p.ldb = Nc; p.C = c->d_Kcr.p; p.ldc = rows;
+        p.M = mine; p.N = Nc; p.K = Nc; p.alpha = 1.0; p.beta = 0.0;
+        plan.add(p);
+        plan.upload(s);
+        plan.run(l0, s);
+      }
       VB_STAGE();
     }
   }

@@ -143,19 +143,26 @@ static void split_rows(int n, int P, std::vector<std::pair<int, int>> &out, doub
   while ((int)out.size() < P) out.push_back({nt, nt});
 }
 
-// distributed coarse solve: y = K_rows x for this rank's rows (row-major), warp per row
+// distributed coarse solve: y = K_rows x for this rank's rows (column-major rows x n), thread per
+// row (consecutive threads read consecutive addresses), 4 independent accumulators
+// (blockIdx.y: column chunk, partial sums y[chunk * rows + r], summed in chunk order afterwards)
 __global__ void __launch_bounds__(256) rows_gemv_kernel(const double *__restrict__ K, int64_t rows, int64_t n,
                                                         const double *__restrict__ x, double *y) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= rows) return;
-  const double *row = K + r * n;
-  double a0 = 0.0, a1 = 0.0;
-  int64_t j = lane;
-  for (; j + 32 < n; j += 64) { a0 += __ldg(row + j) * __ldg(x + j); a1 += __ldg(row + j + 32) * __ldg(x + j + 32); }
-  for (; j < n; j += 32) a0 += __ldg(row + j) * __ldg(x + j);
-  const double v = warp_sum(a0 + a1);
-  if (lane == 0) y[r] = v;
+  const int64_t cw = (n + gridDim.y - 1) / gridDim.y;
+  const int64_t j0 = blockIdx.y * cw, j1 = min(n, j0 + cw);
+  y += blockIdx.y * rows;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t j = j0;
+  for (; j + 3 < j1; j += 4) {
+    a0 += __ldg(K + r + j * rows) * __ldg(x + j);
+    a1 += __ldg(K + r + (j + 1) * rows) * __ldg(x + j + 1);
+    a2 += __ldg(K + r + (j + 2) * rows) * __ldg(x + j + 2);
+    a3 += __ldg(K + r + (j + 3) * rows) * __ldg(x + j + 3);
+  }
+  for (; j < j1; ++j) a0 += __ldg(K + r + j * rows) * __ldg(x + j);
+  y[r] = (a0 + a1) + (a2 + a3);
 }
 
 // ------------------------------------------------------------------ small kernels of the loop
@@ -673,6 +680,7 @@ struct SolveState {
   DBuf<GemvWork> w_kd;
   int nw_op = 0, nw_loc = 0, nw_c = 0, nw_kd = 0, max_nd = 1;
   bool big_c = false;                // coarse vectors exceed shared memory: BIG GEMV variant
+  int c_chunks = 1;                  // distributed coarse: column chunks of the row-block GEMV
   DBuf<DlxDesc> dlx_r, dlx_e;        // deluxe restriction / extension descriptors (active slots)
   int dlx_threads = 32;
   size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_rx = 0, sm_ex = 0, sm_kd = 0;
@@ -833,8 +841,10 @@ static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   tick(c, st, 2, true, s2);
   if (c->nranks > 1) {
     // rows of the coarse inverse owned here, then the allgather of the row blocks (C2)
-    rows_gemv_kernel<<<(unsigned)((c->coarse_rows + 7) / 8), 256, 0, s2>>>(c->d_Kcr.p, c->coarse_rows, c->Nc, c->w_rc.p,
-                                                                        st->ucl.p);
+    const unsigned rb = (unsigned)((c->coarse_rows + 255) / 256);
+    rows_gemv_kernel<<<dim3(rb, st->c_chunks), 256, 0, s2>>>(c->d_Kcr.p, c->coarse_rows, c->Nc, c->w_rc.p, c->w_ucp.p);
+    sum_chunks_kernel<<<(unsigned)((c->coarse_rows + 31) / 32), 256, 0, s2>>>(c->w_ucp.p, c->coarse_rows, st->c_chunks,
+                                                                          c->coarse_rows, st->ucl.p);
     tick(c, st, 2, false, s2);
     c->comm->allgather(st->ucl.p, c->w_uc.p, c->coarse_rows, s2);
   } else {
@@ -934,6 +944,11 @@ void prepare_solve(vb_ctx *c) {
   wl.clear();
   int Pc = c->nranks > 1 ? 0 : std::max(1, std::min<int>(c->P_c, (int)((c->Nc + 31) / 32)));
   c->w_ucp.alloc(std::max<int64_t>((int64_t)Pc * c->Nc, 1));
+  if (c->nranks > 1) {
+    const int64_t rb = (c->coarse_rows + 255) / 256;
+    st->c_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, (4 * 148 + rb - 1) / rb));
+    c->w_ucp.alloc(std::max<int64_t>((int64_t)st->c_chunks * c->coarse_rows, 1));
+  }
   split_rows(c->Nc, Pc, rows, 4.0);
   for (int q = 0; q < Pc; ++q)
     wl.push_back(GemvWork{c->d_Kcp.p, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, rows[q].first, rows[q].second, 0});
