@@ -315,7 +315,7 @@ def main():
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        r = run_oracle_sample(2, 1)
+        r = run_oracle_sample(1, 0)
         line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
                                 "sample": r["sample"]}
     if rank == 0:

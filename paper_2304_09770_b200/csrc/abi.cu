@@ -409,6 +409,8 @@ vb_status vb_factor(vb_ctx *c) {
     double t0 = now_s();
     factor_device(c);
     prepare_solve(c);
+    if (getenv("VB_FACTOR_TIMES") && atoi(getenv("VB_FACTOR_TIMES")))
+      fprintf(stderr, "[vb factor rank %d] total incl. solve preparation %8.3f s\n", c->rank, now_s() - t0);
     c->t_factor = now_s() - t0;
     c->state = 2;
   })

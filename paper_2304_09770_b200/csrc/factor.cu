@@ -11,6 +11,7 @@
 #include <map>
 #include <set>
 #include <cstring>
+#include <chrono>
 #include "dense.cuh"
 #include "setup.h"
 #include "exchange.h"
@@ -219,6 +220,28 @@ __global__ void transpose_slot_kernel(const SlotDev *__restrict__ slots, const i
   }
 }
 
+// batched: out[o_b + i] = 1 / A_b(i, i) for the matrices described by MatDesc (A, n = order, ld)
+struct DiagDesc {
+  const double *A;
+  int64_t ld, out_off;
+  int n, pad;
+};
+__global__ void recip_diag_batched_kernel(const DiagDesc *__restrict__ d, double *out) {
+  const DiagDesc D = d[blockIdx.y];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D.n; i += gridDim.x * blockDim.x)
+    out[D.out_off + i] = 1.0 / D.A[i + i * D.ld];
+}
+
+static void recip_diag_batched(const std::vector<DiagDesc> &v, double *out, cudaStream_t s) {
+  if (v.empty()) return;
+  DBuf<DiagDesc> d;
+  std::vector<DiagDesc> h(v);
+  d.upload(h, s);
+  recip_diag_batched_kernel<<<dim3(8, v.size()), 256, 0, s>>>(d.p, out);
+  VB_CHECK_LAUNCH();
+  VB_CUDA(cudaStreamSynchronize(s));
+}
+
 __global__ void recip_diag_kernel(const double *A, int64_t ld, int n, double *out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = 1.0 / A[i + i * ld];
 }
@@ -419,9 +442,13 @@ static void stage_dirichlet(vb_ctx *c) {
     }
     tri_inverse_batched(td, s);
     dD.alloc(c->len_Dn);
-    for (int i = 0; i < N; ++i) {
-      const SubDev &S = c->h_sub[i];
-      recip_diag_kernel<<<(S.nD + 255) / 256, 256, 0, s>>>(c->d_K.p + S.off_K, S.n, S.nD, dD.p + S.off_Dn);
+    {
+      std::vector<DiagDesc> dd;
+      for (int i = 0; i < N; ++i) {
+        const SubDev &S = c->h_sub[i];
+        dd.push_back(DiagDesc{c->d_K.p + S.off_K, S.n, S.off_Dn, S.nD, 0});
+      }
+      recip_diag_batched(dd, dD.p, s);
     }
     VB_STAGE();
     c->d_Psi.alloc(std::max<int64_t>(lenPsi, 1));
@@ -610,9 +637,13 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     tri_inverse_batched(td, s);
   }
   dinv.alloc(std::max<int64_t>(c->len_Dv, 1));
-  for (int i = 0; i < N; ++i) {
-    const SubDev &S = c->h_sub[i];
-    if (S.nd) recip_diag_kernel<<<(S.nd + 255) / 256, 256, 0, s>>>(c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.n, S.nd, dinv.p + S.off_Dv);
+  {
+    std::vector<DiagDesc> dd;
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      if (S.nd) dd.push_back(DiagDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.n, S.off_Dv, S.nd, 0});
+    }
+    recip_diag_batched(dd, dinv.p, s);
   }
   VB_STAGE();
   c->d_Phi.alloc(std::max<int64_t>(c->len_Phi, 1));
@@ -679,8 +710,11 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     tri_inverse_batched(td, s);
     DBuf<double> edinv;
     edinv.alloc(std::max<int64_t>(c->len_sum, 1));
-    for (auto &M : em)
-      recip_diag_kernel<<<(M.n + 255) / 256, 256, 0, s>>>(M.A, M.n, M.n, edinv.p + (M.A - sumbuf.p));
+    {
+      std::vector<DiagDesc> dd;
+      for (auto &M : em) dd.push_back(DiagDesc{M.A, M.n, (int64_t)(M.A - sumbuf.p), M.n, 0});
+      recip_diag_batched(dd, edinv.p, s);
+    }
     VB_STAGE();
     {
       GemmPlan plan;
@@ -866,9 +900,22 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
   c->flux_violation = fv;
 }
 
+// VB_FACTOR_TIMES=1: wall time of each factor stage on stderr (the stages synchronise)
+static void stage_time(vb_ctx *c, const char *name) {
+  static const bool on = getenv("VB_FACTOR_TIMES") && atoi(getenv("VB_FACTOR_TIMES"));
+  if (!on) return;
+  static double last = 0;
+  VB_CUDA(cudaStreamSynchronize(c->stream));
+  const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  if (name) fprintf(stderr, "[vb factor rank %d] %-22s %8.3f s\n", c->rank, name, now - last);
+  last = now;
+}
+
 void factor_device(vb_ctx *c) {
   cudaStream_t s = c->stream;
+  stage_time(c, nullptr);
   stage_dirichlet(c);
+  stage_time(c, "dirichlet (A1/A2)");
   DBuf<double> sidebuf, sumbuf;
   const double tau = c->cons.adaptive_tau;
   c->extra_rows.assign(c->ents.size(), std::vector<double>());
@@ -884,7 +931,9 @@ void factor_device(vb_ctx *c) {
                                 S.nG * 8, S.nG, cudaMemcpyDeviceToDevice, s));
     }
     stage_interface(c, sidebuf, sumbuf);
+    stage_time(c, "interface (A3/A4)");
     adaptive_enrich(c, tau, sidebuf);           // A6: face GEVPs -> c->extra_rows
+    stage_time(c, "adaptive (A6)");
     for (int i = 0; i < c->N; ++i) {
       const SubDev &S = c->h_sub[i];
       VB_CUDA(cudaMemcpy2DAsync(c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), (size_t)S.n * 8, SG.p + S.off_X, S.nG * 8,
@@ -893,7 +942,9 @@ void factor_device(vb_ctx *c) {
     sync(c);
   }
   stage_interface(c, sidebuf, sumbuf);
+  stage_time(c, "interface (A3/A4)");
   stage_dual(c, sidebuf, sumbuf);
+  stage_time(c, "dual + coarse (A3-A5)");
 }
 
 }  // namespace vb

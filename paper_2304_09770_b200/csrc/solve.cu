@@ -20,6 +20,14 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Programmatic dependent launch (PDL): a kernel of the PCG step waits for its predecessor grid to
+// complete before touching memory, and lets its successor be scheduled as soon as all of its own
+// CTAs have started (the successor's CTAs fill this kernel's last wave and wait in turn).
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // ------------------------------------------------------------------ packed symmetric GEMV (K3)
 // Work item: one CTA multiplies the tile rows [r0, r1) of one packed symmetric matrix with x and
 // writes a full-length partial result.  Row contributions of a tile row are reduced in fixed warp
@@ -41,6 +49,7 @@ constexpr int GV_WARPS_C = 8;    // the single coarse matrix (one CTA per SM)
 // partial vector (each column J is owned by one warp, so there are no races).
 template <int GV_WARPS, bool BIG = false>
 __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork *__restrict__ work) {
+  pdl_prologue();
   extern __shared__ double sm[];
   const GemvWork W = work[blockIdx.x];
   const int n = W.n, nt = (n + 31) / 32;
@@ -148,6 +157,7 @@ static void split_rows(int n, int P, std::vector<std::pair<int, int>> &out, doub
 // (blockIdx.y: column chunk, partial sums y[chunk * rows + r], summed in chunk order afterwards)
 __global__ void __launch_bounds__(256) rows_gemv_kernel(const double *__restrict__ K, int64_t rows, int64_t n,
                                                         const double *__restrict__ x, double *y) {
+  pdl_prologue();
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const int64_t cw = (n + gridDim.y - 1) / gridDim.y;
@@ -172,6 +182,7 @@ __global__ void __launch_bounds__(256) rows_gemv_kernel(const double *__restrict
 __global__ void chunk_sum_b0_kernel(const SubDev *__restrict__ subs, const double *__restrict__ part, int64_t stride,
                                     int P, const double *__restrict__ b0T, const int64_t *__restrict__ loc2x,
                                     const double *__restrict__ p, int64_t p0off, double *sbuf, double *q) {
+  pdl_prologue();
   const SubDev S = subs[blockIdx.y];
   const double p0 = p[p0off + blockIdx.y];
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S.nG; j += gridDim.x * blockDim.x) {
@@ -191,6 +202,7 @@ __global__ void chunk_sum_b0_kernel(const SubDev *__restrict__ subs, const doubl
 // out[g] = sum over the CSR sources of g (fixed order: sharers in global subdomain order)
 __global__ void gather_src_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ idx,
                                   const double *__restrict__ src, int64_t n, double *out) {
+  pdl_prologue();
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
     double v = 0.0;
     for (int64_t q = ptr[g]; q < ptr[g + 1]; ++q) v += src[idx[q]];
@@ -231,12 +243,14 @@ __global__ void dot_final_kernel(const double *__restrict__ part, int nb, double
 // scal: [0] rz, [1] pq, [2] rr, [3] rz_new, [4] alpha, [5] beta
 
 __global__ void update_p_kernel(double *p, const double *z, int64_t n, double *scal, int first) {
+  pdl_prologue();
   const double beta = first ? 0.0 : scal[3] / scal[0];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
 }
 
 __global__ void rotate_rz_kernel(double *scal, double *hist) {
+  pdl_prologue();
   // record beta of this step and rotate rz <- rz_new (it = scal[6] already counts this step)
   const int it = (int)scal[6];
   if (it >= 1 && it <= 4096) hist[2 * (it - 1) + 1] = scal[3] / scal[0];
@@ -270,6 +284,7 @@ __device__ __forceinline__ void block_reduce_last(double v, double *part, unsign
 
 __global__ void dot_kernel(const double *__restrict__ a, const double *__restrict__ b, const double *__restrict__ mask,
                            int64_t n, double *part, unsigned *ticket, double *dst) {
+  pdl_prologue();
   double v = 0.0;
   if (mask) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -284,6 +299,7 @@ __global__ void dot_kernel(const double *__restrict__ a, const double *__restric
 // x += alpha p, r -= alpha q (alpha = rz / pq), fused with the partial of r.r -> dst
 __global__ void update_xr_rr_kernel(double *x, double *r, const double *p, const double *q, const double *mask,
                                     int64_t n, const double *scal, double *part, unsigned *ticket, double *dst) {
+  pdl_prologue();
   const double alpha = scal[0] / scal[1];
   double v = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -318,6 +334,7 @@ __global__ void pcg_init_kernel(double *scal, double rtol, int maxit) {
 }
 
 __global__ void pcg_check_kernel(double *scal, double *hist, cudaGraphConditionalHandle hw, int use_graph) {
+  pdl_prologue();
   const double rz = scal[0], pq = scal[1];
   int it = (int)scal[6];
   double status = 0.0;
@@ -345,6 +362,7 @@ struct DlxDesc {
 
 __global__ void __launch_bounds__(256) dlx_apply_kernel(const DlxDesc *__restrict__ desc, const double *__restrict__ M,
                                                         const double *__restrict__ in, double *out) {
+  pdl_prologue();
   extern __shared__ double xs[];
   const DlxDesc D = desc[blockIdx.x];
   const int nd = D.nd;
@@ -369,6 +387,7 @@ __global__ void __launch_bounds__(256) dlx_apply_kernel(const DlxDesc *__restric
 constexpr int PHIT_SPLIT = 4;
 __global__ void __launch_bounds__(256) phit_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
                             const double *__restrict__ rD, double *cpart) {
+  pdl_prologue();
   const SubDev S = subs[blockIdx.y];
   const double *F = Phi + S.off_Phi;
   const double *x = rD + S.off_Dv;
@@ -389,6 +408,7 @@ __global__ void __launch_bounds__(256) phit_kernel(const SubDev *__restrict__ su
 // p0 projections of the coarse problem (gauge sum vol_i p0_i = 0, A5):
 // mode 0 (input):  rc_p0 -= vol * (sum rc_p0) / sum vol ;  mode 1 (output): uc_p0 -= (vol . uc_p0)/sum vol
 __global__ void coarse_p0_project_kernel(const double *__restrict__ vol, int N, double *v, int mode) {
+  pdl_prologue();
   __shared__ double red[32];
   double a = 0.0, w = 0.0;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -413,6 +433,7 @@ __global__ void coarse_p0_project_kernel(const double *__restrict__ vol, int N, 
 __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
                               const double *__restrict__ part, int64_t part_stride, int P,
                               const int64_t *__restrict__ pi_glob, const double *__restrict__ uc, double *w) {
+  pdl_prologue();
   const SubDev S = subs[blockIdx.y];
   const double *F = Phi + S.off_Phi;
   extern __shared__ double us[];
@@ -660,6 +681,7 @@ __global__ void axpby_kernel(const double *a, const double *b, double *out, int6
 // the 8 warp partials are added in fixed order.
 __global__ void __launch_bounds__(256) sum_chunks_kernel(const double *__restrict__ part, int64_t stride, int P,
                                                          int64_t n, double *out) {
+  pdl_prologue();
   __shared__ double red[8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i = blockIdx.x * 32 + lane;
@@ -707,6 +729,7 @@ struct SolveState {
   // the PCG iteration as a CUDA graph: WHILE(status == 0) { S-part; check; IF(status == 0) M-part }
   cudaGraphExec_t gexec = nullptr;
   bool capturing = false;
+  bool pdl = true;                   // programmatic dependent launch inside the PCG step
   // optional per-kernel timing (VB_KERNEL_TIMING=1, host-driven iterations): event pairs per
   // launch category
   std::vector<cudaEvent_t> ev;
@@ -721,6 +744,25 @@ struct SolveState {
     if (sg) cudaStreamDestroy(sg);
   }
 };
+
+// launch with the PDL attribute when enabled (kernels of the PCG step start with pdl_prologue)
+template <typename... KArgs, typename... Args>
+static void launch_pdl(const SolveState *st, void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t s,
+                       Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (st->pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  VB_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 
 static const char *kCatNames[] = {"sym_gemv S_T (operator, B1)", "sym_gemv S_DD^-1 (local, B5)",
                                   "sym_gemv coarse inverse (B6)", "apply_S total (B1-B2)",
@@ -777,7 +819,7 @@ static SolveState *get_state(vb_ctx *c) {
 // C3: block partials -> rank partial -> fixed-order sum over ranks
 static void dot(vb_ctx *c, const double *a, const double *b, int64_t n, double *dst) {
   SolveState *st = get_state(c);
-  dot_kernel<<<DOT_BLOCKS, 256, 0, c->stream>>>(a, b, c->nranks > 1 ? st->mask.p : nullptr, n, c->w_dots.p,
+  launch_pdl(st, dot_kernel, dim3(DOT_BLOCKS), dim3(256), 0, c->stream, a, b, c->nranks > 1 ? st->mask.p : nullptr, n, c->w_dots.p,
                                                 st->ticket.p, dst);
   allreduce_sum_fixed(c, dst, 1);
 }
@@ -788,16 +830,16 @@ static void apply_S(vb_ctx *c, SolveState *st) {   // q = S^ p  (B1, B2)
   cudaStream_t s = c->stream;
   tick(c, st, 3, true);
   tick(c, st, 0, true);
-  sym_gemv_kernel<GV_WARPS><<<st->nw_op, GV_WARPS * 32, st->sm_op, s>>>(st->w_op.p);
+  launch_pdl(st, sym_gemv_kernel<GV_WARPS>, dim3(st->nw_op), dim3(GV_WARPS * 32), st->sm_op, s, st->w_op.p);
   tick(c, st, 0, false);
   int maxnG = 1;
   for (auto &S : c->h_sub) maxnG = std::max(maxnG, S.nG);
-  chunk_sum_b0_kernel<<<dim3((maxnG + 255) / 256, c->N), 256, 0, s>>>(c->d_sub.p, c->w_part.p, c->len_G, c->P_op,
+  launch_pdl(st, chunk_sum_b0_kernel, dim3((maxnG + 255) / 256, c->N), dim3(256), 0, s, c->d_sub.p, c->w_part.p, c->len_G, c->P_op,
                                                                      c->d_b0T.p, c->d_loc2x.p, c->w_p.p,
                                                                      c->n_delta_glob + c->NPi, st->sx.p, c->w_q.p);
   run_slot_exchange(c, st->XS, st->sx.p, st->sx.p + c->len_G);      // C1 (cross-rank copies)
   int64_t nxp = c->n_delta_glob + c->NPi;
-  gather_src_kernel<<<grid_for(nxp), 256, 0, s>>>(st->xptr.p, st->xidx.p, st->sx.p, nxp, c->w_q.p);
+  launch_pdl(st, gather_src_kernel, dim3(grid_for(nxp)), dim3(256), 0, s, st->xptr.p, st->xidx.p, st->sx.p, nxp, c->w_q.p);
   tick(c, st, 3, false);
   VB_STAGE();
 }
@@ -820,50 +862,50 @@ static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   cudaStream_t s = c->stream, s2 = st->s2;
   tick(c, st, 4, true);
   if (c->n_act_slots)
-    dlx_apply_kernel<<<c->n_act_slots, st->dlx_threads, st->sm_rx, s>>>(st->dlx_r.p, c->d_Dt.p, c->w_r.p, c->w_locD.p);
+    launch_pdl(st, dlx_apply_kernel, dim3(c->n_act_slots), dim3(st->dlx_threads), st->sm_rx, s, st->dlx_r.p, c->d_Dt.p, c->w_r.p, c->w_locD.p);
   trace_norm(c, "rD", c->w_locD.p, c->len_Dv, false);
   // fork: the coarse branch (B6) runs on s2 while the local dual solves (B5) stream on s
   VB_CUDA(cudaEventRecord(st->ev_fork, s));
   VB_CUDA(cudaStreamWaitEvent(s2, st->ev_fork, 0));
   tick(c, st, 1, true);
-  if (st->nw_loc) sym_gemv_kernel<GV_WARPS><<<st->nw_loc, GV_WARPS * 32, st->sm_loc, s>>>(st->w_loc.p);
+  if (st->nw_loc) launch_pdl(st, sym_gemv_kernel<GV_WARPS>, dim3(st->nw_loc), dim3(GV_WARPS * 32), st->sm_loc, s, st->w_loc.p);
   tick(c, st, 1, false);
   // coarse pieces (C2): [Phi_i^T rD_i per local subdomain | r0_i | r_Pi of the owned entities]
-  phit_kernel<<<dim3(PHIT_SPLIT, c->N), 256, 0, s2>>>(c->d_sub.p, c->d_Phi.p, c->w_locD.p, st->cbuf.p);
+  launch_pdl(st, phit_kernel, dim3(PHIT_SPLIT, c->N), dim3(256), 0, s2, c->d_sub.p, c->d_Phi.p, c->w_locD.p, st->cbuf.p);
   dev_gather(c->w_r.p, st->cpack.p, (int64_t)st->cpack.n, st->cbuf.p + c->len_Pi, s2);
   const double *pieces = st->cbuf.p;
   if (c->nranks > 1) {
     c->comm->allgather(st->cbuf.p, st->cgath.p, st->cmax, s2);
     pieces = st->cgath.p;
   }
-  gather_src_kernel<<<grid_for(c->Nc), 256, 0, s2>>>(st->pptr.p, st->pidx.p, pieces, c->Nc, c->w_rc.p);
-  coarse_p0_project_kernel<<<1, 256, 0, s2>>>(st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
+  launch_pdl(st, gather_src_kernel, dim3(grid_for(c->Nc)), dim3(256), 0, s2, st->pptr.p, st->pidx.p, pieces, c->Nc, c->w_rc.p);
+  launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
   tick(c, st, 2, true, s2);
   if (c->nranks > 1) {
     // rows of the coarse inverse owned here, then the allgather of the row blocks (C2)
     const unsigned rb = (unsigned)((c->coarse_rows + 255) / 256);
-    rows_gemv_kernel<<<dim3(rb, st->c_chunks), 256, 0, s2>>>(c->d_Kcr.p, c->coarse_rows, c->Nc, c->w_rc.p, c->w_ucp.p);
-    sum_chunks_kernel<<<(unsigned)((c->coarse_rows + 31) / 32), 256, 0, s2>>>(c->w_ucp.p, c->coarse_rows, st->c_chunks,
+    launch_pdl(st, rows_gemv_kernel, dim3(rb, st->c_chunks), dim3(256), 0, s2, c->d_Kcr.p, c->coarse_rows, c->Nc, c->w_rc.p, c->w_ucp.p);
+    launch_pdl(st, sum_chunks_kernel, dim3((unsigned)((c->coarse_rows + 31) / 32)), dim3(256), 0, s2, c->w_ucp.p, c->coarse_rows, st->c_chunks,
                                                                           c->coarse_rows, st->ucl.p);
     tick(c, st, 2, false, s2);
     c->comm->allgather(st->ucl.p, c->w_uc.p, c->coarse_rows, s2);
   } else {
   if (st->big_c)
-    sym_gemv_kernel<GV_WARPS_C, true><<<st->nw_c, GV_WARPS_C * 32, GV_WARPS_C * 32 * sizeof(double), s2>>>(st->w_c.p);
+    launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, true>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), GV_WARPS_C * 32 * sizeof(double), s2, st->w_c.p);
   else
-    sym_gemv_kernel<GV_WARPS_C><<<st->nw_c, GV_WARPS_C * 32, st->sm_c, s2>>>(st->w_c.p);
+    launch_pdl(st, sym_gemv_kernel<GV_WARPS_C>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), st->sm_c, s2, st->w_c.p);
   tick(c, st, 2, false, s2);
-  sum_chunks_kernel<<<(c->Nc + 31) / 32, 256, 0, s2>>>(c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
+  launch_pdl(st, sum_chunks_kernel, dim3((c->Nc + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
   }
-  coarse_p0_project_kernel<<<1, 256, 0, s2>>>(st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
+  launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
   VB_CUDA(cudaEventRecord(st->ev_join, s2));
   VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
   trace_norm(c, "uc", c->w_uc.p, c->Nc, true);
-  local2_kernel<<<dim3((st->max_nd + 127) / 128, c->N), 128, c->max_npi * sizeof(double), s>>>(
+  launch_pdl(st, local2_kernel, dim3((st->max_nd + 127) / 128, c->N), dim3(128), c->max_npi * sizeof(double), s,
       c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p);
   trace_norm(c, "w", c->w_locD.p, c->len_Dv, false);
   if (c->n_act_slots)
-    dlx_apply_kernel<<<c->n_act_slots, st->dlx_threads, st->sm_rx, s>>>(st->dlx_e.p, c->d_Dlx.p, c->w_locD.p, st->tx.p);
+    launch_pdl(st, dlx_apply_kernel, dim3(c->n_act_slots), dim3(st->dlx_threads), st->sm_rx, s, st->dlx_e.p, c->d_Dlx.p, c->w_locD.p, st->tx.p);
   run_slot_exchange(c, st->XE, st->tx.p, st->tx.p + st->len_t);    // C1 (cross-rank products)
   trace_norm(c, "t", st->tx.p, st->len_t, false);
   run_entity_sum(c, st->ESE, st->tx.p, c->w_z.p);
@@ -903,6 +945,7 @@ void prepare_solve(vb_ctx *c) {
   if (c->nranks > 1) st->ucl.alloc(std::max<int64_t>(c->coarse_rows, 1));
   c->w_scal.alloc(16); c->w_scal.zero(s);
   st->ticket.alloc(4); st->ticket.zero(s);
+  st->pdl = !(getenv("VB_NO_PDL") && atoi(getenv("VB_NO_PDL")));
   if (!st->s2) {
     VB_CUDA(cudaStreamCreateWithFlags(&st->s2, cudaStreamNonBlocking));
     VB_CUDA(cudaStreamCreateWithFlags(&st->sg, cudaStreamNonBlocking));
@@ -1262,11 +1305,11 @@ static void pcg_step(vb_ctx *c, SolveState *st, cudaGraphConditionalHandle hw, b
   const int64_t nx = c->nx;
   apply_S(c, st);
   dot(c, c->w_p.p, c->w_q.p, nx, sc + 1);
-  update_xr_rr_kernel<<<DOT_BLOCKS, 256, 0, s>>>(c->w_x.p, c->w_r.p, c->w_p.p, c->w_q.p,
+  launch_pdl(st, update_xr_rr_kernel, dim3(DOT_BLOCKS), dim3(256), 0, s, c->w_x.p, c->w_r.p, c->w_p.p, c->w_q.p,
                                                  c->nranks > 1 ? st->mask.p : nullptr, nx, sc, c->w_dots.p,
                                                  st->ticket.p, sc + 2);
   allreduce_sum_fixed(c, sc + 2, 1);
-  pcg_check_kernel<<<1, 1, 0, s>>>(sc, st->hist.p, hw, graph ? 1 : 0);
+  launch_pdl(st, pcg_check_kernel, dim3(1), dim3(1), 0, s, sc, st->hist.p, hw, graph ? 1 : 0);
   VB_STAGE();
 }
 
@@ -1277,8 +1320,8 @@ static void pcg_mstep(vb_ctx *c, SolveState *st) {
   const int64_t nx = c->nx;
   apply_M(c, st);
   dot(c, c->w_r.p, c->w_z.p, nx, sc + 3);
-  update_p_kernel<<<grid_for(nx), 256, 0, s>>>(c->w_p.p, c->w_z.p, nx, sc, 0);
-  rotate_rz_kernel<<<1, 1, 0, s>>>(sc, st->hist.p);
+  launch_pdl(st, update_p_kernel, dim3(grid_for(nx)), dim3(256), 0, s, c->w_p.p, c->w_z.p, nx, sc, 0);
+  launch_pdl(st, rotate_rz_kernel, dim3(1), dim3(1), 0, s, sc, st->hist.p);
   VB_STAGE();
 }
 
@@ -1326,8 +1369,16 @@ static void build_iteration_graph(vb_ctx *c, SolveState *st) {
   }
   st->capturing = false;
   c->stream = user;
-  VB_CUDA(cudaGraphInstantiate(&st->gexec, g, 0));
-  VB_CUDA(cudaGraphDestroy(g));
+  cudaError_t e = cudaGraphInstantiate(&st->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess && st->pdl) {     // programmatic edges not accepted here: capture without them
+    (void)cudaGetLastError();
+    st->gexec = nullptr;
+    st->pdl = false;
+    build_iteration_graph(c, st);
+    return;
+  }
+  VB_CUDA(e);
 }
 
 void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int maxit, vb_report *rep) {
