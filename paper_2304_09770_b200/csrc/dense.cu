@@ -56,14 +56,17 @@ __device__ __forceinline__ void load_slab(const GemmProb &P, int m0, int n0, int
   }
 }
 
+// DENSE: one large problem (id = tile0) on a 2D grid of tiles (no tile list)
+template <bool DENSE>
 __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
                                                                   const int4 *__restrict__ tiles, int tile0) {
-  const int4 t = tiles[tile0 + blockIdx.x];
+  const int4 t = DENSE ? make_int4(tile0, blockIdx.y, blockIdx.x, 0) : tiles[tile0 + blockIdx.x];
   __shared__ GemmProb Ps;                 // problem descriptor in shared memory (register pressure)
   if (threadIdx.x == 0) Ps = probs[t.x];
   __syncthreads();
   const GemmProb &P = Ps;
   const int m0 = t.y * GBM, n0 = t.z * GBN;
+  if (DENSE && P.lower && m0 + GBM - 1 < n0) return;   // tile strictly above the diagonal
   __shared__ double As[GBM][GBK + GPAD];
   __shared__ double Bs[GBK][GBN + GPAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -124,6 +127,10 @@ void GemmPlan::add(const GemmProb &p) {
   int pid = probs.size();
   probs.push_back(p);
   int tm = (p.M + GBM - 1) / GBM, tn = (p.N + GBN - 1) / GBN;
+  if ((int64_t)tm * tn >= 4096 && tm < 65536) {   // large: a 2D grid instead of a tile list
+    dense.back().push_back(pid);
+    return;
+  }
   for (int i = 0; i < tm; ++i)
     for (int j = 0; j < tn; ++j) {
       if (p.lower && (i * GBM + GBM - 1) < j * GBN) continue;   // tile strictly above diagonal
@@ -142,9 +149,16 @@ void GemmPlan::upload(cudaStream_t s) {
 
 void GemmPlan::run(int launch, cudaStream_t s) {
   auto &L = launches[launch];
-  if (L.second == 0) return;
-  gemm_grouped_kernel<<<L.second, GTHREADS, 0, s>>>(d_probs.p, d_tiles.p, L.first);
-  VB_CHECK_LAUNCH();
+  if (L.second > 0) {
+    gemm_grouped_kernel<false><<<L.second, GTHREADS, 0, s>>>(d_probs.p, d_tiles.p, L.first);
+    VB_CHECK_LAUNCH();
+  }
+  for (int pid : dense[launch]) {
+    const GemmProb &p = probs[pid];
+    dim3 grid((p.N + GBN - 1) / GBN, (p.M + GBM - 1) / GBM);
+    gemm_grouped_kernel<true><<<grid, GTHREADS, 0, s>>>(d_probs.p, d_tiles.p, pid);
+    VB_CHECK_LAUNCH();
+  }
 }
 
 void gemm_grouped(GemmPlan &plan, int launch, cudaStream_t s) { plan.run(launch, s); }

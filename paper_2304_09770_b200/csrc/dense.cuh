@@ -14,9 +14,14 @@ struct GemmPlan {
   std::vector<GemmProb> probs;
   std::vector<int4> tiles;                 // (prob, tile_m, tile_n, 0)
   std::vector<std::pair<int, int>> launches;  // (tile_begin, tile_count)
+  std::vector<std::vector<int>> dense;        // per launch: large problems run as 2D grids
   DBuf<GemmProb> d_probs;
   DBuf<int4> d_tiles;
-  int begin_launch() { launches.push_back({(int)tiles.size(), 0}); return launches.size() - 1; }
+  int begin_launch() {
+    launches.push_back({(int)tiles.size(), 0});
+    dense.push_back({});
+    return launches.size() - 1;
+  }
   void add(const GemmProb &p);             // adds tiles to the current launch
   void upload(cudaStream_t s);
   void run(int launch, cudaStream_t s);
