@@ -13,6 +13,7 @@ namespace vb {
 constexpr int GBM = 128, GBN = 64, GBK = 16;
 constexpr int GPAD = 4;
 constexpr int GTHREADS = 256;
+constexpr int LDL_NB = 128;        // wide-panel width of the blocked LDL^T and triangular inverse
 constexpr int GA_PER = GBM * GBK / GTHREADS;   // 8
 constexpr int GB_PER = GBK * GBN / GTHREADS;   // 4
 
@@ -238,8 +239,6 @@ __global__ void ldl_panel_kernel(const MatDesc *__restrict__ mats, int j0, int *
 // panels of LDL_NB columns; inside a wide panel only its remaining columns are updated (K = 32), the
 // trailing matrix once per wide panel with K = LDL_NB (DMMA GEMM, 4x fewer passes over the trailing
 // matrix than a 32-column right-looking update).
-constexpr int LDL_NB = 128;
-
 void ldl_partial_batched(const std::vector<MatDesc> &mats, int *info_dev, cudaStream_t s) {
   if (mats.empty()) return;
   DBuf<MatDesc> dm;
@@ -346,30 +345,54 @@ void tri_inverse_batched(const std::vector<TriDesc> &mats, cudaStream_t s) {
   if (maxm == 0) return;
   set_identity_kernel<<<dim3((maxm + 255) / 256, mats.size()), 256, 0, s>>>(dm.p);
   VB_CHECK_LAUNCH();
+  // blocked like the LDL^T: 32-row diagonal solves, updates inside a 128-row wide block with K = 32,
+  // the rows below the wide block once per wide block with K = 128
   int nblk = (maxm + 31) / 32;
   GemmPlan plan;
-  for (int J = 0; J < nblk; ++J) {
-    plan.begin_launch();
+  std::vector<int> intra(nblk, -1), trail;
+  for (int J0 = 0; J0 < maxm; J0 += LDL_NB) {
+    for (int r0 = J0; r0 < std::min(J0 + LDL_NB, maxm); r0 += 32) {
+      intra[r0 / 32] = plan.begin_launch();
+      for (auto &T : mats) {
+        if (r0 >= T.m) continue;
+        const int nb = std::min(32, T.m - r0);
+        const int Je = std::min(J0 + LDL_NB, T.m);
+        const int rows = Je - r0 - nb;
+        if (rows <= 0) continue;
+        GemmProb p{};
+        p.A = T.L + (r0 + nb) + (int64_t)r0 * T.ldl; p.lda = T.ldl; p.transA = 0;
+        p.B = T.X + r0; p.ldb = T.ldx; p.transB = 0;
+        p.C = T.X + (r0 + nb); p.ldc = T.ldx;
+        p.M = rows; p.N = r0 + nb; p.K = nb;
+        p.alpha = -1.0; p.beta = 1.0; p.lower = 0;
+        plan.add(p);
+      }
+    }
+    trail.push_back(plan.begin_launch());
     for (auto &T : mats) {
-      int r0 = 32 * J;
-      if (r0 >= T.m) continue;
-      int nb = std::min(32, T.m - r0);
-      int rows = T.m - r0 - nb;
+      if (J0 >= T.m) continue;
+      const int Je = std::min(J0 + LDL_NB, T.m);
+      const int rows = T.m - Je;
       if (rows <= 0) continue;
       GemmProb p{};
-      p.A = T.L + (r0 + nb) + (int64_t)r0 * T.ldl; p.lda = T.ldl; p.transA = 0;
-      p.B = T.X + r0; p.ldb = T.ldx; p.transB = 0;
-      p.C = T.X + (r0 + nb); p.ldc = T.ldx;
-      p.M = rows; p.N = std::min(T.m, r0 + nb); p.K = nb;
+      p.A = T.L + Je + (int64_t)J0 * T.ldl; p.lda = T.ldl; p.transA = 0;
+      p.B = T.X + J0; p.ldb = T.ldx; p.transB = 0;
+      p.C = T.X + Je; p.ldc = T.ldx;
+      p.M = rows; p.N = Je; p.K = Je - J0;
       p.alpha = -1.0; p.beta = 1.0; p.lower = 0;
       plan.add(p);
     }
   }
   plan.upload(s);
-  for (int J = 0; J < nblk; ++J) {
-    trsm_diag_kernel<<<dim3(J + 1, mats.size()), 32, 0, s>>>(dm.p, J);
-    VB_CHECK_LAUNCH();
-    plan.run(J, s);
+  int wide = 0;
+  for (int J0 = 0; J0 < maxm; J0 += LDL_NB, ++wide) {
+    for (int r0 = J0; r0 < std::min(J0 + LDL_NB, maxm); r0 += 32) {
+      const int J = r0 / 32;
+      trsm_diag_kernel<<<dim3(J + 1, mats.size()), 32, 0, s>>>(dm.p, J);
+      VB_CHECK_LAUNCH();
+      plan.run(intra[J], s);
+    }
+    plan.run(trail[wide], s);
   }
   VB_CUDA(cudaStreamSynchronize(s));
 }

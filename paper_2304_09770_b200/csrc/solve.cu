@@ -455,10 +455,6 @@ __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ 
   w[S.off_Dv + j] = v + ((a0 + a1) + (a2 + a3));
 }
 
-__global__ void copy_kernel(const double *a, double *b, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
-}
-
 // ------------------------------------------------------------------ B0 / B8
 // B0 (GEMV form): b_D = [b_I ; Pi^T b_P] and g0_i = c^T b_P (p0 rhs, A5)
 __global__ void rhs_D_kernel(const SubDev *__restrict__ subs, const int64_t *__restrict__ Ifree,
@@ -669,11 +665,6 @@ __global__ void elem_gather_kernel(const int64_t *__restrict__ ptr, const int64_
       y[nvf + gid[K] * np + a] = yel[K * stride + nvmax + a];
     }
   }
-}
-
-__global__ void axpby_kernel(const double *a, const double *b, double *out, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = a[i] - b[i];
 }
 
 // ------------------------------------------------------------------ host side
