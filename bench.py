@@ -308,10 +308,10 @@ def main():
                                 names[3]: {"ms": kt[names[3]]}, names[4]: {"ms": kt[names[4]]}}},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ctx.n_free,
                 "d2h_bytes_per_step": 8 * ctx.n_free, "ms_per_step": e2e_ms},
-        # kernels per solve (single rank): B0 8 + init 2 + first M^-1 15 + it S-steps x 6 +
-        # (it-1) M-steps x 16 + B8 6 = 15 + 22 it (cross-checked against the ncu launch list in
-        # profiles/); multi-rank adds the exchange pack/sum kernels
-        "gpu_launches": int(args.steps * (15 + 22 * it)),
+        # kernels per solve (single rank): B0 8 + init 2 + first M^-1 15 + it S-steps x 4 +
+        # (it-1) M-steps x 16 + B8 6 = 15 + 20 it (cross-checked against the ncu launch list of a
+        # host-driven solve in profiles/); multi-rank adds the exchange pack/sum kernels
+        "gpu_launches": int(args.steps * (15 + 20 * it)),
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

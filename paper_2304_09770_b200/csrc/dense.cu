@@ -425,20 +425,13 @@ __global__ void pack_tiles_kernel(const PackDesc *__restrict__ mats) {
   if (32 * I >= M.n) return;
   const int rows = min(32, M.n - 32 * I);
   double *out = M.out + ptile_off(M.n, I, J);
-  if (J < I) {
-    for (int idx = threadIdx.x; idx < rows * 32; idx += blockDim.x) {
-      const int r = idx >> 5, cc = idx & 31;
-      const int row = 32 * I + r, col = 32 * J + cc;
-      out[idx] = M.A[row + (int64_t)col * M.ld];   // row > col: lower triangle
-    }
-  } else {   // diagonal tile: lower triangle, row r holds columns 0..r
-    for (int idx = threadIdx.x; idx < rows * (rows + 1) / 2; idx += blockDim.x) {
-      int r = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
-      while (r * (r + 1) / 2 > idx) --r;
-      while ((r + 1) * (r + 2) / 2 <= idx) ++r;
-      const int cc = idx - r * (r + 1) / 2;
-      out[idx] = M.A[(32 * I + r) + (int64_t)(32 * J + cc) * M.ld];
-    }
+  for (int idx = threadIdx.x; idx < rows * 32; idx += blockDim.x) {
+    const int r = idx >> 5, cc = idx & 31;
+    const int row = 32 * I + r, col = 32 * J + cc;
+    double v = 0.0;
+    if (row < M.n && col < M.n)
+      v = row >= col ? M.A[row + (int64_t)col * M.ld] : M.A[col + (int64_t)row * M.ld];
+    out[idx] = v;
   }
 }
 

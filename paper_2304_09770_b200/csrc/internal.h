@@ -87,9 +87,9 @@ struct GemmProb {
 
 // ------------------------------------------------------------------ packed symmetric tiles
 // Lower triangle of a symmetric n x n matrix as 32x32 tiles (I >= J) in row-of-tiles order, each
-// tile row-major; diagonal tiles store only their lower triangle (row r: r+1 entries) and the tiles
-// of the last tile row only its rv = n - 32 (nt - 1) valid rows -- nothing but the matrix is stored.
-HD_INLINE int64_t ptile_row_start(int64_t I) { return 1024 * (I * (I - 1) / 2) + 528 * I; }
+// tile row-major (diagonal tiles hold the full symmetric block); the tiles of the last tile row
+// store only its rv = n - 32 (nt - 1) valid rows, so no padding rows are streamed.
+HD_INLINE int64_t ptile_row_start(int64_t I) { return 1024 * (I * (I + 1) / 2); }
 HD_INLINE int64_t ptile_off(int n, int I, int J) {   // offset of tile (I, J), J <= I
   const int nt = (n + 31) / 32;
   const int64_t rows = (I == nt - 1) ? n - 32 * (nt - 1) : 32;
@@ -99,7 +99,7 @@ HD_INLINE int64_t packed_size(int n) {               // doubles
   if (n <= 0) return 0;
   const int nt = (n + 31) / 32;
   const int64_t rv = n - 32 * (nt - 1);
-  return ptile_row_start(nt - 1) + (int64_t)(nt - 1) * rv * 32 + rv * (rv + 1) / 2;
+  return ptile_row_start(nt - 1) + (int64_t)nt * rv * 32;
 }
 
 struct GEnt {                  // global interface entity (every rank holds the whole list)

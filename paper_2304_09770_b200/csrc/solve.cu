@@ -82,25 +82,21 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
     for (int J = warp; J <= I; J += GV_WARPS) {
       const double *T = W.M + ptile_off(n, I, J);
       double t[32];
-      if (J < I) {
+      if (rows == 32) {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) t[r] = __ldg(T + r * 32 + lane);
+      } else {   // short last tile row
 #pragma unroll
         for (int r = 0; r < 32; ++r) t[r] = r < rows ? __ldg(T + r * 32 + lane) : 0.0;
-      } else {     // diagonal tile, lower triangle only: row r holds columns 0..r
-#pragma unroll
-        for (int r = 0; r < 32; ++r) t[r] = (r < rows && lane <= r) ? __ldg(T + r * (r + 1) / 2 + lane) : 0.0;
       }
       const double xJ = X(32 * J + lane);
-      double csum = 0.0, dval = 0.0;
+      double csum = 0.0;
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         rsum[r] += t[r] * xJ;
         csum += t[r] * __shfl_sync(FULL, xI_lane, r);
-        if (r == lane) dval = t[r];
       }
-      // transposed part (one warp per J): entries (r, lane) add to output lane; on the diagonal tile
-      // the stored triangle is transposed without its diagonal
-      if (J == I) csum -= dval * xI_lane;
-      if (!BIG || 32 * J + lane < n) ys[32 * J + lane] += csum;
+      if (J < I && (!BIG || 32 * J + lane < n)) ys[32 * J + lane] += csum;   // transpose part, one warp per J
     }
     // transpose-reduce rsum across lanes: lane l ends with sum over lanes of rsum[l]
 #pragma unroll
@@ -259,7 +255,7 @@ __global__ void rotate_rz_kernel(double *scal, double *hist) {
 
 // ---- single-launch deterministic reductions: block partials, the last block to finish sums them
 // in block order (threadfence + ticket), then resets the ticket for the next use.
-__device__ __forceinline__ void block_reduce_last(double v, double *part, unsigned *ticket, double *dst) {
+__device__ __forceinline__ bool block_reduce_last(double v, double *part, unsigned *ticket, double *dst) {
   __shared__ double red[32];
   __shared__ bool last;
   v = warp_sum(v);
@@ -280,6 +276,7 @@ __device__ __forceinline__ void block_reduce_last(double v, double *part, unsign
     t = warp_sum(t);
     if (threadIdx.x == 0) { *dst = t; *ticket = 0u; }
   }
+  return last && threadIdx.x == 0;   // the thread that wrote *dst
 }
 
 __global__ void dot_kernel(const double *__restrict__ a, const double *__restrict__ b, const double *__restrict__ mask,
@@ -297,20 +294,6 @@ __global__ void dot_kernel(const double *__restrict__ a, const double *__restric
 }
 
 // x += alpha p, r -= alpha q (alpha = rz / pq), fused with the partial of r.r -> dst
-__global__ void update_xr_rr_kernel(double *x, double *r, const double *p, const double *q, const double *mask,
-                                    int64_t n, const double *scal, double *part, unsigned *ticket, double *dst) {
-  pdl_prologue();
-  const double alpha = scal[0] / scal[1];
-  double v = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] += alpha * p[i];
-    const double ri = r[i] - alpha * q[i];
-    r[i] = ri;
-    v += mask ? mask[i] * (ri * ri) : ri * ri;
-  }
-  block_reduce_last(v, part, ticket, dst);
-}
-
 // p0 block of the condensed rhs: the compatibility sum_i g0_i = 0 holds up to rounding; remove the
 // rounding (mode 0: local sum into *acc; mode 1: subtract acc[0] / n_total from every entry)
 __global__ void p0_compat_kernel(double *p0, int n, double *acc, int mode, int n_total) {
@@ -333,8 +316,7 @@ __global__ void pcg_init_kernel(double *scal, double rtol, int maxit) {
   scal[7] = (r0n <= rtol * r0n) ? 1.0 : (maxit <= 0 ? 3.0 : 0.0);
 }
 
-__global__ void pcg_check_kernel(double *scal, double *hist, cudaGraphConditionalHandle hw, int use_graph) {
-  pdl_prologue();
+__device__ void pcg_check(double *scal, double *hist, cudaGraphConditionalHandle hw, int use_graph) {
   const double rz = scal[0], pq = scal[1];
   int it = (int)scal[6];
   double status = 0.0;
@@ -349,6 +331,47 @@ __global__ void pcg_check_kernel(double *scal, double *hist, cudaGraphConditiona
   }
   scal[7] = status;
   if (use_graph) cudaGraphSetConditional(hw, status == 0.0 ? 1u : 0u);
+}
+
+__global__ void pcg_check_kernel(double *scal, double *hist, cudaGraphConditionalHandle hw, int use_graph) {
+  pdl_prologue();
+  pcg_check(scal, hist, hw, use_graph);
+}
+
+// check >= 0: one rank -- the last block also runs the stopping test (check = use_graph)
+__global__ void update_xr_rr_kernel(double *x, double *r, const double *p, const double *q, const double *mask,
+                                    int64_t n, double *scal, double *part, unsigned *ticket, double *dst,
+                                    double *hist, cudaGraphConditionalHandle hw, int check) {
+  pdl_prologue();
+  const double alpha = scal[0] / scal[1];
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    v += mask ? mask[i] * (ri * ri) : ri * ri;
+  }
+  if (block_reduce_last(v, part, ticket, dst) && check >= 0) pcg_check(scal, hist, hw, check);
+}
+
+// q[g] = sum over the CSR sources of g, fused with the partial of p.q (C3 after the launch)
+__global__ void gather_src_dot_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ idx,
+                                      const double *__restrict__ src, int64_t n, double *out,
+                                      const double *__restrict__ p, const double *__restrict__ mask, int64_t n_all,
+                                      double *part, unsigned *ticket, double *dst) {
+  pdl_prologue();
+  double acc = 0.0;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_all; g += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (g < n) {
+      for (int64_t q = ptr[g]; q < ptr[g + 1]; ++q) v += src[idx[q]];
+      out[g] = v;
+    } else {
+      v = out[g];      // the p0 rows, written by chunk_sum_b0
+    }
+    acc += mask ? mask[g] * (p[g] * v) : p[g] * v;
+  }
+  block_reduce_last(acc, part, ticket, dst);
 }
 
 // deluxe restriction / extension per active slot: out[j] = sum_i M[i nd + j] in[i], M row-major
@@ -817,7 +840,7 @@ static void dot(vb_ctx *c, const double *a, const double *b, int64_t n, double *
 
 static int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
 
-static void apply_S(vb_ctx *c, SolveState *st) {   // q = S^ p  (B1, B2)
+static void apply_S(vb_ctx *c, SolveState *st, bool with_pq = false) {   // q = S^ p  (B1, B2) [+ p.q]
   cudaStream_t s = c->stream;
   tick(c, st, 3, true);
   tick(c, st, 0, true);
@@ -830,7 +853,15 @@ static void apply_S(vb_ctx *c, SolveState *st) {   // q = S^ p  (B1, B2)
                                                                      c->n_delta_glob + c->NPi, st->sx.p, c->w_q.p);
   run_slot_exchange(c, st->XS, st->sx.p, st->sx.p + c->len_G);      // C1 (cross-rank copies)
   int64_t nxp = c->n_delta_glob + c->NPi;
-  launch_pdl(st, gather_src_kernel, dim3(grid_for(nxp)), dim3(256), 0, s, st->xptr.p, st->xidx.p, st->sx.p, nxp, c->w_q.p);
+  if (with_pq) {   // q and the partial of p.q in one pass (C3 follows)
+    launch_pdl(st, gather_src_dot_kernel, dim3(DOT_BLOCKS), dim3(256), 0, s, st->xptr.p, st->xidx.p, st->sx.p, nxp,
+               c->w_q.p, c->w_p.p, c->nranks > 1 ? st->mask.p : nullptr, c->nx, c->w_dots.p, st->ticket.p,
+               c->w_scal.p + 1);
+    allreduce_sum_fixed(c, c->w_scal.p + 1, 1);
+  } else {
+    launch_pdl(st, gather_src_kernel, dim3(grid_for(nxp)), dim3(256), 0, s, st->xptr.p, st->xidx.p, st->sx.p, nxp,
+               c->w_q.p);
+  }
   tick(c, st, 3, false);
   VB_STAGE();
 }
@@ -1294,13 +1325,16 @@ static void pcg_step(vb_ctx *c, SolveState *st, cudaGraphConditionalHandle hw, b
   cudaStream_t s = c->stream;
   double *sc = c->w_scal.p;
   const int64_t nx = c->nx;
-  apply_S(c, st);
-  dot(c, c->w_p.p, c->w_q.p, nx, sc + 1);
+  apply_S(c, st, true);                                   // q = S^ p and p.q
+  // x, r update fused with r.r; one rank: the last block also runs the stopping test
+  const int check = c->nranks == 1 ? (graph ? 1 : 0) : -1;
   launch_pdl(st, update_xr_rr_kernel, dim3(DOT_BLOCKS), dim3(256), 0, s, c->w_x.p, c->w_r.p, c->w_p.p, c->w_q.p,
-                                                 c->nranks > 1 ? st->mask.p : nullptr, nx, sc, c->w_dots.p,
-                                                 st->ticket.p, sc + 2);
-  allreduce_sum_fixed(c, sc + 2, 1);
-  launch_pdl(st, pcg_check_kernel, dim3(1), dim3(1), 0, s, sc, st->hist.p, hw, graph ? 1 : 0);
+             c->nranks > 1 ? st->mask.p : nullptr, nx, sc, c->w_dots.p, st->ticket.p, sc + 2, st->hist.p, hw,
+             check);
+  if (check < 0) {
+    allreduce_sum_fixed(c, sc + 2, 1);
+    launch_pdl(st, pcg_check_kernel, dim3(1), dim3(1), 0, s, sc, st->hist.p, hw, graph ? 1 : 0);
+  }
   VB_STAGE();
 }
 
