@@ -112,7 +112,8 @@ class ElementSet:
         nproc = processes or min(os.cpu_count() or 1, 16)
         if len(todo) > 64 and nproc > 1:
             import multiprocessing as mp
-            with mp.get_context("fork").Pool(nproc) as pool:
+            # spawn, not fork: forking a process whose BLAS threads are running can deadlock
+            with mp.get_context("spawn").Pool(nproc) as pool:
                 ops = pool.map(_build_op, todo, chunksize=16)
         else:
             ops = [_build_op(t) for t in todo]

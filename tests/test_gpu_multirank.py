@@ -63,6 +63,7 @@ def _global_free_ids(gs):
     ("c1", {}, (2, 2, 2)),
     ("c1", dict(n=8), (1, 2, 2)),
     ("c4", dict(n=8, constraints=dict(adaptive_tau=0.0)), (2, 1, 1)),
+    ("c3", dict(n=8), (2, 1, 1)),
 ])
 def test_multirank_matches_oracle_and_single_rank(name, kw, rank_grid):
     import torch
@@ -110,19 +111,21 @@ def test_multirank_matches_oracle_and_single_rank(name, kw, rank_grid):
     assert np.linalg.norm(rR) <= 1e-8 * np.linalg.norm(bR)
 
 
-def test_multirank_adaptive():
-    """Adaptive enrichment across a rank boundary: faces shared by two ranks are solved redundantly
-    (bitwise-identical inputs), so the primal space and the iterates match the single-rank run."""
+@pytest.mark.parametrize("n,rank_grid", [(8, (2, 1, 1)), (16, (2, 2, 1))])
+def test_multirank_adaptive(n, rank_grid):
+    """Adaptive enrichment across rank boundaries: faces shared by two ranks are solved redundantly
+    (bitwise-identical inputs), so the primal space and the iterates match the single-rank run;
+    n = 16 has floating subdomains (singular face Schur complements, DESIGN A28) on the cut."""
     import torch
     import paper_2304_09770_b200 as vb
-    prob = make_problem("c4", n=8)
+    prob = make_problem("c4", n=n)
     ctx = vb.context_for(prob)
     ctx.factor()
     rhs1 = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
     ctx.build_rhs(vb.problem_args(prob), rhs1)
     x1 = torch.zeros_like(rhs1)
     rep1 = ctx.pcg_solve(rhs1, x1, rtol=1e-10)
-    outs = _run_ranks(prob, (2, 1, 1), check_operator=False)
+    outs = _run_ranks(prob, rank_grid, check_operator=False)
     for o in outs:
         assert o["rep"]["n_adaptive"] == rep1["n_adaptive"]
         assert o["rep"]["n_primal"] == rep1["n_primal"]
