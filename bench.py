@@ -306,6 +306,11 @@ def main():
                      "others": {names[1]: {"ms": loc_ms, "GBps": loc_bytes / (loc_ms / 1e3) / 1e9 if loc_ms else None},
                                 names[2]: {"ms": c_ms, "GBps": c_bytes / (c_ms / 1e3) / 1e9 if c_ms else None},
                                 names[3]: {"ms": kt[names[3]]}, names[4]: {"ms": kt[names[4]]}}},
+        "factor": {"t_s": t_factor, "dmma_gemm_flops": st["factor_gemm_flops"],
+                   "tflops": st["factor_gemm_flops"] / t_factor / 1e12,
+                   "frac_of_dmma_peak": st["factor_gemm_flops"] / t_factor / 37.2e12,
+                   "peak_note": "DMMA 37.2 TFLOP/s measured by tools/fp64_peak.cu (profiles/r01_fp64_peak.txt); "
+                                "t_s includes the non-GEMM kernels and host work of vb_factor"},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ctx.n_free,
                 "d2h_bytes_per_step": 8 * ctx.n_free, "ms_per_step": e2e_ms},
         # kernels per solve (single rank): B0 8 + init 2 + first M^-1 15 + it S-steps x 4 +

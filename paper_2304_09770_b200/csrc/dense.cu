@@ -123,8 +123,15 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmPro
       }
 }
 
+double g_gemm_flops = 0.0;   // DMMA GEMM flops issued (factor-stage accounting, single driving thread)
+
 void GemmPlan::add(const GemmProb &p) {
   if (p.M <= 0 || p.N <= 0) return;
+  {
+    double f = 2.0 * p.M * (double)p.N * p.K;
+    if (p.lower) f *= 0.5 * (1.0 + 1.0 / std::max(1, std::min(p.M, p.N)));   // lower triangle (square C)
+    g_gemm_flops += f;
+  }
   int pid = probs.size();
   probs.push_back(p);
   int tm = (p.M + GBM - 1) / GBM, tn = (p.N + GBN - 1) / GBN;

@@ -913,6 +913,7 @@ static void stage_time(vb_ctx *c, const char *name) {
 
 void factor_device(vb_ctx *c) {
   cudaStream_t s = c->stream;
+  g_gemm_flops = 0.0;
   stage_time(c, nullptr);
   stage_dirichlet(c);
   stage_time(c, "dirichlet (A1/A2)");
@@ -945,6 +946,7 @@ void factor_device(vb_ctx *c) {
   stage_time(c, "interface (A3/A4)");
   stage_dual(c, sidebuf, sumbuf);
   stage_time(c, "dual + coarse (A3-A5)");
+  c->factor_flops = g_gemm_flops;
 }
 
 }  // namespace vb
