@@ -82,7 +82,8 @@ typedef struct {
   int32_t iterations, converged;
   double r0_norm, r_final_norm, rel_residual;   /* interface residual ||r||_2        */
   double lambda_min, lambda_max, kappa;         /* Lanczos from the CG coefficients  */
-  double true_rel_residual;                     /* ||b - K x|| / ||b|| by the element operator */
+  double true_rel_residual;                     /* -1: not computed by vb_pcg_solve (one extra
+                                                   element pass); vb_apply_operator gives b - K x */
   double t_setup_s, t_factor_s, t_solve_s;
   double bytes_per_iter_model, flux_violation_max;
   int32_t n_primal, n_coarse;

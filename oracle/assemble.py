@@ -112,9 +112,21 @@ class ElementSet:
         nproc = processes or min(os.cpu_count() or 1, 16)
         if len(todo) > 64 and nproc > 1:
             import multiprocessing as mp
-            # spawn, not fork: forking a process whose BLAS threads are running can deadlock
-            with mp.get_context("spawn").Pool(nproc) as pool:
-                ops = pool.map(_build_op, todo, chunksize=16)
+            # spawn, not fork: forking a process whose BLAS threads are running can deadlock;
+            # one BLAS thread per worker (the children inherit the environment at spawn)
+            keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+            saved = {key: os.environ.get(key) for key in keys}
+            for key in keys:
+                os.environ[key] = "1"
+            try:
+                with mp.get_context("spawn").Pool(nproc) as pool:
+                    ops = pool.map(_build_op, todo, chunksize=16)
+            finally:
+                for key, v in saved.items():
+                    if v is None:
+                        os.environ.pop(key, None)
+                    else:
+                        os.environ[key] = v
         else:
             ops = [_build_op(t) for t in todo]
         self.ops = dict(zip(uniq.keys(), ops))

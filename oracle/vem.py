@@ -193,6 +193,11 @@ def d4_basis(k):
 class ElementOps:
     """All VEM operators of one cell as dense matrices acting on the local velocity DOF vector."""
 
+    def Gram(self, n1, n2):
+        """(int_K m_a m_b) for |a| <= n1, |b| <= n2 by the cell quadrature (a method, not a closure,
+        so element operators can be returned from worker processes)."""
+        return (self.Mq[:, :dim3(n1)] * self.wq[:, None]).T @ self.Mq[:, :dim3(n2)]
+
     def __init__(self, mesh, K, eidx, k, nu):
         self.k, self.nu = k, nu
         g = self.g = CellGeom(mesh, K, eidx, k)
@@ -205,8 +210,7 @@ class ElementOps:
         Mk1, Gk1 = mono3(xq, g.xc, g.h, k + 1)
         self.Mq, self.Gq, self.wq = Mk1, Gk1, wq
         d = lambda n: dim3(n)
-        Gram = lambda n1, n2: (Mk1[:, :d(n1)] * wq[:, None]).T @ Mk1[:, :d(n2)]
-        self.Gram = Gram
+        Gram = self.Gram
         # ---- (1) divergence: div v in P_{k-1} (Ṽ_h^K (iii)); moments via flux + D5
         Rdiv = np.zeros((d(k - 1), nv))
         for lf, F in enumerate(g.F):

@@ -10,12 +10,15 @@ namespace vb {
 // CTA tile 128 x 64 x 16, 8 warps (4 along M x 2 along N), warp tile 32 x 32 = 4 x 4 DMMA 8x8x4.
 // The next K-slab is prefetched from global memory into registers while the current one is
 // multiplied out of shared memory (one smem buffer, two barriers per slab).
-constexpr int GBM = 128, GBN = 64, GBK = 16;
+// CTA tile GBM x GBN x 16, 8 warps; warp tile (GBM / WARPS_M) x 32 of DMMA 8x8x4 tiles.
+constexpr int GBM = 128, GBN = 128, GBK = 16;
 constexpr int GPAD = 4;
 constexpr int GTHREADS = 256;
 constexpr int LDL_NB = 128;        // wide-panel width of the blocked LDL^T and triangular inverse
-constexpr int GA_PER = GBM * GBK / GTHREADS;   // 8
-constexpr int GB_PER = GBK * GBN / GTHREADS;   // 4
+constexpr int GWARPS_N = GBN / 32, GWARPS_M = (GTHREADS / 32) / GWARPS_N;
+constexpr int GMI = GBM / GWARPS_M / 8;         // DMMA tiles per warp along M
+constexpr int GA_PER = GBM * GBK / GTHREADS;
+constexpr int GB_PER = GBK * GBN / GTHREADS;
 
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -57,9 +60,11 @@ __device__ __forceinline__ void load_slab(const GemmProb &P, int m0, int n0, int
   }
 }
 
-// DENSE: one large problem (id = tile0) on a 2D grid of tiles (no tile list)
+// The next K-slab is prefetched from global memory into registers while the current one is
+// multiplied out of shared memory (one smem buffer, two barriers per slab).
+// DENSE: one large problem (id = tile0) on a 2D grid of tiles (no tile list).
 template <bool DENSE>
-__global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
+__global__ void __launch_bounds__(GTHREADS, 1) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
                                                                   const int4 *__restrict__ tiles, int tile0) {
   const int4 t = DENSE ? make_int4(tile0, blockIdx.y, blockIdx.x, 0) : tiles[tile0 + blockIdx.x];
   __shared__ GemmProb Ps;                 // problem descriptor in shared memory (register pressure)
@@ -71,10 +76,10 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmPro
   __shared__ double As[GBM][GBK + GPAD];
   __shared__ double Bs[GBK][GBN + GPAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  double acc[4][4][2];
+  const int wm = (warp / GWARPS_N) * (GBM / GWARPS_M), wn = (warp % GWARPS_N) * 32;
+  double acc[GMI][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < GMI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   double ra[GA_PER], rb[GB_PER];
@@ -96,20 +101,20 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmPro
     if (k0 + GBK < P.K) load_slab(P, m0, n0, k0 + GBK, tid, ra, rb);   // in flight during the DMMAs
 #pragma unroll
     for (int kk = 0; kk < GBK; kk += 4) {
-      double a[4], b[4];
+      double a[GMI], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[wm + 8 * i + (lane >> 2)][kk + (lane & 3)];
+      for (int i = 0; i < GMI; ++i) a[i] = As[wm + 8 * i + (lane >> 2)][kk + (lane & 3)];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = Bs[kk + (lane & 3)][wn + 8 * j + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < GMI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < GMI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll

@@ -1519,6 +1519,7 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
     rep->r0_norm = r0n;
     rep->r_final_norm = rn;
     rep->rel_residual = r0n > 0 ? rn / r0n : 0.0;
+    rep->true_rel_residual = -1.0;
     // Lanczos T from the CG coefficients (SURVEY O-15 index convention): beta_j pairs alpha_j, alpha_{j+1}
     std::vector<double> bb(betas.begin(), betas.end());
     double lmin = 1, lmax = 1;
