@@ -11,7 +11,7 @@ namespace vb {
 // The next K-slab is prefetched from global memory into registers while the current one is
 // multiplied out of shared memory (one smem buffer, two barriers per slab).
 // CTA tile GBM x GBN x 16, 8 warps; warp tile (GBM / WARPS_M) x 32 of DMMA 8x8x4 tiles.
-constexpr int GBM = 128, GBN = 128, GBK = 16;
+constexpr int GBM = 128, GBN = 64, GBK = 16;   // 128x128 measured slower (1 CTA/SM, padding on small N)
 constexpr int GPAD = 4;
 constexpr int GTHREADS = 256;
 constexpr int LDL_NB = 128;        // wide-panel width of the blocked LDL^T and triangular inverse
@@ -64,7 +64,7 @@ __device__ __forceinline__ void load_slab(const GemmProb &P, int m0, int n0, int
 // multiplied out of shared memory (one smem buffer, two barriers per slab).
 // DENSE: one large problem (id = tile0) on a 2D grid of tiles (no tile list).
 template <bool DENSE>
-__global__ void __launch_bounds__(GTHREADS, 1) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
+__global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
                                                                   const int4 *__restrict__ tiles, int tile0) {
   const int4 t = DENSE ? make_int4(tile0, blockIdx.y, blockIdx.x, 0) : tiles[tile0 + blockIdx.x];
   __shared__ GemmProb Ps;                 // problem descriptor in shared memory (register pressure)
