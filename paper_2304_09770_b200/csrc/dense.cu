@@ -35,33 +35,51 @@ __device__ __forceinline__ void b_coord(const GemmProb &P, int idx, int &kk, int
   if (!P.transB) { kk = idx % GBK; j = idx / GBK; } else { j = idx % GBN; kk = idx / GBN; }
 }
 
-__device__ __forceinline__ void load_slab(const GemmProb &P, int m0, int n0, int k0, int tid, double (&ra)[GA_PER],
-                                          double (&rb)[GB_PER]) {
+// ---- asynchronous K-slab loads: cp.async 8-byte copies into a 2-stage shared-memory ring
+// (zero-filled outside the matrix); the diagonal scaling d of op(A)'s columns is applied to the A
+// fragments, so A and B are copied unmodified.
+constexpr int GSTAGES = 2;
+struct GemmSmem {
+  double A[GSTAGES][GBM][GBK + GPAD];
+  double B[GSTAGES][GBK][GBN + GPAD];
+  double D[GSTAGES][GBK];
+};
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int bytes = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+__device__ __forceinline__ void issue_slab(const GemmProb &P, int m0, int n0, int k0, int tid, GemmSmem &sm,
+                                           int stage) {
 #pragma unroll
   for (int q = 0; q < GA_PER; ++q) {
     int i, kk;
     a_coord(P, tid + q * GTHREADS, i, kk);
     const int gi = m0 + i, gk = k0 + kk;
-    double v = 0.0;
-    if (gi < P.M && gk < P.K) {
-      v = P.transA ? P.A[gk + (int64_t)gi * P.lda] : P.A[gi + (int64_t)gk * P.lda];
-      if (P.d) v *= P.d[(int64_t)gk * P.dstride];
-    }
-    ra[q] = v;
+    const bool ok = gi < P.M && gk < P.K;
+    const double *src = ok ? (P.transA ? P.A + gk + (int64_t)gi * P.lda : P.A + gi + (int64_t)gk * P.lda) : P.A;
+    cp_async8(&sm.A[stage][i][kk], src, ok);
   }
 #pragma unroll
   for (int q = 0; q < GB_PER; ++q) {
     int kk, j;
     b_coord(P, tid + q * GTHREADS, kk, j);
     const int gj = n0 + j, gk = k0 + kk;
-    double v = 0.0;
-    if (gj < P.N && gk < P.K) v = P.transB ? P.B[gj + (int64_t)gk * P.ldb] : P.B[gk + (int64_t)gj * P.ldb];
-    rb[q] = v;
+    const bool ok = gj < P.N && gk < P.K;
+    const double *src = ok ? (P.transB ? P.B + gj + (int64_t)gk * P.ldb : P.B + gk + (int64_t)gj * P.ldb) : P.B;
+    cp_async8(&sm.B[stage][kk][j], src, ok);
+  }
+  if (P.d && tid < GBK) {
+    const int gk = k0 + tid;
+    const bool ok = gk < P.K;
+    cp_async8(&sm.D[stage][tid], ok ? P.d + (int64_t)gk * P.dstride : P.d, ok);
   }
 }
 
-// The next K-slab is prefetched from global memory into registers while the current one is
-// multiplied out of shared memory (one smem buffer, two barriers per slab).
 // DENSE: one large problem (id = tile0) on a 2D grid of tiles (no tile list).
 template <bool DENSE>
 __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
@@ -73,45 +91,41 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmPro
   const GemmProb &P = Ps;
   const int m0 = t.y * GBM, n0 = t.z * GBN;
   if (DENSE && P.lower && m0 + GBM - 1 < n0) return;   // tile strictly above the diagonal
-  __shared__ double As[GBM][GBK + GPAD];
-  __shared__ double Bs[GBK][GBN + GPAD];
+  extern __shared__ __align__(16) unsigned char gsm_raw[];
+  GemmSmem &sm = *reinterpret_cast<GemmSmem *>(gsm_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp / GWARPS_N) * (GBM / GWARPS_M), wn = (warp % GWARPS_N) * 32;
+  const bool scaled = P.d != nullptr;
   double acc[GMI][4][2];
 #pragma unroll
   for (int i = 0; i < GMI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  double ra[GA_PER], rb[GB_PER];
-  load_slab(P, m0, n0, 0, tid, ra, rb);
-  for (int k0 = 0; k0 < P.K; k0 += GBK) {
-#pragma unroll
-    for (int q = 0; q < GA_PER; ++q) {
-      int i, kk;
-      a_coord(P, tid + q * GTHREADS, i, kk);
-      As[i][kk] = ra[q];
-    }
-#pragma unroll
-    for (int q = 0; q < GB_PER; ++q) {
-      int kk, j;
-      b_coord(P, tid + q * GTHREADS, kk, j);
-      Bs[kk][j] = rb[q];
-    }
+  issue_slab(P, m0, n0, 0, tid, sm, 0);
+  cp_async_commit();
+  if (GBK < P.K) issue_slab(P, m0, n0, GBK, tid, sm, 1);
+  cp_async_commit();
+  int ks = 0;
+  for (int k0 = 0; k0 < P.K; k0 += GBK, ++ks) {
+    cp_async_wait1();       // all groups but the newest are complete: slab ks has landed
     __syncthreads();
-    if (k0 + GBK < P.K) load_slab(P, m0, n0, k0 + GBK, tid, ra, rb);   // in flight during the DMMAs
+    const int st = ks & 1;
 #pragma unroll
     for (int kk = 0; kk < GBK; kk += 4) {
       double a[GMI], b[4];
+      const double dk = scaled ? sm.D[st][kk + (lane & 3)] : 1.0;
 #pragma unroll
-      for (int i = 0; i < GMI; ++i) a[i] = As[wm + 8 * i + (lane >> 2)][kk + (lane & 3)];
+      for (int i = 0; i < GMI; ++i) a[i] = sm.A[st][wm + 8 * i + (lane >> 2)][kk + (lane & 3)] * dk;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk + (lane & 3)][wn + 8 * j + (lane >> 2)];
+      for (int j = 0; j < 4; ++j) b[j] = sm.B[st][kk + (lane & 3)][wn + 8 * j + (lane >> 2)];
 #pragma unroll
       for (int i = 0; i < GMI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    __syncthreads();
+    __syncthreads();        // everyone is done with stage st before it is refilled
+    if (k0 + 2 * GBK < P.K) issue_slab(P, m0, n0, k0 + 2 * GBK, tid, sm, st);
+    cp_async_commit();
   }
 #pragma unroll
   for (int i = 0; i < GMI; ++i)
@@ -126,6 +140,16 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmPro
           *c = (P.beta == 0.0 ? 0.0 : P.beta * *c) + P.alpha * acc[i][j][h];
         }
       }
+}
+
+static void gemm_kernel_attributes() {
+  static bool done = false;
+  if (done) return;
+  VB_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(GemmSmem)));
+  VB_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(GemmSmem)));
+  done = true;
 }
 
 double g_gemm_flops = 0.0;   // DMMA GEMM flops issued (factor-stage accounting, single driving thread)
@@ -161,15 +185,16 @@ void GemmPlan::upload(cudaStream_t s) {
 }
 
 void GemmPlan::run(int launch, cudaStream_t s) {
+  gemm_kernel_attributes();
   auto &L = launches[launch];
   if (L.second > 0) {
-    gemm_grouped_kernel<false><<<L.second, GTHREADS, 0, s>>>(d_probs.p, d_tiles.p, L.first);
+    gemm_grouped_kernel<false><<<L.second, GTHREADS, sizeof(GemmSmem), s>>>(d_probs.p, d_tiles.p, L.first);
     VB_CHECK_LAUNCH();
   }
   for (int pid : dense[launch]) {
     const GemmProb &p = probs[pid];
     dim3 grid((p.N + GBN - 1) / GBN, (p.M + GBM - 1) / GBM);
-    gemm_grouped_kernel<true><<<grid, GTHREADS, 0, s>>>(d_probs.p, d_tiles.p, pid);
+    gemm_grouped_kernel<true><<<grid, GTHREADS, sizeof(GemmSmem), s>>>(d_probs.p, d_tiles.p, pid);
     VB_CHECK_LAUNCH();
   }
 }
