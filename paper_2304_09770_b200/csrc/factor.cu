@@ -18,6 +18,20 @@
 
 namespace vb {
 
+
+static void stage_time(vb_ctx *c, const char *name) {
+  static const bool on = getenv("VB_FACTOR_TIMES") && atoi(getenv("VB_FACTOR_TIMES"));
+  if (!on) return;
+  static double last = 0;
+  VB_CUDA(cudaStreamSynchronize(c->stream));
+  const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  if (name) fprintf(stderr, "[vb factor rank %d] %-22s %8.3f s\n", c->rank, name, now - last);
+  last = now;
+}
+
+#define STAGE_T(name) stage_time(c, name)
+
+
 // ------------------------------------------------------------------ assembly (one CTA / subdomain)
 __global__ void assemble_kernel(const SubDev *__restrict__ subs, const int *__restrict__ sub_cells,
                                 const int *__restrict__ cell_loc, const int *__restrict__ cell_nv,
@@ -411,8 +425,10 @@ static void stage_dirichlet(vb_ctx *c) {
     const SubDev &S = c->h_sub[i];
     mats[i] = MatDesc{c->d_K.p + S.off_K, S.n, S.n, S.nD};
   }
+  STAGE_T("  assembly");
   ldl_partial_batched(mats, c->d_info.p, s);
   check_info(c, N, "subdomain Dirichlet LDL^T (A1)");
+  STAGE_T("  Dirichlet LDL^T");
   std::vector<MatDesc> sg(N);
   for (int i = 0; i < N; ++i) {
     const SubDev &S = c->h_sub[i];
@@ -441,6 +457,7 @@ static void stage_dirichlet(vb_ctx *c) {
       td[i] = TriDesc{c->d_K.p + S.off_K, S.n, WD.p + offWD[i], S.nD, S.nD};
     }
     tri_inverse_batched(td, s);
+    STAGE_T("  L_DD^-1");
     dD.alloc(c->len_Dn);
     {
       std::vector<DiagDesc> dd;
@@ -901,16 +918,6 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
 }
 
 // VB_FACTOR_TIMES=1: wall time of each factor stage on stderr (the stages synchronise)
-static void stage_time(vb_ctx *c, const char *name) {
-  static const bool on = getenv("VB_FACTOR_TIMES") && atoi(getenv("VB_FACTOR_TIMES"));
-  if (!on) return;
-  static double last = 0;
-  VB_CUDA(cudaStreamSynchronize(c->stream));
-  const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-  if (name) fprintf(stderr, "[vb factor rank %d] %-22s %8.3f s\n", c->rank, name, now - last);
-  last = now;
-}
-
 void factor_device(vb_ctx *c) {
   cudaStream_t s = c->stream;
   g_gemm_flops = 0.0;
