@@ -18,6 +18,11 @@
 
 namespace vb {
 
+double g_malloc_s = 0.0, g_free_s = 0.0;
+double wall_now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 
 static void stage_time(vb_ctx *c, const char *name) {
   static const bool on = getenv("VB_FACTOR_TIMES") && atoi(getenv("VB_FACTOR_TIMES"));
@@ -25,7 +30,9 @@ static void stage_time(vb_ctx *c, const char *name) {
   static double last = 0;
   VB_CUDA(cudaStreamSynchronize(c->stream));
   const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-  if (name) fprintf(stderr, "[vb factor rank %d] %-22s %8.3f s\n", c->rank, name, now - last);
+  if (name)
+    fprintf(stderr, "[vb factor rank %d] %-22s %8.3f s  (cumulative cudaMalloc %.3f s, cudaFree %.3f s)\n", c->rank,
+            name, now - last, g_malloc_s, g_free_s);
   last = now;
 }
 

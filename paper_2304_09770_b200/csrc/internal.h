@@ -35,6 +35,10 @@ struct Error {
   } while (0)
 
 // ------------------------------------------------------------------ device buffer
+// cumulative wall time (s) spent in cudaMalloc / cudaFree by DBuf (diagnostics, VB_FACTOR_TIMES)
+extern double g_malloc_s, g_free_s;
+double wall_now();
+
 template <class T>
 struct DBuf {
   T *p = nullptr;
@@ -44,14 +48,20 @@ struct DBuf {
   DBuf &operator=(const DBuf &) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      const double t0 = wall_now();
+      cudaFree(p);
+      g_free_s += wall_now() - t0;
+    }
     p = nullptr;
     n = 0;
   }
   void alloc(size_t count) {
     release();
     if (count == 0) return;
+    const double t0 = wall_now();
     cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    g_malloc_s += wall_now() - t0;
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       throw Error{VB_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed"};
