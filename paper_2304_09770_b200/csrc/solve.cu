@@ -47,7 +47,9 @@ constexpr int GV_WARPS_C = 8;    // the single coarse matrix (one CTA per SM)
 // BIG: vectors too long for shared memory (large coarse problems): x is read through the L2 (it is
 // small next to the streamed matrix) and the partial output accumulates in the CTA's own global
 // partial vector (each column J is owned by one warp, so there are no races).
-template <int GV_WARPS, bool BIG = false>
+// PAIR: each warp streams two tiles per step (twice the loads in flight; for the coarse matrix,
+// which runs one CTA per SM)
+template <int GV_WARPS, bool BIG = false, bool PAIR = false>
 __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork *__restrict__ work) {
   pdl_prologue();
   extern __shared__ double sm[];
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
 #pragma unroll
     for (int r = 0; r < 32; ++r) rsum[r] = 0.0;
     const double xI_lane = X(32 * I + lane);
-    for (int J = warp; J <= I; J += GV_WARPS) {
+    for (int J = warp; J <= I; J += (PAIR ? 2 : 1) * GV_WARPS) {
       const double *T = W.M + ptile_off(n, I, J);
       double t[32];
       if (rows == 32) {
@@ -89,6 +91,13 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
 #pragma unroll
         for (int r = 0; r < 32; ++r) t[r] = r < rows ? __ldg(T + r * 32 + lane) : 0.0;
       }
+      const int J2 = J + GV_WARPS;
+      double t2[PAIR ? 32 : 1];
+      if (PAIR) {
+        const double *T2 = W.M + ptile_off(n, I, J2 <= I ? J2 : J);
+#pragma unroll
+        for (int r = 0; r < 32; ++r) t2[r] = (J2 <= I && r < rows) ? __ldg(T2 + r * 32 + lane) : 0.0;
+      }
       const double xJ = X(32 * J + lane);
       double csum = 0.0;
 #pragma unroll
@@ -97,6 +106,16 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
         csum += t[r] * __shfl_sync(FULL, xI_lane, r);
       }
       if (J < I && (!BIG || 32 * J + lane < n)) ys[32 * J + lane] += csum;   // transpose part, one warp per J
+      if (PAIR && J2 <= I) {
+        const double xJ2 = X(32 * J2 + lane);
+        double csum2 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          rsum[r] += t2[r] * xJ2;
+          csum2 += t2[r] * __shfl_sync(FULL, xI_lane, r);
+        }
+        if (J2 < I && (!BIG || 32 * J2 + lane < n)) ys[32 * J2 + lane] += csum2;
+      }
     }
     // transpose-reduce rsum across lanes: lane l ends with sum over lanes of rsum[l]
 #pragma unroll
@@ -913,9 +932,9 @@ static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
     c->comm->allgather(st->ucl.p, c->w_uc.p, c->coarse_rows, s2);
   } else {
   if (st->big_c)
-    launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, true>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), GV_WARPS_C * 32 * sizeof(double), s2, st->w_c.p);
+    launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, true, true>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), GV_WARPS_C * 32 * sizeof(double), s2, st->w_c.p);
   else
-    launch_pdl(st, sym_gemv_kernel<GV_WARPS_C>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), st->sm_c, s2, st->w_c.p);
+    launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, false, true>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), st->sm_c, s2, st->w_c.p);
   tick(c, st, 2, false, s2);
   launch_pdl(st, sum_chunks_kernel, dim3((c->Nc + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
   }
@@ -1023,7 +1042,8 @@ void prepare_solve(vb_ctx *c) {
   VB_REQUIRE(smmax <= 227 * 1024, VB_EINVAL, "packed GEMV vector exceeds shared memory (subdomain interface too large)");
   VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smmax));
   if (!st->big_c)
-    VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS_C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st->sm_c));
+    VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS_C, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)st->sm_c));
   // deluxe restriction / extension shared memory (vector + per-warp partials)
   int maxnd_e = 1;
   for (auto &E : c->h_ent)

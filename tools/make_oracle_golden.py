@@ -28,7 +28,9 @@ def make(name, outdir=None):
     t0 = time.time()
     prob = make_problem(name)
     gs = GlobalSystem(prob)
+    print(name, "system assembled %.0f s" % (time.time() - t0), flush=True)
     bd = BDDC(gs)
+    print(name, "BDDC set up %.0f s" % (time.time() - t0), flush=True)
     u, p, rep = bd.solve(rtol=1e-10)
     x = np.concatenate([u, p])
     rng = np.random.default_rng(12345)
