@@ -228,19 +228,6 @@ __global__ void multiplicity_kernel(const SlotDev *__restrict__ slots, const Ent
     Dlx[s.off_Dlx + idx] = (idx % s.nd == idx / s.nd) ? v : 0.0;
 }
 
-// column-major nd x nd deluxe block -> row-major (unpadded)
-__global__ void transpose_slot_kernel(const SlotDev *__restrict__ slots, const int *__restrict__ act,
-                                      const double *__restrict__ Dlx, double *Dt) {
-  const SlotDev s = slots[act[blockIdx.y]];
-  const int nd = s.nd;
-  const double *D = Dlx + s.off_Dlx;
-  double *out = Dt + s.off_Dt;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nd * nd; idx += gridDim.x * blockDim.x) {
-    const int i = idx / nd, j = idx % nd;     // out row-major (i, j)
-    out[idx] = D[i + (int64_t)j * nd];
-  }
-}
-
 // batched: out[o_b + i] = 1 / A_b(i, i) for the matrices described by MatDesc (A, n = order, ld)
 struct DiagDesc {
   const double *A;
@@ -694,15 +681,6 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     plan.run(l0, s);
     sync(c);
   }
-  c->d_SDi.alloc(c->len_SDi);
-  {
-    std::vector<PackDesc> pk(N);
-    for (int i = 0; i < N; ++i) {
-      const SubDev &S = c->h_sub[i];
-      pk[i] = PackDesc{Y.p + S.off_X, S.nd, S.nd, c->d_SDi.p + S.off_SDi};
-    }
-    pack_tiles_batched(pk, s);
-  }
   // ---------------- b~0 and the benign check
   c->d_b0T.alloc(std::max<int64_t>(c->len_Pi, 1));
   c->d_b0T.zero(s);
@@ -778,27 +756,84 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
       sync(c);
     }
   }
-  // ---------------- deluxe blocks: also row-major (= D^T column-major) for the restriction
+  // ---------------- active slots / entities
   {
     std::vector<int> act_s, act_e;
-    for (int q = 0; q < nslot; ++q) {
-      SlotDev &sl = c->h_slot[q];
-      sl.off_Dt = sl.off_Dlx;
-      if (sl.nd) act_s.push_back(q);
-    }
+    for (int q = 0; q < nslot; ++q)
+      if (c->h_slot[q].nd) act_s.push_back(q);
     for (int e = 0; e < nent; ++e)
       if (c->h_ent[e].nd) act_e.push_back(e);
-    c->d_Dt.alloc(std::max<int64_t>(c->len_Dlx, 1));
-    c->d_slot.upload(c->h_slot, s);
     c->d_act_slots.upload(act_s, s);
     c->d_act_ents.upload(act_e, s);
     c->n_act_slots = act_s.size();
     c->n_act_ents = act_e.size();
-    if (c->n_act_slots) {
-      transpose_slot_kernel<<<dim3(16, c->n_act_slots), 256, 0, s>>>(c->d_slot.p, c->d_act_slots.p, c->d_Dlx.p, c->d_Dt.p);
-      VB_STAGE();
-    }
   }
+  // ---------------- deluxe scaling folded into the per-iteration operators (DESIGN.md "scaled local
+  // operators"): with D^(m) = blockdiag over the dual slots of D_G^(m), the local part of M^-1 is
+  // D S_DD^-1 D^T and the coarse basis enters as D Phi, so the iteration never applies D itself:
+  //   S^_DD = D (S_DD^-1) D^T  (packed into d_SDi),  Phi^ = D Phi  (replaces d_Phi).
+  {
+    std::vector<MatDesc> ym;
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      if (S.nd) ym.push_back(MatDesc{Y.p + S.off_X, S.nd, S.nd, 0});
+    }
+    symmetrize_lower_batched(ym, s);
+    DBuf<double> PhiH;
+    PhiH.alloc(std::max<int64_t>(c->len_Phi, 1));
+    {
+      GemmPlan plan;
+      int l0 = plan.begin_launch();
+      for (int q = 0; q < nslot; ++q) {        // Z = D Y (row blocks), Phi^ = D Phi (row blocks)
+        const SlotDev &sl = c->h_slot[q];
+        if (!sl.nd) continue;
+        const SubDev &S = c->h_sub[sl.sub];
+        GemmProb p{};
+        p.A = c->d_Dlx.p + sl.off_Dlx; p.lda = sl.nd;
+        p.B = Y.p + S.off_X + sl.offD; p.ldb = S.nd;
+        p.C = X.p + S.off_X + sl.offD; p.ldc = S.nd;
+        p.M = sl.nd; p.N = S.nd; p.K = sl.nd; p.alpha = 1.0; p.beta = 0.0;
+        plan.add(p);
+        if (S.npi) {
+          GemmProb f{};
+          f.A = c->d_Dlx.p + sl.off_Dlx; f.lda = sl.nd;
+          f.B = c->d_Phi.p + S.off_Phi + sl.offD; f.ldb = S.nd;
+          f.C = PhiH.p + S.off_Phi + sl.offD; f.ldc = S.nd;
+          f.M = sl.nd; f.N = S.npi; f.K = sl.nd; f.alpha = 1.0; f.beta = 0.0;
+          plan.add(f);
+        }
+      }
+      int l1 = plan.begin_launch();
+      for (int q = 0; q < nslot; ++q) {        // S^ = Z D^T (column blocks)
+        const SlotDev &sl = c->h_slot[q];
+        if (!sl.nd) continue;
+        const SubDev &S = c->h_sub[sl.sub];
+        GemmProb p{};
+        p.A = X.p + S.off_X + (int64_t)sl.offD * S.nd; p.lda = S.nd;
+        p.B = c->d_Dlx.p + sl.off_Dlx; p.ldb = sl.nd; p.transB = 1;
+        p.C = Y.p + S.off_X + (int64_t)sl.offD * S.nd; p.ldc = S.nd;
+        p.M = S.nd; p.N = sl.nd; p.K = sl.nd; p.alpha = 1.0; p.beta = 0.0;
+        plan.add(p);
+      }
+      plan.upload(s);
+      plan.run(l0, s);
+      plan.run(l1, s);
+      sync(c);
+    }
+    if (c->len_Phi) VB_CUDA(cudaMemcpyAsync(c->d_Phi.p, PhiH.p, c->len_Phi * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    sync(c);
+  }
+  c->d_SDi.alloc(c->len_SDi);
+  {
+    std::vector<PackDesc> pk(N);
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      pk[i] = PackDesc{Y.p + S.off_X, S.nd, S.nd, c->d_SDi.p + S.off_SDi};
+    }
+    pack_tiles_batched(pk, s);
+  }
+  VB_STAGE();
+  c->d_Dlx.release();
   // ---------------- A5: coarse saddle matrix on (u_Pi, p_0) of ALL subdomains, dense inverse
   //   C4: every rank gathers every subdomain's (S_c, b~0) and assembles/factors the same matrix
   const int Ng = c->Ng;

@@ -185,7 +185,6 @@ struct SlotDev {              // one (entity, sharer) pair; slots are entity-maj
   int64_t off_T;              // T_G of the entity
   int64_t off_Dlx;            // deluxe block D_G^(sub) (nd x nd, column-major)
   int64_t off_side;           // scratch for S_GD^(sub)
-  int64_t off_Dt;             // D_G^(sub) as row-major 32x32 tiles (nt x nt, zero padded)
 };
 
 struct EntDev {
@@ -267,10 +266,9 @@ struct vb_ctx {
   int max_npi = 0, geo_stride = 0;
   std::vector<double> cellgeo;       // host copy of d_cellgeo
   vb::DBuf<double> d_K;              // subdomain dense matrices
-  vb::DBuf<double> d_ST, d_STp, d_SDi, d_Phi, d_Sc, d_Psi, d_KDi;
+  vb::DBuf<double> d_ST, d_STp, d_SDi /* D S_DD^-1 D^T */, d_Phi /* D Phi */, d_Sc, d_Psi, d_KDi;
   int64_t len_KDi = 0;
   vb::DBuf<double> d_T, d_C, d_Dlx;  // per-entity T_G, constraint rows, deluxe blocks
-  vb::DBuf<double> d_Dt;             // deluxe blocks as row-major 32x32 tiles (per-iteration layout)
   vb::DBuf<int> d_act_slots, d_act_ents;   // slots / entities with a dual part (nd > 0)
   int n_act_slots = 0, n_act_ents = 0;
   vb::DBuf<double> d_Kc, d_Kcp;      // coarse dense & packed inverse

@@ -393,46 +393,17 @@ __global__ void gather_src_dot_kernel(const int64_t *__restrict__ ptr, const int
   block_reduce_last(acc, part, ticket, dst);
 }
 
-// deluxe restriction / extension per active slot: out[j] = sum_i M[i nd + j] in[i], M row-major
-// nd x nd, unpadded: thread per column j, rows streamed coalesced (4 independent accumulators, fixed
-// order).  Restriction: M = D^(m) row-major, giving D^T r_e; extension: M = D^(m)
-// column-major (= (D^(m))^T row-major), giving D^(m) w^(m).
-struct DlxDesc {
-  int64_t moff, in_off, out_off;
-  int nd, pad;
-};
-
-__global__ void __launch_bounds__(256) dlx_apply_kernel(const DlxDesc *__restrict__ desc, const double *__restrict__ M,
-                                                        const double *__restrict__ in, double *out) {
-  pdl_prologue();
-  extern __shared__ double xs[];
-  const DlxDesc D = desc[blockIdx.x];
-  const int nd = D.nd;
-  for (int i = threadIdx.x; i < nd; i += blockDim.x) xs[i] = in[D.in_off + i];
-  __syncthreads();
-  for (int j = threadIdx.x; j < nd; j += blockDim.x) {
-    const double *m = M + D.moff + j;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int i = 0;
-    for (; i + 3 < nd; i += 4) {
-      a0 += __ldg(m + (int64_t)i * nd) * xs[i];
-      a1 += __ldg(m + (int64_t)(i + 1) * nd) * xs[i + 1];
-      a2 += __ldg(m + (int64_t)(i + 2) * nd) * xs[i + 2];
-      a3 += __ldg(m + (int64_t)(i + 3) * nd) * xs[i + 3];
-    }
-    for (; i < nd; ++i) a0 += __ldg(m + (int64_t)i * nd) * xs[i];
-    out[D.out_off + j] = (a0 + a1) + (a2 + a3);
-  }
-}
-
-// c_i = Phi_i^T rD_i (coarse rhs pieces): PHIT_SPLIT CTAs per subdomain, warp per primal column
+// c_i = Phi^_i^T r_i = Phi_i^T D^T r_i (coarse rhs pieces, Phi^ = D Phi, r_i = the dual coordinates of
+// subdomain i gathered from r): PHIT_SPLIT CTAs per subdomain, warp per primal column
 constexpr int PHIT_SPLIT = 4;
 __global__ void __launch_bounds__(256) phit_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
-                            const double *__restrict__ rD, double *cpart) {
+                            const int64_t *__restrict__ loc2x, const double *__restrict__ r, double *cpart) {
   pdl_prologue();
+  extern __shared__ double x[];
   const SubDev S = subs[blockIdx.y];
   const double *F = Phi + S.off_Phi;
-  const double *x = rD + S.off_Dv;
+  for (int j = threadIdx.x; j < S.nd; j += blockDim.x) x[j] = r[loc2x[S.off_G + j]];
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int a = blockIdx.x * nw + warp; a < S.npi; a += gridDim.x * nw) {
     const double *col = F + (int64_t)a * S.nd;
@@ -471,7 +442,8 @@ __global__ void coarse_p0_project_kernel(const double *__restrict__ vol, int N, 
   for (int i = threadIdx.x; i < N; i += blockDim.x) v[i] -= mode == 0 ? vol[i] * mean : mean;
 }
 
-// w_i = sum_chunks y_i + Phi_i u_Pi^(i)   (thread per row of column-major Phi, 4 accumulators)
+// t_i = sum_chunks y_i + Phi^_i u_Pi^(i) = D (S_DD^-1 D^T r_i + Phi_i u_Pi^(i)), the scaled extension
+// product of subdomain i (thread per row of column-major Phi^, 4 accumulators)
 __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
                               const double *__restrict__ part, int64_t part_stride, int P,
                               const int64_t *__restrict__ pi_glob, const double *__restrict__ uc, double *w) {
@@ -736,20 +708,16 @@ struct SolveState {
   int nw_op = 0, nw_loc = 0, nw_c = 0, nw_kd = 0, max_nd = 1;
   bool big_c = false;                // coarse vectors exceed shared memory: BIG GEMV variant
   int c_chunks = 1;                  // distributed coarse: column chunks of the row-block GEMV
-  DBuf<DlxDesc> dlx_r, dlx_e;        // deluxe restriction / extension descriptors (active slots)
-  int dlx_threads = 32;
-  size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_rx = 0, sm_ex = 0, sm_kd = 0;
+  size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_ex = 0, sm_kd = 0;
   DBuf<int64_t> xptr, xidx;          // B2: x coordinate <- copies (local s or received), sharer order
   DBuf<int64_t> pptr, pidx;          // B6: global coarse index <- coarse pieces, fixed order
   DBuf<int64_t> cpack, zmap;         // coarse piece packing (r0, owned r_Pi); z tail <- u_c
-  DBuf<int64_t> toff;                // per slot: offset of its extension product
   DBuf<double> hist, mask, gvol;
   DBuf<double> sx;                   // [s (len_G) | received copies]
-  DBuf<double> tx;                   // [slot products | received]
   DBuf<double> cbuf, cgath;          // coarse pieces (local), gathered (nranks x cmax)
   DBuf<double> ucl;                  // distributed coarse: this rank's rows of u_c
   DBuf<double> gam2, gbuf, hbuf;     // B0: entity-major b_e; [zG | received]; DOF halo receive
-  int64_t cmax = 0, len_t = 0;
+  int64_t cmax = 0;
   SlotExchange XS, XE, XB, XH, XR;   // apply_S copies, extension products, B0 zG, DOF halo, rank partials
   EntitySum ESE, ESB, ESR;
   DBuf<int64_t> gh_dst;              // DOF halo: destination free ids of received owner values
@@ -902,9 +870,6 @@ static void trace_norm(vb_ctx *c, const char *name, const double *v, int64_t n, 
 static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   cudaStream_t s = c->stream, s2 = st->s2;
   tick(c, st, 4, true);
-  if (c->n_act_slots)
-    launch_pdl(st, dlx_apply_kernel, dim3(c->n_act_slots), dim3(st->dlx_threads), st->sm_rx, s, st->dlx_r.p, c->d_Dt.p, c->w_r.p, c->w_locD.p);
-  trace_norm(c, "rD", c->w_locD.p, c->len_Dv, false);
   // fork: the coarse branch (B6) runs on s2 while the local dual solves (B5) stream on s
   VB_CUDA(cudaEventRecord(st->ev_fork, s));
   VB_CUDA(cudaStreamWaitEvent(s2, st->ev_fork, 0));
@@ -912,7 +877,8 @@ static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   if (st->nw_loc) launch_pdl(st, sym_gemv_kernel<GV_WARPS>, dim3(st->nw_loc), dim3(GV_WARPS * 32), st->sm_loc, s, st->w_loc.p);
   tick(c, st, 1, false);
   // coarse pieces (C2): [Phi_i^T rD_i per local subdomain | r0_i | r_Pi of the owned entities]
-  launch_pdl(st, phit_kernel, dim3(PHIT_SPLIT, c->N), dim3(256), 0, s2, c->d_sub.p, c->d_Phi.p, c->w_locD.p, st->cbuf.p);
+  launch_pdl(st, phit_kernel, dim3(PHIT_SPLIT, c->N), dim3(256), st->max_nd * sizeof(double), s2, c->d_sub.p, c->d_Phi.p,
+             c->d_loc2x.p, c->w_r.p, st->cbuf.p);
   dev_gather(c->w_r.p, st->cpack.p, (int64_t)st->cpack.n, st->cbuf.p + c->len_Pi, s2);
   const double *pieces = st->cbuf.p;
   if (c->nranks > 1) {
@@ -944,12 +910,9 @@ static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   trace_norm(c, "uc", c->w_uc.p, c->Nc, true);
   launch_pdl(st, local2_kernel, dim3((st->max_nd + 127) / 128, c->N), dim3(128), c->max_npi * sizeof(double), s,
       c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p);
-  trace_norm(c, "w", c->w_locD.p, c->len_Dv, false);
-  if (c->n_act_slots)
-    launch_pdl(st, dlx_apply_kernel, dim3(c->n_act_slots), dim3(st->dlx_threads), st->sm_rx, s, st->dlx_e.p, c->d_Dlx.p, c->w_locD.p, st->tx.p);
-  run_slot_exchange(c, st->XE, st->tx.p, st->tx.p + st->len_t);    // C1 (cross-rank products)
-  trace_norm(c, "t", st->tx.p, st->len_t, false);
-  run_entity_sum(c, st->ESE, st->tx.p, c->w_z.p);
+  trace_norm(c, "t", c->w_locD.p, c->len_Dv, false);
+  run_slot_exchange(c, st->XE, c->w_locD.p, c->w_locD.p + c->len_Dv);    // C1 (cross-rank products)
+  run_entity_sum(c, st->ESE, c->w_locD.p, c->w_z.p);
   trace_norm(c, "zdual", c->w_z.p, c->n_delta_glob, false);
   dev_gather(c->w_uc.p, st->zmap.p, c->NPi + c->N, c->w_z.p + c->n_delta_glob, s);
   tick(c, st, 4, false);
@@ -1019,7 +982,7 @@ void prepare_solve(vb_ctx *c) {
     nmaxD = std::max<size_t>(nmaxD, S.nd);
     split_rows(S.nd, c->P_loc, rows);
     for (int q = 0; q < c->P_loc; ++q)
-      wl.push_back(GemvWork{c->d_SDi.p + S.off_SDi, nullptr, c->w_locD.p + S.off_Dv,
+      wl.push_back(GemvWork{c->d_SDi.p + S.off_SDi, c->d_loc2x.p + S.off_G, c->w_r.p,
                             c->w_locY.p + (int64_t)q * c->len_Dv + S.off_Dv, S.nd, rows[q].first, rows[q].second, 0});
   }
   // sub-domains with nd = 0 still need zero partials
@@ -1044,13 +1007,9 @@ void prepare_solve(vb_ctx *c) {
   if (!st->big_c)
     VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS_C, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)st->sm_c));
-  // deluxe restriction / extension shared memory (vector + per-warp partials)
-  int maxnd_e = 1;
-  for (auto &E : c->h_ent)
-    if (E.nd) maxnd_e = std::max(maxnd_e, E.nd);
-  st->sm_rx = (size_t)maxnd_e * sizeof(double);
-  st->dlx_threads = std::min(256, (maxnd_e + 31) / 32 * 32);
   st->max_nd = nmaxD;
+  if (st->max_nd * sizeof(double) > 48 * 1024)
+    VB_CUDA(cudaFuncSetAttribute(phit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(st->max_nd * sizeof(double))));
   const int ne = c->ents.size();
   // ---------------- B2 (apply_S): copies of each x coordinate, local and received, in sharer order
   {
@@ -1086,32 +1045,16 @@ void prepare_solve(vb_ctx *c) {
     });
     build_csr(c->n_delta_glob + c->NPi, pr, st->xptr, st->xidx, s);
   }
-  // ---------------- B7 (extension): per-slot products and their sums over all sharers
+  // ---------------- B7 (extension): per-slot scaled products (in w_locD, subdomain-major) and their
+  // sums over all sharers
   {
-    std::vector<int64_t> toff(c->h_slot.size(), 0);
-    int64_t o = 0;
-    for (size_t q = 0; q < c->h_slot.size(); ++q) { toff[q] = o; o += c->h_slot[q].nd; }
-    st->len_t = o;
-    st->toff.upload(toff, s);
-    // deluxe descriptors of the active slots (same order as d_act_slots)
-    std::vector<DlxDesc> dr, de;
-    for (size_t q = 0; q < c->h_slot.size(); ++q) {
-      const SlotDev &sl = c->h_slot[q];
-      if (!sl.nd) continue;
-      const SubDev &S = c->h_sub[sl.sub];
-      const int64_t wl = S.off_Dv + sl.offD;
-      dr.push_back(DlxDesc{sl.off_Dt, c->h_ent[sl.ent].off_xd, wl, sl.nd, 0});
-      de.push_back(DlxDesc{sl.off_Dlx, wl, toff[q], sl.nd, 0});
-    }
-    st->dlx_r.upload(dr, s);
-    st->dlx_e.upload(de, s);
     auto L = [&](int e) { return (int64_t)c->h_ent[e].nd; };
+    auto tb = [&](int sl) { return c->h_sub[c->h_slot[sl].sub].off_Dv + c->h_slot[sl].offD; };
     build_slot_exchange(c, st->XE, L, [&](int sl, std::vector<int64_t> &out) {
-      for (int t = 0; t < c->h_slot[sl].nd; ++t) out.push_back(toff[sl] + t);
+      for (int t = 0; t < c->h_slot[sl].nd; ++t) out.push_back(tb(sl) + t);
     });
-    st->tx.alloc(std::max<int64_t>(st->len_t + st->XE.recv_len, 1));
-    build_entity_sum(c, st->ESE, st->XE, L, [&](int sl) { return toff[sl]; }, st->len_t,
-                     [&](int e) { return c->h_ent[e].off_xd; });
+    c->w_locD.alloc(std::max<int64_t>(c->len_Dv + st->XE.recv_len, 1));
+    build_entity_sum(c, st->ESE, st->XE, L, tb, c->len_Dv, [&](int e) { return c->h_ent[e].off_xd; });
   }
   // ---------------- B0: zG copies of each entity DOF, summed over all sharers after b_e
   {
@@ -1264,7 +1207,7 @@ void prepare_solve(vb_ctx *c) {
   for (auto &S : c->h_sub) {
     b += 8.0 * packed_size(S.nG) + 8.0 * packed_size(S.nd) + 2 * 8.0 * S.nd * S.npi;
   }
-  for (auto &sl : c->h_slot) b += 2 * 8.0 * sl.nd * sl.nd;
+  // (the deluxe blocks are folded into S_DD^-1 and Phi at factor time: no per-iteration D traffic)
   b += c->nranks > 1 ? 8.0 * c->coarse_rows * c->Nc : 8.0 * packed_size(c->Nc);
   c->bytes_per_iter = b;
 }
