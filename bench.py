@@ -37,9 +37,9 @@ def _peaks():
 
 def _ncu_traffic(role_key="S_T packed GEMV"):
     """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu --set full
-    capture (profiles/*ncu_full_sym_gemv.json), or None."""
+    capture (the latest profiles/r*_ncu_full_*.json), or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full_sym_gemv.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_*.json")))
     if not files:
         return None, None
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -313,10 +313,10 @@ def main():
                                 "t_s includes the non-GEMM kernels and host work of vb_factor"},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ctx.n_free,
                 "d2h_bytes_per_step": 8 * ctx.n_free, "ms_per_step": e2e_ms},
-        # kernels per solve (single rank): B0 8 + init 2 + first M^-1 15 + it S-steps x 4 +
-        # (it-1) M-steps x 16 + B8 6 = 15 + 20 it (cross-checked against the ncu launch list of a
+        # kernels per solve (single rank): 15 + 18 it (deluxe folded into the operators;
+        # cross-checked against the ncu launch list of a
         # host-driven solve in profiles/); multi-rank adds the exchange pack/sum kernels
-        "gpu_launches": int(args.steps * (15 + 20 * it)),
+        "gpu_launches": int(args.steps * (15 + 18 * it)),
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

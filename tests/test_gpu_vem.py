@@ -119,9 +119,10 @@ def check_against_golden(ctx, rhs, x, rep, name):
     return meta
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2"])
 def test_full_size_parity(name):
-    """BASELINE configs 2 and 3 at full size, GPU product path vs the stored oracle solve."""
+    """BASELINE config 2 at full size, GPU product path vs the stored oracle solve (config 3 at full
+    size needs ~200 GB of dense oracle subdomain matrices: test_c3_full_size_properties)."""
     import torch
     import paper_2304_09770_b200 as vb
     prob = make_problem(name)
@@ -165,3 +166,38 @@ def test_c5_full_size_properties():
     nb = np.linalg.norm(rhs.cpu().numpy())
     assert np.linalg.norm(res[:ctx.n_vel]) <= 1e-8 * nb
     assert np.linalg.norm(res[ctx.n_vel:]) <= 1e-8 * nb     # B u = g (discrete div-free)
+
+
+def test_c3_full_size_properties():
+    """Config 3 at full size (k = 3, triangulated faces, jittered vertices, 478,387 DOFs): the dense
+    oracle does not fit a CPU host, so check sampled element matrices against the oracle cell by
+    cell, the DOF counts against the oracle's DOF map, and size-independent properties: convergence,
+    true residual of the full system, lambda_min ~ 1 (Theorem teoEst)."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    from oracle.assemble import GlobalDofs
+    from oracle.vem import ElementOps, mesh_edges, EdgeIndex
+    prob = make_problem("c3")
+    ctx = _ctx(prob)
+    dofs = GlobalDofs(prob.mesh, 3)
+    assert ctx.n_vel == dofs.n_free_vel and ctx.n_free == dofs.n_free_vel + dofs.npres
+    ei = EdgeIndex(mesh_edges(prob.mesh), prob.mesh.n_vertices)
+    for K in np.random.default_rng(3).choice(prob.mesh.n_cells, 6, replace=False):
+        op = ElementOps(prob.mesh, int(K), ei, 3, prob.nu_cell[K])
+        A, B = ctx.element_matrices(int(K))
+        assert np.abs(A - op.A).max() <= 1e-11 * np.abs(op.A).max()
+        assert np.abs(B - op.B).max() <= 1e-11 * np.abs(op.B).max()
+    ctx.factor()
+    st = ctx.stats()
+    assert st["n_dofs_paper"] == dofs.n_dofs_paper()
+    rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+    ctx.build_rhs(vb.problem_args(prob), rhs)
+    x = torch.zeros_like(rhs)
+    rep = ctx.pcg_solve(rhs, x, rtol=1e-10)
+    assert rep["status"] == "OK" and rep["rel_residual"] <= 1e-10 and 0.999 <= rep["lambda_min"] <= 1.01
+    y = torch.zeros_like(rhs)
+    ctx.apply_operator(x, y)
+    res = (rhs - y).cpu().numpy()
+    nb = np.linalg.norm(rhs.cpu().numpy())
+    assert np.linalg.norm(res[:ctx.n_vel]) <= 1e-8 * nb
+    assert np.linalg.norm(res[ctx.n_vel:]) <= 1e-8 * nb
