@@ -19,6 +19,7 @@ static vb_status fail(vb_ctx *c, const Error &e) {
 
 #define ABI_GUARD(ctx, ...)                                                                     \
   try {                                                                                         \
+    ::vb::AllocStreamScope _alloc_scope(ctx_stream(ctx));                                       \
     __VA_ARGS__;                                                                                \
   } catch (const Error &e) {                                                                    \
     return fail(ctx, e);                                                                        \
@@ -26,6 +27,9 @@ static vb_status fail(vb_ctx *c, const Error &e) {
     return fail(ctx, Error{VB_EINVAL, e.what()});                                               \
   }                                                                                             \
   return VB_OK;
+
+static cudaStream_t ctx_stream(const vb_ctx *c) { return c ? c->stream : nullptr; }
+static cudaStream_t ctx_stream(std::nullptr_t) { return nullptr; }
 
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -257,6 +261,7 @@ static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, i
   if (dist) {
     c->rank = dist->rank; c->nranks = dist->nranks; c->device = dist->device;
     c->stream = (cudaStream_t)dist->stream;
+    g_alloc_stream = c->stream;
   }
   VB_REQUIRE(c->nranks >= 1 && c->rank >= 0 && c->rank < c->nranks, VB_EINVAL, "bad rank / nranks");
   VB_CUDA(cudaSetDevice(c->device));
@@ -350,6 +355,7 @@ vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n
   if (!out) return VB_EINVAL;
   *out = nullptr;
   vb_ctx *c = new vb_ctx();
+  AllocStreamScope alloc_scope(nullptr);   // common_setup switches it to the context's stream
   try {
     double t0 = now_s();
     common_setup(c, mesh, cell_subdomain, n_subdomains, subdomain_rank, cons, cell_viscosity, dist);
@@ -374,6 +380,7 @@ vb_status vb_setup_from_elements(const vb_mesh *mesh, const int32_t *cell_subdom
   if (!out) return VB_EINVAL;
   *out = nullptr;
   vb_ctx *c = new vb_ctx();
+  AllocStreamScope alloc_scope(nullptr);   // common_setup switches it to the context's stream
   try {
     double t0 = now_s();
     common_setup(c, mesh, cell_subdomain, n_subdomains, subdomain_rank, cons, cell_viscosity, dist);
@@ -551,10 +558,15 @@ const char *vb_last_error(const vb_ctx *c) { return c ? c->err.c_str() : g_last_
 
 vb_status vb_destroy(vb_ctx *c) {
   if (!c) return VB_EINVAL;
-  cudaStreamSynchronize(c->stream);
-  destroy_solve_state(c);
-  delete c->comm;
-  delete c;
+  cudaStream_t s = c->stream;
+  cudaStreamSynchronize(s);
+  {
+    AllocStreamScope alloc_scope(s);
+    destroy_solve_state(c);
+    delete c->comm;
+    delete c;
+  }
+  pool_trim(s);   // return the context's device memory (other live contexts keep theirs)
   return VB_OK;
 }
 

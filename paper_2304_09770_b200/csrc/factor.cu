@@ -19,6 +19,27 @@
 namespace vb {
 
 double g_malloc_s = 0.0, g_free_s = 0.0;
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
+void pool_init() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done_dev = dev;
+}
+
+void pool_trim(cudaStream_t s) {
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaStreamSynchronize(s) == cudaSuccess && cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+    cudaMemPoolTrimTo(pool, 0);
+}
 double wall_now() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -681,6 +702,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     plan.run(l0, s);
     sync(c);
   }
+  STAGE_T("  L_DD^-1 / S_DD^-1 / Phi");
   // ---------------- b~0 and the benign check
   c->d_b0T.alloc(std::max<int64_t>(c->len_Pi, 1));
   c->d_b0T.zero(s);
@@ -756,6 +778,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
       sync(c);
     }
   }
+  STAGE_T("  deluxe D_G (A4)");
   // ---------------- active slots / entities
   {
     std::vector<int> act_s, act_e;
@@ -834,6 +857,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
   }
   VB_STAGE();
   c->d_Dlx.release();
+  STAGE_T("  fold D S_DD^-1 D^T, D Phi");
   // ---------------- A5: coarse saddle matrix on (u_Pi, p_0) of ALL subdomains, dense inverse
   //   C4: every rank gathers every subdomain's (S_c, b~0) and assembles/factors the same matrix
   const int Ng = c->Ng;
@@ -905,10 +929,12 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     coarse_augment_kernel<<<(int)std::min<int64_t>(((int64_t)Ng * Ng + 255) / 256, 4096), 256, 0, s>>>(
         gvol.p, Ng, 1.0 / (nubar * volO), Kc.p, Nc, c->NPi_g);
     VB_STAGE();
+    STAGE_T("  coarse pieces + assembly (C4)");
     c->d_info.zero(s);
     std::vector<MatDesc> cm{MatDesc{Kc.p, (int)Nc, (int)Nc, (int)Nc}};
     ldl_partial_batched(cm, c->d_info.p, s);
     check_info(c, 1, "coarse saddle LDL^T (A5)");
+    STAGE_T("  coarse LDL^T");
     Wc.alloc(Nc * Nc);
     Wc.zero(s);
     tri_inverse_batched({TriDesc{Kc.p, (int)Nc, Wc.p, (int)Nc, (int)Nc}}, s);

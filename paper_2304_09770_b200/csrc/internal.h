@@ -35,9 +35,23 @@ struct Error {
   } while (0)
 
 // ------------------------------------------------------------------ device buffer
-// cumulative wall time (s) spent in cudaMalloc / cudaFree by DBuf (diagnostics, VB_FACTOR_TIMES)
+// cumulative wall time (s) spent in allocation / release by DBuf (diagnostics, VB_FACTOR_TIMES)
 extern double g_malloc_s, g_free_s;
 double wall_now();
+
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync / cudaFreeAsync on the
+// stream of the context being served, release threshold raised so freed blocks are reused instead
+// of unmapped): the factorisation allocates and frees multi-GB scratch per stage, and plain
+// cudaMalloc/cudaFree cost it 0.5-1 s of synchronous mapping work.  Every ABI entry point sets
+// g_alloc_stream (AllocStreamScope) to its context's stream.
+extern thread_local cudaStream_t g_alloc_stream;
+void pool_init();
+void pool_trim(cudaStream_t s);   // sync s, then return unused pool memory to the device
+struct AllocStreamScope {
+  cudaStream_t prev;
+  explicit AllocStreamScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+  ~AllocStreamScope() { g_alloc_stream = prev; }
+};
 
 template <class T>
 struct DBuf {
@@ -50,7 +64,7 @@ struct DBuf {
   void release() {
     if (p) {
       const double t0 = wall_now();
-      cudaFree(p);
+      cudaFreeAsync(p, g_alloc_stream);
       g_free_s += wall_now() - t0;
     }
     p = nullptr;
@@ -59,12 +73,14 @@ struct DBuf {
   void alloc(size_t count) {
     release();
     if (count == 0) return;
+    pool_init();
     const double t0 = wall_now();
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    cudaError_t e = cudaMallocAsync((void **)&p, count * sizeof(T), g_alloc_stream);
     g_malloc_s += wall_now() - t0;
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
-      throw Error{VB_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed"};
+      p = nullptr;
+      throw Error{VB_ENOMEM, "cudaMallocAsync of " + std::to_string(count * sizeof(T)) + " bytes failed"};
     }
     n = count;
   }
