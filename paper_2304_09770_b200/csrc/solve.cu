@@ -725,6 +725,7 @@ struct SolveState {
   bool ready = false;
   DBuf<unsigned> ticket;             // single-launch reductions
   cudaStream_t s2 = nullptr;         // coarse branch of M^-1, concurrent with the local solves
+  int prio_hi = 0;                   // its (higher) scheduling priority
   cudaStream_t sg = nullptr;         // stream the iteration graph is captured on and launched on
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // the PCG iteration as a CUDA graph: WHILE(status == 0) { S-part; check; IF(status == 0) M-part }
@@ -755,13 +756,21 @@ static void launch_pdl(const SolveState *st, void (*k)(KArgs...), dim3 g, dim3 b
   cfg.blockDim = b;
   cfg.dynamicSmemBytes = sm;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
+  int na = 0;
   if (st->pdl) {
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
   }
+  if (s == st->s2 && st->prio_hi != 0) {
+    // the coarse branch of M^-1 ahead of the queued CTAs of the local GEMV (it is on the critical path)
+    at[na].id = cudaLaunchAttributePriority;
+    at[na].val.priority = st->prio_hi;
+    ++na;
+  }
+  cfg.attrs = na ? at : nullptr;
+  cfg.numAttrs = na;
   VB_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
 
@@ -951,7 +960,10 @@ void prepare_solve(vb_ctx *c) {
   st->ticket.alloc(4); st->ticket.zero(s);
   st->pdl = !(getenv("VB_NO_PDL") && atoi(getenv("VB_NO_PDL")));
   if (!st->s2) {
-    VB_CUDA(cudaStreamCreateWithFlags(&st->s2, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;
+    VB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    st->prio_hi = (getenv("VB_NO_PRIO") && atoi(getenv("VB_NO_PRIO"))) ? 0 : hi;
+    VB_CUDA(cudaStreamCreateWithPriority(&st->s2, cudaStreamNonBlocking, st->prio_hi));
     VB_CUDA(cudaStreamCreateWithFlags(&st->sg, cudaStreamNonBlocking));
     VB_CUDA(cudaEventCreateWithFlags(&st->ev_fork, cudaEventDisableTiming));
     VB_CUDA(cudaEventCreateWithFlags(&st->ev_join, cudaEventDisableTiming));
@@ -1357,7 +1369,7 @@ static void build_iteration_graph(vb_ctx *c, SolveState *st) {
   }
   st->capturing = false;
   c->stream = user;
-  cudaError_t e = cudaGraphInstantiate(&st->gexec, g, 0);
+  cudaError_t e = cudaGraphInstantiate(&st->gexec, g, cudaGraphInstantiateFlagUseNodePriority);
   cudaGraphDestroy(g);
   if (e != cudaSuccess && st->pdl) {     // programmatic edges not accepted here: capture without them
     (void)cudaGetLastError();
