@@ -158,6 +158,16 @@ vb_status vb_apply_operator(vb_ctx *ctx, const double *x_dev, double *y_dev);
  * HOST vector in original interface coordinates: the vb_interface_dofs order (entity-major),
  * then one p_0 per subdomain.  Requires vb_factor.                                            */
 vb_status vb_debug_interface_op(vb_ctx *ctx, int32_t which, const double *in_host, double *out_host);
+
+/* Parity/debug and microbenchmark: the factorisation's grouped DMMA GEMM on DEVICE buffers,
+ *   C_b = alpha * op(A_b) * diag(d) * op(B_b) + beta * C_b,   b = 0 .. batch-1,
+ * column-major, op(X) = X or X^T (trans* = 0/1), X_b = X + b * strideX (elements); d (length K,
+ * unit stride) may be NULL.  Runs on `stream` (a cudaStream_t, NULL = legacy default) and
+ * synchronises it before returning.  VB_EINVAL on non-positive sizes or leading dimensions.      */
+vb_status vb_debug_gemm(int32_t M, int32_t N, int32_t K, double alpha, const double *A, int32_t lda,
+                        int32_t transA, const double *B, int32_t ldb, int32_t transB, const double *d,
+                        double beta, double *C, int32_t ldc, int32_t batch, int64_t strideA,
+                        int64_t strideB, int64_t strideC, void *stream);
 /* Interface DOFs (free velocity ids) in the library's entity-major order; *n = count.
  * ids may be NULL to query the count only.                                                     */
 vb_status vb_interface_dofs(const vb_ctx *ctx, int64_t *ids, int64_t *n);

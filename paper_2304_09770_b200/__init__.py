@@ -96,9 +96,13 @@ _vb_destroy = _sig("vb_destroy", ctypes.c_int, [_p])
 _vb_nccl_unique_id = _sig("vb_nccl_unique_id", ctypes.c_int, [_p])
 _vb_debug_iop = _sig("vb_debug_interface_op", ctypes.c_int, [_p, ctypes.c_int32, _dp, _dp])
 _vb_interface_dofs = _sig("vb_interface_dofs", ctypes.c_int, [_p, _i64p, _i64p])
+_vb_debug_gemm = _sig("vb_debug_gemm", ctypes.c_int,
+                     [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _p, ctypes.c_int32,
+                      ctypes.c_int32, _p, ctypes.c_int32, ctypes.c_int32, _p, ctypes.c_double, _p,
+                      ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _p])
 
 EXPORTED = ["vb_plan_exchange", "vb_nccl_unique_id", "vb_loopback_world_create", "vb_loopback_world_destroy", "vb_setup", "vb_setup_from_elements", "vb_factor", "vb_build_rhs",
-            "vb_pcg_solve", "vb_pcg_solve_host", "vb_apply_operator", "vb_debug_interface_op",
+            "vb_pcg_solve", "vb_pcg_solve_host", "vb_apply_operator", "vb_debug_interface_op", "vb_debug_gemm",
             "vb_interface_dofs", "vb_num_free_dofs", "vb_dof_layout",
             "vb_cell_local_dofs", "vb_get_element_matrices", "vb_stats", "vb_kernel_times",
             "vb_kernel_time_name", "vb_last_error", "vb_destroy"]
@@ -293,6 +297,28 @@ def nccl_unique_id():
     if st != VB_OK:
         raise VBError(st, _vb_last_error(None).decode())
     return bytes(buf.raw)
+
+
+def debug_gemm(A, B, C, alpha=1.0, beta=0.0, d=None, transA=False, transB=False):
+    """C_b = alpha op(A_b) diag(d) op(B_b) + beta C_b with the factorisation's DMMA GEMM
+    (vb_debug_gemm).  A, B, C: CUDA float64 tensors of shape (batch, cols, rows) holding each matrix
+    COLUMN-major (i.e. the transposes of the logical matrices, contiguous); C is updated in place."""
+    import torch
+    for t in (A, B, C):
+        assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.dim() == 3
+    batch = C.shape[0]
+    M, N = C.shape[2], C.shape[1]
+    K = A.shape[2] if transA else A.shape[1]
+    st = _vb_debug_gemm(M, N, K, alpha, ctypes.c_void_p(A.data_ptr()), A.shape[2], int(transA),
+                        ctypes.c_void_p(B.data_ptr()), B.shape[2], int(transB),
+                        ctypes.c_void_p(d.data_ptr()) if d is not None else None, beta,
+                        ctypes.c_void_p(C.data_ptr()), C.shape[2], batch,
+                        A.shape[1] * A.shape[2] if A.shape[0] > 1 else 0,
+                        B.shape[1] * B.shape[2] if B.shape[0] > 1 else 0, C.shape[1] * C.shape[2],
+                        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if st != VB_OK:
+        raise VBError(st, _vb_last_error(None).decode())
+    return C
 
 
 class LoopbackWorld:

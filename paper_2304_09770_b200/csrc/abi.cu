@@ -5,6 +5,7 @@
 #include <map>
 #include "setup.h"
 #include "exchange.h"
+#include "dense.cuh"
 
 using namespace vb;
 
@@ -555,6 +556,32 @@ vb_status vb_kernel_times(const vb_ctx *c, double *ms, int32_t n_max, int32_t *n
 const char *vb_kernel_time_name(int32_t i) { return vb::kernel_time_name(i); }
 
 const char *vb_last_error(const vb_ctx *c) { return c ? c->err.c_str() : g_last_error.c_str(); }
+
+vb_status vb_debug_gemm(int32_t M, int32_t N, int32_t K, double alpha, const double *A, int32_t lda,
+                        int32_t transA, const double *B, int32_t ldb, int32_t transB, const double *d,
+                        double beta, double *C, int32_t ldc, int32_t batch, int64_t strideA,
+                        int64_t strideB, int64_t strideC, void *stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || batch <= 0 || !A || !B || !C) return VB_EINVAL;
+  if (lda < (transA ? K : M) || ldb < (transB ? N : K) || ldc < M) return VB_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  ABI_GUARD(nullptr, {
+    AllocStreamScope scope(s);
+    GemmPlan plan;
+    int l0 = plan.begin_launch();
+    for (int b = 0; b < batch; ++b) {
+      GemmProb p{};
+      p.A = A + b * strideA; p.lda = lda; p.transA = transA != 0;
+      p.B = B + b * strideB; p.ldb = ldb; p.transB = transB != 0;
+      p.C = C + b * strideC; p.ldc = ldc;
+      p.d = d; p.dstride = 1;
+      p.M = M; p.N = N; p.K = K; p.alpha = alpha; p.beta = beta;
+      plan.add(p);
+    }
+    plan.upload(s);
+    plan.run(l0, s);
+    VB_CUDA(cudaStreamSynchronize(s));
+  })
+}
 
 vb_status vb_destroy(vb_ctx *c) {
   if (!c) return VB_EINVAL;

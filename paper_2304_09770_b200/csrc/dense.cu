@@ -7,38 +7,33 @@
 namespace vb {
 
 // ------------------------------------------------------------------ grouped GEMM (DMMA)
-// CTA tile 128 x 64 x 16, 8 warps (4 along M x 2 along N), warp tile 32 x 32 = 4 x 4 DMMA 8x8x4.
-// The next K-slab is prefetched from global memory into registers while the current one is
-// multiplied out of shared memory (one smem buffer, two barriers per slab).
-// CTA tile GBM x GBN x 16, 8 warps; warp tile (GBM / WARPS_M) x 32 of DMMA 8x8x4 tiles.
+// CTA tile 128 x 64 x 16, 8 warps (4 along M x 2 along N), warp tile 32 x 32 = 2 x 4 tiles of
+// mma.sync.m16n8k16.f64 (SASS DMMA.16816: 8x fewer tensor instructions than m8n8k4 for the same
+// work).  K-slabs of 16 stream through a 3-stage cp.async shared-memory ring, one barrier per slab.
 constexpr int GBM = 128, GBN = 64, GBK = 16;   // 128x128 measured slower (1 CTA/SM, padding on small N)
 constexpr int GPAD = 4;
 constexpr int GTHREADS = 256;
 constexpr int LDL_NB = 128;        // wide-panel width of the blocked LDL^T and triangular inverse
 constexpr int GWARPS_N = GBN / 32, GWARPS_M = (GTHREADS / 32) / GWARPS_N;
-constexpr int GMI = GBM / GWARPS_M / 8;         // DMMA tiles per warp along M
+constexpr int GMI = GBM / GWARPS_M / 16;        // m16n8k16 tiles per warp along M
 constexpr int GA_PER = GBM * GBK / GTHREADS;
 constexpr int GB_PER = GBK * GBN / GTHREADS;
 
-__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+// D(16x8) += A(16x16) B(16x8); fragments (PTX ISA, f64 m16n8k16; g = lane / 4, t = lane % 4):
+//   a[v] = A(g + 8 (v % 2), t + 4 (v / 2)),  b[v] = B(t + 4 v, g),  c[v] = C(g + 8 (v / 2), 2 t + v % 2)
+__device__ __forceinline__ void dmma_16x8x16(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+      "{%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]),
+        "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
-// element (i, kk) of the op(A) slab / (kk, j) of the op(B) slab handled by thread `tid`, slot q:
-// the index order makes consecutive threads read consecutive addresses for every transpose case
-__device__ __forceinline__ void a_coord(const GemmProb &P, int idx, int &i, int &kk) {
-  if (!P.transA) { i = idx % GBM; kk = idx / GBM; } else { kk = idx % GBK; i = idx / GBK; }
-}
-__device__ __forceinline__ void b_coord(const GemmProb &P, int idx, int &kk, int &j) {
-  if (!P.transB) { kk = idx % GBK; j = idx / GBK; } else { j = idx % GBN; kk = idx / GBN; }
-}
-
-// ---- asynchronous K-slab loads: cp.async 8-byte copies into a 2-stage shared-memory ring
+// ---- asynchronous K-slab loads: cp.async 8-byte copies into a 3-stage shared-memory ring
 // (zero-filled outside the matrix); the diagonal scaling d of op(A)'s columns is applied to the A
 // fragments, so A and B are copied unmodified.
-constexpr int GSTAGES = 2;
+constexpr int GSTAGES = 3;
 struct GemmSmem {
   double A[GSTAGES][GBM][GBK + GPAD];
   double B[GSTAGES][GBK][GBN + GPAD];
@@ -53,35 +48,56 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool val
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-__device__ __forceinline__ void issue_slab(const GemmProb &P, int m0, int n0, int k0, int tid, GemmSmem &sm,
-                                           int stage) {
+// Per-thread copy pattern of the K-slabs, fixed for the whole K loop (only k0 moves).  With 256
+// threads, thread tid copies for slot q:
+//   op(A) slab (i, kk):  A not transposed (i contiguous): i = tid % 128, kk = tid / 128 + 2 q
+//                        A transposed (k contiguous):     kk = tid % 16,  i = tid / 16 + 16 q
+//   op(B) slab (kk, j):  B not transposed (k contiguous): kk = tid % 16,  j = tid / 16 + 16 q
+//                        B transposed (j contiguous):     j = tid % 64,   kk = tid / 64 + 4 q
+// so consecutive threads read consecutive addresses in every case.
+static_assert(GTHREADS == 256 && GBM == 128 && GBN == 64 && GBK == 16, "copy pattern assumes these");
+template <bool TA> struct ACopy {
+  static constexpr int DI = TA ? 16 : 0, DKK = TA ? 0 : 2;
+  __device__ static int i0(int tid) { return TA ? tid / GBK : tid % GBM; }
+  __device__ static int kk0(int tid) { return TA ? tid % GBK : tid / GBM; }
+};
+template <bool TB> struct BCopy {
+  static constexpr int DJ = TB ? 0 : 16, DKK = TB ? 4 : 0;
+  __device__ static int j0(int tid) { return TB ? tid % GBN : tid / GBK; }
+  __device__ static int kk0(int tid) { return TB ? tid / GBN : tid % GBK; }
+};
+
+template <bool TA, bool TB>
+__device__ __forceinline__ void issue_slab(const double *pa, const double *pb, int lda, int ldb, const double *A0,
+                                           const double *B0, int rows_left, int cols_left, int k_left,
+                                           const double *d, int dstride, int tid, GemmSmem &sm, int stage) {
+  // pa / pb: this thread's slot-0 sources in the current slab; *_left: extents past the tile origin
+  const int ai = ACopy<TA>::i0(tid), akk = ACopy<TA>::kk0(tid);
 #pragma unroll
   for (int q = 0; q < GA_PER; ++q) {
-    int i, kk;
-    a_coord(P, tid + q * GTHREADS, i, kk);
-    const int gi = m0 + i, gk = k0 + kk;
-    const bool ok = gi < P.M && gk < P.K;
-    const double *src = ok ? (P.transA ? P.A + gk + (int64_t)gi * P.lda : P.A + gi + (int64_t)gk * P.lda) : P.A;
-    cp_async8(&sm.A[stage][i][kk], src, ok);
+    const int i = ai + q * ACopy<TA>::DI, kk = akk + q * ACopy<TA>::DKK;
+    const bool ok = i < rows_left && kk < k_left;
+    const int64_t off = TA ? (int64_t)(q * 16) * lda : (int64_t)(q * 2) * lda;
+    cp_async8(&sm.A[stage][i][kk], ok ? pa + off : A0, ok);
   }
+  const int bj = BCopy<TB>::j0(tid), bkk = BCopy<TB>::kk0(tid);
 #pragma unroll
   for (int q = 0; q < GB_PER; ++q) {
-    int kk, j;
-    b_coord(P, tid + q * GTHREADS, kk, j);
-    const int gj = n0 + j, gk = k0 + kk;
-    const bool ok = gj < P.N && gk < P.K;
-    const double *src = ok ? (P.transB ? P.B + gj + (int64_t)gk * P.ldb : P.B + gk + (int64_t)gj * P.ldb) : P.B;
-    cp_async8(&sm.B[stage][kk][j], src, ok);
+    const int j = bj + q * BCopy<TB>::DJ, kk = bkk + q * BCopy<TB>::DKK;
+    const bool ok = j < cols_left && kk < k_left;
+    const int64_t off = TB ? (int64_t)(q * 4) * ldb : (int64_t)(q * 16) * ldb;
+    cp_async8(&sm.B[stage][kk][j], ok ? pb + off : B0, ok);
   }
-  if (P.d && tid < GBK) {
-    const int gk = k0 + tid;
-    const bool ok = gk < P.K;
-    cp_async8(&sm.D[stage][tid], ok ? P.d + (int64_t)gk * P.dstride : P.d, ok);
+  if (d && tid < GBK) {
+    const bool ok = tid < k_left;
+    cp_async8(&sm.D[stage][tid], ok ? d + (int64_t)tid * dstride : d, ok);
   }
 }
 
 // DENSE: one large problem (id = tile0) on a 2D grid of tiles (no tile list).
-template <bool DENSE>
+// SCALED: some problem of the launch has a diagonal scaling d (else the multiply is compiled out).
+// TA / TB: op(A) = A^T / op(B) = B^T for every problem of the launch.
+template <bool DENSE, bool SCALED, bool TA, bool TB>
 __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmProb *__restrict__ probs,
                                                                   const int4 *__restrict__ tiles, int tile0) {
   const int4 t = DENSE ? make_int4(tile0, blockIdx.y, blockIdx.x, 0) : tiles[tile0 + blockIdx.x];
@@ -94,63 +110,104 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmPro
   extern __shared__ __align__(16) unsigned char gsm_raw[];
   GemmSmem &sm = *reinterpret_cast<GemmSmem *>(gsm_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tg = lane & 3;
   const int wm = (warp / GWARPS_N) * (GBM / GWARPS_M), wn = (warp % GWARPS_N) * 32;
-  const bool scaled = P.d != nullptr;
-  double acc[GMI][4][2];
+  const bool scaled = SCALED && P.d != nullptr;
+  double acc[GMI][4][4];
 #pragma unroll
   for (int i = 0; i < GMI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  issue_slab(P, m0, n0, 0, tid, sm, 0);
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+  const int lda = P.lda, ldb = P.ldb, K = P.K, dstride = P.dstride;
+  const int rows_left = P.M - m0, cols_left = P.N - n0;
+  const double *dvec = SCALED ? P.d : nullptr;
+  // slot-0 sources at k0 = 0 and their advance per slab
+  const double *pa = TA ? P.A + ACopy<TA>::kk0(tid) + (int64_t)(m0 + ACopy<TA>::i0(tid)) * lda
+                        : P.A + (m0 + ACopy<TA>::i0(tid)) + (int64_t)ACopy<TA>::kk0(tid) * lda;
+  const double *pb = TB ? P.B + (n0 + BCopy<TB>::j0(tid)) + (int64_t)BCopy<TB>::kk0(tid) * ldb
+                        : P.B + BCopy<TB>::kk0(tid) + (int64_t)(n0 + BCopy<TB>::j0(tid)) * ldb;
+  const int64_t astep = TA ? GBK : (int64_t)GBK * lda, bstep = TB ? (int64_t)GBK * ldb : GBK;
+  const double *A0 = P.A, *B0 = P.B;
+  issue_slab<TA, TB>(pa, pb, lda, ldb, A0, B0, rows_left, cols_left, K, dvec, dstride, tid, sm, 0);
   cp_async_commit();
-  if (GBK < P.K) issue_slab(P, m0, n0, GBK, tid, sm, 1);
+  if (GBK < K)
+    issue_slab<TA, TB>(pa + astep, pb + bstep, lda, ldb, A0, B0, rows_left, cols_left, K - GBK,
+                       dvec ? dvec + (int64_t)GBK * dstride : nullptr, dstride, tid, sm, 1);
   cp_async_commit();
-  int ks = 0;
-  for (int k0 = 0; k0 < P.K; k0 += GBK, ++ks) {
-    cp_async_wait1();       // all groups but the newest are complete: slab ks has landed
-    __syncthreads();
-    const int st = ks & 1;
-#pragma unroll
-    for (int kk = 0; kk < GBK; kk += 4) {
-      double a[GMI], b[4];
-      const double dk = scaled ? sm.D[st][kk + (lane & 3)] : 1.0;
-#pragma unroll
-      for (int i = 0; i < GMI; ++i) a[i] = sm.A[st][wm + 8 * i + (lane >> 2)][kk + (lane & 3)] * dk;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = sm.B[st][kk + (lane & 3)][wn + 8 * j + (lane >> 2)];
-#pragma unroll
-      for (int i = 0; i < GMI; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  pa += 2 * astep;
+  pb += 2 * bstep;
+  int st = 0;
+  for (int k0 = 0; k0 < K; k0 += GBK) {
+    cp_async_wait1();       // all groups but the newest are complete: this slab has landed
+    __syncthreads();        // ... for every thread; and every thread is done with the previous slab
+    {
+      int nst = st + 2;
+      if (nst >= GSTAGES) nst -= GSTAGES;   // = the stage of the previous slab, free again
+      if (k0 + 2 * GBK < K)
+        issue_slab<TA, TB>(pa, pb, lda, ldb, A0, B0, rows_left, cols_left, K - k0 - 2 * GBK,
+                           dvec ? dvec + (int64_t)(k0 + 2 * GBK) * dstride : nullptr, dstride, tid, sm, nst);
+      cp_async_commit();
+      pa += astep;
+      pb += bstep;
     }
-    __syncthreads();        // everyone is done with stage st before it is refilled
-    if (k0 + 2 * GBK < P.K) issue_slab(P, m0, n0, k0 + 2 * GBK, tid, sm, st);
-    cp_async_commit();
+#pragma unroll
+    for (int i = 0; i < GMI; ++i) {
+      double a[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        a[v] = sm.A[st][wm + 16 * i + g + 8 * (v & 1)][tg + 4 * (v >> 1)];
+        if (SCALED && scaled) a[v] *= sm.D[st][tg + 4 * (v >> 1)];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double b[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) b[v] = sm.B[st][tg + 4 * v][wn + 8 * j + g];
+        dmma_16x8x16(acc[i][j], a, b);
+      }
+    }
+    if (++st == GSTAGES) st = 0;
   }
 #pragma unroll
   for (int i = 0; i < GMI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int gi = m0 + wm + 8 * i + (lane >> 2);
-        int gj = n0 + wn + 8 * j + 2 * (lane & 3) + h;
+      for (int v = 0; v < 4; ++v) {
+        const int gi = m0 + wm + 16 * i + g + 8 * (v >> 1);
+        const int gj = n0 + wn + 8 * j + 2 * tg + (v & 1);
         if (gi < P.M && gj < P.N && (!P.lower || gi >= gj)) {
           double *c = P.C + gi + (int64_t)gj * P.ldc;
-          *c = (P.beta == 0.0 ? 0.0 : P.beta * *c) + P.alpha * acc[i][j][h];
+          *c = (P.beta == 0.0 ? 0.0 : P.beta * *c) + P.alpha * acc[i][j][v];
         }
       }
 }
 
-static void gemm_kernel_attributes() {
-  static bool done = false;
-  if (done) return;
-  VB_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sizeof(GemmSmem)));
-  VB_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sizeof(GemmSmem)));
-  done = true;
+template <bool DENSE, bool SCALED, bool TA, bool TB>
+static void launch_gemm(dim3 grid, const GemmProb *probs, const int4 *tiles, int tile0, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    VB_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<DENSE, SCALED, TA, TB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GemmSmem)));
+    attr = true;
+  }
+  gemm_grouped_kernel<DENSE, SCALED, TA, TB><<<grid, GTHREADS, sizeof(GemmSmem), s>>>(probs, tiles, tile0);
+  VB_CHECK_LAUNCH();
 }
+
+template <bool DENSE, bool SCALED>
+static void launch_gemm_cls(int cls, dim3 grid, const GemmProb *probs, const int4 *tiles, int tile0, cudaStream_t s) {
+  switch (cls) {
+    case 0: launch_gemm<DENSE, SCALED, false, false>(grid, probs, tiles, tile0, s); break;
+    case 1: launch_gemm<DENSE, SCALED, true, false>(grid, probs, tiles, tile0, s); break;
+    case 2: launch_gemm<DENSE, SCALED, false, true>(grid, probs, tiles, tile0, s); break;
+    default: launch_gemm<DENSE, SCALED, true, true>(grid, probs, tiles, tile0, s); break;
+  }
+}
+
+static int trans_class(const GemmProb &p) { return (p.transA ? 1 : 0) + (p.transB ? 2 : 0); }
 
 double g_gemm_flops = 0.0;   // DMMA GEMM flops issued (factor-stage accounting, single driving thread)
 
@@ -168,34 +225,45 @@ void GemmPlan::add(const GemmProb &p) {
     dense.back().push_back(pid);
     return;
   }
+  if (p.d) scaled.back() = 1;
+  auto &tl = ltiles.back()[trans_class(p)];
   for (int i = 0; i < tm; ++i)
     for (int j = 0; j < tn; ++j) {
       if (p.lower && (i * GBM + GBM - 1) < j * GBN) continue;   // tile strictly above diagonal
-      tiles.push_back(make_int4(pid, i, j, 0));
-      launches.back().second++;
+      tl.push_back(make_int4(pid, i, j, 0));
     }
 }
 
 void GemmPlan::upload(cudaStream_t s) {
   std::vector<GemmProb> hp(probs);
-  std::vector<int4> ht(tiles);
+  std::vector<int4> ht;
+  lrange.assign(ltiles.size(), {});
+  for (size_t l = 0; l < ltiles.size(); ++l)
+    for (int c = 0; c < 4; ++c) {
+      lrange[l][c] = {(int)ht.size(), (int)ltiles[l][c].size()};
+      ht.insert(ht.end(), ltiles[l][c].begin(), ltiles[l][c].end());
+    }
   d_probs.upload(hp, s);
   d_tiles.upload(ht, s);
   VB_CUDA(cudaStreamSynchronize(s));
 }
 
 void GemmPlan::run(int launch, cudaStream_t s) {
-  gemm_kernel_attributes();
-  auto &L = launches[launch];
-  if (L.second > 0) {
-    gemm_grouped_kernel<false><<<L.second, GTHREADS, sizeof(GemmSmem), s>>>(d_probs.p, d_tiles.p, L.first);
-    VB_CHECK_LAUNCH();
+  for (int c = 0; c < 4; ++c) {
+    const auto &R = lrange[launch][c];
+    if (R.second <= 0) continue;
+    if (scaled[launch])
+      launch_gemm_cls<false, true>(c, dim3(R.second), d_probs.p, d_tiles.p, R.first, s);
+    else
+      launch_gemm_cls<false, false>(c, dim3(R.second), d_probs.p, d_tiles.p, R.first, s);
   }
   for (int pid : dense[launch]) {
     const GemmProb &p = probs[pid];
     dim3 grid((p.N + GBN - 1) / GBN, (p.M + GBM - 1) / GBM);
-    gemm_grouped_kernel<true><<<grid, GTHREADS, sizeof(GemmSmem), s>>>(d_probs.p, d_tiles.p, pid);
-    VB_CHECK_LAUNCH();
+    if (p.d)
+      launch_gemm_cls<true, true>(trans_class(p), grid, d_probs.p, d_tiles.p, pid, s);
+    else
+      launch_gemm_cls<true, false>(trans_class(p), grid, d_probs.p, d_tiles.p, pid, s);
   }
 }
 

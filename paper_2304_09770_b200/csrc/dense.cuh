@@ -1,5 +1,6 @@
 // Batched dense FP64 kernels for the factorisations.
 #pragma once
+#include <array>
 #include "internal.h"
 
 namespace vb {
@@ -9,18 +10,22 @@ struct MatDesc {      // column-major square matrix
   int n, ld, m;       // m = number of leading columns to eliminate
 };
 
-// A sequence of grouped-GEMM launches planned on the host and uploaded once.
+// A sequence of grouped-GEMM launches planned on the host and uploaded once.  Within a launch the
+// tiles are grouped by transpose class (op(A), op(B)) so each class runs the kernel specialised for
+// its copy pattern.
 struct GemmPlan {
   std::vector<GemmProb> probs;
-  std::vector<int4> tiles;                 // (prob, tile_m, tile_n, 0)
-  std::vector<std::pair<int, int>> launches;  // (tile_begin, tile_count)
+  std::vector<std::array<std::vector<int4>, 4>> ltiles;   // per launch, per class: (prob, tm, tn, 0)
+  std::vector<std::array<std::pair<int, int>, 4>> lrange;  // after upload: (tile_begin, tile_count)
   std::vector<std::vector<int>> dense;        // per launch: large problems run as 2D grids
+  std::vector<char> scaled;                   // per launch: some tile-list problem has d != null
   DBuf<GemmProb> d_probs;
   DBuf<int4> d_tiles;
   int begin_launch() {
-    launches.push_back({(int)tiles.size(), 0});
+    ltiles.push_back({});
     dense.push_back({});
-    return launches.size() - 1;
+    scaled.push_back(0);
+    return ltiles.size() - 1;
   }
   void add(const GemmProb &p);             // adds tiles to the current launch
   void upload(cudaStream_t s);

@@ -45,8 +45,10 @@ double wall_now();
 // cudaMalloc/cudaFree cost it 0.5-1 s of synchronous mapping work.  Every ABI entry point sets
 // g_alloc_stream (AllocStreamScope) to its context's stream.
 extern thread_local cudaStream_t g_alloc_stream;
+extern bool g_use_pool;   // VB_NO_POOL=1: plain cudaMalloc / cudaFree
 void pool_init();
-void pool_trim(cudaStream_t s);   // sync s, then return unused pool memory to the device
+void pool_trim(cudaStream_t s);
+struct vb_ctx_fwd;   // sync s, then return unused pool memory to the device
 struct AllocStreamScope {
   cudaStream_t prev;
   explicit AllocStreamScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
@@ -64,7 +66,7 @@ struct DBuf {
   void release() {
     if (p) {
       const double t0 = wall_now();
-      cudaFreeAsync(p, g_alloc_stream);
+      if (g_use_pool) cudaFreeAsync(p, g_alloc_stream); else cudaFree(p);
       g_free_s += wall_now() - t0;
     }
     p = nullptr;
@@ -75,7 +77,8 @@ struct DBuf {
     if (count == 0) return;
     pool_init();
     const double t0 = wall_now();
-    cudaError_t e = cudaMallocAsync((void **)&p, count * sizeof(T), g_alloc_stream);
+    cudaError_t e = g_use_pool ? cudaMallocAsync((void **)&p, count * sizeof(T), g_alloc_stream)
+                               : cudaMalloc((void **)&p, count * sizeof(T));
     g_malloc_s += wall_now() - t0;
     if (e != cudaSuccess) {
       (void)cudaGetLastError();

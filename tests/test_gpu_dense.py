@@ -1,0 +1,34 @@
+"""The factorisation's grouped DMMA GEMM (dense.cu, used by A1-A5) against torch float64 matmul:
+all transpose cases, diagonal scaling, beta accumulation, ragged sizes that span several
+128 x 64 x 16 tiles with partial edge tiles, batched problems and the large-problem 2-D grid path."""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _colmajor(X):
+    return X.transpose(-1, -2).contiguous()
+
+
+@pytest.mark.parametrize("M,N,K,batch", [(1, 1, 1, 1), (37, 5, 3, 2), (130, 70, 33, 3), (257, 129, 200, 4),
+                                         (1285, 1158, 129, 2), (9001, 4097, 70, 1)])
+@pytest.mark.parametrize("tA,tB", [(False, False), (True, False), (False, True), (True, True)])
+def test_gemm_vs_torch(M, N, K, batch, tA, tB):
+    import torch
+    import paper_2304_09770_b200 as vb
+    if M * N > 4e6 and (tA or tB):
+        pytest.skip("large case: one transpose combination is enough")
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn(batch, K if tA else M, M if tA else K, dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn(batch, N if tB else K, K if tB else N, dtype=torch.float64, device="cuda", generator=g)
+    C0 = torch.randn(batch, M, N, dtype=torch.float64, device="cuda", generator=g)
+    d = torch.rand(K, dtype=torch.float64, device="cuda", generator=g) + 0.5
+    opA = A.transpose(1, 2) if tA else A
+    opB = B.transpose(1, 2) if tB else B
+    ref = -0.5 * (opA * d) @ opB + 2.0 * C0
+    C = _colmajor(C0)
+    vb.debug_gemm(_colmajor(A), _colmajor(B), C, alpha=-0.5, beta=2.0, d=d, transA=tA, transB=tB)
+    got = C.transpose(1, 2)
+    err = (got - ref).abs().max().item()
+    scale = ((opA.abs() * d) @ opB.abs()).max().item()
+    assert err <= 1e-14 * K * scale + 1e-13, err

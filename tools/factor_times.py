@@ -14,7 +14,9 @@ def main():
     from synthetic import make_problem
     from synthetic.configs import C5_DIMS
     prob = make_problem(sys.argv[1] if len(sys.argv) > 1 else "c5", dims=C5_DIMS[1])
+    t = time.time()
     ctx = vb.context_for(prob)
+    print("setup %.3f s" % (time.time() - t), flush=True)
     for _ in range(2):
         t = time.time()
         ctx.factor()
