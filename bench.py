@@ -309,8 +309,11 @@ def main():
         "factor": {"t_s": t_factor, "dmma_gemm_flops": st["factor_gemm_flops"],
                    "tflops": st["factor_gemm_flops"] / t_factor / 1e12,
                    "frac_of_dmma_peak": st["factor_gemm_flops"] / t_factor / 37.2e12,
+                   "alloc_s": st["factor_alloc_us"] / 1e6,
+                   "tflops_excl_alloc": st["factor_gemm_flops"] / max(t_factor - st["factor_alloc_us"] / 1e6, 1e-9) / 1e12,
                    "peak_note": "DMMA 37.2 TFLOP/s measured by tools/fp64_peak.cu (profiles/r01_fp64_peak.txt); "
-                                "t_s includes the non-GEMM kernels and host work of vb_factor"},
+                                "t_s includes the non-GEMM kernels, host work and device allocation (alloc_s: "
+                                "first-touch mapping of the factor workspace, varies run to run) of vb_factor"},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ctx.n_free,
                 "d2h_bytes_per_step": 8 * ctx.n_free, "ms_per_step": e2e_ms},
         # kernels per solve (single rank): 15 + 18 it (deluxe folded into the operators;

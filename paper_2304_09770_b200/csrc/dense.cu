@@ -13,7 +13,7 @@ namespace vb {
 constexpr int GBM = 128, GBN = 64, GBK = 16;   // 128x128 measured slower (1 CTA/SM, padding on small N)
 constexpr int GPAD = 4;
 constexpr int GTHREADS = 256;
-constexpr int LDL_NB = 128;        // wide-panel width of the blocked LDL^T and triangular inverse
+constexpr int LDL_NB = 256;        // wide-panel width of the blocked LDL^T and triangular inverse
 constexpr int GWARPS_N = GBN / 32, GWARPS_M = (GTHREADS / 32) / GWARPS_N;
 constexpr int GMI = GBM / GWARPS_M / 16;        // m16n8k16 tiles per warp along M
 constexpr int GA_PER = GBM * GBK / GTHREADS;

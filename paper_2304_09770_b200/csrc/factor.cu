@@ -990,6 +990,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
 void factor_device(vb_ctx *c) {
   cudaStream_t s = c->stream;
   g_gemm_flops = 0.0;
+  const double alloc0 = g_malloc_s + g_free_s;
   stage_time(c, nullptr);
   stage_dirichlet(c);
   stage_time(c, "dirichlet (A1/A2)");
@@ -1023,6 +1024,7 @@ void factor_device(vb_ctx *c) {
   stage_dual(c, sidebuf, sumbuf);
   stage_time(c, "dual + coarse (A3-A5)");
   c->factor_flops = g_gemm_flops;
+  c->factor_alloc_s = g_malloc_s + g_free_s - alloc0;
 }
 
 }  // namespace vb

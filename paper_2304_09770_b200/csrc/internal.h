@@ -347,5 +347,6 @@ struct vb_ctx {
   vb::DBuf<double> w_rhsg, w_xg;     // global-layout free vectors (nranks > 1)
   vb::DBuf<double> d_Kcr;            // distributed coarse: this rank's rows of the coarse inverse
   int64_t coarse_rows = 0, coarse_lo = 0;
-  double factor_flops = 0;           // DMMA GEMM flops of the last vb_factor
+  double factor_flops = 0;     // DMMA GEMM flops of the last vb_factor
+  double factor_alloc_s = 0;   // wall time of device allocation / release inside the last vb_factor
 };
