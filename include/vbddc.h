@@ -112,7 +112,8 @@ vb_status vb_plan_exchange(const vb_mesh *mesh, const int32_t *cell_subdomain, i
  * classification, interface entities, and the VEM element matrices A^K, B^K computed
  * on the device from the geometry and the per-cell viscosity.
  *   cell_subdomain[n_cells]  subdomain id per cell (0..n_subdomains-1)
- *   subdomain_rank[n_subdomains] owning rank (NULL = all rank 0)
+ *   subdomain_rank[n_subdomains] owning rank (NULL = all rank 0); every rank must own at
+ *                            least one subdomain (VB_EINVAL naming the rank otherwise)
  *   cell_viscosity[n_cells]  nu_K > 0                                               */
 vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
                    const int32_t *subdomain_rank, const vb_constraints *cons,

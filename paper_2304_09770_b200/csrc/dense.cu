@@ -209,7 +209,7 @@ static void launch_gemm_cls(int cls, dim3 grid, const GemmProb *probs, const int
 
 static int trans_class(const GemmProb &p) { return (p.transA ? 1 : 0) + (p.transB ? 2 : 0); }
 
-double g_gemm_flops = 0.0;   // DMMA GEMM flops issued (factor-stage accounting, single driving thread)
+thread_local double g_gemm_flops = 0.0;   // DMMA GEMM flops issued by this thread (factor-stage accounting)
 
 void GemmPlan::add(const GemmProb &p) {
   if (p.M <= 0 || p.N <= 0) return;

@@ -33,7 +33,7 @@ struct GemmPlan {
 };
 
 void gemm_grouped(GemmPlan &plan, int launch, cudaStream_t s);
-extern double g_gemm_flops;   // flops of the GEMMs planned since the last reset
+extern thread_local double g_gemm_flops;   // flops of the GEMMs planned since the last reset
 
 // Partial LDL^T (no pivoting, velocity-first quasi-definite ordering) of a batch:
 // eliminates the first m columns; on exit the strictly lower part of those columns holds L, the

@@ -18,7 +18,7 @@
 
 namespace vb {
 
-double g_malloc_s = 0.0, g_free_s = 0.0;
+thread_local double g_malloc_s = 0.0, g_free_s = 0.0;
 thread_local cudaStream_t g_alloc_stream = nullptr;
 bool g_use_pool = !(getenv("VB_NO_POOL") && atoi(getenv("VB_NO_POOL")));
 

@@ -36,7 +36,7 @@ struct Error {
 
 // ------------------------------------------------------------------ device buffer
 // cumulative wall time (s) spent in allocation / release by DBuf (diagnostics, VB_FACTOR_TIMES)
-extern double g_malloc_s, g_free_s;
+extern thread_local double g_malloc_s, g_free_s;
 double wall_now();
 
 // Device memory comes from the device's stream-ordered pool (cudaMallocAsync / cudaFreeAsync on the

@@ -5,6 +5,8 @@
 // PCG vectors live in transformed interface coordinates x = [dual coords per entity | u_Pi | p_0];
 // T_G is orthogonal, so Euclidean norms, CG coefficients and the stopping test equal those of the
 // original coordinates.
+#include <mutex>
+#include <map>
 #include <algorithm>
 #include <cmath>
 #include "dense.cuh"
@@ -140,6 +142,21 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
   }
   if (!BIG)
     for (int j = tid; j < n; j += blockDim.x) W.out[j] = ys[j];
+}
+
+// Raise (never lower) a kernel's dynamic shared-memory limit.  The attribute is process-wide, and
+// several contexts in one process (or loopback ranks on threads) size the same kernels differently:
+// a context must never shrink the limit another one launches with.
+static void raise_smem_limit(const void *func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> cur;
+  int dev = 0;
+  VB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t &c = cur[{func, dev}];
+  if (bytes <= c) return;
+  VB_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  c = bytes;
 }
 
 static size_t gemv_smem(int nmax, int warps = GV_WARPS) {
@@ -1015,13 +1032,12 @@ void prepare_solve(vb_ctx *c) {
   st->big_c = st->sm_c > 200 * 1024;
   size_t smmax = std::max(st->sm_op, st->sm_loc);
   VB_REQUIRE(smmax <= 227 * 1024, VB_EINVAL, "packed GEMV vector exceeds shared memory (subdomain interface too large)");
-  VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smmax));
+  raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS>, smmax);
   if (!st->big_c)
-    VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS_C, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)st->sm_c));
+    raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS_C, false, true>, st->sm_c);
   st->max_nd = nmaxD;
   if (st->max_nd * sizeof(double) > 48 * 1024)
-    VB_CUDA(cudaFuncSetAttribute(phit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(st->max_nd * sizeof(double))));
+    raise_smem_limit((const void *)phit_kernel, st->max_nd * sizeof(double));
   const int ne = c->ents.size();
   // ---------------- B2 (apply_S): copies of each x coordinate, local and received, in sharer order
   {
@@ -1207,10 +1223,10 @@ void prepare_solve(vb_ctx *c) {
     st->sm_kd = gemv_smem(nmaxDn);
     VB_REQUIRE(st->sm_kd <= 227 * 1024, VB_EINVAL, "Dirichlet block too large for the packed GEMV");
     size_t smg = std::max(std::max(st->sm_op, st->sm_loc), st->sm_kd);
-    VB_CUDA(cudaFuncSetAttribute(sym_gemv_kernel<GV_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smg));
+    raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS>, smg);
     int64_t mg = 1;
     for (auto &S : c->h_sub) mg = std::max<int64_t>(mg, S.nG);
-    VB_CUDA(cudaFuncSetAttribute(xD_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(mg * 8)));
+    raise_smem_limit((const void *)xD_kernel, (size_t)mg * 8);
   }
   VB_CUDA(cudaStreamSynchronize(s));
   st->ready = true;

@@ -14,11 +14,12 @@ from synthetic import make_problem
 pytestmark = pytest.mark.gpu
 
 
-def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True):
+def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=None):
     import torch
     import paper_2304_09770_b200 as vb
-    R = int(np.prod(rank_grid))
-    srank = vb.box_ranks(prob.sub_grid, rank_grid)
+    if srank is None:
+        R = int(np.prod(rank_grid))
+        srank = vb.box_ranks(prob.sub_grid, rank_grid)
     world = vb.LoopbackWorld(R)
     streams = [torch.cuda.Stream() for _ in range(R)]
 
@@ -130,3 +131,41 @@ def test_multirank_adaptive(n, rank_grid):
         assert o["rep"]["n_adaptive"] == rep1["n_adaptive"]
         assert o["rep"]["n_primal"] == rep1["n_primal"]
         assert o["rep"]["iterations"] == rep1["iterations"]
+
+
+@pytest.mark.parametrize("assign", ["checkerboard", "stripes3"])
+def test_multirank_irregular_assignment(assign):
+    """Non-box subdomain-to-rank maps: a checkerboard (every interface entity crosses ranks; vertices
+    shared by 8 subdomains on 2 ranks) and 3 ranks owning interleaved x-stripes (ragged rank sizes,
+    every rank pair adjacent).  Same gates as above against the 1-rank solve."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    prob = make_problem("c1", n=8)
+    sub = np.arange(int(np.prod(prob.sub_grid)))
+    gx, gy, gz = prob.sub_grid
+    i, j, k = sub % gx, (sub // gx) % gy, sub // (gx * gy)
+    if assign == "checkerboard":
+        srank, R = ((i + j + k) % 2).astype(np.int32), 2
+    else:
+        srank, R = (i % 3).astype(np.int32), 3
+    ctx = vb.context_for(prob)
+    ctx.factor()
+    rhs1 = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+    ctx.build_rhs(vb.problem_args(prob), rhs1)
+    x1 = torch.zeros_like(rhs1)
+    rep1 = ctx.pcg_solve(rhs1, x1, rtol=1e-10)
+    ids1 = ctx.dof_layout()
+    x1 = x1.cpu().numpy()
+    outs = _run_ranks(prob, None, srank=srank, R=R)
+    ids = np.concatenate([o["ids"] for o in outs])
+    assert np.array_equal(np.sort(ids), np.sort(ids1))
+    pos = {int(g): q for q, g in enumerate(ids1)}
+    xR = np.full(ids1.size, np.nan)
+    for o in outs:
+        xR[[pos[int(g)] for g in o["ids"]]] = o["x"]
+    for o in outs:
+        assert abs(o["rep"]["iterations"] - rep1["iterations"]) <= 1
+        assert abs(o["rep"]["kappa"] - rep1["kappa"]) <= 1e-4 * rep1["kappa"]
+    assert np.linalg.norm(xR - x1) <= 1e-10 * np.linalg.norm(x1)
+    rR = np.concatenate([o["res"] for o in outs])
+    assert np.linalg.norm(rR) <= 1e-8 * np.linalg.norm(rhs1.cpu().numpy())

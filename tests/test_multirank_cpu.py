@@ -23,6 +23,36 @@ def _free_port():
     return port
 
 
+def _layout(vb, prob, rank_grid):
+    """Subdomain -> rank: a box layout (tuple), a checkerboard over 2 ranks, or 3 ranks of which
+    rank 2 owns no subdomain."""
+    if isinstance(rank_grid, tuple):
+        return vb.box_ranks(prob.sub_grid, rank_grid)
+    sub = np.arange(int(np.prod(prob.sub_grid)))
+    gx, gy, _ = prob.sub_grid
+    i, j, k = sub % gx, (sub // gx) % gy, sub // (gx * gy)
+    if rank_grid == "checker":
+        return ((i + j + k) % 2).astype(np.int32)
+    return (sub % 2).astype(np.int32)
+
+
+def _world(rank_grid):
+    return int(np.prod(rank_grid)) if isinstance(rank_grid, tuple) else {"checker": 2, "idle3": 3}[rank_grid]
+
+
+def test_rank_without_subdomains_is_rejected():
+    """Every rank must own at least one subdomain (include/vbddc.h, vb_setup): VB_EINVAL, named."""
+    import paper_2304_09770_b200 as vb
+    from synthetic import make_problem
+    prob = make_problem("c1", n=8)
+    srank = _layout(vb, prob, "idle3")
+    snd, rcv, own = vb.plan_exchange(prob.mesh, prob.k, prob.cell_subdomain, srank, 0, 3, 0)
+    assert own > 0
+    with pytest.raises(vb.VBError) as e:
+        vb.plan_exchange(prob.mesh, prob.k, prob.cell_subdomain, srank, 2, 3, 0)
+    assert e.value.status == vb.VB_EINVAL and "owns no subdomain" in str(e.value)
+
+
 def _worker(rank, world, port, name, kw, rank_grid, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -31,7 +61,7 @@ def _worker(rank, world, port, name, kw, rank_grid, q):
         import paper_2304_09770_b200 as vb
         from synthetic import make_problem
         prob = make_problem(name, **kw)
-        srank = vb.box_ranks(prob.sub_grid, rank_grid)
+        srank = _layout(vb, prob, rank_grid)
         ok = True
         owned = None
         for mode in (0, 1, 2):
@@ -57,9 +87,10 @@ def _worker(rank, world, port, name, kw, rank_grid, q):
 
 
 @pytest.mark.parametrize("name,kw,rank_grid", [("c1", dict(n=8), (1, 1, 2)), ("c1", dict(n=8), (2, 2, 1)),
-                                              ("c3", dict(n=8), (1, 2, 1)), ("c1", dict(n=8), (2, 2, 2))])
+                                              ("c3", dict(n=8), (1, 2, 1)), ("c1", dict(n=8), (2, 2, 2)),
+                                              ("c1", dict(n=8), "checker")])
 def test_exchange_plans_agree_across_ranks(name, kw, rank_grid):
-    world = int(np.prod(rank_grid))
+    world = _world(rank_grid)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
