@@ -103,3 +103,23 @@ def test_maxit_and_state_errors():
     assert rep["rel_residual"] > 1e-14
     rep = ctx.pcg_solve(rhs, x, rtol=1e-10)          # the context is still usable
     assert rep["status"] == "OK"
+
+
+def test_two_contexts_interleaved():
+    """Two live contexts of different subdomain sizes in one process, solved alternately: kernel
+    launch limits are process-wide, so preparing the small one must not break the large one, and
+    each keeps its own results (bitwise repeatable solves)."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    big = make_problem("c1", n=8, sub=(4, 4, 4))
+    small = make_problem("c1")
+    cb, rb, xb, repb = _gpu_solve(big)
+    cs, rs, xs, reps = _gpu_solve(small)
+    xb2 = torch.zeros_like(xb)
+    rep2 = cb.pcg_solve(rb, xb2, rtol=1e-10)
+    assert rep2["iterations"] == repb["iterations"] and torch.equal(xb2, xb)
+    xs2 = torch.zeros_like(xs)
+    rep3 = cs.pcg_solve(rs, xs2, rtol=1e-10)
+    assert rep3["iterations"] == reps["iterations"] and torch.equal(xs2, xs)
+    cb.close()
+    cs.close()
