@@ -46,7 +46,7 @@ struct GemvWork {
 constexpr int GV_WARPS = 4;      // subdomain matrices (several CTAs per SM)
 constexpr int GV_WARPS_C = 8;    // the single coarse matrix (one CTA per SM)
 
-// BIG: vectors too long for shared memory (large coarse problems): x is read through the L2 (it is
+// BIG: vectors too long for shared memory (large coarse problems, very large subdomains): x is read through the L2 (it is
 // small next to the streamed matrix) and the partial output accumulates in the CTA's own global
 // partial vector (each column J is owned by one warp, so there are no races).
 // PAIR: each warp streams two tiles per step (twice the loads in flight; for the coarse matrix,
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
   double *rowred = BIG ? sm : sm + 2 * npad;    // GV_WARPS * 32
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto X = [&](int j) -> double {
-    if (BIG) return j < n ? __ldg(W.xsrc + j) : 0.0;
+    if (BIG) return j < n ? (W.map ? __ldg(W.xsrc + __ldg(W.map + j)) : __ldg(W.xsrc + j)) : 0.0;
     return xs[j];
   };
   if (BIG) {
@@ -724,6 +724,7 @@ struct SolveState {
   DBuf<GemvWork> w_kd;
   int nw_op = 0, nw_loc = 0, nw_c = 0, nw_kd = 0, max_nd = 1;
   bool big_c = false;                // coarse vectors exceed shared memory: BIG GEMV variant
+  bool big_op = false, big_loc = false, big_kd = false;   // the same for the subdomain matrices
   int c_chunks = 1;                  // distributed coarse: column chunks of the row-block GEMV
   size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_ex = 0, sm_kd = 0;
   DBuf<int64_t> xptr, xidx;          // B2: x coordinate <- copies (local s or received), sharer order
@@ -789,6 +790,15 @@ static void launch_pdl(const SolveState *st, void (*k)(KArgs...), dim3 g, dim3 b
   cfg.attrs = na ? at : nullptr;
   cfg.numAttrs = na;
   VB_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
+// packed GEMV over a subdomain work list; BIG when the vectors do not fit in shared memory
+static void run_sub_gemv(const SolveState *st, const GemvWork *w, int nw, size_t sm, bool big, cudaStream_t s) {
+  if (nw <= 0) return;
+  if (big)
+    launch_pdl(st, sym_gemv_kernel<GV_WARPS, true>, dim3(nw), dim3(GV_WARPS * 32), GV_WARPS * 32 * sizeof(double), s, w);
+  else
+    launch_pdl(st, sym_gemv_kernel<GV_WARPS>, dim3(nw), dim3(GV_WARPS * 32), sm, s, w);
 }
 
 static const char *kCatNames[] = {"sym_gemv S_T (operator, B1)", "sym_gemv S_DD^-1 (local, B5)",
@@ -857,7 +867,7 @@ static void apply_S(vb_ctx *c, SolveState *st, bool with_pq = false) {   // q = 
   cudaStream_t s = c->stream;
   tick(c, st, 3, true);
   tick(c, st, 0, true);
-  launch_pdl(st, sym_gemv_kernel<GV_WARPS>, dim3(st->nw_op), dim3(GV_WARPS * 32), st->sm_op, s, st->w_op.p);
+  run_sub_gemv(st, st->w_op.p, st->nw_op, st->sm_op, st->big_op, s);
   tick(c, st, 0, false);
   int maxnG = 1;
   for (auto &S : c->h_sub) maxnG = std::max(maxnG, S.nG);
@@ -900,7 +910,7 @@ static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   VB_CUDA(cudaEventRecord(st->ev_fork, s));
   VB_CUDA(cudaStreamWaitEvent(s2, st->ev_fork, 0));
   tick(c, st, 1, true);
-  if (st->nw_loc) launch_pdl(st, sym_gemv_kernel<GV_WARPS>, dim3(st->nw_loc), dim3(GV_WARPS * 32), st->sm_loc, s, st->w_loc.p);
+  run_sub_gemv(st, st->w_loc.p, st->nw_loc, st->sm_loc, st->big_loc, s);
   tick(c, st, 1, false);
   // coarse pieces (C2): [Phi_i^T rD_i per local subdomain | r0_i | r_Pi of the owned entities]
   launch_pdl(st, phit_kernel, dim3(PHIT_SPLIT, c->N), dim3(256), st->max_nd * sizeof(double), s2, c->d_sub.p, c->d_Phi.p,
@@ -1030,8 +1040,9 @@ void prepare_solve(vb_ctx *c) {
     wl.push_back(GemvWork{c->d_Kcp.p, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, rows[q].first, rows[q].second, 0});
   st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = c->nranks > 1 ? 0 : gemv_smem(c->Nc, GV_WARPS_C);
   st->big_c = st->sm_c > 200 * 1024;
-  size_t smmax = std::max(st->sm_op, st->sm_loc);
-  VB_REQUIRE(smmax <= 227 * 1024, VB_EINVAL, "packed GEMV vector exceeds shared memory (subdomain interface too large)");
+  st->big_op = st->sm_op > 200 * 1024;
+  st->big_loc = st->sm_loc > 200 * 1024;
+  size_t smmax = std::max(st->big_op ? 0 : st->sm_op, st->big_loc ? 0 : st->sm_loc);
   raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS>, smmax);
   if (!st->big_c)
     raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS_C, false, true>, st->sm_c);
@@ -1221,8 +1232,8 @@ void prepare_solve(vb_ctx *c) {
     st->w_kd.upload(wk, s);
     st->nw_kd = wk.size();
     st->sm_kd = gemv_smem(nmaxDn);
-    VB_REQUIRE(st->sm_kd <= 227 * 1024, VB_EINVAL, "Dirichlet block too large for the packed GEMV");
-    size_t smg = std::max(std::max(st->sm_op, st->sm_loc), st->sm_kd);
+    st->big_kd = st->sm_kd > 200 * 1024;
+    size_t smg = std::max(std::max(st->big_op ? 0 : st->sm_op, st->big_loc ? 0 : st->sm_loc), st->big_kd ? 0 : st->sm_kd);
     raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS>, smg);
     int64_t mg = 1;
     for (auto &S : c->h_sub) mg = std::max<int64_t>(mg, S.nG);
@@ -1422,7 +1433,7 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   c->w_r.zero(s);
   rhs_D_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p, c->d_mvec.p, rhs, nvf,
                                  c->w_bD.p, c->w_r.p + NDelta + c->NPi);
-  sym_gemv_kernel<GV_WARPS><<<st->nw_kd, GV_WARPS * 32, st->sm_kd, s>>>(st->w_kd.p);   // y_D = K_DD^-1 b_D
+  run_sub_gemv(st, st->w_kd.p, st->nw_kd, st->sm_kd, st->big_kd, s);   // y_D = K_DD^-1 b_D
   zG_kernel<<<dim3((maxnG + 127) / 128, N), 128, 0, s>>>(c->d_sub.p, c->d_Psi.p, c->w_bD.p, st->gbuf.p);
   VB_STAGE();
   dev_gather(rhs, c->d_gam_free.p, c->nGamma, st->gam2.p, s);                // b_e (entity-major)

@@ -123,3 +123,28 @@ def test_two_contexts_interleaved():
     assert rep3["iterations"] == reps["iterations"] and torch.equal(xs2, xs)
     cb.close()
     cs.close()
+
+
+def test_large_subdomains_big_gemv():
+    """Subdomains of 9^3 cells (n_D ~ 17.6k): the packed-GEMV vectors exceed shared memory, so the
+    subdomain GEMVs run the L2-vector (BIG) variant.  The discrete solution is unique, so it must equal
+    the solve of the same mesh with 3^3-cell subdomains (shared-memory GEMVs); both reach the true
+    residual of the element-by-element operator, and lambda_min ~ 1 (Theorem teoEst)."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    pb = make_problem("c1", n=18, sub=(9, 9, 9))
+    ps = make_problem("c1", n=18, sub=(3, 3, 3))
+    cb, rb, xb, repb = _gpu_solve(pb)
+    assert max(cb.stats()["max_n"], 1) > 17000
+    cs, rs, xs, reps = _gpu_solve(ps)
+    assert torch.equal(rb, rs)
+    for c, r, x, rep in ((cb, rb, xb, repb), (cs, rs, xs, reps)):
+        assert rep["status"] == "OK" and 0.999 <= rep["lambda_min"] <= 1.01
+        y = torch.zeros_like(r)
+        c.apply_operator(x, y)
+        assert torch.linalg.norm(r - y) <= 1e-8 * torch.linalg.norm(r)
+    nv = cb.n_vel
+    assert torch.linalg.norm(xb[:nv] - xs[:nv]) <= 1e-8 * torch.linalg.norm(xs[:nv])
+    assert torch.linalg.norm(xb[nv:] - xs[nv:]) <= 1e-8 * torch.linalg.norm(xs[nv:])
+    cb.close()
+    cs.close()
