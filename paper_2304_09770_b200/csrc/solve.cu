@@ -274,19 +274,25 @@ __global__ void dot_final_kernel(const double *__restrict__ part, int nb, double
 
 // scal: [0] rz, [1] pq, [2] rr, [3] rz_new, [4] alpha, [5] beta
 
-__global__ void update_p_kernel(double *p, const double *z, int64_t n, double *scal, int first) {
+// p = z + beta p (beta = rz_new / rz); unless first, the last block to finish then records beta and
+// rotates rz <- rz_new (every block has read both by then)
+__global__ void update_p_kernel(double *p, const double *z, int64_t n, double *scal, int first, double *hist,
+                                unsigned *ticket) {
   pdl_prologue();
   const double beta = first ? 0.0 : scal[3] / scal[0];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
-}
-
-__global__ void rotate_rz_kernel(double *scal, double *hist) {
-  pdl_prologue();
-  // record beta of this step and rotate rz <- rz_new (it = scal[6] already counts this step)
-  const int it = (int)scal[6];
-  if (it >= 1 && it <= 4096) hist[2 * (it - 1) + 1] = scal[3] / scal[0];
-  scal[0] = scal[3];
+  if (first) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+      const int it = (int)scal[6];   // counts this step already
+      if (it >= 1 && it <= 4096) hist[2 * (it - 1) + 1] = beta;
+      scal[0] = scal[3];
+      *ticket = 0u;
+    }
+  }
 }
 
 // ---- single-launch deterministic reductions: block partials, the last block to finish sums them
@@ -325,6 +331,26 @@ __global__ void dot_kernel(const double *__restrict__ a, const double *__restric
   } else {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
       v += a[i] * b[i];
+  }
+  block_reduce_last(v, part, ticket, dst);
+}
+
+// r.z with the coarse tail of z filled on the way: z[n0 + j] = u_c[zmap[j]] (primal and p0 coordinates
+// of z = M^-1 r, B7), same arithmetic and order as dot_kernel
+__global__ void dot_ztail_kernel(const double *__restrict__ r, double *z, const double *__restrict__ uc,
+                                 const int64_t *__restrict__ zmap, int64_t n0, const double *__restrict__ mask,
+                                 int64_t n, double *part, unsigned *ticket, double *dst) {
+  pdl_prologue();
+  double v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double zi;
+    if (i >= n0) {
+      zi = uc[zmap[i - n0]];
+      z[i] = zi;
+    } else {
+      zi = z[i];
+    }
+    v += mask ? mask[i] * (r[i] * zi) : r[i] * zi;
   }
   block_reduce_last(v, part, ticket, dst);
 }
@@ -861,6 +887,15 @@ static void dot(vb_ctx *c, const double *a, const double *b, int64_t n, double *
   allreduce_sum_fixed(c, dst, 1);
 }
 
+// rz = r.z after apply_M(..., false): fills z's coarse tail in the same pass (C3 follows)
+static void dot_rz(vb_ctx *c, SolveState *st, double *dst) {
+  VB_REQUIRE(c->nx - c->n_delta_glob == (int64_t)st->zmap.n || (c->nx == c->n_delta_glob && st->zmap.n <= 1),
+             VB_EINVAL, "internal: z tail layout");
+  launch_pdl(st, dot_ztail_kernel, dim3(DOT_BLOCKS), dim3(256), 0, c->stream, c->w_r.p, c->w_z.p, c->w_uc.p,
+             st->zmap.p, c->n_delta_glob, c->nranks > 1 ? st->mask.p : nullptr, c->nx, c->w_dots.p, st->ticket.p, dst);
+  allreduce_sum_fixed(c, dst, 1);
+}
+
 static int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
 
 static void apply_S(vb_ctx *c, SolveState *st, bool with_pq = false) {   // q = S^ p  (B1, B2) [+ p.q]
@@ -903,7 +938,8 @@ static void trace_norm(vb_ctx *c, const char *name, const double *v, int64_t n, 
   fprintf(stderr, "[vb rank %d] %s %.17g\n", c->rank, name, h);
 }
 
-static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
+// z = M^-1 r  (B4-B7); fill_tail = false leaves z's coarse tail to dot_rz (fused with r.z)
+static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   cudaStream_t s = c->stream, s2 = st->s2;
   tick(c, st, 4, true);
   // fork: the coarse branch (B6) runs on s2 while the local dual solves (B5) stream on s
@@ -950,7 +986,7 @@ static void apply_M(vb_ctx *c, SolveState *st) {   // z = M^-1 r  (B4-B7)
   run_slot_exchange(c, st->XE, c->w_locD.p, c->w_locD.p + c->len_Dv);    // C1 (cross-rank products)
   run_entity_sum(c, st->ESE, c->w_locD.p, c->w_z.p);
   trace_norm(c, "zdual", c->w_z.p, c->n_delta_glob, false);
-  dev_gather(c->w_uc.p, st->zmap.p, c->NPi + c->N, c->w_z.p + c->n_delta_glob, s);
+  if (fill_tail) dev_gather(c->w_uc.p, st->zmap.p, c->NPi + c->N, c->w_z.p + c->n_delta_glob, s);
   tick(c, st, 4, false);
   VB_STAGE();
 }
@@ -1345,10 +1381,10 @@ static void pcg_mstep(vb_ctx *c, SolveState *st) {
   cudaStream_t s = c->stream;
   double *sc = c->w_scal.p;
   const int64_t nx = c->nx;
-  apply_M(c, st);
-  dot(c, c->w_r.p, c->w_z.p, nx, sc + 3);
-  launch_pdl(st, update_p_kernel, dim3(grid_for(nx)), dim3(256), 0, s, c->w_p.p, c->w_z.p, nx, sc, 0);
-  launch_pdl(st, rotate_rz_kernel, dim3(1), dim3(1), 0, s, sc, st->hist.p);
+  apply_M(c, st, false);
+  dot_rz(c, st, sc + 3);
+  launch_pdl(st, update_p_kernel, dim3(grid_for(nx)), dim3(256), 0, s, c->w_p.p, c->w_z.p, nx, sc, 0, st->hist.p,
+             st->ticket.p);
   VB_STAGE();
 }
 
@@ -1456,9 +1492,9 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   const double r0n = h[4];
   if (trace) fprintf(stderr, "[vb rank %d] rr0 %.17g\n", c->rank, h[2]);
   if (h[7] == 0.0) {
-    apply_M(c, st);
-    dot(c, c->w_r.p, c->w_z.p, nx, sc + 0);
-    update_p_kernel<<<grid_for(nx), 256, 0, s>>>(c->w_p.p, c->w_z.p, nx, sc, 1);
+    apply_M(c, st, false);
+    dot_rz(c, st, sc + 0);
+    update_p_kernel<<<grid_for(nx), 256, 0, s>>>(c->w_p.p, c->w_z.p, nx, sc, 1, st->hist.p, st->ticket.p);
     VB_STAGE();
     const bool graph = use_graph(c);
     while (true) {
