@@ -13,7 +13,11 @@ namespace vb {
 constexpr int GBM = 128, GBN = 64, GBK = 16;   // 128x128 measured slower (1 CTA/SM, padding on small N)
 constexpr int GPAD = 4;
 constexpr int GTHREADS = 256;
-constexpr int LDL_NB = 256;        // wide-panel width of the blocked LDL^T and triangular inverse
+constexpr int LDL_NB = 256;        // wide-panel width of the blocked LDL^T
+#ifndef TRI_NB_CFG
+#define TRI_NB_CFG 256
+#endif
+constexpr int TRI_NB = TRI_NB_CFG;   // wide-block width of the triangular inverse
 constexpr int GWARPS_N = GBN / 32, GWARPS_M = (GTHREADS / 32) / GWARPS_N;
 constexpr int GMI = GBM / GWARPS_M / 16;        // m16n8k16 tiles per warp along M
 constexpr int GA_PER = GBM * GBK / GTHREADS;
@@ -455,13 +459,13 @@ void tri_inverse_batched(const std::vector<TriDesc> &mats, cudaStream_t s) {
   int nblk = (maxm + 31) / 32;
   GemmPlan plan;
   std::vector<int> intra(nblk, -1), trail;
-  for (int J0 = 0; J0 < maxm; J0 += LDL_NB) {
-    for (int r0 = J0; r0 < std::min(J0 + LDL_NB, maxm); r0 += 32) {
+  for (int J0 = 0; J0 < maxm; J0 += TRI_NB) {
+    for (int r0 = J0; r0 < std::min(J0 + TRI_NB, maxm); r0 += 32) {
       intra[r0 / 32] = plan.begin_launch();
       for (auto &T : mats) {
         if (r0 >= T.m) continue;
         const int nb = std::min(32, T.m - r0);
-        const int Je = std::min(J0 + LDL_NB, T.m);
+        const int Je = std::min(J0 + TRI_NB, T.m);
         const int rows = Je - r0 - nb;
         if (rows <= 0) continue;
         GemmProb p{};
@@ -476,7 +480,7 @@ void tri_inverse_batched(const std::vector<TriDesc> &mats, cudaStream_t s) {
     trail.push_back(plan.begin_launch());
     for (auto &T : mats) {
       if (J0 >= T.m) continue;
-      const int Je = std::min(J0 + LDL_NB, T.m);
+      const int Je = std::min(J0 + TRI_NB, T.m);
       const int rows = T.m - Je;
       if (rows <= 0) continue;
       GemmProb p{};
@@ -490,8 +494,8 @@ void tri_inverse_batched(const std::vector<TriDesc> &mats, cudaStream_t s) {
   }
   plan.upload(s);
   int wide = 0;
-  for (int J0 = 0; J0 < maxm; J0 += LDL_NB, ++wide) {
-    for (int r0 = J0; r0 < std::min(J0 + LDL_NB, maxm); r0 += 32) {
+  for (int J0 = 0; J0 < maxm; J0 += TRI_NB, ++wide) {
+    for (int r0 = J0; r0 < std::min(J0 + TRI_NB, maxm); r0 += 32) {
       const int J = r0 / 32;
       trsm_diag_kernel<<<dim3(J + 1, mats.size()), 32, 0, s>>>(dm.p, J);
       VB_CHECK_LAUNCH();
