@@ -277,6 +277,23 @@ __global__ void recip_diag_kernel(const double *A, int64_t ld, int n, double *ou
 }
 
 // ------------------------------------------------------------------ coarse assembly (colored)
+// tile rows [tlo, tlo + gridDim.y) of the packed symmetric layout (internal.h) from a row block
+// Kr = A[lo:hi, :] (column-major, leading dimension ld) of a symmetric n x n matrix A; tile (I, J)
+// goes to ptile_off(n, I, J) - ptile_row_start(tlo)
+__global__ void pack_rows_kernel(const double *__restrict__ Kr, int64_t ld, int64_t lo, int64_t n, int64_t tlo,
+                                 double *out) {
+  const int64_t I = tlo + blockIdx.y, J = blockIdx.x;
+  if (J > I) return;
+  const int64_t nt = (n + 31) / 32;
+  const int rows = (I == nt - 1) ? (int)(n - 32 * (nt - 1)) : 32;
+  double *o = out + ptile_off(n, I, J) - ptile_row_start(tlo);
+  for (int e = threadIdx.x; e < rows * 32; e += blockDim.x) {
+    const int r = e >> 5, cc = e & 31;
+    const int64_t gj = 32 * J + cc;
+    o[e] = gj < n ? Kr[(32 * I + r - lo) + gj * ld] : 0.0;
+  }
+}
+
 __global__ void coarse_augment_kernel(const double *__restrict__ vol, int N, double gam, double *Kc, int64_t ldc, int64_t NPi) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)N * N; idx += (int64_t)gridDim.x * blockDim.x) {
     int a = idx % N, b = idx / N;
@@ -957,25 +974,40 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
       c->d_Kcp.alloc(packed_size(Nc));
       pack_tiles_batched({PackDesc{Kc.p, (int)Nc, (int)Nc, c->d_Kcp.p}}, s);
     } else {
-      // distributed coarse solve: this rank computes and keeps only rows [lo, lo + rows) of the
-      // inverse, (W[:, lo:hi])^T D^-1 W, column-major rows x N_c (zero rows past N_c); the
-      // solve is a row-block GEMV and an allgather of the row blocks (C2)
-      const int64_t rows = (Nc + c->nranks - 1) / c->nranks;
-      c->coarse_rows = rows;
-      c->coarse_lo = std::min<int64_t>(Nc, rows * c->rank);
-      c->d_Kcr.alloc(rows * Nc);
-      c->d_Kcr.zero(s);
-      const int64_t mine = std::min<int64_t>(rows, Nc - c->coarse_lo);
+      // distributed coarse solve: this rank computes and keeps only the tile rows [tlo, thi) of the
+      // packed symmetric inverse (a contiguous slice of the 1-rank layout, split by tile count), from
+      // the row block (W[:, lo:hi])^T D^-1 W[:, :hi] (W lower triangular: k >= lo suffices).  The
+      // solve streams the slice with the packed GEMV (row and transpose parts) and sums the ranks'
+      // partial vectors in rank order (C2): N_c^2 / (2R) doubles per rank per iteration.
+      const int64_t nt = (Nc + 31) / 32, R = c->nranks;
+      std::vector<int64_t> T(R + 1, nt);
+      T[0] = 0;
+      const double total = (double)nt * (nt + 1) / 2;
+      for (int64_t r = 1, I = 0; r < R; ++r) {
+        while (I < nt && (double)(I + 1) * (I + 2) / 2 < total * r / R) ++I;
+        T[r] = std::max(T[r - 1], std::min<int64_t>(nt, I + 1));
+      }
+      c->coarse_tlo = T[c->rank];
+      c->coarse_thi = T[c->rank + 1];
+      const int64_t lo = 32 * c->coarse_tlo, hi = std::min<int64_t>(Nc, 32 * c->coarse_thi), mine = hi - lo;
+      const int64_t slice = c->coarse_thi == nt ? packed_size(Nc) - ptile_row_start(c->coarse_tlo)
+                                                : ptile_row_start(c->coarse_thi) - ptile_row_start(c->coarse_tlo);
+      c->d_Kcs.alloc(std::max<int64_t>(slice, 1));
       if (mine > 0) {
+        DBuf<double> Kr;
+        Kr.alloc(mine * hi);
         GemmPlan plan;
         int l0 = plan.begin_launch();
         GemmProb p{};
-        p.A = Wc.p + c->coarse_lo * Nc; p.lda = Nc; p.transA = 1; p.d = dc.p; p.dstride = 1;
-        p.B = Wc.p; p.ldb = Nc; p.C = c->d_Kcr.p; p.ldc = rows;
-        p.M = mine; p.N = Nc; p.K = Nc; p.alpha = 1.0; p.beta = 0.0;
+        p.A = Wc.p + lo * Nc + lo; p.lda = Nc; p.transA = 1; p.d = dc.p + lo; p.dstride = 1;
+        p.B = Wc.p + lo; p.ldb = Nc; p.C = Kr.p; p.ldc = mine;
+        p.M = mine; p.N = hi; p.K = Nc - lo; p.alpha = 1.0; p.beta = 0.0;
         plan.add(p);
         plan.upload(s);
         plan.run(l0, s);
+        pack_rows_kernel<<<dim3(c->coarse_thi, c->coarse_thi - c->coarse_tlo), 256, 0, s>>>(
+            Kr.p, mine, lo, Nc, c->coarse_tlo, c->d_Kcs.p);
+        sync(c);
       }
       VB_STAGE();
     }

@@ -345,8 +345,8 @@ struct vb_ctx {
   std::vector<int64_t> owned_free;   // ABI layout: owned free DOF ids (global free numbering)
   vb::DBuf<int64_t> d_owned_free;
   vb::DBuf<double> w_rhsg, w_xg;     // global-layout free vectors (nranks > 1)
-  vb::DBuf<double> d_Kcr;            // distributed coarse: this rank's rows of the coarse inverse
-  int64_t coarse_rows = 0, coarse_lo = 0;
+  vb::DBuf<double> d_Kcs;            // distributed coarse: this rank's tile rows of the packed inverse
+  int64_t coarse_tlo = 0, coarse_thi = 0;   // ... tile rows [tlo, thi) (balanced by tile count)
   double factor_flops = 0;     // DMMA GEMM flops of the last vb_factor
   double factor_alloc_s = 0;   // wall time of device allocation / release inside the last vb_factor
 };

@@ -184,29 +184,6 @@ static void split_rows(int n, int P, std::vector<std::pair<int, int>> &out, doub
   while ((int)out.size() < P) out.push_back({nt, nt});
 }
 
-// distributed coarse solve: y = K_rows x for this rank's rows (column-major rows x n), thread per
-// row (consecutive threads read consecutive addresses), 4 independent accumulators
-// (blockIdx.y: column chunk, partial sums y[chunk * rows + r], summed in chunk order afterwards)
-__global__ void __launch_bounds__(256) rows_gemv_kernel(const double *__restrict__ K, int64_t rows, int64_t n,
-                                                        const double *__restrict__ x, double *y) {
-  pdl_prologue();
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  const int64_t cw = (n + gridDim.y - 1) / gridDim.y;
-  const int64_t j0 = blockIdx.y * cw, j1 = min(n, j0 + cw);
-  y += blockIdx.y * rows;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  int64_t j = j0;
-  for (; j + 3 < j1; j += 4) {
-    a0 += __ldg(K + r + j * rows) * __ldg(x + j);
-    a1 += __ldg(K + r + (j + 1) * rows) * __ldg(x + j + 1);
-    a2 += __ldg(K + r + (j + 2) * rows) * __ldg(x + j + 2);
-    a3 += __ldg(K + r + (j + 3) * rows) * __ldg(x + j + 3);
-  }
-  for (; j < j1; ++j) a0 += __ldg(K + r + j * rows) * __ldg(x + j);
-  y[r] = (a0 + a1) + (a2 + a3);
-}
-
 // ------------------------------------------------------------------ small kernels of the loop
 // per local subdomain: s_j = sum over the P partial chunks of the packed GEMV (fixed order), plus
 // the b0 coupling on the primal coordinates: s_Pi += b~0 p0_i (Eq.(globInt) row 1); and
@@ -727,6 +704,16 @@ __global__ void elem_gather_kernel(const int64_t *__restrict__ ptr, const int64_
 // ------------------------------------------------------------------ host side
 // out[i] = sum_c part[c][i]: block = 32 outputs x 8 warps (warp w sums chunks w, w+8, ...), then
 // the 8 warp partials are added in fixed order.
+// distributed coarse: u_c = sum over ranks (in rank order) of the gathered partial vectors
+__global__ void rank_sum_vec_kernel(const double *__restrict__ g, int R, int64_t n, double *out) {
+  pdl_prologue();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int r = 0; r < R; ++r) v += g[r * n + i];
+    out[i] = v;
+  }
+}
+
 __global__ void __launch_bounds__(256) sum_chunks_kernel(const double *__restrict__ part, int64_t stride, int P,
                                                          int64_t n, double *out) {
   pdl_prologue();
@@ -751,7 +738,6 @@ struct SolveState {
   int nw_op = 0, nw_loc = 0, nw_c = 0, nw_kd = 0, max_nd = 1;
   bool big_c = false;                // coarse vectors exceed shared memory: BIG GEMV variant
   bool big_op = false, big_loc = false, big_kd = false;   // the same for the subdomain matrices
-  int c_chunks = 1;                  // distributed coarse: column chunks of the row-block GEMV
   size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_ex = 0, sm_kd = 0;
   DBuf<int64_t> xptr, xidx;          // B2: x coordinate <- copies (local s or received), sharer order
   DBuf<int64_t> pptr, pidx;          // B6: global coarse index <- coarse pieces, fixed order
@@ -759,7 +745,7 @@ struct SolveState {
   DBuf<double> hist, mask, gvol;
   DBuf<double> sx;                   // [s (len_G) | received copies]
   DBuf<double> cbuf, cgath;          // coarse pieces (local), gathered (nranks x cmax)
-  DBuf<double> ucl;                  // distributed coarse: this rank's rows of u_c
+  DBuf<double> ucp, ucg;             // distributed coarse: this rank's partial u_c; gathered (R x N_c)
   DBuf<double> gam2, gbuf, hbuf;     // B0: entity-major b_e; [zG | received]; DOF halo receive
   int64_t cmax = 0;
   SlotExchange XS, XE, XB, XH, XR;   // apply_S copies, extension products, B0 zG, DOF halo, rank partials
@@ -960,21 +946,19 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   launch_pdl(st, gather_src_kernel, dim3(grid_for(c->Nc)), dim3(256), 0, s2, st->pptr.p, st->pidx.p, pieces, c->Nc, c->w_rc.p);
   launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
   tick(c, st, 2, true, s2);
-  if (c->nranks > 1) {
-    // rows of the coarse inverse owned here, then the allgather of the row blocks (C2)
-    const unsigned rb = (unsigned)((c->coarse_rows + 255) / 256);
-    launch_pdl(st, rows_gemv_kernel, dim3(rb, st->c_chunks), dim3(256), 0, s2, c->d_Kcr.p, c->coarse_rows, c->Nc, c->w_rc.p, c->w_ucp.p);
-    launch_pdl(st, sum_chunks_kernel, dim3((unsigned)((c->coarse_rows + 31) / 32)), dim3(256), 0, s2, c->w_ucp.p, c->coarse_rows, st->c_chunks,
-                                                                          c->coarse_rows, st->ucl.p);
-    tick(c, st, 2, false, s2);
-    c->comm->allgather(st->ucl.p, c->w_uc.p, c->coarse_rows, s2);
-  } else {
+  // the packed inverse (all of it on one rank; this rank's tile rows otherwise)
   if (st->big_c)
     launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, true, true>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), GV_WARPS_C * 32 * sizeof(double), s2, st->w_c.p);
   else
     launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, false, true>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), st->sm_c, s2, st->w_c.p);
   tick(c, st, 2, false, s2);
-  launch_pdl(st, sum_chunks_kernel, dim3((c->Nc + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
+  if (c->nranks > 1) {
+    // this rank's partial, then the rank-order sum of all partials (C2)
+    launch_pdl(st, sum_chunks_kernel, dim3((c->Nc + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, c->Nc, st->nw_c, c->Nc, st->ucp.p);
+    c->comm->allgather(st->ucp.p, st->ucg.p, c->Nc, s2);
+    launch_pdl(st, rank_sum_vec_kernel, dim3(grid_for(c->Nc)), dim3(256), 0, s2, st->ucg.p, c->nranks, c->Nc, c->w_uc.p);
+  } else {
+    launch_pdl(st, sum_chunks_kernel, dim3((c->Nc + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
   }
   launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
   VB_CUDA(cudaEventRecord(st->ev_join, s2));
@@ -1017,8 +1001,8 @@ void prepare_solve(vb_ctx *c) {
   c->w_part.alloc((int64_t)c->P_op * std::max<int64_t>(c->len_G, 1));
   c->w_locD.alloc(std::max<int64_t>(c->len_Dv, 1));
   c->w_locY.alloc((int64_t)c->P_loc * std::max<int64_t>(c->len_Dv, 1));
-  c->w_uc.alloc(std::max<int64_t>(c->Nc, c->coarse_rows * c->nranks)); c->w_rc.alloc(c->Nc);
-  if (c->nranks > 1) st->ucl.alloc(std::max<int64_t>(c->coarse_rows, 1));
+  c->w_uc.alloc(c->Nc); c->w_rc.alloc(c->Nc);
+  if (c->nranks > 1) { st->ucp.alloc(c->Nc); st->ucg.alloc((int64_t)c->Nc * c->nranks); }
   c->w_scal.alloc(16); c->w_scal.zero(s);
   st->ticket.alloc(4); st->ticket.zero(s);
   st->pdl = !(getenv("VB_NO_PDL") && atoi(getenv("VB_NO_PDL")));
@@ -1064,17 +1048,28 @@ void prepare_solve(vb_ctx *c) {
   c->w_locY.zero(s);
   st->w_loc.upload(wl, s); st->nw_loc = wl.size(); st->sm_loc = gemv_smem(nmaxD);
   wl.clear();
-  int Pc = c->nranks > 1 ? 0 : std::max(1, std::min<int>(c->P_c, (int)((c->Nc + 31) / 32)));
+  // coarse work list: the tile rows [tlo, thi) of the packed inverse (all of them on one rank)
+  const int64_t ntc = (c->Nc + 31) / 32;
+  const int64_t tlo = c->nranks > 1 ? c->coarse_tlo : 0, thi = c->nranks > 1 ? c->coarse_thi : ntc;
+  const double *Kc0 = c->nranks > 1 ? c->d_Kcs.p - ptile_row_start(tlo) : c->d_Kcp.p;   // global tile offsets
+  int Pc = (int)std::max<int64_t>(1, std::min<int64_t>(c->P_c, thi - tlo));
   c->w_ucp.alloc(std::max<int64_t>((int64_t)Pc * c->Nc, 1));
-  if (c->nranks > 1) {
-    const int64_t rb = (c->coarse_rows + 255) / 256;
-    st->c_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(64, (4 * 148 + rb - 1) / rb));
-    c->w_ucp.alloc(std::max<int64_t>((int64_t)st->c_chunks * c->coarse_rows, 1));
+  c->w_ucp.zero(s);
+  {
+    // split [tlo, thi) into Pc chunks balanced by tiles + row cost (as split_rows over the slice)
+    auto cum = [&](int64_t r) { return (double)r * (r + 1) / 2 + 4.0 * r; };
+    const double c0 = cum(tlo), tot = cum(thi) - c0;
+    int64_t r = tlo;
+    for (int q = 0; q < Pc; ++q) {
+      int64_t r1 = r;
+      while (r1 < thi && cum(r1 + 1) - c0 <= tot * (q + 1) / Pc) ++r1;
+      if (r1 == r && r < thi) r1 = r + 1;
+      if (q == Pc - 1) r1 = thi;
+      wl.push_back(GemvWork{Kc0, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, (int)r, (int)r1, 0});
+      r = r1;
+    }
   }
-  split_rows(c->Nc, Pc, rows, 4.0);
-  for (int q = 0; q < Pc; ++q)
-    wl.push_back(GemvWork{c->d_Kcp.p, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, rows[q].first, rows[q].second, 0});
-  st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = c->nranks > 1 ? 0 : gemv_smem(c->Nc, GV_WARPS_C);
+  st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = gemv_smem(c->Nc, GV_WARPS_C);
   st->big_c = st->sm_c > 200 * 1024;
   st->big_op = st->sm_op > 200 * 1024;
   st->big_loc = st->sm_loc > 200 * 1024;
@@ -1283,7 +1278,7 @@ void prepare_solve(vb_ctx *c) {
     b += 8.0 * packed_size(S.nG) + 8.0 * packed_size(S.nd) + 2 * 8.0 * S.nd * S.npi;
   }
   // (the deluxe blocks are folded into S_DD^-1 and Phi at factor time: no per-iteration D traffic)
-  b += c->nranks > 1 ? 8.0 * c->coarse_rows * c->Nc : 8.0 * packed_size(c->Nc);
+  b += 8.0 * (c->nranks > 1 ? (double)c->d_Kcs.n : (double)packed_size(c->Nc));
   c->bytes_per_iter = b;
 }
 
