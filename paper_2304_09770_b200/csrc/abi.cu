@@ -171,6 +171,7 @@ void layout_phase_a(vb_ctx *c) {
     }
   }
   c->d_cell_loc.upload(loc, s);
+  c->h_cell_loc = loc;
   // element-by-element operator / rhs: free velocity dof -> contribution slots (local cells, in order)
   {
     std::vector<std::pair<int64_t, int64_t>> pr;

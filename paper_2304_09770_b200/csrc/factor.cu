@@ -468,17 +468,15 @@ static void stage_dirichlet(vb_ctx *c) {
     sg[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.nG, S.n, 0};
   }
   symmetrize_lower_batched(sg, s);
-  // ---------------- Dirichlet operators for B0/B8 as dense GEMV operands:
-  //   Psi^T = K_GD K_DD^-1 = L_GD L_DD^-1  (nG x nD),  K_DD^-1 = L_DD^-T D^-1 L_DD^-1 (packed)
+  // ---------------- Dirichlet solve operator for B0/B8 as a packed GEMV operand:
+  //   K_DD^-1 = L_DD^-T D^-1 L_DD^-1 (the couplings K_GD, K_DG are applied element by element)
   {
-    int64_t lenWD = 0, lenPsi = 0, lenKDi = 0;
-    std::vector<int64_t> offWD(N), offPsi(N), offKDi(N);
+    int64_t lenWD = 0, lenKDi = 0;
+    std::vector<int64_t> offWD(N), offKDi(N);
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
       offWD[i] = lenWD; lenWD += (int64_t)S.nD * S.nD;
-      offPsi[i] = lenPsi; lenPsi += (int64_t)S.nG * S.nD;
       offKDi[i] = lenKDi; lenKDi += packed_size(S.nD);
-      c->h_sub[i].off_Psi = offPsi[i];
       c->h_sub[i].off_KDi = offKDi[i];
     }
     DBuf<double> WD, WD2, dD;
@@ -501,18 +499,11 @@ static void stage_dirichlet(vb_ctx *c) {
       recip_diag_batched(dd, dD.p, s);
     }
     VB_STAGE();
-    c->d_Psi.alloc(std::max<int64_t>(lenPsi, 1));
     WD2.alloc(lenWD);
     GemmPlan plan;
     int l0 = plan.begin_launch();
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      GemmProb p{};
-      p.A = c->d_K.p + S.off_K + S.nD; p.lda = S.n;                 // L_GD (nG x nD)
-      p.B = WD.p + offWD[i]; p.ldb = S.nD;                          // L_DD^-1
-      p.C = c->d_Psi.p + offPsi[i]; p.ldc = S.nG;
-      p.M = S.nG; p.N = S.nD; p.K = S.nD; p.alpha = 1.0; p.beta = 0.0;
-      plan.add(p);
       GemmProb q{};
       q.A = WD.p + offWD[i]; q.lda = S.nD; q.transA = 1;
       q.d = dD.p + S.off_Dn; q.dstride = 1;

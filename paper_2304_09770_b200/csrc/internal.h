@@ -191,7 +191,6 @@ struct SubDev {
   int64_t off_I;              // offset into length-nI vectors
   int64_t off_Dn;             // offset into length-nD vectors
   int64_t off_X;              // scratch square (nG x nG) offset
-  int64_t off_Psi;            // Psi^T = K_GD K_DD^-1 (nG x nD, column-major, ld = nG)
   int64_t off_KDi;            // packed tiles of K_DD^-1 (Q_I-augmented, A5)
   double vol, gamma;
 };
@@ -275,6 +274,7 @@ struct vb_ctx {
   vb::DBuf<double> d_elA, d_elB;     // element matrices: A [nK][nv_max^2], B [nK][np*nv_max]
   vb::DBuf<int64_t> d_cell_l2g;      // [nK][nv_max] global velocity ids (-1 pad)
   vb::DBuf<int> d_cell_loc;          // [nK][nv_max + np] position in subdomain matrix (-1 = drop)
+  std::vector<int> h_cell_loc;       // host copy (B0/B8 coupling plans)
   vb::DBuf<int> d_cell_nv;
   vb::DBuf<int64_t> d_vel2free;
   double flux_violation = 0;
@@ -285,7 +285,7 @@ struct vb_ctx {
   int max_npi = 0, geo_stride = 0;
   std::vector<double> cellgeo;       // host copy of d_cellgeo
   vb::DBuf<double> d_K;              // subdomain dense matrices
-  vb::DBuf<double> d_ST, d_STp, d_SDi /* D S_DD^-1 D^T */, d_Phi /* D Phi */, d_Sc, d_Psi, d_KDi;
+  vb::DBuf<double> d_ST, d_STp, d_SDi /* D S_DD^-1 D^T */, d_Phi /* D Phi */, d_Sc, d_KDi;
   int64_t len_KDi = 0;
   vb::DBuf<double> d_T, d_C, d_Dlx;  // per-entity T_G, constraint rows, deluxe blocks
   vb::DBuf<int> d_act_slots, d_act_ents;   // slots / entities with a dual part (nd > 0)

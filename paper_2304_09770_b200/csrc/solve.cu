@@ -512,51 +512,103 @@ __global__ void rhs_D_kernel(const SubDev *__restrict__ subs, const int64_t *__r
     b[S.nI + a] = rhs[nvf + Pglob[S.off_P + a]] - mvec[S.off_P + a] * g / S.vol;
 }
 
-// B0: z_G = -Psi^T b_D = -K_GD K_DD^-1 b_D (thread per interface row, column-major Psi^T)
-__global__ void __launch_bounds__(128) zG_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Psi,
-                                                 const double *__restrict__ bD, double *zG) {
-  const SubDev S = subs[blockIdx.y];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= S.nG) return;
-  const double *P = Psi + S.off_Psi;
-  const double *b = bD + S.off_Dn;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  int j = 0;
-  for (; j + 3 < S.nD; j += 4) {
-    a0 += P[i + (int64_t)j * S.nG] * b[j];
-    a1 += P[i + (int64_t)(j + 1) * S.nG] * b[j + 1];
-    a2 += P[i + (int64_t)(j + 2) * S.nG] * b[j + 2];
-    a3 += P[i + (int64_t)(j + 3) * S.nG] * b[j + 3];
+// B0 / B8 coupling blocks applied element by element (no dense K_GD K_DD^-1 is stored): the
+// coupling of the assembled, pressure-projected subdomain matrix (assemble_kernel) is
+//   K_GI = sum_K A^K[G, I],   K_GP = sum_K B^K[P, G]^T - b0 m^T / vol   (the Pi^T projection of the
+//   pressure rows; b0 = c^T B[P, G] is the stored flux row), K_DG = K_GD^T.
+// MODE 0 (B0): zG = -(K_GI x_I + K_GP x_P)   with x_D = K_DD^-1 b_D  (= -K_GD K_DD^-1 b_D)
+// MODE 1 (B8): t  = [K_IG u_G ; K_PG u_G]    with u_G gathered from the free-DOF vector
+// Three deterministic passes: the per-subdomain projection scalar (m . x_P or b0 . u_G), the element
+// rows (warp per row, one CTA per cell, into a per-(cell, row) buffer), and a gather of each output
+// row over its (cell, row) contributions in cell order (CSR built on the host) with the projection.
+template <int MODE>
+__global__ void coupling_scalar_kernel(const SubDev *__restrict__ subs, const double *__restrict__ mvec,
+                                       const double *__restrict__ b0all, const double *__restrict__ xin,
+                                       const int64_t *__restrict__ Gfree, double *scal) {
+  __shared__ double red[32];
+  const SubDev S = subs[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double v = 0.0;
+  if (MODE == 0)
+    for (int a = threadIdx.x; a < S.nP; a += blockDim.x) v += mvec[S.off_P + a] * xin[S.off_Dn + S.nI + a];
+  else
+    for (int g = threadIdx.x; g < S.nG; g += blockDim.x) v += b0all[S.off_G + g] * xin[Gfree[S.off_G + g]];
+  v = warp_sum(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += red[w];
+    scal[blockIdx.x] = t / S.vol;
   }
-  for (; j < S.nD; ++j) a0 += P[i + (int64_t)j * S.nG] * b[j];
-  zG[S.off_G + i] = -((a0 + a1) + (a2 + a3));
 }
 
-// B8: x_D[j] = y_D[j] - sum_i Psi^T[i, j] x_G[i]  (y_D = K_DD^-1 b_D from the packed GEMV partials);
-// warp per column j of Psi^T (contiguous), XD_SPLIT CTAs per subdomain.
-constexpr int XD_SPLIT = 4;
-__global__ void __launch_bounds__(256) xD_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Psi,
-                                                 const double *__restrict__ ypart, int64_t pstride, int P,
-                                                 const int64_t *__restrict__ Gfree, const double *__restrict__ x_in,
-                                                 double *xD) {
-  extern __shared__ double xg[];
-  const SubDev S = subs[blockIdx.y];
-  for (int i = threadIdx.x; i < S.nG; i += blockDim.x) xg[i] = x_in[Gfree[S.off_G + i]];
-  __syncthreads();
+template <int MODE>
+__global__ void __launch_bounds__(128) coupling_cell_kernel(
+    const int *__restrict__ cell_sub, const SubDev *__restrict__ subs, const int *__restrict__ cell_loc,
+    const int *__restrict__ cell_nv, const double *__restrict__ elA, const double *__restrict__ elB, int nvmax, int np,
+    const double *__restrict__ xin, const int64_t *__restrict__ Gfree, double *ycell) {
+  const int cell = blockIdx.x;
+  const SubDev S = subs[cell_sub[cell]];
+  const int nI = S.nI, nIP = S.nI + S.nP;
+  const int nv = cell_nv[cell], stride = nvmax + np;
+  const int *loc = cell_loc + (int64_t)cell * stride;
+  const double *A = elA + (int64_t)cell * nvmax * nvmax;
+  const double *B = elB + (int64_t)cell * np * nvmax;
+  const double *xD = xin + S.off_Dn;
+  double *y = ycell + (int64_t)cell * stride;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double *Pm = Psi + S.off_Psi;
-  for (int j = blockIdx.x * nw + warp; j < S.nD; j += gridDim.x * nw) {
-    const double *col = Pm + (int64_t)j * S.nG;
-    double v0 = 0.0, v1 = 0.0;
-    int i = lane;
-    for (; i + 32 < S.nG; i += 64) { v0 += col[i] * xg[i]; v1 += col[i + 32] * xg[i + 32]; }
-    for (; i < S.nG; i += 32) v0 += col[i] * xg[i];
-    const double v = warp_sum(v0 + v1);
-    if (lane == 0) {
-      double y = 0.0;
-      for (int c = 0; c < P; ++c) y += ypart[c * pstride + S.off_Dn + j];
-      xD[S.off_Dn + j] = y - v;
+  for (int a = warp; a < nv + np; a += nw) {
+    const bool pres = a >= nv;
+    const int la = pres ? loc[nvmax + (a - nv)] : loc[a];
+    double v = 0.0;
+    if (MODE == 0) {            // interface velocity rows
+      if (pres || la < nIP) continue;
+      for (int b = lane; b < nv; b += 32) {
+        const int lb = loc[b];
+        if (lb >= 0 && lb < nI) v += A[(int64_t)a * nv + b] * xD[lb];
+      }
+      for (int p = lane; p < np; p += 32) v += B[(int64_t)p * nv + a] * xD[loc[nvmax + p]];
+    } else {                    // interior velocity rows and pressure rows
+      if (!pres && (la < 0 || la >= nI)) continue;
+      const double *row = pres ? B + (int64_t)(a - nv) * nv : A + (int64_t)a * nv;
+      for (int b = lane; b < nv; b += 32) {
+        const int lb = loc[b];
+        if (lb >= nIP) v += row[b] * __ldg(xin + __ldg(Gfree + S.off_G + (lb - nIP)));
+      }
     }
+    v = warp_sum(v);
+    if (lane == 0) y[pres ? nvmax + (a - nv) : a] = v;
+  }
+}
+
+// out[r] = sum of its (cell, row) contributions in order, with the projection and (MODE 0) the sign
+template <int MODE>
+__global__ void coupling_gather_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ src,
+                                       const int *__restrict__ rsub, const SubDev *__restrict__ subs,
+                                       const double *__restrict__ ycell, const double *__restrict__ mvec,
+                                       const double *__restrict__ b0all, const double *__restrict__ scal, int64_t n,
+                                       double *out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int64_t q = ptr[r]; q < ptr[r + 1]; ++q) v += ycell[src[q]];
+    const int i = rsub[r];
+    if (MODE == 0) {
+      out[r] = -(v - b0all[r] * scal[i]);
+    } else {
+      const SubDev S = subs[i];
+      const int64_t l = r - S.off_Dn;
+      out[r] = l >= S.nI ? v - mvec[S.off_P + (l - S.nI)] * scal[i] : v;
+    }
+  }
+}
+
+// B8: x_D = y_D - sum over the GEMV chunks of K_DD^-1 t (fixed chunk order)
+__global__ void xd_update_kernel(double *xD, const double *__restrict__ part, int64_t stride, int P, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int c = 0; c < P; ++c) v += part[c * stride + i];
+    xD[i] -= v;
   }
 }
 
@@ -751,6 +803,9 @@ struct SolveState {
   SlotExchange XS, XE, XB, XH, XR;   // apply_S copies, extension products, B0 zG, DOF halo, rank partials
   EntitySum ESE, ESB, ESR;
   DBuf<int64_t> gh_dst;              // DOF halo: destination free ids of received owner values
+  DBuf<int64_t> cp_ptr[2], cp_src[2];   // B0 (zG rows) / B8 (D rows) coupling gathers: (cell, row) slots
+  DBuf<int> cp_rsub[2], cell_sub;
+  DBuf<double> ycell, cscal;
   int64_t n_gh = 0;
   bool ready = false;
   DBuf<unsigned> ticket;             // single-launch reductions
@@ -1266,9 +1321,44 @@ void prepare_solve(vb_ctx *c) {
     st->big_kd = st->sm_kd > 200 * 1024;
     size_t smg = std::max(std::max(st->big_op ? 0 : st->sm_op, st->big_loc ? 0 : st->sm_loc), st->big_kd ? 0 : st->sm_kd);
     raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS>, smg);
-    int64_t mg = 1;
-    for (auto &S : c->h_sub) mg = std::max<int64_t>(mg, S.nG);
-    raise_smem_limit((const void *)xD_kernel, (size_t)mg * 8);
+  }
+  // ---------------- B0 / B8 coupling gathers: output row <- (cell, element row) slots in cell order
+  {
+    const int stride = c->nv_max + c->np;
+    std::vector<int> csub(std::max<int64_t>(c->nKl, 1), 0);
+    std::vector<std::pair<int64_t, int64_t>> e0, e1;
+    std::vector<int> rs0(std::max<int64_t>(c->len_G, 1), 0), rs1(std::max<int64_t>(c->len_Dn, 1), 0);
+    std::vector<int> hcells;
+    for (int i = 0; i < N; ++i) {
+      const SubDev &S = c->h_sub[i];
+      for (int g = 0; g < S.nG; ++g) rs0[S.off_G + g] = i;
+      for (int d = 0; d < S.nD; ++d) rs1[S.off_Dn + d] = i;
+      for (int cell : c->subs[i].cells) {
+        csub[cell] = i;
+        const int *loc = c->h_cell_loc.data() + (size_t)cell * stride;
+        const int nv = c->cell_nv[c->cell_gid[cell]];
+        for (int a = 0; a < nv; ++a) {
+          const int la = loc[a];
+          if (la >= S.nD) e0.push_back({S.off_G + (la - S.nD), (int64_t)cell * stride + a});
+          else if (la >= 0 && la < S.nI) e1.push_back({S.off_Dn + la, (int64_t)cell * stride + a});
+        }
+        for (int p = 0; p < c->np; ++p) {
+          const int lp = loc[c->nv_max + p];
+          if (lp >= S.nI && lp < S.nD) e1.push_back({S.off_Dn + lp, (int64_t)cell * stride + c->nv_max + p});
+        }
+      }
+    }
+    auto byrow = [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) { return a.first < b.first; };
+    std::stable_sort(e0.begin(), e0.end(), byrow);
+    std::stable_sort(e1.begin(), e1.end(), byrow);
+    build_csr(std::max<int64_t>(c->len_G, 1), e0, st->cp_ptr[0], st->cp_src[0], s);
+    build_csr(std::max<int64_t>(c->len_Dn, 1), e1, st->cp_ptr[1], st->cp_src[1], s);
+    st->cp_rsub[0].upload(rs0, s);
+    st->cp_rsub[1].upload(rs1, s);
+    st->cell_sub.upload(csub, s);
+    st->ycell.alloc(std::max<int64_t>((int64_t)c->nKl * stride, 1));
+    st->ycell.zero(s);
+    st->cscal.alloc(std::max(N, 1));
   }
   VB_CUDA(cudaStreamSynchronize(s));
   st->ready = true;
@@ -1439,6 +1529,27 @@ static void build_iteration_graph(vb_ctx *c, SolveState *st) {
   VB_CUDA(e);
 }
 
+// B0 / B8 couplings (see coupling_cell_kernel): mode 0 zG = -K_GD x_D, mode 1 t = K_DG u_G
+static void coupling(vb_ctx *c, SolveState *st, int mode, const double *xin, double *out) {
+  cudaStream_t s = c->stream;
+  if (mode == 0) {
+    coupling_scalar_kernel<0><<<c->N, 256, 0, s>>>(c->d_sub.p, c->d_mvec.p, c->d_b0.p, xin, c->d_subG_free.p, st->cscal.p);
+    if (c->nKl)
+      coupling_cell_kernel<0><<<c->nKl, 128, 0, s>>>(st->cell_sub.p, c->d_sub.p, c->d_cell_loc.p, c->d_cell_nv.p, c->d_elA.p,
+                                                     c->d_elB.p, c->nv_max, c->np, xin, c->d_subG_free.p, st->ycell.p);
+    coupling_gather_kernel<0><<<grid_for(c->len_G), 256, 0, s>>>(st->cp_ptr[0].p, st->cp_src[0].p, st->cp_rsub[0].p, c->d_sub.p,
+                                                                  st->ycell.p, c->d_mvec.p, c->d_b0.p, st->cscal.p, c->len_G, out);
+  } else {
+    coupling_scalar_kernel<1><<<c->N, 256, 0, s>>>(c->d_sub.p, c->d_mvec.p, c->d_b0.p, xin, c->d_subG_free.p, st->cscal.p);
+    if (c->nKl)
+      coupling_cell_kernel<1><<<c->nKl, 128, 0, s>>>(st->cell_sub.p, c->d_sub.p, c->d_cell_loc.p, c->d_cell_nv.p, c->d_elA.p,
+                                                     c->d_elB.p, c->nv_max, c->np, xin, c->d_subG_free.p, st->ycell.p);
+    coupling_gather_kernel<1><<<grid_for(c->len_Dn), 256, 0, s>>>(st->cp_ptr[1].p, st->cp_src[1].p, st->cp_rsub[1].p, c->d_sub.p,
+                                                                   st->ycell.p, c->d_mvec.p, c->d_b0.p, st->cscal.p, c->len_Dn, out);
+  }
+  VB_CHECK_LAUNCH();
+}
+
 void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int maxit, vb_report *rep) {
   prepare_solve(c);
   SolveState *st = get_state(c);
@@ -1464,8 +1575,9 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   c->w_r.zero(s);
   rhs_D_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p, c->d_mvec.p, rhs, nvf,
                                  c->w_bD.p, c->w_r.p + NDelta + c->NPi);
-  run_sub_gemv(st, st->w_kd.p, st->nw_kd, st->sm_kd, st->big_kd, s);   // y_D = K_DD^-1 b_D
-  zG_kernel<<<dim3((maxnG + 127) / 128, N), 128, 0, s>>>(c->d_sub.p, c->d_Psi.p, c->w_bD.p, st->gbuf.p);
+  run_sub_gemv(st, st->w_kd.p, st->nw_kd, st->sm_kd, st->big_kd, s);   // x_D = K_DD^-1 b_D (chunks)
+  sum_chunks_kernel<<<(unsigned)((c->len_Dn + 31) / 32), 256, 0, s>>>(c->w_yDp.p, c->len_Dn, c->P_kd, c->len_Dn, c->w_xD.p);
+  coupling(c, st, 0, c->w_xD.p, st->gbuf.p);                             // zG = -K_GD x_D
   VB_STAGE();
   dev_gather(rhs, c->d_gam_free.p, c->nGamma, st->gam2.p, s);                // b_e (entity-major)
   run_slot_exchange(c, st->XB, st->gbuf.p, st->gbuf.p + c->len_G);          // C1 (cross-rank zG)
@@ -1529,8 +1641,11 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
     gamma_back_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_gam_free.p, c->d_T.p, c->w_x.p, NDelta,
                                                     c->w_gam.p, x);
   VB_STAGE();
-  xD_kernel<<<dim3(XD_SPLIT, N), 256, maxnG * 8, s>>>(c->d_sub.p, c->d_Psi.p, c->w_yDp.p, c->len_Dn, c->P_kd,
-                                                      c->d_subG_free.p, x, c->w_xD.p);
+  // u_D = x_D - K_DD^-1 (K_DG u_G): the coupling element by element into w_bD (b_D is spent), the packed
+  // K_DD^-1 GEMV over it (same work list), then the update of x_D
+  coupling(c, st, 1, x, c->w_bD.p);                                      // t = K_DG u_G
+  run_sub_gemv(st, st->w_kd.p, st->nw_kd, st->sm_kd, st->big_kd, s);
+  xd_update_kernel<<<grid_for(c->len_Dn), 256, 0, s>>>(c->w_xD.p, c->w_yDp.p, c->len_Dn, c->P_kd, c->len_Dn);
   xout_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->w_xD.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p, c->d_mvec.p,
                                 c->w_x.p + NDelta + c->NPi, nvf, x);
   VB_STAGE();
