@@ -39,13 +39,13 @@ struct Error {
 extern thread_local double g_malloc_s, g_free_s;
 double wall_now();
 
-// Device memory comes from the device's stream-ordered pool (cudaMallocAsync / cudaFreeAsync on the
-// stream of the context being served, release threshold raised so freed blocks are reused instead
-// of unmapped): the factorisation allocates and frees multi-GB scratch per stage, and plain
-// cudaMalloc/cudaFree cost it 0.5-1 s of synchronous mapping work.  Every ABI entry point sets
-// g_alloc_stream (AllocStreamScope) to its context's stream.
+// Device memory: cudaMalloc / cudaFree by default; with VB_POOL=1 the device's stream-ordered pool
+// (cudaMallocAsync / cudaFreeAsync on the stream of the context being served, release threshold
+// raised so freed blocks are reused).  Measured on config 5 the pool removed the synchronous cudaFree
+// cost but raised the factor's first-touch mapping (its footprint grows), 1.25 s against 0.8 s
+// typical.  Every ABI entry point sets g_alloc_stream (AllocStreamScope).
 extern thread_local cudaStream_t g_alloc_stream;
-extern bool g_use_pool;   // VB_NO_POOL=1: plain cudaMalloc / cudaFree
+extern bool g_use_pool;   // VB_POOL=1: stream-ordered pool; default plain cudaMalloc / cudaFree
 void pool_init();
 void pool_trim(cudaStream_t s);
 struct vb_ctx_fwd;   // sync s, then return unused pool memory to the device
