@@ -479,7 +479,7 @@ static void stage_dirichlet(vb_ctx *c) {
       offKDi[i] = lenKDi; lenKDi += packed_size(S.nD);
       c->h_sub[i].off_KDi = offKDi[i];
     }
-    DBuf<double> WD, WD2, dD;
+    DBuf<double> WD, dD;
     WD.alloc(lenWD);
     WD.zero(s);
     std::vector<TriDesc> td(N);
@@ -499,7 +499,7 @@ static void stage_dirichlet(vb_ctx *c) {
       recip_diag_batched(dd, dD.p, s);
     }
     VB_STAGE();
-    WD2.alloc(lenWD);
+    // K_DD^-1 (lower) overwrites the consumed L_DD block of K (leading dimension n)
     GemmPlan plan;
     int l0 = plan.begin_launch();
     for (int i = 0; i < N; ++i) {
@@ -508,7 +508,7 @@ static void stage_dirichlet(vb_ctx *c) {
       q.A = WD.p + offWD[i]; q.lda = S.nD; q.transA = 1;
       q.d = dD.p + S.off_Dn; q.dstride = 1;
       q.B = WD.p + offWD[i]; q.ldb = S.nD;
-      q.C = WD2.p + offWD[i]; q.ldc = S.nD;
+      q.C = c->d_K.p + S.off_K; q.ldc = S.n;
       q.M = q.N = q.K = S.nD; q.alpha = 1.0; q.beta = 0.0; q.lower = 1;
       plan.add(q);
     }
@@ -519,7 +519,7 @@ static void stage_dirichlet(vb_ctx *c) {
     std::vector<PackDesc> pk(N);
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      pk[i] = PackDesc{WD2.p + offWD[i], S.nD, S.nD, c->d_KDi.p + offKDi[i]};
+      pk[i] = PackDesc{c->d_K.p + S.off_K, S.nD, S.n, c->d_KDi.p + offKDi[i]};
     }
     pack_tiles_batched(pk, s);
     c->len_KDi = lenKDi;
@@ -563,9 +563,8 @@ static void stage_interface(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumb
   c->d_sub.upload(c->h_sub, s);
   build_transformed_maps(c);
   // ---------------- S_T = T^T S_G T (into the trailing block of K), via scratch X = S_G T
-  DBuf<double> X, Y;
+  DBuf<double> X;
   X.alloc(c->len_X);
-  Y.alloc(c->len_X);
   {
     GemmPlan plan;
     int l0 = plan.begin_launch();
@@ -650,9 +649,11 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
   const int nslot = c->h_slot.size();
   const int nent = c->h_ent.size();
   std::vector<MatDesc> mats(N), sg(N);
-  DBuf<double> X, Y, Wbuf, dinv;
+  // Y = S_DD^-1 (and later D S_DD^-1 D^T) lives in the dual block of the trailing matrix of K
+  // (leading dimension n), whose L_DD is consumed by the triangular inverse into X
+  DBuf<double> X, Wbuf, dinv;
   X.alloc(c->len_X);
-  Y.alloc(c->len_X);
+  auto Yp = [&](const SubDev &S) { return c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1); };
   Wbuf.alloc(std::max<int64_t>(c->len_sum, 1));
   // ---------------- A3: partial LDL^T of S_T eliminating the dual block -> S_c trailing
   c->d_info.zero(s);
@@ -697,7 +698,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
       p.A = X.p + S.off_X; p.lda = S.nd; p.transA = 1;
       p.d = dinv.p + S.off_Dv; p.dstride = 1;
       p.B = X.p + S.off_X; p.ldb = S.nd;
-      p.C = Y.p + S.off_X; p.ldc = S.nd;
+      p.C = Yp(S); p.ldc = S.n;
       p.M = p.N = p.K = S.nd; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
       plan.add(p);
       GemmProb q{};
@@ -808,7 +809,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     std::vector<MatDesc> ym;
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      if (S.nd) ym.push_back(MatDesc{Y.p + S.off_X, S.nd, S.nd, 0});
+      if (S.nd) ym.push_back(MatDesc{Yp(S), S.nd, S.n, 0});
     }
     symmetrize_lower_batched(ym, s);
     DBuf<double> PhiH;
@@ -822,7 +823,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
         const SubDev &S = c->h_sub[sl.sub];
         GemmProb p{};
         p.A = c->d_Dlx.p + sl.off_Dlx; p.lda = sl.nd;
-        p.B = Y.p + S.off_X + sl.offD; p.ldb = S.nd;
+        p.B = Yp(S) + sl.offD; p.ldb = S.n;
         p.C = X.p + S.off_X + sl.offD; p.ldc = S.nd;
         p.M = sl.nd; p.N = S.nd; p.K = sl.nd; p.alpha = 1.0; p.beta = 0.0;
         plan.add(p);
@@ -843,7 +844,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
         GemmProb p{};
         p.A = X.p + S.off_X + (int64_t)sl.offD * S.nd; p.lda = S.nd;
         p.B = c->d_Dlx.p + sl.off_Dlx; p.ldb = sl.nd; p.transB = 1;
-        p.C = Y.p + S.off_X + (int64_t)sl.offD * S.nd; p.ldc = S.nd;
+        p.C = Yp(S) + (int64_t)sl.offD * S.n; p.ldc = S.n;
         p.M = S.nd; p.N = sl.nd; p.K = sl.nd; p.alpha = 1.0; p.beta = 0.0;
         plan.add(p);
       }
@@ -860,7 +861,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     std::vector<PackDesc> pk(N);
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      pk[i] = PackDesc{Y.p + S.off_X, S.nd, S.nd, c->d_SDi.p + S.off_SDi};
+      pk[i] = PackDesc{Yp(S), S.nd, S.n, c->d_SDi.p + S.off_SDi};
     }
     pack_tiles_batched(pk, s);
   }

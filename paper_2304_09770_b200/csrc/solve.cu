@@ -1165,9 +1165,7 @@ void prepare_solve(vb_ctx *c) {
         for (int t = 0; t < D.r; ++t) pr.push_back({c->n_delta_glob + D.off_pl + t, src[D.nd + t]});
       }
     }
-    std::stable_sort(pr.begin(), pr.end(), [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) {
-      return a.first < b.first;
-    });
+    // (build_csr keeps the generation order within each row)
     build_csr(c->n_delta_glob + c->NPi, pr, st->xptr, st->xidx, s);
   }
   // ---------------- B7 (extension): per-slot scaled products (in w_locD, subdomain-major) and their
@@ -1274,9 +1272,7 @@ void prepare_solve(vb_ctx *c) {
       const int r = c->sub_rank[g];
       pr.push_back({c->NPi_g + g, base(r) + lenPi[r] + sub_r0[g]});
     }
-    std::stable_sort(pr.begin(), pr.end(), [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) {
-      return a.first < b.first;
-    });
+    // (build_csr keeps the generation order within each row)
     build_csr(c->Nc, pr, st->pptr, st->pidx, s);
     // z tail <- u_c: local primal coordinates, then the local p0
     std::vector<int64_t> zm(c->NPi + N, 0);
@@ -1348,9 +1344,7 @@ void prepare_solve(vb_ctx *c) {
         }
       }
     }
-    auto byrow = [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) { return a.first < b.first; };
-    std::stable_sort(e0.begin(), e0.end(), byrow);
-    std::stable_sort(e1.begin(), e1.end(), byrow);
+    // build_csr keeps the generation order (subdomain, then cell order) within each row
     build_csr(std::max<int64_t>(c->len_G, 1), e0, st->cp_ptr[0], st->cp_src[0], s);
     build_csr(std::max<int64_t>(c->len_Dn, 1), e1, st->cp_ptr[1], st->cp_src[1], s);
     st->cp_rsub[0].upload(rs0, s);
