@@ -540,7 +540,7 @@ vb_status vb_stats(const vb_ctx *c, int64_t *o) {
   for (auto &sl : c->h_slot) ndsq += (int64_t)sl.nd * sl.nd;
   int64_t v[25] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
                    c->NPi_g, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max,
-                   c->ncolors, pkG, pkD, ndsq, ndpi, c->Nc * (c->Nc + 1) / 2, c->last_iterations, c->nK,
+                   c->ncolors, pkG, pkD, ndsq, ndpi, (c->nranks > 1 ? (int64_t)c->d_Kcs.n : c->Nc * (c->Nc + 1) / 2), c->last_iterations, c->nK,
                    (int64_t)c->factor_flops, (int64_t)(c->factor_alloc_s * 1e6)};
   memcpy(o, v, sizeof(v));
   return VB_OK;
