@@ -789,18 +789,6 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     }
   }
   STAGE_T("  deluxe D_G (A4)");
-  // ---------------- active slots / entities
-  {
-    std::vector<int> act_s, act_e;
-    for (int q = 0; q < nslot; ++q)
-      if (c->h_slot[q].nd) act_s.push_back(q);
-    for (int e = 0; e < nent; ++e)
-      if (c->h_ent[e].nd) act_e.push_back(e);
-    c->d_act_slots.upload(act_s, s);
-    c->d_act_ents.upload(act_e, s);
-    c->n_act_slots = act_s.size();
-    c->n_act_ents = act_e.size();
-  }
   // ---------------- deluxe scaling folded into the per-iteration operators (DESIGN.md "scaled local
   // operators"): with D^(m) = blockdiag over the dual slots of D_G^(m), the local part of M^-1 is
   // D S_DD^-1 D^T and the coarse basis enters as D Phi, so the iteration never applies D itself:

@@ -288,8 +288,6 @@ struct vb_ctx {
   vb::DBuf<double> d_ST, d_STp, d_SDi /* D S_DD^-1 D^T */, d_Phi /* D Phi */, d_Sc, d_KDi;
   int64_t len_KDi = 0;
   vb::DBuf<double> d_T, d_C, d_Dlx;  // per-entity T_G, constraint rows, deluxe blocks
-  vb::DBuf<int> d_act_slots, d_act_ents;   // slots / entities with a dual part (nd > 0)
-  int n_act_slots = 0, n_act_ents = 0;
   vb::DBuf<double> d_Kc, d_Kcp;      // coarse dense & packed inverse
   int64_t Nc = 0;
   // descriptors

@@ -1049,6 +1049,9 @@ static void build_csr(int64_t nrows, const std::vector<std::pair<int64_t, int64_
 void prepare_solve(vb_ctx *c) {
   SolveState *st = get_state(c);
   if (st->ready) return;
+  // row chunks per subdomain matrix for the packed GEMVs (tuning knobs VB_P_OP / VB_P_LOC)
+  if (getenv("VB_P_OP")) c->P_op = std::max(1, atoi(getenv("VB_P_OP")));
+  if (getenv("VB_P_LOC")) c->P_loc = std::max(1, atoi(getenv("VB_P_LOC")));
   cudaStream_t s = c->stream;
   const int N = c->N;
   const int64_t nx = c->nx;
@@ -1426,13 +1429,6 @@ void apply_operator_device(vb_ctx *c, const double *x, double *y) {
                                                                  c->w_elt.p);
   VB_STAGE();
   element_gather(c, c->w_elt.p, y);
-}
-
-static double read_scalar(vb_ctx *c, int i) {
-  double v;
-  VB_CUDA(cudaMemcpyAsync(&v, c->w_scal.p + i, 8, cudaMemcpyDeviceToHost, c->stream));
-  VB_CUDA(cudaStreamSynchronize(c->stream));
-  return v;
 }
 
 void lanczos_extremes(const std::vector<double> &al, const std::vector<double> &be, double *lmin, double *lmax);
