@@ -1049,7 +1049,13 @@ static void build_csr(int64_t nrows, const std::vector<std::pair<int64_t, int64_
 void prepare_solve(vb_ctx *c) {
   SolveState *st = get_state(c);
   if (st->ready) return;
-  // row chunks per subdomain matrix for the packed GEMVs (tuning knobs VB_P_OP / VB_P_LOC)
+  // row chunks per subdomain matrix for the packed GEMVs: about 2048 work items in all (4 per
+  // subdomain at 512 subdomains, more when there are few large subdomains, e.g. config 3);
+  // tuning knobs VB_P_OP / VB_P_LOC
+  {
+    const int P = std::max(4, std::min(32, (2048 + c->N - 1) / std::max(c->N, 1)));
+    c->P_op = c->P_loc = c->P_kd = P;
+  }
   if (getenv("VB_P_OP")) c->P_op = std::max(1, atoi(getenv("VB_P_OP")));
   if (getenv("VB_P_LOC")) c->P_loc = std::max(1, atoi(getenv("VB_P_LOC")));
   cudaStream_t s = c->stream;
