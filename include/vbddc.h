@@ -163,12 +163,15 @@ vb_status vb_debug_interface_op(vb_ctx *ctx, int32_t which, const double *in_hos
 /* Parity/debug and microbenchmark: the factorisation's grouped DMMA GEMM on DEVICE buffers,
  *   C_b = alpha * op(A_b) * diag(d) * op(B_b) + beta * C_b,   b = 0 .. batch-1,
  * column-major, op(X) = X or X^T (trans* = 0/1), X_b = X + b * strideX (elements); d (length K,
- * unit stride) may be NULL.  Runs on `stream` (a cudaStream_t, NULL = legacy default) and
+ * unit stride) may be NULL.  kz_on = 1 declares triangular operands, op(A)(i, k) = 0 for
+ * k < i + kzA and op(B)(k, j) = 0 for k < j + kzB, whose zero K slabs are skipped (the caller
+ * guarantees the zeros).  Runs on `stream` (a cudaStream_t, NULL = legacy default) and
  * synchronises it before returning.  VB_EINVAL on non-positive sizes or leading dimensions.      */
 vb_status vb_debug_gemm(int32_t M, int32_t N, int32_t K, double alpha, const double *A, int32_t lda,
                         int32_t transA, const double *B, int32_t ldb, int32_t transB, const double *d,
                         double beta, double *C, int32_t ldc, int32_t batch, int64_t strideA,
-                        int64_t strideB, int64_t strideC, void *stream);
+                        int64_t strideB, int64_t strideC, void *stream, int32_t kz_on, int32_t kzA,
+                        int32_t kzB);
 /* Interface DOFs (free velocity ids) in the library's entity-major order; *n = count.
  * ids may be NULL to query the count only.                                                     */
 vb_status vb_interface_dofs(const vb_ctx *ctx, int64_t *ids, int64_t *n);

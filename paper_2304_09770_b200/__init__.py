@@ -99,7 +99,8 @@ _vb_interface_dofs = _sig("vb_interface_dofs", ctypes.c_int, [_p, _i64p, _i64p])
 _vb_debug_gemm = _sig("vb_debug_gemm", ctypes.c_int,
                      [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _p, ctypes.c_int32,
                       ctypes.c_int32, _p, ctypes.c_int32, ctypes.c_int32, _p, ctypes.c_double, _p,
-                      ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _p])
+                      ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _p,
+                      ctypes.c_int32, ctypes.c_int32, ctypes.c_int32])
 
 EXPORTED = ["vb_plan_exchange", "vb_nccl_unique_id", "vb_loopback_world_create", "vb_loopback_world_destroy", "vb_setup", "vb_setup_from_elements", "vb_factor", "vb_build_rhs",
             "vb_pcg_solve", "vb_pcg_solve_host", "vb_apply_operator", "vb_debug_interface_op", "vb_debug_gemm",
@@ -299,10 +300,12 @@ def nccl_unique_id():
     return bytes(buf.raw)
 
 
-def debug_gemm(A, B, C, alpha=1.0, beta=0.0, d=None, transA=False, transB=False):
+def debug_gemm(A, B, C, alpha=1.0, beta=0.0, d=None, transA=False, transB=False, kz=None):
     """C_b = alpha op(A_b) diag(d) op(B_b) + beta C_b with the factorisation's DMMA GEMM
     (vb_debug_gemm).  A, B, C: CUDA float64 tensors of shape (batch, cols, rows) holding each matrix
-    COLUMN-major (i.e. the transposes of the logical matrices, contiguous); C is updated in place."""
+    COLUMN-major (i.e. the transposes of the logical matrices, contiguous); C is updated in place.
+    kz = (kzA, kzB): triangular operands, op(A)(i, k) = 0 for k < i + kzA, op(B)(k, j) = 0 for
+    k < j + kzB (the kernel skips those K slabs)."""
     import torch
     for t in (A, B, C):
         assert t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.dim() == 3
@@ -315,7 +318,8 @@ def debug_gemm(A, B, C, alpha=1.0, beta=0.0, d=None, transA=False, transB=False)
                         ctypes.c_void_p(C.data_ptr()), C.shape[2], batch,
                         A.shape[1] * A.shape[2] if A.shape[0] > 1 else 0,
                         B.shape[1] * B.shape[2] if B.shape[0] > 1 else 0, C.shape[1] * C.shape[2],
-                        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+                        ctypes.c_void_p(torch.cuda.current_stream().cuda_stream), 1 if kz else 0,
+                        kz[0] if kz else 0, kz[1] if kz else 0)
     if st != VB_OK:
         raise VBError(st, _vb_last_error(None).decode())
     return C

@@ -561,7 +561,8 @@ const char *vb_last_error(const vb_ctx *c) { return c ? c->err.c_str() : g_last_
 vb_status vb_debug_gemm(int32_t M, int32_t N, int32_t K, double alpha, const double *A, int32_t lda,
                         int32_t transA, const double *B, int32_t ldb, int32_t transB, const double *d,
                         double beta, double *C, int32_t ldc, int32_t batch, int64_t strideA,
-                        int64_t strideB, int64_t strideC, void *stream) {
+                        int64_t strideB, int64_t strideC, void *stream, int32_t kz_on, int32_t kzA,
+                        int32_t kzB) {
   if (M <= 0 || N <= 0 || K <= 0 || batch <= 0 || !A || !B || !C) return VB_EINVAL;
   if (lda < (transA ? K : M) || ldb < (transB ? N : K) || ldc < M) return VB_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
@@ -576,6 +577,7 @@ vb_status vb_debug_gemm(int32_t M, int32_t N, int32_t K, double alpha, const dou
       p.C = C + b * strideC; p.ldc = ldc;
       p.d = d; p.dstride = 1;
       p.M = M; p.N = N; p.K = K; p.alpha = alpha; p.beta = beta;
+      p.kz_on = kz_on != 0; p.kzA = kzA; p.kzB = kzB;
       plan.add(p);
     }
     plan.upload(s);

@@ -134,16 +134,25 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmPro
                         : P.B + BCopy<TB>::kk0(tid) + (int64_t)(n0 + BCopy<TB>::j0(tid)) * ldb;
   const int64_t astep = TA ? GBK : (int64_t)GBK * lda, bstep = TB ? (int64_t)GBK * ldb : GBK;
   const double *A0 = P.A, *B0 = P.B;
-  issue_slab<TA, TB>(pa, pb, lda, ldb, A0, B0, rows_left, cols_left, K, dvec, dstride, tid, sm, 0);
+  int kb = 0;   // first K slab with non-zero products (triangular operands)
+  if (P.kz_on) {
+    kb = max(0, max(m0 + P.kzA, n0 + P.kzB)) / GBK * GBK;
+    if (kb > K) kb = K;
+    pa += (kb / GBK) * astep;
+    pb += (kb / GBK) * bstep;
+  }
+  if (kb < K)
+    issue_slab<TA, TB>(pa, pb, lda, ldb, A0, B0, rows_left, cols_left, K - kb,
+                       dvec ? dvec + (int64_t)kb * dstride : nullptr, dstride, tid, sm, 0);
   cp_async_commit();
-  if (GBK < K)
-    issue_slab<TA, TB>(pa + astep, pb + bstep, lda, ldb, A0, B0, rows_left, cols_left, K - GBK,
-                       dvec ? dvec + (int64_t)GBK * dstride : nullptr, dstride, tid, sm, 1);
+  if (kb + GBK < K)
+    issue_slab<TA, TB>(pa + astep, pb + bstep, lda, ldb, A0, B0, rows_left, cols_left, K - kb - GBK,
+                       dvec ? dvec + (int64_t)(kb + GBK) * dstride : nullptr, dstride, tid, sm, 1);
   cp_async_commit();
   pa += 2 * astep;
   pb += 2 * bstep;
   int st = 0;
-  for (int k0 = 0; k0 < K; k0 += GBK) {
+  for (int k0 = kb; k0 < K; k0 += GBK) {
     cp_async_wait1();       // all groups but the newest are complete: this slab has landed
     __syncthreads();        // ... for every thread; and every thread is done with the previous slab
     {
@@ -220,6 +229,18 @@ void GemmPlan::add(const GemmProb &p) {
   {
     double f = 2.0 * p.M * (double)p.N * p.K;
     if (p.lower) f *= 0.5 * (1.0 + 1.0 / std::max(1, std::min(p.M, p.N)));   // lower triangle (square C)
+    if (p.kz_on) {   // executed work: per tile, the K slabs from its first non-zero one
+      f = 0.0;
+      const int tm = (p.M + GBM - 1) / GBM, tn = (p.N + GBN - 1) / GBN;
+      for (int i = 0; i < tm; ++i)
+        for (int j = 0; j < tn; ++j) {
+          if (p.lower && (i * GBM + GBM - 1) < j * GBN) continue;
+          const int64_t kb = std::min<int64_t>(p.K, std::max<int64_t>(0, std::max<int64_t>((int64_t)i * GBM + p.kzA,
+                                                                                             (int64_t)j * GBN + p.kzB)) / GBK * GBK);
+          const int rows = std::min(GBM, p.M - i * GBM), cols = std::min(GBN, p.N - j * GBN);
+          f += 2.0 * rows * cols * (double)(p.K - kb);
+        }
+    }
     g_gemm_flops += f;
   }
   int pid = probs.size();

@@ -112,6 +112,9 @@ struct GemmProb {
   double alpha, beta;
   int transA, transB;
   int lower;         // only compute tiles intersecting the lower triangle (i >= j)
+  // triangular operands: op(A)(i, k) = 0 for k < i + kzA and op(B)(k, j) = 0 for k < j + kzB, so
+  // tile (m0, n0) starts its K loop at max(m0 + kzA, n0 + kzB) (kz_on = 1 enables it)
+  int kz_on, kzA, kzB;
 };
 
 // ------------------------------------------------------------------ packed symmetric tiles

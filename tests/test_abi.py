@@ -36,13 +36,13 @@ def test_debug_gemm_argument_checks_without_gpu():
     f = vb._vb_debug_gemm
     dummy = ctypes.c_void_p(16)
     # M = 0
-    assert f(0, 4, 4, 1.0, dummy, 4, 0, dummy, 4, 0, None, 0.0, dummy, 4, 1, 0, 0, 0, None) == vb.VB_EINVAL
+    assert f(0, 4, 4, 1.0, dummy, 4, 0, dummy, 4, 0, None, 0.0, dummy, 4, 1, 0, 0, 0, None, 0, 0, 0) == vb.VB_EINVAL
     # lda < M (A not transposed)
-    assert f(8, 4, 4, 1.0, dummy, 4, 0, dummy, 4, 0, None, 0.0, dummy, 8, 1, 0, 0, 0, None) == vb.VB_EINVAL
+    assert f(8, 4, 4, 1.0, dummy, 4, 0, dummy, 4, 0, None, 0.0, dummy, 8, 1, 0, 0, 0, None, 0, 0, 0) == vb.VB_EINVAL
     # ldb < N (B transposed)
-    assert f(8, 6, 4, 1.0, dummy, 8, 0, dummy, 4, 1, None, 0.0, dummy, 8, 1, 0, 0, 0, None) == vb.VB_EINVAL
+    assert f(8, 6, 4, 1.0, dummy, 8, 0, dummy, 4, 1, None, 0.0, dummy, 8, 1, 0, 0, 0, None, 0, 0, 0) == vb.VB_EINVAL
     # ldc < M
-    assert f(8, 4, 4, 1.0, dummy, 8, 0, dummy, 4, 0, None, 0.0, dummy, 4, 1, 0, 0, 0, None) == vb.VB_EINVAL
+    assert f(8, 4, 4, 1.0, dummy, 8, 0, dummy, 4, 0, None, 0.0, dummy, 4, 1, 0, 0, 0, None, 0, 0, 0) == vb.VB_EINVAL
     # null C / batch 0
-    assert f(8, 4, 4, 1.0, dummy, 8, 0, dummy, 4, 0, None, 0.0, None, 8, 1, 0, 0, 0, None) == vb.VB_EINVAL
-    assert f(8, 4, 4, 1.0, dummy, 8, 0, dummy, 4, 0, None, 0.0, dummy, 8, 0, 0, 0, 0, None) == vb.VB_EINVAL
+    assert f(8, 4, 4, 1.0, dummy, 8, 0, dummy, 4, 0, None, 0.0, None, 8, 1, 0, 0, 0, None, 0, 0, 0) == vb.VB_EINVAL
+    assert f(8, 4, 4, 1.0, dummy, 8, 0, dummy, 4, 0, None, 0.0, dummy, 8, 0, 0, 0, 0, None, 0, 0, 0) == vb.VB_EINVAL

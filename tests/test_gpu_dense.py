@@ -32,3 +32,21 @@ def test_gemm_vs_torch(M, N, K, batch, tA, tB):
     err = (got - ref).abs().max().item()
     scale = ((opA.abs() * d) @ opB.abs()).max().item()
     assert err <= 1e-14 * K * scale + 1e-13, err
+
+
+@pytest.mark.parametrize("n,batch", [(70, 3), (300, 2), (1300, 1)])
+def test_gemm_triangular_skip(n, batch):
+    """Triangular-operand K skipping (GemmProb.kz_on, used for W^T D W with W = L^-1 lower): the
+    kernel starts each tile's K loop at its first non-zero slab; the result must equal the full
+    product (the skipped slabs are exactly zero)."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    g = torch.Generator(device="cuda").manual_seed(n)
+    W = torch.tril(torch.randn(batch, n, n, dtype=torch.float64, device="cuda", generator=g))
+    d = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) + 0.5
+    ref = (W.transpose(1, 2) * d) @ W
+    C = torch.zeros(batch, n, n, dtype=torch.float64, device="cuda")
+    Wc = _colmajor(W)
+    vb.debug_gemm(Wc, Wc, C, d=d, transA=True, kz=(0, 0))
+    got = C.transpose(1, 2)
+    assert (got - ref).abs().max().item() <= 1e-12 * ref.abs().max().item()
