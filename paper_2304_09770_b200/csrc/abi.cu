@@ -416,6 +416,10 @@ vb_status vb_factor(vb_ctx *c) {
   if (c->state < 1) return fail(c, Error{VB_ESTATE, "vb_factor before vb_setup"});
   ABI_GUARD(c, {
     double t0 = now_s();
+    if (c->state >= 2) {   // re-factorisation: the solve state points into the old factors
+      VB_CUDA(cudaStreamSynchronize(c->stream));
+      destroy_solve_state(c);
+    }
     factor_device(c);
     prepare_solve(c);
     if (getenv("VB_FACTOR_TIMES") && atoi(getenv("VB_FACTOR_TIMES")))

@@ -148,3 +148,16 @@ def test_large_subdomains_big_gemv():
     assert torch.linalg.norm(xb[nv:] - xs[nv:]) <= 1e-8 * torch.linalg.norm(xs[nv:])
     cb.close()
     cs.close()
+
+
+def test_refactor_then_solve():
+    """vb_factor twice on one context (e.g. new viscosity data would do the same): the solve state
+    is rebuilt against the new factors; the solve is bitwise that of a single factorisation."""
+    import torch
+    prob = make_problem("c1", n=8)
+    c1, rhs, x1, r1 = _gpu_solve(prob)
+    c1.factor()
+    x2 = torch.zeros_like(rhs)
+    r2 = c1.pcg_solve(rhs, x2, rtol=1e-10)
+    assert r2["iterations"] == r1["iterations"] and torch.equal(x1, x2)
+    c1.close()
