@@ -2,6 +2,8 @@
 // FP64 tensor path of sm_100a; tcgen05 has no f64 kind), blocked partial LDL^T,
 // triangular inverse, packing.  Used by the factor stage.
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include "dense.cuh"
 
 namespace vb {
@@ -198,14 +200,23 @@ __global__ void __launch_bounds__(GTHREADS, 2) gemm_grouped_kernel(const GemmPro
       }
 }
 
+// Raise (never lower) a kernel's dynamic shared-memory limit: the attribute is process-wide and
+// several contexts / loopback ranks (threads) launch the same kernels.
+void raise_smem_limit(const void *func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> cur;
+  int dev = 0;
+  VB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t &c = cur[{func, dev}];
+  if (bytes <= c) return;
+  VB_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  c = bytes;
+}
+
 template <bool DENSE, bool SCALED, bool TA, bool TB>
 static void launch_gemm(dim3 grid, const GemmProb *probs, const int4 *tiles, int tile0, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    VB_CUDA(cudaFuncSetAttribute(gemm_grouped_kernel<DENSE, SCALED, TA, TB>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GemmSmem)));
-    attr = true;
-  }
+  raise_smem_limit((const void *)gemm_grouped_kernel<DENSE, SCALED, TA, TB>, sizeof(GemmSmem));
   gemm_grouped_kernel<DENSE, SCALED, TA, TB><<<grid, GTHREADS, sizeof(GemmSmem), s>>>(probs, tiles, tile0);
   VB_CHECK_LAUNCH();
 }

@@ -33,6 +33,8 @@ struct GemmPlan {
 };
 
 void gemm_grouped(GemmPlan &plan, int launch, cudaStream_t s);
+// process-wide kernel attribute, only ever raised (thread-safe; several contexts share kernels)
+void raise_smem_limit(const void *func, size_t bytes);
 extern thread_local double g_gemm_flops;   // flops of the GEMMs planned since the last reset
 
 // Partial LDL^T (no pivoting, velocity-first quasi-definite ordering) of a batch:

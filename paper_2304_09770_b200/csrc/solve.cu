@@ -144,21 +144,6 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
     for (int j = tid; j < n; j += blockDim.x) W.out[j] = ys[j];
 }
 
-// Raise (never lower) a kernel's dynamic shared-memory limit.  The attribute is process-wide, and
-// several contexts in one process (or loopback ranks on threads) size the same kernels differently:
-// a context must never shrink the limit another one launches with.
-static void raise_smem_limit(const void *func, size_t bytes) {
-  static std::mutex mu;
-  static std::map<std::pair<const void *, int>, size_t> cur;
-  int dev = 0;
-  VB_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> lock(mu);
-  size_t &c = cur[{func, dev}];
-  if (bytes <= c) return;
-  VB_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  c = bytes;
-}
-
 static size_t gemv_smem(int nmax, int warps = GV_WARPS) {
   return (size_t)(2 * ((nmax + 31) / 32) * 32 + warps * 32) * sizeof(double);
 }

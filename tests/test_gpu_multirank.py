@@ -40,9 +40,17 @@ def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=N
         ctx.close()
         return out
 
+    def guarded(r):
+        try:
+            return rank_main(r)
+        except Exception as e:   # keep every rank's error: the first failure aborts the others
+            return e
+
     with cf.ThreadPoolExecutor(R) as ex:
-        outs = list(ex.map(rank_main, range(R)))
+        outs = list(ex.map(guarded, range(R)))
     world.close()
+    errs = [(r, o) for r, o in enumerate(outs) if isinstance(o, Exception)]
+    assert not errs, "rank errors: " + "; ".join("rank %d: %s" % (r, e) for r, e in errs)
     return outs
 
 
