@@ -573,6 +573,7 @@ vb_status vb_debug_gemm(int32_t M, int32_t N, int32_t K, double alpha, const dou
   ABI_GUARD(nullptr, {
     AllocStreamScope scope(s);
     GemmPlan plan;
+    plan.allow_kz = true;
     int l0 = plan.begin_launch();
     for (int b = 0; b < batch; ++b) {
       GemmProb p{};

@@ -819,8 +819,27 @@ struct SolveState {
 
 // launch with the PDL attribute when enabled (kernels of the PCG step start with pdl_prologue)
 template <typename... KArgs, typename... Args>
+static void launch_k(const SolveState *st, bool pdl, void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t s,
+                     Args &&...args);
+
+template <typename... KArgs, typename... Args>
 static void launch_pdl(const SolveState *st, void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t s,
                        Args &&...args) {
+  launch_k(st, true, k, g, b, sm, s, std::forward<Args>(args)...);
+}
+
+// the first kernel after a cross-stream event wait (fork / join of the coarse branch) is launched
+// without the programmatic-serialisation attribute: its launch must wait for the event, not only
+// for the previous kernel of its own stream
+template <typename... KArgs, typename... Args>
+static void launch_after_event(const SolveState *st, void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t s,
+                               Args &&...args) {
+  launch_k(st, false, k, g, b, sm, s, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_k(const SolveState *st, bool pdl, void (*k)(KArgs...), dim3 g, dim3 b, size_t sm, cudaStream_t s,
+                     Args &&...args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = g;
   cfg.blockDim = b;
@@ -828,7 +847,7 @@ static void launch_pdl(const SolveState *st, void (*k)(KArgs...), dim3 g, dim3 b
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   int na = 0;
-  if (st->pdl) {
+  if (st->pdl && pdl) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
@@ -975,7 +994,7 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   run_sub_gemv(st, st->w_loc.p, st->nw_loc, st->sm_loc, st->big_loc, s);
   tick(c, st, 1, false);
   // coarse pieces (C2): [Phi_i^T rD_i per local subdomain | r0_i | r_Pi of the owned entities]
-  launch_pdl(st, phit_kernel, dim3(PHIT_SPLIT, c->N), dim3(256), st->max_nd * sizeof(double), s2, c->d_sub.p, c->d_Phi.p,
+  launch_after_event(st, phit_kernel, dim3(PHIT_SPLIT, c->N), dim3(256), st->max_nd * sizeof(double), s2, c->d_sub.p, c->d_Phi.p,
              c->d_loc2x.p, c->w_r.p, st->cbuf.p);
   dev_gather(c->w_r.p, st->cpack.p, (int64_t)st->cpack.n, st->cbuf.p + c->len_Pi, s2);
   const double *pieces = st->cbuf.p;
@@ -1004,7 +1023,7 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   VB_CUDA(cudaEventRecord(st->ev_join, s2));
   VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
   trace_norm(c, "uc", c->w_uc.p, c->Nc, true);
-  launch_pdl(st, local2_kernel, dim3((st->max_nd + 127) / 128, c->N), dim3(128), c->max_npi * sizeof(double), s,
+  launch_after_event(st, local2_kernel, dim3((st->max_nd + 127) / 128, c->N), dim3(128), c->max_npi * sizeof(double), s,
       c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p);
   trace_norm(c, "t", c->w_locD.p, c->len_Dv, false);
   run_slot_exchange(c, st->XE, c->w_locD.p, c->w_locD.p + c->len_Dv);    // C1 (cross-rank products)
