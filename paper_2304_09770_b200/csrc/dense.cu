@@ -241,8 +241,8 @@ void GemmPlan::add(const GemmProb &p_in) {
   // triangular-operand K skipping is opt-in (VB_KZ=1): correct on every single-GPU and GEMM parity
   // test, but with it the loopback multi-rank tests failed intermittently (EBREAKDOWN in ~1 of 7
   // runs; 0 of 36 without), cause not yet found -- see DESIGN.md §9
-  static const bool kz = getenv("VB_KZ") && atoi(getenv("VB_KZ"));
-  if (!kz && !allow_kz) p.kz_on = 0;
+  static const int kz_mask = getenv("VB_KZ") ? atoi(getenv("VB_KZ")) : 0;   // 1 = all sites, else site bits
+  if (!allow_kz) p.kz_on = (kz_mask == 1 || (p.kz_on & kz_mask)) ? p.kz_on : 0;
   {
     double f = 2.0 * p.M * (double)p.N * p.K;
     if (p.lower) f *= 0.5 * (1.0 + 1.0 / std::max(1, std::min(p.M, p.N)));   // lower triangle (square C)

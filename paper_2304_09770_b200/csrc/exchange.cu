@@ -121,7 +121,10 @@ void build_slot_exchange(vb_ctx *c, SlotExchange &X, const std::function<int64_t
 }
 
 void run_slot_exchange(vb_ctx *c, SlotExchange &X, const double *local, double *recv) {
-  if (c->nranks == 1 || X.xfers.empty()) return;
+  // every rank takes part, even with nothing to move: the loopback transport's exchange is a
+  // collective (a rank skipping it would pair its next collective with the others' exchange);
+  // the NCCL transport returns at once for an empty peer list (point-to-point semantics)
+  if (c->nranks == 1) return;
   if (X.send_len) {
     const int grid = (int)std::min<int64_t>((X.send_len + 255) / 256, 148 * 8);
     pack_kernel<<<grid, 256, 0, c->stream>>>(local, X.send_idx.p, X.send_len, X.sendbuf.p);

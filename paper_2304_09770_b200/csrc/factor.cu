@@ -510,7 +510,7 @@ static void stage_dirichlet(vb_ctx *c) {
       q.B = WD.p + offWD[i]; q.ldb = S.nD;
       q.C = c->d_K.p + S.off_K; q.ldc = S.n;
       q.M = q.N = q.K = S.nD; q.alpha = 1.0; q.beta = 0.0; q.lower = 1;
-      q.kz_on = 1;   // W lower triangular: only k >= max(i, j) contributes
+      q.kz_on = 1;   // W lower triangular: only k >= max(i, j) contributes (site bit 1)
       plan.add(q);
     }
     plan.upload(s);
@@ -701,14 +701,14 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
       p.B = X.p + S.off_X; p.ldb = S.nd;
       p.C = Yp(S); p.ldc = S.n;
       p.M = p.N = p.K = S.nd; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
-      p.kz_on = 1;   // W lower triangular
+      p.kz_on = 2;   // W lower triangular (site bit 2)
       plan.add(p);
       GemmProb q{};
       q.A = X.p + S.off_X; q.lda = S.nd; q.transA = 1;
       q.B = c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1) + S.nd; q.ldb = S.n; q.transB = 1;
       q.C = c->d_Phi.p + S.off_Phi; q.ldc = S.nd;
       q.M = S.nd; q.N = S.npi; q.K = S.nd; q.alpha = -1.0; q.beta = 0.0;
-      q.kz_on = 1; q.kzB = -(1 << 30);   // W^T: only k >= i contributes
+      q.kz_on = 4; q.kzB = -(1 << 30);   // W^T: only k >= i contributes (site bit 4)
       plan.add(q);
     }
     plan.upload(s);
@@ -950,7 +950,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
       p.A = Wc.p; p.lda = Nc; p.transA = 1; p.d = dc.p; p.dstride = 1;
       p.B = Wc.p; p.ldb = Nc; p.C = Kc.p; p.ldc = Nc;
       p.M = p.N = p.K = Nc; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
-      p.kz_on = 1;   // W lower triangular
+      p.kz_on = 8;   // W lower triangular (site bit 8)
       plan.add(p);
       plan.upload(s);
       plan.run(l0, s);
@@ -986,7 +986,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
         p.A = Wc.p + lo * Nc + lo; p.lda = Nc; p.transA = 1; p.d = dc.p + lo; p.dstride = 1;
         p.B = Wc.p + lo; p.ldb = Nc; p.C = Kr.p; p.ldc = mine;
         p.M = mine; p.N = hi; p.K = Nc - lo; p.alpha = 1.0; p.beta = 0.0;
-        p.kz_on = 1; p.kzB = (int)-lo;   // W(lo + k, lo + i) = 0 for k < i, W(lo + k, j) = 0 for k < j - lo
+        p.kz_on = 16; p.kzB = (int)-lo;   // (site bit 16)   // W(lo + k, lo + i) = 0 for k < i, W(lo + k, j) = 0 for k < j - lo
         plan.add(p);
         plan.upload(s);
         plan.run(l0, s);

@@ -4,7 +4,7 @@ cd "$(dirname "$0")/.."
 for mode in ${MODES:-default VB_NO_PDL VB_NO_PRIO}; do
   fails=0
   for i in $(seq 1 ${1:-6}); do
-    if [ "$mode" = default ]; then env=""; else env="$mode=1"; fi
+    if [ "$mode" = default ]; then env=""; else case "$mode" in *=*) env="$mode";; *) env="$mode=1";; esac; fi
     out=$(env $env timeout 200 python -m pytest tests/test_gpu_multirank.py -q -x -k "irregular or rank_grid0 or rank_grid1" 2>&1)
     if echo "$out" | tail -1 | grep -q failed; then
       fails=$((fails+1))
