@@ -241,10 +241,14 @@ __global__ void dot_final_kernel(const double *__restrict__ part, int nb, double
 __global__ void update_p_kernel(double *p, const double *z, int64_t n, double *scal, int first, double *hist,
                                 unsigned *ticket) {
   pdl_prologue();
-  const double beta = first ? 0.0 : scal[3] / scal[0];
+  if (first) {   // p_0 = z_0 (p holds no previous direction: never read it, it may hold NaN bits)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+      p[i] = z[i];
+    return;
+  }
+  const double beta = scal[3] / scal[0];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
-  if (first) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
