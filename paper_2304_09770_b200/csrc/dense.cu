@@ -238,11 +238,10 @@ thread_local double g_gemm_flops = 0.0;   // DMMA GEMM flops issued by this thre
 void GemmPlan::add(const GemmProb &p_in) {
   if (p_in.M <= 0 || p_in.N <= 0) return;
   GemmProb p = p_in;
-  // triangular-operand K skipping is opt-in (VB_KZ=1): correct on every single-GPU and GEMM parity
-  // test, but with it the loopback multi-rank tests failed intermittently (EBREAKDOWN in ~1 of 7
-  // runs; 0 of 36 without), cause not yet found -- see DESIGN.md §9
-  static const int kz_mask = getenv("VB_KZ") ? atoi(getenv("VB_KZ")) : 0;   // 1 = all sites, else site bits
-  if (!allow_kz) p.kz_on = (kz_mask == 1 || (p.kz_on & kz_mask)) ? p.kz_on : 0;
+  // triangular-operand K skipping (GemmProb.kz_on: a site bit, see factor.cu); VB_KZ=0 disables it,
+  // VB_KZ=<bits> keeps only those sites (diagnostics)
+  static const int kz_mask = getenv("VB_KZ") ? atoi(getenv("VB_KZ")) : -1;
+  if (!allow_kz) p.kz_on = (p.kz_on & kz_mask) ? p.kz_on : 0;
   {
     double f = 2.0 * p.M * (double)p.N * p.K;
     if (p.lower) f *= 0.5 * (1.0 + 1.0 / std::max(1, std::min(p.M, p.N)));   // lower triangle (square C)

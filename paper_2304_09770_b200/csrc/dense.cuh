@@ -19,7 +19,7 @@ struct GemmPlan {
   std::vector<std::array<std::pair<int, int>, 4>> lrange;  // after upload: (tile_begin, tile_count)
   std::vector<std::vector<int>> dense;        // per launch: large problems run as 2D grids
   std::vector<char> scaled;                   // per launch: some tile-list problem has d != null
-  bool allow_kz = false;                      // honour GemmProb.kz_on without VB_KZ (vb_debug_gemm)
+  bool allow_kz = false;                      // honour GemmProb.kz_on regardless of VB_KZ (vb_debug_gemm)
   DBuf<GemmProb> d_probs;
   DBuf<int4> d_tiles;
   int begin_launch() {
