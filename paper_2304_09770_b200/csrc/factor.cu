@@ -21,6 +21,7 @@ namespace vb {
 thread_local double g_malloc_s = 0.0, g_free_s = 0.0;
 thread_local cudaStream_t g_alloc_stream = nullptr;
 bool g_use_pool = getenv("VB_POOL") && atoi(getenv("VB_POOL"));   // opt-in
+bool g_poison = getenv("VB_POISON") && atoi(getenv("VB_POISON"));
 
 void pool_init() {
   static thread_local int done_dev = -1;

@@ -46,6 +46,7 @@ double wall_now();
 // typical.  Every ABI entry point sets g_alloc_stream (AllocStreamScope).
 extern thread_local cudaStream_t g_alloc_stream;
 extern bool g_use_pool;   // VB_POOL=1: stream-ordered pool; default plain cudaMalloc / cudaFree
+extern bool g_poison;     // VB_POISON=1: fill every new device allocation with NaN bits (tests)
 void pool_init();
 void pool_trim(cudaStream_t s);
 struct vb_ctx_fwd;   // sync s, then return unused pool memory to the device
@@ -86,6 +87,7 @@ struct DBuf {
       throw Error{VB_ENOMEM, "cudaMallocAsync of " + std::to_string(count * sizeof(T)) + " bytes failed"};
     }
     n = count;
+    if (g_poison) cudaMemsetAsync(p, 0xFF, count * sizeof(T), g_alloc_stream);   // all-ones = NaN
   }
   void zero(cudaStream_t s) {
     if (n) VB_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));

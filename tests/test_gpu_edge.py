@@ -161,3 +161,45 @@ def test_refactor_then_solve():
     r2 = c1.pcg_solve(rhs, x2, rtol=1e-10)
     assert r2["iterations"] == r1["iterations"] and torch.equal(x1, x2)
     c1.close()
+
+
+def test_no_uninitialised_reads_poisoned_memory():
+    """Every device allocation filled with NaN bits (VB_POISON=1, in a fresh process): a 1-rank solve,
+    an adaptive solve and a 2-rank loopback solve must still converge to the same answers -- no kernel
+    may read memory it has not written (regression: the first CG direction once read p)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r'''
+import sys, concurrent.futures as cf, numpy as np, torch
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_2304_09770_b200 as vb
+from synthetic import make_problem
+def solve(prob, **kw):
+    ctx = vb.context_for(prob, **kw); ctx.factor()
+    rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda"); x = torch.zeros_like(rhs)
+    torch.cuda.synchronize(); ctx.build_rhs(vb.problem_args(prob), rhs)
+    rep = ctx.pcg_solve(rhs, x, rtol=1e-10); ids = ctx.dof_layout(); xh = x.cpu().numpy(); ctx.close()
+    return rep, ids, xh
+for name, kw in (("c1", dict(n=8)), ("c4", dict(n=8))):
+    rep, ids, x = solve(make_problem(name, **kw))
+    assert rep["status"] == "OK" and np.all(np.isfinite(x)), (name, rep)
+prob = make_problem("c1", n=8)
+rep1, ids1, x1 = solve(prob)
+world = vb.LoopbackWorld(2); srank = vb.box_ranks(prob.sub_grid, (1, 1, 2))
+streams = [torch.cuda.Stream() for _ in range(2)]
+with cf.ThreadPoolExecutor(2) as ex:
+    outs = list(ex.map(lambda r: solve(prob, stream=streams[r], rank=r, nranks=2, subdomain_rank=srank, world=world), range(2)))
+world.close()
+pos = {int(g): i for i, g in enumerate(ids1)}
+xr = np.full(x1.size, np.nan)
+for rep, ids, x in outs:
+    assert rep["status"] == "OK"
+    xr[[pos[int(g)] for g in ids]] = x
+assert np.linalg.norm(xr - x1) <= 1e-10 * np.linalg.norm(x1)
+print("POISON_OK")
+''' % (root, os.path.join(root, "tests"))
+    env = dict(os.environ, VB_POISON="1")
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert "POISON_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
