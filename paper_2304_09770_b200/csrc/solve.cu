@@ -43,7 +43,10 @@ struct GemvWork {
   int n, r0, r1, pad;
 };
 
-constexpr int GV_WARPS = 4;      // subdomain matrices (several CTAs per SM)
+#ifndef GV_WARPS_CFG
+#define GV_WARPS_CFG 4
+#endif
+constexpr int GV_WARPS = GV_WARPS_CFG;   // subdomain matrices (several CTAs per SM)
 constexpr int GV_WARPS_C = 8;    // the single coarse matrix (one CTA per SM)
 
 // BIG: vectors too long for shared memory (large coarse problems, very large subdomains): x is read through the L2 (it is
