@@ -36,11 +36,12 @@ __device__ __forceinline__ void pdl_prologue() {
 // order; column contributions of one tile row go to distinct tile columns (one warp each), so the
 // accumulation order is fixed: the kernel is deterministic.
 struct GemvWork {
-  const double *M;        // packed tiles
+  const double *M;        // packed tiles; tile (I, J) at M + ptile_off(n, I, J) - moff
   const int64_t *map;     // x gather map (or null: x contiguous at xsrc)
   const double *xsrc;
   double *out;            // partial output (length n)
   int n, r0, r1, pad;
+  int64_t moff;           // offset of the stored slice in the full packed layout (a rank's coarse rows)
 };
 
 #ifndef GV_WARPS_CFG
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
     for (int r = 0; r < 32; ++r) rsum[r] = 0.0;
     const double xI_lane = X(32 * I + lane);
     for (int J = warp; J <= I; J += (PAIR ? 2 : 1) * GV_WARPS) {
-      const double *T = W.M + ptile_off(n, I, J);
+      const double *T = W.M + (ptile_off(n, I, J) - W.moff);
       double t[32];
       if (rows == 32) {
 #pragma unroll
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(GV_WARPS * 32) sym_gemv_kernel(const GemvWork 
       const int J2 = J + GV_WARPS;
       double t2[PAIR ? 32 : 1];
       if (PAIR) {
-        const double *T2 = W.M + ptile_off(n, I, J2 <= I ? J2 : J);
+        const double *T2 = W.M + (ptile_off(n, I, J2 <= I ? J2 : J) - W.moff);
 #pragma unroll
         for (int r = 0; r < 32; ++r) t2[r] = (J2 <= I && r < rows) ? __ldg(T2 + r * 32 + lane) : 0.0;
       }
@@ -1126,7 +1127,8 @@ void prepare_solve(vb_ctx *c) {
   // coarse work list: the tile rows [tlo, thi) of the packed inverse (all of them on one rank)
   const int64_t ntc = (c->Nc + 31) / 32;
   const int64_t tlo = c->nranks > 1 ? c->coarse_tlo : 0, thi = c->nranks > 1 ? c->coarse_thi : ntc;
-  const double *Kc0 = c->nranks > 1 ? c->d_Kcs.p - ptile_row_start(tlo) : c->d_Kcp.p;   // global tile offsets
+  const double *Kc0 = c->nranks > 1 ? c->d_Kcs.p : c->d_Kcp.p;
+  const int64_t Kc_off = c->nranks > 1 ? ptile_row_start(tlo) : 0;   // the slice starts at tile row tlo
   int Pc = (int)std::max<int64_t>(1, std::min<int64_t>(c->P_c, thi - tlo));
   c->w_ucp.alloc(std::max<int64_t>((int64_t)Pc * c->Nc, 1));
   c->w_ucp.zero(s);
@@ -1140,7 +1142,7 @@ void prepare_solve(vb_ctx *c) {
       while (r1 < thi && cum(r1 + 1) - c0 <= tot * (q + 1) / Pc) ++r1;
       if (r1 == r && r < thi) r1 = r + 1;
       if (q == Pc - 1) r1 = thi;
-      wl.push_back(GemvWork{Kc0, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, (int)r, (int)r1, 0});
+      wl.push_back(GemvWork{Kc0, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, (int)r, (int)r1, 0, Kc_off});
       r = r1;
     }
   }
