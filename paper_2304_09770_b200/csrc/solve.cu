@@ -925,7 +925,10 @@ static void collect_times(vb_ctx *c, SolveState *st) {
 
 const char *kernel_time_name(int i) { return (i >= 0 && i < N_CAT) ? kCatNames[i] : ""; }
 
-constexpr int DOT_BLOCKS = 296;
+#ifndef DOT_BLOCKS_CFG
+#define DOT_BLOCKS_CFG 296
+#endif
+constexpr int DOT_BLOCKS = DOT_BLOCKS_CFG;
 
 static SolveState *get_state(vb_ctx *c) {
   if (!c->solve_state) c->solve_state = new SolveState();
