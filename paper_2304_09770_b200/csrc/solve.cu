@@ -407,8 +407,8 @@ __global__ void gather_src_dot_kernel(const int64_t *__restrict__ ptr, const int
 }
 
 // c_i = Phi^_i^T r_i = Phi_i^T D^T r_i (coarse rhs pieces, Phi^ = D Phi, r_i = the dual coordinates of
-// subdomain i gathered from r): PHIT_SPLIT CTAs per subdomain, warp per primal column
-constexpr int PHIT_SPLIT = 4;
+// subdomain i gathered from r): phit_split CTAs per subdomain (4 at 512 subdomains, more when there
+// are few large subdomains), warp per primal column
 __global__ void __launch_bounds__(256) phit_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
                             const int64_t *__restrict__ loc2x, const double *__restrict__ r, double *cpart) {
   pdl_prologue();
@@ -781,6 +781,7 @@ struct SolveState {
   DBuf<GemvWork> w_op, w_loc, w_c;
   DBuf<GemvWork> w_kd;
   int nw_op = 0, nw_loc = 0, nw_c = 0, nw_kd = 0, max_nd = 1;
+  int phit_split = 4;                // CTAs per subdomain of phit_kernel
   bool big_c = false;                // coarse vectors exceed shared memory: BIG GEMV variant
   bool big_op = false, big_loc = false, big_kd = false;   // the same for the subdomain matrices
   size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_ex = 0, sm_kd = 0;
@@ -1005,7 +1006,7 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   run_sub_gemv(st, st->w_loc.p, st->nw_loc, st->sm_loc, st->big_loc, s);
   tick(c, st, 1, false);
   // coarse pieces (C2): [Phi_i^T rD_i per local subdomain | r0_i | r_Pi of the owned entities]
-  launch_after_event(st, phit_kernel, dim3(PHIT_SPLIT, c->N), dim3(256), st->max_nd * sizeof(double), s2, c->d_sub.p, c->d_Phi.p,
+  launch_after_event(st, phit_kernel, dim3(st->phit_split, c->N), dim3(256), st->max_nd * sizeof(double), s2, c->d_sub.p, c->d_Phi.p,
              c->d_loc2x.p, c->w_r.p, st->cbuf.p);
   dev_gather(c->w_r.p, st->cpack.p, (int64_t)st->cpack.n, st->cbuf.p + c->len_Pi, s2);
   const double *pieces = st->cbuf.p;
@@ -1071,6 +1072,7 @@ void prepare_solve(vb_ctx *c) {
     const int P = std::max(4, std::min(32, (2048 + c->N - 1) / std::max(c->N, 1)));
     c->P_op = c->P_loc = c->P_kd = P;
   }
+  st->phit_split = std::max(4, std::min(32, (2048 + c->N - 1) / std::max(c->N, 1)));
   if (getenv("VB_P_OP")) c->P_op = std::max(1, atoi(getenv("VB_P_OP")));
   if (getenv("VB_P_LOC")) c->P_loc = std::max(1, atoi(getenv("VB_P_LOC")));
   cudaStream_t s = c->stream;
@@ -1595,7 +1597,7 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   run_slot_exchange(c, st->XB, st->gbuf.p, st->gbuf.p + c->len_G);          // C1 (cross-rank zG)
   run_entity_sum(c, st->ESB, st->gbuf.p, c->w_gam.p, st->gam2.p);             // ghat = b + sum_m zG^(m)
   if (!c->h_ent.empty())
-    gamma_rhs_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_T.p, c->w_gam.p, NDelta, c->w_r.p);
+    gamma_rhs_kernel<<<c->h_ent.size(), 512, 0, s>>>(c->d_ent.p, c->d_T.p, c->w_gam.p, NDelta, c->w_r.p);
   p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + 220, 0, c->Ng);
   allreduce_sum_fixed(c, c->w_dots.p + 220, 1);
   p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + 220, 1, c->Ng);
@@ -1650,7 +1652,7 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   }
   // ---------------- B8: back to original coordinates and back-substitution
   if (!c->h_ent.empty())
-    gamma_back_kernel<<<c->h_ent.size(), 128, 0, s>>>(c->d_ent.p, c->d_gam_free.p, c->d_T.p, c->w_x.p, NDelta,
+    gamma_back_kernel<<<c->h_ent.size(), 512, 0, s>>>(c->d_ent.p, c->d_gam_free.p, c->d_T.p, c->w_x.p, NDelta,
                                                     c->w_gam.p, x);
   VB_STAGE();
   // u_D = x_D - K_DD^-1 (K_DG u_G): the coupling element by element into w_bD (b_D is spent), the packed
