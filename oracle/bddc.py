@@ -16,11 +16,14 @@ Follows PAPER.md §4 and §6:
   * adaptive coarse space: per-face generalized eigenproblems on deluxe Schur complements
     (SURVEY O-12).
 Everything is in ORIGINAL interface coordinates with T_G = [N_G, C_G^T (C_G C_G^T)^-1]
-(SURVEY A9).  Q_I is handled with an explicit orthonormal basis Z of {q : int q = 0}
-("Z-basis").
+(SURVEY A9).  Q_I is handled with an explicit (sparse) basis Z of {q : int q = 0}
+("Z-basis").  Per subdomain only S_G (dense), the sparse LU of K_DD and the factored
+dual block are kept, so the full-size configs 3 and 5 fit a CPU host (SURVEY O-8).
 """
 import numpy as np
 import scipy.linalg as sla
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
 
 
 def _sym(M):
@@ -32,8 +35,10 @@ class Entity:
 
 
 class BDDC:
-    def __init__(self, gs, scaling="deluxe", constraints=None, adaptive_tau=None, svd_tol=1e-10):
+    def __init__(self, gs, scaling="deluxe", constraints=None, adaptive_tau=None, svd_tol=1e-10,
+                 keep_pencils=False):
         self.gs = gs
+        self.keep_pencils = keep_pencils      # tests: keep each face's (N_F, S~^(m), S_FD^(m), A, B)
         prob = gs.prob
         self.prob = prob
         mesh, dofs, k = prob.mesh, gs.dofs, prob.k
@@ -102,13 +107,17 @@ class BDDC:
 
     # ------------------------------------------------------------------ subdomain operators
     def _subdomain_matrices(self):
+        """K^(i) = sum of element saddle matrices (O-8), stored sparse; K_DD^(i) on (u_I, Q_I) is
+        factored by a sparse LU (library solve); S_G^(i) = K_GG - K_GD K_DD^-1 K_DG
+        (Eq.(firstSchur)) is the only dense per-subdomain matrix kept (memory-lean:
+        configs 3 and 5 at full size fit a CPU host, SURVEY O-8)."""
         gs, dofs, el = self.gs, self.gs.dofs, self.gs.el
         nu = self.prob.nu_cell
         for i, S in enumerate(self.sub):
             lv = {int(d): j for j, d in enumerate(np.concatenate([S.I, S.G]))}
             lp = {int(d): j for j, d in enumerate(S.P)}
             nI, nGl, nP = len(S.I), len(S.G), len(S.P)
-            A = np.zeros((nI + nGl, nI + nGl)); B = np.zeros((nP, nI + nGl))
+            ar, ac, av, br, bc, bv = [], [], [], [], [], []
             c = np.zeros(nP); m = np.zeros(nP)
             for K in self.sub_cells[i]:
                 op = el.op(K)
@@ -117,28 +126,37 @@ class BDDC:
                 keep = fr >= 0
                 li = np.array([lv[int(x)] for x in fr[keep]])
                 pi = np.array([lp[int(x)] for x in ip])
-                A[np.ix_(li, li)] += nu[K] * op.A[np.ix_(keep, keep)]
-                B[np.ix_(pi, li)] += op.B[:, keep]
+                ar.append(np.repeat(li, li.size)); ac.append(np.tile(li, li.size))
+                av.append((nu[K] * op.A[np.ix_(keep, keep)]).ravel())
+                br.append(np.repeat(pi, li.size)); bc.append(np.tile(li, pi.size))
+                bv.append(op.B[:, keep].ravel())
                 # DOFs of the constant 1 (D_Q of q=1) and m = int psi_j
                 c[pi] = op.Gram(self.k - 1, 0)[:, 0] / op.g.vol
                 m[pi[0]] = op.g.vol
-            S.A, S.B, S.c, S.m = A, B, c, m
+            n = nI + nGl
+            A = sp.csr_matrix((np.concatenate(av), (np.concatenate(ar), np.concatenate(ac))), shape=(n, n))
+            B = sp.csr_matrix((np.concatenate(bv), (np.concatenate(br), np.concatenate(bc))), shape=(nP, n))
+            S.c, S.m = c, m
             S.vol = float(m.sum())
             S.nI, S.nGl = nI, nGl
-            # Q_I basis: orthonormal basis of {q : m^T q = 0}
-            S.Z = sla.null_space(m[None, :])
+            # Q_I basis: columns e_j - (m_j / m_j0) e_j0, j != j0 (m^T z = 0; sparse)
+            j0 = int(np.flatnonzero(m)[0])
+            oth = np.delete(np.arange(nP), j0)
+            S.Z = sp.csr_matrix((np.concatenate([np.ones(nP - 1), -m[oth] / m[j0]]),
+                                 (np.concatenate([oth, np.full(nP - 1, j0)]),
+                                  np.concatenate([np.arange(nP - 1)] * 2))), shape=(nP, nP - 1))
             AII, AIG, AGG = A[:nI, :nI], A[:nI, nI:], A[nI:, nI:]
             BI, BG = B[:, :nI], B[:, nI:]
-            ZB = S.Z.T @ BI
-            nz = S.Z.shape[1]
-            KDD = np.block([[AII, ZB.T], [ZB, np.zeros((nz, nz))]])
-            KDG = np.vstack([AIG, S.Z.T @ BG])
-            S.KDD, S.KDG = KDD, KDG
-            S.KDD_lu = sla.lu_factor(KDD)
-            X = sla.lu_solve(S.KDD_lu, KDG)
-            S.SG = _sym(AGG - KDG.T @ X)                         # Eq.(firstSchur)
-            S.b0 = S.c @ BG                                      # flux row B_0G^(i)
-            S.b0_int = S.c @ BI                                  # must vanish (interior DOFs)
+            ZB = (S.Z.T @ BI).tocsr()
+            KDD = sp.bmat([[AII, ZB.T], [ZB, None]]).tocsc()
+            KDG = sp.vstack([AIG, S.Z.T @ BG]).tocsc()
+            S.KDG = KDG
+            S.KDD_lu = spla.splu(KDD)
+            X = S.KDD_lu.solve(KDG.toarray())
+            S.SG = _sym(AGG.toarray() - KDG.T @ X)               # Eq.(firstSchur)
+            del X
+            S.b0 = BG.T @ S.c                                    # flux row B_0G^(i)
+            S.b0_int = BI.T @ S.c                                # must vanish (interior DOFs)
 
     # ------------------------------------------------------------------ primal constraints
     def _entity_constraints(self, E):
@@ -231,6 +249,8 @@ class BDDC:
             self._local_transform()
             self._deluxe()
         self._coarse()
+        for S in self.sub:                  # transformed blocks are factor-time only (memory-lean)
+            S.T = S.ST = S.SDD = S.SDP = S.SPP = None
 
     def _local_transform(self):
         """S_T = T^T S_G T, S_DD, Phi_D = -S_DD^-1 S_DP, S_c = S_PP + S_PD Phi (O-10)."""
@@ -368,7 +388,7 @@ class BDDC:
             gp = gs.rhs_p[S.P]
             bD = np.concatenate([bI, S.Z.T @ gp])
             self._bD.append(bD)
-            g[S.Gpos] -= S.KDG.T @ sla.lu_solve(S.KDD_lu, bD)
+            g[S.Gpos] -= S.KDG.T @ S.KDD_lu.solve(bD)
             g0[i] = S.c @ gp
         return np.concatenate([g, g0])
 
@@ -379,7 +399,7 @@ class BDDC:
         uG, p0 = x[:self.nG], x[self.nG:]
         u[self.gamma] = uG
         for i, S in enumerate(self.sub):
-            y = sla.lu_solve(S.KDD_lu, self._bD[i] - S.KDG @ uG[S.Gpos])
+            y = S.KDD_lu.solve(self._bD[i] - S.KDG @ uG[S.Gpos])
             u[S.I] = y[:S.nI]
             p[S.P] = S.Z @ y[S.nI:] + p0[i] * S.c
         mean = (gs.pmass @ p) / gs.pmass[::dofs.np_].sum()
@@ -398,6 +418,7 @@ class BDDC:
         self.adaptive_spectra = {}
         self.adaptive_margin = np.inf
         self.adaptive_count = 0
+        self.adaptive_pencils = {}
         for e, E in enumerate(self.ents):
             if E.kind != "face" or E.nd == 0:
                 continue
@@ -418,6 +439,8 @@ class BDDC:
             Aop = par(St[0], St[1]); Bop = par(Sf[0], Sf[1])
             lam, Psi = sla.eigh(Aop, Bop)
             self.adaptive_spectra[e] = lam
+            if self.keep_pencils:
+                self.adaptive_pencils[e] = dict(N=E.N.copy(), St=St, Sf=Sf, A=Aop, B=Bop)
             sel = lam < 1.0 / tau
             self.adaptive_margin = min(self.adaptive_margin, float(np.min(np.abs(lam - 1.0 / tau))))
             if np.any(sel):

@@ -187,6 +187,21 @@ class Context:
         self.n_vel, self.n_p = nv.value, npr.value
         self.n_free = self.n_vel + self.n_p
 
+    def _dev(self, t, name):
+        """Device vector argument: CUDA, float64, contiguous, exactly this rank's n_free entries."""
+        import torch
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()
+                and t.numel() == self.n_free):
+            raise ValueError("%s must be a contiguous float64 CUDA tensor of %d entries" % (name, self.n_free))
+        return ctypes.c_void_p(t.data_ptr())
+
+    def _host(self, a, name):
+        """Host vector argument: float64 numpy array, C-contiguous, exactly n_free entries."""
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+                and a.size == self.n_free):
+            raise ValueError("%s must be a C-contiguous float64 numpy array of %d entries" % (name, self.n_free))
+        return _ptr(a, ctypes.c_double)
+
     def _check(self, st):
         if st != VB_OK:
             raise VBError(st, _vb_last_error(self._h).decode())
@@ -202,12 +217,12 @@ class Context:
             p = VBProblem(1, cen.shape[0], _ptr(cen, ctypes.c_double), problem["delta"], problem["omega"], problem["beta"])
         else:
             p = VBProblem(0, 0, None, 0.0, 0.0, 0.0)
-        self._check(_vb_build_rhs(self._h, ctypes.byref(p), ctypes.c_void_p(out.data_ptr())))
+        self._check(_vb_build_rhs(self._h, ctypes.byref(p), self._dev(out, "out")))
         return out
 
     def pcg_solve(self, rhs, x, rtol=1e-10, maxit=2000, raise_on_error=True):
         rep = VBReport()
-        st = _vb_pcg_solve(self._h, ctypes.c_void_p(rhs.data_ptr()), ctypes.c_void_p(x.data_ptr()), float(rtol),
+        st = _vb_pcg_solve(self._h, self._dev(rhs, "rhs"), self._dev(x, "x"), float(rtol),
                            int(maxit), ctypes.byref(rep))
         d = rep.as_dict()
         d["status"] = STATUS[st]
@@ -217,12 +232,12 @@ class Context:
 
     def pcg_solve_host(self, rhs_host, x_host, rtol=1e-10, maxit=2000):
         rep = VBReport()
-        self._check(_vb_pcg_solve_host(self._h, _ptr(rhs_host, ctypes.c_double), _ptr(x_host, ctypes.c_double),
+        self._check(_vb_pcg_solve_host(self._h, self._host(rhs_host, "rhs_host"), self._host(x_host, "x_host"),
                                        float(rtol), int(maxit), ctypes.byref(rep)))
         return rep.as_dict()
 
     def apply_operator(self, x, y):
-        self._check(_vb_apply_operator(self._h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr())))
+        self._check(_vb_apply_operator(self._h, self._dev(x, "x"), self._dev(y, "y")))
         return y
 
     def interface_dofs(self):

@@ -456,7 +456,8 @@ vb_status vb_pcg_solve_host(vb_ctx *c, const double *rhs_host, double *x_host, d
   if (!c || !rhs_host || !x_host) return VB_EINVAL;
   if (c->state < 2) return fail(c, Error{VB_ESTATE, "vb_pcg_solve_host before vb_factor"});
   ABI_GUARD(c, {
-    const int64_t n = c->n_free_vel + c->npres;
+    // this rank's owned free DOFs (vb_num_free_dofs): the caller's host buffers hold only those
+    const int64_t n = (int64_t)c->owned_free.size();
     if (c->w_hostio.n < (size_t)(2 * n)) c->w_hostio.alloc(2 * n);
     VB_CUDA(cudaMemcpyAsync(c->w_hostio.p, rhs_host, n * 8, cudaMemcpyHostToDevice, c->stream));
     vb_status st = vb_pcg_solve(c, c->w_hostio.p, c->w_hostio.p + n, rtol, maxit, rep);

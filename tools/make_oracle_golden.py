@@ -3,10 +3,11 @@
 Calls ONLY oracle/ (and the seeded input recipe in synthetic/); nothing here touches the CUDA
 library.  The full-size oracle solves take minutes to an hour on a CPU, far too long for the GPU
 test run, so the GPU parity tests at full size compare against these stored oracle values:
-iterations, Lanczos kappa, primal counts, solution norms and a seeded sample of 20000 solution
-entries (SURVEY §8(c) gates; sampled outputs at full size).
+the WHOLE solution vector (free DOFs in the exported order; gated per block at relative L2
+<= 1e-8), iterations, Lanczos kappa, primal counts, norms and a seeded sample of 20000 rhs
+entries (SURVEY §8(c) gates).
 
-  python tools/make_oracle_golden.py c2 c3 c4
+  python tools/make_oracle_golden.py c2 c3 c4 c5
 """
 import json
 import os
@@ -46,7 +47,7 @@ def make(name, outdir=None):
                 seconds=time.time() - t0,
                 source="tools/make_oracle_golden.py (oracle/ only), rtol 1e-10, seed 20230419")
     rhs = np.concatenate([gs.rhs_u, gs.rhs_p])
-    np.savez_compressed(out, idx=idx, x=x[idx], rhs=rhs[idx], meta=json.dumps(meta))
+    np.savez_compressed(out, idx=idx, x_full=x, rhs=rhs[idx], meta=json.dumps(meta))
     print(name, json.dumps(meta), flush=True)
 
 
