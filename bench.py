@@ -36,23 +36,23 @@ def _peaks():
 
 
 def _ncu_traffic(role_key="S_T packed GEMV"):
-    """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu --set full
-    capture (the latest profiles/r*_ncu_full_*.json), or None."""
+    """DRAM bytes (read + write) per launch of the dominant kernel from the newest committed
+    ncu --set full capture that contains it (profiles/r*_ncu_full_*.json entries carry a "role"),
+    or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_*.json")))
-    if not files:
-        return None, None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_*.json")), reverse=True)
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    try:
-        for d in json.load(open(files[-1])):
-            if role_key in d.get("role", ""):
-                tot = 0.0
-                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                    v, u = d[k].split()
-                    tot += float(v) * scale[u]
-                return tot, os.path.basename(files[-1])
-    except Exception:
-        pass
+    for path in files:
+        try:
+            for d in json.load(open(path)):
+                if role_key in d.get("role", ""):
+                    tot = 0.0
+                    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                        v, u = d[k].split()
+                        tot += float(v) * scale[u]
+                    return tot, os.path.basename(path)
+        except Exception:
+            continue
     return None, None
 
 
@@ -128,10 +128,24 @@ def run_oracle_sample(steps, warmup):
         its.append(rep["iterations"])
     t = float(np.mean(ts))
     return dict(value=ndofs * float(np.mean(its)) / t, t=t, it=float(np.mean(its)), ndofs=ndofs,
-                cores=os.cpu_count(),
-                sample="oracle BDDC-PCG solve (B0+PCG+B8, setup excluded) on config 2: 16^3 cells, "
-                       "4^3 subdomains of 4^3 cells (same subdomain size/k/constraints/rtol as the "
-                       "config-5 1-GPU slice, 1/8 of its subdomains), mean of %d solves" % steps)
+                cores=_blas_threads(),
+                sample="c5 sampled as c2: the oracle BDDC-PCG solve (B0+PCG+B8, setup excluded) on 64 of "
+                       "c5's 512 subdomains (16^3 cells, 4^3 subdomains of 4^3 cells: the same subdomain "
+                       "size, k, constraints and rtol; the oracle's per-iteration work is per subdomain, so "
+                       "DOF*it/s of the sample stands for c5; the oracle's c5 setup alone takes ~30 min), "
+                       "mean of %d solves" % steps)
+
+
+def _blas_threads():
+    """Threads the oracle's BLAS actually uses (threadpoolctl), else the host's core count."""
+    try:
+        from threadpoolctl import threadpool_info
+        n = [d.get("num_threads") for d in threadpool_info() if d.get("user_api") == "blas"]
+        if n and n[0]:
+            return int(n[0])
+    except Exception:
+        pass
+    return os.cpu_count()
 
 
 def reference_arm(args):
@@ -143,7 +157,8 @@ def reference_arm(args):
     line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["t"] * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c2 sample of c5 (see cpu_baseline.sample)", "iterations": r["it"],
+            "config": {"workload": "c5, sampled as c2 (64 of its 512 subdomains; see cpu_baseline.sample)",
+                       "iterations": r["it"],
                        "n_dofs": r["ndofs"]},
             "cpu_baseline": cpu,
             "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -292,8 +307,9 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "c5: %dx%dx%d hex cells, k=2, %d subdomains of 4^3 cells (32^3 cells per GPU)"
-                               % (tuple(prob.mesh.dims) + (int(prob.cell_subdomain.max()) + 1,)),
+        "config": {"workload": "%s: %dx%dx%d hex cells, k=%d, %d subdomains%s"
+                               % ((args.config,) + tuple(prob.mesh.dims) + (prob.k, int(prob.cell_subdomain.max()) + 1,
+                                  " of 4^3 cells (32^3 cells per GPU)" if args.config == "c5" else "")),
                    "n_dofs": ndofs, "iterations": it, "kappa": rep["kappa"], "rel_residual": rep["rel_residual"],
                    "n_primal": st["n_primal"], "n_coarse": st["n_coarse"], "rtol": 1e-10,
                    "t_setup_s": t_setup, "t_factor_s": t_factor,

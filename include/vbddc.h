@@ -82,10 +82,16 @@ typedef struct {
   int32_t iterations, converged;
   double r0_norm, r_final_norm, rel_residual;   /* interface residual ||r||_2        */
   double lambda_min, lambda_max, kappa;         /* Lanczos from the CG coefficients  */
-  double true_rel_residual;                     /* -1: not computed by vb_pcg_solve (one extra
-                                                   element pass); vb_apply_operator gives b - K x */
+  double true_rel_residual;                     /* ||b - K x||_2 / ||b||_2 of the full saddle
+                                                   system through the element-by-element K7
+                                                    when vb_set_option(ctx,
+                                                   "true_residual", 1); else -1 (one extra pass) */
   double t_setup_s, t_factor_s, t_solve_s;
-  double bytes_per_iter_model, flux_violation_max;
+  double bytes_per_iter_model;
+  double flux_violation_max;                    /* max_i |b_0^(i) x_Gamma^(i)| of the final
+                                                   interface iterate (benign space, Assumption
+                                                   ass1 P:526-528); meaningful on
+                                                   VB_EBREAKDOWN                               */
   int32_t n_primal, n_coarse;
   int64_t n_dofs_paper;                         /* nDofs as counted in T2-T4                   */
   int32_t n_adaptive;                           /* primal rows added by the face GEVPs */
@@ -144,9 +150,26 @@ vb_status vb_build_rhs(vb_ctx *ctx, const vb_problem *prob, double *rhs_dev);
  * velocity DOFs whose lowest sharing subdomain is on this rank, then the pressure DOFs of its
  * cells; for one rank, all free DOFs in global order); x gets the full solution (interior
  * back-substitution, pressure with zero global mean).  maxit <= 0 means 2000.
+ * The pressure rows of rhs must be flux-compatible, sum_i g0_i = 0 (integral of the pressure rhs
+ * against constants): |sum_i g0_i| > 1e-8 sum_i |g0_i| returns VB_EINVAL; within that
+ * bound the rounding is removed (reading A30).  VB_EBREAKDOWN (p^T S p <= 0 or
+ * r^T z <= 0) and VB_ENOTCONV (maxit) leave the last iterate in x and fill the report.
  * Collective: every rank calls it with the same rtol/maxit. */
 vb_status vb_pcg_solve(vb_ctx *ctx, const double *rhs_dev, double *x_dev, double rtol,
                        int32_t maxit, vb_report *rep);
+
+/* Context options (host, any time after vb_setup):
+ *   "true_residual" (0/1, default 0): vb_pcg_solve also fills vb_report.true_rel_residual
+ *                   (one element-by-element K7 pass and two norms after the solve).
+ * VB_EINVAL on an unknown name. */
+vb_status vb_set_option(vb_ctx *ctx, const char *name, double value);
+
+/* Self-test of the NCCL transport on ONE GPU (1-rank communicator): a grouped send/recv to self
+ * and an all-gather, eagerly and captured inside a CUDA-graph conditional WHILE body (the way
+ * the PCG iteration graph captures them).  result[4] = {eager ok, graph ok, graph iterations,
+ * max abs error}; VB_ENCCL if NCCL is not loaded; capture failures are reported in result[1] = 0
+ * with the message in vb_last_error(NULL), not as an error status. */
+vb_status vb_debug_nccl_selftest(int32_t device, double *result);
 
 /* Same, with HOST rhs/x buffers: the host<->device copies are part of the call (e2e timing). */
 vb_status vb_pcg_solve_host(vb_ctx *ctx, const double *rhs_host, double *x_host, double rtol,

@@ -242,15 +242,16 @@ class BDDC:
         self.NPi = off
 
     def _factor(self, tau):
+        adaptive = bool(tau and tau > 0)
+        self._keep_ST = adaptive            # the face pencils need S_T (memory-lean otherwise)
         self._local_transform()
         self._deluxe()
-        if tau and tau > 0:
+        if adaptive:
             self._adaptive(tau)
+            self._keep_ST = False
             self._local_transform()
             self._deluxe()
         self._coarse()
-        for S in self.sub:                  # transformed blocks are factor-time only (memory-lean)
-            S.T = S.ST = S.SDD = S.SDP = S.SPP = None
 
     def _local_transform(self):
         """S_T = T^T S_G T, S_DD, Phi_D = -S_DD^-1 S_DP, S_c = S_PP + S_PD Phi (O-10)."""
@@ -285,6 +286,9 @@ class BDDC:
             S.SDD_chol = sla.cho_factor(S.SDD)
             S.Phi = -sla.cho_solve(S.SDD_chol, S.SDP)
             S.Sc = _sym(S.SPP + S.SDP.T @ S.Phi)
+            S.T = S.SDD = S.SDP = S.SPP = None          # factor-time only (memory-lean)
+            if not self._keep_ST:
+                S.ST = None
 
     def _deluxe(self):
         """D_G^(m) = (sum_m' S_GD^(m'))^-1 S_GD^(m) or 1/card(I_x) (Eq.(pseudoinv))."""

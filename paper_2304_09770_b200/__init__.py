@@ -96,6 +96,8 @@ _vb_destroy = _sig("vb_destroy", ctypes.c_int, [_p])
 _vb_nccl_unique_id = _sig("vb_nccl_unique_id", ctypes.c_int, [_p])
 _vb_debug_iop = _sig("vb_debug_interface_op", ctypes.c_int, [_p, ctypes.c_int32, _dp, _dp])
 _vb_interface_dofs = _sig("vb_interface_dofs", ctypes.c_int, [_p, _i64p, _i64p])
+_vb_set_option = _sig("vb_set_option", ctypes.c_int, [_p, ctypes.c_char_p, ctypes.c_double])
+_vb_nccl_selftest = _sig("vb_debug_nccl_selftest", ctypes.c_int, [ctypes.c_int32, _dp])
 _vb_debug_gemm = _sig("vb_debug_gemm", ctypes.c_int,
                      [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _p, ctypes.c_int32,
                       ctypes.c_int32, _p, ctypes.c_int32, ctypes.c_int32, _p, ctypes.c_double, _p,
@@ -106,7 +108,7 @@ EXPORTED = ["vb_plan_exchange", "vb_nccl_unique_id", "vb_loopback_world_create",
             "vb_pcg_solve", "vb_pcg_solve_host", "vb_apply_operator", "vb_debug_interface_op", "vb_debug_gemm",
             "vb_interface_dofs", "vb_num_free_dofs", "vb_dof_layout",
             "vb_cell_local_dofs", "vb_get_element_matrices", "vb_stats", "vb_kernel_times",
-            "vb_kernel_time_name", "vb_last_error", "vb_destroy"]
+            "vb_kernel_time_name", "vb_last_error", "vb_destroy", "vb_set_option", "vb_debug_nccl_selftest"]
 
 
 class VBError(RuntimeError):
@@ -208,6 +210,10 @@ class Context:
 
     def factor(self):
         self._check(_vb_factor(self._h))
+
+    def set_option(self, name, value):
+        """vb_set_option: "true_residual" (0/1) -> vb_report.true_rel_residual through K7."""
+        self._check(_vb_set_option(self._h, name.encode(), float(value)))
 
     def build_rhs(self, problem, out):
         """problem: dict(kind='manufactured'|'sinker', centres, delta, omega, beta); out: cuda float64 tensor."""
@@ -313,6 +319,16 @@ def nccl_unique_id():
     if st != VB_OK:
         raise VBError(st, _vb_last_error(None).decode())
     return bytes(buf.raw)
+
+
+def nccl_selftest(device=0):
+    """vb_debug_nccl_selftest on one GPU: dict(eager_ok, graph_ok, graph_iterations, max_err, message)."""
+    out = np.zeros(4)
+    st = _vb_nccl_selftest(int(device), _ptr(out, ctypes.c_double))
+    if st != VB_OK:
+        raise VBError(st, _vb_last_error(None).decode())
+    return dict(eager_ok=bool(out[0]), graph_ok=bool(out[1]), graph_iterations=int(out[2]), max_err=float(out[3]),
+                message=_vb_last_error(None).decode() if not out[1] else "")
 
 
 def debug_gemm(A, B, C, alpha=1.0, beta=0.0, d=None, transA=False, transB=False, kz=None):

@@ -307,6 +307,24 @@ static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, i
 // ------------------------------------------------------------------ ABI
 extern "C" {
 
+vb_status vb_debug_nccl_selftest(int32_t device, double *result) {
+  if (!result) return VB_EINVAL;
+  ABI_GUARD(nullptr, {
+    std::string msg;
+    vb::nccl_selftest(device, result, msg);
+    if (!msg.empty()) g_last_error = msg;
+  })
+}
+
+vb_status vb_set_option(vb_ctx *c, const char *name, double value) {
+  if (!c || !name) return VB_EINVAL;
+  if (!strcmp(name, "true_residual")) {
+    c->opt_true_residual = value != 0.0;
+    return VB_OK;
+  }
+  return fail(c, Error{VB_EINVAL, std::string("unknown option ") + name});
+}
+
 vb_status vb_nccl_unique_id(void *out128) {
   if (!out128) return VB_EINVAL;
   ABI_GUARD(nullptr, { vb::nccl_unique_id(out128); })

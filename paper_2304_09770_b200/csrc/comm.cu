@@ -3,6 +3,9 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
+#include <cmath>
+#include <memory>
+#include <algorithm>
 #include <mutex>
 #include <string>
 #include "comm.h"
@@ -28,6 +31,8 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommCount)(ncclComm_t, int *) = nullptr;
+  ncclResult_t (*GetVersion)(int *) = nullptr;
 };
 
 static NcclApi &nccl() {
@@ -49,6 +54,8 @@ static NcclApi &nccl() {
     api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
     api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.CommCount = (decltype(api.CommCount))dlsym(h, "ncclCommCount");
+    api.GetVersion = (decltype(api.GetVersion))dlsym(h, "ncclGetVersion");
   });
   VB_REQUIRE(api.h && api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.AllGather &&
                  api.GroupStart && api.GroupEnd,
@@ -102,12 +109,112 @@ Comm *make_nccl_comm(int rank, int nranks, const void *id128, int device) {
   NcclComm *c = new NcclComm();
   c->rank = rank;
   c->nranks = nranks;
+  // the PCG iteration graph captures the exchanges inside a conditional WHILE body, which takes
+  // kernel/memcpy nodes only: keep NCCL from adding its graph-mixing event nodes (read at init;
+  // a value set by the user wins)
+  setenv("NCCL_GRAPH_MIXING_SUPPORT", "0", 0);
   ncclResult_t r = a.CommInitRank(&c->comm, nranks, id, rank);
   if (r != 0) {
     delete c;
     throw Error{VB_ENCCL, std::string("ncclCommInitRank: ") + (a.GetErrorString ? a.GetErrorString(r) : "?")};
   }
+  int cnt = -1, ver = 0;
+  if (a.CommCount) a.CommCount(c->comm, &cnt);
+  if (a.GetVersion) a.GetVersion(&ver);
+  fprintf(stderr, "[vb] NCCL communicator: rank %d nranks %d (ncclCommCount %d) device %d, NCCL %d\n", rank, nranks,
+          cnt, device, ver);
+  VB_REQUIRE(cnt < 0 || cnt == nranks, VB_ENCCL, "NCCL communicator size differs from nranks");
   return c;
+}
+
+// ------------------------------------------------------------------ NCCL self-test (one GPU)
+__global__ void selftest_step_kernel(double *a, int n, int *counter) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] += 1.0;
+  if (threadIdx.x == 0) ++*counter;
+}
+__global__ void selftest_cond_kernel(const int *counter, int stop, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, *counter < stop ? 1u : 0u);
+}
+
+void nccl_selftest(int device, double *result, std::string &msg) {
+  NcclApi &a = nccl();
+  VB_CUDA(cudaSetDevice(device));
+  result[0] = result[1] = result[2] = 0.0;
+  result[3] = INFINITY;
+  ncclUniqueId id;
+  VB_NCCL(a.GetUniqueId(&id));
+  NcclComm *cm = (NcclComm *)make_nccl_comm(0, 1, &id, device);
+  std::unique_ptr<NcclComm> guard(cm);
+  const int n = 4096;
+  DBuf<double> buf;
+  buf.alloc(3 * n);
+  DBuf<int> counter;
+  counter.alloc(1);
+  cudaStream_t s;
+  VB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  std::vector<double> h(3 * n);
+  for (int i = 0; i < n; ++i) h[i] = 0.5 * i;
+  VB_CUDA(cudaMemcpyAsync(buf.p, h.data(), n * 8, cudaMemcpyHostToDevice, s));
+  counter.zero(s);
+  const std::vector<PeerXfer> self{PeerXfer{0, 0, n, 0, n}};
+  auto step = [&]() {   // a += 1; b <- a (send/recv to self); g <- allgather(a)
+    selftest_step_kernel<<<1, 256, 0, s>>>(buf.p, n, counter.p);
+    cm->exchange(self, buf.p, buf.p + n, s);
+    cm->allgather(buf.p, buf.p + 2 * n, n, s);
+  };
+  auto check = [&](int steps) {
+    VB_CUDA(cudaMemcpyAsync(h.data(), buf.p, 3 * n * 8, cudaMemcpyDeviceToHost, s));
+    VB_CUDA(cudaStreamSynchronize(s));
+    double err = 0;
+    for (int i = 0; i < n; ++i)
+      err = std::max({err, fabs(h[i] - (0.5 * i + steps)), fabs(h[n + i] - h[i]), fabs(h[2 * n + i] - h[i])});
+    return err;
+  };
+  step();
+  double e1 = check(1);
+  result[0] = e1 == 0.0;
+  // the same step 3 times inside a conditional WHILE body (captured)
+  cudaGraph_t g;
+  VB_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle hw;
+  VB_CUDA(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams wp = {};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  VB_CUDA(cudaGraphAddNode(&wnode, g, nullptr, 0, &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  cudaGraphExec_t ge = nullptr;
+  try {
+    VB_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    try {
+      step();
+      selftest_cond_kernel<<<1, 1, 0, s>>>(counter.p, 4, hw);
+    } catch (...) {
+      cudaGraph_t dummy;
+      cudaStreamEndCapture(s, &dummy);
+      throw;
+    }
+    VB_CUDA(cudaStreamEndCapture(s, &body));
+    VB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    VB_CUDA(cudaGraphLaunch(ge, s));
+    double e2 = check(4);
+    int cnt = 0;
+    VB_CUDA(cudaMemcpy(&cnt, counter.p, sizeof(int), cudaMemcpyDeviceToHost));
+    result[1] = (e2 == 0.0 && cnt == 4) ? 1.0 : 0.0;
+    result[2] = cnt - 1;
+    result[3] = std::max(e1, e2);
+  } catch (const Error &e) {
+    (void)cudaGetLastError();
+    msg = "NCCL capture in a conditional graph body failed: " + e.msg;
+    result[3] = e1;
+  }
+  if (ge) cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
 }
 
 // ------------------------------------------------------------------ loopback (threads, one GPU)

@@ -7,6 +7,7 @@
 //     path run against the oracle on a single GPU; no kernel ever waits on another rank).
 #pragma once
 #include <cstdint>
+#include <string>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -34,5 +35,7 @@ Comm *make_loopback_comm(void *world, int rank);
 void *loopback_world_create(int nranks);
 void loopback_world_destroy(void *world);
 int nccl_unique_id(void *out128);   // 0 on success
+// vb_debug_nccl_selftest: result[4] = {eager ok, graph ok, graph iterations, max abs error}
+void nccl_selftest(int device, double *result, std::string &msg);
 
 }  // namespace vb

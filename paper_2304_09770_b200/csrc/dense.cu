@@ -313,7 +313,23 @@ void gemm_grouped(GemmPlan &plan, int launch, cudaStream_t s) { plan.run(launch,
 // ------------------------------------------------------------------ partial LDL^T
 // Phase 1 (blockIdx.x == 0 launch): factor the nb x nb diagonal block in place.
 // Phase 2 (separate launch): panel rows below read the factored block (no read/write race).
-__global__ void ldl_panel_kernel(const MatDesc *__restrict__ mats, int j0, int *info, int phase) {
+// max |diag A| of each matrix before the factorisation (scale of the relative pivot test)
+__global__ void diag_absmax_kernel(const MatDesc *__restrict__ mats, double *scale) {
+  const MatDesc M = mats[blockIdx.x];
+  __shared__ double red[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < M.n; i += blockDim.x) v = fmax(v, fabs(M.A[(int64_t)i * (M.ld + 1)]));
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    scale[blockIdx.x] = fmax(red[0], v);
+  }
+}
+
+__global__ void ldl_panel_kernel(const MatDesc *__restrict__ mats, int j0, int *info, int phase,
+                                 const double *__restrict__ scale) {
   const MatDesc M = mats[blockIdx.y];
   if (j0 >= M.m) return;
   const int nb = min(32, M.m - j0);
@@ -360,9 +376,12 @@ __global__ void ldl_panel_kernel(const MatDesc *__restrict__ mats, int j0, int *
       double d = L11[j][j];
       if (lane == 0) {
         dd[j] = d;
-        if (!(fabs(d) > 1e-300) || !isfinite(d)) {
-          if (info && blockIdx.x == 0) atomicCAS(&info[blockIdx.y], 0, 1 + j0 + j);
+        bool bad = !(fabs(d) > 1e-300) || !isfinite(d);
+        if (M.npos >= 0) {
+          const double tol = kPivRel * scale[blockIdx.y];
+          bad = bad || (j0 + j < M.npos ? !(d > tol) : !(d < -tol));
         }
+        if (bad && info && blockIdx.x == 0) atomicCAS(&info[blockIdx.y], 0, 1 + j0 + j);
       }
       __syncwarp();
       if (lane > j && lane < nb) L11[lane][j] /= d;
@@ -428,13 +447,17 @@ void ldl_partial_batched(const std::vector<MatDesc> &mats, int *info_dev, cudaSt
     }
   }
   plan.upload(s);
+  DBuf<double> dscale;
+  dscale.alloc(mats.size());
+  diag_absmax_kernel<<<mats.size(), 256, 0, s>>>(dm.p, dscale.p);
+  VB_CHECK_LAUNCH();
   int step = 0, wide = 0;
   for (int J0 = 0; J0 < maxm; J0 += LDL_NB, ++wide) {
     for (int j0 = J0; j0 < std::min(J0 + LDL_NB, maxm); j0 += 32, ++step) {
-      ldl_panel_kernel<<<dim3(1, mats.size()), 128, 0, s>>>(dm.p, j0, info_dev, 0);
+      ldl_panel_kernel<<<dim3(1, mats.size()), 128, 0, s>>>(dm.p, j0, info_dev, 0, dscale.p);
       VB_CHECK_LAUNCH();
       dim3 grid((maxn - j0 + 31) / 32, mats.size());
-      ldl_panel_kernel<<<grid, 32, 0, s>>>(dm.p, j0, info_dev, 1);
+      ldl_panel_kernel<<<grid, 32, 0, s>>>(dm.p, j0, info_dev, 1, dscale.p);
       VB_CHECK_LAUNCH();
       plan.run(intra_launch[step], s);
     }

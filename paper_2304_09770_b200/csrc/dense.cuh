@@ -8,7 +8,13 @@ namespace vb {
 struct MatDesc {      // column-major square matrix
   double *A;
   int n, ld, m;       // m = number of leading columns to eliminate
+  // pivot test (SURVEY §8(b) VB_ESINGULAR): npos < 0 -> only |d| > 1e-300 and finite (blocks that
+  // may be semidefinite); else pivots of columns < npos must be > kPivRel * max|diag A| and those
+  // of columns >= npos < -kPivRel * max|diag A| (velocity-first saddle LDL^T: A_II SPD, the
+  // pressure Schur complement negative definite, reading A5)
+  int npos = -1;
 };
+constexpr double kPivRel = 1e-13;
 
 // A sequence of grouped-GEMM launches planned on the host and uploaded once.  Within a launch the
 // tiles are grouped by transpose class (op(A), op(B)) so each class runs the kernel specialised for

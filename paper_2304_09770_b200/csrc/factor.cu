@@ -342,14 +342,18 @@ __global__ void coarse_assemble_kernel2(const int *__restrict__ color_subs, cons
 // ------------------------------------------------------------------ host orchestration
 static void sync(vb_ctx *c) { VB_CUDA(cudaStreamSynchronize(c->stream)); }
 
-static void check_info(vb_ctx *c, int nmat, const char *what, const std::vector<int> *names = nullptr) {
+// pivot failures of a batched LDL^T (ldl_panel_kernel: zero, non-finite, or of the wrong sign /
+// below kPivRel * max|diag| where MatDesc::npos asks for it), named by subdomain / entity id
+static void check_info(vb_ctx *c, int nmat, const char *what, const std::vector<int> *names = nullptr,
+                       const char *kind = "matrix") {
   std::vector<int> info(nmat);
   VB_CUDA(cudaMemcpyAsync(info.data(), c->d_info.p, nmat * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   for (int b = 0; b < nmat; ++b)
     if (info[b])
-      throw Error{VB_ESINGULAR, std::string(what) + ": zero pivot at column " + std::to_string(info[b] - 1) +
-                                    " of matrix " + std::to_string(names ? (*names)[b] : b)};
+      throw Error{VB_ESINGULAR, std::string(what) + ": pivot failure (zero, non-finite or wrong sign) at column " +
+                                    std::to_string(info[b] - 1) + " of " + kind + " " +
+                                    std::to_string(names ? (*names)[b] : b)};
 }
 
 // primal ranks of ALL entities (each provided by the entity's owner rank = rank of its lowest
@@ -458,10 +462,11 @@ static void stage_dirichlet(vb_ctx *c) {
   for (int i = 0; i < N; ++i) {
     const SubDev &S = c->h_sub[i];
     mats[i] = MatDesc{c->d_K.p + S.off_K, S.n, S.n, S.nD};
+    mats[i].npos = S.nI;        // [u_I | p (Q_I, augmented) | Gamma]: velocity > 0, pressure < 0
   }
   STAGE_T("  assembly");
   ldl_partial_batched(mats, c->d_info.p, s);
-  check_info(c, N, "subdomain Dirichlet LDL^T (A1)");
+  check_info(c, N, "subdomain Dirichlet LDL^T (A1)", &c->sub_gid, "subdomain");
   STAGE_T("  Dirichlet LDL^T");
   std::vector<MatDesc> sg(N);
   for (int i = 0; i < N; ++i) {
@@ -662,9 +667,10 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
   for (int i = 0; i < N; ++i) {
     const SubDev &S = c->h_sub[i];
     mats[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.nG, S.n, S.nd};
+    mats[i].npos = S.nd;        // S_DD is SPD (the primal constraints remove the rigid modes)
   }
   ldl_partial_batched(mats, c->d_info.p, s);
-  check_info(c, N, "dual Schur LDL^T (A3)");
+  check_info(c, N, "dual Schur LDL^T (A3)", &c->sub_gid, "subdomain");
   for (int i = 0; i < N; ++i) {
     const SubDev &S = c->h_sub[i];
     sg[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)(S.nD + S.nd) * (S.n + 1), S.npi, S.n, 0};
@@ -737,11 +743,15 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     std::vector<int> names;
     for (int e = 0; e < nent; ++e) {
       const EntDev &E = c->h_ent[e];
-      if (E.nd) { em.push_back(MatDesc{sumbuf.p + E.off_sum, E.nd, E.nd, E.nd}); names.push_back(e); }
+      if (E.nd) {
+        em.push_back(MatDesc{sumbuf.p + E.off_sum, E.nd, E.nd, E.nd});
+        em.back().npos = E.nd;  // sum of the sharers' S_GD (SPD)
+        names.push_back(e);
+      }
     }
     c->d_info.zero(s);
     ldl_partial_batched(em, c->d_info.p, s);
-    check_info(c, em.size(), "deluxe sum LDL^T (A4)", &names);
+    check_info(c, em.size(), "deluxe sum LDL^T (A4)", &names, "entity");
     Wbuf.zero(s);
     std::vector<TriDesc> td;
     for (auto &M : em) td.push_back(TriDesc{M.A, M.n, Wbuf.p + (M.A - sumbuf.p), M.n, M.n});
@@ -934,6 +944,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     STAGE_T("  coarse pieces + assembly (C4)");
     c->d_info.zero(s);
     std::vector<MatDesc> cm{MatDesc{Kc.p, (int)Nc, (int)Nc, (int)Nc}};
+    cm[0].npos = (int)c->NPi_g;   // [u_Pi | p_0 (augmented)]: velocity > 0, pressure < 0
     ldl_partial_batched(cm, c->d_info.p, s);
     check_info(c, 1, "coarse saddle LDL^T (A5)");
     STAGE_T("  coarse LDL^T");

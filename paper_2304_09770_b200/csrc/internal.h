@@ -332,6 +332,7 @@ struct vb_ctx {
   double bytes_per_iter = 0;
   // timing
   bool timing = false;
+  int opt_true_residual = 0;         // vb_set_option("true_residual"): ||b - K x|| / ||b|| via K7
   std::vector<double> ktime_ms;
   std::vector<int> ktime_count;
   int last_iterations = 0;

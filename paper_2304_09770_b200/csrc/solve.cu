@@ -326,18 +326,37 @@ __global__ void dot_ztail_kernel(const double *__restrict__ r, double *z, const 
 }
 
 // x += alpha p, r -= alpha q (alpha = rz / pq), fused with the partial of r.r -> dst
-// p0 block of the condensed rhs: the compatibility sum_i g0_i = 0 holds up to rounding; remove the
-// rounding (mode 0: local sum into *acc; mode 1: subtract acc[0] / n_total from every entry)
-__global__ void p0_compat_kernel(double *p0, int n, double *acc, int mode, int n_total) {
+// p0 block of the condensed rhs: the compatibility sum_i g0_i = 0 must hold up to
+// rounding (checked on the host against acc[1] = sum over all pressure DOFs of |c_j g_pj|, the
+// terms g0 is summed from: VB_EINVAL otherwise); remove the rounding (mode 0: local sum and
+// abs-sum into acc[0], acc[1]; mode 1: subtract acc[0] / n_total from every entry, reading A30)
+__global__ void p0_compat_kernel(double *p0, int n, double *acc, int mode, int n_total, const double *g0abs) {
   if (mode == 0) {
-    double v = 0.0;
-    for (int i = threadIdx.x; i < n; i += 32) v += p0[i];
+    double v = 0.0, a = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) { v += p0[i]; a += g0abs[i]; }
     v = warp_sum(v);
-    if (threadIdx.x == 0) *acc = v;
+    a = warp_sum(a);
+    if (threadIdx.x == 0) { acc[0] = v; acc[1] = a; }
   } else {
     const double mean = *acc / n_total;
     for (int i = threadIdx.x; i < n; i += 32) p0[i] -= mean;
   }
+}
+
+// |b_0^(i) x_Gamma^(i)| per local subdomain (reported on VB_EBREAKDOWN; b~0 vanishes
+// on the dual coordinates, so only the primal ones enter), then the max into out[0]
+__global__ void flux_violation_kernel(const SubDev *__restrict__ subs, int N, const double *__restrict__ b0T,
+                                      const int64_t *__restrict__ loc2x, const double *__restrict__ x,
+                                      double *out) {
+  double mx = 0.0;
+  for (int i = 0; i < N; ++i) {
+    const SubDev S = subs[i];
+    double acc = 0.0;
+    for (int a = threadIdx.x; a < S.npi; a += 32) acc += b0T[S.off_Pi + a] * x[loc2x[S.off_G + S.nd + a]];
+    acc = warp_sum(acc);
+    mx = fmax(mx, fabs(acc));
+  }
+  if (threadIdx.x == 0) out[0] = mx;
 }
 
 // scal: [0] rz [1] pq [2] rr [3] rz_new [4] r0n [5] rtol*r0n [6] it [7] status [8] maxit
@@ -487,20 +506,25 @@ __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ 
 __global__ void rhs_D_kernel(const SubDev *__restrict__ subs, const int64_t *__restrict__ Ifree,
                              const int64_t *__restrict__ Pglob, const double *__restrict__ cvec,
                              const double *__restrict__ mvec, const double *__restrict__ rhs, int64_t nvf,
-                             double *bD, double *g0) {
-  __shared__ double red[32];
+                             double *bD, double *g0, double *g0abs) {
+  __shared__ double red[2][32];
   const SubDev S = subs[blockIdx.x];
   const int tid = threadIdx.x, nw = blockDim.x >> 5;
   double *b = bD + S.off_Dn;
   for (int j = tid; j < S.nI; j += blockDim.x) b[j] = rhs[Ifree[S.off_I + j]];
-  double s = 0.0;
-  for (int a = tid; a < S.nP; a += blockDim.x) s += cvec[S.off_P + a] * rhs[nvf + Pglob[S.off_P + a]];
+  double s = 0.0, sa = 0.0;
+  for (int a = tid; a < S.nP; a += blockDim.x) {
+    const double t = cvec[S.off_P + a] * rhs[nvf + Pglob[S.off_P + a]];
+    s += t;
+    sa += fabs(t);
+  }
   s = warp_sum(s);
-  if ((tid & 31) == 0) red[tid >> 5] = s;
+  sa = warp_sum(sa);
+  if ((tid & 31) == 0) { red[0][tid >> 5] = s; red[1][tid >> 5] = sa; }
   __syncthreads();
-  double g = 0.0;
-  for (int w = 0; w < nw; ++w) g += red[w];
-  if (tid == 0) g0[blockIdx.x] = g;
+  double g = 0.0, ga = 0.0;
+  for (int w = 0; w < nw; ++w) { g += red[0][w]; ga += red[1][w]; }
+  if (tid == 0) { g0[blockIdx.x] = g; g0abs[blockIdx.x] = ga; }
   for (int a = tid; a < S.nP; a += blockDim.x)
     b[S.nI + a] = rhs[nvf + Pglob[S.off_P + a]] - mvec[S.off_P + a] * g / S.vol;
 }
@@ -664,8 +688,10 @@ __global__ void gamma_back_kernel(const EntDev *__restrict__ ents, const int64_t
 }
 
 // global zero-mean pressure (Q_{h,0}): p -= c_K * (sum_K vol_K p_K0) / vol_Omega
+// acc: [2 * nb block partials | folded (sum vol p0, sum vol)]; nb = the phase-0 grid size
 __global__ void pressure_mean_kernel(const double *__restrict__ cellgeo, const int64_t *__restrict__ gid,
-                                     int geo_stride, int np, int64_t nK, double *p, int phase, double *acc) {
+                                     int geo_stride, int np, int64_t nK, double *p, int phase, double *acc,
+                                     int nb) {
   if (phase == 0) {
     __shared__ double red[2][32];
     double a = 0.0, w = 0.0;
@@ -682,14 +708,14 @@ __global__ void pressure_mean_kernel(const double *__restrict__ cellgeo, const i
       for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { A += red[0][q]; Wt += red[1][q]; }
       acc[2 * blockIdx.x] = A; acc[2 * blockIdx.x + 1] = Wt;
     }
-  } else if (phase == 1) {   // fold the block partials: acc[200], acc[201]
+  } else if (phase == 1) {   // fold the block partials: acc[2 nb], acc[2 nb + 1]
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       double A = 0, Wt = 0;
-      for (int b = 0; b < 64; ++b) { A += acc[2 * b]; Wt += acc[2 * b + 1]; }
-      acc[200] = A; acc[201] = Wt;
+      for (int b = 0; b < nb; ++b) { A += acc[2 * b]; Wt += acc[2 * b + 1]; }
+      acc[2 * nb] = A; acc[2 * nb + 1] = Wt;
     }
   } else {
-    const double mean = acc[200] / acc[201];
+    const double mean = acc[2 * nb] / acc[2 * nb + 1];
     for (int64_t K = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; K < nK; K += (int64_t)gridDim.x * blockDim.x)
       for (int a = 0; a < np; ++a) p[gid[K] * np + a] -= mean * cellgeo[K * geo_stride + 5 + a];
   }
@@ -802,6 +828,8 @@ struct SolveState {
   DBuf<double> ycell, cscal;
   int64_t n_gh = 0;
   bool ready = false;
+  bool graph_broken = false;
+  DBuf<double> g0abs;                // per local subdomain: sum_j |c_j g_pj| (rhs compatibility scale)         // capture/instantiate failed once: host-driven iterations
   DBuf<unsigned> ticket;             // single-launch reductions
   cudaStream_t s2 = nullptr;         // coarse branch of M^-1, concurrent with the local solves
   int prio_hi = 0;                   // its (higher) scheduling priority
@@ -930,6 +958,15 @@ const char *kernel_time_name(int i) { return (i >= 0 && i < N_CAT) ? kCatNames[i
 #define DOT_BLOCKS_CFG 296
 #endif
 constexpr int DOT_BLOCKS = DOT_BLOCKS_CFG;
+// scalar slots of w_dots (2 DOT_BLOCKS + 256 doubles) AFTER the block-partial region [0, DOT_BLOCKS)
+// that every fused dot's last-block reduction writes
+constexpr int W_P0 = 2 * DOT_BLOCKS;            // p0 compatibility: sum, abs-sum
+constexpr int W_TRACE = 2 * DOT_BLOCKS + 4;     // VB_PCG_TRACE norms
+constexpr int W_FLUX = 2 * DOT_BLOCKS + 6;      // max_i |b0 x_Gamma|
+constexpr int W_PM = 2 * DOT_BLOCKS + 8;        // pressure mean: 2 PM_BLOCKS partials + 2 folded
+constexpr int PM_BLOCKS = 64;
+constexpr double kCompatRel = 1e-8;             // |sum g0| <= kCompatRel * sum |g0|
+static_assert(W_PM + 2 * PM_BLOCKS + 2 <= 2 * DOT_BLOCKS + 256, "w_dots scalar slots");
 
 static SolveState *get_state(vb_ctx *c) {
   if (!c->solve_state) c->solve_state = new SolveState();
@@ -985,7 +1022,7 @@ static void apply_S(vb_ctx *c, SolveState *st, bool with_pq = false) {   // q = 
 static void trace_norm(vb_ctx *c, const char *name, const double *v, int64_t n, bool replicated) {
   static const bool on = getenv("VB_PCG_TRACE") && atoi(getenv("VB_PCG_TRACE")) >= 2;
   if (!on) return;
-  double *d = c->w_dots.p + DOT_BLOCKS + 16;
+  double *d = c->w_dots.p + W_TRACE;
   dot_partial_kernel<<<DOT_BLOCKS, 256, 0, c->stream>>>(v, v, nullptr, n, c->w_dots.p);
   dot_final_kernel<<<1, 32, 0, c->stream>>>(c->w_dots.p, DOT_BLOCKS, d);
   if (!replicated) allreduce_sum_fixed(c, d, 1);
@@ -1381,6 +1418,7 @@ void prepare_solve(vb_ctx *c) {
     st->ycell.zero(s);
     st->cscal.alloc(std::max(N, 1));
   }
+  st->g0abs.alloc(std::max(N, 1));
   VB_CUDA(cudaStreamSynchronize(s));
   st->ready = true;
   // bytes per PCG iteration (model of the streamed operators)
@@ -1456,6 +1494,35 @@ void apply_operator_device(vb_ctx *c, const double *x, double *y) {
 }
 
 void lanczos_extremes(const std::vector<double> &al, const std::vector<double> &be, double *lmin, double *lmax);
+
+__global__ void residual_kernel(const double *__restrict__ b, double *y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = b[i] - y[i];
+}
+
+// ||b - K x|| / ||b|| of the full saddle system through K7 (SURVEY §8(c) "true full-system
+// residual"; vb_set_option "true_residual"); b, x in the ABI layout (owned free DOFs)
+static double true_relative_residual(vb_ctx *c, const double *b, const double *x) {
+  cudaStream_t s = c->stream;
+  const int64_t n = (int64_t)c->owned_free.size();
+  DBuf<double> y, nn;
+  y.alloc(std::max<int64_t>(n, 1));
+  nn.alloc(2);
+  apply_operator_device(c, x, y.p);
+  residual_kernel<<<grid_for(n), 256, 0, s>>>(b, y.p, n);
+  DBuf<double> part;
+  part.alloc(DOT_BLOCKS);
+  dot_partial_kernel<<<DOT_BLOCKS, 256, 0, s>>>(y.p, y.p, nullptr, n, part.p);
+  dot_final_kernel<<<1, 32, 0, s>>>(part.p, DOT_BLOCKS, nn.p);
+  dot_partial_kernel<<<DOT_BLOCKS, 256, 0, s>>>(b, b, nullptr, n, part.p);
+  dot_final_kernel<<<1, 32, 0, s>>>(part.p, DOT_BLOCKS, nn.p + 1);
+  VB_STAGE();
+  allreduce_sum_fixed(c, nn.p, 2);
+  double h[2];
+  VB_CUDA(cudaMemcpyAsync(h, nn.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  VB_CUDA(cudaStreamSynchronize(s));
+  return h[1] > 0 ? sqrt(h[0] / h[1]) : sqrt(h[0]);
+}
 
 // one PCG step up to the stopping test: q = S^ p, pq, x/r update fused with r.r, check (SURVEY O-15)
 static void pcg_step(vb_ctx *c, SolveState *st, cudaGraphConditionalHandle hw, bool graph) {
@@ -1588,7 +1655,7 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   for (auto &S : c->h_sub) { maxnG = std::max<int64_t>(maxnG, S.nG); maxnD = std::max<int64_t>(maxnD, S.nD); }
   c->w_r.zero(s);
   rhs_D_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p, c->d_mvec.p, rhs, nvf,
-                                 c->w_bD.p, c->w_r.p + NDelta + c->NPi);
+                                 c->w_bD.p, c->w_r.p + NDelta + c->NPi, st->g0abs.p);
   run_sub_gemv(st, st->w_kd.p, st->nw_kd, st->sm_kd, st->big_kd, s);   // x_D = K_DD^-1 b_D (chunks)
   sum_chunks_kernel<<<(unsigned)((c->len_Dn + 31) / 32), 256, 0, s>>>(c->w_yDp.p, c->len_Dn, c->P_kd, c->len_Dn, c->w_xD.p);
   coupling(c, st, 0, c->w_xD.p, st->gbuf.p);                             // zG = -K_GD x_D
@@ -1598,18 +1665,23 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   run_entity_sum(c, st->ESB, st->gbuf.p, c->w_gam.p, st->gam2.p);             // ghat = b + sum_m zG^(m)
   if (!c->h_ent.empty())
     gamma_rhs_kernel<<<c->h_ent.size(), 512, 0, s>>>(c->d_ent.p, c->d_T.p, c->w_gam.p, NDelta, c->w_r.p);
-  p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + 220, 0, c->Ng);
-  allreduce_sum_fixed(c, c->w_dots.p + 220, 1);
-  p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + 220, 1, c->Ng);
+  p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + W_P0, 0, c->Ng, st->g0abs.p);
+  allreduce_sum_fixed(c, c->w_dots.p + W_P0, 2);
+  p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + W_P0, 1, c->Ng, st->g0abs.p);
   VB_STAGE();
   // ---------------- PCG (SURVEY O-15), iterations driven on the device (scal[6] = it, scal[7] = status)
   c->w_x.zero(s);
   double *sc = c->w_scal.p;
   dot(c, c->w_r.p, c->w_r.p, nx, sc + 2);
   pcg_init_kernel<<<1, 1, 0, s>>>(sc, rtol, maxit);
-  double h[9];
+  double h[9], compat[2];
   VB_CUDA(cudaMemcpyAsync(h, sc, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  VB_CUDA(cudaMemcpyAsync(compat, c->w_dots.p + W_P0, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
   VB_CUDA(cudaStreamSynchronize(s));
+  // flux compatibility of the rhs: sum_i g0_i = 0 up to rounding, else VB_EINVAL
+  VB_REQUIRE(fabs(compat[0]) <= kCompatRel * compat[1], VB_EINVAL,
+             "flux-incompatible rhs: sum_i g0_i = " + std::to_string(compat[0]) + " (sum_i |g0_i| = " +
+                 std::to_string(compat[1]) + "); the pressure rows must integrate to zero against constants");
   const double r0n = h[4];
   if (trace) fprintf(stderr, "[vb rank %d] rr0 %.17g\n", c->rank, h[2]);
   if (h[7] == 0.0) {
@@ -1625,17 +1697,44 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
       if (trace)
         fprintf(stderr, "[vb rank %d] it %d rz %.17g pq %.17g rr %.17g\n", c->rank, (int)h[6], h[0], h[1], h[2]);
       if (h[7] != 0.0) break;
-      if (graph) {     // the remaining steps as one graph launch, stopping on the device
-        if (!st->gexec) build_iteration_graph(c, st);
-        VB_CUDA(cudaEventRecord(st->ev_fork, s));
-        VB_CUDA(cudaStreamWaitEvent(st->sg, st->ev_fork, 0));
-        VB_CUDA(cudaGraphLaunch(st->gexec, st->sg));
-        VB_CUDA(cudaEventRecord(st->ev_join, st->sg));
-        VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
-        break;
+      if (graph && !st->graph_broken) {   // the remaining steps as one graph launch, stopping on the device
+        if (!st->gexec) {
+          try {
+            build_iteration_graph(c, st);
+          } catch (const Error &e) {
+            // e.g. a transport whose calls cannot be captured into a conditional body: keep
+            // iterating host-driven (same kernels, same order; one host check per step)
+            (void)cudaGetLastError();
+            st->graph_broken = true;
+            st->gexec = nullptr;
+            fprintf(stderr, "[vb rank %d] iteration graph unavailable (%s); host-driven iterations\n", c->rank,
+                    e.msg.c_str());
+          }
+        }
+        if (st->gexec) {
+          VB_CUDA(cudaEventRecord(st->ev_fork, s));
+          VB_CUDA(cudaStreamWaitEvent(st->sg, st->ev_fork, 0));
+          VB_CUDA(cudaGraphLaunch(st->gexec, st->sg));
+          VB_CUDA(cudaEventRecord(st->ev_join, st->sg));
+          VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
+          break;
+        }
       }
       pcg_mstep(c, st);
     }
+  }
+  flux_violation_kernel<<<1, 32, 0, s>>>(c->d_sub.p, N, c->d_b0T.p, c->d_loc2x.p, c->w_x.p, c->w_dots.p + W_FLUX);
+  VB_STAGE();
+  double flux = 0.0;
+  if (c->nranks > 1) {   // max over ranks
+    if (c->w_red.n < (size_t)c->nranks) c->w_red.alloc(std::max(c->nranks, 8));
+    c->comm->allgather(c->w_dots.p + W_FLUX, c->w_red.p, 1, s);
+    std::vector<double> fl(c->nranks);
+    VB_CUDA(cudaMemcpyAsync(fl.data(), c->w_red.p, c->nranks * sizeof(double), cudaMemcpyDeviceToHost, s));
+    VB_CUDA(cudaStreamSynchronize(s));
+    for (double v : fl) flux = std::max(flux, v);
+  } else {
+    VB_CUDA(cudaMemcpyAsync(&flux, c->w_dots.p + W_FLUX, sizeof(double), cudaMemcpyDeviceToHost, s));
   }
   VB_CUDA(cudaMemcpyAsync(h, sc, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
   VB_CUDA(cudaStreamSynchronize(s));
@@ -1663,15 +1762,18 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   xout_kernel<<<N, 256, 0, s>>>(c->d_sub.p, c->w_xD.p, c->d_subI_free.p, c->d_subP_glob.p, c->d_cvec.p, c->d_mvec.p,
                                 c->w_x.p + NDelta + c->NPi, nvf, x);
   VB_STAGE();
-  pressure_mean_kernel<<<64, 256, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np, c->nKl, x + nvf, 0,
-                                          c->w_dots.p);
+  double *pm = c->w_dots.p + W_PM;
+  pressure_mean_kernel<<<PM_BLOCKS, 256, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np, c->nKl,
+                                                 x + nvf, 0, pm, PM_BLOCKS);
   pressure_mean_kernel<<<1, 32, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np, c->nKl, x + nvf, 1,
-                                        c->w_dots.p);
-  allreduce_sum_fixed(c, c->w_dots.p + 200, 2);
+                                        pm, PM_BLOCKS);
+  allreduce_sum_fixed(c, pm + 2 * PM_BLOCKS, 2);
   pressure_mean_kernel<<<grid_for(c->nKl), 256, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np,
-                                                        c->nKl, x + nvf, 2, c->w_dots.p);
+                                                        c->nKl, x + nvf, 2, pm, PM_BLOCKS);
   VB_STAGE();
   if (c->nranks > 1) dev_gather(x, c->d_owned_free.p, (int64_t)c->owned_free.size(), x_out, s);
+  double true_rel = -1.0;
+  if (c->opt_true_residual && rep) true_rel = true_relative_residual(c, rhs_in, x_out);
   VB_CUDA(cudaStreamSynchronize(s));
   c->last_iterations = it;
   collect_times(c, st);
@@ -1681,14 +1783,14 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
     rep->r0_norm = r0n;
     rep->r_final_norm = rn;
     rep->rel_residual = r0n > 0 ? rn / r0n : 0.0;
-    rep->true_rel_residual = -1.0;
+    rep->true_rel_residual = true_rel;
     // Lanczos T from the CG coefficients (SURVEY O-15 index convention): beta_j pairs alpha_j, alpha_{j+1}
     std::vector<double> bb(betas.begin(), betas.end());
     double lmin = 1, lmax = 1;
     lanczos_extremes(alphas, bb, &lmin, &lmax);
     rep->lambda_min = lmin; rep->lambda_max = lmax; rep->kappa = lmin > 0 ? lmax / lmin : INFINITY;
     rep->bytes_per_iter_model = c->bytes_per_iter;
-    rep->flux_violation_max = c->flux_violation;
+    rep->flux_violation_max = flux;
     rep->n_primal = c->NPi_g; rep->n_coarse = c->Nc;
     rep->n_dofs_paper = c->nvel + c->npres;
     rep->n_adaptive = c->n_adaptive;

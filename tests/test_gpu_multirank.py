@@ -36,7 +36,11 @@ def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=N
             y = torch.zeros_like(rhs)
             ctx.apply_operator(x, y)
             res = (rhs - y).cpu().numpy()
-        out = dict(rep=rep, ids=ctx.dof_layout(), x=x.cpu().numpy(), rhs=rhs.cpu().numpy(), res=res)
+        # the host-buffer entry point on the same rank-local layout (vb_pcg_solve_host: owned DOFs)
+        rh = rhs.cpu().numpy()
+        xh = np.zeros(ctx.n_free)
+        ctx.pcg_solve_host(rh, xh, rtol=rtol)
+        out = dict(rep=rep, ids=ctx.dof_layout(), x=x.cpu().numpy(), rhs=rh, res=res, x_host=xh)
         ctx.close()
         return out
 
@@ -93,6 +97,8 @@ def test_multirank_matches_oracle_and_single_rank(name, kw, rank_grid):
     x1 = x1.cpu().numpy()
     outs = _run_ranks(prob, rank_grid)
     gid = _global_free_ids(gs)
+    for o in outs:      # vb_pcg_solve_host == vb_pcg_solve on every rank (owned-DOF sizes)
+        assert np.abs(o["x_host"] - o["x"]).max() <= 1e-14 * np.abs(o["x"]).max()
     assert np.array_equal(np.sort(np.concatenate([o["ids"] for o in outs])), np.sort(gid))   # a partition
     pos = {int(g): i for i, g in enumerate(gid)}
     n = gid.size

@@ -94,38 +94,45 @@ def load_golden(name):
     import os
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "oracle_%s_full.npz" % name)
     z = np.load(path)
-    return z["idx"], z["x"], z["rhs"], json.loads(str(z["meta"]))
+    return z, json.loads(str(z["meta"]))
 
 
 def check_against_golden(ctx, rhs, x, rep, name):
-    """SURVEY §8(c) gates against the stored full-size oracle solve: sampled solution entries
-    (each within 1e-8 of the block norm), iterations +-1, kappa 1%, counts exact."""
-    idx, xs, rs, meta = load_golden(name)
+    """SURVEY §8(c) gates against the stored full-size oracle solve: the WHOLE solution vector,
+    velocity and pressure blocks separately at relative L2 <= 1e-8 (pressures both zero-mean),
+    final relative residual <= 1e-10, iterations +-1, kappa 1 %, counts exact; the rhs on a seeded
+    sample of entries and in norm."""
+    z, meta = load_golden(name)
     nv = meta["n_free_vel"]
-    assert ctx.n_vel == nv and rep["n_dofs_paper"] == meta["n_dofs_paper"]
+    assert ctx.n_vel == nv and ctx.n_free == nv + meta["n_pres"]
+    assert rep["n_dofs_paper"] == meta["n_dofs_paper"]
     assert rep["n_primal"] == meta["n_primal"] and rep["n_coarse"] == meta["n_coarse"]
+    idx = z["idx"]
     rh = rhs.cpu().numpy()
     assert abs(np.linalg.norm(rh) - meta["norm_rhs"]) <= 1e-12 * meta["norm_rhs"]
-    assert np.abs(rh[idx] - rs).max() <= 1e-12 * meta["norm_rhs"]
+    assert np.abs(rh[idx] - z["rhs"]).max() <= 1e-12 * meta["norm_rhs"]
     xh = x.cpu().numpy()
-    assert abs(np.linalg.norm(xh[:nv]) - meta["norm_u"]) <= 1e-8 * meta["norm_u"]
-    assert abs(np.linalg.norm(xh[nv:]) - meta["norm_p"]) <= 1e-8 * meta["norm_p"]
-    v, p = idx < nv, idx >= nv
-    assert np.abs(xh[idx[v]] - xs[v]).max() <= 1e-8 * meta["norm_u"]
-    assert np.abs(xh[idx[p]] - xs[p]).max() <= 1e-8 * meta["norm_p"]
+    xo = z["x_full"]
+    du = np.linalg.norm(xh[:nv] - xo[:nv]) / np.linalg.norm(xo[:nv])
+    dp = np.linalg.norm(xh[nv:] - xo[nv:]) / np.linalg.norm(xo[nv:])
+    assert du <= 1e-8 and dp <= 1e-8, (du, dp)
     assert rep["rel_residual"] <= 1e-10
     assert abs(rep["iterations"] - meta["iterations"]) <= 1, (rep["iterations"], meta["iterations"])
     assert abs(rep["kappa"] - meta["kappa"]) <= 0.01 * meta["kappa"], (rep["kappa"], meta["kappa"])
+    print("%s full-size parity: du %.2e dp %.2e it %d (oracle %d) kappa %.6f (oracle %.6f)"
+          % (name, du, dp, rep["iterations"], meta["iterations"], rep["kappa"], meta["kappa"]))
     return meta
 
 
-@pytest.mark.parametrize("name", ["c2"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
 def test_full_size_parity(name):
-    """BASELINE config 2 at full size, GPU product path vs the stored oracle solve (config 3 at full
-    size needs ~200 GB of dense oracle subdomain matrices: test_c3_full_size_properties)."""
+    """BASELINE configs 2, 3 and 5 (the bench workload, in bench.py's launch configuration: one
+    GPU, 32^3 cells, 512 subdomains) at full size: GPU product path vs the stored oracle solve
+    (whole solution vector; config 4 with its adaptive enrichment: test_gpu_adaptive.py)."""
     import torch
     import paper_2304_09770_b200 as vb
-    prob = make_problem(name)
+    from synthetic.configs import C5_DIMS
+    prob = make_problem(name, dims=C5_DIMS[1]) if name == "c5" else make_problem(name)
     ctx = _ctx(prob)
     ctx.factor()
     rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
