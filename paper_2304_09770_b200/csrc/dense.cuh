@@ -21,17 +21,23 @@ constexpr double kPivRel = 1e-13;
 // its copy pattern.
 struct GemmPlan {
   std::vector<GemmProb> probs;
-  std::vector<std::array<std::vector<int4>, 4>> ltiles;   // per launch, per class: (prob, tm, tn, 0)
-  std::vector<std::array<std::pair<int, int>, 4>> lrange;  // after upload: (tile_begin, tile_count)
+  // per launch, per class: segments {problem, first tile, tiles per row, lower} (gemm_dmma.cuh seg_tile)
+  std::vector<std::array<std::vector<int4>, 4>> ltiles;
+  std::vector<std::array<int64_t, 4>> ltcount;             // tiles per launch and class
+  std::vector<std::array<std::pair<int, int>, 4>> lrange;  // after upload: (segment_begin, segment_count)
+  std::vector<std::array<int, 4>> lntile;                  // after upload: tiles (= grid size)
   std::vector<std::vector<int>> dense;        // per launch: large problems run as 2D grids
   std::vector<char> scaled;                   // per launch: some tile-list problem has d != null
+  std::vector<std::array<char, 4>> novec;     // per launch and class: some operand not 16-byte aligned
   bool allow_kz = false;                      // honour GemmProb.kz_on regardless of VB_KZ (vb_debug_gemm)
   DBuf<GemmProb> d_probs;
   DBuf<int4> d_tiles;
   int begin_launch() {
     ltiles.push_back({});
+    ltcount.push_back({0, 0, 0, 0});
     dense.push_back({});
     scaled.push_back(0);
+    novec.push_back({0, 0, 0, 0});
     return ltiles.size() - 1;
   }
   void add(const GemmProb &p);             // adds tiles to the current launch

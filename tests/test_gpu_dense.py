@@ -1,6 +1,6 @@
 """The factorisation's grouped DMMA GEMM (dense.cu, used by A1-A5) against torch float64 matmul:
 all transpose cases, diagonal scaling, beta accumulation, ragged sizes that span several
-128 x 64 x 16 tiles with partial edge tiles, batched problems and the large-problem 2-D grid path."""
+64 x 64 x 16 tiles with partial edge tiles (odd leading dimensions: 8-byte copy path; even: 16-byte), batched problems and the large-problem 2-D grid path."""
 import pytest
 
 pytestmark = pytest.mark.gpu

@@ -67,6 +67,25 @@ def test_multiplicity_scaling_parity(name, kw):
     assert np.linalg.norm(xh[ctx.n_vel:] - p_o) <= 1e-8 * np.linalg.norm(p_o)
 
 
+@pytest.mark.parametrize("name,kw", [("c1", dict(n=8)), ("c1", dict(n=8, k=3)),
+                                     ("c3", dict(n=8, sub=(2, 2, 2)))])
+def test_minimal_coarse_space_parity(name, kw):
+    """The paper's minimal primal space: vertices + face fluxes only (nu_tol = infinity, P:1197-1199;
+    SURVEY f3), against the oracle with the same constraints (SURVEY §8(c) gates)."""
+    from oracle.assemble import GlobalSystem
+    from oracle.bddc import BDDC
+    cons = dict(vertex=1, edge_avg=0, face_avg=0, face_flux=1)
+    prob = make_problem(name, constraints=cons, **kw)
+    ctx, rhs, x, rep = _gpu_solve(prob)
+    u_o, p_o, rep_o = BDDC(GlobalSystem(prob)).solve()
+    assert rep["n_primal"] == rep_o["n_primal"]
+    assert abs(rep["iterations"] - rep_o["iterations"]) <= 1, (rep["iterations"], rep_o["iterations"])
+    assert abs(rep["kappa"] - rep_o["kappa"]) <= 0.01 * rep_o["kappa"]
+    xh = x.cpu().numpy()
+    assert np.linalg.norm(xh[:ctx.n_vel] - u_o) <= 1e-8 * np.linalg.norm(u_o)
+    assert np.linalg.norm(xh[ctx.n_vel:] - p_o) <= 1e-8 * np.linalg.norm(p_o)
+
+
 def test_viscosity_scaling_invariance():
     """F9: nu -> 1000 nu with the same rhs: identical iterations and kappa, u / 1000, p unchanged."""
     import torch
