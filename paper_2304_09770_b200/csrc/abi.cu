@@ -53,12 +53,13 @@ void layout_phase_a(vb_ctx *c) {
     D.cell_begin = sub_cells.size();
     for (int cell : S.cells) sub_cells.push_back(cell);
     D.cell_end = sub_cells.size();
-    D.off_K = K; K += (int64_t)S.n * S.n;
+    D.ldk = ld4(S.n);
+    D.off_K = K; K += (int64_t)D.ldk * S.n;
     D.off_G = G; G += S.nG;
     D.off_P = P; P += S.nP;
     D.off_I = I; I += S.nI;
     D.off_Dn = Dn; Dn += S.nD;
-    D.off_X = X; X += (int64_t)S.nG * S.nG;
+    D.off_X = X; X += (int64_t)ld4(S.nG) * S.nG;
     double vol = 0, nus = 0;
     for (int cell : S.cells) { vol += c->cellgeo[(int64_t)cell * c->geo_stride]; nus += c->nu[c->cell_gid[cell]]; }
     D.vol = vol;

@@ -389,7 +389,7 @@ void adaptive_enrich(vb_ctx *c, double tau, const DBuf<double> &sidebuf) {
         const SlotDev &sl = c->h_slot[fslots[q]];
         const SubDev &S = c->h_sub[sl.sub];
         double *o = buf.p + off[q - a];
-        pd.push_back(PermDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.n, S.nG, sl.offD, sl.nd, o});
+        pd.push_back(PermDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1), S.ldk, S.nG, sl.offD, sl.nd, o});
         md.push_back(MatDesc{o, S.nG, S.nG, S.nG - sl.nd});
         cd.push_back(CopyDesc{o + (int64_t)(S.nG - sl.nd) * (S.nG + 1), S.nG, sl.nd, Stl.p + st_off[fslots[q]]});
       }

@@ -12,7 +12,7 @@ namespace vb {
 
 // ------------------------------------------------------------------ grouped GEMM (DMMA)
 // gemm_dmma.cuh: CTA tile 64 x 64 x 16, 4 warps of 16 x 64 warp tiles (m16n8k16 f64 MMAs), 3-stage
-// cp.async ring, 16-byte copies where the launch's operands allow, 4 CTAs per SM.  Chosen over
+// cp.async ring, 16-byte copies (pairs of 8-byte ones for unaligned problems), 4 CTAs per SM.  Chosen over
 // 128 x 64 / 128 x 128 / 64 x 128 / 64 x 32 / 32 x 64 and 16 or 32-deep slabs by tools/gemm_proto.cu
 // on the factor's shapes (profiles/r02_gemm_proto.txt).
 using GCfg = g2::Cfg<64, 64, 16, 4, 1, 3, 4>;
@@ -47,28 +47,14 @@ static void launch_gemm(dim3 grid, const GemmProb *probs, const int4 *segs, int 
 }
 
 template <bool DENSE, bool SCALED>
-static void launch_gemm_cls(int cls, bool vec, dim3 grid, const GemmProb *probs, const int4 *tiles, int tile0,
-                            int nseg, cudaStream_t s) {
-  if (vec) {
-    switch (cls) {
-      case 0: launch_gemm<DENSE, SCALED, false, false, true>(grid, probs, tiles, tile0, nseg, s); break;
-      case 1: launch_gemm<DENSE, SCALED, true, false, true>(grid, probs, tiles, tile0, nseg, s); break;
-      case 2: launch_gemm<DENSE, SCALED, false, true, true>(grid, probs, tiles, tile0, nseg, s); break;
-      default: launch_gemm<DENSE, SCALED, true, true, true>(grid, probs, tiles, tile0, nseg, s); break;
-    }
-  } else {
-    switch (cls) {
-      case 0: launch_gemm<DENSE, SCALED, false, false, false>(grid, probs, tiles, tile0, nseg, s); break;
-      case 1: launch_gemm<DENSE, SCALED, true, false, false>(grid, probs, tiles, tile0, nseg, s); break;
-      case 2: launch_gemm<DENSE, SCALED, false, true, false>(grid, probs, tiles, tile0, nseg, s); break;
-      default: launch_gemm<DENSE, SCALED, true, true, false>(grid, probs, tiles, tile0, nseg, s); break;
-    }
+static void launch_gemm_cls(int cls, dim3 grid, const GemmProb *probs, const int4 *segs, int seg0, int nseg,
+                            cudaStream_t s) {
+  switch (cls) {
+    case 0: launch_gemm<DENSE, SCALED, false, false, true>(grid, probs, segs, seg0, nseg, s); break;
+    case 1: launch_gemm<DENSE, SCALED, true, false, true>(grid, probs, segs, seg0, nseg, s); break;
+    case 2: launch_gemm<DENSE, SCALED, false, true, true>(grid, probs, segs, seg0, nseg, s); break;
+    default: launch_gemm<DENSE, SCALED, true, true, true>(grid, probs, segs, seg0, nseg, s); break;
   }
-}
-
-// 16-byte copies need 16-byte aligned operand columns: aligned base, even leading dimension
-static bool vec_ok(const GemmProb &p) {
-  return ((uintptr_t)p.A % 16 == 0) && ((uintptr_t)p.B % 16 == 0) && p.lda % 2 == 0 && p.ldb % 2 == 0;
 }
 
 static int trans_class(const GemmProb &p) { return (p.transA ? 1 : 0) + (p.transB ? 2 : 0); }
@@ -107,7 +93,6 @@ void GemmPlan::add(const GemmProb &p_in) {
     return;
   }
   if (p.d) scaled.back() = 1;
-  if (!vec_ok(p)) novec.back()[trans_class(p)] = 1;
   auto &tl = ltiles.back()[trans_class(p)];
   auto &cnt = ltcount.back()[trans_class(p)];
   int64_t ntile = 0;   // tiles of this problem (lower: j <= i only, square tiles)
@@ -137,20 +122,19 @@ void GemmPlan::run(int launch, cudaStream_t s) {
   for (int c = 0; c < 4; ++c) {
     const auto &R = lrange[launch][c];
     if (R.second <= 0) continue;
-    const bool vec = !novec[launch][c];
     const dim3 grid(lntile[launch][c]);
     if (scaled[launch])
-      launch_gemm_cls<false, true>(c, vec, grid, d_probs.p, d_tiles.p, R.first, R.second, s);
+      launch_gemm_cls<false, true>(c, grid, d_probs.p, d_tiles.p, R.first, R.second, s);
     else
-      launch_gemm_cls<false, false>(c, vec, grid, d_probs.p, d_tiles.p, R.first, R.second, s);
+      launch_gemm_cls<false, false>(c, grid, d_probs.p, d_tiles.p, R.first, R.second, s);
   }
   for (int pid : dense[launch]) {
     const GemmProb &p = probs[pid];
     dim3 grid((p.N + GBN - 1) / GBN, (p.M + GBM - 1) / GBM);
     if (p.d)
-      launch_gemm_cls<true, true>(trans_class(p), vec_ok(p), grid, d_probs.p, d_tiles.p, pid, 0, s);
+      launch_gemm_cls<true, true>(trans_class(p), grid, d_probs.p, d_tiles.p, pid, 0, s);
     else
-      launch_gemm_cls<true, false>(trans_class(p), vec_ok(p), grid, d_probs.p, d_tiles.p, pid, 0, s);
+      launch_gemm_cls<true, false>(trans_class(p), grid, d_probs.p, d_tiles.p, pid, 0, s);
   }
 }
 
@@ -208,65 +192,72 @@ __device__ void ldl_diag32(const MatDesc &M, int j0, int nb, double (*L11)[33], 
   __syncthreads();
 }
 
-// One launch per 32-column panel of the blocked LDL^T (ldl_partial_batched).  Every CTA factors the
-// 32 x 32 diagonal block in shared memory (redundantly: ~6 kflop against its 128 rows x 528 FMAs),
-// forms W = L11^{-T} D11^{-1} (lane j: column j, back substitution) and computes its rows of
-// L21 = A21 W as independent dot products (one thread per row; column-major rows are coalesced);
-// CTA 0 also stores the factored diagonal block in `diag` (every CTA reads the unfactored one, so
-// it goes back into the matrix in a second, trivial launch: ldl_diag_store_kernel).
+// Panel of the blocked LDL^T (ldl_partial_batched), two launches.  (a) one CTA per matrix: factor
+// the nb x nb diagonal block D11 L11 (one warp, ldl_diag32), write it back, and form
+// W = L11^{-T} D11^{-1} (lane j: column j, back substitution) into `wbuf`; (b) the rows below:
+// L21 = A21 W as independent dot products (one thread per row; column-major rows are coalesced),
+// W read once per CTA into shared memory.  The serial 32-step work is done once per matrix.
 constexpr int PANEL_ROWS = 128;
-__global__ void __launch_bounds__(PANEL_ROWS) ldl_panel_kernel(const MatDesc *__restrict__ mats, int j0, int *info,
-                                                               const double *__restrict__ scale, double *diag) {
+__global__ void __launch_bounds__(128) ldl_panel_a_kernel(const MatDesc *__restrict__ mats, int j0, int *info,
+                                                          const double *__restrict__ scale, double *wbuf) {
+  const MatDesc M = mats[blockIdx.x];
+  if (j0 >= M.m) return;
+  const int nb = min(32, M.m - j0);
+  __shared__ double L11[32][33], dd[32];
+  ldl_diag32(M, j0, nb, L11, dd, info ? info + blockIdx.x : nullptr, true, scale[blockIdx.x]);
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < 1024; idx += blockDim.x) {
+    const int i = idx & 31, j = idx >> 5;
+    if (i < nb && j < nb && i >= j) M.A[(j0 + i) + (int64_t)(j0 + j) * M.ld] = (i == j) ? dd[i] : L11[i][j];
+  }
+  if (tid < 32) {   // W = U^{-1} D^{-1}, U = L11^T unit upper: lane j back-substitutes column j
+    const int j = tid;
+    double w[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) w[t] = 0.0;
+    if (j < nb) {
+      w[j] = 1.0 / dd[j];
+#pragma unroll
+      for (int t = 31; t >= 0; --t) {
+        if (t < j) {
+          double v = 0.0;
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (q > t && q <= j) v -= L11[q][t] * w[q];   // U[t][q] = L11[q][t]
+          w[t] = v;
+        }
+      }
+    }
+    double *W = wbuf + (int64_t)blockIdx.x * 1024;   // W[t + 32 j]
+#pragma unroll
+    for (int t = 0; t < 32; ++t) W[t + 32 * j] = w[t];
+  }
+}
+
+__global__ void __launch_bounds__(PANEL_ROWS) ldl_panel_b_kernel(const MatDesc *__restrict__ mats, int j0,
+                                                                 const double *__restrict__ wbuf) {
   const MatDesc M = mats[blockIdx.y];
   if (j0 >= M.m) return;
   const int nb = min(32, M.m - j0);
   const int r0 = j0 + nb + PANEL_ROWS * blockIdx.x;
-  if (blockIdx.x > 0 && r0 >= M.n) return;
-  __shared__ double L11[32][33], W[32][33], dd[32];
-  ldl_diag32(M, j0, nb, L11, dd, info ? info + blockIdx.y : nullptr, blockIdx.x == 0, scale[blockIdx.y]);
-  const int tid = threadIdx.x;
-  if (blockIdx.x == 0)
-    for (int idx = tid; idx < 1024; idx += blockDim.x) {
-      const int i = idx & 31, j = idx >> 5;
-      diag[blockIdx.y * 1024 + idx] = (i == j) ? dd[i] : L11[i][j];
-    }
   if (r0 >= M.n) return;
-  if (tid < 32) {   // W = U^{-1} D^{-1}, U = L11^T unit upper: lane j back-substitutes column j
-    const int j = tid;
-    if (j < nb) {
-      W[j][j] = 1.0 / dd[j];
-      for (int t = j - 1; t >= 0; --t) {
-        double v = 0.0;
-        for (int q = t + 1; q <= j; ++q) v -= L11[q][t] * W[q][j];   // U[t][q] = L11[q][t]
-        W[t][j] = v;
-      }
-    }
-  }
+  __shared__ double W[32][33];
+  const double *Wg = wbuf + (int64_t)blockIdx.y * 1024;
+  for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) W[idx & 31][idx >> 5] = Wg[idx];
   __syncthreads();
-  const int row = r0 + tid;
-  if (row < M.n) {
-    double a[32];
+  const int row = r0 + threadIdx.x;
+  if (row >= M.n) return;
+  double a[32];
 #pragma unroll
-    for (int t = 0; t < 32; ++t) a[t] = t < nb ? M.A[row + (int64_t)(j0 + t) * M.ld] : 0.0;
+  for (int t = 0; t < 32; ++t) a[t] = t < nb ? M.A[row + (int64_t)(j0 + t) * M.ld] : 0.0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j < nb) {
-        double v = 0.0;
+  for (int j = 0; j < 32; ++j) {
+    if (j < nb) {
+      double v = 0.0;
 #pragma unroll
-        for (int t = 0; t <= j; ++t) v += a[t] * W[t][j];
-        M.A[row + (int64_t)(j0 + j) * M.ld] = v;
-      }
+      for (int t = 0; t <= j; ++t) v += a[t] * W[t][j];
+      M.A[row + (int64_t)(j0 + j) * M.ld] = v;
     }
-  }
-}
-
-__global__ void ldl_diag_store_kernel(const MatDesc *__restrict__ mats, int j0, const double *__restrict__ diag) {
-  const MatDesc M = mats[blockIdx.x];
-  if (j0 >= M.m) return;
-  const int nb = min(32, M.m - j0);
-  for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
-    const int i = idx & 31, j = idx >> 5;
-    if (i < nb && j < nb && i >= j) M.A[(j0 + i) + (int64_t)(j0 + j) * M.ld] = diag[blockIdx.x * 1024 + idx];
   }
 }
 
@@ -274,7 +265,7 @@ __global__ void ldl_diag_store_kernel(const MatDesc *__restrict__ mats, int j0, 
 // panel they are split recursively in halves (multiples of 32): factor the left half, update the
 // right half's columns (all rows below) with K = the left half's width, factor the right half -- so
 // the intra-panel updates run as K = 128 / 64 / 32 DMMA GEMMs instead of a sequence of K = 32 ones;
-// the 32-column leaves are ldl_panel_kernel launches.  The trailing matrix is updated once per wide
+// the 32-column leaves are ldl_panel_a/b_kernel launches.  The trailing matrix is updated once per wide
 // panel (K = LDL_NB).  Every step is one launch over all matrices of the batch.
 void ldl_partial_batched(const std::vector<MatDesc> &mats, int *info_dev, cudaStream_t s) {
   if (mats.empty()) return;
@@ -337,10 +328,10 @@ void ldl_partial_batched(const std::vector<MatDesc> &mats, int *info_dev, cudaSt
   for (auto &op : ops) {
     if (op.first == 0) {
       const int j0 = op.second;
-      dim3 grid(std::max(1, (maxn - j0 - 1) / PANEL_ROWS + 1), mats.size());
-      ldl_panel_kernel<<<grid, PANEL_ROWS, 0, s>>>(dm.p, j0, info_dev, dscale.p, ddiag.p);
+      ldl_panel_a_kernel<<<mats.size(), 128, 0, s>>>(dm.p, j0, info_dev, dscale.p, ddiag.p);
       VB_CHECK_LAUNCH();
-      ldl_diag_store_kernel<<<mats.size(), 256, 0, s>>>(dm.p, j0, ddiag.p);
+      dim3 grid(std::max(1, (maxn - j0 - 1) / PANEL_ROWS + 1), mats.size());
+      ldl_panel_b_kernel<<<grid, PANEL_ROWS, 0, s>>>(dm.p, j0, ddiag.p);
       VB_CHECK_LAUNCH();
     } else {
       plan.run(op.second, s);
@@ -356,34 +347,55 @@ __global__ void set_identity_kernel(const TriDesc *mats) {
     T.X[i + (int64_t)i * T.ldx] = 1.0;
 }
 
-// X_J <- L_JJ^{-1} X_J for the 32-row block J (unit lower L_JJ) on the columns 0 .. 32 J + nb - 1:
-// each CTA inverts the 32 x 32 block in shared memory (lane j: column j of the inverse, forward
-// substitution) and applies it to TRI_COLS columns, one thread per column (independent dot products).
+// Inverses of all 32 x 32 unit-lower diagonal blocks of L (known before the blocked inversion
+// starts): CTA (J, matrix), lane j computes column j of L_JJ^{-1} by forward substitution in
+// registers into linv[matrix offset + 1024 J] (column-major 32 x 32, zero above the diagonal).
+__global__ void tri_diag_inv_kernel(const TriDesc *__restrict__ mats, const int64_t *__restrict__ off,
+                                    double *linv) {
+  const TriDesc T = mats[blockIdx.y];
+  const int J = blockIdx.x, r0 = 32 * J;
+  if (r0 >= T.m) return;
+  const int nb = min(32, T.m - r0);
+  __shared__ double L[32][33];
+  for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
+    const int i = idx & 31, j = idx >> 5;
+    L[i][j] = (i < nb && j < nb && i > j) ? T.L[(r0 + i) + (int64_t)(r0 + j) * T.ldl] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  double *Li = linv + off[blockIdx.y] + 1024 * (int64_t)J;
+  const int j = threadIdx.x;
+  double col[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) col[i] = (i == j && j < nb) ? 1.0 : 0.0;
+#pragma unroll
+  for (int i = 1; i < 32; ++i) {
+    if (i > j && i < nb) {
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        if (q >= j && q < i) v -= L[i][q] * col[q];
+      col[i] = v;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Li[i + 32 * j] = col[i];
+}
+
+// X_J <- L_JJ^{-1} X_J for the 32-row block J on the columns 0 .. 32 J + nb - 1, one thread per
+// column (independent dot products with the precomputed inverse, read once per CTA).
 constexpr int TRI_COLS = 128;
-__global__ void __launch_bounds__(TRI_COLS) trsm_diag_kernel(const TriDesc *__restrict__ mats, int J) {
+__global__ void __launch_bounds__(TRI_COLS) trsm_diag_kernel(const TriDesc *__restrict__ mats, int J,
+                                                             const int64_t *__restrict__ off,
+                                                             const double *__restrict__ linv) {
   const TriDesc T = mats[blockIdx.y];
   const int r0 = 32 * J;
   if (r0 >= T.m) return;
   const int nb = min(32, T.m - r0);
   if (TRI_COLS * (int)blockIdx.x >= r0 + nb) return;
-  __shared__ double L[32][33], Li[32][33];
-  for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
-    const int i = idx & 31, j = idx >> 5;
-    L[i][j] = (i < nb && j < nb && i > j) ? T.L[(r0 + i) + (int64_t)(r0 + j) * T.ldl] : 0.0;
-    Li[i][j] = 0.0;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {   // Li = L^{-1} (unit lower), column j = lane: Li[i][j] = -sum_{j<=q<i} L[i][q] Li[q][j]
-    const int j = threadIdx.x;
-    if (j < nb) {
-      Li[j][j] = 1.0;
-      for (int i = j + 1; i < nb; ++i) {
-        double v = 0.0;
-        for (int q = j; q < i; ++q) v -= L[i][q] * Li[q][j];
-        Li[i][j] = v;
-      }
-    }
-  }
+  __shared__ double Li[32][33];
+  const double *Lg = linv + off[blockIdx.y] + 1024 * (int64_t)J;
+  for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) Li[idx & 31][idx >> 5] = Lg[idx];
   __syncthreads();
   const int col = TRI_COLS * blockIdx.x + threadIdx.x;
   if (col >= r0 + nb) return;
@@ -461,11 +473,20 @@ void tri_inverse_batched(const std::vector<TriDesc> &mats, cudaStream_t s) {
     ops.push_back({1, lid});
   }
   plan.upload(s);
+  std::vector<int64_t> off(mats.size());
+  int64_t tot = 0;
+  for (size_t b = 0; b < mats.size(); ++b) { off[b] = tot; tot += 1024 * (int64_t)((mats[b].m + 31) / 32); }
+  DBuf<int64_t> doff;
+  DBuf<double> linv;
+  doff.upload(off, s);
+  linv.alloc(std::max<int64_t>(tot, 1));
+  tri_diag_inv_kernel<<<dim3((maxm + 31) / 32, mats.size()), 64, 0, s>>>(dm.p, doff.p, linv.p);
+  VB_CHECK_LAUNCH();
   for (auto &op : ops) {
     if (op.first == 0) {
       const int J = op.second;
       dim3 grid((32 * J + 32 + TRI_COLS - 1) / TRI_COLS, mats.size());
-      trsm_diag_kernel<<<grid, TRI_COLS, 0, s>>>(dm.p, J);
+      trsm_diag_kernel<<<grid, TRI_COLS, 0, s>>>(dm.p, J, doff.p, linv.p);
       VB_CHECK_LAUNCH();
     } else {
       plan.run(op.second, s);

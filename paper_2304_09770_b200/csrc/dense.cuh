@@ -28,7 +28,6 @@ struct GemmPlan {
   std::vector<std::array<int, 4>> lntile;                  // after upload: tiles (= grid size)
   std::vector<std::vector<int>> dense;        // per launch: large problems run as 2D grids
   std::vector<char> scaled;                   // per launch: some tile-list problem has d != null
-  std::vector<std::array<char, 4>> novec;     // per launch and class: some operand not 16-byte aligned
   bool allow_kz = false;                      // honour GemmProb.kz_on regardless of VB_KZ (vb_debug_gemm)
   DBuf<GemmProb> d_probs;
   DBuf<int4> d_tiles;
@@ -37,7 +36,6 @@ struct GemmPlan {
     ltcount.push_back({0, 0, 0, 0});
     dense.push_back({});
     scaled.push_back(0);
-    novec.push_back({0, 0, 0, 0});
     return ltiles.size() - 1;
   }
   void add(const GemmProb &p);             // adds tiles to the current launch

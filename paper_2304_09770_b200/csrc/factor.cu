@@ -73,7 +73,7 @@ __global__ void assemble_kernel(const SubDev *__restrict__ subs, const int *__re
   const double *c = cvec + S.off_P;
   const double *m = mvec + S.off_P;
   double *b0 = b0all + S.off_G;
-  const int64_t ld = S.n;
+  const int64_t ld = S.ldk;
   const int nI = S.nI, nP = S.nP, nG = S.nG;
   const int stride = nvmax + np;
   for (int q = S.cell_begin; q < S.cell_end; ++q) {
@@ -233,8 +233,8 @@ __global__ void deluxe_gather_kernel(const SlotDev *__restrict__ slots, const Su
                                      const double *__restrict__ Kall, double *sidebuf) {
   const SlotDev s = slots[blockIdx.y];
   const SubDev S = subs[s.sub];
-  const double *ST = Kall + S.off_K + (int64_t)S.nD * (S.n + 1);
-  const int64_t ld = S.n;
+  const double *ST = Kall + S.off_K + (int64_t)S.nD * (S.ldk + 1);
+  const int64_t ld = S.ldk;
   const int nd = s.nd;
   double *out = sidebuf + s.off_side;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nd * nd; idx += gridDim.x * blockDim.x) {
@@ -307,12 +307,12 @@ __global__ void coarse_piece_kernel(const SubDev *__restrict__ subs, const doubl
                                     const double *__restrict__ b0T, const int64_t *__restrict__ poff, double *buf) {
   const SubDev S = subs[blockIdx.y];
   const int npi = S.npi;
-  const double *Sc = Kall + S.off_K + (int64_t)(S.nD + S.nd) * (S.n + 1);
+  const double *Sc = Kall + S.off_K + (int64_t)(S.nD + S.nd) * (S.ldk + 1);
   double *o = buf + poff[blockIdx.y];
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < npi * npi + npi; idx += gridDim.x * blockDim.x) {
     if (idx < npi * npi) {
       const int a = idx % npi, b = idx / npi;
-      o[idx] = a >= b ? Sc[a + (int64_t)b * S.n] : Sc[b + (int64_t)a * S.n];
+      o[idx] = a >= b ? Sc[a + (int64_t)b * S.ldk] : Sc[b + (int64_t)a * S.ldk];
     } else {
       o[idx] = b0T[S.off_Pi + (idx - npi * npi)];
     }
@@ -461,7 +461,7 @@ static void stage_dirichlet(vb_ctx *c) {
   std::vector<MatDesc> mats(N);
   for (int i = 0; i < N; ++i) {
     const SubDev &S = c->h_sub[i];
-    mats[i] = MatDesc{c->d_K.p + S.off_K, S.n, S.n, S.nD};
+    mats[i] = MatDesc{c->d_K.p + S.off_K, S.n, S.ldk, S.nD};
     mats[i].npos = S.nI;        // [u_I | p (Q_I, augmented) | Gamma]: velocity > 0, pressure < 0
   }
   STAGE_T("  assembly");
@@ -471,7 +471,7 @@ static void stage_dirichlet(vb_ctx *c) {
   std::vector<MatDesc> sg(N);
   for (int i = 0; i < N; ++i) {
     const SubDev &S = c->h_sub[i];
-    sg[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.nG, S.n, 0};
+    sg[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1), S.nG, S.ldk, 0};
   }
   symmetrize_lower_batched(sg, s);
   // ---------------- Dirichlet solve operator for B0/B8 as a packed GEMV operand:
@@ -481,7 +481,7 @@ static void stage_dirichlet(vb_ctx *c) {
     std::vector<int64_t> offWD(N), offKDi(N);
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      offWD[i] = lenWD; lenWD += (int64_t)S.nD * S.nD;
+      offWD[i] = lenWD; lenWD += (int64_t)ld4(S.nD) * S.nD;
       offKDi[i] = lenKDi; lenKDi += packed_size(S.nD);
       c->h_sub[i].off_KDi = offKDi[i];
     }
@@ -491,7 +491,7 @@ static void stage_dirichlet(vb_ctx *c) {
     std::vector<TriDesc> td(N);
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      td[i] = TriDesc{c->d_K.p + S.off_K, S.n, WD.p + offWD[i], S.nD, S.nD};
+      td[i] = TriDesc{c->d_K.p + S.off_K, S.ldk, WD.p + offWD[i], ld4(S.nD), S.nD};
     }
     tri_inverse_batched(td, s);
     STAGE_T("  L_DD^-1");
@@ -500,7 +500,7 @@ static void stage_dirichlet(vb_ctx *c) {
       std::vector<DiagDesc> dd;
       for (int i = 0; i < N; ++i) {
         const SubDev &S = c->h_sub[i];
-        dd.push_back(DiagDesc{c->d_K.p + S.off_K, S.n, S.off_Dn, S.nD, 0});
+        dd.push_back(DiagDesc{c->d_K.p + S.off_K, S.ldk, S.off_Dn, S.nD, 0});
       }
       recip_diag_batched(dd, dD.p, s);
     }
@@ -511,10 +511,10 @@ static void stage_dirichlet(vb_ctx *c) {
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
       GemmProb q{};
-      q.A = WD.p + offWD[i]; q.lda = S.nD; q.transA = 1;
+      q.A = WD.p + offWD[i]; q.lda = ld4(S.nD); q.transA = 1;
       q.d = dD.p + S.off_Dn; q.dstride = 1;
-      q.B = WD.p + offWD[i]; q.ldb = S.nD;
-      q.C = c->d_K.p + S.off_K; q.ldc = S.n;
+      q.B = WD.p + offWD[i]; q.ldb = ld4(S.nD);
+      q.C = c->d_K.p + S.off_K; q.ldc = S.ldk;
       q.M = q.N = q.K = S.nD; q.alpha = 1.0; q.beta = 0.0; q.lower = 1;
       q.kz_on = 1;   // W lower triangular: only k >= max(i, j) contributes (site bit 1)
       plan.add(q);
@@ -526,7 +526,7 @@ static void stage_dirichlet(vb_ctx *c) {
     std::vector<PackDesc> pk(N);
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      pk[i] = PackDesc{c->d_K.p + S.off_K, S.nD, S.n, c->d_KDi.p + offKDi[i]};
+      pk[i] = PackDesc{c->d_K.p + S.off_K, S.nD, S.ldk, c->d_KDi.p + offKDi[i]};
     }
     pack_tiles_batched(pk, s);
     c->len_KDi = lenKDi;
@@ -577,16 +577,16 @@ static void stage_interface(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumb
     int l0 = plan.begin_launch();
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      double *SG = c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1);
+      double *SG = c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1);
       for (int q = S.slot_begin; q < S.slot_end; ++q) {
         const SlotDev &sl = c->h_slot[c->h_sub_slots[q]];
         const double *Te = c->d_T.p + sl.off_T;
         for (int part = 0; part < 2; ++part) {
           GemmProb p{};
-          p.A = SG + (int64_t)sl.offG * S.n; p.lda = S.n;
+          p.A = SG + (int64_t)sl.offG * S.ldk; p.lda = S.ldk;
           p.B = Te + (part ? (int64_t)sl.nd * sl.n : 0); p.ldb = sl.n;
           int oc = part ? S.nd + sl.offPi : sl.offD;
-          p.C = X.p + S.off_X + (int64_t)oc * S.nG; p.ldc = S.nG;
+          p.C = X.p + S.off_X + (int64_t)oc * ld4(S.nG); p.ldc = ld4(S.nG);
           p.M = S.nG; p.N = part ? sl.r : sl.nd; p.K = sl.n; p.alpha = 1.0; p.beta = 0.0;
           plan.add(p);
         }
@@ -595,16 +595,16 @@ static void stage_interface(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumb
     int l1 = plan.begin_launch();
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      double *ST = c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1);
+      double *ST = c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1);
       for (int q = S.slot_begin; q < S.slot_end; ++q) {
         const SlotDev &sl = c->h_slot[c->h_sub_slots[q]];
         const double *Te = c->d_T.p + sl.off_T;
         for (int part = 0; part < 2; ++part) {
           GemmProb p{};
           p.A = Te + (part ? (int64_t)sl.nd * sl.n : 0); p.lda = sl.n; p.transA = 1;
-          p.B = X.p + S.off_X + sl.offG; p.ldb = S.nG;
+          p.B = X.p + S.off_X + sl.offG; p.ldb = ld4(S.nG);
           int orow = part ? S.nd + sl.offPi : sl.offD;
-          p.C = ST + orow; p.ldc = S.n;
+          p.C = ST + orow; p.ldc = S.ldk;
           p.M = part ? sl.r : sl.nd; p.N = S.nG; p.K = sl.n; p.alpha = 1.0; p.beta = 0.0;
           plan.add(p);
         }
@@ -621,7 +621,7 @@ static void stage_interface(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumb
     std::vector<PackDesc> pk(N);
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      pk[i] = PackDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.nG, S.n, c->d_STp.p + S.off_STp};
+      pk[i] = PackDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1), S.nG, S.ldk, c->d_STp.p + S.off_STp};
     }
     pack_tiles_batched(pk, s);
   }
@@ -660,20 +660,20 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
   // (leading dimension n), whose L_DD is consumed by the triangular inverse into X
   DBuf<double> X, Wbuf, dinv;
   X.alloc(c->len_X);
-  auto Yp = [&](const SubDev &S) { return c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1); };
+  auto Yp = [&](const SubDev &S) { return c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1); };
   Wbuf.alloc(std::max<int64_t>(c->len_sum, 1));
   // ---------------- A3: partial LDL^T of S_T eliminating the dual block -> S_c trailing
   c->d_info.zero(s);
   for (int i = 0; i < N; ++i) {
     const SubDev &S = c->h_sub[i];
-    mats[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.nG, S.n, S.nd};
+    mats[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1), S.nG, S.ldk, S.nd};
     mats[i].npos = S.nd;        // S_DD is SPD (the primal constraints remove the rigid modes)
   }
   ldl_partial_batched(mats, c->d_info.p, s);
   check_info(c, N, "dual Schur LDL^T (A3)", &c->sub_gid, "subdomain");
   for (int i = 0; i < N; ++i) {
     const SubDev &S = c->h_sub[i];
-    sg[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)(S.nD + S.nd) * (S.n + 1), S.npi, S.n, 0};
+    sg[i] = MatDesc{c->d_K.p + S.off_K + (int64_t)(S.nD + S.nd) * (S.ldk + 1), S.npi, S.ldk, 0};
   }
   symmetrize_lower_batched(sg, s);
   // W = L_DD^-1 (in X), Y = W^T D^-1 W = S_DD^-1, Phi = -W^T L_PiD^T
@@ -682,7 +682,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     std::vector<TriDesc> td(N);
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      td[i] = TriDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.n, X.p + S.off_X, S.nd, S.nd};
+      td[i] = TriDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1), S.ldk, X.p + S.off_X, ld4(S.nd), S.nd};
     }
     tri_inverse_batched(td, s);
   }
@@ -691,7 +691,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     std::vector<DiagDesc> dd;
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      if (S.nd) dd.push_back(DiagDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), S.n, S.off_Dv, S.nd, 0});
+      if (S.nd) dd.push_back(DiagDesc{c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1), S.ldk, S.off_Dv, S.nd, 0});
     }
     recip_diag_batched(dd, dinv.p, s);
   }
@@ -703,16 +703,16 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
       GemmProb p{};
-      p.A = X.p + S.off_X; p.lda = S.nd; p.transA = 1;
+      p.A = X.p + S.off_X; p.lda = ld4(S.nd); p.transA = 1;
       p.d = dinv.p + S.off_Dv; p.dstride = 1;
-      p.B = X.p + S.off_X; p.ldb = S.nd;
-      p.C = Yp(S); p.ldc = S.n;
+      p.B = X.p + S.off_X; p.ldb = ld4(S.nd);
+      p.C = Yp(S); p.ldc = S.ldk;
       p.M = p.N = p.K = S.nd; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
       p.kz_on = 2;   // W lower triangular (site bit 2)
       plan.add(p);
       GemmProb q{};
-      q.A = X.p + S.off_X; q.lda = S.nd; q.transA = 1;
-      q.B = c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1) + S.nd; q.ldb = S.n; q.transB = 1;
+      q.A = X.p + S.off_X; q.lda = ld4(S.nd); q.transA = 1;
+      q.B = c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1) + S.nd; q.ldb = S.ldk; q.transB = 1;
       q.C = c->d_Phi.p + S.off_Phi; q.ldc = S.nd;
       q.M = S.nd; q.N = S.npi; q.K = S.nd; q.alpha = -1.0; q.beta = 0.0;
       q.kz_on = 4; q.kzB = -(1 << 30);   // W^T: only k >= i contributes (site bit 4)
@@ -811,7 +811,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     std::vector<MatDesc> ym;
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      if (S.nd) ym.push_back(MatDesc{Yp(S), S.nd, S.n, 0});
+      if (S.nd) ym.push_back(MatDesc{Yp(S), S.nd, S.ldk, 0});
     }
     symmetrize_lower_batched(ym, s);
     DBuf<double> PhiH;
@@ -825,8 +825,8 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
         const SubDev &S = c->h_sub[sl.sub];
         GemmProb p{};
         p.A = c->d_Dlx.p + sl.off_Dlx; p.lda = sl.nd;
-        p.B = Yp(S) + sl.offD; p.ldb = S.n;
-        p.C = X.p + S.off_X + sl.offD; p.ldc = S.nd;
+        p.B = Yp(S) + sl.offD; p.ldb = S.ldk;
+        p.C = X.p + S.off_X + sl.offD; p.ldc = ld4(S.nd);
         p.M = sl.nd; p.N = S.nd; p.K = sl.nd; p.alpha = 1.0; p.beta = 0.0;
         plan.add(p);
         if (S.npi) {
@@ -844,9 +844,9 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
         if (!sl.nd) continue;
         const SubDev &S = c->h_sub[sl.sub];
         GemmProb p{};
-        p.A = X.p + S.off_X + (int64_t)sl.offD * S.nd; p.lda = S.nd;
+        p.A = X.p + S.off_X + (int64_t)sl.offD * ld4(S.nd); p.lda = ld4(S.nd);
         p.B = c->d_Dlx.p + sl.off_Dlx; p.ldb = sl.nd; p.transB = 1;
-        p.C = Yp(S) + (int64_t)sl.offD * S.n; p.ldc = S.n;
+        p.C = Yp(S) + (int64_t)sl.offD * S.ldk; p.ldc = S.ldk;
         p.M = S.nd; p.N = sl.nd; p.K = sl.nd; p.alpha = 1.0; p.beta = 0.0;
         plan.add(p);
       }
@@ -863,7 +863,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     std::vector<PackDesc> pk(N);
     for (int i = 0; i < N; ++i) {
       const SubDev &S = c->h_sub[i];
-      pk[i] = PackDesc{Yp(S), S.nd, S.n, c->d_SDi.p + S.off_SDi};
+      pk[i] = PackDesc{Yp(S), S.nd, S.ldk, c->d_SDi.p + S.off_SDi};
     }
     pack_tiles_batched(pk, s);
   }
@@ -920,7 +920,8 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     if (pimap.empty()) pimap.push_back(0);
     dpimap.upload(pimap, s);
     DBuf<double> Kc, Wc, dc, gvol;
-    Kc.alloc(Nc * Nc);
+    const int64_t ldC = ld4((int)Nc);   // 32-byte aligned columns (16-byte copies in the DMMA GEMM)
+    Kc.alloc(ldC * Nc);
     Kc.zero(s);
     std::vector<std::vector<int>> colors(c->ncolors);
     for (int g = 0; g < Ng; ++g) colors[c->gsub_color[g]].push_back(g);
@@ -929,7 +930,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
       DBuf<int> dcol;
       dcol.upload(col, s);
       coarse_assemble_kernel2<<<dim3(8, col.size()), 256, 0, s>>>(dcol.p, dpoff.p, dgnpi.p, dpimoff.p, dpimap.p,
-                                                                 pieces, Kc.p, Nc, c->NPi_g);
+                                                                 pieces, Kc.p, ldC, c->NPi_g);
       VB_STAGE();
       sync(c);
     }
@@ -939,28 +940,28 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     for (int g = 0; g < Ng; ++g) volO += c->gsub_vol[g];
     gvol.upload(c->gsub_vol, s);
     coarse_augment_kernel<<<(int)std::min<int64_t>(((int64_t)Ng * Ng + 255) / 256, 4096), 256, 0, s>>>(
-        gvol.p, Ng, 1.0 / (nubar * volO), Kc.p, Nc, c->NPi_g);
+        gvol.p, Ng, 1.0 / (nubar * volO), Kc.p, ldC, c->NPi_g);
     VB_STAGE();
     STAGE_T("  coarse pieces + assembly (C4)");
     c->d_info.zero(s);
-    std::vector<MatDesc> cm{MatDesc{Kc.p, (int)Nc, (int)Nc, (int)Nc}};
+    std::vector<MatDesc> cm{MatDesc{Kc.p, (int)Nc, (int)ldC, (int)Nc}};
     cm[0].npos = (int)c->NPi_g;   // [u_Pi | p_0 (augmented)]: velocity > 0, pressure < 0
     ldl_partial_batched(cm, c->d_info.p, s);
     check_info(c, 1, "coarse saddle LDL^T (A5)");
     STAGE_T("  coarse LDL^T");
-    Wc.alloc(Nc * Nc);
+    Wc.alloc(ldC * Nc);
     Wc.zero(s);
-    tri_inverse_batched({TriDesc{Kc.p, (int)Nc, Wc.p, (int)Nc, (int)Nc}}, s);
+    tri_inverse_batched({TriDesc{Kc.p, (int)ldC, Wc.p, (int)ldC, (int)Nc}}, s);
     dc.alloc(Nc);
-    recip_diag_kernel<<<(Nc + 255) / 256, 256, 0, s>>>(Kc.p, Nc, Nc, dc.p);
+    recip_diag_kernel<<<(Nc + 255) / 256, 256, 0, s>>>(Kc.p, ldC, Nc, dc.p);
     VB_STAGE();
     if (c->nranks == 1) {
       // (K_c)^-1 = W^T D^-1 W (lower), packed
       GemmPlan plan;
       int l0 = plan.begin_launch();
       GemmProb p{};
-      p.A = Wc.p; p.lda = Nc; p.transA = 1; p.d = dc.p; p.dstride = 1;
-      p.B = Wc.p; p.ldb = Nc; p.C = Kc.p; p.ldc = Nc;
+      p.A = Wc.p; p.lda = ldC; p.transA = 1; p.d = dc.p; p.dstride = 1;
+      p.B = Wc.p; p.ldb = ldC; p.C = Kc.p; p.ldc = ldC;
       p.M = p.N = p.K = Nc; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
       p.kz_on = 8;   // W lower triangular (site bit 8)
       plan.add(p);
@@ -968,7 +969,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
       plan.run(l0, s);
       sync(c);
       c->d_Kcp.alloc(packed_size(Nc));
-      pack_tiles_batched({PackDesc{Kc.p, (int)Nc, (int)Nc, c->d_Kcp.p}}, s);
+      pack_tiles_batched({PackDesc{Kc.p, (int)Nc, (int)ldC, c->d_Kcp.p}}, s);
     } else {
       // distributed coarse solve: this rank computes and keeps only the tile rows [tlo, thi) of the
       // packed symmetric inverse (a contiguous slice of the 1-rank layout, split by tile count), from
@@ -995,8 +996,8 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
         GemmPlan plan;
         int l0 = plan.begin_launch();
         GemmProb p{};
-        p.A = Wc.p + lo * Nc + lo; p.lda = Nc; p.transA = 1; p.d = dc.p + lo; p.dstride = 1;
-        p.B = Wc.p + lo; p.ldb = Nc; p.C = Kr.p; p.ldc = mine;
+        p.A = Wc.p + lo * ldC + lo; p.lda = ldC; p.transA = 1; p.d = dc.p + lo; p.dstride = 1;
+        p.B = Wc.p + lo; p.ldb = ldC; p.C = Kr.p; p.ldc = mine;
         p.M = mine; p.N = hi; p.K = Nc - lo; p.alpha = 1.0; p.beta = 0.0;
         p.kz_on = 16; p.kzB = (int)-lo;   // (site bit 16)   // W(lo + k, lo + i) = 0 for k < i, W(lo + k, j) = 0 for k < j - lo
         plan.add(p);
@@ -1034,7 +1035,7 @@ void factor_device(vb_ctx *c) {
     SG.alloc(c->len_X);
     for (int i = 0; i < c->N; ++i) {
       const SubDev &S = c->h_sub[i];
-      VB_CUDA(cudaMemcpy2DAsync(SG.p + S.off_X, S.nG * 8, c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), (size_t)S.n * 8,
+      VB_CUDA(cudaMemcpy2DAsync(SG.p + S.off_X, S.nG * 8, c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1), (size_t)S.ldk * 8,
                                 S.nG * 8, S.nG, cudaMemcpyDeviceToDevice, s));
     }
     stage_interface(c, sidebuf, sumbuf);
@@ -1043,7 +1044,7 @@ void factor_device(vb_ctx *c) {
     stage_time(c, "adaptive (A6)");
     for (int i = 0; i < c->N; ++i) {
       const SubDev &S = c->h_sub[i];
-      VB_CUDA(cudaMemcpy2DAsync(c->d_K.p + S.off_K + (int64_t)S.nD * (S.n + 1), (size_t)S.n * 8, SG.p + S.off_X, S.nG * 8,
+      VB_CUDA(cudaMemcpy2DAsync(c->d_K.p + S.off_K + (int64_t)S.nD * (S.ldk + 1), (size_t)S.ldk * 8, SG.p + S.off_X, S.nG * 8,
                                 S.nG * 8, S.nG, cudaMemcpyDeviceToDevice, s));
     }
     sync(c);

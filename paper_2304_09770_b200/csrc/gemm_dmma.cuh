@@ -10,8 +10,9 @@
 //    [k][m]; transposed: [m][k]; B not transposed: [n][k]; transposed: [k][n]) with a pad of 4
 //    doubles, so both the 16-byte global->shared copies and the fragment reads (two 16-lane
 //    phases of 8-byte loads) are free of bank conflicts;
-//  * 16-byte cp.async (VEC) when every operand column of the launch is 16-byte aligned, 8-byte
-//    otherwise; ragged edges zero-filled through the copy's source size;
+//  * 16-byte cp.async (VEC) for problems whose operand columns are 16-byte aligned, pairs of
+//    8-byte copies with the same thread mapping for the others (decided per CTA); ragged edges
+//    zero-filled through the copy's source size;
 //  * the diagonal scaling multiplies whichever fragment set is smaller per thread.
 #pragma once
 #include <cstdint>
@@ -85,9 +86,11 @@ struct CopyPlan {
 // Issue the copies of one operand slab.  g: global element (c0, o0) of this thread's first chunk
 // for this slab; ld: stride between "rows" o; c_left / o_left: extents still inside the matrix
 // measured from the tile origin; s: the stage's shared tile.
+// With VEC, `al` (uniform per CTA) says whether this problem's operand columns are 16-byte
+// aligned; if not, each 2-element chunk goes as two 8-byte copies (same thread mapping).
 template <int CONTIG, int OTHER, int THREADS, bool VEC>
 __device__ __forceinline__ void copy_tile(double *s, const double *g, const double *safe, int64_t ld, int tid,
-                                          int c_left, int o_left) {
+                                          int c_left, int o_left, bool al = true) {
   using P = CopyPlan<CONTIG, OTHER, THREADS, VEC>;
   const int c = P::c0(tid), o = P::o0(tid);
   constexpr int LD = CONTIG + 4;
@@ -97,8 +100,13 @@ __device__ __forceinline__ void copy_tile(double *s, const double *g, const doub
     const double *src = g + (int64_t)(q * P::ROW_STEP) * ld;
     double *dst = s + oo * LD + c;
     if (VEC) {
-      int bytes = (oo < o_left) ? 8 * max(0, min(2, c_left - c)) : 0;
-      cp16(dst, bytes ? src : safe, bytes);
+      const int nvalid = (oo < o_left) ? max(0, min(2, c_left - c)) : 0;
+      if (al) {
+        cp16(dst, nvalid ? src : safe, 8 * nvalid);
+      } else {
+        cp8(dst, nvalid > 0 ? src : safe, nvalid > 0 ? 8 : 0);
+        cp8(dst + 1, nvalid > 1 ? src + 1 : safe, nvalid > 1 ? 8 : 0);
+      }
     } else {
       const int bytes = (oo < o_left && c < c_left) ? 8 : 0;
       cp8(dst, bytes ? src : safe, bytes);
@@ -173,6 +181,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm2_kernel(const GemmPr
   const double *gb = TB ? P.B + (n0 + bc) + (int64_t)(kb + bo) * P.ldb : P.B + (kb + bc) + (int64_t)(n0 + bo) * P.ldb;
   const int64_t astep = TA ? BK : (int64_t)BK * P.lda, bstep = TB ? (int64_t)BK * P.ldb : BK;
   const double *dv = SCALED ? P.d : nullptr;
+  // 16-byte copies need 16-byte aligned columns (aligned base, even leading dimension)
+  const bool alA = ((reinterpret_cast<uintptr_t>(P.A) & 15) == 0) && !(P.lda & 1);
+  const bool alB = ((reinterpret_cast<uintptr_t>(P.B) & 15) == 0) && !(P.ldb & 1);
 
   auto stage_ptr = [&](int st) { return g2_smem + st * S::STAGE; };
   auto issue = [&](int st, int k0) {   // slab starting at k0 (k0 - kb a multiple of BK)
@@ -180,13 +191,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm2_kernel(const GemmPr
     const int k_left = K - k0;
     const int64_t ks = (k0 - kb) / BK;
     if (TA)
-      copy_tile<ACONT, AOTH, T, VEC>(sA, ga + ks * astep, P.A, P.lda, tid, k_left - 0, rows_left);
+      copy_tile<ACONT, AOTH, T, VEC>(sA, ga + ks * astep, P.A, P.lda, tid, k_left, rows_left, alA);
     else
-      copy_tile<ACONT, AOTH, T, VEC>(sA, ga + ks * astep, P.A, P.lda, tid, rows_left, k_left);
+      copy_tile<ACONT, AOTH, T, VEC>(sA, ga + ks * astep, P.A, P.lda, tid, rows_left, k_left, alA);
     if (TB)
-      copy_tile<BCONT, BOTH, T, VEC>(sB, gb + ks * bstep, P.B, P.ldb, tid, cols_left, k_left);
+      copy_tile<BCONT, BOTH, T, VEC>(sB, gb + ks * bstep, P.B, P.ldb, tid, cols_left, k_left, alB);
     else
-      copy_tile<BCONT, BOTH, T, VEC>(sB, gb + ks * bstep, P.B, P.ldb, tid, k_left, cols_left);
+      copy_tile<BCONT, BOTH, T, VEC>(sB, gb + ks * bstep, P.B, P.ldb, tid, k_left, cols_left, alB);
     if (SCALED && tid < BK) {
       const bool ok = scaled && tid < k_left;
       cp8(sD + tid, ok ? dv + (int64_t)(k0 + tid) * P.dstride : P.A, ok ? 8 : 0);

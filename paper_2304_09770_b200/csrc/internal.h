@@ -124,6 +124,7 @@ struct GemmProb {
 // tile row-major (diagonal tiles hold the full symmetric block); the tiles of the last tile row
 // store only its rv = n - 32 (nt - 1) valid rows, so no padding rows are streamed.
 HD_INLINE int64_t ptile_row_start(int64_t I) { return 1024 * (I * (I + 1) / 2); }
+HD_INLINE int ld4(int n) { return (n + 3) & ~3; }   // leading dimensions with 32-byte aligned columns
 HD_INLINE int64_t ptile_off(int n, int I, int J) {   // offset of tile (I, J), J <= I
   const int nt = (n + 31) / 32;
   const int64_t rows = (I == nt - 1) ? n - 32 * (nt - 1) : 32;
@@ -183,8 +184,8 @@ struct SubDev {
   int nI, nP, nG, nD, n, nd, npi;
   int cell_begin, cell_end;   // into sub_cells
   int slot_begin, slot_end;   // into the subdomain-major slot index list
-  int pad;
-  int64_t off_K;              // dense n x n (column-major, ld = n)
+  int ldk;                    // leading dimension of the dense subdomain matrix: n rounded up to 4
+  int64_t off_K;              // dense n x n (column-major, ld = ldk; 32-byte aligned columns)
   int64_t off_ST;             // dense nG x nG: S_T, then its partial LDL^T
   int64_t off_STp;            // packed tiles of S_T
   int64_t off_SDi;            // packed tiles of S_DD^-1

@@ -189,11 +189,13 @@ def test_c3_full_size_properties():
     dofs = GlobalDofs(prob.mesh, 3)
     assert ctx.n_vel == dofs.n_free_vel and ctx.n_free == dofs.n_free_vel + dofs.npres
     ei = EdgeIndex(mesh_edges(prob.mesh), prob.mesh.n_vertices)
+    worst = 0.0
     for K in np.random.default_rng(3).choice(prob.mesh.n_cells, 6, replace=False):
         op = ElementOps(prob.mesh, int(K), ei, 3, prob.nu_cell[K])
         A, B = ctx.element_matrices(int(K))
-        assert np.abs(A - op.A).max() <= 1e-11 * np.abs(op.A).max()
-        assert np.abs(B - op.B).max() <= 1e-11 * np.abs(op.B).max()
+        worst = max(worst, np.abs(A - op.A).max() / np.abs(op.A).max(), np.abs(B - op.B).max() / np.abs(op.B).max())
+    print("c3 sampled element matrices: worst relative entry difference %.2e" % worst)
+    assert worst <= 1e-12, worst
     ctx.factor()
     st = ctx.stats()
     assert st["n_dofs_paper"] == dofs.n_dofs_paper()
