@@ -252,6 +252,15 @@ void build_transformed_maps(vb_ctx *c) {
 }
 
 // ------------------------------------------------------------------ common setup
+// VB_SETUP_TIMES=1: wall time of each setup stage on stderr
+static void setup_time(const char *what, double &t) {
+  static const bool on = getenv("VB_SETUP_TIMES") && atoi(getenv("VB_SETUP_TIMES"));
+  if (!on) return;
+  const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  fprintf(stderr, "[vb setup] %-28s %8.3f s\n", what, now - t);
+  t = now;
+}
+
 static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, int32_t nsub,
                          const int32_t *sub_rank, const vb_constraints *cons, const double *nu,
                          const vb_dist *dist) {
@@ -274,10 +283,13 @@ static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, i
     else c->comm = make_nccl_comm(c->rank, c->nranks, dist->nccl_unique_id, c->device);
     VB_REQUIRE(c->comm->nranks == c->nranks, VB_EINVAL, "communicator size differs from nranks");
   }
+  double ts = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
   build_topology(c, m);
+  setup_time("topology", ts);
   c->nu.assign(nu, nu + c->nK);
   for (int64_t K = 0; K < c->nK; ++K) VB_REQUIRE(c->nu[K] > 0, VB_EINVAL, "viscosity must be positive (P:108)");
   build_subdomains(c, cell_sub, nsub, c->nranks > 1 ? sub_rank : nullptr);
+  setup_time("subdomains / DOF maps", ts);
   cudaStream_t s = c->stream;
   // device copies of the LOCAL cells (topology, viscosity, dof maps); vertices and the dof status are global
   std::vector<int> topo((size_t)c->nKl * TOPO_STRIDE);
@@ -298,9 +310,12 @@ static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, i
   c->d_vel2free.upload(c->vel2free, s);
   c->d_cell_l2g.upload(l2g, s);
   c->d_cell_gid.upload(c->cell_gid, s);
+  VB_CUDA(cudaStreamSynchronize(s));
+  setup_time("local copies + upload", ts);
   cell_geometry_device(c);
   c->d_cellgeo.download(c->cellgeo, s);
   VB_CUDA(cudaStreamSynchronize(s));
+  setup_time("cell geometry (device)", ts);
 }
 
 }  // namespace vb
@@ -380,8 +395,12 @@ vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n
   try {
     double t0 = now_s();
     common_setup(c, mesh, cell_subdomain, n_subdomains, subdomain_rank, cons, cell_viscosity, dist);
+    double ts = now_s();
     element_matrices_device(c);
+    VB_CUDA(cudaStreamSynchronize(c->stream));
+    setup_time("element matrices K9 (device)", ts);
     layout_phase_a(c);
+    setup_time("layout", ts);
     c->t_setup = now_s() - t0;
     c->state = 1;
   } catch (const Error &e) {
