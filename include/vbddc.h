@@ -151,7 +151,8 @@ vb_status vb_build_rhs(vb_ctx *ctx, const vb_problem *prob, double *rhs_dev);
  * cells; for one rank, all free DOFs in global order); x gets the full solution (interior
  * back-substitution, pressure with zero global mean).  maxit <= 0 means 2000.
  * The pressure rows of rhs must be flux-compatible, sum_i g0_i = 0 (integral of the pressure rhs
- * against constants): |sum_i g0_i| > 1e-8 sum_i |g0_i| returns VB_EINVAL; within that
+ * against constants): |sum_i g0_i| > 1e-8 (sum_j |c_j g_pj| + ||r0||_2) returns VB_EINVAL
+ * (c = DOFs of the constant pressure, g_p = the pressure rows, r0 = the condensed rhs); within that
  * bound the rounding is removed (reading A30).  VB_EBREAKDOWN (p^T S p <= 0 or
  * r^T z <= 0) and VB_ENOTCONV (maxit) leave the last iterate in x and fill the report.
  * Collective: every rank calls it with the same rtol/maxit. */

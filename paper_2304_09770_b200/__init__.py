@@ -267,7 +267,9 @@ class Context:
         return ids
 
     def cell_local_dofs(self, cell):
-        v = np.zeros(512, np.int64); p = np.zeros(64, np.int64)
+        if not hasattr(self, "_nv_max"):
+            self._nv_max = int(self.stats()["nv_max"])
+        v = np.zeros(self._nv_max, np.int64); p = np.zeros(64, np.int64)
         nv, npr = ctypes.c_int32(), ctypes.c_int32()
         self._check(_vb_cell_local_dofs(self._h, int(cell), _ptr(v, ctypes.c_int64), ctypes.byref(nv),
                                         _ptr(p, ctypes.c_int64), ctypes.byref(npr)))

@@ -150,6 +150,9 @@ void build_topology(vb_ctx *c, const vb_mesh *m) {
     std::sort(es.begin(), es.end()); es.erase(std::unique(es.begin(), es.end()), es.end());
     VB_REQUIRE((int)vs.size() <= MAXV && (int)es.size() <= MAXE, VB_EINVAL,
                "cell " + std::to_string(K) + " exceeds the supported vertex/edge count");
+    int ntri = 0;
+    for (auto &fs : fl) ntri += (int)(c->face_ptr[fs.first + 1] - c->face_ptr[fs.first]) - 2;
+    VB_REQUIRE(ntri <= MAXT, VB_EINVAL, "cell " + std::to_string(K) + " exceeds the supported fan-triangle count");
     int *T = &c->cell_topo[(size_t)K * TOPO_STRIDE];
     T[0] = vs.size(); T[1] = es.size(); T[2] = nf;
     for (size_t i = 0; i < vs.size(); ++i) T[TOPO_V + i] = (int)vs[i];

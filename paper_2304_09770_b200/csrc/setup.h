@@ -3,10 +3,13 @@
 
 namespace vb {
 // Local cell topology packing (one int block of TOPO_STRIDE per cell).
-constexpr int MAXV = 8;      // vertices per cell (hexahedra, jittered/triangulated hexahedra)
-constexpr int MAXE = 18;     // edges per cell
-constexpr int MAXF = 12;     // faces per cell
-constexpr int MAXL = 4;      // vertices per face loop
+// General polyhedra: hexahedra, triangulated jittered hexahedra and centroidal Voronoi
+// cells (up to ~17 faces, 30 vertices, 45 edges and 8-gon faces on the CVT family).
+constexpr int MAXV = 40;     // vertices per cell
+constexpr int MAXE = 64;     // edges per cell
+constexpr int MAXF = 24;     // faces per cell
+constexpr int MAXL = 10;     // vertices per face loop
+constexpr int MAXT = 96;     // fan triangles per cell (sum over faces of loop length - 2)
 constexpr int FACE_STRIDE = 2 + 3 * MAXL;    // sign, len, loop vertices, loop edges, forward flags
 constexpr int TOPO_V = 3;
 constexpr int TOPO_E = TOPO_V + MAXV;

@@ -1679,7 +1679,9 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   VB_CUDA(cudaMemcpyAsync(compat, c->w_dots.p + W_P0, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
   VB_CUDA(cudaStreamSynchronize(s));
   // flux compatibility of the rhs: sum_i g0_i = 0 up to rounding, else VB_EINVAL
-  VB_REQUIRE(fabs(compat[0]) <= kCompatRel * compat[1], VB_EINVAL,
+  // scale: the terms g0 is summed from, plus ||r0|| (rounding-level pressure data, e.g. a lifted trace
+  // with u.n = 0 on the boundary, makes both sides pure rounding)
+  VB_REQUIRE(fabs(compat[0]) <= kCompatRel * (compat[1] + h[4]), VB_EINVAL,
              "flux-incompatible rhs: sum_i g0_i = " + std::to_string(compat[0]) + " (sum_i |g0_i| = " +
                  std::to_string(compat[1]) + "); the pressure rows must integrate to zero against constants");
   const double r0n = h[4];

@@ -18,8 +18,8 @@ struct CellGeo {
   int ev[MAXE][2];
   double apex[3];
   int ntet;
-  short tet_face[2 * MAXF];
-  short tet_i[2 * MAXF];     // fan triangle (0, i, i+1) of the face loop
+  short tet_face[MAXT];
+  short tet_i[MAXT];         // fan triangle (0, i, i+1) of the face loop
   double vol, xc[3], h;
 };
 

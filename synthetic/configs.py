@@ -16,7 +16,7 @@ Multi-sinker (config 4; BASELINE.json configs[3]):
 """
 from dataclasses import dataclass, field
 import numpy as np
-from .mesh import hex_mesh, box_partition
+from .mesh import hex_mesh, box_partition, cvt_mesh, centroid_partition, octa_mesh
 
 
 @dataclass
@@ -115,3 +115,31 @@ def make_problem(name, seed=20230419, n=None, sub=None, k=None, dims=None, nu=1.
     return Problem(name=name, k=cfg["k"], mesh=mesh, cell_subdomain=cell_sub, sub_grid=grid,
                    nu_cell=nu_cell.astype(np.float64), kind=cfg["kind"], constraints=cons,
                    params=params)
+
+
+def make_cvt_problem(m=5, grid=(2, 2, 2), k=2, seed=20230419, lloyd=20, nu=1.0, constraints=None):
+    """The paper's CVT mesh family (Test 3 uses 125 cells): m^3 centroidal Voronoi
+    cells of [0,1]^3 (synthetic.mesh.cvt_mesh), box partition into `grid` subdomains by cell
+    generator, the manufactured solution of configs 1/2/3/5, vertex + edge + face constraints with
+    deluxe scaling, homogeneous Dirichlet data lifted."""
+    mesh = cvt_mesh(m, seed=seed, lloyd=lloyd)
+    return poly_problem(mesh, grid, k, nu, constraints, name="cvt")
+
+
+def make_octa_problem(n=3, grid=(2, 2, 2), k=2, nu=1.0, constraints=None):
+    """The paper's OCTA family (SPEC reading: clipped BCC truncated-octahedron tiling,
+    2 n^3 cells), partitioned and posed like make_cvt_problem."""
+    return poly_problem(octa_mesh(n), grid, k, nu, constraints, name="octa")
+
+
+def poly_problem(mesh, grid=(2, 2, 2), k=2, nu=1.0, constraints=None, name="poly"):
+    """A general polyhedral mesh of [0,1]^3 with generators (cvt_mesh, octa_mesh, or an imported mesh
+    given `generators` = cell centroids) posed as configs 1/2/3/5: manufactured solution,
+    vertex + edge + face constraints, deluxe scaling, box partition into `grid` by generator."""
+    cell_sub, g = centroid_partition(mesh, grid)
+    cons = dict(vertex=1, edge_avg=1, face_avg=1, face_flux=1, adaptive_tau=0.0)
+    if constraints:
+        cons.update(constraints)
+    return Problem(name=name, k=k, mesh=mesh, cell_subdomain=cell_sub, sub_grid=g,
+                   nu_cell=np.full(mesh.n_cells, float(nu)), kind="manufactured", constraints=cons,
+                   params=dict(nu=float(nu)))

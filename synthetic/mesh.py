@@ -163,3 +163,166 @@ def box_partition(mesh, sub):
     gx, gy, gz = nx // sx, ny // sy, nz // sz
     c = mesh.cell_ijk
     return ((c[:, 0] // sx) + gx * ((c[:, 1] // sy) + gy * (c[:, 2] // sz))).astype(np.int32), (gx, gy, gz)
+
+
+# ------------------------------------------------------------------ CVT (Voronoi) meshes, SURVEY f4
+def _voronoi_cells(P):
+    """Bounded Voronoi tessellation of the unit cube for generators P [N,3] (scipy.spatial.Voronoi
+    of P and its mirror images across the 6 faces: the cells of P are exactly clipped by the cube).
+    Returns (vertices [nV,3], faces [list of (loop, cell_a, cell_b)] with cell_b = -1 on the
+    boundary, loop ordered counter-clockwise about the normal pointing from cell_a to cell_b)."""
+    from scipy.spatial import Voronoi
+    N = P.shape[0]
+    mirrors = [P]
+    for d in range(3):
+        for w in (0.0, 1.0):
+            Q = P.copy()
+            Q[:, d] = 2 * w - Q[:, d]
+            mirrors.append(Q)
+    A = np.concatenate(mirrors, 0)
+    vor = Voronoi(A)
+    V = vor.vertices.copy()
+    # refine every used vertex as the point equidistant from all generators whose cells meet there
+    # (least squares over the bisector planes): Qhull's coordinates of nearly degenerate vertices
+    # are only ~1e-9 accurate, which would leave faces non-planar at that level
+    gens = {}
+    for (a, b), rv in zip(vor.ridge_points, vor.ridge_vertices):
+        if a >= N and b >= N:
+            continue
+        for v in rv:
+            if v >= 0:
+                gens.setdefault(v, set()).update((int(a), int(b)))
+    for v, g in gens.items():
+        g = sorted(g)
+        p0 = A[g[0]]
+        M = 2.0 * (A[g[1:]] - p0)
+        rhs = (A[g[1:]] ** 2).sum(1) - (p0 ** 2).sum()
+        V[v] = np.linalg.lstsq(M, rhs, rcond=None)[0]
+    V[np.abs(V) < 1e-12] = 0.0
+    V[np.abs(V - 1.0) < 1e-12] = 1.0
+    faces = []
+    for (a, b), rv in zip(vor.ridge_points, vor.ridge_vertices):
+        if a >= N and b >= N:
+            continue
+        if a >= N:
+            a, b = b, a
+        rv = [v for v in rv if v >= 0]
+        if len(rv) < 3:
+            continue
+        nrm = A[b] - A[a]
+        nrm /= np.linalg.norm(nrm)
+        X = V[rv]
+        c = X.mean(0)
+        t1 = X[0] - c
+        t1 -= (t1 @ nrm) * nrm
+        t1 /= np.linalg.norm(t1)
+        t2 = np.cross(nrm, t1)
+        ang = np.arctan2((X - c) @ t2, (X - c) @ t1)
+        loop = [rv[i] for i in np.argsort(ang)]
+        faces.append((loop, int(a), int(b) if b < N else -1))
+    return V, faces
+
+
+def _cell_centroids(V, faces, N):
+    vol = np.zeros(N); m1 = np.zeros((N, 3))
+    apex = np.zeros((N, 3)); cnt = np.zeros(N)
+    for loop, a, b in faces:
+        for cidx in (a, b):
+            if cidx >= 0:
+                apex[cidx] += V[loop].sum(0); cnt[cidx] += len(loop)
+    apex /= cnt[:, None]
+    for loop, a, b in faces:
+        for cidx, sgn in ((a, 1.0), (b, -1.0)):
+            if cidx < 0:
+                continue
+            p0 = V[loop[0]]
+            for i in range(1, len(loop) - 1):
+                p1, p2 = V[loop[i]], V[loop[i + 1]]
+                v6 = sgn * np.dot(p0 - apex[cidx], np.cross(p1 - apex[cidx], p2 - apex[cidx]))
+                vol[cidx] += v6 / 6
+                m1[cidx] += v6 / 6 * (apex[cidx] + p0 + p1 + p2) / 4
+    return m1 / vol[:, None], vol
+
+
+def cvt_mesh(m, seed=0, lloyd=20):
+    """CVT mesh of [0,1]^3 with m^3 cells (the paper's CVT family): generators
+    drawn by numpy.random.default_rng(seed).uniform(0, 1, (m^3, 3)), `lloyd` Lloyd iterations
+    (generators -> centroids of their bounded Voronoi cells), then the bounded Voronoi cells.
+    Vertices are the Voronoi vertices used by the cells (coordinates within 1e-12 of the cube
+    faces snapped onto them); faces are the ridges (planar convex polygons), interior ones stored
+    once, loops counter-clockwise about the normal out of their first cell (sign +1 there, -1 in
+    the neighbour); boundary faces are the ridges towards mirror images."""
+    rng = np.random.default_rng(seed)
+    N = m ** 3
+    P = rng.uniform(0.0, 1.0, (N, 3))
+    for _ in range(lloyd):
+        V, faces = _voronoi_cells(P)
+        P, _ = _cell_centroids(V, faces, N)
+    V, faces = _voronoi_cells(P)
+    used = sorted({v for loop, _, _ in faces for v in loop})
+    remap = {v: i for i, v in enumerate(used)}
+    xyz = V[used].astype(np.float64)
+    face_ptr = [0]; face_vtx = []; fb = []
+    cell_faces = [[] for _ in range(N)]
+    for f, (loop, a, b) in enumerate(faces):
+        face_vtx += [remap[v] for v in loop]
+        face_ptr.append(len(face_vtx))
+        fb.append(1 if b < 0 else 0)
+        cell_faces[a].append((f, 1))
+        if b >= 0:
+            cell_faces[b].append((f, -1))
+    cell_ptr = np.concatenate([[0], np.cumsum([len(c) for c in cell_faces])]).astype(np.int64)
+    cell_face = np.array([f for c in cell_faces for f, _ in c], dtype=np.int64)
+    cell_sign = np.array([s for c in cell_faces for _, s in c], dtype=np.int8)
+    mesh = PolyMesh(xyz, np.array(face_ptr, dtype=np.int64), np.array(face_vtx, dtype=np.int64), cell_ptr,
+                    cell_face, cell_sign, np.array(fb, dtype=np.uint8), None, (0, 0, 0), 1.0 / m)
+    mesh.generators = P
+    return mesh
+
+
+def centroid_partition(mesh, grid):
+    """Subdomain id per cell for an sx x sy x sz box partition of [0,1]^3 by cell generator (CVT:
+    the generator is the cell centroid), numbered lexicographically (x fastest)."""
+    sx, sy, sz = grid
+    P = mesh.generators
+    ix = np.minimum((P[:, 0] * sx).astype(int), sx - 1)
+    iy = np.minimum((P[:, 1] * sy).astype(int), sy - 1)
+    iz = np.minimum((P[:, 2] * sz).astype(int), sz - 1)
+    return (ix + sx * (iy + sy * iz)).astype(np.int32), (sx, sy, sz)
+
+
+def _voronoi_mesh(P, h):
+    """PolyMesh of the bounded Voronoi cells of generators P in [0,1]^3 (see _voronoi_cells)."""
+    N = P.shape[0]
+    V, faces = _voronoi_cells(P)
+    used = sorted({v for loop, _, _ in faces for v in loop})
+    remap = {v: i for i, v in enumerate(used)}
+    xyz = V[used].astype(np.float64)
+    face_ptr = [0]; face_vtx = []; fb = []
+    cell_faces = [[] for _ in range(N)]
+    for f, (loop, a, b) in enumerate(faces):
+        face_vtx += [remap[v] for v in loop]
+        face_ptr.append(len(face_vtx))
+        fb.append(1 if b < 0 else 0)
+        cell_faces[a].append((f, 1))
+        if b >= 0:
+            cell_faces[b].append((f, -1))
+    cell_ptr = np.concatenate([[0], np.cumsum([len(c) for c in cell_faces])]).astype(np.int64)
+    cell_face = np.array([f for c in cell_faces for f, _ in c], dtype=np.int64)
+    cell_sign = np.array([s for c in cell_faces for _, s in c], dtype=np.int8)
+    mesh = PolyMesh(xyz, np.array(face_ptr, dtype=np.int64), np.array(face_vtx, dtype=np.int64), cell_ptr,
+                    cell_face, cell_sign, np.array(fb, dtype=np.uint8), None, (0, 0, 0), h)
+    mesh.generators = P
+    return mesh
+
+
+def octa_mesh(n):
+    """OCTA family (SPEC's reading: a clipped BCC truncated-octahedron tiling): the Voronoi
+    cells of the body-centred cubic lattice {(i + 1/4)/n} u {(i + 3/4)/n} (i = 0..n-1 per axis),
+    2 n^3 cells; interior cells are 14-faced truncated octahedra (8 hexagons, 6 squares), the
+    boundary ones are clipped by the cube."""
+    a = (np.arange(n) + 0.25) / n
+    b = (np.arange(n) + 0.75) / n
+    A = np.stack(np.meshgrid(a, a, a, indexing="ij"), -1).reshape(-1, 3)
+    B = np.stack(np.meshgrid(b, b, b, indexing="ij"), -1).reshape(-1, 3)
+    return _voronoi_mesh(np.concatenate([A, B], 0), 1.0 / n)

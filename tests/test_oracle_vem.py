@@ -256,3 +256,73 @@ def test_convergence_order_k2():
         assert np.max(np.abs(gs.Bf @ u + gs.B[:, gs.dofs.bnd_vel] @ gs.uD[gs.dofs.bnd_vel])) < 1e-12
     ru = np.log2(eu[1] / eu[2]); rp = np.log2(ep[1] / ep[2])
     assert 1.8 < ru < 2.3 and 1.8 < rp < 2.4, (eu, ep)
+
+
+# ------------------------------------------------------------------ CVT (Voronoi) polyhedra, SURVEY f4
+@pytest.fixture(scope="module")
+def cvt5():
+    from synthetic import cvt_mesh
+    return cvt_mesh(5, seed=20230419)
+
+
+def test_cvt_mesh_is_a_valid_polyhedral_partition(cvt5):
+    """Planar convex faces, closed cells (sum_f s_f |f| n_f = 0), positive volumes summing to |[0,1]^3|,
+    every interior face in exactly two cells with opposite signs (S:28-33 checks)."""
+    m = cvt5
+    from oracle.vem import face_geometry
+    count = np.zeros(m.n_faces, dtype=int)
+    total = 0.0
+    for K in range(m.n_cells):
+        fs, ss = m.cell_faces(K)
+        acc = np.zeros(3)
+        for f, s in zip(fs, ss):
+            F = face_geometry(m, f, 2)
+            X = m.xyz[m.face(f)]
+            assert np.abs((X - X.mean(0)) @ F.n).max() < 1e-12          # planar
+            acc += s * F.area * F.n
+            count[f] += 1
+        assert np.linalg.norm(acc) < 1e-13
+        ei = EdgeIndex(mesh_edges(m), m.n_vertices)
+        total += ElementOps(m, K, ei, 2, 1.0).g.vol
+    assert abs(total - 1.0) < 1e-12
+    assert np.all(count[m.face_on_boundary == 1] == 1) and np.all(count[m.face_on_boundary == 0] == 2)
+    assert np.diff(m.face_ptr).max() > 4 and np.diff(m.cell_ptr).max() > 12   # genuinely polyhedral
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_cvt_projectors_and_kernel(cvt5, k):
+    """On Voronoi cells (up to 17 faces, 8-gon faces): projectors reproduce [P_k]^3, ker a_h^K = the
+    six rigid modes, a_h^K symmetric PSD."""
+    m = cvt5
+    ei = EdgeIndex(mesh_edges(m), m.n_vertices)
+    K = int(np.argmax(np.diff(m.cell_ptr)))          # the cell with the most faces
+    op = ElementOps(m, K, ei, k, 1.0)
+    Dk = dim3(k)
+    a = np.random.default_rng(2).standard_normal(3 * Dk)
+    dofs = op.DOFpoly @ a
+    for c in range(3):
+        assert np.allclose(op.PiN[c] @ dofs, a[c * Dk:(c + 1) * Dk], atol=1e-9)
+        assert np.allclose(op.P0[c] @ dofs, a[c * Dk:(c + 1) * Dk], atol=1e-8)
+    ev = np.linalg.eigvalsh(op.A)
+    assert np.sum(np.abs(ev) < 1e-11 * ev[-1]) == 6 and ev[0] > -1e-11 * ev[-1]
+
+
+def test_cvt_patch_test_k2():
+    """Global patch test on the CVT mesh: div-free u in [P_2]^3 and p in P_1 reproduced exactly."""
+    from synthetic import make_cvt_problem
+    u, p, lap, gp = _patch_fields(2)
+    f = lambda nuK: (lambda x: np.tile(-0.5 * nuK * lap - gp, (x.shape[0], 1)))
+    pr = make_cvt_problem(4, grid=(1, 1, 1))
+    gs = GlobalSystem(pr, u_bc=u, f_of_nu=f)
+    uh, ph = gs.direct_solve()
+    ui = np.zeros(gs.dofs.nvel)
+    for K in range(pr.mesh.n_cells):
+        op = gs.el.op(K)
+        iv, _ = gs.el.l2g[K]
+        ui[iv] = op.dofs_of_field(lambda x: u(x + gs.el.shift[K]))
+    assert np.max(np.abs(uh - ui[gs.dofs.free_vel])) < 1e-9
+    err = 0.0
+    for K in range(pr.mesh.n_cells):
+        op = gs.el.op(K); _, ip = gs.el.l2g[K]
+        err += op.l2_pressure_error_sq(ph[ip], p, gs.el.shift[K], pmean=0.5 - 1.0 + 0.25)
+    assert np.sqrt(err) < 1e-9
