@@ -184,9 +184,22 @@ def cross_coeffs(e, c, n_out):
 
 
 def d4_basis(k):
-    """Basis of x^[P_{k-3}]^3 used by D4 (k<=3: x^e_c for k=3, none for k=2)."""
-    assert k <= 3, "k=4 (NEXT f3) needs a D4 basis selection"
-    return [((0, 0, 0), c) for c in range(3)] if k == 3 else []
+    """Basis of x^[P_{k-3}]^3 used by the D4 moments (SURVEY O-4 reading A24): the fields
+    x^(m e_c) for monomials m of degree 0..k-3 (exps3 order), components c = 1, 2, 3, omitting
+    c = 1 when x_1 divides m (x^(x_1 q e_1) = x_1 x^(q e_1) ... the relation x^(x q) = 0 removes
+    exactly one field per monomial of degree >= 1: dim = 3 dim P_{k-3} - dim P_{k-4}).
+    k = 2: none; k = 3: x^e_1, x^e_2, x^e_3; k = 4: 11 fields."""
+    out = []
+    for d in range(k - 2):
+        for e in exps3(d):
+            if sum(e) != d:
+                continue
+            for c in range(3):
+                if c == 0 and e[0] > 0:
+                    continue
+                out.append((e, c))
+    assert len(out) == 3 * dim3(k - 3) - dim3(k - 4)
+    return out
 
 
 # ----------------------------------------------------------------------------- element operators
@@ -404,8 +417,8 @@ class ElementOps:
                 out[L.fdof(lf, t, 0):L.fdof(lf, t, 0) + L.nm] = ((F.qw * (uq @ tau)) @ mv) / F.area
         uq = u(g.qp)
         for i, (e, c) in enumerate(d4_basis(k)):
-            w = cross_coeffs(e, c, 1)
-            D1 = dim3(1)
+            D1 = dim3(k - 2)
+            w = cross_coeffs(e, c, k - 2)
             wq = np.stack([self.Mq[:, :D1] @ w[cc * D1:(cc + 1) * D1] for cc in range(3)], 1)
             out[L.o4 + i] = (g.qw * np.sum(uq * wq, 1)).sum() / g.vol
         if L.n5:
@@ -444,9 +457,9 @@ class ElementOps:
             for t, tau in enumerate((F.n, F.t1, F.t2)):
                 for c in range(3):
                     out[L.fdof(lf, t, 0):L.fdof(lf, t, 0) + L.nm, c * Dk:(c + 1) * Dk] += tau[c] * I
-        D1 = dim3(1)
+        D1 = dim3(k - 2)
         for i, (e, c0) in enumerate(d4_basis(k)):
-            w = cross_coeffs(e, c0, 1)
+            w = cross_coeffs(e, c0, k - 2)
             for c in range(3):
                 wq = self.Mq[:, :D1] @ w[c * D1:(c + 1) * D1]
                 out[L.o4 + i, c * Dk:(c + 1) * Dk] = ((g.qw * wq) @ self.Mq[:, :Dk]) / g.vol

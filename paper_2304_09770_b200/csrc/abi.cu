@@ -265,7 +265,7 @@ static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, i
                          const int32_t *sub_rank, const vb_constraints *cons, const double *nu,
                          const vb_dist *dist) {
   VB_REQUIRE(m && cell_sub && nu && cons, VB_EINVAL, "null argument");
-  VB_REQUIRE(m->k == 2 || m->k == 3, VB_EINVAL, "k must be 2 or 3");
+  VB_REQUIRE(m->k >= 2 && m->k <= 4, VB_EINVAL, "k must be 2, 3 or 4");
   VB_REQUIRE(nsub >= 1, VB_EINVAL, "n_subdomains must be >= 1");
   c->k = m->k;
   c->cons = *cons;
@@ -366,7 +366,7 @@ vb_status vb_plan_exchange(const vb_mesh *mesh, const int32_t *cell_subdomain, i
     return VB_EINVAL;
   vb_ctx c;   // host bookkeeping only: no device work
   try {
-    VB_REQUIRE(mesh->k == 2 || mesh->k == 3, VB_EINVAL, "k must be 2 or 3");
+    VB_REQUIRE(mesh->k >= 2 && mesh->k <= 4, VB_EINVAL, "k must be 2, 3 or 4");
     c.k = mesh->k;
     c.rank = rank;
     c.nranks = nranks;

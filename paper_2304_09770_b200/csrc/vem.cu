@@ -92,6 +92,23 @@ __device__ inline void cross_e(int i, int comp, int *j, int *sgn) {
   *sgn = tab[i][comp][1];
 }
 
+// The D4 fields x^(m e_cp), same order as the oracle's d4_basis (reading A24): monomials m of
+// degree 0..K-3 (exps3 order), cp = 0, 1, 2, omitting cp = 0 when x_1 divides m.  Calls
+// fn(i, em, cp) for field i.
+template <int K, class Fn>
+__device__ inline void for_d4(Fn fn) {
+  int i = 0;
+  for (int d = 0; d <= K - 3; ++d)
+    for (int mi = d3(d - 1); mi < d3(d); ++mi) {
+      int em[3];
+      exp3(mi, em);
+      for (int cp = 0; cp < 3; ++cp) {
+        if (cp == 0 && em[0] > 0) continue;
+        fn(i++, em, cp);
+      }
+    }
+}
+
 template <int K>
 __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict__ topo, const double *__restrict__ xyz,
                                                           const double *__restrict__ nu, int64_t K0, int64_t nE,
@@ -129,7 +146,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
     for (int q = 0; q < np_; ++q) {
       double x[3], w;
       face_point(g, f, nqf, q, x, &w);
-      double m3[d3(4)], m2[d2(4)], g2[d2(4)][2];
+      double m3[d3(K + 1)], m2[d2(K + 1)], g2[d2(K + 1)][2];
       mono3(x, g.xc, g.h, K + 1, m3);
       double xi = 0, eta = 0;
       for (int d = 0; d < 3; ++d) { xi += (x[d] - F.xc[d]) * F.t1[d]; eta += (x[d] - F.xc[d]) * F.t2[d]; }
@@ -153,7 +170,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
           const double xd = Pa[d] + c_lobx[j] * (Pb[d] - Pa[d]) - F.xc[d];
           xi += xd * F.t1[d]; eta += xd * F.t2[d];
         }
-        double m2[d2(4)];
+        double m2[d2(K + 1)];
         mono2(xi, eta, F.h, K, m2, nullptr);
         for (int b = 0; b < q2k; ++b) FGn(b) += el * c_lobw[j] * m2[b];
       }
@@ -177,7 +194,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
             const double xd = Pa[d] + c_lobx[j] * dv[d] - F.xc[d];
             xi += xd * F.t1[d]; eta += xd * F.t2[d];
           }
-          double m2[d2(4)], g2[d2(4)][2];
+          double m2[d2(K + 1)], g2[d2(K + 1)][2];
           mono2(xi, eta, F.h, K, m2, g2);
           int l;
           if (j == 0) l = i;
@@ -237,7 +254,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
       for (int q = 0; q < qt.npts(); ++q) {
         double x[3], w;
         qt.point(g, t, q, x, &w);
-        double m[d3(4)], gr[d3(4)][3];
+        double m[d3(K + 1)], gr[d3(K + 1)][3];
         mono3g(x, g.xc, g.h, K + 1, m, gr);
         for (int a = 0; a < Dk1; ++a)
           for (int b = 0; b <= a; ++b) G(a * Dk1 + b) += w * m[a] * m[b];
@@ -283,16 +300,18 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
       for (int f = 0; f < g.nf; ++f)
         for (int c = 0; c < 3; ++c) face_int(f, c, b, g.fsign[f] * fn[f][c], M2, (int64_t)s * nv);
     }
-    if (K == 3) {
-      for (int i = 0; i < 3; ++i, ++s) {
-        for (int comp = 0; comp < 3; ++comp) {
-          int j, sg;
-          cross_e(i, comp, &j, &sg);
-          if (j >= 0) TT(s * ns + comp * D2m + (1 + j)) += sg;
-        }
-        M2(s * nv + L.o4 + i) = g.vol;
+    for_d4<K>([&](int i, const int em[3], int cp) {   // D4 rows: int v . x^(m e_cp) = |K| D4_i
+      for (int comp = 0; comp < 3; ++comp) {
+        int j, sg;
+        cross_e(cp, comp, &j, &sg);
+        if (j < 0) continue;
+        int ee[3] = {em[0], em[1], em[2]};
+        ee[j]++;
+        TT(s * ns + comp * D2m + idx3(ee[0], ee[1], ee[2])) += sg;
       }
-    }
+      M2(s * nv + L.o4 + i) = g.vol;
+      ++s;
+    });
     lu_solve(TT, ns, M2, nv);
   }
   // ================= (3) Pi^nabla_{k,K} per component
@@ -345,16 +364,18 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
       for (int f = 0; f < g.nf; ++f)
         for (int c = 0; c < 3; ++c) face_int(f, c, b, g.fsign[f] * fn[f][c], MK, (int64_t)s * nv);
     }
-    if (K == 3) {   // D4: x^e_i (degree 0)
-      for (int i = 0; i < 3; ++i, ++s) {
-        for (int comp = 0; comp < 3; ++comp) {
-          int j, sg;
-          cross_e(i, comp, &j, &sg);
-          if (j >= 0) TT(s * S3 + comp * Dk + (1 + j)) += sg;
-        }
-        MK(s * nv + L.o4 + i) = g.vol;
+    for_d4<K>([&](int i, const int em[3], int cp) {   // D4 rows
+      for (int comp = 0; comp < 3; ++comp) {
+        int j, sg;
+        cross_e(cp, comp, &j, &sg);
+        if (j < 0) continue;
+        int ee[3] = {em[0], em[1], em[2]};
+        ee[j]++;
+        TT(s * S3 + comp * Dk + idx3(ee[0], ee[1], ee[2])) += sg;
       }
-    }
+      MK(s * nv + L.o4 + i) = g.vol;
+      ++s;
+    });
     // super-enhancement rows: x^(m e_cp) for |m| = d in {k-2, k-1}, skipping (cp = 0, x1 | m)
     for (int d = K - 2; d <= K - 1; ++d)
       for (int mi = d3(d - 1); mi < d3(d); ++mi) {
@@ -441,7 +462,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
   // ================= (7) DOFs of the polynomial basis {m_g e_c}: DP (nv x 3Dk)
   for (int i = 0; i < nv * S3; ++i) DP(i) = 0.0;
   for (int lv = 0; lv < g.nv; ++lv) {
-    double m[d3(3)];
+    double m[d3(K)];
     mono3(g.X[lv], g.xc, g.h, K, m);
     for (int c = 0; c < 3; ++c)
       for (int gg = 0; gg < Dk; ++gg) DP((int64_t)L.vdof(lv, c) * S3 + c * Dk + gg) = m[gg];
@@ -451,7 +472,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
     for (int j = 0; j < K - 1; ++j) {
       double x[3];
       for (int d = 0; d < 3; ++d) x[d] = Pa[d] + c_lobx[j + 1] * (Pb[d] - Pa[d]);
-      double m[d3(3)];
+      double m[d3(K)];
       mono3(x, g.xc, g.h, K, m);
       for (int c = 0; c < 3; ++c)
         for (int gg = 0; gg < Dk; ++gg) DP((int64_t)L.edof(le, j, c) * S3 + c * Dk + gg) = m[gg];
@@ -467,14 +488,17 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
           for (int gg = 0; gg < Dk; ++gg)
             DP((int64_t)L.fdof(f, t, a) * S3 + c * Dk + gg) = tau[t][c] * FM(f * Dk1 * q2k1 + gg * q2k1 + a) / F.area;
   }
-  if (K == 3)
-    for (int i = 0; i < 3; ++i)
-      for (int c = 0; c < 3; ++c) {
-        int j, sg;
-        cross_e(i, c, &j, &sg);
-        if (j < 0) continue;
-        for (int gg = 0; gg < Dk; ++gg) DP((int64_t)(L.o4 + i) * S3 + c * Dk + gg) = sg * G(gg * Dk1 + (1 + j)) / g.vol;
-      }
+  for_d4<K>([&](int i, const int em[3], int cp) {   // D4 of m_g e_c: (1/|K|) int m_g (x^(m e_cp))_c
+    for (int c = 0; c < 3; ++c) {
+      int j, sg;
+      cross_e(cp, c, &j, &sg);
+      if (j < 0) continue;
+      int ee[3] = {em[0], em[1], em[2]};
+      ee[j]++;
+      const int wi = idx3(ee[0], ee[1], ee[2]);
+      for (int gg = 0; gg < Dk; ++gg) DP((int64_t)(L.o4 + i) * S3 + c * Dk + gg) = sg * G(gg * Dk1 + wi) / g.vol;
+    }
+  });
   for (int a = 1; a < D1; ++a)
     for (int c = 0; c < 3; ++c)
       for (int gg = 0; gg < Dk; ++gg) {
@@ -525,11 +549,11 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
 void element_matrices_device(vb_ctx *c) {
   cudaStream_t s = c->stream;
   const int nvm = c->nv_max;
-  const int S3 = 3 * (c->k == 2 ? 10 : 20);
+  const int S3 = 3 * (c->k == 2 ? 10 : (c->k == 3 ? 20 : 35));
   c->d_elA.alloc((size_t)c->nKl * nvm * nvm);
   c->d_elB.alloc((size_t)c->nKl * c->np * nvm);
   c->d_P0.alloc((size_t)c->nKl * S3 * nvm);
-  const int64_t per = c->k == 2 ? Arena<2>(nvm).total : Arena<3>(nvm).total;
+  const int64_t per = c->k == 2 ? Arena<2>(nvm).total : (c->k == 3 ? Arena<3>(nvm).total : Arena<4>(nvm).total);
   int64_t NE = std::max<int64_t>(128, std::min<int64_t>(c->nKl, (int64_t)(3.0e9 / 8 / per)));
   NE = (NE + 127) / 128 * 128;
   DBuf<double> scratch;
@@ -537,12 +561,13 @@ void element_matrices_device(vb_ctx *c) {
   for (int64_t K0 = 0; K0 < c->nKl; K0 += NE) {
     const int64_t n = std::min<int64_t>(NE, c->nKl - K0);
     const int blocks = (n + 127) / 128;
-    if (c->k == 2)
-      vem_element_kernel<2><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, K0, n, nvm, scratch.p, NE,
-                                                   c->d_elA.p, c->d_elB.p, c->d_P0.p);
-    else
-      vem_element_kernel<3><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, K0, n, nvm, scratch.p, NE,
-                                                   c->d_elA.p, c->d_elB.p, c->d_P0.p);
+#define VB_K9(KK)                                                                                           \
+  vem_element_kernel<KK><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, K0, n, nvm, scratch.p, NE, \
+                                                c->d_elA.p, c->d_elB.p, c->d_P0.p)
+    if (c->k == 2) VB_K9(2);
+    else if (c->k == 3) VB_K9(3);
+    else VB_K9(4);
+#undef VB_K9
     VB_STAGE();
   }
   VB_CUDA(cudaStreamSynchronize(s));
@@ -593,7 +618,7 @@ __global__ void rhs_element_kernel(const int *__restrict__ topo, const double *_
                                    const double *__restrict__ nu, const int64_t *__restrict__ l2g,
                                    const int64_t *__restrict__ vel2free, const double *__restrict__ elA,
                                    const double *__restrict__ elB, const double *__restrict__ P0all, int64_t nK,
-                                   int nvmax, ProbDev P, double *yel) {
+                                   int nvmax, ProbDev P, double *yel, double *uDall) {
   constexpr int Dk = d3(K), D1 = d3(K - 1), S3 = 3 * d3(K), nm = d2(K - 2);
   const int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (cell >= nK) return;
@@ -607,7 +632,7 @@ __global__ void rhs_element_kernel(const int *__restrict__ topo, const double *_
   QuadTet qt(K + 3);
   for (int t = 0; t < g.ntet; ++t)
     for (int q = 0; q < qt.npts(); ++q) {
-      double x[3], w, f[3], m[d3(3)];
+      double x[3], w, f[3], m[d3(K)];
       qt.point(g, t, q, x, &w);
       f_problem(P, x, nuK, f);
       mono3(x, g.xc, g.h, K, m);
@@ -617,8 +642,9 @@ __global__ void rhs_element_kernel(const int *__restrict__ topo, const double *_
   const double *P0 = P0all + cell * (int64_t)S3 * nvmax;
   const int stride = nvmax + D1;
   double *y = yel + cell * stride;
-  // lifted boundary DOFs (interpolant of the exact trace; zero for the sinker problem)
-  double uD[512];
+  // lifted boundary DOFs (interpolant of the exact trace; zero for the sinker problem), per cell in
+  // global scratch (general polyhedra: up to a thousand DOFs per cell)
+  double *uD = uDall + cell * (int64_t)nvmax;
   bool any = false;
   for (int j = 0; j < nv; ++j) {
     uD[j] = 0.0;
@@ -695,12 +721,16 @@ void build_rhs_device(vb_ctx *c, const vb_problem *p, double *rhs) {
   }
   cudaStream_t s = c->stream;
   const int blocks = (c->nKl + 127) / 128;
-  if (c->k == 2)
-    rhs_element_kernel<2><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, c->d_cell_l2g.p, c->d_vel2free.p,
-                                                 c->d_elA.p, c->d_elB.p, c->d_P0.p, c->nKl, c->nv_max, P, c->w_elt.p);
-  else
-    rhs_element_kernel<3><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, c->d_cell_l2g.p, c->d_vel2free.p,
-                                                 c->d_elA.p, c->d_elB.p, c->d_P0.p, c->nKl, c->nv_max, P, c->w_elt.p);
+  DBuf<double> uD;
+  uD.alloc(std::max<int64_t>((int64_t)c->nKl * c->nv_max, 1));
+#define VB_RHS_K(KK)                                                                                        \
+  rhs_element_kernel<KK><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, c->d_cell_l2g.p,       \
+                                                c->d_vel2free.p, c->d_elA.p, c->d_elB.p, c->d_P0.p, c->nKl, \
+                                                c->nv_max, P, c->w_elt.p, uD.p)
+  if (c->k == 2) VB_RHS_K(2);
+  else if (c->k == 3) VB_RHS_K(3);
+  else VB_RHS_K(4);
+#undef VB_RHS_K
   VB_STAGE();
   element_gather(c, c->w_elt.p, rhs);   // owned layout (multi-rank: interface sums exchanged)
   VB_CUDA(cudaStreamSynchronize(s));

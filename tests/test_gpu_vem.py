@@ -11,7 +11,8 @@ pytestmark = pytest.mark.gpu
 
 # c4 here without the adaptive enrichment (the adaptive path has its own test)
 CASES = [("c1", {}), ("c3", dict(n=4, sub=(2, 2, 2))), ("c1", dict(n=4, k=3)),
-         ("c4", dict(n=8, sub=(4, 4, 4), constraints=dict(adaptive_tau=0.0)))]
+         ("c4", dict(n=8, sub=(4, 4, 4), constraints=dict(adaptive_tau=0.0))),
+         ("c1", dict(n=4, k=4)), ("c3", dict(n=4, sub=(2, 2, 2), k=4))]
 
 
 def _ctx(prob):
@@ -210,3 +211,12 @@ def test_c3_full_size_properties():
     nb = np.linalg.norm(rhs.cpu().numpy())
     assert np.linalg.norm(res[:ctx.n_vel]) <= 1e-8 * nb
     assert np.linalg.norm(res[ctx.n_vel:]) <= 1e-8 * nb
+
+
+def test_k4_dof_count_table3():
+    """k = 4 (T3 row CUBE 512 k=4): the GPU DOF numbering gives the paper's 76,387
+    nDofs on the 8^3 cube, and one solve converges to the oracle-pinned gates of test_full_solve_parity."""
+    import paper_2304_09770_b200 as vb
+    prob = make_problem("c1", n=8, k=4, sub=(4, 4, 4))
+    ctx = vb.context_for(prob)
+    assert ctx.stats()["n_dofs_paper"] == 76387

@@ -96,7 +96,7 @@ def test_gauss_lobatto():
 
 
 # ------------------------------------------------------------------ projector reproduction
-CELLS = [(2, 0.0, False), (3, 0.0, False), (2, 0.2, True), (3, 0.2, True)]
+CELLS = [(2, 0.0, False), (3, 0.0, False), (2, 0.2, True), (3, 0.2, True), (4, 0.0, False), (4, 0.2, True)]
 
 
 @pytest.mark.parametrize("k,jit,tri", CELLS)
@@ -108,7 +108,7 @@ def test_projectors_reproduce_polynomials(k, jit, tri):
     dofs = op.DOFpoly @ a
     for c in range(3):
         assert np.allclose(op.PiN[c] @ dofs, a[c * Dk:(c + 1) * Dk], atol=1e-10)
-        assert np.allclose(op.P0[c] @ dofs, a[c * Dk:(c + 1) * Dk], atol=1e-9)
+        assert np.allclose(op.P0[c] @ dofs, a[c * Dk:(c + 1) * Dk], atol=1e-9 if k < 4 else 1e-8)
     # Pi^0_{k-1} grad reproduces grad p exactly (degree k-1)
     E = exps3(k); idx = {e: i for i, e in enumerate(exps3(k - 1))}
     for c in range(3):
