@@ -266,6 +266,20 @@ def main():
         barrier()
         ms_instr = e0.elapsed_time(e1) / args.steps
         os.environ["VB_KERNEL_TIMING"] = "0"
+    # K7, the element-by-element saddle operator (north-star subsystem 3; not in the solve, which applies
+    # the explicit interface Schur complement): device time of elem_apply per launch (CUDA events on the
+    # library stream), algorithmic bytes 8 sum_K (nv (nv + 1) / 2 + np nv) (SURVEY §8(d) b_e)
+    k7_ms = None
+    if not args.no_kernel_timing:
+        os.environ["VB_KERNEL_TIMING"] = "1"
+        y = torch.empty_like(rhs)
+        ctx.apply_operator(x, y)
+        k7 = []
+        for _ in range(max(3, args.steps)):
+            ctx.apply_operator(x, y)
+            k7.append(ctx.kernel_times().get("elem_apply K7 (packed element matrices)", float("nan")))
+        k7_ms = float(np.mean(k7))
+        os.environ["VB_KERNEL_TIMING"] = "0"
     it = float(np.mean(its))
     ndofs = st["n_dofs_paper"]          # the whole (global) problem, all ranks together
     value = ndofs * it / (ms / 1e3)
@@ -301,6 +315,12 @@ def main():
     c_ms, c_bytes = kt[names[2]], 8.0 * st["pk_coarse"]
     achieved = op_bytes / (op_ms / 1e3) / 1e9
     traffic, traffic_src = _ncu_traffic()
+    npr = {2: 4, 3: 10, 4: 20}[prob.k]
+    k7_bytes = 8.0 * st["n_cells"] * (st["nv_max"] * (st["nv_max"] + 1) / 2 + npr * st["nv_max"])
+    k7_entry = {"ms": k7_ms, "bytes_per_launch": k7_bytes,
+                "GBps": k7_bytes / (k7_ms / 1e3) / 1e9 if k7_ms else None,
+                "frac": k7_bytes / (k7_ms / 1e3) / 1e9 / peak if k7_ms else None,
+                "bytes_note": "hexahedral cells (c5): every cell has nv = nv_max"}
     iter_ms = ms / max(it, 1)
     per_iter_bytes = st["bytes_per_iter"]
     line = {
@@ -327,7 +347,8 @@ def main():
                      "bytes_per_launch": op_bytes, "ms_per_launch": op_ms,
                      "others": {names[1]: {"ms": loc_ms, "GBps": loc_bytes / (loc_ms / 1e3) / 1e9 if loc_ms else None},
                                 names[2]: {"ms": c_ms, "GBps": c_bytes / (c_ms / 1e3) / 1e9 if c_ms else None},
-                                names[3]: {"ms": kt[names[3]]}, names[4]: {"ms": kt[names[4]]}}},
+                                names[3]: {"ms": kt[names[3]]}, names[4]: {"ms": kt[names[4]]},
+                                "elem_apply K7 (element-by-element operator, packed A^K)": k7_entry}},
         "factor": {"t_s": t_factor, "dmma_gemm_flops": st["factor_gemm_flops"],
                    "tflops": st["factor_gemm_flops"] / t_factor / 1e12,
                    "frac_of_dmma_peak": st["factor_gemm_flops"] / t_factor / 37.2e12,

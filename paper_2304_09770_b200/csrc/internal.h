@@ -278,6 +278,7 @@ struct vb_ctx {
   vb::DBuf<double> d_xyz, d_nu;
   vb::DBuf<int> d_topo;
   vb::DBuf<double> d_elA, d_elB;     // element matrices: A [nK][nv_max^2], B [nK][np*nv_max]
+  vb::DBuf<double> d_elAp;           // K7: lower triangles of A^K, packed rows [nK][nv_max (nv_max+1)/2]
   vb::DBuf<int64_t> d_cell_l2g;      // [nK][nv_max] global velocity ids (-1 pad)
   vb::DBuf<int> d_cell_loc;          // [nK][nv_max + np] position in subdomain matrix (-1 = drop)
   std::vector<int> h_cell_loc;       // host copy (B0/B8 coupling plans)

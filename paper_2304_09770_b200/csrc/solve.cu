@@ -723,35 +723,147 @@ __global__ void pressure_mean_kernel(const double *__restrict__ cellgeo, const i
 
 // ------------------------------------------------------------------ K7: element-by-element operator
 // y_K = [A_K B_K^T; B_K 0] x_K per element, then a deterministic per-DOF gather-sum.
-__global__ void elem_apply_kernel(const double *__restrict__ elA, const double *__restrict__ elB,
-                                  const int64_t *__restrict__ l2g, const int64_t *__restrict__ vel2free,
-                                  const int *__restrict__ cell_nv, const int64_t *__restrict__ gid, int nvmax,
-                                  int np, int64_t nK, int64_t nvf, const double *__restrict__ x, double *yel) {
+// K7 on packed symmetric element matrices: A^K stored as its lower triangle row by row
+// (nv (nv + 1) / 2 doubles: the algorithmic bytes of SURVEY §8(d), half of the dense A^K).
+// One CTA per cell, K7_WARPS warps, rows interleaved over the warps.  Warp w reads row i once
+// (coalesced over j <= i) and uses it twice: y_i += A_ij x_j (row part, warp sum) and
+// t_w[j] += A_ij x_i for j < i (transpose part, lane-owned entries of the warp's shared-memory
+// partial vector t_w).  y_i = row_i + sum_w t_w[i] in fixed warp order: no atomics, deterministic.
+constexpr int K7_WARPS = 4;
+__global__ void __launch_bounds__(K7_WARPS * 32) elem_apply_packed_kernel(
+    const double *__restrict__ elAp, int64_t slotA, const double *__restrict__ elB,
+    const int64_t *__restrict__ l2g, const int64_t *__restrict__ vel2free, const int *__restrict__ cell_nv,
+    const int64_t *__restrict__ gid, int nvmax, int np, int64_t nK, int64_t nvf, const double *__restrict__ x,
+    double *yel) {
   const int64_t K = blockIdx.x;
   if (K >= nK) return;
-  extern __shared__ double xs[];
+  extern __shared__ double k7s[];
+  double *xs = k7s;                          // nv + np gathered inputs
+  double *rowv = xs + nvmax + np;            // row parts
+  double *tw = rowv + nvmax;                 // K7_WARPS partial transpose vectors (nvmax each)
   const int nv = cell_nv[K];
   const int stride = nvmax + np;
   for (int j = threadIdx.x; j < nv; j += blockDim.x) {
     const int64_t f = vel2free[l2g[K * nvmax + j]];
     xs[j] = f >= 0 ? x[f] : 0.0;
   }
-  for (int a = threadIdx.x; a < np; a += blockDim.x) xs[nvmax + a] = x[nvf + gid[K] * np + a];
+  for (int a = threadIdx.x; a < np; a += blockDim.x) xs[nv + a] = x[nvf + gid[K] * np + a];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *t = tw + warp * nvmax;
+  for (int j = lane; j < nv; j += 32) t[j] = 0.0;
   __syncthreads();
-  const double *A = elA + K * nvmax * nvmax;
+  const double *A = elAp + K * slotA;
   const double *B = elB + K * np * nvmax;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = warp; i < nv + np; i += nw) {
+  for (int i = warp; i < nv; i += K7_WARPS) {
+    const double *row = A + (int64_t)i * (i + 1) / 2;
+    const double xi = xs[i];
+    double v = 0.0;
+    for (int j = lane; j <= i; j += 32) {
+      const double a = __ldg(row + j);
+      v += a * xs[j];
+      if (j < i) t[j] += a * xi;
+    }
+    for (int q = lane; q < np; q += 32) v += B[(int64_t)q * nv + i] * xs[nv + q];
+    v = warp_sum(v);
+    if (lane == 0) rowv[i] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    double v = rowv[i];
+    for (int w = 0; w < K7_WARPS; ++w) v += tw[w * nvmax + i];
+    yel[K * stride + i] = v;
+  }
+  for (int q = warp; q < np; q += K7_WARPS) {   // pressure rows: B x
+    double v = 0.0;
+    for (int j = lane; j < nv; j += 32) v += B[(int64_t)q * nv + j] * xs[j];
+    v = warp_sum(v);
+    if (lane == 0) yel[K * stride + nvmax + q] = v;
+  }
+}
+
+// K7 with the element matrices staged by the bulk-copy engine: one cp.async.bulk of the cell's packed
+// lower triangle (~26 KB for k = 2 hexahedra) and one of B^K into shared memory per CTA, signalled
+// on an mbarrier, while the threads gather the cell's inputs; rows then come from shared memory
+// (the streaming kernel above waits on one global-memory row segment at a time), one thread per
+// row summing its row and its column of the lower triangle (no warp reductions).  Needs
+// (nv_max (nv_max+1)/2 + np nv_max) doubles of shared memory: used while that fits (k = 2
+// hexahedra and small polyhedra).
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(128) elem_apply_bulk_kernel(
+    const double *__restrict__ elAp, int64_t slotA, const double *__restrict__ elB,
+    const int64_t *__restrict__ l2g, const int64_t *__restrict__ vel2free, const int *__restrict__ cell_nv,
+    const int64_t *__restrict__ gid, int nvmax, int np, int64_t nK, int64_t nvf, const double *__restrict__ x,
+    double *yel) {
+  const int64_t K = blockIdx.x;
+  if (K >= nK) return;
+  extern __shared__ __align__(16) double k7b[];
+  __shared__ __align__(8) uint64_t bar;
+  const int nv = cell_nv[K];
+  const int64_t lenA = (int64_t)nv * (nv + 1) / 2;
+  const int lenA16 = (int)((lenA + 1) & ~1LL);            // 16-byte multiple
+  double *As = k7b;                                      // packed lower triangle
+  double *Bs = As + ((slotA + 1) & ~1LL);                // np x nv
+  double *xs = Bs + (int64_t)np * nvmax;                 // nv + np inputs
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned bA = 8u * lenA16, bB = 8u * (unsigned)(np * nv);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(bA + bB)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(As)),
+                 "l"(elAp + K * slotA), "r"(bA), "r"(smem_u32(&bar))
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(Bs)),
+                 "l"(elB + K * np * nvmax), "r"(bB), "r"(smem_u32(&bar))
+                 : "memory");
+  }
+  const int stride = nvmax + np;
+  for (int j = threadIdx.x; j < nv; j += blockDim.x) {   // overlaps with the bulk copies
+    const int64_t f = vel2free[l2g[K * nvmax + j]];
+    xs[j] = f >= 0 ? x[f] : 0.0;
+  }
+  for (int a = threadIdx.x; a < np; a += blockDim.x) xs[nv + a] = x[nvf + gid[K] * np + a];
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(&bar))
+      : "memory");
+  __syncthreads();
+  // one thread per row, no reductions: y_i = sum_{j <= i} L_ij x_j + sum_{k > i} L_ki x_k + (B^T p)_i
+  for (int i = threadIdx.x; i < nv + np; i += blockDim.x) {
     double v = 0.0;
     if (i < nv) {
-      for (int j = lane; j < nv; j += 32) v += A[(int64_t)i * nv + j] * xs[j];
-      for (int a = lane; a < np; a += 32) v += B[(int64_t)a * nv + i] * xs[nvmax + a];
+      const double *row = As + (int64_t)i * (i + 1) / 2;
+      for (int j = 0; j <= i; ++j) v += row[j] * xs[j];
+      for (int k = i + 1; k < nv; ++k) v += As[(int64_t)k * (k + 1) / 2 + i] * xs[k];
+      for (int q = 0; q < np; ++q) v += Bs[q * nv + i] * xs[nv + q];
+      yel[K * stride + i] = v;
     } else {
-      const int a = i - nv;
-      for (int j = lane; j < nv; j += 32) v += B[(int64_t)a * nv + j] * xs[j];
+      const int q = i - nv;
+      for (int j = 0; j < nv; ++j) v += Bs[q * nv + j] * xs[j];
+      yel[K * stride + nvmax + q] = v;
     }
-    v = warp_sum(v);
-    if (lane == 0) yel[K * stride + (i < nv ? i : nvmax + (i - nv))] = v;
+  }
+}
+
+__global__ void pack_element_lower_kernel(const double *__restrict__ elA, const int *__restrict__ cell_nv, int nvmax,
+                                          int64_t slotA, double *elAp) {
+  const int64_t K = blockIdx.y;
+  const int nv = cell_nv[K];
+  const int64_t n = (int64_t)nv * (nv + 1) / 2;
+  const double *A = elA + K * (int64_t)nvmax * nvmax;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    // row i, column j <= i of packed index e = i (i + 1) / 2 + j
+    int64_t i = (int64_t)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+    while ((i + 1) * (i + 2) / 2 <= e) ++i;
+    while (i * (i + 1) / 2 > e) --i;
+    const int64_t j = e - i * (i + 1) / 2;
+    elAp[K * slotA + e] = A[i * nv + j];
   }
 }
 
@@ -911,8 +1023,8 @@ static void run_sub_gemv(const SolveState *st, const GemvWork *w, int nw, size_t
 
 static const char *kCatNames[] = {"sym_gemv S_T (operator, B1)", "sym_gemv S_DD^-1 (local, B5)",
                                   "sym_gemv coarse inverse (B6)", "apply_S total (B1-B2)",
-                                  "apply_M total (B4-B7)"};
-constexpr int N_CAT = 5;
+                                  "apply_M total (B4-B7)", "elem_apply K7 (packed element matrices)"};
+constexpr int N_CAT = 6;
 
 static void tick(vb_ctx *c, SolveState *st, int cat, bool begin, cudaStream_t strm = nullptr) {
   if (!c->timing) return;
@@ -1474,8 +1586,13 @@ void element_gather(vb_ctx *c, const double *yel, double *out) {
   }
 }
 
+// per-cell slot of the packed element matrices: even (16-byte aligned cells for the bulk copies)
+static int64_t k7_slot(int nvmax) { return (((int64_t)nvmax * (nvmax + 1) / 2) + 1) & ~1LL; }
+constexpr size_t kK7BulkSmem = 100 * 1024;   // beyond: the streaming kernel (several CTAs per SM kept)
+
 void apply_operator_device(vb_ctx *c, const double *x, double *y) {
   cudaStream_t s = c->stream;
+  c->timing = getenv("VB_KERNEL_TIMING") && atoi(getenv("VB_KERNEL_TIMING"));
   const int stride = c->nv_max + c->np;
   const double *xin = x;
   if (c->nranks > 1) {
@@ -1485,12 +1602,35 @@ void apply_operator_device(vb_ctx *c, const double *x, double *y) {
     dof_halo(c, st, c->w_xg.p);
     xin = c->w_xg.p;
   }
-  elem_apply_kernel<<<c->nKl, 128, stride * sizeof(double), s>>>(c->d_elA.p, c->d_elB.p, c->d_cell_l2g.p,
+  if (!c->d_elAp.p) {   // packed lower triangles of the element matrices (once per context)
+    const int64_t slot = k7_slot(c->nv_max);
+    c->d_elAp.alloc(std::max<int64_t>((int64_t)c->nKl * slot, 1));
+    if (c->nKl)
+      pack_element_lower_kernel<<<dim3(16, c->nKl), 256, 0, s>>>(c->d_elA.p, c->d_cell_nv.p, c->nv_max, slot,
+                                                                  c->d_elAp.p);
+    VB_STAGE();
+  }
+  const int64_t slot = k7_slot(c->nv_max);
+  const size_t smem = (size_t)(stride + c->nv_max + K7_WARPS * c->nv_max) * sizeof(double);
+  const size_t smem_bulk = (size_t)(((slot + 1) & ~1LL) + (int64_t)c->np * c->nv_max + stride) * sizeof(double);
+  SolveState *st = get_state(c);
+  tick(c, st, 5, true);
+  if (smem_bulk <= kK7BulkSmem && !(getenv("VB_K7_STREAM") && atoi(getenv("VB_K7_STREAM")))) {
+    raise_smem_limit((const void *)elem_apply_bulk_kernel, smem_bulk);
+    elem_apply_bulk_kernel<<<c->nKl, 128, smem_bulk, s>>>(
+        c->d_elAp.p, slot, c->d_elB.p, c->d_cell_l2g.p, c->d_vel2free.p, c->d_cell_nv.p, c->d_cell_gid.p, c->nv_max,
+        c->np, c->nKl, c->n_free_vel, xin, c->w_elt.p);
+  } else {
+    raise_smem_limit((const void *)elem_apply_packed_kernel, smem);
+    elem_apply_packed_kernel<<<c->nKl, K7_WARPS * 32, smem, s>>>(c->d_elAp.p, slot, c->d_elB.p, c->d_cell_l2g.p,
                                                                  c->d_vel2free.p, c->d_cell_nv.p, c->d_cell_gid.p,
                                                                  c->nv_max, c->np, c->nKl, c->n_free_vel, xin,
                                                                  c->w_elt.p);
+  }
+  tick(c, st, 5, false);
   VB_STAGE();
   element_gather(c, c->w_elt.p, y);
+  if (c->timing) collect_times(c, st);
 }
 
 void lanczos_extremes(const std::vector<double> &al, const std::vector<double> &be, double *lmin, double *lmax);
