@@ -344,19 +344,19 @@ __global__ void p0_compat_kernel(double *p0, int n, double *acc, int mode, int n
 }
 
 // |b_0^(i) x_Gamma^(i)| per local subdomain (reported on VB_EBREAKDOWN; b~0 vanishes
-// on the dual coordinates, so only the primal ones enter), then the max into out[0]
+// on the dual coordinates, so only the primal ones enter), one warp per subdomain; the max over
+// subdomains by an atomic max on the bit patterns (order-independent for non-negative doubles; out[0]
+// zeroed before the launch)
 __global__ void flux_violation_kernel(const SubDev *__restrict__ subs, int N, const double *__restrict__ b0T,
                                       const int64_t *__restrict__ loc2x, const double *__restrict__ x,
                                       double *out) {
-  double mx = 0.0;
-  for (int i = 0; i < N; ++i) {
-    const SubDev S = subs[i];
-    double acc = 0.0;
-    for (int a = threadIdx.x; a < S.npi; a += 32) acc += b0T[S.off_Pi + a] * x[loc2x[S.off_G + S.nd + a]];
-    acc = warp_sum(acc);
-    mx = fmax(mx, fabs(acc));
-  }
-  if (threadIdx.x == 0) out[0] = mx;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= N) return;
+  const SubDev S = subs[i];
+  double acc = 0.0;
+  for (int a = lane; a < S.npi; a += 32) acc += b0T[S.off_Pi + a] * x[loc2x[S.off_G + S.nd + a]];
+  acc = warp_sum(acc);
+  if (lane == 0) atomicMax(reinterpret_cast<unsigned long long *>(out), (unsigned long long)__double_as_longlong(fabs(acc)));
 }
 
 // scal: [0] rz [1] pq [2] rr [3] rz_new [4] r0n [5] rtol*r0n [6] it [7] status [8] maxit
@@ -1865,7 +1865,9 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
       pcg_mstep(c, st);
     }
   }
-  flux_violation_kernel<<<1, 32, 0, s>>>(c->d_sub.p, N, c->d_b0T.p, c->d_loc2x.p, c->w_x.p, c->w_dots.p + W_FLUX);
+  VB_CUDA(cudaMemsetAsync(c->w_dots.p + W_FLUX, 0, sizeof(double), s));
+  flux_violation_kernel<<<(N + 7) / 8, 256, 0, s>>>(c->d_sub.p, N, c->d_b0T.p, c->d_loc2x.p, c->w_x.p,
+                                                    c->w_dots.p + W_FLUX);
   VB_STAGE();
   double flux = 0.0;
   if (c->nranks > 1) {   // max over ranks

@@ -11,6 +11,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c5")
     ap.add_argument("--factor", action="store_true", help="profile the factorisation instead")
+    ap.add_argument("--with-k7", action="store_true", help="also one vb_apply_operator (K7) in the profiled range")
     args = ap.parse_args()
     import torch
     import paper_2304_09770_b200 as vb
@@ -32,6 +33,9 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
     rep = ctx.pcg_solve(rhs, x)
+    if args.with_k7:
+        y = torch.empty_like(x)
+        ctx.apply_operator(x, y)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
     print("iterations", rep["iterations"])
