@@ -218,6 +218,14 @@ def main():
     ctx.factor()
     t_factor_warm = time.perf_counter() - t0
     st_warm = ctx.stats()
+    # a third factorisation with CUDA events around every DMMA GEMM launch set: the GEMM kernels'
+    # own time (the factor's dominant kernel; its DMMA roofline), not reported as the factor time
+    gemm_s = None
+    if not args.no_kernel_timing:
+        os.environ["VB_KERNEL_TIMING"] = "1"
+        ctx.factor()
+        os.environ["VB_KERNEL_TIMING"] = "0"
+        gemm_s = ctx.stats()["factor_gemm_us"] / 1e6 or None
     rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
     ctx.build_rhs(vb.problem_args(prob), rhs)
     x = torch.zeros_like(rhs)
@@ -357,6 +365,9 @@ def main():
                    "t_warm_s": t_factor_warm, "alloc_warm_s": st_warm["factor_alloc_us"] / 1e6,
                    "tflops_warm": st["factor_gemm_flops"] / t_factor_warm / 1e12,
                    "frac_of_dmma_peak_warm": st["factor_gemm_flops"] / t_factor_warm / 37.2e12,
+                   "gemm_kernel_s": gemm_s,
+                   "gemm_kernel_tflops": st["factor_gemm_flops"] / gemm_s / 1e12 if gemm_s else None,
+                   "gemm_kernel_frac_of_dmma_peak": st["factor_gemm_flops"] / gemm_s / 37.2e12 if gemm_s else None,
                    "peak_note": "DMMA 37.2 TFLOP/s measured by tools/fp64_peak.cu (profiles/r01_fp64_peak.txt); "
                                 "t_s includes the non-GEMM kernels, host work and device allocation (alloc_s: "
                                 "first-touch mapping of the factor workspace, varies run to run) of vb_factor; "

@@ -206,7 +206,11 @@ vb_status vb_dof_layout(const vb_ctx *ctx, int64_t *global_ids);   /* free -> gl
 vb_status vb_cell_local_dofs(const vb_ctx *ctx, int64_t cell, int64_t *vel_ids, int32_t *n_vel,
                              int64_t *p_ids, int32_t *n_p);       /* local order -> global id  */
 vb_status vb_get_element_matrices(const vb_ctx *ctx, int64_t cell, double *A, double *B);
-vb_status vb_stats(const vb_ctx *ctx, int64_t *out25);            /* sizes: see DESIGN.md      */
+/* 26 counters (host-owned out26): sizes of the decomposition and operators, bytes per iteration,
+ * factor GEMM flops, factor allocation time (us) and, after a vb_factor run with
+ * VB_KERNEL_TIMING=1 in the environment, the GEMM kernel time of that factorisation (us; else 0).
+ * Order: the keys of paper_2304_09770_b200.Context.stats. */
+vb_status vb_stats(const vb_ctx *ctx, int64_t *out26);
 /* Average per-launch device time (ms) of each timed launch category of the last vb_pcg_solve,
  * recorded with CUDA events on the library stream when VB_KERNEL_TIMING=1 in the environment. */
 vb_status vb_kernel_times(const vb_ctx *ctx, double *ms_out, int32_t n_max, int32_t *n_out);

@@ -282,12 +282,12 @@ class Context:
         return A, B
 
     def stats(self):
-        o = np.zeros(25, np.int64)
+        o = np.zeros(26, np.int64)
         self._check(_vb_stats(self._h, _ptr(o, ctypes.c_int64)))
         keys = ["n_dofs_paper", "n_free_vel", "n_pres", "n_sub", "n_ent", "n_gamma", "n_primal", "n_coarse",
                 "n_delta", "max_n", "max_nG", "max_nd", "n_edges", "bytes_per_iter", "nv_max", "n_colors",
                 "sum_pk_G", "sum_pk_D", "sum_dlx_sq", "sum_phi", "pk_coarse", "last_iterations", "n_cells",
-                "factor_gemm_flops", "factor_alloc_us"]
+                "factor_gemm_flops", "factor_alloc_us", "factor_gemm_us"]
         return dict(zip(keys, o.tolist()))
 
     def kernel_times(self):

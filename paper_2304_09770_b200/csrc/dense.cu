@@ -60,6 +60,22 @@ static void launch_gemm_cls(int cls, dim3 grid, const GemmProb *probs, const int
 static int trans_class(const GemmProb &p) { return (p.transA ? 1 : 0) + (p.transB ? 2 : 0); }
 
 thread_local double g_gemm_flops = 0.0;   // DMMA GEMM flops issued by this thread (factor-stage accounting)
+thread_local bool g_gemm_timing = false;  // record CUDA events around every GemmPlan::run (kernel time)
+thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_gemm_events;
+
+double gemm_timing_collect(cudaStream_t s) {
+  double ms = 0.0;
+  if (!g_gemm_events.empty()) VB_CUDA(cudaStreamSynchronize(s));
+  for (auto &e : g_gemm_events) {
+    float t = 0.0f;
+    VB_CUDA(cudaEventElapsedTime(&t, e.first, e.second));
+    ms += t;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  g_gemm_events.clear();
+  return ms / 1e3;
+}
 
 void GemmPlan::add(const GemmProb &p_in) {
   if (p_in.M <= 0 || p_in.N <= 0) return;
@@ -119,6 +135,12 @@ void GemmPlan::upload(cudaStream_t s) {
 }
 
 void GemmPlan::run(int launch, cudaStream_t s) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (g_gemm_timing) {
+    VB_CUDA(cudaEventCreate(&e0));
+    VB_CUDA(cudaEventCreate(&e1));
+    VB_CUDA(cudaEventRecord(e0, s));
+  }
   for (int c = 0; c < 4; ++c) {
     const auto &R = lrange[launch][c];
     if (R.second <= 0) continue;
@@ -135,6 +157,10 @@ void GemmPlan::run(int launch, cudaStream_t s) {
       launch_gemm_cls<true, true>(trans_class(p), grid, d_probs.p, d_tiles.p, pid, 0, s);
     else
       launch_gemm_cls<true, false>(trans_class(p), grid, d_probs.p, d_tiles.p, pid, 0, s);
+  }
+  if (g_gemm_timing) {
+    VB_CUDA(cudaEventRecord(e1, s));
+    g_gemm_events.push_back({e0, e1});
   }
 }
 

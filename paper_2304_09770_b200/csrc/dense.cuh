@@ -47,6 +47,8 @@ void gemm_grouped(GemmPlan &plan, int launch, cudaStream_t s);
 // process-wide kernel attribute, only ever raised (thread-safe; several contexts share kernels)
 void raise_smem_limit(const void *func, size_t bytes);
 extern thread_local double g_gemm_flops;   // flops of the GEMMs planned since the last reset
+extern thread_local bool g_gemm_timing;    // VB_KERNEL_TIMING: CUDA events around every GEMM launch set
+double gemm_timing_collect(cudaStream_t s);   // seconds of GEMM kernel time since the last collect
 
 // Partial LDL^T (no pivoting, velocity-first quasi-definite ordering) of a batch:
 // eliminates the first m columns; on exit the strictly lower part of those columns holds L, the

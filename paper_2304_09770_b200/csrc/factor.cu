@@ -1020,6 +1020,8 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
 void factor_device(vb_ctx *c) {
   cudaStream_t s = c->stream;
   g_gemm_flops = 0.0;
+  g_gemm_timing = getenv("VB_KERNEL_TIMING") && atoi(getenv("VB_KERNEL_TIMING"));
+  gemm_timing_collect(s);
   const double alloc0 = g_malloc_s + g_free_s;
   stage_time(c, nullptr);
   stage_dirichlet(c);
@@ -1055,6 +1057,8 @@ void factor_device(vb_ctx *c) {
   stage_time(c, "dual + coarse (A3-A5)");
   c->factor_flops = g_gemm_flops;
   c->factor_alloc_s = g_malloc_s + g_free_s - alloc0;
+  c->factor_gemm_s = g_gemm_timing ? gemm_timing_collect(s) : 0.0;
+  g_gemm_timing = false;
 }
 
 }  // namespace vb

@@ -354,5 +354,6 @@ struct vb_ctx {
   vb::DBuf<double> d_Kcs;            // distributed coarse: this rank's tile rows of the packed inverse
   int64_t coarse_tlo = 0, coarse_thi = 0;   // ... tile rows [tlo, thi) (balanced by tile count)
   double factor_flops = 0;     // DMMA GEMM flops of the last vb_factor
+  double factor_gemm_s = 0;    // their kernel time (CUDA events; VB_KERNEL_TIMING=1 only, else 0)
   double factor_alloc_s = 0;   // wall time of device allocation / release inside the last vb_factor
 };
