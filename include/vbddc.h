@@ -184,6 +184,16 @@ vb_status vb_apply_operator(vb_ctx *ctx, const double *x_dev, double *y_dev);
  * then one p_0 per subdomain.  Requires vb_factor.                                            */
 vb_status vb_debug_interface_op(vb_ctx *ctx, int32_t which, const double *in_host, double *out_host);
 
+/* Parity/debug (setup-stage gates): a dense operator of the rank-local subdomain
+ * `sub` (0-based, local order) in ORIGINAL local interface coordinates -- its interface entities in
+ * the library's order, each entity's free velocity DOFs increasing; ids (may be NULL) receives those
+ * free velocity ids:
+ *   which 0: S_Gamma^(i) (Eq.(firstSchur)), assembled back as T S_T T^T;
+ *   which 1: the deluxe-scaled local dual operator N_G (D S_DD^-1 D^T) N_G^T.
+ * out: host, nG x nG column-major, or NULL to query *n.  Requires vb_factor.                  */
+vb_status vb_debug_subdomain_op(vb_ctx *ctx, int32_t sub, int32_t which, int64_t *ids, double *out,
+                                int64_t *n);
+
 /* Parity/debug and microbenchmark: the factorisation's grouped DMMA GEMM on DEVICE buffers,
  *   C_b = alpha * op(A_b) * diag(d) * op(B_b) + beta * C_b,   b = 0 .. batch-1,
  * column-major, op(X) = X or X^T (trans* = 0/1), X_b = X + b * strideX (elements); d (length K,

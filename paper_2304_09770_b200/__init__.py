@@ -97,6 +97,7 @@ _vb_nccl_unique_id = _sig("vb_nccl_unique_id", ctypes.c_int, [_p])
 _vb_debug_iop = _sig("vb_debug_interface_op", ctypes.c_int, [_p, ctypes.c_int32, _dp, _dp])
 _vb_interface_dofs = _sig("vb_interface_dofs", ctypes.c_int, [_p, _i64p, _i64p])
 _vb_set_option = _sig("vb_set_option", ctypes.c_int, [_p, ctypes.c_char_p, ctypes.c_double])
+_vb_debug_subop = _sig("vb_debug_subdomain_op", ctypes.c_int, [_p, ctypes.c_int32, ctypes.c_int32, _i64p, _dp, _i64p])
 _vb_nccl_selftest = _sig("vb_debug_nccl_selftest", ctypes.c_int, [ctypes.c_int32, _dp])
 _vb_debug_gemm = _sig("vb_debug_gemm", ctypes.c_int,
                      [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, _p, ctypes.c_int32,
@@ -108,7 +109,8 @@ EXPORTED = ["vb_plan_exchange", "vb_nccl_unique_id", "vb_loopback_world_create",
             "vb_pcg_solve", "vb_pcg_solve_host", "vb_apply_operator", "vb_debug_interface_op", "vb_debug_gemm",
             "vb_interface_dofs", "vb_num_free_dofs", "vb_dof_layout",
             "vb_cell_local_dofs", "vb_get_element_matrices", "vb_stats", "vb_kernel_times",
-            "vb_kernel_time_name", "vb_last_error", "vb_destroy", "vb_set_option", "vb_debug_nccl_selftest"]
+            "vb_kernel_time_name", "vb_last_error", "vb_destroy", "vb_set_option", "vb_debug_nccl_selftest",
+            "vb_debug_subdomain_op"]
 
 
 class VBError(RuntimeError):
@@ -260,6 +262,18 @@ class Context:
         self._check(_vb_debug_iop(self._h, 0 if which == "S" else 1, _ptr(v, ctypes.c_double),
                                   _ptr(out, ctypes.c_double)))
         return out
+
+    def subdomain_op(self, sub, which):
+        """(free velocity ids, dense operator) of local subdomain `sub`: which 'S' = S_Gamma^(i),
+        'M' = N (D S_DD^-1 D^T) N^T (vb_debug_subdomain_op)."""
+        n = ctypes.c_int64()
+        w = 0 if which == "S" else 1
+        self._check(_vb_debug_subop(self._h, int(sub), w, None, None, ctypes.byref(n)))
+        ids = np.zeros(n.value, np.int64)
+        out = np.zeros((n.value, n.value))
+        self._check(_vb_debug_subop(self._h, int(sub), w, _ptr(ids, ctypes.c_int64), _ptr(out, ctypes.c_double),
+                                    ctypes.byref(n)))
+        return ids, out.T.copy()     # column-major -> row-major
 
     def dof_layout(self):
         ids = np.zeros(self.n_free, np.int64)

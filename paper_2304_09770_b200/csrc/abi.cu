@@ -521,6 +521,12 @@ vb_status vb_debug_interface_op(vb_ctx *c, int32_t which, const double *in, doub
   ABI_GUARD(c, { debug_interface_op(c, which, in, out); })
 }
 
+vb_status vb_debug_subdomain_op(vb_ctx *c, int32_t sub, int32_t which, int64_t *ids, double *out, int64_t *n) {
+  if (!c || !n) return VB_EINVAL;
+  if (c->state < 2) return fail(c, Error{VB_ESTATE, "vb_debug_subdomain_op before vb_factor"});
+  ABI_GUARD(c, { debug_subdomain_op(c, sub, which, ids, out, n); })
+}
+
 vb_status vb_interface_dofs(const vb_ctx *c, int64_t *ids, int64_t *n) {
   if (!c || !n) return VB_EINVAL;
   *n = c->nGamma;

@@ -52,6 +52,7 @@ void adaptive_enrich(vb_ctx *c, double tau, const DBuf<double> &sidebuf);   // a
 void pcg_device(vb_ctx *c, const double *rhs, double *x, double rtol, int maxit, vb_report *rep);
 void apply_operator_device(vb_ctx *c, const double *x, double *y);    // solve.cu (K7)
 void debug_interface_op(vb_ctx *c, int which, const double *in, double *out);   // solve.cu
+void debug_subdomain_op(vb_ctx *c, int sub, int which, int64_t *ids, double *out, int64_t *n);   // solve.cu
 void element_gather(vb_ctx *c, const double *yel, double *out);      // solve.cu: per-DOF sums
 const char *kernel_time_name(int i);                                  // solve.cu
 }  // namespace vb

@@ -1976,6 +1976,72 @@ void debug_interface_op(vb_ctx *c, int which, const double *in, double *out) {
   VB_CUDA(cudaStreamSynchronize(s));
 }
 
+// Parity/debug (setup-stage gates of SURVEY §8(c)): dense operators of local subdomain `sub` in
+// ORIGINAL local interface coordinates (its entities in slot order, each entity's free velocity
+// DOFs in increasing id; ids[] returns that order):
+//   which 0: S_Gamma^(i) = T S_T T^T from the packed S_T (T orthogonal, reading A9);
+//   which 1: the deluxe-scaled local dual operator N (D S_DD^-1 D^T) N^T from the packed
+//            D S_DD^-1 D^T (basis invariant: any orthonormal dual basis N_G gives the same matrix).
+// out: nG x nG column-major, or NULL to query *n (and ids).
+void debug_subdomain_op(vb_ctx *c, int sub, int which, int64_t *ids, double *out, int64_t *n) {
+  VB_REQUIRE(sub >= 0 && sub < c->N, VB_EINVAL, "subdomain index out of range");
+  VB_REQUIRE(which == 0 || which == 1, VB_EINVAL, "which must be 0 (S_Gamma) or 1 (local dual operator)");
+  const SubDev &S = c->h_sub[sub];
+  const int nG = S.nG;
+  *n = nG;
+  if (ids)
+    for (int q = S.slot_begin; q < S.slot_end; ++q) {
+      const SlotDev &sl = c->h_slot[c->h_sub_slots[q]];
+      const auto &dofs = c->ents[sl.ent].dofs;
+      for (int a = 0; a < sl.n; ++a) ids[sl.offG + a] = dofs[a];
+    }
+  if (!out) return;
+  cudaStream_t s = c->stream;
+  const int m = which == 0 ? nG : S.nd;
+  std::vector<double> pk(packed_size(m));
+  const double *src = which == 0 ? c->d_STp.p + S.off_STp : c->d_SDi.p + S.off_SDi;
+  VB_CUDA(cudaMemcpyAsync(pk.data(), src, pk.size() * 8, cudaMemcpyDeviceToHost, s));
+  std::vector<double> M((size_t)m * m, 0.0), T((size_t)nG * m, 0.0);
+  for (int q = S.slot_begin; q < S.slot_end; ++q) {
+    const SlotDev &sl = c->h_slot[c->h_sub_slots[q]];
+    std::vector<double> Te((size_t)sl.n * sl.n);
+    VB_CUDA(cudaMemcpyAsync(Te.data(), c->d_T.p + sl.off_T, Te.size() * 8, cudaMemcpyDeviceToHost, s));
+    VB_CUDA(cudaStreamSynchronize(s));
+    for (int a = 0; a < sl.n; ++a) {
+      for (int j = 0; j < sl.nd; ++j) T[(size_t)(sl.offD + j) * nG + sl.offG + a] = Te[a + (size_t)j * sl.n];
+      if (which == 0)
+        for (int j = 0; j < sl.r; ++j)
+          T[(size_t)(S.nd + sl.offPi + j) * nG + sl.offG + a] = Te[a + (size_t)(sl.nd + j) * sl.n];
+    }
+  }
+  VB_CUDA(cudaStreamSynchronize(s));
+  const int nt = (m + 31) / 32;
+  for (int I = 0; I < nt; ++I)
+    for (int J = 0; J <= I; ++J) {
+      const double *t = pk.data() + ptile_off(m, I, J);
+      const int rows = (I == nt - 1) ? m - 32 * (nt - 1) : 32;
+      for (int r = 0; r < rows; ++r)
+        for (int cc = 0; cc < 32; ++cc) {
+          const int i = 32 * I + r, j = 32 * J + cc;
+          if (j >= m || j > i) continue;
+          M[(size_t)j * m + i] = M[(size_t)i * m + j] = t[r * 32 + cc];
+        }
+    }
+  std::vector<double> TM((size_t)nG * m, 0.0);   // T M
+  for (int j = 0; j < m; ++j)
+    for (int k = 0; k < m; ++k) {
+      const double mk = M[(size_t)j * m + k];
+      if (mk == 0.0) continue;
+      for (int i = 0; i < nG; ++i) TM[(size_t)j * nG + i] += T[(size_t)k * nG + i] * mk;
+    }
+  for (int j = 0; j < nG; ++j)   // out = (T M) T^T
+    for (int i = 0; i < nG; ++i) {
+      double v = 0.0;
+      for (int k = 0; k < m; ++k) v += TM[(size_t)k * nG + i] * T[(size_t)k * nG + j];
+      out[(size_t)j * nG + i] = v;
+    }
+}
+
 // Extreme eigenvalues of the Lanczos tridiagonal (symmetric QL on the host; m <= maxit scalars).
 void lanczos_extremes(const std::vector<double> &al, const std::vector<double> &be, double *lmin, double *lmax) {
   int m = al.size();
