@@ -145,9 +145,18 @@ void layout_phase_a(vb_ctx *c) {
   const int stride = c->nv_max + c->np;
   std::vector<int> loc((size_t)c->nKl * stride, -1);
   std::vector<int64_t> posI(c->n_free_vel, -1);
+  // interface dof -> (local entity, position in the entity)
+  std::vector<int> dof_ent(c->n_free_vel, -1), dof_epos(c->n_free_vel, -1);
+  for (size_t e = 0; e < c->ents.size(); ++e)
+    for (size_t a = 0; a < c->ents[e].dofs.size(); ++a) {
+      dof_ent[c->ents[e].dofs[a]] = (int)e;
+      dof_epos[c->ents[e].dofs[a]] = (int)a;
+    }
+  std::vector<int> ent_slot(c->ents.size(), -1);   // entity -> its index t in the current subdomain
   for (int i = 0; i < N; ++i) {
     Sub &S = c->subs[i];
     for (int j = 0; j < S.nI; ++j) posI[S.I[j]] = j;
+    for (size_t t = 0; t < S.ents.size(); ++t) ent_slot[S.ents[t]] = (int)t;
     for (int cell : S.cells) {
       const int64_t Kg = c->cell_gid[cell];
       int *L = &loc[(size_t)cell * stride];
@@ -155,39 +164,43 @@ void layout_phase_a(vb_ctx *c) {
         int64_t f = c->vel2free[c->cell_l2g[j]];
         int q = j - c->cell_l2g_ptr[Kg];
         if (f < 0) continue;
-        if (posI[f] >= 0 && std::binary_search(S.I.begin(), S.I.end(), f)) {
+        if (dof_ent[f] < 0) {
+          VB_REQUIRE(posI[f] >= 0 && posI[f] < S.nI && S.I[posI[f]] == f, VB_EINVAL,
+                     "internal: interior dof not in its subdomain");
           L[q] = posI[f];
         } else {
-          // interface: find the entity of f among this subdomain's entities
-          for (size_t t = 0; t < S.ents.size(); ++t) {
-            const Entity &E = c->ents[S.ents[t]];
-            auto it = std::lower_bound(E.dofs.begin(), E.dofs.end(), f);
-            if (it != E.dofs.end() && *it == f) { L[q] = S.nD + S.ent_offG[t] + (int)(it - E.dofs.begin()); break; }
-          }
-          VB_REQUIRE(L[q] >= 0, VB_EINVAL, "internal: interface dof not found in its subdomain");
+          const int t = ent_slot[dof_ent[f]];
+          VB_REQUIRE(t >= 0 && S.ents[t] == dof_ent[f], VB_EINVAL, "internal: interface dof not found in its subdomain");
+          L[q] = S.nD + S.ent_offG[t] + dof_epos[f];
         }
       }
       int64_t p0 = std::lower_bound(S.P.begin(), S.P.end(), Kg * c->np) - S.P.begin();
       for (int a = 0; a < c->np; ++a) L[c->nv_max + a] = S.nI + p0 + a;
     }
+    for (size_t t = 0; t < S.ents.size(); ++t) ent_slot[S.ents[t]] = -1;
   }
   c->d_cell_loc.upload(loc, s);
   c->h_cell_loc = loc;
   // element-by-element operator / rhs: free velocity dof -> contribution slots (local cells, in order)
   {
-    std::vector<std::pair<int64_t, int64_t>> pr;
+    // counting sort by dof; within a dof the slots stay in (cell, local dof) order
+    std::vector<int64_t> ptr(c->n_free_vel + 1, 0);
     for (int64_t cell = 0; cell < c->nKl; ++cell) {
       const int64_t Kg = c->cell_gid[cell];
       for (int64_t j = c->cell_l2g_ptr[Kg]; j < c->cell_l2g_ptr[Kg + 1]; ++j) {
-        int64_t f = c->vel2free[c->cell_l2g[j]];
-        if (f >= 0) pr.push_back({f, cell * stride + (j - c->cell_l2g_ptr[Kg])});
+        const int64_t f = c->vel2free[c->cell_l2g[j]];
+        if (f >= 0) ptr[f + 1]++;
       }
     }
-    std::sort(pr.begin(), pr.end());
-    std::vector<int64_t> ptr(c->n_free_vel + 1, 0), idx(pr.size());
-    for (auto &q : pr) ptr[q.first + 1]++;
     for (int64_t i = 0; i < c->n_free_vel; ++i) ptr[i + 1] += ptr[i];
-    for (size_t q = 0; q < pr.size(); ++q) idx[q] = pr[q].second;
+    std::vector<int64_t> idx(ptr[c->n_free_vel]), fill(ptr.begin(), ptr.end() - 1);
+    for (int64_t cell = 0; cell < c->nKl; ++cell) {
+      const int64_t Kg = c->cell_gid[cell];
+      for (int64_t j = c->cell_l2g_ptr[Kg]; j < c->cell_l2g_ptr[Kg + 1]; ++j) {
+        const int64_t f = c->vel2free[c->cell_l2g[j]];
+        if (f >= 0) idx[fill[f]++] = cell * stride + (j - c->cell_l2g_ptr[Kg]);
+      }
+    }
     c->d_el_ptr.upload(ptr, s);
     c->d_el_ent.upload(idx, s);
     c->w_elt.alloc((size_t)c->nKl * stride);

@@ -215,15 +215,32 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t 
   c->nKl = c->cell_gid.size();
   c->subs.assign(N, Sub());
   for (int64_t l = 0; l < c->nKl; ++l) c->subs[c->sub_lid[cell_sub[c->cell_gid[l]]]].cells.push_back(l);
-  // (free dof, subdomain) pairs -> sharer sets (global)
+  // (free dof, subdomain) pairs -> sharer sets (global): counting sort by dof (O(cells x nv)), then
+  // each dof's few subdomain ids sorted and de-duplicated
   std::vector<std::pair<int64_t, int>> ds;
-  for (int64_t K = 0; K < c->nK; ++K)
-    for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) {
-      int64_t f = c->vel2free[c->cell_l2g[j]];
-      if (f >= 0) ds.push_back({f, cell_sub[K]});
+  {
+    std::vector<int64_t> cnt(c->n_free_vel + 1, 0);
+    for (int64_t K = 0; K < c->nK; ++K)
+      for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) {
+        const int64_t f = c->vel2free[c->cell_l2g[j]];
+        if (f >= 0) cnt[f + 1]++;
+      }
+    for (int64_t f = 0; f < c->n_free_vel; ++f) cnt[f + 1] += cnt[f];
+    std::vector<int> subs_of(cnt[c->n_free_vel]);
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    for (int64_t K = 0; K < c->nK; ++K)
+      for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) {
+        const int64_t f = c->vel2free[c->cell_l2g[j]];
+        if (f >= 0) subs_of[pos[f]++] = cell_sub[K];
+      }
+    ds.reserve(c->n_free_vel + c->n_free_vel / 4);
+    for (int64_t f = 0; f < c->n_free_vel; ++f) {
+      int *b = subs_of.data() + cnt[f], *e = subs_of.data() + cnt[f + 1];
+      std::sort(b, e);
+      e = std::unique(b, e);
+      for (int *q = b; q < e; ++q) ds.push_back({f, *q});
     }
-  std::sort(ds.begin(), ds.end());
-  ds.erase(std::unique(ds.begin(), ds.end()), ds.end());
+  }
   std::map<std::vector<int>, int> emap;
   std::vector<std::vector<int>> ekeys;
   std::vector<std::vector<int64_t>> edofs;
