@@ -245,24 +245,59 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
       out(row0 + L.fl2e(g, f, c, l)) += s * v;
     }
   };
-  // ================= volume Gram matrices
-  for (int i = 0; i < Dk1 * Dk1; ++i) G(i) = 0.0;
-  for (int i = 0; i < Dk * Dk; ++i) GnK(i) = 0.0;
+  // ================= volume Gram matrices, from the cell moments int m_e of degree <= 2k + 2 (one
+  // accumulator per distinct monomial, in registers/local memory, instead of one read-modify-write
+  // of the global scratch per Gram entry per quadrature point):
+  //   G_ab = int m_a m_b = mom[e_a + e_b],
+  //   GnK_ab = int grad m_a . grad m_b = sum_c (a_c b_c / h^2) mom[e_a + e_b - 2 e_c]   (a >= 1)
   {
+    constexpr int NM = d3(2 * K + 2);
+    double mom[NM];
+    for (int i = 0; i < NM; ++i) mom[i] = 0.0;
     QuadTet qt(nqv);
     for (int t = 0; t < g.ntet; ++t)
       for (int q = 0; q < qt.npts(); ++q) {
         double x[3], w;
         qt.point(g, t, q, x, &w);
-        double m[d3(K + 1)], gr[d3(K + 1)][3];
-        mono3g(x, g.xc, g.h, K + 1, m, gr);
-        for (int a = 0; a < Dk1; ++a)
-          for (int b = 0; b <= a; ++b) G(a * Dk1 + b) += w * m[a] * m[b];
-        for (int a = 1; a < Dk; ++a)
-          for (int b = 0; b < Dk; ++b) GnK(a * Dk + b) += w * (gr[a][0] * gr[b][0] + gr[a][1] * gr[b][1] + gr[a][2] * gr[b][2]);
+        double px[2 * K + 3], py[2 * K + 3], pz[2 * K + 3];
+        px[0] = py[0] = pz[0] = w;   // the weight folded into the x powers
+        py[0] = pz[0] = 1.0;
+        const double X = (x[0] - g.xc[0]) / g.h, Y = (x[1] - g.xc[1]) / g.h, Z = (x[2] - g.xc[2]) / g.h;
+        for (int p = 1; p <= 2 * K + 2; ++p) { px[p] = px[p - 1] * X; py[p] = py[p - 1] * Y; pz[p] = pz[p - 1] * Z; }
+        int j = 0;
+        for (int d = 0; d <= 2 * K + 2; ++d)
+          for (int a = d; a >= 0; --a)
+            for (int b = d - a; b >= 0; --b) mom[j++] += px[a] * py[b] * pz[d - a - b];
       }
-    for (int a = 0; a < Dk1; ++a)
-      for (int b = a + 1; b < Dk1; ++b) G(a * Dk1 + b) = G(b * Dk1 + a);
+    for (int a = 0; a < Dk1; ++a) {
+      int ea[3];
+      exp3(a, ea);
+      for (int b = 0; b <= a; ++b) {
+        int eb[3];
+        exp3(b, eb);
+        const double v = mom[idx3(ea[0] + eb[0], ea[1] + eb[1], ea[2] + eb[2])];
+        G(a * Dk1 + b) = v;
+        G(b * Dk1 + a) = v;
+      }
+    }
+    const double ih2 = 1.0 / (g.h * g.h);
+    for (int b = 0; b < Dk; ++b) GnK(b) = 0.0;
+    for (int a = 1; a < Dk; ++a) {
+      int ea[3];
+      exp3(a, ea);
+      for (int b = 0; b < Dk; ++b) {
+        int eb[3];
+        exp3(b, eb);
+        double v = 0.0;
+        for (int c = 0; c < 3; ++c) {
+          if (ea[c] == 0 || eb[c] == 0) continue;
+          int e[3] = {ea[0] + eb[0], ea[1] + eb[1], ea[2] + eb[2]};
+          e[c] -= 2;
+          v += ea[c] * eb[c] * ih2 * mom[idx3(e[0], e[1], e[2])];
+        }
+        GnK(a * Dk + b) = v;
+      }
+    }
     for (int f = 0; f < g.nf; ++f)
       for (int b = 0; b < Dk; ++b) GnK(b) += FM(f * Dk1 * q2k1 + b * q2k1 + 0);
   }
