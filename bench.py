@@ -132,7 +132,7 @@ def run_oracle_sample(steps, warmup):
                 sample="c5 sampled as c2: the oracle BDDC-PCG solve (B0+PCG+B8, setup excluded) on 64 of "
                        "c5's 512 subdomains (16^3 cells, 4^3 subdomains of 4^3 cells: the same subdomain "
                        "size, k, constraints and rtol; the oracle's per-iteration work is per subdomain, so "
-                       "DOF*it/s of the sample stands for c5; the oracle's c5 setup alone takes ~30 min), "
+                       "DOF*it/s of the sample stands for c5; the oracle's c5 setup alone takes ~18 min), "
                        "mean of %d solves" % steps)
 
 
