@@ -162,6 +162,14 @@ vb_status vb_pcg_solve(vb_ctx *ctx, const double *rhs_dev, double *x_dev, double
 /* Context options (host, any time after vb_setup):
  *   "true_residual" (0/1, default 0): vb_pcg_solve also fills vb_report.true_rel_residual
  *                   (one element-by-element K7 pass and two norms after the solve).
+ *   "p2p" (0/1, default 0; also VB_P2P=1; multi-rank only): the two interface exchanges of every
+ *                   PCG step (copies of p for S^ p, scaled extension products of z = M^-1 r;
+ *                   SURVEY §8(e) C1) become direct stores from the producing kernels into the
+ *                   peers' receive areas (NVLink peer memory mapped by CUDA IPC under NCCL, plain
+ *                   pointers under the loopback transport), followed by a stream barrier -- no
+ *                   pack kernel and no send/recv.  Read by vb_factor (collective: every rank the
+ *                   same value); VB_ESTATE after vb_factor, VB_EINVAL (from vb_factor) together
+ *                   with the VB_POOL allocator.  Results are bit-identical to the default path.
  * VB_EINVAL on an unknown name. */
 vb_status vb_set_option(vb_ctx *ctx, const char *name, double value);
 

@@ -214,7 +214,8 @@ class Context:
         self._check(_vb_factor(self._h))
 
     def set_option(self, name, value):
-        """vb_set_option: "true_residual" (0/1) -> vb_report.true_rel_residual through K7."""
+        """vb_set_option: "true_residual" (0/1) -> vb_report.true_rel_residual through K7;
+        "p2p" (0/1, before factor) -> peer-store interface exchanges in the PCG step."""
         self._check(_vb_set_option(self._h, name.encode(), float(value)))
 
     def build_rhs(self, problem, out):

@@ -351,6 +351,11 @@ vb_status vb_set_option(vb_ctx *c, const char *name, double value) {
     c->opt_true_residual = value != 0.0;
     return VB_OK;
   }
+  if (!strcmp(name, "p2p")) {
+    if (c->state >= 2) return fail(c, Error{VB_ESTATE, "option p2p is read by vb_factor: set it before"});
+    c->opt_p2p = value != 0.0;
+    return VB_OK;
+  }
   return fail(c, Error{VB_EINVAL, std::string("unknown option ") + name});
 }
 

@@ -74,8 +74,37 @@ static NcclApi &nccl() {
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
   bool capturable() const override { return true; }
+  DBuf<double> bar;                  // barrier operand (1 double per rank)
+  std::vector<void *> opened;        // peer allocations mapped by share_buffer
   ~NcclComm() override {
+    for (void *p : opened) cudaIpcCloseMemHandle(p);
     if (comm && nccl().CommDestroy) nccl().CommDestroy(comm);
+  }
+  // an allgather completes on a rank only after every rank has entered it, i.e. after every
+  // rank's earlier stream work (kernel completion flushes its peer stores)
+  void barrier(cudaStream_t s) override {
+    VB_NCCL(nccl().AllGather(bar.p + nranks, bar.p, 1, kNcclDouble, comm, s));
+  }
+  // CUDA IPC: each rank exports its allocation, the handles travel by allgather, every peer's
+  // allocation is mapped into this process (NVLink peer access enabled lazily by the driver)
+  void share_buffer(void *mine, std::vector<void *> &out, cudaStream_t s) override {
+    VB_REQUIRE(!g_use_pool, VB_EINVAL, "direct peer stores need cudaMalloc allocations (unset VB_POOL)");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    VB_CUDA(cudaIpcGetMemHandle(&h, mine));
+    DBuf<double> t;
+    t.alloc((size_t)8 * (nranks + 1));
+    VB_CUDA(cudaMemcpyAsync(t.p + 8 * nranks, &h, 64, cudaMemcpyHostToDevice, s));
+    VB_NCCL(nccl().AllGather(t.p + 8 * nranks, t.p, 8, kNcclDouble, comm, s));
+    std::vector<cudaIpcMemHandle_t> all(nranks);
+    VB_CUDA(cudaMemcpyAsync(all.data(), t.p, 64 * (size_t)nranks, cudaMemcpyDeviceToHost, s));
+    VB_CUDA(cudaStreamSynchronize(s));
+    out.assign(nranks, nullptr);
+    for (int r = 0; r < nranks; ++r) {
+      if (r == rank) { out[r] = mine; continue; }
+      VB_CUDA(cudaIpcOpenMemHandle(&out[r], all[r], cudaIpcMemLazyEnablePeerAccess));
+      opened.push_back(out[r]);
+    }
   }
   void exchange(const std::vector<PeerXfer> &x, const double *send, double *recv, cudaStream_t s) override {
     if (x.empty()) return;
@@ -124,6 +153,8 @@ Comm *make_nccl_comm(int rank, int nranks, const void *id128, int device) {
   fprintf(stderr, "[vb] NCCL communicator: rank %d nranks %d (ncclCommCount %d) device %d, NCCL %d\n", rank, nranks,
           cnt, device, ver);
   VB_REQUIRE(cnt < 0 || cnt == nranks, VB_ENCCL, "NCCL communicator size differs from nranks");
+  c->bar.alloc(nranks + 1);   // (not inside a capture: barrier() may be captured)
+  VB_CUDA(cudaMemset(c->bar.p, 0, (nranks + 1) * sizeof(double)));
   return c;
 }
 
@@ -161,7 +192,11 @@ void nccl_selftest(int device, double *result, std::string &msg) {
     selftest_step_kernel<<<1, 256, 0, s>>>(buf.p, n, counter.p);
     cm->exchange(self, buf.p, buf.p + n, s);
     cm->allgather(buf.p, buf.p + 2 * n, n, s);
+    cm->barrier(s);
   };
+  std::vector<void *> shared;   // IPC export of the buffer (the peer-store path's setup)
+  cm->share_buffer(buf.p, shared, s);
+  VB_REQUIRE(shared.size() == 1 && shared[0] == buf.p, VB_ENCCL, "share_buffer returned a wrong table");
   auto check = [&](int steps) {
     VB_CUDA(cudaMemcpyAsync(h.data(), buf.p, 3 * n * 8, cudaMemcpyDeviceToHost, s));
     VB_CUDA(cudaStreamSynchronize(s));
@@ -227,6 +262,7 @@ struct LoopWorld {
   bool broken = false;
   std::vector<const double *> send;
   std::vector<const std::vector<PeerXfer> *> xfer;
+  std::vector<void *> shared;
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     if (broken) throw Error{VB_ENCCL, "loopback world broken by another rank's failure"};
@@ -250,6 +286,7 @@ void *loopback_world_create(int nranks) {
   w->n = nranks;
   w->send.assign(nranks, nullptr);
   w->xfer.assign(nranks, nullptr);
+  w->shared.assign(nranks, nullptr);
   return w;
 }
 
@@ -277,6 +314,18 @@ struct LoopComm : Comm {
       VB_CUDA(cudaMemcpyAsync(recv + p.roff, w->send[p.peer] + mine->soff, p.rcount * 8, cudaMemcpyDeviceToDevice, s));
     }
     VB_CUDA(cudaStreamSynchronize(s));
+    w->barrier();
+  }
+  void barrier(cudaStream_t s) override {
+    VB_CUDA(cudaStreamSynchronize(s));
+    w->barrier();
+  }
+  // all ranks live in one process on one device: the pointers themselves
+  void share_buffer(void *mine, std::vector<void *> &out, cudaStream_t s) override {
+    VB_CUDA(cudaStreamSynchronize(s));
+    w->shared[rank] = mine;
+    w->barrier();
+    out = w->shared;
     w->barrier();
   }
   void allgather(const double *send, double *recv, int64_t count, cudaStream_t s) override {

@@ -26,6 +26,12 @@ struct Comm {
   virtual void exchange(const std::vector<PeerXfer> &x, const double *send, double *recv, cudaStream_t s) = 0;
   // every rank contributes `count` doubles; recv holds nranks * count in rank order
   virtual void allgather(const double *send, double *recv, int64_t count, cudaStream_t s) = 0;
+  // stream-ordered barrier: work any rank enqueued on its stream before the barrier (including
+  // stores into peer memory) is complete and visible before work any rank enqueues after it runs
+  virtual void barrier(cudaStream_t s) = 0;
+  // direct peer stores: out[r] = the address, usable from THIS rank's kernels, of the buffer
+  // rank r passed as `mine` (a cudaMalloc allocation base; out[rank] = mine).  Collective.
+  virtual void share_buffer(void *mine, std::vector<void *> &out, cudaStream_t s) = 0;
   virtual void abort() {}
   virtual bool capturable() const { return false; }   // may run inside CUDA stream capture
 };

@@ -116,6 +116,7 @@ void build_slot_exchange(vb_ctx *c, SlotExchange &X, const std::function<int64_t
   for (const PeerXfer &x : X.xfers)
     VB_REQUIRE(x.scount == ps[x.peer] && x.rcount == pr[x.peer], VB_EINVAL, "internal: exchange differs from its plan");
   X.send_idx.upload(sidx, c->stream);
+  X.h_send_idx = sidx;
   X.sendbuf.alloc(std::max<int64_t>(X.send_len, 1));
   VB_CUDA(cudaStreamSynchronize(c->stream));
 }
@@ -131,6 +132,53 @@ void run_slot_exchange(vb_ctx *c, SlotExchange &X, const double *local, double *
     VB_CHECK_LAUNCH();
   }
   c->comm->exchange(X.xfers, X.sendbuf.p, recv, c->stream);
+}
+
+void build_slot_p2p(vb_ctx *c, SlotExchange &X, double *alloc, int64_t recv_at, int64_t local_len) {
+  const int R = c->nranks, me = c->rank;
+  X.p2p = false;
+  if (R == 1) return;
+  cudaStream_t s = c->stream;
+  // table of every rank: [recv_at, receive offset of the payload from rank 0 .. R-1 (-1: none),
+  // its length from rank 0 .. R-1]  (int64 bit patterns moved as doubles)
+  const int W = 2 * R + 1;
+  std::vector<int64_t> mine(W, -1), all((size_t)R * W);
+  mine[0] = recv_at;
+  for (int r = 0; r < R; ++r) mine[1 + R + r] = 0;
+  for (const PeerXfer &x : X.xfers) {
+    mine[1 + x.peer] = x.roff;
+    mine[1 + R + x.peer] = x.rcount;
+  }
+  DBuf<double> t;
+  t.alloc((size_t)(R + 1) * W);
+  VB_CUDA(cudaMemcpyAsync(t.p + (size_t)R * W, mine.data(), W * 8, cudaMemcpyHostToDevice, s));
+  c->comm->allgather(t.p + (size_t)R * W, t.p, W, s);
+  VB_CUDA(cudaMemcpyAsync(all.data(), t.p, all.size() * 8, cudaMemcpyDeviceToHost, s));
+  std::vector<void *> base;
+  c->comm->share_buffer(alloc, base, s);   // (synchronises s)
+  std::vector<std::pair<int64_t, double *>> route;
+  for (const PeerXfer &x : X.xfers) {
+    if (!x.scount) continue;
+    const int64_t *T = all.data() + (size_t)x.peer * W;
+    VB_REQUIRE(T[1 + me] >= 0 && T[1 + R + me] == x.scount && base[x.peer], VB_ENCCL,
+               "peer-store plans disagree between ranks");
+    double *dst = (double *)base[x.peer] + T[0] + T[1 + me];
+    for (int64_t i = 0; i < x.scount; ++i) {
+      const int64_t j = X.h_send_idx[x.soff + i];
+      VB_REQUIRE(j >= 0 && j < local_len, VB_EINVAL, "internal: peer-store source outside the local buffer");
+      route.push_back({j, dst + i});
+    }
+  }
+  std::vector<int> ptr(local_len + 1, 0);
+  for (auto &r : route) ++ptr[r.first + 1];
+  for (int64_t j = 0; j < local_len; ++j) ptr[j + 1] += ptr[j];
+  std::vector<double *> dst(std::max<size_t>(route.size(), 1), nullptr);
+  std::vector<int> fill(ptr.begin(), ptr.end() - 1);
+  for (auto &r : route) dst[fill[r.first]++] = r.second;
+  X.p2p_ptr.upload(ptr, s);
+  X.p2p_dst.upload(dst, s);
+  VB_CUDA(cudaStreamSynchronize(s));
+  X.p2p = true;
 }
 
 __global__ void entity_sum_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ off,

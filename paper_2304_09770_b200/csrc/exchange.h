@@ -19,6 +19,13 @@ struct SlotExchange {
   // recv_off[ent_ptr[e] + k] = offset in the receive area of sharer k (position in E.sharers) of
   // local entity e, or -1 when that sharer is local
   std::vector<int64_t> ent_ptr, recv_off;
+  std::vector<int64_t> h_send_idx;   // host copy of send_idx
+  // direct peer stores (build_slot_p2p): the producing kernel stores local position j's value at
+  // every address p2p_dst[p2p_ptr[j] .. p2p_ptr[j+1]) (inside peers' receive areas), then a
+  // stream barrier replaces pack + send/recv
+  bool p2p = false;
+  DBuf<int> p2p_ptr;
+  DBuf<double *> p2p_dst;
 };
 
 // L(e): payload length per slot of local entity e; pos(slot, out): the local buffer positions of
@@ -36,6 +43,11 @@ void plan_slot_counts(const vb_ctx *c, const std::function<int64_t(int)> &L, int
 bool xch_sends(const vb_ctx *c, int e, int k, int mode);
 // pack from `local`, exchange, receive into `recv` (recv_len doubles).  No-op for one rank.
 void run_slot_exchange(vb_ctx *c, SlotExchange &X, const double *local, double *recv);
+// Direct peer stores for X (collective): `alloc` is this rank's cudaMalloc allocation holding the
+// receive area at element offset `recv_at`; local positions are < local_len.  Each rank learns
+// where its payload lands in every peer's receive area (the peer's recv offset for it) and maps
+// the peers' allocations (Comm::share_buffer).
+void build_slot_p2p(vb_ctx *c, SlotExchange &X, double *alloc, int64_t recv_at, int64_t local_len);
 
 // Per-entity sums over ALL sharers (global subdomain order) of slot payloads that live either in
 // a local buffer (contiguous per slot) or in the receive area of a SlotExchange:

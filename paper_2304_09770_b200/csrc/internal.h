@@ -334,6 +334,7 @@ struct vb_ctx {
   double bytes_per_iter = 0;
   // timing
   bool timing = false;
+  int opt_p2p = 0;                   // vb_set_option("p2p"): peer stores for the C1 exchanges of the PCG step
   int opt_true_residual = 0;         // vb_set_option("true_residual"): ||b - K x|| / ||b|| via K7
   std::vector<double> ktime_ms;
   std::vector<int> ktime_count;

@@ -174,12 +174,23 @@ static void split_rows(int n, int P, std::vector<std::pair<int, int>> &out, doub
 }
 
 // ------------------------------------------------------------------ small kernels of the loop
+// direct peer stores (SlotExchange::p2p): local position j's value also goes to every peer
+// address routed to j (NVLink stores into the peers' receive areas, overlapping the rest of the
+// producing kernel); a stream barrier follows the kernel.  rptr == nullptr: no routes.
+__device__ __forceinline__ void peer_store(const int *__restrict__ rptr, double *const *__restrict__ rdst,
+                                           int64_t j, double v) {
+  if (!rptr) return;
+  const int q1 = rptr[j + 1];
+  for (int q = rptr[j]; q < q1; ++q) rdst[q][0] = v;
+}
+
 // per local subdomain: s_j = sum over the P partial chunks of the packed GEMV (fixed order), plus
 // the b0 coupling on the primal coordinates: s_Pi += b~0 p0_i (Eq.(globInt) row 1); and
 // q0_i = b~0 . u_Pi^(i) (row 2), written to the rank-local p0 position of q.
 __global__ void chunk_sum_b0_kernel(const SubDev *__restrict__ subs, const double *__restrict__ part, int64_t stride,
                                     int P, const double *__restrict__ b0T, const int64_t *__restrict__ loc2x,
-                                    const double *__restrict__ p, int64_t p0off, double *sbuf, double *q) {
+                                    const double *__restrict__ p, int64_t p0off, double *sbuf, double *q,
+                                    const int *__restrict__ rptr, double *const *__restrict__ rdst) {
   pdl_prologue();
   const SubDev S = subs[blockIdx.y];
   const double p0 = p[p0off + blockIdx.y];
@@ -188,6 +199,7 @@ __global__ void chunk_sum_b0_kernel(const SubDev *__restrict__ subs, const doubl
     for (int c = 0; c < P; ++c) v += part[c * stride + S.off_G + j];
     if (j >= S.nd) v += b0T[S.off_Pi + (j - S.nd)] * p0;
     sbuf[S.off_G + j] = v;
+    peer_store(rptr, rdst, S.off_G + j, v);
   }
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     double acc = 0.0;
@@ -478,7 +490,8 @@ __global__ void coarse_p0_project_kernel(const double *__restrict__ vol, int N, 
 // product of subdomain i (thread per row of column-major Phi^, 4 accumulators)
 __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
                               const double *__restrict__ part, int64_t part_stride, int P,
-                              const int64_t *__restrict__ pi_glob, const double *__restrict__ uc, double *w) {
+                              const int64_t *__restrict__ pi_glob, const double *__restrict__ uc, double *w,
+                              const int *__restrict__ rptr, double *const *__restrict__ rdst) {
   pdl_prologue();
   const SubDev S = subs[blockIdx.y];
   const double *F = Phi + S.off_Phi;
@@ -498,7 +511,9 @@ __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ 
     a3 += F[j + (int64_t)(a + 3) * S.nd] * us[a + 3];
   }
   for (; a < S.npi; ++a) a0 += F[j + (int64_t)a * S.nd] * us[a];
-  w[S.off_Dv + j] = v + ((a0 + a1) + (a2 + a3));
+  const double t = v + ((a0 + a1) + (a2 + a3));
+  w[S.off_Dv + j] = t;
+  peer_store(rptr, rdst, S.off_Dv + j, t);
 }
 
 // ------------------------------------------------------------------ B0 / B8
@@ -1112,10 +1127,17 @@ static void apply_S(vb_ctx *c, SolveState *st, bool with_pq = false) {   // q = 
   tick(c, st, 0, false);
   int maxnG = 1;
   for (auto &S : c->h_sub) maxnG = std::max(maxnG, S.nG);
+  // peer stores only where a collective (the p.q sum) separates this receive from the next write
+  const bool p2p = with_pq && st->XS.p2p;
   launch_pdl(st, chunk_sum_b0_kernel, dim3((maxnG + 255) / 256, c->N), dim3(256), 0, s, c->d_sub.p, c->w_part.p, c->len_G, c->P_op,
                                                                      c->d_b0T.p, c->d_loc2x.p, c->w_p.p,
-                                                                     c->n_delta_glob + c->NPi, st->sx.p, c->w_q.p);
-  run_slot_exchange(c, st->XS, st->sx.p, st->sx.p + c->len_G);      // C1 (cross-rank copies)
+                                                                     c->n_delta_glob + c->NPi, st->sx.p, c->w_q.p,
+                                                                     p2p ? st->XS.p2p_ptr.p : nullptr,
+                                                                     p2p ? st->XS.p2p_dst.p : nullptr);
+  if (p2p)
+    c->comm->barrier(s);                                             // C1 (peer stores done)
+  else
+    run_slot_exchange(c, st->XS, st->sx.p, st->sx.p + c->len_G);    // C1 (cross-rank copies)
   int64_t nxp = c->n_delta_glob + c->NPi;
   if (with_pq) {   // q and the partial of p.q in one pass (C3 follows)
     launch_pdl(st, gather_src_dot_kernel, dim3(DOT_BLOCKS), dim3(256), 0, s, st->xptr.p, st->xidx.p, st->sx.p, nxp,
@@ -1147,6 +1169,8 @@ static void trace_norm(vb_ctx *c, const char *name, const double *v, int64_t n, 
 // z = M^-1 r  (B4-B7); fill_tail = false leaves z's coarse tail to dot_rz (fused with r.z)
 static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   cudaStream_t s = c->stream, s2 = st->s2;
+  // peer stores only inside the PCG step, where the r.z sum separates this receive from the next write
+  const bool p2p = !fill_tail && st->XE.p2p;
   tick(c, st, 4, true);
   // fork: the coarse branch (B6) runs on s2 while the local dual solves (B5) stream on s
   VB_CUDA(cudaEventRecord(st->ev_fork, s));
@@ -1185,9 +1209,13 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
   trace_norm(c, "uc", c->w_uc.p, c->Nc, true);
   launch_after_event(st, local2_kernel, dim3((st->max_nd + 127) / 128, c->N), dim3(128), c->max_npi * sizeof(double), s,
-      c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p);
+      c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p,
+      p2p ? st->XE.p2p_ptr.p : nullptr, p2p ? st->XE.p2p_dst.p : nullptr);
   trace_norm(c, "t", c->w_locD.p, c->len_Dv, false);
-  run_slot_exchange(c, st->XE, c->w_locD.p, c->w_locD.p + c->len_Dv);    // C1 (cross-rank products)
+  if (p2p)
+    c->comm->barrier(s);                                                  // C1 (peer stores done)
+  else
+    run_slot_exchange(c, st->XE, c->w_locD.p, c->w_locD.p + c->len_Dv);  // C1 (cross-rank products)
   run_entity_sum(c, st->ESE, c->w_locD.p, c->w_z.p);
   trace_norm(c, "zdual", c->w_z.p, c->n_delta_glob, false);
   if (fill_tail) dev_gather(c->w_uc.p, st->zmap.p, c->NPi + c->N, c->w_z.p + c->n_delta_glob, s);
@@ -1531,6 +1559,13 @@ void prepare_solve(vb_ctx *c) {
     st->cscal.alloc(std::max(N, 1));
   }
   st->g0abs.alloc(std::max(N, 1));
+  // direct peer stores for the two per-iteration interface exchanges (vb_set_option("p2p") or
+  // VB_P2P=1; collective: every rank factors with the same setting)
+  const char *pe = getenv("VB_P2P");
+  if ((c->opt_p2p || (pe && atoi(pe))) && c->nranks > 1) {
+    build_slot_p2p(c, st->XS, st->sx.p, c->len_G, c->len_G);
+    build_slot_p2p(c, st->XE, c->w_locD.p, c->len_Dv, c->len_Dv);
+  }
   VB_CUDA(cudaStreamSynchronize(s));
   st->ready = true;
   // bytes per PCG iteration (model of the streamed operators)
