@@ -486,12 +486,11 @@ __global__ void coarse_p0_project_kernel(const double *__restrict__ vol, int N, 
   for (int i = threadIdx.x; i < N; i += blockDim.x) v[i] -= mode == 0 ? vol[i] * mean : mean;
 }
 
-// t_i = sum_chunks y_i + Phi^_i u_Pi^(i) = D (S_DD^-1 D^T r_i + Phi_i u_Pi^(i)), the scaled extension
-// product of subdomain i (thread per row of column-major Phi^, 4 accumulators)
-__global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
-                              const double *__restrict__ part, int64_t part_stride, int P,
-                              const int64_t *__restrict__ pi_glob, const double *__restrict__ uc, double *w,
-                              const int *__restrict__ rptr, double *const *__restrict__ rdst) {
+// coarse extension DPhi_i u_Pi^(i) of subdomain i (thread per row of column-major DPhi, 4
+// accumulators): runs on the coarse stream right after the coarse solve, concurrently with the
+// local dual GEMV, so its DPhi read leaves the critical path
+__global__ void __launch_bounds__(128) coarse_ext_kernel(const SubDev *__restrict__ subs, const double *__restrict__ Phi,
+                              const int64_t *__restrict__ pi_glob, const double *__restrict__ uc, double *wc) {
   pdl_prologue();
   const SubDev S = subs[blockIdx.y];
   const double *F = Phi + S.off_Phi;
@@ -500,8 +499,6 @@ __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ 
   __syncthreads();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= S.nd) return;
-  double v = 0.0;
-  for (int c = 0; c < P; ++c) v += part[c * part_stride + S.off_Dv + j];
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int a = 0;
   for (; a + 3 < S.npi; a += 4) {
@@ -511,9 +508,22 @@ __global__ void __launch_bounds__(128) local2_kernel(const SubDev *__restrict__ 
     a3 += F[j + (int64_t)(a + 3) * S.nd] * us[a + 3];
   }
   for (; a < S.npi; ++a) a0 += F[j + (int64_t)a * S.nd] * us[a];
-  const double t = v + ((a0 + a1) + (a2 + a3));
-  w[S.off_Dv + j] = t;
-  peer_store(rptr, rdst, S.off_Dv + j, t);
+  wc[S.off_Dv + j] = (a0 + a1) + (a2 + a3);
+}
+
+// t_i = sum_chunks y_i + DPhi_i u_Pi^(i) = D (S_DD^-1 D^T r_i + Phi_i u_Pi^(i)), the scaled
+// extension product of subdomain i (its coarse part from coarse_ext_kernel)
+__global__ void local2_kernel(const double *__restrict__ part, int64_t part_stride, int P,
+                              const double *__restrict__ wc, int64_t n, double *w,
+                              const int *__restrict__ rptr, double *const *__restrict__ rdst) {
+  pdl_prologue();
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int c = 0; c < P; ++c) v += part[c * part_stride + j];
+    const double t = v + wc[j];
+    w[j] = t;
+    peer_store(rptr, rdst, j, t);
+  }
 }
 
 // ------------------------------------------------------------------ B0 / B8
@@ -1205,12 +1215,14 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
     launch_pdl(st, sum_chunks_kernel, dim3((c->Nc + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
   }
   launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
+  launch_pdl(st, coarse_ext_kernel, dim3((st->max_nd + 127) / 128, c->N), dim3(128), c->max_npi * sizeof(double), s2,
+             c->d_sub.p, c->d_Phi.p, c->d_pi_glob.p, c->w_uc.p, c->w_locC.p);
   VB_CUDA(cudaEventRecord(st->ev_join, s2));
   VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
   trace_norm(c, "uc", c->w_uc.p, c->Nc, true);
-  launch_after_event(st, local2_kernel, dim3((st->max_nd + 127) / 128, c->N), dim3(128), c->max_npi * sizeof(double), s,
-      c->d_sub.p, c->d_Phi.p, c->w_locY.p, c->len_Dv, c->P_loc, c->d_pi_glob.p, c->w_uc.p, c->w_locD.p,
-      p2p ? st->XE.p2p_ptr.p : nullptr, p2p ? st->XE.p2p_dst.p : nullptr);
+  launch_after_event(st, local2_kernel, dim3(grid_for(c->len_Dv)), dim3(256), 0, s, c->w_locY.p, c->len_Dv, c->P_loc,
+                     c->w_locC.p, c->len_Dv, c->w_locD.p, p2p ? st->XE.p2p_ptr.p : nullptr,
+                     p2p ? st->XE.p2p_dst.p : nullptr);
   trace_norm(c, "t", c->w_locD.p, c->len_Dv, false);
   if (p2p)
     c->comm->barrier(s);                                                  // C1 (peer stores done)
@@ -1258,6 +1270,7 @@ void prepare_solve(vb_ctx *c) {
   c->w_x.alloc(nx); c->w_r.alloc(nx); c->w_z.alloc(nx); c->w_p.alloc(nx); c->w_q.alloc(nx);
   c->w_part.alloc((int64_t)c->P_op * std::max<int64_t>(c->len_G, 1));
   c->w_locD.alloc(std::max<int64_t>(c->len_Dv, 1));
+  c->w_locC.alloc(std::max<int64_t>(c->len_Dv, 1));
   c->w_locY.alloc((int64_t)c->P_loc * std::max<int64_t>(c->len_Dv, 1));
   c->w_uc.alloc(c->Nc); c->w_rc.alloc(c->Nc);
   if (c->nranks > 1) { st->ucp.alloc(c->Nc); st->ucg.alloc((int64_t)c->Nc * c->nranks); }
