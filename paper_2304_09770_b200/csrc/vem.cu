@@ -59,10 +59,10 @@ struct Arena {
   static constexpr int q2k = d2(K), q2k1 = d2(K + 1), nm = d2(K - 2), NLM = MAXL * K + 3 * d2(K - 2);
   static constexpr int S3 = 3 * Dk;
   int64_t PF, FM, FW, G, GnK, DIV, RDV, M2, PIN, MK, P0, GR, E, GE, DP, Q, QP, WK, TT, ACD, total;
-  __host__ __device__ Arena(int nv) {
+  __host__ __device__ Arena(int nv, int nf) {   // nv, nf: the largest cell of the launch
     int64_t o = 0;
-    PF = o; o += (int64_t)MAXF * 3 * q2k1 * NLM;
-    FM = o; o += (int64_t)MAXF * Dk1 * q2k1;
+    PF = o; o += (int64_t)nf * 3 * q2k1 * NLM;
+    FM = o; o += (int64_t)nf * Dk1 * q2k1;
     FW = o; o += q2k * q2k + q2k1 * q2k1 + 2 * q2k1 * NLM + q2k1 * q2k1;
     G = o; o += Dk1 * Dk1;
     GnK = o; o += Dk * Dk;
@@ -112,7 +112,7 @@ __device__ inline void for_d4(Fn fn) {
 template <int K>
 __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict__ topo, const double *__restrict__ xyz,
                                                           const double *__restrict__ nu, int64_t K0, int64_t nE,
-                                                          int nvmax, double *scratch, int64_t NE, double *elA,
+                                                          int nvmax, int nfmax, double *scratch, int64_t NE, double *elA,
                                                           double *elB, double *P0out) {
   using Ar = Arena<K>;
   constexpr int D1 = Ar::D1, Dk = Ar::Dk, Dk1 = Ar::Dk1, D2m = Ar::D2m, q2k = Ar::q2k, q2k1 = Ar::q2k1;
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
   const Lay L(g, K);
   const int nv = L.nv;
   const double nuK = nu[cell];
-  const Ar ar(nvmax);
+  const Ar ar(nvmax, nfmax);
   auto S = [&](int64_t off) { return SM{scratch + off * NE + e, NE}; };
   const SM PF = S(ar.PF), FM = S(ar.FM), G = S(ar.G), GnK = S(ar.GnK), DIV = S(ar.DIV), RDV = S(ar.RDV);
   const SM M2 = S(ar.M2), PIN = S(ar.PIN), MK = S(ar.MK), P0 = S(ar.P0), GR = S(ar.GR), E = S(ar.E), GE = S(ar.GE);
@@ -588,16 +588,27 @@ void element_matrices_device(vb_ctx *c) {
   c->d_elA.alloc((size_t)c->nKl * nvm * nvm);
   c->d_elB.alloc((size_t)c->nKl * c->np * nvm);
   c->d_P0.alloc((size_t)c->nKl * S3 * nvm);
-  const int64_t per = c->k == 2 ? Arena<2>(nvm).total : (c->k == 3 ? Arena<3>(nvm).total : Arena<4>(nvm).total);
-  int64_t NE = std::max<int64_t>(128, std::min<int64_t>(c->nKl, (int64_t)(3.0e9 / 8 / per)));
+  int nfm = 1;
+  for (int64_t l = 0; l < c->nKl; ++l) nfm = std::max(nfm, c->cell_topo[c->cell_gid[l] * TOPO_STRIDE + 2]);
+  const int64_t per = c->k == 2 ? Arena<2>(nvm, nfm).total
+                                : (c->k == 3 ? Arena<3>(nvm, nfm).total : Arena<4>(nvm, nfm).total);
+  // all cells in one launch when the scratch fits (one thread per cell: a launch needs every cell it
+  // can get to fill 148 SMs), else chunks within a third of the free memory, at most 24 GB
+  size_t fr = 0, tot = 0;
+  VB_CUDA(cudaMemGetInfo(&fr, &tot));
+  const double budget = std::min(24e9, fr / 3.0);
+  int64_t NE = std::max<int64_t>(128, std::min<int64_t>(c->nKl, (int64_t)(budget / 8 / per)));
   NE = (NE + 127) / 128 * 128;
   DBuf<double> scratch;
   scratch.alloc((size_t)per * NE);
+  // threads per block: one cell per thread, so the block size only sets how evenly the cells
+  // spread over the 148 SMs (VB_K9_BLOCK: experiment knob)
+  static const int k9_block = getenv("VB_K9_BLOCK") ? std::max(32, std::min(128, atoi(getenv("VB_K9_BLOCK")))) : 64;
   for (int64_t K0 = 0; K0 < c->nKl; K0 += NE) {
     const int64_t n = std::min<int64_t>(NE, c->nKl - K0);
-    const int blocks = (n + 127) / 128;
+    const int blocks = (int)((n + k9_block - 1) / k9_block);
 #define VB_K9(KK)                                                                                           \
-  vem_element_kernel<KK><<<blocks, 128, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, K0, n, nvm, scratch.p, NE, \
+  vem_element_kernel<KK><<<blocks, k9_block, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, K0, n, nvm, nfm, scratch.p, NE, \
                                                 c->d_elA.p, c->d_elB.p, c->d_P0.p)
     if (c->k == 2) VB_K9(2);
     else if (c->k == 3) VB_K9(3);
