@@ -170,6 +170,15 @@ vb_status vb_pcg_solve(vb_ctx *ctx, const double *rhs_dev, double *x_dev, double
  *                   pack kernel and no send/recv.  Read by vb_factor (collective: every rank the
  *                   same value); VB_ESTATE after vb_factor, VB_EINVAL (from vb_factor) together
  *                   with the VB_POOL allocator.  Results are bit-identical to the default path.
+ *   "coarse_dissection" (1 on, 0 off, -1 auto = the default: on for nranks > 1; SURVEY f1,
+ *                   DESIGN.md §9): the coarse saddle problem by block elimination -- each
+ *                   rank eliminates the primal DOFs of entities all of whose sharers it owns
+ *                   (explicit local inverse and coupling kept packed), and only the separator
+ *                   primal DOFs between rank boxes plus every p_0 form the root problem that all
+ *                   ranks assemble (allgathered Schur contributions, rank order), factor and
+ *                   invert (sliced over ranks).  Off: the whole N_c x N_c coarse matrix is
+ *                   assembled, factored and inverted on every rank.  Same solution up to rounding.
+ *                   Read by vb_factor (collective: every rank the same value); VB_ESTATE after it.
  * VB_EINVAL on an unknown name. */
 vb_status vb_set_option(vb_ctx *ctx, const char *name, double value);
 
@@ -224,11 +233,11 @@ vb_status vb_dof_layout(const vb_ctx *ctx, int64_t *global_ids);   /* free -> gl
 vb_status vb_cell_local_dofs(const vb_ctx *ctx, int64_t cell, int64_t *vel_ids, int32_t *n_vel,
                              int64_t *p_ids, int32_t *n_p);       /* local order -> global id  */
 vb_status vb_get_element_matrices(const vb_ctx *ctx, int64_t cell, double *A, double *B);
-/* 26 counters (host-owned out26): sizes of the decomposition and operators, bytes per iteration,
+/* 28 counters (host-owned out28): sizes of the decomposition and operators, bytes per iteration,
  * factor GEMM flops, factor allocation time (us) and, after a vb_factor run with
  * VB_KERNEL_TIMING=1 in the environment, the GEMM kernel time of that factorisation (us; else 0).
  * Order: the keys of paper_2304_09770_b200.Context.stats. */
-vb_status vb_stats(const vb_ctx *ctx, int64_t *out26);
+vb_status vb_stats(const vb_ctx *ctx, int64_t *out28);
 /* Average per-launch device time (ms) of each timed launch category of the last vb_pcg_solve,
  * recorded with CUDA events on the library stream when VB_KERNEL_TIMING=1 in the environment. */
 vb_status vb_kernel_times(const vb_ctx *ctx, double *ms_out, int32_t n_max, int32_t *n_out);

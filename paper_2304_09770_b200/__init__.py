@@ -215,7 +215,8 @@ class Context:
 
     def set_option(self, name, value):
         """vb_set_option: "true_residual" (0/1) -> vb_report.true_rel_residual through K7;
-        "p2p" (0/1, before factor) -> peer-store interface exchanges in the PCG step."""
+        "p2p" (0/1, before factor) -> peer-store interface exchanges in the PCG step;
+        "coarse_dissection" (1/0/-1 auto, before factor) -> rank-level dissection of the coarse problem."""
         self._check(_vb_set_option(self._h, name.encode(), float(value)))
 
     def build_rhs(self, problem, out):
@@ -297,12 +298,12 @@ class Context:
         return A, B
 
     def stats(self):
-        o = np.zeros(26, np.int64)
+        o = np.zeros(28, np.int64)
         self._check(_vb_stats(self._h, _ptr(o, ctypes.c_int64)))
         keys = ["n_dofs_paper", "n_free_vel", "n_pres", "n_sub", "n_ent", "n_gamma", "n_primal", "n_coarse",
                 "n_delta", "max_n", "max_nG", "max_nd", "n_edges", "bytes_per_iter", "nv_max", "n_colors",
                 "sum_pk_G", "sum_pk_D", "sum_dlx_sq", "sum_phi", "pk_coarse", "last_iterations", "n_cells",
-                "factor_gemm_flops", "factor_alloc_us", "factor_gemm_us"]
+                "factor_gemm_flops", "factor_alloc_us", "factor_gemm_us", "n_coarse_root", "n_coarse_local"]
         return dict(zip(keys, o.tolist()))
 
     def kernel_times(self):

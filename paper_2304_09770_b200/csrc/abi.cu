@@ -351,6 +351,11 @@ vb_status vb_set_option(vb_ctx *c, const char *name, double value) {
     c->opt_true_residual = value != 0.0;
     return VB_OK;
   }
+  if (!strcmp(name, "coarse_dissection")) {
+    if (c->state >= 2) return fail(c, Error{VB_ESTATE, "option coarse_dissection is read by vb_factor: set it before"});
+    c->opt_coarse_dis = value < 0 ? -1 : (value != 0.0);
+    return VB_OK;
+  }
   if (!strcmp(name, "p2p")) {
     if (c->state >= 2) return fail(c, Error{VB_ESTATE, "option p2p is read by vb_factor: set it before"});
     c->opt_p2p = value != 0.0;
@@ -605,10 +610,11 @@ vb_status vb_stats(const vb_ctx *c, int64_t *o) {
   int64_t pkG = 0, pkD = 0, ndsq = 0, ndpi = 0;
   for (auto &S : c->h_sub) { pkG += (int64_t)S.nG * (S.nG + 1) / 2; pkD += (int64_t)S.nd * (S.nd + 1) / 2; ndpi += (int64_t)S.nd * S.npi; }
   for (auto &sl : c->h_slot) ndsq += (int64_t)sl.nd * sl.nd;
-  int64_t v[26] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
+  int64_t v[28] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
                    c->NPi_g, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max,
-                   c->ncolors, pkG, pkD, ndsq, ndpi, (c->nranks > 1 ? (int64_t)c->d_Kcs.n : c->Nc * (c->Nc + 1) / 2), c->last_iterations, c->nK,
-                   (int64_t)c->factor_flops, (int64_t)(c->factor_alloc_s * 1e6), (int64_t)(c->factor_gemm_s * 1e6)};
+                   c->ncolors, pkG, pkD, ndsq, ndpi, (c->nranks > 1 ? (int64_t)c->d_Kcs.n : (c->cdis ? c->Nroot * (c->Nroot + 1) / 2 : c->Nc * (c->Nc + 1) / 2)), c->last_iterations, c->nK,
+                   (int64_t)c->factor_flops, (int64_t)(c->factor_alloc_s * 1e6), (int64_t)(c->factor_gemm_s * 1e6),
+                   c->cdis ? c->Nroot : 0, c->cdis ? c->cd_nloc : 0};
   memcpy(o, v, sizeof(v));
   return VB_OK;
 }

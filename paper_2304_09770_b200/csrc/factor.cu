@@ -339,6 +339,51 @@ __global__ void coarse_assemble_kernel2(const int *__restrict__ color_subs, cons
   }
 }
 
+// f1 (coarse dissection): this rank's coarse matrix on [interior | pad | separator + p_0] from the
+// pieces of one colour class of its LOCAL subdomains (lmap: piece row -> local position)
+__global__ void coarse_assemble_local_kernel(const int *__restrict__ lsubs, const int64_t *__restrict__ lpoff,
+                                             const int *__restrict__ lnpi, const int64_t *__restrict__ mapoff,
+                                             const int64_t *__restrict__ lmap, const int64_t *__restrict__ p0pos,
+                                             const double *__restrict__ buf, double *K, int64_t ld) {
+  const int i = lsubs[blockIdx.y];
+  const int npi = lnpi[i];
+  const double *Sc = buf + lpoff[i];
+  const double *b0 = Sc + (int64_t)npi * npi;
+  const int64_t *g = lmap + mapoff[i];
+  const int64_t p = p0pos[i];
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < npi * npi; idx += gridDim.x * blockDim.x) {
+    const int a = idx % npi, b = idx / npi;
+    K[g[a] + g[b] * ld] += Sc[idx];
+  }
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < npi; a += gridDim.x * blockDim.x) {
+    K[p + g[a] * ld] += b0[a];
+    K[g[a] + p * ld] += b0[a];
+  }
+}
+
+__global__ void unit_diag_kernel(double *K, int64_t ld, int64_t lo, int64_t hi) {
+  for (int64_t j = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < hi; j += (int64_t)gridDim.x * blockDim.x)
+    K[j + j * ld] = 1.0;
+}
+
+// dst (n x n, ld dst_ld) = the symmetric matrix whose lower triangle is src's
+__global__ void copy_sym_lower_kernel(const double *__restrict__ src, int64_t lds, int64_t n, double *dst, int64_t ldd) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = idx % n, b = idx / n;
+    dst[a + b * ldd] = a >= b ? src[a + b * lds] : src[b + a * lds];
+  }
+}
+
+// root += one rank's Schur contribution (n x n, ld ldp) at root positions rp (one launch per rank,
+// ranks in order: the summation order is fixed and the same on every rank)
+__global__ void root_scatter_add_kernel(const double *__restrict__ piece, int64_t ldp, int64_t n,
+                                        const int64_t *__restrict__ rp, double *Kr, int64_t ldr) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = idx % n, b = idx / n;
+    Kr[rp[a] + rp[b] * ldr] += piece[a + b * ldp];
+  }
+}
+
 // ------------------------------------------------------------------ host orchestration
 static void sync(vb_ctx *c) { VB_CUDA(cudaStreamSynchronize(c->stream)); }
 
@@ -649,6 +694,311 @@ static void stage_interface(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumb
   sync(c);
 }
 
+// VB_CD_DUMP=<dir>: debug dumps of the coarse matrices (dense Kc, the dissection root and lists)
+static void cd_dump(vb_ctx *c, const char *name, const double *dev, int64_t rows, int64_t cols, int64_t ld) {
+  const char *dir = getenv("VB_CD_DUMP");
+  if (!dir) return;
+  std::vector<double> h(rows * cols);
+  VB_CUDA(cudaStreamSynchronize(c->stream));
+  VB_CUDA(cudaMemcpy2D(h.data(), rows * 8, dev, ld * 8, rows * 8, cols, cudaMemcpyDeviceToHost));
+  std::string f = std::string(dir) + "/" + name + "_r" + std::to_string(c->rank) + ".bin";
+  FILE *fp = fopen(f.c_str(), "wb");
+  if (!fp) return;
+  int64_t hd[2] = {rows, cols};
+  fwrite(hd, 8, 2, fp);
+  fwrite(h.data(), 8, h.size(), fp);
+  fclose(fp);
+}
+static void cd_dump_i(vb_ctx *c, const char *name, const std::vector<int64_t> &v) {
+  const char *dir = getenv("VB_CD_DUMP");
+  if (!dir) return;
+  std::string f = std::string(dir) + "/" + name + "_r" + std::to_string(c->rank) + ".bin";
+  FILE *fp = fopen(f.c_str(), "wb");
+  if (!fp) return;
+  int64_t hd[2] = {(int64_t)v.size(), 1};
+  fwrite(hd, 8, 2, fp);
+  fwrite(v.data(), 8, v.size(), fp);
+  fclose(fp);
+}
+
+// Explicit inverse of an LDL^T-factored coarse (or dissection root) matrix of order n, packed
+// (DESIGN.md §9): (K)^-1 = W^T D^-1 W with W = L^-1.  One rank keeps all of it; with R ranks,
+// rank r computes and keeps only the tile rows [tlo, thi) of the packed symmetric inverse (a
+// contiguous slice of the 1-rank layout, split by tile count), from the row block
+// (W[:, lo:hi])^T D^-1 W[:, :hi] (W lower triangular: k >= lo suffices).  The solve streams the
+// slice with the packed GEMV (row and transpose parts) and sums the ranks' partial vectors in rank
+// order (C2): n^2 / (2R) doubles per rank per iteration.
+static void coarse_inverse_pack(vb_ctx *c, DBuf<double> &Kc, int64_t ldC, int64_t Nc) {
+  cudaStream_t s = c->stream;
+  DBuf<double> Wc, dc;
+  Wc.alloc(ldC * Nc);
+  Wc.zero(s);
+  tri_inverse_batched({TriDesc{Kc.p, (int)ldC, Wc.p, (int)ldC, (int)Nc}}, s);
+  dc.alloc(Nc);
+  recip_diag_kernel<<<(Nc + 255) / 256, 256, 0, s>>>(Kc.p, ldC, Nc, dc.p);
+  VB_STAGE();
+  if (c->nranks == 1) {
+    GemmPlan plan;
+    int l0 = plan.begin_launch();
+    GemmProb p{};
+    p.A = Wc.p; p.lda = ldC; p.transA = 1; p.d = dc.p; p.dstride = 1;
+    p.B = Wc.p; p.ldb = ldC; p.C = Kc.p; p.ldc = ldC;
+    p.M = p.N = p.K = Nc; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
+    p.kz_on = 8;   // W lower triangular (site bit 8)
+    plan.add(p);
+    plan.upload(s);
+    plan.run(l0, s);
+    sync(c);
+    c->d_Kcp.alloc(packed_size(Nc));
+    pack_tiles_batched({PackDesc{Kc.p, (int)Nc, (int)ldC, c->d_Kcp.p}}, s);
+  } else {
+    const int64_t nt = (Nc + 31) / 32, R = c->nranks;
+    std::vector<int64_t> T(R + 1, nt);
+    T[0] = 0;
+    const double total = (double)nt * (nt + 1) / 2;
+    for (int64_t r = 1, I = 0; r < R; ++r) {
+      while (I < nt && (double)(I + 1) * (I + 2) / 2 < total * r / R) ++I;
+      T[r] = std::max(T[r - 1], std::min<int64_t>(nt, I + 1));
+    }
+    c->coarse_tlo = T[c->rank];
+    c->coarse_thi = T[c->rank + 1];
+    const int64_t lo = 32 * c->coarse_tlo, hi = std::min<int64_t>(Nc, 32 * c->coarse_thi), mine = hi - lo;
+    const int64_t slice = c->coarse_thi == nt ? packed_size(Nc) - ptile_row_start(c->coarse_tlo)
+                                              : ptile_row_start(c->coarse_thi) - ptile_row_start(c->coarse_tlo);
+    c->d_Kcs.alloc(std::max<int64_t>(slice, 1));
+    if (mine > 0) {
+      DBuf<double> Kr;
+      Kr.alloc(mine * hi);
+      GemmPlan plan;
+      int l0 = plan.begin_launch();
+      GemmProb p{};
+      p.A = Wc.p + lo * ldC + lo; p.lda = ldC; p.transA = 1; p.d = dc.p + lo; p.dstride = 1;
+      p.B = Wc.p + lo; p.ldb = ldC; p.C = Kr.p; p.ldc = mine;
+      p.M = mine; p.N = hi; p.K = Nc - lo; p.alpha = 1.0; p.beta = 0.0;
+      p.kz_on = 16; p.kzB = (int)-lo;   // (site bit 16)   // W(lo + k, lo + i) = 0 for k < i, W(lo + k, j) = 0 for k < j - lo
+      plan.add(p);
+      plan.upload(s);
+      plan.run(l0, s);
+      pack_rows_kernel<<<dim3(c->coarse_thi, c->coarse_thi - c->coarse_tlo), 256, 0, s>>>(
+          Kr.p, mine, lo, Nc, c->coarse_tlo, c->d_Kcs.p);
+      sync(c);
+    }
+    VB_STAGE();
+  }
+}
+
+// rank-level dissection of the coarse saddle problem (solved by block
+// elimination).  The primal DOFs of an entity whose sharers all live on rank r are
+// interior to r: only r's subdomains contribute to their rows and columns, so r eliminates them
+// alone.  The other primal DOFs (the separator between rank boxes) and every p_0 (coupled globally
+// by the gauge augmentation -gamma m m^T, reading A5) form the root.  Rank r keeps E = A_II^-1 and
+// F^T = A_SI A_II^-1 = L_SI L_II^-1 (its partial LDL^T gives A_SI = L_SI D L_II^T), packed as one
+// symmetric matrix [[E, .], [F^T, 0]]; the root Schur complement sum_r (A_SS^(r) - A_SI A_II^-1
+// A_IS) - gamma m m^T is assembled on every rank from the allgathered contributions (summed in
+// rank order) and inverted like the dense coarse matrix (coarse_inverse_pack, sliced over ranks).
+// Solve: y_I = E g_I, t = F^T g_I (one GEMV); x_S = S^-1 (g_S - sum_r t_r); x_I = y_I - F x_S.
+// Velocity DOFs first in the local and the root orderings (A_II SPD; the root's pressure Schur
+// complement negative definite: the pivot test of ldl_panel).
+static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector<int64_t> &lpoff,
+                              const std::vector<int> &gnpi, const std::vector<int64_t> &pimoff,
+                              const std::vector<int64_t> &pimap, double gam_c) {
+  cudaStream_t s = c->stream;
+  const int R = c->nranks, me = c->rank, Ng = c->Ng, N = c->N;
+  const int64_t NPi = c->NPi_g, Nc = c->Nc;
+  const int ne = c->gents.size();
+  std::vector<int> erank(ne, -1);   // the one rank of all sharers, or -1 (separator)
+  for (int e = 0; e < ne; ++e) {
+    const GEnt &E = c->gents[e];
+    if (E.r <= 0 || E.sharers.empty()) continue;
+    int r0 = c->sub_rank[E.sharers[0]];
+    for (int g : E.sharers)
+      if (c->sub_rank[g] != r0) { r0 = -1; break; }
+    erank[e] = r0;
+  }
+  std::vector<int64_t> root, Iglob;
+  for (int e = 0; e < ne; ++e) {
+    const GEnt &E = c->gents[e];
+    if (E.r <= 0) continue;
+    for (int t = 0; t < E.r; ++t) {
+      if (erank[e] < 0) root.push_back(E.off_pi + t);
+      else if (erank[e] == me) Iglob.push_back(E.off_pi + t);
+    }
+  }
+  std::sort(root.begin(), root.end());
+  std::sort(Iglob.begin(), Iglob.end());
+  const int64_t nsep = root.size();
+  for (int g = 0; g < Ng; ++g) root.push_back(NPi + g);
+  const int64_t nroot = root.size();
+  std::vector<int64_t> rpos(Nc, -1);
+  for (int64_t j = 0; j < nroot; ++j) rpos[root[j]] = j;
+  // every rank's root list: the separator DOFs its subdomains touch (sorted), then its p_0's
+  std::vector<std::vector<int64_t>> Sr(R);
+  {
+    for (int g = 0; g < Ng; ++g) {
+      const int r = c->sub_rank[g];
+      for (int e : c->gsub_ents[g])
+        if (c->gents[e].r > 0 && erank[e] < 0)
+          for (int t = 0; t < c->gents[e].r; ++t) Sr[r].push_back(c->gents[e].off_pi + t);
+    }
+    for (int r = 0; r < R; ++r) {   // an entity is seen once per sharing subdomain of the rank
+      std::sort(Sr[r].begin(), Sr[r].end());
+      Sr[r].erase(std::unique(Sr[r].begin(), Sr[r].end()), Sr[r].end());
+    }
+    for (int g = 0; g < Ng; ++g) Sr[c->sub_rank[g]].push_back(NPi + g);
+  }
+  int64_t maxS = 1;
+  for (int r = 0; r < R; ++r) maxS = std::max<int64_t>(maxS, Sr[r].size());
+  // root rhs sources: root entry j <- t_r[q] (gathered at r * maxS + q) for every S_r[q] = root[j]
+  std::vector<int64_t> rptr(nroot + 1, 0), ridx;
+  for (int r = 0; r < R; ++r)
+    for (int64_t v : Sr[r]) ++rptr[rpos[v] + 1];
+  for (int64_t j = 0; j < nroot; ++j) rptr[j + 1] += rptr[j];
+  ridx.resize(rptr[nroot]);
+  {
+    std::vector<int64_t> fill(rptr.begin(), rptr.end() - 1);
+    for (int r = 0; r < R; ++r)
+      for (size_t q = 0; q < Sr[r].size(); ++q) ridx[fill[rpos[Sr[r][q]]]++] = (int64_t)r * maxS + q;
+  }
+  const int64_t nI = Iglob.size(), nIp = (nI + 31) / 32 * 32, nS = Sr[me].size(), nloc = nIp + nS;
+  std::vector<int64_t> lp(Nc, -1);
+  for (int64_t a = 0; a < nI; ++a) lp[Iglob[a]] = a;
+  for (int64_t q = 0; q < nS; ++q) lp[Sr[me][q]] = nIp + q;
+  // ---- local matrix on [I | pad | S] from this rank's pieces (no communication)
+  std::vector<int64_t> lmap, mapoff(N + 1, 0), p0pos(N);
+  std::vector<int> lnpi(N);
+  for (int i = 0; i < N; ++i) {
+    const int g = c->sub_gid[i];
+    for (int64_t q = pimoff[g]; q < pimoff[g + 1]; ++q) {
+      VB_REQUIRE(lp[pimap[q]] >= 0, VB_EINVAL, "internal: coarse dissection map");
+      lmap.push_back(lp[pimap[q]]);
+    }
+    mapoff[i + 1] = lmap.size();
+    p0pos[i] = lp[NPi + g];
+    lnpi[i] = gnpi[g];
+  }
+  if (lmap.empty()) lmap.push_back(0);
+  DBuf<int64_t> dlpoff, dmapoff, dlmap, dp0;
+  DBuf<int> dlnpi;
+  dlpoff.upload(lpoff, s); dmapoff.upload(mapoff, s); dlmap.upload(lmap, s); dp0.upload(p0pos, s);
+  dlnpi.upload(lnpi, s);
+  const int64_t ldK = ld4((int)nloc);
+  DBuf<double> K;
+  K.alloc(ldK * nloc);
+  K.zero(s);
+  {
+    std::vector<std::vector<int>> colors(c->ncolors);
+    for (int i = 0; i < N; ++i) colors[c->gsub_color[c->sub_gid[i]]].push_back(i);
+    for (auto &col : colors) {
+      if (col.empty()) continue;
+      DBuf<int> dcol;
+      dcol.upload(col, s);
+      coarse_assemble_local_kernel<<<dim3(8, col.size()), 256, 0, s>>>(dcol.p, dlpoff.p, dlnpi.p, dmapoff.p, dlmap.p,
+                                                                       dp0.p, pieces.p, K.p, ldK);
+      VB_STAGE();
+      sync(c);
+    }
+  }
+  if (nIp > nI) {
+    unit_diag_kernel<<<1, 64, 0, s>>>(K.p, ldK, nI, nIp);
+    VB_STAGE();
+  }
+  STAGE_T("  coarse local assembly (f1)");
+  cd_dump(c, "kloc", K.p, nloc, nloc, ldK);
+  cd_dump_i(c, "Iglob", Iglob);
+  cd_dump_i(c, "Sglob", Sr[me]);
+  cd_dump_i(c, "root", root);
+  c->d_Kloc.release();
+  c->d_Kloc.alloc(std::max<int64_t>(packed_size((int)nloc), 1));
+  if (nIp > 0) {
+    c->d_info.zero(s);
+    std::vector<MatDesc> lm{MatDesc{K.p, (int)nloc, (int)ldK, (int)nIp}};
+    lm[0].npos = (int)nIp;   // A_II SPD
+    ldl_partial_batched(lm, c->d_info.p, s);
+    const std::vector<int> who{me};
+    check_info(c, 1, "coarse interior LDL^T (f1)", &who, "rank");
+    const int64_t ldW = ld4((int)nIp);
+    DBuf<double> W, dI, M;
+    W.alloc(ldW * nIp);
+    W.zero(s);
+    tri_inverse_batched({TriDesc{K.p, (int)ldK, W.p, (int)ldW, (int)nIp}}, s);
+    dI.alloc(nIp);
+    recip_diag_kernel<<<(nIp + 255) / 256, 256, 0, s>>>(K.p, ldK, nIp, dI.p);
+    VB_STAGE();
+    M.alloc(ldK * nloc);
+    M.zero(s);
+    GemmPlan plan;
+    int l0 = plan.begin_launch();
+    GemmProb p{};
+    p.A = W.p; p.lda = ldW; p.transA = 1; p.d = dI.p; p.dstride = 1;   // E = W^T D^-1 W (lower)
+    p.B = W.p; p.ldb = ldW; p.C = M.p; p.ldc = ldK;
+    p.M = p.N = p.K = nIp; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
+    p.kz_on = 8;   // W lower triangular (site bit 8)
+    plan.add(p);
+    GemmProb q{};
+    q.A = K.p + nIp; q.lda = ldK;                                      // F^T = L_SI W
+    q.B = W.p; q.ldb = ldW; q.C = M.p + nIp; q.ldc = ldK;
+    q.M = nS; q.N = nIp; q.K = nIp; q.alpha = 1.0; q.beta = 0.0;
+    plan.add(q);
+    plan.upload(s);
+    plan.run(l0, s);
+    sync(c);
+    pack_tiles_batched({PackDesc{M.p, (int)nloc, (int)ldK, c->d_Kloc.p}}, s);
+  } else {
+    c->d_Kloc.zero(s);
+  }
+  STAGE_T("  coarse local elimination (f1)");
+  // ---- root: allgather the Schur contributions, sum in rank order, augment, factor, invert
+  DBuf<double> piece, gath;
+  piece.alloc(maxS * maxS);
+  piece.zero(s);
+  copy_sym_lower_kernel<<<(int)std::min<int64_t>((nS * nS + 255) / 256, 8192), 256, 0, s>>>(
+      K.p + nIp * (ldK + 1), ldK, nS, piece.p, maxS);
+  VB_STAGE();
+  K.release();
+  const double *all = piece.p;
+  if (R > 1) {
+    gath.alloc((size_t)maxS * maxS * R);
+    c->comm->allgather(piece.p, gath.p, maxS * maxS, s);
+    all = gath.p;
+  }
+  const int64_t ldR = ld4((int)nroot);
+  DBuf<double> Kr, gvol;
+  DBuf<int64_t> drp;
+  Kr.alloc(ldR * nroot);
+  Kr.zero(s);
+  {
+    std::vector<int64_t> rp((size_t)maxS * R, 0);
+    for (int r = 0; r < R; ++r)
+      for (size_t q = 0; q < Sr[r].size(); ++q) rp[(size_t)r * maxS + q] = rpos[Sr[r][q]];
+    drp.upload(rp, s);
+  }
+  for (int r = 0; r < R; ++r) {
+    const int64_t n = Sr[r].size();
+    root_scatter_add_kernel<<<(int)std::min<int64_t>((n * n + 255) / 256, 8192), 256, 0, s>>>(
+        all + (size_t)r * maxS * maxS, maxS, n, drp.p + (size_t)r * maxS, Kr.p, ldR);
+    VB_STAGE();
+  }
+  gvol.upload(c->gsub_vol, s);
+  coarse_augment_kernel<<<(int)std::min<int64_t>(((int64_t)Ng * Ng + 255) / 256, 4096), 256, 0, s>>>(
+      gvol.p, Ng, gam_c, Kr.p, ldR, nsep);
+  VB_STAGE();
+  gath.release();
+  STAGE_T("  coarse root assembly (f1)");
+  cd_dump(c, "kroot", Kr.p, nroot, nroot, ldR);
+  cd_dump(c, "piece", piece.p, maxS, maxS, maxS);
+  c->d_info.zero(s);
+  std::vector<MatDesc> rm{MatDesc{Kr.p, (int)nroot, (int)ldR, (int)nroot}};
+  rm[0].npos = (int)nsep;   // [separator u_Pi | p_0 (augmented)]
+  ldl_partial_batched(rm, c->d_info.p, s);
+  check_info(c, 1, "coarse root LDL^T (f1)");
+  coarse_inverse_pack(c, Kr, ldR, nroot);
+  STAGE_T("  coarse root inverse (f1)");
+  c->Nroot = nroot; c->cd_nsep = nsep;
+  c->cd_nI = nI; c->cd_nIp = nIp; c->cd_nS = nS; c->cd_nloc = nloc; c->cd_maxS = maxS;
+  c->cd_Iglob = Iglob; c->cd_Sglob = Sr[me]; c->cd_root_glob = root;
+  c->cd_rptr = rptr; c->cd_ridx = ridx;
+}
+
 // A3 (second half) .. A5: dual Schur inverse, Phi, S_c, b~0, deluxe D_G^(m), coarse inverse.
 static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
   cudaStream_t s = c->stream;
@@ -870,11 +1220,11 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
   VB_STAGE();
   c->d_Dlx.release();
   STAGE_T("  fold D S_DD^-1 D^T, D Phi");
-  // ---------------- A5: coarse saddle matrix on (u_Pi, p_0) of ALL subdomains, dense inverse
-  //   C4: every rank gathers every subdomain's (S_c, b~0) and assembles/factors the same matrix
+  // ---------------- A5: coarse saddle matrix on (u_Pi, p_0) of ALL subdomains
   const int Ng = c->Ng;
   const int64_t Nc = c->NPi_g + Ng;
   c->Nc = Nc;
+  c->cdis = c->opt_coarse_dis < 0 ? c->nranks > 1 : c->opt_coarse_dis != 0;
   {
     // global piece layout: rank-major, subdomains in order within a rank
     std::vector<int> gnpi(Ng, 0);
@@ -908,106 +1258,54 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     VB_STAGE();
     sync(c);
     c->d_K.release();   // the dense subdomain matrices are not needed by the solve (frees ~48 MB per subdomain)
-    const double *pieces = mine.p;
-    if (c->nranks > 1) {
-      gathered.alloc((size_t)maxlen * c->nranks);
-      c->comm->allgather(mine.p, gathered.p, maxlen, s);
-      pieces = gathered.p;
-    }
-    dpoff.upload(poff, s);
-    dgnpi.upload(gnpi, s);
-    dpimoff.upload(pimoff, s);
-    if (pimap.empty()) pimap.push_back(0);
-    dpimap.upload(pimap, s);
-    DBuf<double> Kc, Wc, dc, gvol;
-    const int64_t ldC = ld4((int)Nc);   // 32-byte aligned columns (16-byte copies in the DMMA GEMM)
-    Kc.alloc(ldC * Nc);
-    Kc.zero(s);
-    std::vector<std::vector<int>> colors(c->ncolors);
-    for (int g = 0; g < Ng; ++g) colors[c->gsub_color[g]].push_back(g);
-    for (auto &col : colors) {
-      if (col.empty()) continue;
-      DBuf<int> dcol;
-      dcol.upload(col, s);
-      coarse_assemble_kernel2<<<dim3(8, col.size()), 256, 0, s>>>(dcol.p, dpoff.p, dgnpi.p, dpimoff.p, dpimap.p,
-                                                                 pieces, Kc.p, ldC, c->NPi_g);
-      VB_STAGE();
-      sync(c);
-    }
     double nubar = 0, volO = 0;
     for (int64_t K = 0; K < c->nK; ++K) nubar += c->nu[K];
     nubar /= c->nK;
     for (int g = 0; g < Ng; ++g) volO += c->gsub_vol[g];
-    gvol.upload(c->gsub_vol, s);
-    coarse_augment_kernel<<<(int)std::min<int64_t>(((int64_t)Ng * Ng + 255) / 256, 4096), 256, 0, s>>>(
-        gvol.p, Ng, 1.0 / (nubar * volO), Kc.p, ldC, c->NPi_g);
-    VB_STAGE();
-    STAGE_T("  coarse pieces + assembly (C4)");
-    c->d_info.zero(s);
-    std::vector<MatDesc> cm{MatDesc{Kc.p, (int)Nc, (int)ldC, (int)Nc}};
-    cm[0].npos = (int)c->NPi_g;   // [u_Pi | p_0 (augmented)]: velocity > 0, pressure < 0
-    ldl_partial_batched(cm, c->d_info.p, s);
-    check_info(c, 1, "coarse saddle LDL^T (A5)");
-    STAGE_T("  coarse LDL^T");
-    Wc.alloc(ldC * Nc);
-    Wc.zero(s);
-    tri_inverse_batched({TriDesc{Kc.p, (int)ldC, Wc.p, (int)ldC, (int)Nc}}, s);
-    dc.alloc(Nc);
-    recip_diag_kernel<<<(Nc + 255) / 256, 256, 0, s>>>(Kc.p, ldC, Nc, dc.p);
-    VB_STAGE();
-    if (c->nranks == 1) {
-      // (K_c)^-1 = W^T D^-1 W (lower), packed
-      GemmPlan plan;
-      int l0 = plan.begin_launch();
-      GemmProb p{};
-      p.A = Wc.p; p.lda = ldC; p.transA = 1; p.d = dc.p; p.dstride = 1;
-      p.B = Wc.p; p.ldb = ldC; p.C = Kc.p; p.ldc = ldC;
-      p.M = p.N = p.K = Nc; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
-      p.kz_on = 8;   // W lower triangular (site bit 8)
-      plan.add(p);
-      plan.upload(s);
-      plan.run(l0, s);
-      sync(c);
-      c->d_Kcp.alloc(packed_size(Nc));
-      pack_tiles_batched({PackDesc{Kc.p, (int)Nc, (int)ldC, c->d_Kcp.p}}, s);
+    const double gam_c = 1.0 / (nubar * volO);
+    if (c->cdis) {
+      coarse_dissection(c, mine, lpoff, gnpi, pimoff, pimap, gam_c);
     } else {
-      // distributed coarse solve: this rank computes and keeps only the tile rows [tlo, thi) of the
-      // packed symmetric inverse (a contiguous slice of the 1-rank layout, split by tile count), from
-      // the row block (W[:, lo:hi])^T D^-1 W[:, :hi] (W lower triangular: k >= lo suffices).  The
-      // solve streams the slice with the packed GEMV (row and transpose parts) and sums the ranks'
-      // partial vectors in rank order (C2): N_c^2 / (2R) doubles per rank per iteration.
-      const int64_t nt = (Nc + 31) / 32, R = c->nranks;
-      std::vector<int64_t> T(R + 1, nt);
-      T[0] = 0;
-      const double total = (double)nt * (nt + 1) / 2;
-      for (int64_t r = 1, I = 0; r < R; ++r) {
-        while (I < nt && (double)(I + 1) * (I + 2) / 2 < total * r / R) ++I;
-        T[r] = std::max(T[r - 1], std::min<int64_t>(nt, I + 1));
+      // C4: every rank gathers every subdomain's (S_c, b~0) and assembles/factors the same matrix
+      const double *pieces = mine.p;
+      if (c->nranks > 1) {
+        gathered.alloc((size_t)maxlen * c->nranks);
+        c->comm->allgather(mine.p, gathered.p, maxlen, s);
+        pieces = gathered.p;
       }
-      c->coarse_tlo = T[c->rank];
-      c->coarse_thi = T[c->rank + 1];
-      const int64_t lo = 32 * c->coarse_tlo, hi = std::min<int64_t>(Nc, 32 * c->coarse_thi), mine = hi - lo;
-      const int64_t slice = c->coarse_thi == nt ? packed_size(Nc) - ptile_row_start(c->coarse_tlo)
-                                                : ptile_row_start(c->coarse_thi) - ptile_row_start(c->coarse_tlo);
-      c->d_Kcs.alloc(std::max<int64_t>(slice, 1));
-      if (mine > 0) {
-        DBuf<double> Kr;
-        Kr.alloc(mine * hi);
-        GemmPlan plan;
-        int l0 = plan.begin_launch();
-        GemmProb p{};
-        p.A = Wc.p + lo * ldC + lo; p.lda = ldC; p.transA = 1; p.d = dc.p + lo; p.dstride = 1;
-        p.B = Wc.p + lo; p.ldb = ldC; p.C = Kr.p; p.ldc = mine;
-        p.M = mine; p.N = hi; p.K = Nc - lo; p.alpha = 1.0; p.beta = 0.0;
-        p.kz_on = 16; p.kzB = (int)-lo;   // (site bit 16)   // W(lo + k, lo + i) = 0 for k < i, W(lo + k, j) = 0 for k < j - lo
-        plan.add(p);
-        plan.upload(s);
-        plan.run(l0, s);
-        pack_rows_kernel<<<dim3(c->coarse_thi, c->coarse_thi - c->coarse_tlo), 256, 0, s>>>(
-            Kr.p, mine, lo, Nc, c->coarse_tlo, c->d_Kcs.p);
+      dpoff.upload(poff, s);
+      dgnpi.upload(gnpi, s);
+      dpimoff.upload(pimoff, s);
+      if (pimap.empty()) pimap.push_back(0);
+      dpimap.upload(pimap, s);
+      DBuf<double> Kc, gvol;
+      const int64_t ldC = ld4((int)Nc);   // 32-byte aligned columns (16-byte copies in the DMMA GEMM)
+      Kc.alloc(ldC * Nc);
+      Kc.zero(s);
+      std::vector<std::vector<int>> colors(c->ncolors);
+      for (int g = 0; g < Ng; ++g) colors[c->gsub_color[g]].push_back(g);
+      for (auto &col : colors) {
+        if (col.empty()) continue;
+        DBuf<int> dcol;
+        dcol.upload(col, s);
+        coarse_assemble_kernel2<<<dim3(8, col.size()), 256, 0, s>>>(dcol.p, dpoff.p, dgnpi.p, dpimoff.p, dpimap.p,
+                                                                   pieces, Kc.p, ldC, c->NPi_g);
+        VB_STAGE();
         sync(c);
       }
+      gvol.upload(c->gsub_vol, s);
+      coarse_augment_kernel<<<(int)std::min<int64_t>(((int64_t)Ng * Ng + 255) / 256, 4096), 256, 0, s>>>(
+          gvol.p, Ng, gam_c, Kc.p, ldC, c->NPi_g);
       VB_STAGE();
+      STAGE_T("  coarse pieces + assembly (C4)");
+      cd_dump(c, "kc", Kc.p, Nc, Nc, ldC);
+      c->d_info.zero(s);
+      std::vector<MatDesc> cm{MatDesc{Kc.p, (int)Nc, (int)ldC, (int)Nc}};
+      cm[0].npos = (int)c->NPi_g;   // [u_Pi | p_0 (augmented)]: velocity > 0, pressure < 0
+      ldl_partial_batched(cm, c->d_info.p, s);
+      check_info(c, 1, "coarse saddle LDL^T (A5)");
+      STAGE_T("  coarse LDL^T");
+      coarse_inverse_pack(c, Kc, ldC, Nc);
     }
   }
   sync(c);

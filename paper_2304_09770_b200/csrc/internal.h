@@ -354,6 +354,16 @@ struct vb_ctx {
   vb::DBuf<double> w_rhsg, w_xg;     // global-layout free vectors (nranks > 1)
   vb::DBuf<double> d_Kcs;            // distributed coarse: this rank's tile rows of the packed inverse
   int64_t coarse_tlo = 0, coarse_thi = 0;   // ... tile rows [tlo, thi) (balanced by tile count)
+  // rank-level dissection of the coarse saddle problem (factor.cu coarse_dissection,
+  // DESIGN.md §9).  Interior = primal DOFs of entities whose sharers all live on one rank (local,
+  // eliminated by that rank alone); root = the other primal DOFs and every p_0 (replicated, sliced).
+  int opt_coarse_dis = -1;           // vb_set_option("coarse_dissection"): -1 auto = on for nranks > 1
+  bool cdis = false;                 // the last vb_factor used it
+  int64_t Nroot = 0, cd_nsep = 0;    // root size (= cd_nsep separator velocity DOFs + Ng p_0)
+  int64_t cd_nI = 0, cd_nIp = 0, cd_nS = 0, cd_nloc = 0, cd_maxS = 0;   // local sizes (nIp = nI padded to 32)
+  std::vector<int64_t> cd_Iglob, cd_Sglob, cd_root_glob;   // -> global coarse index (u_Pi, then p_0)
+  std::vector<int64_t> cd_rptr, cd_ridx;   // root entry <- gathered t entries r * maxS + q, rank order
+  vb::DBuf<double> d_Kloc;           // packed [[A_II^-1, sym], [A_SI A_II^-1, 0]] (n_loc = nIp + nS)
   double factor_flops = 0;     // DMMA GEMM flops of the last vb_factor
   double factor_gemm_s = 0;    // their kernel time (CUDA events; VB_KERNEL_TIMING=1 only, else 0)
   double factor_alloc_s = 0;   // wall time of device allocation / release inside the last vb_factor

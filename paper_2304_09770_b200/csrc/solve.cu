@@ -922,6 +922,54 @@ __global__ void rank_sum_vec_kernel(const double *__restrict__ g, int R, int64_t
   }
 }
 
+// f1 coarse dissection (factor.cu coarse_dissection): root rhs g_S = rc[root] - sum_r t_r (the
+// gathered F^T g_I of every rank, rank order), then the gauge projection of its p_0 part (mode 0)
+__global__ void cd_root_rhs_kernel(const int64_t *__restrict__ rptr, const int64_t *__restrict__ ridx,
+                                   const double *__restrict__ tg, const double *__restrict__ rc,
+                                   const int64_t *__restrict__ root, int64_t nroot, double *g) {
+  pdl_prologue();
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nroot; j += (int64_t)gridDim.x * blockDim.x) {
+    double v = rc[root[j]];
+    for (int64_t q = rptr[j]; q < rptr[j + 1]; ++q) v -= tg[ridx[q]];
+    g[j] = v;
+  }
+}
+
+// root solution: gauge projection of its p_0 part (sum vol_i p0_i = 0, mode 1 of
+// coarse_p0_project_kernel), then scattered to its global coarse positions (one CTA)
+__global__ void cd_root_finish_kernel(const double *__restrict__ vol, int Ng, int64_t nsep, const double *__restrict__ x,
+                                      const int64_t *__restrict__ root, int64_t nroot, double *uc) {
+  pdl_prologue();
+  __shared__ double ra[32], rw[32], mean;
+  double a = 0.0, w = 0.0;
+  for (int i = threadIdx.x; i < Ng; i += blockDim.x) {
+    a += vol[i] * x[nsep + i];
+    w += vol[i];
+  }
+  a = warp_sum(a); w = warp_sum(w);
+  if ((threadIdx.x & 31) == 0) { ra[threadIdx.x >> 5] = a; rw[threadIdx.x >> 5] = w; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double A = 0, Wt = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { A += ra[q]; Wt += rw[q]; }
+    mean = A / Wt;
+  }
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < nroot; j += blockDim.x) uc[root[j]] = j >= nsep ? x[j] - mean : x[j];
+}
+
+// interior coarse values x_I = y_I - F x_S (F x_S: the transpose part of the second GEMV pass,
+// summed over its chunks in fixed order)
+__global__ void cd_interior_kernel(const double *__restrict__ part, int64_t stride, int P, const double *__restrict__ y,
+                                   int64_t nI, const int64_t *__restrict__ Iglob, double *uc) {
+  pdl_prologue();
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nI; a += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int c = 0; c < P; ++c) v += part[c * stride + a];
+    uc[Iglob[a]] = y[a] - v;
+  }
+}
+
 __global__ void __launch_bounds__(256) sum_chunks_kernel(const double *__restrict__ part, int64_t stride, int P,
                                                          int64_t n, double *out) {
   pdl_prologue();
@@ -955,6 +1003,14 @@ struct SolveState {
   DBuf<double> sx;                   // [s (len_G) | received copies]
   DBuf<double> cbuf, cgath;          // coarse pieces (local), gathered (nranks x cmax)
   DBuf<double> ucp, ucg;             // distributed coarse: this rank's partial u_c; gathered (R x N_c)
+  // f1 coarse dissection: GEMV passes over the local packed [[E, .], [F^T, 0]] (pass 1: all tile
+  // rows, x = [g_I; 0]; pass 2: the S tile rows, x = [0; x_S]), root rhs / solution
+  DBuf<GemvWork> w_cd1, w_cd2;
+  int nw_cd1 = 0, nw_cd2 = 0;
+  size_t sm_cd = 0;
+  bool big_cd = false;
+  DBuf<int64_t> cd_map1, cd_map2, cd_Iglob, cd_root, cd_rptr, cd_ridx;
+  DBuf<double> cd_part1, cd_part2, cd_v1, cd_tg, cd_groot, cd_xroot;
   DBuf<double> gam2, gbuf, hbuf;     // B0: entity-major b_e; [zG | received]; DOF halo receive
   int64_t cmax = 0;
   SlotExchange XS, XE, XB, XH, XR;   // apply_S copies, extension products, B0 zG, DOF halo, rank partials
@@ -1200,21 +1256,53 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   launch_pdl(st, gather_src_kernel, dim3(grid_for(c->Nc)), dim3(256), 0, s2, st->pptr.p, st->pidx.p, pieces, c->Nc, c->w_rc.p);
   launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
   tick(c, st, 2, true, s2);
+  auto coarse_gemv = [&](const GemvWork *w, int nw, size_t sm, bool big) {
+    if (big)
+      launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, true, true>, dim3(nw), dim3(GV_WARPS_C * 32), GV_WARPS_C * 32 * sizeof(double), s2, w);
+    else
+      launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, false, true>, dim3(nw), dim3(GV_WARPS_C * 32), sm, s2, w);
+  };
+  // f1 dissection: local pass 1 (y_I = E g_I, t = F^T g_I), root rhs from every rank's t
+  const int64_t nC = c->cdis ? c->Nroot : c->Nc;       // order of the (root or whole) inverse
+  double *ucout = c->cdis ? st->cd_xroot.p : c->w_uc.p;
+  if (c->cdis) {
+    if (st->nw_cd1) {
+      coarse_gemv(st->w_cd1.p, st->nw_cd1, st->sm_cd, st->big_cd);
+      launch_pdl(st, sum_chunks_kernel, dim3((c->cd_nloc + 31) / 32), dim3(256), 0, s2, st->cd_part1.p, c->cd_nloc,
+                 st->nw_cd1, c->cd_nloc, st->cd_v1.p);
+    }
+    const double *tg = st->cd_v1.p + c->cd_nIp;
+    if (c->nranks > 1) {
+      c->comm->allgather(st->cd_v1.p + c->cd_nIp, st->cd_tg.p, c->cd_maxS, s2);
+      tg = st->cd_tg.p;
+    }
+    launch_pdl(st, cd_root_rhs_kernel, dim3(grid_for(c->Nroot)), dim3(256), 0, s2, st->cd_rptr.p, st->cd_ridx.p, tg,
+               c->w_rc.p, st->cd_root.p, c->Nroot, st->cd_groot.p);
+    launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, st->cd_groot.p + c->cd_nsep, 0);
+  }
   // the packed inverse (all of it on one rank; this rank's tile rows otherwise)
-  if (st->big_c)
-    launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, true, true>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), GV_WARPS_C * 32 * sizeof(double), s2, st->w_c.p);
-  else
-    launch_pdl(st, sym_gemv_kernel<GV_WARPS_C, false, true>, dim3(st->nw_c), dim3(GV_WARPS_C * 32), st->sm_c, s2, st->w_c.p);
+  coarse_gemv(st->w_c.p, st->nw_c, st->sm_c, st->big_c);
   tick(c, st, 2, false, s2);
   if (c->nranks > 1) {
     // this rank's partial, then the rank-order sum of all partials (C2)
-    launch_pdl(st, sum_chunks_kernel, dim3((c->Nc + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, c->Nc, st->nw_c, c->Nc, st->ucp.p);
-    c->comm->allgather(st->ucp.p, st->ucg.p, c->Nc, s2);
-    launch_pdl(st, rank_sum_vec_kernel, dim3(grid_for(c->Nc)), dim3(256), 0, s2, st->ucg.p, c->nranks, c->Nc, c->w_uc.p);
+    launch_pdl(st, sum_chunks_kernel, dim3((nC + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, nC, st->nw_c, nC, st->ucp.p);
+    c->comm->allgather(st->ucp.p, st->ucg.p, nC, s2);
+    launch_pdl(st, rank_sum_vec_kernel, dim3(grid_for(nC)), dim3(256), 0, s2, st->ucg.p, c->nranks, nC, ucout);
   } else {
-    launch_pdl(st, sum_chunks_kernel, dim3((c->Nc + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, c->Nc, st->nw_c, c->Nc, c->w_uc.p);
+    launch_pdl(st, sum_chunks_kernel, dim3((nC + 31) / 32), dim3(256), 0, s2, c->w_ucp.p, nC, st->nw_c, nC, ucout);
   }
-  launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
+  if (c->cdis) {
+    // x_S (gauge-projected) to its global positions; pass 2: x_I = y_I - F x_S
+    launch_pdl(st, cd_root_finish_kernel, dim3(1), dim3(1024), 0, s2, st->gvol.p, c->Ng, c->cd_nsep, st->cd_xroot.p,
+               st->cd_root.p, c->Nroot, c->w_uc.p);
+    if (st->nw_cd2) {
+      coarse_gemv(st->w_cd2.p, st->nw_cd2, st->sm_cd, st->big_cd);
+      launch_pdl(st, cd_interior_kernel, dim3(grid_for(c->cd_nI)), dim3(256), 0, s2, st->cd_part2.p, c->cd_nloc,
+                 st->nw_cd2, st->cd_v1.p, c->cd_nI, st->cd_Iglob.p, c->w_uc.p);
+    }
+  } else {
+    launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
+  }
   launch_pdl(st, coarse_ext_kernel, dim3((st->max_nd + 127) / 128, c->N), dim3(128), c->max_npi * sizeof(double), s2,
              c->d_sub.p, c->d_Phi.p, c->d_pi_glob.p, c->w_uc.p, c->w_locC.p);
   VB_CUDA(cudaEventRecord(st->ev_join, s2));
@@ -1272,8 +1360,11 @@ void prepare_solve(vb_ctx *c) {
   c->w_locD.alloc(std::max<int64_t>(c->len_Dv, 1));
   c->w_locC.alloc(std::max<int64_t>(c->len_Dv, 1));
   c->w_locY.alloc((int64_t)c->P_loc * std::max<int64_t>(c->len_Dv, 1));
-  c->w_uc.alloc(c->Nc); c->w_rc.alloc(c->Nc);
-  if (c->nranks > 1) { st->ucp.alloc(c->Nc); st->ucg.alloc((int64_t)c->Nc * c->nranks); }
+  // w_rc[Nc] = w_uc[Nc] = 0: the gather target of the zero blocks of the dissection GEMV inputs
+  c->w_uc.alloc(c->Nc + 1); c->w_rc.alloc(c->Nc + 1);
+  c->w_uc.zero(s); c->w_rc.zero(s);
+  const int64_t nC = c->cdis ? c->Nroot : c->Nc;   // order of the (root or whole) coarse inverse
+  if (c->nranks > 1) { st->ucp.alloc(nC); st->ucg.alloc(nC * c->nranks); }
   c->w_scal.alloc(16); c->w_scal.zero(s);
   st->ticket.alloc(4); st->ticket.zero(s);
   st->pdl = !(getenv("VB_NO_PDL") && atoi(getenv("VB_NO_PDL")));
@@ -1319,16 +1410,12 @@ void prepare_solve(vb_ctx *c) {
   c->w_locY.zero(s);
   st->w_loc.upload(wl, s); st->nw_loc = wl.size(); st->sm_loc = gemv_smem(nmaxD);
   wl.clear();
-  // coarse work list: the tile rows [tlo, thi) of the packed inverse (all of them on one rank)
-  const int64_t ntc = (c->Nc + 31) / 32;
-  const int64_t tlo = c->nranks > 1 ? c->coarse_tlo : 0, thi = c->nranks > 1 ? c->coarse_thi : ntc;
-  const double *Kc0 = c->nranks > 1 ? c->d_Kcs.p : c->d_Kcp.p;
-  const int64_t Kc_off = c->nranks > 1 ? ptile_row_start(tlo) : 0;   // the slice starts at tile row tlo
-  int Pc = (int)std::max<int64_t>(1, std::min<int64_t>(c->P_c, thi - tlo));
-  c->w_ucp.alloc(std::max<int64_t>((int64_t)Pc * c->Nc, 1));
-  c->w_ucp.zero(s);
-  {
-    // split [tlo, thi) into Pc chunks balanced by tiles + row cost (as split_rows over the slice)
+  // coarse work list: the tile rows [tlo, thi) of the packed inverse (all of them on one rank) --
+  // of the whole coarse matrix, or of the dissection root
+  // split the tile rows [tlo, thi) of a packed matrix of order n into Pc chunks balanced by tiles +
+  // row cost (as split_rows over the slice); chunk q writes the partial vector out + q n
+  auto slice_work = [&](const double *M, int64_t moff, const int64_t *map, const double *x, double *out, int64_t n,
+                        int64_t tlo, int64_t thi, int Pc) {
     auto cum = [&](int64_t r) { return (double)r * (r + 1) / 2 + 4.0 * r; };
     const double c0 = cum(tlo), tot = cum(thi) - c0;
     int64_t r = tlo;
@@ -1337,12 +1424,52 @@ void prepare_solve(vb_ctx *c) {
       while (r1 < thi && cum(r1 + 1) - c0 <= tot * (q + 1) / Pc) ++r1;
       if (r1 == r && r < thi) r1 = r + 1;
       if (q == Pc - 1) r1 = thi;
-      wl.push_back(GemvWork{Kc0, nullptr, c->w_rc.p, c->w_ucp.p + (int64_t)q * c->Nc, (int)c->Nc, (int)r, (int)r1, 0, Kc_off});
+      wl.push_back(GemvWork{M, map, x, out + (int64_t)q * n, (int)n, (int)r, (int)r1, 0, moff});
       r = r1;
     }
+  };
+  const int64_t ntc = (nC + 31) / 32;
+  const int64_t tlo = c->nranks > 1 ? c->coarse_tlo : 0, thi = c->nranks > 1 ? c->coarse_thi : ntc;
+  const double *Kc0 = c->nranks > 1 ? c->d_Kcs.p : c->d_Kcp.p;
+  const int64_t Kc_off = c->nranks > 1 ? ptile_row_start(tlo) : 0;   // the slice starts at tile row tlo
+  int Pc = (int)std::max<int64_t>(1, std::min<int64_t>(c->P_c, thi - tlo));
+  c->w_ucp.alloc(std::max<int64_t>((int64_t)Pc * nC, 1));
+  c->w_ucp.zero(s);
+  if (c->cdis) {
+    st->cd_groot.alloc(nC); st->cd_xroot.alloc(nC);
   }
-  st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = gemv_smem(c->Nc, GV_WARPS_C);
+  slice_work(Kc0, Kc_off, nullptr, c->cdis ? st->cd_groot.p : c->w_rc.p, c->w_ucp.p, nC, tlo, thi, Pc);
+  st->w_c.upload(wl, s); st->nw_c = wl.size(); st->sm_c = gemv_smem(nC, GV_WARPS_C);
   st->big_c = st->sm_c > 200 * 1024;
+  wl.clear();
+  if (c->cdis) {
+    // f1 dissection: the local packed [[E, .], [F^T, 0]] of order n_loc = nIp + nS
+    const int64_t nl = c->cd_nloc, ntl = (nl + 31) / 32, tS = c->cd_nIp / 32;
+    std::vector<int64_t> m1(nl, c->Nc), m2(nl, c->Nc);
+    for (int64_t a = 0; a < c->cd_nI; ++a) m1[a] = c->cd_Iglob[a];
+    for (int64_t q = 0; q < c->cd_nS; ++q) m2[c->cd_nIp + q] = c->cd_Sglob[q];
+    st->cd_map1.upload(m1, s); st->cd_map2.upload(m2, s);
+    st->cd_Iglob.upload(c->cd_Iglob.empty() ? std::vector<int64_t>{0} : c->cd_Iglob, s);
+    st->cd_root.upload(c->cd_root_glob, s);
+    st->cd_rptr.upload(c->cd_rptr, s);
+    st->cd_ridx.upload(c->cd_ridx.empty() ? std::vector<int64_t>{0} : c->cd_ridx, s);
+    st->cd_v1.alloc(c->cd_nIp + c->cd_maxS); st->cd_v1.zero(s);
+    if (c->nranks > 1) st->cd_tg.alloc(c->cd_maxS * c->nranks);
+    st->nw_cd1 = st->nw_cd2 = 0;
+    if (c->cd_nIp > 0) {
+      const int P1 = (int)std::max<int64_t>(1, std::min<int64_t>(c->P_c, ntl));
+      const int P2 = (int)std::max<int64_t>(1, std::min<int64_t>(c->P_c, ntl - tS));
+      st->cd_part1.alloc((int64_t)P1 * nl); st->cd_part2.alloc((int64_t)P2 * nl);
+      slice_work(c->d_Kloc.p, 0, st->cd_map1.p, c->w_rc.p, st->cd_part1.p, nl, 0, ntl, P1);
+      st->w_cd1.upload(wl, s); st->nw_cd1 = wl.size(); wl.clear();
+      slice_work(c->d_Kloc.p, 0, st->cd_map2.p, c->w_uc.p, st->cd_part2.p, nl, tS, ntl, P2);
+      st->w_cd2.upload(wl, s); st->nw_cd2 = wl.size(); wl.clear();
+    }
+    st->sm_cd = gemv_smem(nl, GV_WARPS_C);
+    st->big_cd = st->sm_cd > 200 * 1024;
+    if (!st->big_cd)
+      raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS_C, false, true>, st->sm_cd);
+  }
   st->big_op = st->sm_op > 200 * 1024;
   st->big_loc = st->sm_loc > 200 * 1024;
   size_t smmax = std::max(st->big_op ? 0 : st->sm_op, st->big_loc ? 0 : st->sm_loc);
@@ -1587,7 +1714,9 @@ void prepare_solve(vb_ctx *c) {
     b += 8.0 * packed_size(S.nG) + 8.0 * packed_size(S.nd) + 2 * 8.0 * S.nd * S.npi;
   }
   // (the deluxe blocks are folded into S_DD^-1 and Phi at factor time: no per-iteration D traffic)
-  b += 8.0 * (c->nranks > 1 ? (double)c->d_Kcs.n : (double)packed_size(c->Nc));
+  b += 8.0 * (c->nranks > 1 ? (double)c->d_Kcs.n : (double)packed_size(c->cdis ? c->Nroot : c->Nc));
+  if (c->cdis && c->cd_nIp > 0)   // dissection passes 1 (all of the local matrix) and 2 (its S tile rows)
+    b += 8.0 * (2.0 * packed_size(c->cd_nloc) - ptile_row_start(c->cd_nIp / 32));
   c->bytes_per_iter = b;
 }
 

@@ -14,7 +14,7 @@ from synthetic import make_problem
 pytestmark = pytest.mark.gpu
 
 
-def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=None, p2p=False):
+def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=None, p2p=False, coarse=None):
     import torch
     import paper_2304_09770_b200 as vb
     if srank is None:
@@ -27,7 +27,10 @@ def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=N
         ctx = vb.context_for(prob, stream=streams[r], rank=r, nranks=R, subdomain_rank=srank, world=world)
         if p2p:
             ctx.set_option("p2p", 1)
+        if coarse is not None:
+            ctx.set_option("coarse_dissection", coarse)
         ctx.factor()
+        stats = ctx.stats()
         rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
         x = torch.zeros_like(rhs)
         torch.cuda.synchronize()
@@ -42,7 +45,7 @@ def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=N
         rh = rhs.cpu().numpy()
         xh = np.zeros(ctx.n_free)
         ctx.pcg_solve_host(rh, xh, rtol=rtol)
-        out = dict(rep=rep, ids=ctx.dof_layout(), x=x.cpu().numpy(), rhs=rh, res=res, x_host=xh)
+        out = dict(rep=rep, ids=ctx.dof_layout(), x=x.cpu().numpy(), rhs=rh, res=res, x_host=xh, stats=stats)
         ctx.close()
         return out
 
@@ -77,6 +80,7 @@ def _global_free_ids(gs):
     ("c1", {}, (1, 1, 2)),
     ("c1", {}, (2, 2, 2)),
     ("c1", dict(n=8), (1, 2, 2)),
+    ("c1", dict(n=8), (2, 2, 2)),
     ("c4", dict(n=8, constraints=dict(adaptive_tau=0.0)), (2, 1, 1)),
     ("c3", dict(n=8), (2, 1, 1)),
 ])
@@ -222,3 +226,91 @@ def test_multirank_peer_stores_bitwise(name, kw, assign):
         assert np.array_equal(a["x"], b["x"])
         assert np.array_equal(a["x_host"], b["x_host"])
         assert a["rep"]["rel_residual"] == b["rep"]["rel_residual"]
+
+
+@pytest.mark.parametrize("name,kw,grid", [
+    ("c1", dict(n=8), 1),                 # one rank: root = the p_0's only
+    ("c1", dict(n=8), (2, 2, 2)),         # 8 rank boxes of 2^3 subdomains (interior entities on every rank)
+    ("c1", dict(n=8), "checkerboard"),    # every entity crosses ranks: no interior DOFs anywhere
+    ("c1", dict(n=8), "stripes3"),        # ragged rank sizes
+    ("c3", dict(n=8), (2, 1, 1)),         # k = 3, jittered triangulated cells
+    ("c4", dict(n=16, constraints=dict(adaptive_tau=2.0)), (2, 2, 1)),   # adaptive rows on the separator
+])
+def test_coarse_dissection_matches_dense_coarse(name, kw, grid):
+    """the rank-level dissection of the coarse saddle problem (block elimination of every
+    rank's interior primal DOFs, root = separator + p_0) gives the solve of the
+    replicated dense coarse inverse up to rounding: iterations within 1, kappa to 1e-4, solutions to 1e-10;
+    its root is smaller than N_c whenever a rank owns interior entities."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    prob = make_problem(name, **kw)
+    if grid == 1:
+        runs = []
+        for opt in (0, 1):
+            ctx = vb.context_for(prob)
+            ctx.set_option("coarse_dissection", opt)
+            ctx.factor()
+            st = ctx.stats()
+            rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
+            ctx.build_rhs(vb.problem_args(prob), rhs)
+            x = torch.zeros_like(rhs)
+            rep = ctx.pcg_solve(rhs, x, rtol=1e-10)
+            runs.append([dict(rep=rep, x=x.cpu().numpy(), ids=ctx.dof_layout(), stats=st)])
+            ctx.close()
+        n_sub = int(np.prod(prob.sub_grid))
+        assert runs[1][0]["stats"]["n_coarse_root"] == n_sub          # only the p_0's
+        assert runs[0][0]["stats"]["n_coarse_root"] == 0
+    else:
+        if isinstance(grid, str):
+            srank, R = _srank(prob, grid)
+            runs = [_run_ranks(prob, None, srank=srank, R=R, coarse=opt, check_operator=False) for opt in (0, 1)]
+        else:
+            runs = [_run_ranks(prob, grid, coarse=opt, check_operator=False) for opt in (0, 1)]
+    dense, dis = runs
+    for a, b in zip(dense, dis):
+        assert np.array_equal(a["ids"], b["ids"])
+        assert abs(a["rep"]["iterations"] - b["rep"]["iterations"]) <= 1
+        assert abs(a["rep"]["kappa"] - b["rep"]["kappa"]) <= 1e-4 * a["rep"]["kappa"]
+        assert a["rep"]["n_coarse"] == b["rep"]["n_coarse"]
+        st = b["stats"]
+        assert 0 < st["n_coarse_root"] <= st["n_coarse"]
+        if grid == (2, 2, 2):
+            assert st["n_coarse_root"] < st["n_coarse"] // 2
+    xa = np.concatenate([o["x"] for o in dense])
+    xb = np.concatenate([o["x"] for o in dis])
+    assert np.linalg.norm(xb - xa) <= 1e-10 * np.linalg.norm(xa)
+
+
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_full_size_eight_ranks_vs_oracle_golden(name):
+    """SURVEY f1 / §8(e) at full size: config 2 (64 subdomains) and config 5 (the bench workload,
+    512 subdomains, 954,947 DOFs) split over 8 loopback ranks in 2x2x2 boxes, coarse problem by
+    rank-level dissection (the default for R > 1), against the stored whole-vector oracle solve
+    (tests/golden, oracle/ only): velocity and pressure blocks at relative L2 <= 1e-8, iterations
+    +-1, kappa 1 %."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    from synthetic.configs import C5_DIMS
+    from test_gpu_vem import load_golden
+    prob = make_problem(name, dims=C5_DIMS[1]) if name == "c5" else make_problem(name)
+    z, meta = load_golden(name)
+    ctx1 = vb.context_for(prob)
+    ids1 = ctx1.dof_layout()   # 1-rank free order = the golden's order (setup only)
+    ctx1.close()
+    pos = np.full(int(ids1.max()) + 1, -1, np.int64)
+    pos[ids1] = np.arange(ids1.size)
+    outs = _run_ranks(prob, (2, 2, 2), check_operator=False)
+    x = np.full(ids1.size, np.nan)
+    for o in outs:
+        x[pos[o["ids"]]] = o["x"]
+        assert o["stats"]["n_coarse_root"] < o["stats"]["n_coarse"]
+        assert abs(o["rep"]["iterations"] - meta["iterations"]) <= 1
+        assert abs(o["rep"]["kappa"] - meta["kappa"]) <= 0.01 * meta["kappa"]
+    nv = meta["n_free_vel"]
+    xo = z["x_full"]
+    du = np.linalg.norm(x[:nv] - xo[:nv]) / np.linalg.norm(xo[:nv])
+    dp = np.linalg.norm(x[nv:] - xo[nv:]) / np.linalg.norm(xo[nv:])
+    print("%s 8 ranks: du %.2e dp %.2e it %d (oracle %d), root %d of N_c %d, local %s"
+          % (name, du, dp, outs[0]["rep"]["iterations"], meta["iterations"], outs[0]["stats"]["n_coarse_root"],
+             outs[0]["stats"]["n_coarse"], [o["stats"]["n_coarse_local"] for o in outs]))
+    assert du <= 1e-8 and dp <= 1e-8, (du, dp)
