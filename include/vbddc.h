@@ -114,6 +114,17 @@ vb_status vb_plan_exchange(const vb_mesh *mesh, const int32_t *cell_subdomain, i
                            const int32_t *subdomain_rank, int32_t rank, int32_t nranks, int32_t mode,
                            int64_t *send_counts, int64_t *recv_counts, int64_t *n_owned_free);
 
+/* Host-only planning, no GPU needed: the sizes of the rank-level coarse
+ * dissection this rank would build if every interface entity of kind q (0 vertex, 1 edge, 2 face)
+ * carried min(n_e, primal_per_kind[q]) primal DOFs (the factor computes the true counts by the
+ * pivoted QR of the constraint rows; for the BASELINE constraints on hexahedral meshes they are
+ * 3 / 3 / 3).  out6 = {interior DOFs n_I of this rank, its root list n_S (touched separator DOFs +
+ * its p_0's), separator DOFs n_sep, root order n_root = n_sep + n_subdomains, local packed order
+ * ceil32(n_I) + n_S, N_Pi}. */
+vb_status vb_plan_coarse_dissection(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
+                                    const int32_t *subdomain_rank, int32_t rank, int32_t nranks,
+                                    const int32_t *primal_per_kind, int64_t *out6);
+
 /* Build the context: topology, DOF numbering, box-free general subdomain
  * classification, interface entities, and the VEM element matrices A^K, B^K computed
  * on the device from the geometry and the per-cell viscosity.

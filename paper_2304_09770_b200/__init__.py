@@ -105,7 +105,7 @@ _vb_debug_gemm = _sig("vb_debug_gemm", ctypes.c_int,
                       ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _p,
                       ctypes.c_int32, ctypes.c_int32, ctypes.c_int32])
 
-EXPORTED = ["vb_plan_exchange", "vb_nccl_unique_id", "vb_loopback_world_create", "vb_loopback_world_destroy", "vb_setup", "vb_setup_from_elements", "vb_factor", "vb_build_rhs",
+EXPORTED = ["vb_plan_exchange", "vb_plan_coarse_dissection", "vb_nccl_unique_id", "vb_loopback_world_create", "vb_loopback_world_destroy", "vb_setup", "vb_setup_from_elements", "vb_factor", "vb_build_rhs",
             "vb_pcg_solve", "vb_pcg_solve_host", "vb_apply_operator", "vb_debug_interface_op", "vb_debug_gemm",
             "vb_interface_dofs", "vb_num_free_dofs", "vb_dof_layout",
             "vb_cell_local_dofs", "vb_get_element_matrices", "vb_stats", "vb_kernel_times",
@@ -423,6 +423,26 @@ def plan_exchange(mesh, k, cell_subdomain, subdomain_rank, rank, nranks, mode=0)
     if st != VB_OK:
         raise VBError(st, _vb_last_error(None).decode())
     return snd, rcv, own.value
+
+
+_vb_plan_cd = _sig("vb_plan_coarse_dissection", ctypes.c_int, [ctypes.POINTER(VBMesh), _i32p, ctypes.c_int32, _i32p,
+                                                              ctypes.c_int32, ctypes.c_int32, _i32p, _i64p])
+
+
+def plan_coarse_dissection(mesh, k, cell_subdomain, subdomain_rank, rank, nranks, primal_per_kind=(3, 3, 3)):
+    """Host-only (no GPU): sizes of this rank's coarse dissection (vb_plan_coarse_dissection):
+    dict(n_interior, n_S, n_sep, n_root, n_local, n_primal)."""
+    keep = []
+    m = _mesh_struct(mesh, k, keep)
+    sub = _arr(cell_subdomain, np.int32)
+    sr = _arr(subdomain_rank if subdomain_rank is not None else np.zeros(int(sub.max()) + 1), np.int32)
+    ppk = np.asarray(primal_per_kind, np.int32)
+    out = np.zeros(6, np.int64)
+    st = _vb_plan_cd(ctypes.byref(m), _ptr(sub, ctypes.c_int32), int(sub.max()) + 1, _ptr(sr, ctypes.c_int32),
+                     int(rank), int(nranks), _ptr(ppk, ctypes.c_int32), _ptr(out, ctypes.c_int64))
+    if st != VB_OK:
+        raise VBError(st, _vb_last_error(None).decode())
+    return dict(zip(["n_interior", "n_S", "n_sep", "n_root", "n_local", "n_primal"], out.tolist()))
 
 
 def _mesh_struct(mesh, k, keep):

@@ -408,6 +408,38 @@ vb_status vb_plan_exchange(const vb_mesh *mesh, const int32_t *cell_subdomain, i
   return VB_OK;
 }
 
+vb_status vb_plan_coarse_dissection(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
+                                    const int32_t *subdomain_rank, int32_t rank, int32_t nranks,
+                                    const int32_t *primal_per_kind, int64_t *out6) {
+  if (!mesh || !cell_subdomain || !primal_per_kind || !out6 || nranks < 1 || rank < 0 || rank >= nranks ||
+      (nranks > 1 && !subdomain_rank))
+    return VB_EINVAL;
+  vb_ctx c;   // host bookkeeping only: no device work
+  try {
+    VB_REQUIRE(mesh->k >= 2 && mesh->k <= 4, VB_EINVAL, "k must be 2, 3 or 4");
+    for (int q = 0; q < 3; ++q) VB_REQUIRE(primal_per_kind[q] >= 0, VB_EINVAL, "negative primal count");
+    c.k = mesh->k;
+    c.rank = rank;
+    c.nranks = nranks;
+    build_topology(&c, mesh);
+    build_subdomains(&c, cell_subdomain, n_subdomains, nranks > 1 ? subdomain_rank : nullptr);
+    int64_t off = 0;
+    for (auto &G : c.gents) {
+      G.r = std::min(G.n, (int)primal_per_kind[G.kind]);
+      G.off_pi = off;
+      off += G.r;
+    }
+    c.NPi_g = off;
+    const CoarsePlan P = plan_coarse_dissection(&c);
+    const int64_t nI = P.Iglob.size(), nS = P.Sr[rank].size();
+    const int64_t v[6] = {nI, nS, P.nsep, (int64_t)P.root.size(), (nI + 31) / 32 * 32 + nS, c.NPi_g};
+    memcpy(out6, v, sizeof(v));
+  } catch (const Error &e) {
+    return fail(nullptr, e);
+  }
+  return VB_OK;
+}
+
 vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n_subdomains,
                    const int32_t *subdomain_rank, const vb_constraints *cons, const double *cell_viscosity,
                    const vb_dist *dist, vb_ctx **out) {

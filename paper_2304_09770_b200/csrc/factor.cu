@@ -787,6 +787,73 @@ static void coarse_inverse_pack(vb_ctx *c, DBuf<double> &Kc, int64_t ldC, int64_
   }
 }
 
+// Host part of the coarse dissection (also vb_plan_coarse_dissection, no device work): interior
+// DOFs of rank `me`, the root, every rank's root list S_r and the root-rhs sources.
+CoarsePlan plan_coarse_dissection(const vb_ctx *c) {
+  CoarsePlan P;
+  const int R = c->nranks, me = c->rank, Ng = c->Ng;
+  const int64_t NPi = c->NPi_g, Nc = NPi + Ng;
+  const int ne = c->gents.size();
+  std::vector<int> erank(ne, -1);   // the one rank of all sharers, or -1 (separator)
+  for (int e = 0; e < ne; ++e) {
+    const GEnt &E = c->gents[e];
+    if (E.r <= 0 || E.sharers.empty()) continue;
+    int r0 = c->sub_rank[E.sharers[0]];
+    for (int g : E.sharers)
+      if (c->sub_rank[g] != r0) { r0 = -1; break; }
+    erank[e] = r0;
+  }
+  std::vector<int64_t> &root = P.root, &Iglob = P.Iglob;
+  for (int e = 0; e < ne; ++e) {
+    const GEnt &E = c->gents[e];
+    if (E.r <= 0) continue;
+    for (int t = 0; t < E.r; ++t) {
+      if (erank[e] < 0) root.push_back(E.off_pi + t);
+      else if (erank[e] == me) Iglob.push_back(E.off_pi + t);
+    }
+  }
+  std::sort(root.begin(), root.end());
+  std::sort(Iglob.begin(), Iglob.end());
+  const int64_t nsep = root.size();
+  P.nsep = nsep;
+  for (int g = 0; g < Ng; ++g) root.push_back(NPi + g);
+  const int64_t nroot = root.size();
+  std::vector<int64_t> rpos(Nc, -1);
+  for (int64_t j = 0; j < nroot; ++j) rpos[root[j]] = j;
+  // every rank's root list: the separator DOFs its subdomains touch (sorted), then its p_0's
+  std::vector<std::vector<int64_t>> &Sr = P.Sr;
+  Sr.assign(R, {});
+  {
+    for (int g = 0; g < Ng; ++g) {
+      const int r = c->sub_rank[g];
+      for (int e : c->gsub_ents[g])
+        if (c->gents[e].r > 0 && erank[e] < 0)
+          for (int t = 0; t < c->gents[e].r; ++t) Sr[r].push_back(c->gents[e].off_pi + t);
+    }
+    for (int r = 0; r < R; ++r) {   // an entity is seen once per sharing subdomain of the rank
+      std::sort(Sr[r].begin(), Sr[r].end());
+      Sr[r].erase(std::unique(Sr[r].begin(), Sr[r].end()), Sr[r].end());
+    }
+    for (int g = 0; g < Ng; ++g) Sr[c->sub_rank[g]].push_back(NPi + g);
+  }
+  int64_t &maxS = P.maxS;
+  maxS = 1;
+  for (int r = 0; r < R; ++r) maxS = std::max<int64_t>(maxS, Sr[r].size());
+  // root rhs sources: root entry j <- t_r[q] (gathered at r * maxS + q) for every S_r[q] = root[j]
+  std::vector<int64_t> &rptr = P.rptr, &ridx = P.ridx;
+  rptr.assign(nroot + 1, 0);
+  for (int r = 0; r < R; ++r)
+    for (int64_t v : Sr[r]) ++rptr[rpos[v] + 1];
+  for (int64_t j = 0; j < nroot; ++j) rptr[j + 1] += rptr[j];
+  ridx.resize(rptr[nroot]);
+  {
+    std::vector<int64_t> fill(rptr.begin(), rptr.end() - 1);
+    for (int r = 0; r < R; ++r)
+      for (size_t q = 0; q < Sr[r].size(); ++q) ridx[fill[rpos[Sr[r][q]]]++] = (int64_t)r * maxS + q;
+  }
+  return P;
+}
+
 // rank-level dissection of the coarse saddle problem (solved by block
 // elimination).  The primal DOFs of an entity whose sharers all live on rank r are
 // interior to r: only r's subdomains contribute to their rows and columns, so r eliminates them
@@ -805,60 +872,12 @@ static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector
   cudaStream_t s = c->stream;
   const int R = c->nranks, me = c->rank, Ng = c->Ng, N = c->N;
   const int64_t NPi = c->NPi_g, Nc = c->Nc;
-  const int ne = c->gents.size();
-  std::vector<int> erank(ne, -1);   // the one rank of all sharers, or -1 (separator)
-  for (int e = 0; e < ne; ++e) {
-    const GEnt &E = c->gents[e];
-    if (E.r <= 0 || E.sharers.empty()) continue;
-    int r0 = c->sub_rank[E.sharers[0]];
-    for (int g : E.sharers)
-      if (c->sub_rank[g] != r0) { r0 = -1; break; }
-    erank[e] = r0;
-  }
-  std::vector<int64_t> root, Iglob;
-  for (int e = 0; e < ne; ++e) {
-    const GEnt &E = c->gents[e];
-    if (E.r <= 0) continue;
-    for (int t = 0; t < E.r; ++t) {
-      if (erank[e] < 0) root.push_back(E.off_pi + t);
-      else if (erank[e] == me) Iglob.push_back(E.off_pi + t);
-    }
-  }
-  std::sort(root.begin(), root.end());
-  std::sort(Iglob.begin(), Iglob.end());
-  const int64_t nsep = root.size();
-  for (int g = 0; g < Ng; ++g) root.push_back(NPi + g);
-  const int64_t nroot = root.size();
+  const CoarsePlan P = plan_coarse_dissection(c);
+  const std::vector<int64_t> &root = P.root, &Iglob = P.Iglob, &rptr = P.rptr, &ridx = P.ridx;
+  const std::vector<std::vector<int64_t>> &Sr = P.Sr;
+  const int64_t nsep = P.nsep, nroot = root.size(), maxS = P.maxS;
   std::vector<int64_t> rpos(Nc, -1);
   for (int64_t j = 0; j < nroot; ++j) rpos[root[j]] = j;
-  // every rank's root list: the separator DOFs its subdomains touch (sorted), then its p_0's
-  std::vector<std::vector<int64_t>> Sr(R);
-  {
-    for (int g = 0; g < Ng; ++g) {
-      const int r = c->sub_rank[g];
-      for (int e : c->gsub_ents[g])
-        if (c->gents[e].r > 0 && erank[e] < 0)
-          for (int t = 0; t < c->gents[e].r; ++t) Sr[r].push_back(c->gents[e].off_pi + t);
-    }
-    for (int r = 0; r < R; ++r) {   // an entity is seen once per sharing subdomain of the rank
-      std::sort(Sr[r].begin(), Sr[r].end());
-      Sr[r].erase(std::unique(Sr[r].begin(), Sr[r].end()), Sr[r].end());
-    }
-    for (int g = 0; g < Ng; ++g) Sr[c->sub_rank[g]].push_back(NPi + g);
-  }
-  int64_t maxS = 1;
-  for (int r = 0; r < R; ++r) maxS = std::max<int64_t>(maxS, Sr[r].size());
-  // root rhs sources: root entry j <- t_r[q] (gathered at r * maxS + q) for every S_r[q] = root[j]
-  std::vector<int64_t> rptr(nroot + 1, 0), ridx;
-  for (int r = 0; r < R; ++r)
-    for (int64_t v : Sr[r]) ++rptr[rpos[v] + 1];
-  for (int64_t j = 0; j < nroot; ++j) rptr[j + 1] += rptr[j];
-  ridx.resize(rptr[nroot]);
-  {
-    std::vector<int64_t> fill(rptr.begin(), rptr.end() - 1);
-    for (int r = 0; r < R; ++r)
-      for (size_t q = 0; q < Sr[r].size(); ++q) ridx[fill[rpos[Sr[r][q]]]++] = (int64_t)r * maxS + q;
-  }
   const int64_t nI = Iglob.size(), nIp = (nI + 31) / 32 * 32, nS = Sr[me].size(), nloc = nIp + nS;
   std::vector<int64_t> lp(Nc, -1);
   for (int64_t a = 0; a < nI; ++a) lp[Iglob[a]] = a;

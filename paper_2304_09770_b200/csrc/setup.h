@@ -39,6 +39,16 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t 
 void face_frame(const vb_ctx *c, int64_t f, double *area, double n[3], double t1[3], double t2[3]);
 void build_constraint_rows(vb_ctx *c, std::vector<double> &rows_out);
 
+// SURVEY f1 (factor.cu): the host plan of the rank-level coarse dissection from the global entity
+// list (gents[].r, off_pi, sharers), gsub_ents, sub_rank, NPi_g, Ng, rank and nranks
+struct CoarsePlan {
+  std::vector<int64_t> root, Iglob;          // global coarse indices (root: separator, then every p_0)
+  std::vector<std::vector<int64_t>> Sr;      // per rank: touched separator DOFs (sorted), then its p_0's
+  std::vector<int64_t> rptr, ridx;           // root entry <- gathered t entries r * maxS + q
+  int64_t nsep = 0, maxS = 1;
+};
+CoarsePlan plan_coarse_dissection(const vb_ctx *c);
+
 // device-side stages (defined in the .cu files)
 void cell_geometry_device(vb_ctx *c);                    // vem.cu
 void layout_phase_a(vb_ctx *c);                          // abi.cu

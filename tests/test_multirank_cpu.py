@@ -104,3 +104,74 @@ def test_exchange_plans_agree_across_ranks(name, kw, rank_grid):
     assert ok
     assert total == nfree
 
+
+
+def _cd_worker(rank, world, port, name, kw, rank_grid, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2304_09770_b200 as vb
+        from synthetic import make_problem
+        prob = make_problem(name, **kw)
+        srank = _layout(vb, prob, rank_grid)
+        p = vb.plan_coarse_dissection(prob.mesh, prob.k, prob.cell_subdomain, srank, rank, world)
+        v = torch.tensor([p["n_interior"], p["n_S"], p["n_sep"], p["n_root"], p["n_primal"],
+                          int(np.sum(srank == rank))])
+        V = [torch.zeros(6, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(V, v)
+        if rank == 0:
+            q.put((torch.stack(V).numpy(), int(np.prod(prob.sub_grid))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,kw,rank_grid", [("c5", dict(dims=(32, 32, 64)), (1, 1, 2)),
+                                              ("c1", dict(n=8), (2, 2, 1)),
+                                              ("c1", dict(n=8), "checker")])
+def test_coarse_dissection_plans_agree_across_ranks(name, kw, rank_grid):
+    """SURVEY f1 host plan over gloo: every rank derives the same separator and root (the root is
+    replicated), the interior sets and the separator partition the primal DOFs, the root is the
+    separator plus one p_0 per subdomain, and each rank's root list holds its own p_0's.  c5 at its
+    2-GPU size (1,024 subdomains): one cut plane of 8 x 8 subdomain faces."""
+    world = _world(rank_grid)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cd_worker, args=(r, world, port, name, kw, rank_grid, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    V, nsub = q.get(timeout=10)
+    nI, nS, nsep, nroot, npi, nown = V.T
+    assert len(set(nsep)) == 1 and len(set(nroot)) == 1 and len(set(npi)) == 1
+    assert nI.sum() + nsep[0] == npi[0]
+    assert nroot[0] == nsep[0] + nsub
+    assert np.all(nS >= nown) and np.all(nS - nown <= nsep[0])
+    if rank_grid == "checker":
+        assert np.all(nI == 0)             # every entity crosses ranks
+    if name == "c5":
+        # one cut plane z = 8 of the 8 x 8 x 16 subdomain grid: 64 faces, 2 * 8 * 7 edges, 7 * 7
+        # vertices, 3 primal DOFs each; every other primal DOF is interior to one rank
+        assert nsep[0] == 3 * (64 + 112 + 49)
+        assert np.array_equal(nS, nsep + 512)
+
+
+def test_coarse_dissection_plan_at_eight_gpus():
+    """The 8-GPU sizes DESIGN.md §9 quotes, from the host planner on rank 0 of c5 at 64^3 cells
+    (4,096 subdomains, 2x2x2 rank boxes): separator 3 (768 + 1,392 + 631) = 8,373 DOFs (three cut
+    planes, inclusion-exclusion on their lines and centre point), root 8,373 + 4,096 = 12,469,
+    8,589 interior DOFs per rank (= N_Pi of one 8^3-subdomain box)."""
+    import paper_2304_09770_b200 as vb
+    from synthetic import make_problem
+    from synthetic.configs import C5_DIMS
+    prob = make_problem("c5", dims=C5_DIMS[8])
+    srank = vb.box_ranks(prob.sub_grid, (2, 2, 2))
+    p = vb.plan_coarse_dissection(prob.mesh, prob.k, prob.cell_subdomain, srank, 0, 8)
+    assert p["n_primal"] + 4096 == 81181          # N_c at 8 GPUs (DESIGN.md §9)
+    assert p["n_sep"] == 8373 and p["n_root"] == 12469
+    assert p["n_interior"] == 8589
+    assert p["n_S"] == 2675 and p["n_local"] == 8608 + 2675   # 2,163 touched separator DOFs + 512 p_0
+    print("8-GPU plan rank 0:", p)
