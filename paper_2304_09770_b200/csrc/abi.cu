@@ -152,8 +152,10 @@ void layout_phase_a(vb_ctx *c) {
       dof_ent[c->ents[e].dofs[a]] = (int)e;
       dof_epos[c->ents[e].dofs[a]] = (int)a;
     }
+  // threads over subdomains (interior DOFs and cells belong to one subdomain: disjoint writes)
+  parallel_for(N, [&](int64_t i0, int64_t i1) {
   std::vector<int> ent_slot(c->ents.size(), -1);   // entity -> its index t in the current subdomain
-  for (int i = 0; i < N; ++i) {
+  for (int64_t i = i0; i < i1; ++i) {
     Sub &S = c->subs[i];
     for (int j = 0; j < S.nI; ++j) posI[S.I[j]] = j;
     for (size_t t = 0; t < S.ents.size(); ++t) ent_slot[S.ents[t]] = (int)t;
@@ -179,6 +181,7 @@ void layout_phase_a(vb_ctx *c) {
     }
     for (size_t t = 0; t < S.ents.size(); ++t) ent_slot[S.ents[t]] = -1;
   }
+  }, 16);
   c->d_cell_loc.upload(loc, s);
   c->h_cell_loc = loc;
   // element-by-element operator / rhs: free velocity dof -> contribution slots (local cells, in order)
@@ -305,21 +308,31 @@ static void common_setup(vb_ctx *c, const vb_mesh *m, const int32_t *cell_sub, i
   setup_time("subdomains / DOF maps", ts);
   cudaStream_t s = c->stream;
   // device copies of the LOCAL cells (topology, viscosity, dof maps); vertices and the dof status are global
-  std::vector<int> topo((size_t)c->nKl * TOPO_STRIDE);
-  std::vector<double> nul(c->nKl);
-  std::vector<int> nvl(c->nKl);
-  std::vector<int64_t> l2g((size_t)c->nKl * c->nv_max, -1);
-  for (int64_t l = 0; l < c->nKl; ++l) {
-    const int64_t K = c->cell_gid[l];
-    std::copy(c->cell_topo.begin() + K * TOPO_STRIDE, c->cell_topo.begin() + (K + 1) * TOPO_STRIDE, topo.begin() + l * TOPO_STRIDE);
-    nul[l] = c->nu[K];
-    nvl[l] = c->cell_nv[K];
-    for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) l2g[l * c->nv_max + (j - c->cell_l2g_ptr[K])] = c->cell_l2g[j];
-  }
+  // (all cells local, one rank: the global arrays are uploaded as they are)
+  const bool all_local = c->nKl == c->nK;
+  std::vector<int> topo(all_local ? 0 : (size_t)c->nKl * TOPO_STRIDE);
+  std::vector<double> nul(all_local ? 0 : c->nKl);
+  std::vector<int> nvl(all_local ? 0 : c->nKl);
+  std::vector<int64_t> l2g((size_t)c->nKl * c->nv_max);
+  parallel_for(c->nKl, [&](int64_t l0, int64_t l1) {
+    for (int64_t l = l0; l < l1; ++l) {
+      const int64_t K = c->cell_gid[l];
+      if (!all_local) {
+        std::copy(c->cell_topo.begin() + K * TOPO_STRIDE, c->cell_topo.begin() + (K + 1) * TOPO_STRIDE,
+                  topo.begin() + l * TOPO_STRIDE);
+        nul[l] = c->nu[K];
+        nvl[l] = c->cell_nv[K];
+      }
+      int64_t *o = l2g.data() + l * c->nv_max;
+      const int64_t n = c->cell_l2g_ptr[K + 1] - c->cell_l2g_ptr[K];
+      std::copy(c->cell_l2g.begin() + c->cell_l2g_ptr[K], c->cell_l2g.begin() + c->cell_l2g_ptr[K + 1], o);
+      std::fill(o + n, o + c->nv_max, (int64_t)-1);
+    }
+  });
   c->d_xyz.upload(c->xyz, s);
-  c->d_topo.upload(topo, s);
-  c->d_nu.upload(nul, s);
-  c->d_cell_nv.upload(nvl, s);
+  c->d_topo.upload(all_local ? c->cell_topo : topo, s);
+  c->d_nu.upload(all_local ? c->nu : nul, s);
+  c->d_cell_nv.upload(all_local ? c->cell_nv : nvl, s);
   c->d_vel2free.upload(c->vel2free, s);
   c->d_cell_l2g.upload(l2g, s);
   c->d_cell_gid.upload(c->cell_gid, s);

@@ -3,9 +3,12 @@
 // This is index bookkeeping and O(#interface DOFs) geometry; every O(n^2)/O(n^3) numeric step
 // of the method runs on the device (vem.cu, dense.cu, factor.cu, solve.cu).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <map>
+#include <unordered_map>
 #include <numeric>
+#include <chrono>
 #include "internal.h"
 #include "setup.h"
 
@@ -64,9 +67,22 @@ void gauss_lobatto01(int npts, double *x, double *w) {
 static inline int dim2(int n) { return n < 0 ? 0 : (n + 1) * (n + 2) / 2; }
 static inline int dim3(int n) { return n < 0 ? 0 : (n + 1) * (n + 2) * (n + 3) / 6; }
 
+static double wall_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+// VB_SETUP_TIMES=2: fine timers of the host setup passes
+static void fine_time(const char *what, double &t) {
+  static const bool on = getenv("VB_SETUP_TIMES") && atoi(getenv("VB_SETUP_TIMES")) >= 2;
+  if (!on) return;
+  const double now = wall_s();
+  fprintf(stderr, "[vb setup]   %-30s %.3f s\n", what, now - t);
+  t = now;
+}
+
 // ------------------------------------------------------------------ topology and numbering
 void build_topology(vb_ctx *c, const vb_mesh *m) {
   int k = c->k;
+  double tf = wall_s();
   c->nV = m->n_vertices; c->nF = m->n_faces; c->nK = m->n_cells;
   c->xyz.assign(m->xyz, m->xyz + 3 * c->nV);
   c->face_ptr.assign(m->face_ptr, m->face_ptr + c->nF + 1);
@@ -90,11 +106,19 @@ void build_topology(vb_ctx *c, const vb_mesh *m) {
   std::sort(keys.begin(), keys.end());
   keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
   c->nE = keys.size();
+  fine_time("edges", tf);
   c->edges.resize(2 * c->nE);
   for (int64_t i = 0; i < c->nE; ++i) { c->edges[2 * i] = keys[i] / nV; c->edges[2 * i + 1] = keys[i] % nV; }
+  // edges grouped by their smaller vertex (keys are sorted by (min, max)): an edge id is a search
+  // among the few edges of one vertex instead of over all keys
+  std::vector<int64_t> eptr(nV + 1, 0);
+  for (int64_t i = 0; i < c->nE; ++i) ++eptr[c->edges[2 * i] + 1];
+  for (int64_t v = 0; v < nV; ++v) eptr[v + 1] += eptr[v];
   auto edge_id = [&](int64_t a, int64_t b) {
-    int64_t key = std::min(a, b) * nV + std::max(a, b);
-    return (int64_t)(std::lower_bound(keys.begin(), keys.end(), key) - keys.begin());
+    const int64_t lo = std::min(a, b), hi = std::max(a, b);
+    int64_t i = eptr[lo];
+    while (i < eptr[lo + 1] && c->edges[2 * i + 1] < hi) ++i;
+    return i;
   };
   // numbering (identical convention to DESIGN.md §Layout)
   c->nm = dim2(k - 2);
@@ -124,6 +148,7 @@ void build_topology(vb_ctx *c, const vb_mesh *m) {
   for (int64_t g = 0; g < c->nvel; ++g)
     if (!isb[g]) { c->vel2free[g] = c->free2vel.size(); c->free2vel.push_back(g); }
   c->n_free_vel = c->free2vel.size();
+  fine_time("numbering", tf);
   // per-cell local topology (vertices / edges / faces in increasing global id)
   c->topo_stride = TOPO_STRIDE;
   c->cell_topo.assign((size_t)c->nK * TOPO_STRIDE, 0);
@@ -131,58 +156,82 @@ void build_topology(vb_ctx *c, const vb_mesh *m) {
   c->cell_l2g_ptr.assign(c->nK + 1, 0);
   c->cell_l2g.clear();
   c->nv_max = 0;
-  for (int64_t K = 0; K < c->nK; ++K) {
-    int64_t s = c->cell_ptr[K], e = c->cell_ptr[K + 1];
-    int nf = e - s;
-    VB_REQUIRE(nf >= 4 && nf <= MAXF, VB_EINVAL, "cell " + std::to_string(K) + " has an unsupported face count");
-    std::vector<std::pair<int64_t, int>> fl;
-    for (int64_t j = s; j < e; ++j) fl.push_back({c->cell_face[j], (int)c->cell_sign[j]});
-    std::sort(fl.begin(), fl.end());
-    std::vector<int64_t> vs, es;
-    for (auto &fs : fl) {
-      int64_t a0 = c->face_ptr[fs.first], a1 = c->face_ptr[fs.first + 1];
-      for (int64_t i = a0; i < a1; ++i) {
-        vs.push_back(c->face_vtx[i]);
-        es.push_back(edge_id(c->face_vtx[i], c->face_vtx[i + 1 < a1 ? i + 1 : a0]));
+  // pass 1 (threads over cells): sorted faces, vertices and edges of each cell, its packed topology
+  // and DOF count; the global face / edge ids are kept for pass 2
+  std::vector<int64_t> cface((size_t)c->nK * MAXF), cedge((size_t)c->nK * MAXE);
+  std::vector<int> nvmax_part(64, 0);
+  std::atomic<int> chunk_id{0};
+  parallel_for(c->nK, [&](int64_t K0, int64_t K1) {
+    const int my = chunk_id++;
+    int nvm = 0;
+    std::pair<int64_t, int> fl[MAXF];
+    int64_t vs[MAXF * MAXL], es[MAXF * MAXL];
+    for (int64_t K = K0; K < K1; ++K) {
+      int64_t s = c->cell_ptr[K], e = c->cell_ptr[K + 1];
+      int nf = e - s;
+      VB_REQUIRE(nf >= 4 && nf <= MAXF, VB_EINVAL, "cell " + std::to_string(K) + " has an unsupported face count");
+      for (int64_t j = s; j < e; ++j) fl[j - s] = {c->cell_face[j], (int)c->cell_sign[j]};
+      std::sort(fl, fl + nf);
+      int nvs = 0, nes = 0;
+      for (int f = 0; f < nf; ++f) {
+        int64_t a0 = c->face_ptr[fl[f].first], a1 = c->face_ptr[fl[f].first + 1];
+        for (int64_t i = a0; i < a1; ++i) {
+          vs[nvs++] = c->face_vtx[i];
+          es[nes++] = edge_id(c->face_vtx[i], c->face_vtx[i + 1 < a1 ? i + 1 : a0]);
+        }
       }
-    }
-    std::sort(vs.begin(), vs.end()); vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
-    std::sort(es.begin(), es.end()); es.erase(std::unique(es.begin(), es.end()), es.end());
-    VB_REQUIRE((int)vs.size() <= MAXV && (int)es.size() <= MAXE, VB_EINVAL,
-               "cell " + std::to_string(K) + " exceeds the supported vertex/edge count");
-    int ntri = 0;
-    for (auto &fs : fl) ntri += (int)(c->face_ptr[fs.first + 1] - c->face_ptr[fs.first]) - 2;
-    VB_REQUIRE(ntri <= MAXT, VB_EINVAL, "cell " + std::to_string(K) + " exceeds the supported fan-triangle count");
-    int *T = &c->cell_topo[(size_t)K * TOPO_STRIDE];
-    T[0] = vs.size(); T[1] = es.size(); T[2] = nf;
-    for (size_t i = 0; i < vs.size(); ++i) T[TOPO_V + i] = (int)vs[i];
-    auto lv = [&](int64_t g) { return (int)(std::lower_bound(vs.begin(), vs.end(), g) - vs.begin()); };
-    for (size_t i = 0; i < es.size(); ++i) {
-      T[TOPO_E + 2 * i] = lv(c->edges[2 * es[i]]);
-      T[TOPO_E + 2 * i + 1] = lv(c->edges[2 * es[i] + 1]);
-    }
-    for (int f = 0; f < nf; ++f) {
-      int *F = T + TOPO_F + f * FACE_STRIDE;
-      int64_t gf = fl[f].first, a0 = c->face_ptr[gf], a1 = c->face_ptr[gf + 1];
-      F[0] = fl[f].second; F[1] = a1 - a0;
-      for (int64_t i = a0; i < a1; ++i) {
-        int64_t a = c->face_vtx[i], b = c->face_vtx[i + 1 < a1 ? i + 1 : a0];
-        int q = i - a0;
-        F[2 + q] = lv(a);
-        F[2 + MAXL + q] = (int)(std::lower_bound(es.begin(), es.end(), edge_id(a, b)) - es.begin());
-        F[2 + 2 * MAXL + q] = a < b ? 1 : 0;
+      std::sort(vs, vs + nvs); nvs = std::unique(vs, vs + nvs) - vs;
+      std::sort(es, es + nes); nes = std::unique(es, es + nes) - es;
+      VB_REQUIRE(nvs <= MAXV && nes <= MAXE, VB_EINVAL,
+                 "cell " + std::to_string(K) + " exceeds the supported vertex/edge count");
+      int ntri = 0;
+      for (int f = 0; f < nf; ++f) ntri += (int)(c->face_ptr[fl[f].first + 1] - c->face_ptr[fl[f].first]) - 2;
+      VB_REQUIRE(ntri <= MAXT, VB_EINVAL, "cell " + std::to_string(K) + " exceeds the supported fan-triangle count");
+      int *T = &c->cell_topo[(size_t)K * TOPO_STRIDE];
+      T[0] = nvs; T[1] = nes; T[2] = nf;
+      for (int i = 0; i < nvs; ++i) T[TOPO_V + i] = (int)vs[i];
+      auto lv = [&](int64_t g) { return (int)(std::lower_bound(vs, vs + nvs, g) - vs); };
+      for (int i = 0; i < nes; ++i) {
+        T[TOPO_E + 2 * i] = lv(c->edges[2 * es[i]]);
+        T[TOPO_E + 2 * i + 1] = lv(c->edges[2 * es[i] + 1]);
       }
+      for (int f = 0; f < nf; ++f) {
+        int *F = T + TOPO_F + f * FACE_STRIDE;
+        int64_t gf = fl[f].first, a0 = c->face_ptr[gf], a1 = c->face_ptr[gf + 1];
+        F[0] = fl[f].second; F[1] = a1 - a0;
+        for (int64_t i = a0; i < a1; ++i) {
+          int64_t a = c->face_vtx[i], b = c->face_vtx[i + 1 < a1 ? i + 1 : a0];
+          int q = i - a0;
+          F[2 + q] = lv(a);
+          F[2 + MAXL + q] = (int)(std::lower_bound(es, es + nes, edge_id(a, b)) - es);
+          F[2 + 2 * MAXL + q] = a < b ? 1 : 0;
+        }
+        cface[(size_t)K * MAXF + f] = gf;
+      }
+      for (int i = 0; i < nes; ++i) cedge[(size_t)K * MAXE + i] = es[i];
+      const int nv = 3 * nvs + 3 * (k - 1) * nes + 3 * c->nm * nf + c->n4 + c->n5;
+      c->cell_nv[K] = nv;
+      nvm = std::max(nvm, nv);
     }
-    // local -> global velocity map (vertices, edges, faces, cell)
-    int nv = 3 * vs.size() + 3 * (k - 1) * es.size() + 3 * c->nm * nf + c->n4 + c->n5;
-    c->cell_nv[K] = nv;
-    c->nv_max = std::max(c->nv_max, nv);
-    for (auto g : vs) for (int q = 0; q < 3; ++q) c->cell_l2g.push_back(3 * g + q);
-    for (auto ed : es) for (int q = 0; q < 3 * (k - 1); ++q) c->cell_l2g.push_back(c->oE + 3 * (k - 1) * ed + q);
-    for (auto &fs : fl) for (int q = 0; q < 3 * c->nm; ++q) c->cell_l2g.push_back(c->oF + 3 * c->nm * fs.first + q);
-    for (int q = 0; q < c->n4 + c->n5; ++q) c->cell_l2g.push_back(c->oC + K * (c->n4 + c->n5) + q);
-    c->cell_l2g_ptr[K + 1] = c->cell_l2g.size();
-  }
+    nvmax_part[my] = nvm;
+  });
+  for (int v : nvmax_part) c->nv_max = std::max(c->nv_max, v);
+  fine_time("cell topology", tf);
+  for (int64_t K = 0; K < c->nK; ++K) c->cell_l2g_ptr[K + 1] = c->cell_l2g_ptr[K] + c->cell_nv[K];
+  // pass 2: local -> global velocity map (vertices, edges, faces, cell), in increasing global id
+  c->cell_l2g.resize(c->cell_l2g_ptr[c->nK]);
+  parallel_for(c->nK, [&](int64_t K0, int64_t K1) {
+    for (int64_t K = K0; K < K1; ++K) {
+      const int *T = &c->cell_topo[(size_t)K * TOPO_STRIDE];
+      int64_t *o = c->cell_l2g.data() + c->cell_l2g_ptr[K];
+      for (int i = 0; i < T[0]; ++i) for (int q = 0; q < 3; ++q) *o++ = 3 * (int64_t)T[TOPO_V + i] + q;
+      for (int i = 0; i < T[1]; ++i)
+        for (int q = 0; q < 3 * (k - 1); ++q) *o++ = c->oE + 3 * (k - 1) * cedge[(size_t)K * MAXE + i] + q;
+      for (int f = 0; f < T[2]; ++f)
+        for (int q = 0; q < 3 * c->nm; ++q) *o++ = c->oF + 3 * c->nm * cface[(size_t)K * MAXF + f] + q;
+      for (int q = 0; q < c->n4 + c->n5; ++q) *o++ = c->oC + K * (c->n4 + c->n5) + q;
+    }
+  });
 }
 
 // ------------------------------------------------------------------ subdomains and entities
@@ -192,6 +241,7 @@ void build_topology(vb_ctx *c, const vb_mesh *m) {
 // (renumbered in global order) and the entities they touch (renumbered in global order).
 void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t *sub_rank) {
   c->Ng = Ng;
+  double tf = wall_s();
   c->cell_sub.assign(cell_sub, cell_sub + c->nK);
   c->sub_rank.assign(Ng, 0);
   if (sub_rank) c->sub_rank.assign(sub_rank, sub_rank + Ng);
@@ -241,26 +291,40 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t 
       for (int *q = b; q < e; ++q) ds.push_back({f, *q});
     }
   }
-  std::map<std::vector<int>, int> emap;
+  fine_time("dof sharers", tf);
+  // entity classes: DOFs with equal sharer sets (hash of the sorted sharer list; the lookup key is
+  // a reused scratch vector, a new key is stored only for a new class)
+  struct VecHash {
+    size_t operator()(const std::vector<int> &v) const {
+      uint64_t h = 1469598103934665603ull;
+      for (int x : v) h = (h ^ (uint64_t)(uint32_t)x) * 1099511628211ull;
+      return (size_t)h;
+    }
+  };
+  std::unordered_map<std::vector<int>, int, VecHash> emap;
+  emap.reserve(1 << 16);
   std::vector<std::vector<int>> ekeys;
   std::vector<std::vector<int64_t>> edofs;
   c->dof_owner_sub.assign(c->n_free_vel, -1);
   c->dof_nsh.assign(c->n_free_vel, 0);
+  std::vector<int> sh;
   for (size_t i = 0; i < ds.size();) {
     size_t j = i;
-    std::vector<int> sh;
-    while (j < ds.size() && ds[j].first == ds[i].first) sh.push_back(ds[j++].second);
-    c->dof_owner_sub[ds[i].first] = sh[0];
-    c->dof_nsh[ds[i].first] = sh.size();
-    if (sh.size() > 1) {
+    while (j < ds.size() && ds[j].first == ds[i].first) ++j;
+    c->dof_owner_sub[ds[i].first] = ds[i].second;
+    c->dof_nsh[ds[i].first] = j - i;
+    if (j - i > 1) {
+      sh.clear();
+      for (size_t q = i; q < j; ++q) sh.push_back(ds[q].second);
       auto it = emap.find(sh);
       int e;
-      if (it == emap.end()) { e = ekeys.size(); emap[sh] = e; ekeys.push_back(sh); edofs.push_back({}); }
+      if (it == emap.end()) { e = ekeys.size(); emap.emplace(sh, e); ekeys.push_back(sh); edofs.push_back({}); }
       else e = it->second;
       edofs[e].push_back(ds[i].first);
     }
     i = j;
   }
+  fine_time("entity classes", tf);
   // global entities ordered by their smallest DOF
   std::vector<int> order(ekeys.size());
   std::iota(order.begin(), order.end(), 0);
@@ -295,8 +359,10 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t 
       if (c->sub_lid[s] >= 0) c->subs[c->sub_lid[s]].ents.push_back(c->ents.size());
     c->ents.push_back(std::move(E));
   }
-  // per-subdomain orderings (local subdomains)
-  for (int i = 0; i < N; ++i) {
+  fine_time("entities", tf);
+  // per-subdomain orderings (local subdomains; threads over subdomains, each writes only its own)
+  parallel_for(N, [&](int64_t i0, int64_t i1) {
+  for (int64_t i = i0; i < i1; ++i) {
     Sub &S = c->subs[i];
     const int gi = c->sub_gid[i];
     std::sort(S.ents.begin(), S.ents.end());
@@ -318,6 +384,7 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t 
     S.nD = S.nI + S.nP;
     S.n = S.nD + S.nG;
   }
+  }, 16);
 }
 
 // ------------------------------------------------------------------ face geometry (host)

@@ -1,4 +1,7 @@
 #pragma once
+#include <algorithm>
+#include <exception>
+#include <thread>
 #include "internal.h"
 
 namespace vb {
@@ -31,6 +34,24 @@ inline void dbg(vb_ctx *c, const char *what) {
     VB_CHECK_LAUNCH();                                                                          \
     dbg(c, __FILE__ ":" VB_XSTR(__LINE__));                                                     \
   } while (0)
+
+// host thread pool for the per-cell / per-subdomain setup passes: f(begin, end) on contiguous
+// chunks of [0, n); an exception thrown in any chunk is rethrown on the caller's thread
+template <class F>
+void parallel_for(int64_t n, F f, int64_t min_chunk = 2048) {
+  static const int env_threads = getenv("VB_HOST_THREADS") ? atoi(getenv("VB_HOST_THREADS")) : 0;
+  int T = (int)std::min<int64_t>(env_threads > 0 ? env_threads : std::max(1u, std::thread::hardware_concurrency()), 32);
+  T = (int)std::min<int64_t>(T, (n + min_chunk - 1) / min_chunk);
+  if (T <= 1) { if (n > 0) f((int64_t)0, n); return; }
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(T);
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      try { f(n * t / T, n * (t + 1) / T); } catch (...) { err[t] = std::current_exception(); }
+    });
+  for (auto &x : th) x.join();
+  for (auto &e : err) if (e) std::rethrow_exception(e);
+}
 
 void gauss_legendre01(int n, double *x, double *w);
 void gauss_lobatto01(int npts, double *x, double *w);
