@@ -337,6 +337,60 @@ __global__ void dot_ztail_kernel(const double *__restrict__ r, double *z, const 
   block_reduce_last(v, part, ticket, dst);
 }
 
+// one rank (no cross-rank copies): chunk_sum_b0 and gather_src_dot in one pass.  Every copy of an x
+// coordinate is formed as chunk_sum_b0 forms it (the P chunk partials in order, then + b~0 p0_i on
+// the primal coordinates: bcoef / bsub expand b~0 and the subdomain over the local Gamma positions)
+// and the copies are summed as gather_src sums them, so q is bitwise the two-kernel q; the p0 rows
+// q0_i = b~0 . u_Pi^(i) by one warp per subdomain as in chunk_sum_b0.  p.q -> dst (its partials in
+// another order than gather_src_dot's).
+__global__ void chunk_gather_dot_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ idx,
+                                        const double *__restrict__ part, int64_t stride, int P,
+                                        const double *__restrict__ bcoef, const int *__restrict__ bsub,
+                                        const double *__restrict__ p, int64_t p0off, int64_t n, double *q,
+                                        const SubDev *__restrict__ subs, int N, const double *__restrict__ b0T,
+                                        const int64_t *__restrict__ loc2x, double *dpart, unsigned *ticket,
+                                        double *dst) {
+  pdl_prologue();
+  double acc = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = blockIdx.x * nw + warp; i < N; i += gridDim.x * nw) {
+    const SubDev S = subs[i];
+    double a = 0.0;
+    for (int t = lane; t < S.npi; t += 32) a += b0T[S.off_Pi + t] * p[loc2x[S.off_G + S.nd + t]];
+    a = warp_sum(a);
+    if (lane == 0) {
+      q[p0off + i] = a;
+      acc += p[p0off + i] * a;
+    }
+  }
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int64_t k = ptr[g]; k < ptr[g + 1]; ++k) {
+      const int64_t j = idx[k];
+      double t = 0.0;
+      for (int c = 0; c < P; ++c) t += part[c * stride + j];
+      const int sb = bsub[j];
+      if (sb >= 0) t += bcoef[j] * p[p0off + sb];
+      v += t;
+    }
+    q[g] = v;
+    acc += p[g] * v;
+  }
+  block_reduce_last(acc, dpart, ticket, dst);
+}
+
+// bcoef / bsub of chunk_gather_dot_kernel: per local Gamma position, b~0 and the subdomain on the
+// primal coordinates, 0 / -1 on the dual ones
+__global__ void b0_expand_kernel(const SubDev *__restrict__ subs, const double *__restrict__ b0T, double *bcoef,
+                                 int *bsub) {
+  const SubDev S = subs[blockIdx.x];
+  for (int j = threadIdx.x; j < S.nG; j += blockDim.x) {
+    const bool prim = j >= S.nd;
+    bcoef[S.off_G + j] = prim ? b0T[S.off_Pi + (j - S.nd)] : 0.0;
+    bsub[S.off_G + j] = prim ? (int)blockIdx.x : -1;
+  }
+}
+
 // x += alpha p, r -= alpha q (alpha = rz / pq), fused with the partial of r.r -> dst
 // p0 block of the condensed rhs: the compatibility sum_i g0_i = 0 must hold up to
 // rounding (checked on the host against acc[1] = sum over all pressure DOFs of |c_j g_pj|, the
@@ -509,6 +563,29 @@ __global__ void __launch_bounds__(128) coarse_ext_kernel(const SubDev *__restric
   }
   for (; a < S.npi; ++a) a0 += F[j + (int64_t)a * S.nd] * us[a];
   wc[S.off_Dv + j] = (a0 + a1) + (a2 + a3);
+}
+
+// one rank (no cross-rank copies): local2 and the entity sum in one pass -- z_e[i] = sum over the
+// sharer slots q (EntitySum order) of (sum over the P chunks of y[off_q + i]) + wc[off_q + i], the
+// same additions in the same order as local2_kernel followed by entity_sum_kernel (bitwise equal)
+__global__ void local2_entity_sum_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ off,
+                                         const int64_t *__restrict__ out_off, const int *__restrict__ len,
+                                         const double *__restrict__ part, int64_t part_stride, int P,
+                                         const double *__restrict__ wc, double *out) {
+  pdl_prologue();
+  const int e = blockIdx.x;
+  const int n = len[e];
+  const int64_t q0 = ptr[e], q1 = ptr[e + 1];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double v = 0.0;
+    for (int64_t q = q0; q < q1; ++q) {
+      const int64_t j = off[q] + i;
+      double t = 0.0;
+      for (int c = 0; c < P; ++c) t += part[c * part_stride + j];
+      v += t + wc[j];
+    }
+    out[out_off[e] + i] = v;
+  }
 }
 
 // t_i = sum_chunks y_i + DPhi_i u_Pi^(i) = D (S_DD^-1 D^T r_i + Phi_i u_Pi^(i)), the scaled
@@ -1003,6 +1080,8 @@ struct SolveState {
   DBuf<double> sx;                   // [s (len_G) | received copies]
   DBuf<double> cbuf, cgath;          // coarse pieces (local), gathered (nranks x cmax)
   DBuf<double> ucp, ucg;             // distributed coarse: this rank's partial u_c; gathered (R x N_c)
+  DBuf<double> bcoef;                // one rank: b~0 expanded over the local Gamma positions (chunk_gather_dot)
+  DBuf<int> bsub;
   // f1 coarse dissection: GEMV passes over the local packed [[E, .], [F^T, 0]] (pass 1: all tile
   // rows, x = [g_I; 0]; pass 2: the S tile rows, x = [0; x_S]), root rhs / solution
   DBuf<GemvWork> w_cd1, w_cd2;
@@ -1193,6 +1272,15 @@ static void apply_S(vb_ctx *c, SolveState *st, bool with_pq = false) {   // q = 
   tick(c, st, 0, false);
   int maxnG = 1;
   for (auto &S : c->h_sub) maxnG = std::max(maxnG, S.nG);
+  if (with_pq && c->nranks == 1 && st->bsub.n && !c->debug) {   // one pass: q, its p0 rows and p.q
+    const int64_t nxp1 = c->n_delta_glob + c->NPi;
+    launch_pdl(st, chunk_gather_dot_kernel, dim3(DOT_BLOCKS), dim3(256), 0, s, st->xptr.p, st->xidx.p, c->w_part.p,
+               c->len_G, c->P_op, st->bcoef.p, st->bsub.p, c->w_p.p, nxp1, nxp1, c->w_q.p, c->d_sub.p, c->N,
+               c->d_b0T.p, c->d_loc2x.p, c->w_dots.p, st->ticket.p, c->w_scal.p + 1);
+    tick(c, st, 3, false);
+    VB_STAGE();
+    return;
+  }
   // peer stores only where a collective (the p.q sum) separates this receive from the next write
   const bool p2p = with_pq && st->XS.p2p;
   launch_pdl(st, chunk_sum_b0_kernel, dim3((maxnG + 255) / 256, c->N), dim3(256), 0, s, c->d_sub.p, c->w_part.p, c->len_G, c->P_op,
@@ -1308,15 +1396,21 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   VB_CUDA(cudaEventRecord(st->ev_join, s2));
   VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
   trace_norm(c, "uc", c->w_uc.p, c->Nc, true);
-  launch_after_event(st, local2_kernel, dim3(grid_for(c->len_Dv)), dim3(256), 0, s, c->w_locY.p, c->len_Dv, c->P_loc,
-                     c->w_locC.p, c->len_Dv, c->w_locD.p, p2p ? st->XE.p2p_ptr.p : nullptr,
-                     p2p ? st->XE.p2p_dst.p : nullptr);
-  trace_norm(c, "t", c->w_locD.p, c->len_Dv, false);
-  if (p2p)
-    c->comm->barrier(s);                                                  // C1 (peer stores done)
-  else
-    run_slot_exchange(c, st->XE, c->w_locD.p, c->w_locD.p + c->len_Dv);  // C1 (cross-rank products)
-  run_entity_sum(c, st->ESE, c->w_locD.p, c->w_z.p);
+  if (c->nranks == 1 && st->ESE.n && !c->debug) {
+    launch_after_event(st, local2_entity_sum_kernel, dim3(st->ESE.n), dim3(st->ESE.maxlen > 64 ? 256 : 64), 0, s,
+                       st->ESE.ptr.p, st->ESE.off.p, st->ESE.out_off.p, st->ESE.len.p, c->w_locY.p, c->len_Dv,
+                       c->P_loc, c->w_locC.p, c->w_z.p);
+  } else {
+    launch_after_event(st, local2_kernel, dim3(grid_for(c->len_Dv)), dim3(256), 0, s, c->w_locY.p, c->len_Dv, c->P_loc,
+                       c->w_locC.p, c->len_Dv, c->w_locD.p, p2p ? st->XE.p2p_ptr.p : nullptr,
+                       p2p ? st->XE.p2p_dst.p : nullptr);
+    trace_norm(c, "t", c->w_locD.p, c->len_Dv, false);
+    if (p2p)
+      c->comm->barrier(s);                                                  // C1 (peer stores done)
+    else
+      run_slot_exchange(c, st->XE, c->w_locD.p, c->w_locD.p + c->len_Dv);  // C1 (cross-rank products)
+    run_entity_sum(c, st->ESE, c->w_locD.p, c->w_z.p);
+  }
   trace_norm(c, "zdual", c->w_z.p, c->n_delta_glob, false);
   if (fill_tail) dev_gather(c->w_uc.p, st->zmap.p, c->NPi + c->N, c->w_z.p + c->n_delta_glob, s);
   tick(c, st, 4, false);
@@ -1511,6 +1605,12 @@ void prepare_solve(vb_ctx *c) {
     }
     // (build_csr keeps the generation order within each row)
     build_csr(c->n_delta_glob + c->NPi, pr, st->xptr, st->xidx, s);
+    if (c->nranks == 1 && c->len_G > 0) {   // chunk_gather_dot_kernel's b~0 expansion
+      st->bcoef.alloc(c->len_G);
+      st->bsub.alloc(c->len_G);
+      b0_expand_kernel<<<c->N, 256, 0, s>>>(c->d_sub.p, c->d_b0T.p, st->bcoef.p, st->bsub.p);
+      VB_CHECK_LAUNCH();
+    }
   }
   // ---------------- B7 (extension): per-slot scaled products (in w_locD, subdomain-major) and their
   // sums over all sharers
