@@ -1,5 +1,6 @@
-// Batched dense FP64 kernels: grouped DMMA GEMM (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4, the
-// FP64 tensor path of sm_100a; tcgen05 has no f64 kind), blocked partial LDL^T,
+// Batched dense FP64 kernels: grouped DMMA GEMM (gemm_dmma.cuh: mma.sync.m16n8k16.f64 -> SASS
+// DMMA.8x8x4, the FP64 tensor path of sm_100a; tcgen05 has no f64 kind; per-kernel SASS
+// counts in profiles/r02_sass_summary.txt), blocked partial LDL^T,
 // triangular inverse, packing.  Used by the factor stage.
 #include <algorithm>
 #include <functional>
