@@ -39,9 +39,9 @@ static double now_s() {
 namespace vb {
 
 // ------------------------------------------------------------------ layout before the ranks
-void layout_phase_a(vb_ctx *c) {
+void layout_phase_a(vb_ctx *c, cudaStream_t s_upload) {
   const int N = c->N;
-  cudaStream_t s = c->stream;
+  cudaStream_t s = s_upload ? s_upload : c->stream;
   c->h_sub.assign(N, SubDev{});
   std::vector<int> sub_cells;
   std::vector<double> lvol(N);
@@ -464,11 +464,28 @@ vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n
     double t0 = now_s();
     common_setup(c, mesh, cell_subdomain, n_subdomains, subdomain_rank, cons, cell_viscosity, dist);
     double ts = now_s();
-    element_matrices_device(c);
-    VB_CUDA(cudaStreamSynchronize(c->stream));
-    setup_time("element matrices K9 (device)", ts);
-    layout_phase_a(c);
-    setup_time("layout", ts);
+    // one rank, plain allocator: the element kernel (K9) runs while the host builds the layout,
+    // whose uploads go to a second stream (pageable copies on the K9 stream would wait for it)
+    const bool overlap = c->nranks == 1 && !g_use_pool;
+    element_matrices_device(c, !overlap);
+    if (!overlap) setup_time("element matrices K9 (device)", ts);
+    cudaStream_t ss = nullptr;
+    if (overlap) VB_CUDA(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+    try {
+      layout_phase_a(c, ss);
+    } catch (...) {
+      if (ss) { cudaStreamSynchronize(c->stream); cudaStreamDestroy(ss); }
+      throw;
+    }
+    if (overlap) {
+      VB_CUDA(cudaStreamSynchronize(ss));
+      VB_CUDA(cudaStreamDestroy(ss));
+      VB_CUDA(cudaStreamSynchronize(c->stream));
+      c->w_k9.release();
+      setup_time("K9 (device) || layout (host)", ts);
+    } else {
+      setup_time("layout", ts);
+    }
     c->t_setup = now_s() - t0;
     c->state = 1;
   } catch (const Error &e) {

@@ -289,6 +289,7 @@ struct vb_ctx {
   void *solve_state = nullptr;
   int debug = 0;
   vb::DBuf<double> w_hostio;
+  vb::DBuf<double> w_k9;             // K9 scratch while the element kernel overlaps the host layout (vb_setup)
   int max_npi = 0, geo_stride = 0;
   std::vector<double> cellgeo;       // host copy of d_cellgeo
   vb::DBuf<double> d_K;              // subdomain dense matrices

@@ -72,11 +72,11 @@ CoarsePlan plan_coarse_dissection(const vb_ctx *c);
 
 // device-side stages (defined in the .cu files)
 void cell_geometry_device(vb_ctx *c);                    // vem.cu
-void layout_phase_a(vb_ctx *c);                          // abi.cu
+void layout_phase_a(vb_ctx *c, cudaStream_t s_upload = nullptr);   // abi.cu (uploads on s_upload if given)
 void build_transformed_maps(vb_ctx *c);                  // abi.cu (after the entity ranks)
 void prepare_solve(vb_ctx *c);                           // solve.cu
 void destroy_solve_state(vb_ctx *c);                     // solve.cu
-void element_matrices_device(vb_ctx *c);                 // vem.cu  (K9)
+void element_matrices_device(vb_ctx *c, bool wait = true);   // vem.cu (K9; wait = false: c->w_k9 keeps the scratch)
 void build_rhs_device(vb_ctx *c, const vb_problem *p, double *rhs);   // vem.cu
 void factor_device(vb_ctx *c);                           // factor.cu
 void adaptive_enrich(vb_ctx *c, double tau, const DBuf<double> &sidebuf);   // adaptive.cu (A6)

@@ -1446,6 +1446,7 @@ void prepare_solve(vb_ctx *c) {
   st->phit_split = std::max(4, std::min(32, (2048 + c->N - 1) / std::max(c->N, 1)));
   if (getenv("VB_P_OP")) c->P_op = std::max(1, atoi(getenv("VB_P_OP")));
   if (getenv("VB_P_LOC")) c->P_loc = std::max(1, atoi(getenv("VB_P_LOC")));
+  if (getenv("VB_P_C")) c->P_c = std::max(1, atoi(getenv("VB_P_C")));   // coarse GEMV chunks (experiment knob)
   cudaStream_t s = c->stream;
   const int N = c->N;
   const int64_t nx = c->nx;

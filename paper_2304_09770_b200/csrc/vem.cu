@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
     for (int i = 0; i < nv; ++i) Bout[(int64_t)a * nv + i] = g.vol * DIV(a * nv + i);
 }
 
-void element_matrices_device(vb_ctx *c) {
+void element_matrices_device(vb_ctx *c, bool wait) {
   cudaStream_t s = c->stream;
   const int nvm = c->nv_max;
   const int S3 = 3 * (c->k == 2 ? 10 : (c->k == 3 ? 20 : 35));
@@ -599,7 +599,7 @@ void element_matrices_device(vb_ctx *c) {
   const double budget = std::min(24e9, fr / 3.0);
   int64_t NE = std::max<int64_t>(128, std::min<int64_t>(c->nKl, (int64_t)(budget / 8 / per)));
   NE = (NE + 127) / 128 * 128;
-  DBuf<double> scratch;
+  DBuf<double> &scratch = c->w_k9;
   scratch.alloc((size_t)per * NE);
   // threads per block: one cell per thread, so the block size only sets how evenly the cells
   // spread over the 148 SMs (VB_K9_BLOCK: experiment knob)
@@ -616,7 +616,10 @@ void element_matrices_device(vb_ctx *c) {
 #undef VB_K9
     VB_STAGE();
   }
-  VB_CUDA(cudaStreamSynchronize(s));
+  if (wait) {
+    VB_CUDA(cudaStreamSynchronize(s));
+    scratch.release();
+  }
 }
 
 // ------------------------------------------------------------------ problem data (BASELINE configs)
