@@ -113,7 +113,7 @@ template <int K>
 __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict__ topo, const double *__restrict__ xyz,
                                                           const double *__restrict__ nu, int64_t K0, int64_t nE,
                                                           int nvmax, int nfmax, double *scratch, int64_t NE, double *elA,
-                                                          double *elB, double *P0out) {
+                                                          double *elB, double *P0out, int stop) {
   using Ar = Arena<K>;
   constexpr int D1 = Ar::D1, Dk = Ar::Dk, Dk1 = Ar::Dk1, D2m = Ar::D2m, q2k = Ar::q2k, q2k1 = Ar::q2k1;
   constexpr int nm = Ar::nm, NLM = Ar::NLM, S3 = Ar::S3;
@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
       out(row0 + L.fl2e(g, f, c, l)) += s * v;
     }
   };
+  if (stop == 1) return;   // VB_K9_STOP: stage-time experiment
   // ================= volume Gram matrices, from the cell moments int m_e of degree <= 2k + 2 (one
   // accumulator per distinct monomial, in registers/local memory, instead of one read-modify-write
   // of the global scratch per Gram entry per quadrature point):
@@ -349,6 +350,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
     });
     lu_solve(TT, ns, M2, nv);
   }
+  if (stop == 2) return;   // VB_K9_STOP: stage-time experiment
   // ================= (3) Pi^nabla_{k,K} per component
   for (int c = 0; c < 3; ++c) {
     const int64_t r0 = (int64_t)c * Dk * nv;
@@ -377,6 +379,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
     SM pin{PIN.p + r0 * NE, NE};
     lu_solve(WK, Dk, pin, nv);
   }
+  if (stop == 3) return;   // VB_K9_STOP: stage-time experiment
   // ================= (4) moments against [P_k]^3: grad P_{k+1} (+) x^[P_{k-1}]^3, super-enhancement
   {
     for (int i = 0; i < S3 * S3; ++i) TT(i) = 0.0;
@@ -452,6 +455,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
     lu_solve(WK, Dk, p0, nv);
   }
   for (int i = 0; i < S3 * nv; ++i) P0out[cell * (int64_t)S3 * nvmax + i] = P0(i);
+  if (stop == 5) return;   // VB_K9_STOP: stage-time experiment
   // ================= (6) Pi^0_{k-1} grad v
   for (int c = 0; c < 3; ++c)
     for (int d = 0; d < 3; ++d) {
@@ -494,6 +498,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
     }
     return nuK * v;
   };
+  if (stop == 6) return;   // VB_K9_STOP: stage-time experiment
   // ================= (7) DOFs of the polynomial basis {m_g e_c}: DP (nv x 3Dk)
   for (int i = 0; i < nv * S3; ++i) DP(i) = 0.0;
   for (int lv = 0; lv < g.nv; ++lv) {
@@ -559,6 +564,7 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
       for (int b = 0; b < S3; ++b) v += Q(a * S3 + b) * PIN((int64_t)b * nv + i);
       QP((int64_t)a * nv + i) = v;
     }
+  if (stop == 8) return;   // VB_K9_STOP: stage-time experiment
   // ================= (9) A = A_cons + (I - Pihat)^T D (I - Pihat)  (Eq.(discreteA))
   double *Aout = elA + cell * (int64_t)nvmax * nvmax;
   for (int i = 0; i < nv; ++i)
@@ -603,13 +609,14 @@ void element_matrices_device(vb_ctx *c, bool wait) {
   scratch.alloc((size_t)per * NE);
   // threads per block: one cell per thread, so the block size only sets how evenly the cells
   // spread over the 148 SMs (VB_K9_BLOCK: experiment knob)
+  static const int k9_stop = getenv("VB_K9_STOP") ? atoi(getenv("VB_K9_STOP")) : 0;   // experiment knob
   static const int k9_block = getenv("VB_K9_BLOCK") ? std::max(32, std::min(128, atoi(getenv("VB_K9_BLOCK")))) : 64;
   for (int64_t K0 = 0; K0 < c->nKl; K0 += NE) {
     const int64_t n = std::min<int64_t>(NE, c->nKl - K0);
     const int blocks = (int)((n + k9_block - 1) / k9_block);
 #define VB_K9(KK)                                                                                           \
   vem_element_kernel<KK><<<blocks, k9_block, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, K0, n, nvm, nfm, scratch.p, NE, \
-                                                c->d_elA.p, c->d_elB.p, c->d_P0.p)
+                                                c->d_elA.p, c->d_elB.p, c->d_P0.p, k9_stop)
     if (c->k == 2) VB_K9(2);
     else if (c->k == 3) VB_K9(3);
     else VB_K9(4);
