@@ -466,7 +466,10 @@ vb_status vb_setup(const vb_mesh *mesh, const int32_t *cell_subdomain, int32_t n
     double ts = now_s();
     // one rank, plain allocator: the element kernel (K9) runs while the host builds the layout,
     // whose uploads go to a second stream (pageable copies on the K9 stream would wait for it)
-    const bool overlap = c->nranks == 1 && !g_use_pool && !(getenv("VB_NO_SETUP_OVERLAP") && atoi(getenv("VB_NO_SETUP_OVERLAP")));
+    // (not with VB_POISON: its fill of each new allocation is queued on the K9 stream and would land
+    // after the second stream's upload into it)
+    const bool overlap = c->nranks == 1 && !g_use_pool && !g_poison &&
+                         !(getenv("VB_NO_SETUP_OVERLAP") && atoi(getenv("VB_NO_SETUP_OVERLAP")));
     element_matrices_device(c, !overlap);
     if (!overlap) setup_time("element matrices K9 (device)", ts);
     cudaStream_t ss = nullptr;

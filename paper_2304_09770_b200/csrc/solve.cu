@@ -1272,7 +1272,7 @@ static void apply_S(vb_ctx *c, SolveState *st, bool with_pq = false) {   // q = 
   tick(c, st, 0, false);
   int maxnG = 1;
   for (auto &S : c->h_sub) maxnG = std::max(maxnG, S.nG);
-  if (with_pq && c->nranks == 1 && st->bsub.n && !c->debug) {   // one pass: q, its p0 rows and p.q
+  if (with_pq && c->nranks == 1 && st->bsub.n && !c->debug && c->P_op <= 8) {   // one pass: q, p0 rows, p.q
     const int64_t nxp1 = c->n_delta_glob + c->NPi;
     launch_pdl(st, chunk_gather_dot_kernel, dim3(DOT_BLOCKS), dim3(256), 0, s, st->xptr.p, st->xidx.p, c->w_part.p,
                c->len_G, c->P_op, st->bcoef.p, st->bsub.p, c->w_p.p, nxp1, nxp1, c->w_q.p, c->d_sub.p, c->N,
@@ -1396,7 +1396,9 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   VB_CUDA(cudaEventRecord(st->ev_join, s2));
   VB_CUDA(cudaStreamWaitEvent(s, st->ev_join, 0));
   trace_norm(c, "uc", c->w_uc.p, c->Nc, true);
-  if (c->nranks == 1 && st->ESE.n && !c->debug) {
+  // (the fused kernel sums the P chunks serially per output: kept for few chunks, e.g. P = 4 at 512
+  // subdomains; at P = 32 (64 large subdomains, config 3) the two-kernel path is faster)
+  if (c->nranks == 1 && st->ESE.n && !c->debug && c->P_loc <= 8) {
     launch_after_event(st, local2_entity_sum_kernel, dim3(st->ESE.n), dim3(st->ESE.maxlen > 64 ? 256 : 64), 0, s,
                        st->ESE.ptr.p, st->ESE.off.p, st->ESE.out_off.p, st->ESE.len.p, c->w_locY.p, c->len_Dv,
                        c->P_loc, c->w_locC.p, c->w_z.p);
