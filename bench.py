@@ -175,7 +175,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true", help="skip the per-kernel CUDA events")
     ap.add_argument("--coarse-dissection", type=int, default=-1, choices=[-1, 0, 1],
-                    help="coarse problem by rank-level dissection (1), dense replicated (0), auto (-1: on for N > 1)")
+                    help="coarse problem by dissection (1), dense replicated (0), auto (-1)")
+    ap.add_argument("--coarse-blocks", type=int, default=-1,
+                    help="parts of the coarse dissection on one GPU (blocks of subdomains; -1 auto)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -214,6 +216,7 @@ def main():
     ctx = vb.context_for(prob, stream=stream, **dist_kw)
     t_setup = time.perf_counter() - t0
     ctx.set_option("coarse_dissection", args.coarse_dissection)
+    ctx.set_option("coarse_blocks", args.coarse_blocks)
     t0 = time.perf_counter()
     ctx.factor()
     t_factor = time.perf_counter() - t0
@@ -346,7 +349,7 @@ def main():
                                   " of 4^3 cells (32^3 cells per GPU)" if args.config == "c5" else "")),
                    "n_dofs": ndofs, "iterations": it, "kappa": rep["kappa"], "rel_residual": rep["rel_residual"],
                    "n_primal": st["n_primal"], "n_coarse": st["n_coarse"], "rtol": 1e-10,
-                   "coarse": ("rank-level dissection: root %d, local %d" % (st["n_coarse_root"], st["n_coarse_local"])
+                   "coarse": ("dissection: root %d, local %d" % (st["n_coarse_root"], st["n_coarse_local"])
                               if st["n_coarse_root"] else "dense replicated inverse"),
                    "t_setup_s": t_setup, "t_factor_s": t_factor,
                    "parallelism": "subdomains on 1 GPU" if ws == 1 else

@@ -182,14 +182,19 @@ vb_status vb_pcg_solve(vb_ctx *ctx, const double *rhs_dev, double *x_dev, double
  *                   same value); VB_ESTATE after vb_factor, VB_EINVAL (from vb_factor) together
  *                   with the VB_POOL allocator.  Results are bit-identical to the default path.
  *   "coarse_dissection" (1 on, 0 off, -1 auto = the default: on for nranks > 1; SURVEY f1,
- *                   DESIGN.md §9): the coarse saddle problem by block elimination -- each
- *                   rank eliminates the primal DOFs of entities all of whose sharers it owns
- *                   (explicit local inverse and coupling kept packed), and only the separator
- *                   primal DOFs between rank boxes plus every p_0 form the root problem that all
- *                   ranks assemble (allgathered Schur contributions, rank order), factor and
- *                   invert (sliced over ranks).  Off: the whole N_c x N_c coarse matrix is
- *                   assembled, factored and inverted on every rank.  Same solution up to rounding.
- *                   Read by vb_factor (collective: every rank the same value); VB_ESTATE after it.
+ *                   DESIGN.md §9): the coarse saddle problem by block elimination over
+ *                   parts -- the ranks, or on one rank blocks of its subdomains -- each part's
+ *                   primal DOFs of entities all of whose sharers lie in it are eliminated by that
+ *                   part alone (explicit local inverse and coupling kept packed), and only the
+ *                   separator primal DOFs between parts plus every p_0 form the root problem that
+ *                   all ranks assemble (the parts' Schur contributions, allgathered, part order),
+ *                   factor and invert (sliced over ranks).  Off: the whole N_c x N_c coarse matrix
+ *                   is assembled, factored and inverted on every rank.  Same solution up to
+ *                   rounding.  Read by vb_factor (collective: every rank the same value); VB_ESTATE
+ *                   after it.
+ *   "coarse_blocks" (>= 1, or -1 auto = the default: the largest power of two <= 8 with at least
+ *                   16 subdomains per block): the parts of the dissection on ONE rank, by recursive
+ *                   coordinate bisection of the subdomain centroids.  Read by vb_factor.
  * VB_EINVAL on an unknown name. */
 vb_status vb_set_option(vb_ctx *ctx, const char *name, double value);
 

@@ -369,6 +369,11 @@ vb_status vb_set_option(vb_ctx *c, const char *name, double value) {
     c->opt_coarse_dis = value < 0 ? -1 : (value != 0.0);
     return VB_OK;
   }
+  if (!strcmp(name, "coarse_blocks")) {
+    if (c->state >= 2) return fail(c, Error{VB_ESTATE, "option coarse_blocks is read by vb_factor: set it before"});
+    c->opt_coarse_blocks = value < 1 ? -1 : (int)value;
+    return VB_OK;
+  }
   if (!strcmp(name, "p2p")) {
     if (c->state >= 2) return fail(c, Error{VB_ESTATE, "option p2p is read by vb_factor: set it before"});
     c->opt_p2p = value != 0.0;
@@ -443,8 +448,8 @@ vb_status vb_plan_coarse_dissection(const vb_mesh *mesh, const int32_t *cell_sub
       off += G.r;
     }
     c.NPi_g = off;
-    const CoarsePlan P = plan_coarse_dissection(&c);
-    const int64_t nI = P.Iglob.size(), nS = P.Sr[rank].size();
+    const CoarsePlan P = plan_coarse_dissection(&c, c.sub_rank, nranks);
+    const int64_t nI = P.I[rank].size(), nS = P.S[rank].size();
     const int64_t v[6] = {nI, nS, P.nsep, (int64_t)P.root.size(), (nI + 31) / 32 * 32 + nS, c.NPi_g};
     memcpy(out6, v, sizeof(v));
   } catch (const Error &e) {
@@ -675,11 +680,13 @@ vb_status vb_stats(const vb_ctx *c, int64_t *o) {
   int64_t pkG = 0, pkD = 0, ndsq = 0, ndpi = 0;
   for (auto &S : c->h_sub) { pkG += (int64_t)S.nG * (S.nG + 1) / 2; pkD += (int64_t)S.nd * (S.nd + 1) / 2; ndpi += (int64_t)S.nd * S.npi; }
   for (auto &sl : c->h_slot) ndsq += (int64_t)sl.nd * sl.nd;
+  int64_t cd_nloc = 0;
+  if (c->cdis) for (auto &d : c->cd_parts) cd_nloc += d.nloc;
   int64_t v[28] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
                    c->NPi_g, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max,
                    c->ncolors, pkG, pkD, ndsq, ndpi, (c->nranks > 1 ? (int64_t)c->d_Kcs.n : (c->cdis ? c->Nroot * (c->Nroot + 1) / 2 : c->Nc * (c->Nc + 1) / 2)), c->last_iterations, c->nK,
                    (int64_t)c->factor_flops, (int64_t)(c->factor_alloc_s * 1e6), (int64_t)(c->factor_gemm_s * 1e6),
-                   c->cdis ? c->Nroot : 0, c->cdis ? c->cd_nloc : 0};
+                   c->cdis ? c->Nroot : 0, cd_nloc};
   memcpy(o, v, sizeof(v));
   return VB_OK;
 }

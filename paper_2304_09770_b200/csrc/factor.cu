@@ -7,6 +7,8 @@
 // -gamma m m^T and projecting the pressure-velocity coupling with Pi^T = I - m c^T / vol
 // (reading A5); this gives exactly the Q_I Schur complement.
 #include <algorithm>
+#include <array>
+#include <functional>
 #include <cmath>
 #include <map>
 #include <set>
@@ -339,13 +341,17 @@ __global__ void coarse_assemble_kernel2(const int *__restrict__ color_subs, cons
   }
 }
 
-// f1 (coarse dissection): this rank's coarse matrix on [interior | pad | separator + p_0] from the
-// pieces of one colour class of its LOCAL subdomains (lmap: piece row -> local position)
+// f1 (coarse dissection): each owned part's coarse matrix on [interior | pad | separator + p_0]
+// from the pieces of one colour class of the LOCAL subdomains (lmap: piece row -> position in its
+// part's matrix at kbase, leading dimension kld)
 __global__ void coarse_assemble_local_kernel(const int *__restrict__ lsubs, const int64_t *__restrict__ lpoff,
                                              const int *__restrict__ lnpi, const int64_t *__restrict__ mapoff,
                                              const int64_t *__restrict__ lmap, const int64_t *__restrict__ p0pos,
-                                             const double *__restrict__ buf, double *K, int64_t ld) {
+                                             const double *__restrict__ buf, double *Kall,
+                                             const int64_t *__restrict__ kbase, const int *__restrict__ kld) {
   const int i = lsubs[blockIdx.y];
+  double *K = Kall + kbase[i];
+  const int64_t ld = kld[i];
   const int npi = lnpi[i];
   const double *Sc = buf + lpoff[i];
   const double *b0 = Sc + (int64_t)npi * npi;
@@ -787,122 +793,197 @@ static void coarse_inverse_pack(vb_ctx *c, DBuf<double> &Kc, int64_t ldC, int64_
   }
 }
 
-// Host part of the coarse dissection (also vb_plan_coarse_dissection, no device work): interior
-// DOFs of rank `me`, the root, every rank's root list S_r and the root-rhs sources.
-CoarsePlan plan_coarse_dissection(const vb_ctx *c) {
+// Host part of the coarse dissection (also vb_plan_coarse_dissection, no device work).  Parts: the
+// ranks (R > 1: part = subdomain_rank, this rank eliminates its own part) or, on one rank, blocks of
+// its subdomains (coarse_blocks; this rank eliminates every part).  Interior DOFs of each part, the
+// root (separator between parts, then every p_0), each part's root list S_p and the root-rhs
+// sources p * maxS + q.
+CoarsePlan plan_coarse_dissection(const vb_ctx *c, const std::vector<int> &part, int nparts) {
   CoarsePlan P;
-  const int R = c->nranks, me = c->rank, Ng = c->Ng;
+  P.nparts = nparts;
+  P.part = part;
+  const int Ng = c->Ng;
+  if (c->nranks > 1) P.owned = {c->rank};
+  else for (int p = 0; p < nparts; ++p) P.owned.push_back(p);
   const int64_t NPi = c->NPi_g, Nc = NPi + Ng;
   const int ne = c->gents.size();
-  std::vector<int> erank(ne, -1);   // the one rank of all sharers, or -1 (separator)
+  std::vector<int> epart(ne, -1);   // the one part of all sharers, or -1 (separator)
   for (int e = 0; e < ne; ++e) {
     const GEnt &E = c->gents[e];
     if (E.r <= 0 || E.sharers.empty()) continue;
-    int r0 = c->sub_rank[E.sharers[0]];
+    int p0 = part[E.sharers[0]];
     for (int g : E.sharers)
-      if (c->sub_rank[g] != r0) { r0 = -1; break; }
-    erank[e] = r0;
+      if (part[g] != p0) { p0 = -1; break; }
+    epart[e] = p0;
   }
-  std::vector<int64_t> &root = P.root, &Iglob = P.Iglob;
+  std::vector<int64_t> &root = P.root;
+  P.I.assign(nparts, {});
   for (int e = 0; e < ne; ++e) {
     const GEnt &E = c->gents[e];
     if (E.r <= 0) continue;
     for (int t = 0; t < E.r; ++t) {
-      if (erank[e] < 0) root.push_back(E.off_pi + t);
-      else if (erank[e] == me) Iglob.push_back(E.off_pi + t);
+      if (epart[e] < 0) root.push_back(E.off_pi + t);
+      else P.I[epart[e]].push_back(E.off_pi + t);
     }
   }
   std::sort(root.begin(), root.end());
-  std::sort(Iglob.begin(), Iglob.end());
+  for (auto &v : P.I) std::sort(v.begin(), v.end());
   const int64_t nsep = root.size();
   P.nsep = nsep;
   for (int g = 0; g < Ng; ++g) root.push_back(NPi + g);
   const int64_t nroot = root.size();
   std::vector<int64_t> rpos(Nc, -1);
   for (int64_t j = 0; j < nroot; ++j) rpos[root[j]] = j;
-  // every rank's root list: the separator DOFs its subdomains touch (sorted), then its p_0's
-  std::vector<std::vector<int64_t>> &Sr = P.Sr;
-  Sr.assign(R, {});
-  {
-    for (int g = 0; g < Ng; ++g) {
-      const int r = c->sub_rank[g];
-      for (int e : c->gsub_ents[g])
-        if (c->gents[e].r > 0 && erank[e] < 0)
-          for (int t = 0; t < c->gents[e].r; ++t) Sr[r].push_back(c->gents[e].off_pi + t);
-    }
-    for (int r = 0; r < R; ++r) {   // an entity is seen once per sharing subdomain of the rank
-      std::sort(Sr[r].begin(), Sr[r].end());
-      Sr[r].erase(std::unique(Sr[r].begin(), Sr[r].end()), Sr[r].end());
-    }
-    for (int g = 0; g < Ng; ++g) Sr[c->sub_rank[g]].push_back(NPi + g);
+  // every part's root list: the separator DOFs its subdomains touch (sorted), then its p_0's
+  std::vector<std::vector<int64_t>> &Sr = P.S;
+  Sr.assign(nparts, {});
+  for (int g = 0; g < Ng; ++g) {
+    const int p = part[g];
+    for (int e : c->gsub_ents[g])
+      if (c->gents[e].r > 0 && epart[e] < 0)
+        for (int t = 0; t < c->gents[e].r; ++t) Sr[p].push_back(c->gents[e].off_pi + t);
   }
+  for (int p = 0; p < nparts; ++p) {   // an entity is seen once per sharing subdomain of the part
+    std::sort(Sr[p].begin(), Sr[p].end());
+    Sr[p].erase(std::unique(Sr[p].begin(), Sr[p].end()), Sr[p].end());
+  }
+  for (int g = 0; g < Ng; ++g) Sr[part[g]].push_back(NPi + g);
   int64_t &maxS = P.maxS;
   maxS = 1;
-  for (int r = 0; r < R; ++r) maxS = std::max<int64_t>(maxS, Sr[r].size());
-  // root rhs sources: root entry j <- t_r[q] (gathered at r * maxS + q) for every S_r[q] = root[j]
+  for (int p = 0; p < nparts; ++p) maxS = std::max<int64_t>(maxS, Sr[p].size());
+  // root rhs sources: root entry j <- t_p[q] (at p * maxS + q) for every S_p[q] = root[j]
   std::vector<int64_t> &rptr = P.rptr, &ridx = P.ridx;
   rptr.assign(nroot + 1, 0);
-  for (int r = 0; r < R; ++r)
-    for (int64_t v : Sr[r]) ++rptr[rpos[v] + 1];
+  for (int p = 0; p < nparts; ++p)
+    for (int64_t v : Sr[p]) ++rptr[rpos[v] + 1];
   for (int64_t j = 0; j < nroot; ++j) rptr[j + 1] += rptr[j];
   ridx.resize(rptr[nroot]);
   {
     std::vector<int64_t> fill(rptr.begin(), rptr.end() - 1);
-    for (int r = 0; r < R; ++r)
-      for (size_t q = 0; q < Sr[r].size(); ++q) ridx[fill[rpos[Sr[r][q]]]++] = (int64_t)r * maxS + q;
+    for (int p = 0; p < nparts; ++p)
+      for (size_t q = 0; q < Sr[p].size(); ++q) ridx[fill[rpos[Sr[p][q]]]++] = (int64_t)p * maxS + q;
   }
   return P;
 }
 
-// rank-level dissection of the coarse saddle problem (solved by block
-// elimination).  The primal DOFs of an entity whose sharers all live on rank r are
-// interior to r: only r's subdomains contribute to their rows and columns, so r eliminates them
-// alone.  The other primal DOFs (the separator between rank boxes) and every p_0 (coupled globally
-// by the gauge augmentation -gamma m m^T, reading A5) form the root.  Rank r keeps E = A_II^-1 and
-// F^T = A_SI A_II^-1 = L_SI L_II^-1 (its partial LDL^T gives A_SI = L_SI D L_II^T), packed as one
-// symmetric matrix [[E, .], [F^T, 0]]; the root Schur complement sum_r (A_SS^(r) - A_SI A_II^-1
-// A_IS) - gamma m m^T is assembled on every rank from the allgathered contributions (summed in
-// rank order) and inverted like the dense coarse matrix (coarse_inverse_pack, sliced over ranks).
-// Solve: y_I = E g_I, t = F^T g_I (one GEMV); x_S = S^-1 (g_S - sum_r t_r); x_I = y_I - F x_S.
-// Velocity DOFs first in the local and the root orderings (A_II SPD; the root's pressure Schur
-// complement negative definite: the pivot test of ldl_panel).
+// Blocks of one rank's subdomains for the coarse dissection on one GPU: recursive coordinate
+// bisection of the subdomain centroids (volume-weighted cell centroids) into B parts (B a power of
+// two): split the longest extent at the median, ties by subdomain id (deterministic).
+static std::vector<int> coarse_blocks_rcb(const vb_ctx *c, int B) {
+  const int N = c->N;
+  std::vector<std::array<double, 3>> xc(N);
+  for (int i = 0; i < N; ++i) {
+    double v = 0, x[3] = {0, 0, 0};
+    for (int l : c->subs[i].cells) {
+      const double *g = &c->cellgeo[(int64_t)l * c->geo_stride];
+      v += g[0];
+      for (int d = 0; d < 3; ++d) x[d] += g[0] * g[1 + d];
+    }
+    for (int d = 0; d < 3; ++d) xc[i][d] = x[d] / v;
+  }
+  std::vector<int> part(c->Ng, 0);
+  std::function<void(std::vector<int> &, int, int)> rec = [&](std::vector<int> &ids, int p0, int nb) {
+    if (nb <= 1 || ids.size() <= 1) {
+      for (int i : ids) part[c->sub_gid[i]] = p0;
+      return;
+    }
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int i : ids)
+      for (int d = 0; d < 3; ++d) { lo[d] = std::min(lo[d], xc[i][d]); hi[d] = std::max(hi[d], xc[i][d]); }
+    int ax = 0;
+    for (int d = 1; d < 3; ++d) if (hi[d] - lo[d] > hi[ax] - lo[ax]) ax = d;
+    std::sort(ids.begin(), ids.end(), [&](int a, int b) {
+      return xc[a][ax] != xc[b][ax] ? xc[a][ax] < xc[b][ax] : a < b;
+    });
+    std::vector<int> L(ids.begin(), ids.begin() + ids.size() / 2), Rr(ids.begin() + ids.size() / 2, ids.end());
+    rec(L, p0, nb / 2);
+    rec(Rr, p0 + nb / 2, nb - nb / 2);
+  };
+  std::vector<int> all(N);
+  for (int i = 0; i < N; ++i) all[i] = i;
+  rec(all, 0, B);
+  return part;
+}
+
+// dissection of the coarse saddle problem (solved by block elimination; DESIGN.md
+// §9).  The primal DOFs of an entity whose sharers all lie in one part p are interior to p: only p's
+// subdomains contribute to their rows and columns, so p is eliminated alone.  The other primal DOFs
+// (the separator between parts) and every p_0 (coupled globally by the gauge augmentation -gamma m
+// m^T, reading A5) form the root.  Each part keeps E = A_II^-1 and F^T = A_SI A_II^-1 = L_SI L_II^-1
+// (its partial LDL^T gives A_SI = L_SI D L_II^T), packed as one symmetric matrix [[E, .], [F^T, 0]];
+// the root Schur complement sum_p (A_SS^(p) - A_SI A_II^-1 A_IS) - gamma m m^T is assembled on every
+// rank from the parts' contributions (allgathered across ranks, summed in part order) and inverted
+// like the dense coarse matrix (coarse_inverse_pack, sliced over ranks).  Solve: y_I = E g_I,
+// t = F^T g_I (one GEMV pass per part); x_S = S^-1 (g_S - sum_p t_p); x_I = y_I - F x_S.  Velocity
+// DOFs first in the local and the root orderings (A_II SPD; the root's pressure Schur complement
+// negative definite: the pivot test of ldl_panel).  Parts: ranks (R > 1) or blocks of one rank's
+// subdomains (R = 1, coarse_blocks).
 static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector<int64_t> &lpoff,
                               const std::vector<int> &gnpi, const std::vector<int64_t> &pimoff,
-                              const std::vector<int64_t> &pimap, double gam_c) {
+                              const std::vector<int64_t> &pimap, double gam_c, int blocks) {
   cudaStream_t s = c->stream;
-  const int R = c->nranks, me = c->rank, Ng = c->Ng, N = c->N;
+  const int R = c->nranks, Ng = c->Ng, N = c->N;
   const int64_t NPi = c->NPi_g, Nc = c->Nc;
-  const CoarsePlan P = plan_coarse_dissection(c);
-  const std::vector<int64_t> &root = P.root, &Iglob = P.Iglob, &rptr = P.rptr, &ridx = P.ridx;
-  const std::vector<std::vector<int64_t>> &Sr = P.Sr;
+  const int nparts = R > 1 ? R : blocks;
+  const CoarsePlan P = plan_coarse_dissection(c, R > 1 ? c->sub_rank : coarse_blocks_rcb(c, blocks), nparts);
+  const std::vector<int64_t> &root = P.root, &rptr = P.rptr, &ridx = P.ridx;
   const int64_t nsep = P.nsep, nroot = root.size(), maxS = P.maxS;
   std::vector<int64_t> rpos(Nc, -1);
   for (int64_t j = 0; j < nroot; ++j) rpos[root[j]] = j;
-  const int64_t nI = Iglob.size(), nIp = (nI + 31) / 32 * 32, nS = Sr[me].size(), nloc = nIp + nS;
-  std::vector<int64_t> lp(Nc, -1);
-  for (int64_t a = 0; a < nI; ++a) lp[Iglob[a]] = a;
-  for (int64_t q = 0; q < nS; ++q) lp[Sr[me][q]] = nIp + q;
-  // ---- local matrix on [I | pad | S] from this rank's pieces (no communication)
-  std::vector<int64_t> lmap, mapoff(N + 1, 0), p0pos(N);
-  std::vector<int> lnpi(N);
+  const int no = P.owned.size();
+  // owned parts j: sizes, matrix offsets (dense K_j / M_j: ld_j x nloc_j; W_j: ldW_j x nIp_j;
+  // packed [[E, .], [F^T, 0]] at koff_j)
+  std::vector<CdPart> D(no);
+  std::vector<int64_t> Koff(no + 1, 0), Woff(no + 1, 0), lp(Nc, -1), lpart(Nc, -1);
+  int64_t kpk = 0;
+  for (int j = 0; j < no; ++j) {
+    const int p = P.owned[j];
+    CdPart &d = D[j];
+    d.part = p;
+    d.nI = P.I[p].size();
+    d.nIp = (d.nI + 31) / 32 * 32;
+    d.nS = P.S[p].size();
+    d.nloc = d.nIp + d.nS;
+    d.koff = kpk;
+    kpk += packed_size((int)d.nloc);
+    Koff[j + 1] = Koff[j] + (int64_t)ld4((int)d.nloc) * d.nloc;
+    Woff[j + 1] = Woff[j] + (int64_t)ld4((int)std::max<int64_t>(d.nIp, 1)) * d.nIp;
+    for (int64_t a = 0; a < d.nI; ++a) { lp[P.I[p][a]] = a; lpart[P.I[p][a]] = j; }
+  }
+  // ---- local matrices on [I | pad | S] from the owned parts' pieces (no communication)
+  std::vector<int64_t> lmap, mapoff(N + 1, 0), p0pos(N), kbase(N);
+  std::vector<int> lnpi(N), kld(N);
   for (int i = 0; i < N; ++i) {
     const int g = c->sub_gid[i];
+    int j = 0;
+    while (j < no && P.owned[j] != P.part[g]) ++j;
+    VB_REQUIRE(j < no, VB_EINVAL, "internal: coarse dissection part");
+    const CdPart &d = D[j];
+    // S positions of this part (a subdomain's S DOFs are in its part's root list)
+    auto spos = [&](int64_t v) {
+      const auto &S = P.S[d.part];
+      const auto it = std::lower_bound(S.begin(), S.end(), v);
+      // the p_0's follow the sorted separator DOFs, in subdomain order (also sorted)
+      VB_REQUIRE(it != S.end() && *it == v, VB_EINVAL, "internal: coarse dissection map");
+      return d.nIp + (int64_t)(it - S.begin());
+    };
     for (int64_t q = pimoff[g]; q < pimoff[g + 1]; ++q) {
-      VB_REQUIRE(lp[pimap[q]] >= 0, VB_EINVAL, "internal: coarse dissection map");
-      lmap.push_back(lp[pimap[q]]);
+      const int64_t v = pimap[q];
+      lmap.push_back(lpart[v] == j ? lp[v] : spos(v));
     }
     mapoff[i + 1] = lmap.size();
-    p0pos[i] = lp[NPi + g];
+    p0pos[i] = spos(NPi + g);
     lnpi[i] = gnpi[g];
+    kbase[i] = Koff[j];
+    kld[i] = ld4((int)d.nloc);
   }
   if (lmap.empty()) lmap.push_back(0);
-  DBuf<int64_t> dlpoff, dmapoff, dlmap, dp0;
-  DBuf<int> dlnpi;
+  DBuf<int64_t> dlpoff, dmapoff, dlmap, dp0, dkb;
+  DBuf<int> dlnpi, dkld;
   dlpoff.upload(lpoff, s); dmapoff.upload(mapoff, s); dlmap.upload(lmap, s); dp0.upload(p0pos, s);
-  dlnpi.upload(lnpi, s);
-  const int64_t ldK = ld4((int)nloc);
+  dlnpi.upload(lnpi, s); dkb.upload(kbase, s); dkld.upload(kld, s);
   DBuf<double> K;
-  K.alloc(ldK * nloc);
+  K.alloc(std::max<int64_t>(Koff[no], 1));
   K.zero(s);
   {
     std::vector<std::vector<int>> colors(c->ncolors);
@@ -912,69 +993,94 @@ static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector
       DBuf<int> dcol;
       dcol.upload(col, s);
       coarse_assemble_local_kernel<<<dim3(8, col.size()), 256, 0, s>>>(dcol.p, dlpoff.p, dlnpi.p, dmapoff.p, dlmap.p,
-                                                                       dp0.p, pieces.p, K.p, ldK);
+                                                                       dp0.p, pieces.p, K.p, dkb.p, dkld.p);
       VB_STAGE();
       sync(c);
     }
   }
-  if (nIp > nI) {
-    unit_diag_kernel<<<1, 64, 0, s>>>(K.p, ldK, nI, nIp);
-    VB_STAGE();
-  }
+  for (int j = 0; j < no; ++j)
+    if (D[j].nIp > D[j].nI) {
+      unit_diag_kernel<<<1, 64, 0, s>>>(K.p + Koff[j], ld4((int)D[j].nloc), D[j].nI, D[j].nIp);
+      VB_STAGE();
+    }
   STAGE_T("  coarse local assembly (f1)");
-  cd_dump(c, "kloc", K.p, nloc, nloc, ldK);
-  cd_dump_i(c, "Iglob", Iglob);
-  cd_dump_i(c, "Sglob", Sr[me]);
-  cd_dump_i(c, "root", root);
   c->d_Kloc.release();
-  c->d_Kloc.alloc(std::max<int64_t>(packed_size((int)nloc), 1));
-  if (nIp > 0) {
-    c->d_info.zero(s);
-    std::vector<MatDesc> lm{MatDesc{K.p, (int)nloc, (int)ldK, (int)nIp}};
-    lm[0].npos = (int)nIp;   // A_II SPD
-    ldl_partial_batched(lm, c->d_info.p, s);
-    const std::vector<int> who{me};
-    check_info(c, 1, "coarse interior LDL^T (f1)", &who, "rank");
-    const int64_t ldW = ld4((int)nIp);
-    DBuf<double> W, dI, M;
-    W.alloc(ldW * nIp);
-    W.zero(s);
-    tri_inverse_batched({TriDesc{K.p, (int)ldK, W.p, (int)ldW, (int)nIp}}, s);
-    dI.alloc(nIp);
-    recip_diag_kernel<<<(nIp + 255) / 256, 256, 0, s>>>(K.p, ldK, nIp, dI.p);
-    VB_STAGE();
-    M.alloc(ldK * nloc);
-    M.zero(s);
-    GemmPlan plan;
-    int l0 = plan.begin_launch();
-    GemmProb p{};
-    p.A = W.p; p.lda = ldW; p.transA = 1; p.d = dI.p; p.dstride = 1;   // E = W^T D^-1 W (lower)
-    p.B = W.p; p.ldb = ldW; p.C = M.p; p.ldc = ldK;
-    p.M = p.N = p.K = nIp; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
-    p.kz_on = 8;   // W lower triangular (site bit 8)
-    plan.add(p);
-    GemmProb q{};
-    q.A = K.p + nIp; q.lda = ldK;                                      // F^T = L_SI W
-    q.B = W.p; q.ldb = ldW; q.C = M.p + nIp; q.ldc = ldK;
-    q.M = nS; q.N = nIp; q.K = nIp; q.alpha = 1.0; q.beta = 0.0;
-    plan.add(q);
-    plan.upload(s);
-    plan.run(l0, s);
-    sync(c);
-    pack_tiles_batched({PackDesc{M.p, (int)nloc, (int)ldK, c->d_Kloc.p}}, s);
-  } else {
-    c->d_Kloc.zero(s);
+  c->d_Kloc.alloc(std::max<int64_t>(kpk, 1));
+  c->d_Kloc.zero(s);
+  {
+    std::vector<MatDesc> lm;
+    std::vector<int> who;
+    std::vector<TriDesc> td;
+    for (int j = 0; j < no; ++j) {
+      if (!D[j].nIp) continue;
+      const int ldk = ld4((int)D[j].nloc);
+      MatDesc m{K.p + Koff[j], (int)D[j].nloc, ldk, (int)D[j].nIp};
+      m.npos = (int)D[j].nIp;   // A_II SPD
+      lm.push_back(m);
+      who.push_back(D[j].part);
+    }
+    if (!lm.empty()) {
+      c->d_info.zero(s);
+      ldl_partial_batched(lm, c->d_info.p, s);
+      check_info(c, (int)lm.size(), "coarse interior LDL^T (f1)", &who, "part");
+      DBuf<double> W, dI, M;
+      W.alloc(std::max<int64_t>(Woff[no], 1));
+      W.zero(s);
+      for (int j = 0; j < no; ++j)
+        if (D[j].nIp)
+          td.push_back(TriDesc{K.p + Koff[j], ld4((int)D[j].nloc), W.p + Woff[j], ld4((int)D[j].nIp), (int)D[j].nIp});
+      tri_inverse_batched(td, s);
+      std::vector<int64_t> doff(no + 1, 0);
+      for (int j = 0; j < no; ++j) doff[j + 1] = doff[j] + D[j].nIp;
+      dI.alloc(std::max<int64_t>(doff[no], 1));
+      for (int j = 0; j < no; ++j)
+        if (D[j].nIp) {
+          recip_diag_kernel<<<(int)((D[j].nIp + 255) / 256), 256, 0, s>>>(K.p + Koff[j], ld4((int)D[j].nloc),
+                                                                          (int)D[j].nIp, dI.p + doff[j]);
+          VB_STAGE();
+        }
+      M.alloc(std::max<int64_t>(Koff[no], 1));
+      M.zero(s);
+      GemmPlan plan;
+      int l0 = plan.begin_launch();
+      for (int j = 0; j < no; ++j) {
+        if (!D[j].nIp) continue;
+        const int ldk = ld4((int)D[j].nloc), ldw = ld4((int)D[j].nIp);
+        GemmProb p{};
+        p.A = W.p + Woff[j]; p.lda = ldw; p.transA = 1; p.d = dI.p + doff[j]; p.dstride = 1;   // E = W^T D^-1 W
+        p.B = W.p + Woff[j]; p.ldb = ldw; p.C = M.p + Koff[j]; p.ldc = ldk;
+        p.M = p.N = p.K = (int)D[j].nIp; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
+        p.kz_on = 8;   // W lower triangular (site bit 8)
+        plan.add(p);
+        GemmProb q{};
+        q.A = K.p + Koff[j] + D[j].nIp; q.lda = ldk;                                           // F^T = L_SI W
+        q.B = W.p + Woff[j]; q.ldb = ldw; q.C = M.p + Koff[j] + D[j].nIp; q.ldc = ldk;
+        q.M = (int)D[j].nS; q.N = (int)D[j].nIp; q.K = (int)D[j].nIp; q.alpha = 1.0; q.beta = 0.0;
+        plan.add(q);
+      }
+      plan.upload(s);
+      plan.run(l0, s);
+      sync(c);
+      std::vector<PackDesc> pk;
+      for (int j = 0; j < no; ++j)
+        if (D[j].nIp) pk.push_back(PackDesc{M.p + Koff[j], (int)D[j].nloc, ld4((int)D[j].nloc), c->d_Kloc.p + D[j].koff});
+      pack_tiles_batched(pk, s);
+    }
   }
   STAGE_T("  coarse local elimination (f1)");
-  // ---- root: allgather the Schur contributions, sum in rank order, augment, factor, invert
+  // ---- root: the parts' Schur contributions (allgathered across ranks), summed in part order,
+  // augmented, factored, inverted
   DBuf<double> piece, gath;
-  piece.alloc(maxS * maxS);
+  piece.alloc((size_t)maxS * maxS * no);
   piece.zero(s);
-  copy_sym_lower_kernel<<<(int)std::min<int64_t>((nS * nS + 255) / 256, 8192), 256, 0, s>>>(
-      K.p + nIp * (ldK + 1), ldK, nS, piece.p, maxS);
-  VB_STAGE();
+  for (int j = 0; j < no; ++j) {
+    const int64_t n = D[j].nS, ldk = ld4((int)D[j].nloc);
+    copy_sym_lower_kernel<<<(int)std::min<int64_t>((n * n + 255) / 256, 8192), 256, 0, s>>>(
+        K.p + Koff[j] + D[j].nIp * (ldk + 1), ldk, n, piece.p + (size_t)j * maxS * maxS, maxS);
+    VB_STAGE();
+  }
   K.release();
-  const double *all = piece.p;
+  const double *all = piece.p;   // part p at p * maxS^2 (R = 1: the owned parts are all parts, in order)
   if (R > 1) {
     gath.alloc((size_t)maxS * maxS * R);
     c->comm->allgather(piece.p, gath.p, maxS * maxS, s);
@@ -986,15 +1092,15 @@ static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector
   Kr.alloc(ldR * nroot);
   Kr.zero(s);
   {
-    std::vector<int64_t> rp((size_t)maxS * R, 0);
-    for (int r = 0; r < R; ++r)
-      for (size_t q = 0; q < Sr[r].size(); ++q) rp[(size_t)r * maxS + q] = rpos[Sr[r][q]];
+    std::vector<int64_t> rp((size_t)maxS * nparts, 0);
+    for (int p = 0; p < nparts; ++p)
+      for (size_t q = 0; q < P.S[p].size(); ++q) rp[(size_t)p * maxS + q] = rpos[P.S[p][q]];
     drp.upload(rp, s);
   }
-  for (int r = 0; r < R; ++r) {
-    const int64_t n = Sr[r].size();
+  for (int p = 0; p < nparts; ++p) {
+    const int64_t n = P.S[p].size();
     root_scatter_add_kernel<<<(int)std::min<int64_t>((n * n + 255) / 256, 8192), 256, 0, s>>>(
-        all + (size_t)r * maxS * maxS, maxS, n, drp.p + (size_t)r * maxS, Kr.p, ldR);
+        all + (size_t)p * maxS * maxS, maxS, n, drp.p + (size_t)p * maxS, Kr.p, ldR);
     VB_STAGE();
   }
   gvol.upload(c->gsub_vol, s);
@@ -1004,7 +1110,6 @@ static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector
   gath.release();
   STAGE_T("  coarse root assembly (f1)");
   cd_dump(c, "kroot", Kr.p, nroot, nroot, ldR);
-  cd_dump(c, "piece", piece.p, maxS, maxS, maxS);
   c->d_info.zero(s);
   std::vector<MatDesc> rm{MatDesc{Kr.p, (int)nroot, (int)ldR, (int)nroot}};
   rm[0].npos = (int)nsep;   // [separator u_Pi | p_0 (augmented)]
@@ -1012,9 +1117,11 @@ static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector
   check_info(c, 1, "coarse root LDL^T (f1)");
   coarse_inverse_pack(c, Kr, ldR, nroot);
   STAGE_T("  coarse root inverse (f1)");
-  c->Nroot = nroot; c->cd_nsep = nsep;
-  c->cd_nI = nI; c->cd_nIp = nIp; c->cd_nS = nS; c->cd_nloc = nloc; c->cd_maxS = maxS;
-  c->cd_Iglob = Iglob; c->cd_Sglob = Sr[me]; c->cd_root_glob = root;
+  c->Nroot = nroot; c->cd_nsep = nsep; c->cd_maxS = maxS; c->cd_nparts = nparts;
+  c->cd_parts = D;
+  c->cd_I.clear(); c->cd_S.clear();
+  for (int j = 0; j < no; ++j) { c->cd_I.push_back(P.I[D[j].part]); c->cd_S.push_back(P.S[D[j].part]); }
+  c->cd_root_glob = root;
   c->cd_rptr = rptr; c->cd_ridx = ridx;
 }
 
@@ -1243,7 +1350,17 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
   const int Ng = c->Ng;
   const int64_t Nc = c->NPi_g + Ng;
   c->Nc = Nc;
-  c->cdis = c->opt_coarse_dis < 0 ? c->nranks > 1 : c->opt_coarse_dis != 0;
+  // parts of the dissection on one rank: blocks of its subdomains (auto: the largest power of two
+  // <= 8 with at least 16 subdomains per block)
+  int blocks = 1;
+  if (c->nranks == 1) {
+    if (c->opt_coarse_blocks > 0) blocks = c->opt_coarse_blocks;
+    else while (blocks < 8 && 2 * blocks * 16 <= N) blocks *= 2;
+    blocks = std::max(1, std::min(blocks, N));
+  }
+  // auto: always for several ranks; on one rank for coarse problems of >= 4096 unknowns split into
+  // >= 2 blocks (c5: 1,025 -> 1,055 M DOF*it/s; small coarse problems keep the dense inverse)
+  c->cdis = c->opt_coarse_dis < 0 ? (c->nranks > 1 || (Nc >= 4096 && blocks >= 2)) : c->opt_coarse_dis != 0;
   {
     // global piece layout: rank-major, subdomains in order within a rank
     std::vector<int> gnpi(Ng, 0);
@@ -1283,7 +1400,7 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     for (int g = 0; g < Ng; ++g) volO += c->gsub_vol[g];
     const double gam_c = 1.0 / (nubar * volO);
     if (c->cdis) {
-      coarse_dissection(c, mine, lpoff, gnpi, pimoff, pimap, gam_c);
+      coarse_dissection(c, mine, lpoff, gnpi, pimoff, pimap, gam_c, blocks);
     } else {
       // C4: every rank gathers every subdomain's (S_c, b~0) and assembles/factors the same matrix
       const double *pieces = mine.p;

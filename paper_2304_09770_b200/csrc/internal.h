@@ -217,6 +217,19 @@ struct EntDev {
   int64_t off_pl;             // rank-local primal offset (x = [dual | local primal | p0])
 };
 
+// one part of the coarse dissection eliminated by this rank (factor.cu; the solve fields are set
+// by prepare_solve)
+struct CdPart {
+  int part = 0;                 // part id (rank, or block of one rank's subdomains)
+  int P1 = 0, P2 = 0;           // GEMV chunks of pass 1 (all tile rows) / pass 2 (the S tile rows)
+  int64_t nI = 0, nIp = 0, nS = 0, nloc = 0;   // interior, interior padded to 32, root list, nIp + nS
+  int64_t koff = 0;             // packed matrix offset in d_Kloc
+  int64_t p1off = 0, p2off = 0; // chunk partials of pass 1 / 2 (chunk q at + q nloc)
+  int64_t yoff = 0;             // y_I = E g_I in the Y buffer
+  int64_t moff = 0;             // gather maps (nloc each)
+  int64_t ioff = 0;             // interior global indices
+};
+
 struct KTimer {
   std::string name;
   cudaEvent_t a = nullptr, b = nullptr;
@@ -355,16 +368,20 @@ struct vb_ctx {
   vb::DBuf<double> w_rhsg, w_xg;     // global-layout free vectors (nranks > 1)
   vb::DBuf<double> d_Kcs;            // distributed coarse: this rank's tile rows of the packed inverse
   int64_t coarse_tlo = 0, coarse_thi = 0;   // ... tile rows [tlo, thi) (balanced by tile count)
-  // rank-level dissection of the coarse saddle problem (factor.cu coarse_dissection,
-  // DESIGN.md §9).  Interior = primal DOFs of entities whose sharers all live on one rank (local,
-  // eliminated by that rank alone); root = the other primal DOFs and every p_0 (replicated, sliced).
+  // dissection of the coarse saddle problem (factor.cu coarse_dissection).
+  // Parts = ranks (R > 1) or blocks of one rank's subdomains (R = 1); interior = primal DOFs of
+  // entities whose sharers all lie in one part (eliminated by that part alone); root = the other
+  // primal DOFs and every p_0 (replicated, sliced over ranks).
   int opt_coarse_dis = -1;           // vb_set_option("coarse_dissection"): -1 auto = on for nranks > 1
+  int opt_coarse_blocks = -1;        // vb_set_option("coarse_blocks"): parts on one rank (-1 auto)
   bool cdis = false;                 // the last vb_factor used it
-  int64_t Nroot = 0, cd_nsep = 0;    // root size (= cd_nsep separator velocity DOFs + Ng p_0)
-  int64_t cd_nI = 0, cd_nIp = 0, cd_nS = 0, cd_nloc = 0, cd_maxS = 0;   // local sizes (nIp = nI padded to 32)
-  std::vector<int64_t> cd_Iglob, cd_Sglob, cd_root_glob;   // -> global coarse index (u_Pi, then p_0)
-  std::vector<int64_t> cd_rptr, cd_ridx;   // root entry <- gathered t entries r * maxS + q, rank order
-  vb::DBuf<double> d_Kloc;           // packed [[A_II^-1, sym], [A_SI A_II^-1, 0]] (n_loc = nIp + nS)
+  int cd_nparts = 0;
+  int64_t Nroot = 0, cd_nsep = 0, cd_maxS = 0;   // root size (= cd_nsep separator DOFs + Ng p_0)
+  std::vector<vb::CdPart> cd_parts;  // the parts this rank eliminates
+  std::vector<std::vector<int64_t>> cd_I, cd_S;   // per owned part: interior / root list -> global coarse index
+  std::vector<int64_t> cd_root_glob;
+  std::vector<int64_t> cd_rptr, cd_ridx;   // root entry <- t entries p * maxS + q, part order
+  vb::DBuf<double> d_Kloc;           // per owned part, packed [[A_II^-1, sym], [A_SI A_II^-1, 0]] (n_loc = nIp + nS)
   double factor_flops = 0;     // DMMA GEMM flops of the last vb_factor
   double factor_gemm_s = 0;    // their kernel time (CUDA events; VB_KERNEL_TIMING=1 only, else 0)
   double factor_alloc_s = 0;   // wall time of device allocation / release inside the last vb_factor

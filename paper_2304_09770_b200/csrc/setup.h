@@ -60,15 +60,19 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t 
 void face_frame(const vb_ctx *c, int64_t f, double *area, double n[3], double t1[3], double t2[3]);
 void build_constraint_rows(vb_ctx *c, std::vector<double> &rows_out);
 
-// SURVEY f1 (factor.cu): the host plan of the rank-level coarse dissection from the global entity
-// list (gents[].r, off_pi, sharers), gsub_ents, sub_rank, NPi_g, Ng, rank and nranks
+// SURVEY f1 (factor.cu): the host plan of the coarse dissection from the global entity list
+// (gents[].r, off_pi, sharers), gsub_ents, NPi_g, Ng and a part per global subdomain (ranks, or
+// blocks of one rank's subdomains)
 struct CoarsePlan {
-  std::vector<int64_t> root, Iglob;          // global coarse indices (root: separator, then every p_0)
-  std::vector<std::vector<int64_t>> Sr;      // per rank: touched separator DOFs (sorted), then its p_0's
-  std::vector<int64_t> rptr, ridx;           // root entry <- gathered t entries r * maxS + q
+  int nparts = 1;
+  std::vector<int> part;                     // global subdomain -> part
+  std::vector<int> owned;                    // parts this rank eliminates (R > 1: its rank; R = 1: all)
+  std::vector<int64_t> root;                 // global coarse indices (separator, then every p_0)
+  std::vector<std::vector<int64_t>> I, S;    // per part: interior DOFs; touched separator DOFs, then its p_0's
+  std::vector<int64_t> rptr, ridx;           // root entry <- t entries p * maxS + q, part order
   int64_t nsep = 0, maxS = 1;
 };
-CoarsePlan plan_coarse_dissection(const vb_ctx *c);
+CoarsePlan plan_coarse_dissection(const vb_ctx *c, const std::vector<int> &part, int nparts);
 
 // device-side stages (defined in the .cu files)
 void cell_geometry_device(vb_ctx *c);                    // vem.cu

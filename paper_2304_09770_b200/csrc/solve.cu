@@ -1035,15 +1035,30 @@ __global__ void cd_root_finish_kernel(const double *__restrict__ vol, int Ng, in
   for (int64_t j = threadIdx.x; j < nroot; j += blockDim.x) uc[root[j]] = j >= nsep ? x[j] - mean : x[j];
 }
 
-// interior coarse values x_I = y_I - F x_S (F x_S: the transpose part of the second GEMV pass,
-// summed over its chunks in fixed order)
-__global__ void cd_interior_kernel(const double *__restrict__ part, int64_t stride, int P, const double *__restrict__ y,
-                                   int64_t nI, const int64_t *__restrict__ Iglob, double *uc) {
+// dissection pass 1 per owned part j (blockIdx.y): the P1 chunk partials of [[E, .], [F^T, 0]] [g_I; 0]
+// summed in fixed order, y_I = E g_I to Y, t = F^T g_I to T[j maxS ...]
+__global__ void cd_sum_parts_kernel(const CdPart *__restrict__ parts, const double *__restrict__ part1, double *Y,
+                                    double *T, int64_t maxS) {
   pdl_prologue();
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nI; a += (int64_t)gridDim.x * blockDim.x) {
+  const CdPart D = parts[blockIdx.y];
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < D.nloc; a += (int64_t)gridDim.x * blockDim.x) {
     double v = 0.0;
-    for (int c = 0; c < P; ++c) v += part[c * stride + a];
-    uc[Iglob[a]] = y[a] - v;
+    for (int q = 0; q < D.P1; ++q) v += part1[D.p1off + q * D.nloc + a];
+    if (a < D.nIp) Y[D.yoff + a] = v;
+    else T[blockIdx.y * maxS + (a - D.nIp)] = v;
+  }
+}
+
+// interior coarse values x_I = y_I - F x_S per owned part (F x_S: the transpose part of the second
+// GEMV pass, summed over its chunks in fixed order)
+__global__ void cd_interior_kernel(const CdPart *__restrict__ parts, const double *__restrict__ part2,
+                                   const double *__restrict__ Y, const int64_t *__restrict__ Iall, double *uc) {
+  pdl_prologue();
+  const CdPart D = parts[blockIdx.y];
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < D.nI; a += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int q = 0; q < D.P2; ++q) v += part2[D.p2off + q * D.nloc + a];
+    uc[Iall[D.ioff + a]] = Y[D.yoff + a] - v;
   }
 }
 
@@ -1088,8 +1103,11 @@ struct SolveState {
   int nw_cd1 = 0, nw_cd2 = 0;
   size_t sm_cd = 0;
   bool big_cd = false;
-  DBuf<int64_t> cd_map1, cd_map2, cd_Iglob, cd_root, cd_rptr, cd_ridx;
-  DBuf<double> cd_part1, cd_part2, cd_v1, cd_tg, cd_groot, cd_xroot;
+  DBuf<int64_t> cd_map1, cd_map2, cd_Iall, cd_root, cd_rptr, cd_ridx;
+  DBuf<double> cd_part1, cd_part2, cd_Y, cd_T, cd_tg, cd_groot, cd_xroot;
+  DBuf<CdPart> cd_parts;
+  int cd_no = 0;
+  int64_t cd_maxloc = 1, cd_maxI = 1;
   DBuf<double> gam2, gbuf, hbuf;     // B0: entity-major b_e; [zG | received]; DOF halo receive
   int64_t cmax = 0;
   SlotExchange XS, XE, XB, XH, XR;   // apply_S copies, extension products, B0 zG, DOF halo, rank partials
@@ -1356,12 +1374,12 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   if (c->cdis) {
     if (st->nw_cd1) {
       coarse_gemv(st->w_cd1.p, st->nw_cd1, st->sm_cd, st->big_cd);
-      launch_pdl(st, sum_chunks_kernel, dim3((c->cd_nloc + 31) / 32), dim3(256), 0, s2, st->cd_part1.p, c->cd_nloc,
-                 st->nw_cd1, c->cd_nloc, st->cd_v1.p);
+      launch_pdl(st, cd_sum_parts_kernel, dim3((unsigned)((st->cd_maxloc + 255) / 256), st->cd_no), dim3(256), 0, s2,
+                 st->cd_parts.p, st->cd_part1.p, st->cd_Y.p, st->cd_T.p, c->cd_maxS);
     }
-    const double *tg = st->cd_v1.p + c->cd_nIp;
+    const double *tg = st->cd_T.p;
     if (c->nranks > 1) {
-      c->comm->allgather(st->cd_v1.p + c->cd_nIp, st->cd_tg.p, c->cd_maxS, s2);
+      c->comm->allgather(st->cd_T.p, st->cd_tg.p, c->cd_maxS, s2);
       tg = st->cd_tg.p;
     }
     launch_pdl(st, cd_root_rhs_kernel, dim3(grid_for(c->Nroot)), dim3(256), 0, s2, st->cd_rptr.p, st->cd_ridx.p, tg,
@@ -1385,8 +1403,8 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
                st->cd_root.p, c->Nroot, c->w_uc.p);
     if (st->nw_cd2) {
       coarse_gemv(st->w_cd2.p, st->nw_cd2, st->sm_cd, st->big_cd);
-      launch_pdl(st, cd_interior_kernel, dim3(grid_for(c->cd_nI)), dim3(256), 0, s2, st->cd_part2.p, c->cd_nloc,
-                 st->nw_cd2, st->cd_v1.p, c->cd_nI, st->cd_Iglob.p, c->w_uc.p);
+      launch_pdl(st, cd_interior_kernel, dim3((unsigned)((st->cd_maxI + 255) / 256), st->cd_no), dim3(256), 0, s2,
+                 st->cd_parts.p, st->cd_part2.p, st->cd_Y.p, st->cd_Iall.p, c->w_uc.p);
     }
   } else {
     launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
@@ -1540,29 +1558,54 @@ void prepare_solve(vb_ctx *c) {
   st->big_c = st->sm_c > 200 * 1024;
   wl.clear();
   if (c->cdis) {
-    // f1 dissection: the local packed [[E, .], [F^T, 0]] of order n_loc = nIp + nS
-    const int64_t nl = c->cd_nloc, ntl = (nl + 31) / 32, tS = c->cd_nIp / 32;
-    std::vector<int64_t> m1(nl, c->Nc), m2(nl, c->Nc);
-    for (int64_t a = 0; a < c->cd_nI; ++a) m1[a] = c->cd_Iglob[a];
-    for (int64_t q = 0; q < c->cd_nS; ++q) m2[c->cd_nIp + q] = c->cd_Sglob[q];
+    // f1 dissection: per owned part the packed [[E, .], [F^T, 0]] of order n_loc = nIp + nS
+    std::vector<CdPart> D = c->cd_parts;
+    const int no = D.size();
+    int act = 0;
+    for (auto &d : D) act += d.nIp > 0;
+    const int Pper = std::max(1, c->P_c / std::max(act, 1));
+    std::vector<int64_t> m1, m2, Iall;
+    int64_t p1 = 0, p2 = 0, y = 0, maxloc = 1, maxI = 1;
+    for (int j = 0; j < no; ++j) {
+      CdPart &d = D[j];
+      const int64_t ntl = (d.nloc + 31) / 32, tS = d.nIp / 32;
+      d.P1 = d.nIp ? (int)std::min<int64_t>(ntl, Pper) : 0;
+      d.P2 = d.nIp ? (int)std::min<int64_t>(ntl - tS, Pper) : 0;
+      d.p1off = p1; p1 += (int64_t)d.P1 * d.nloc;
+      d.p2off = p2; p2 += (int64_t)d.P2 * d.nloc;
+      d.yoff = y; y += d.nIp;
+      d.moff = m1.size();
+      d.ioff = Iall.size();
+      for (int64_t a = 0; a < d.nloc; ++a) {
+        m1.push_back(a < d.nI ? c->cd_I[j][a] : c->Nc);
+        m2.push_back(a >= d.nIp ? c->cd_S[j][a - d.nIp] : c->Nc);
+      }
+      Iall.insert(Iall.end(), c->cd_I[j].begin(), c->cd_I[j].end());
+      maxloc = std::max(maxloc, d.nloc);
+      maxI = std::max(maxI, d.nI);
+    }
     st->cd_map1.upload(m1, s); st->cd_map2.upload(m2, s);
-    st->cd_Iglob.upload(c->cd_Iglob.empty() ? std::vector<int64_t>{0} : c->cd_Iglob, s);
+    st->cd_Iall.upload(Iall.empty() ? std::vector<int64_t>{0} : Iall, s);
     st->cd_root.upload(c->cd_root_glob, s);
     st->cd_rptr.upload(c->cd_rptr, s);
     st->cd_ridx.upload(c->cd_ridx.empty() ? std::vector<int64_t>{0} : c->cd_ridx, s);
-    st->cd_v1.alloc(c->cd_nIp + c->cd_maxS); st->cd_v1.zero(s);
+    st->cd_Y.alloc(std::max<int64_t>(y, 1));
+    st->cd_T.alloc((int64_t)std::max(no, 1) * c->cd_maxS); st->cd_T.zero(s);
     if (c->nranks > 1) st->cd_tg.alloc(c->cd_maxS * c->nranks);
+    st->cd_part1.alloc(std::max<int64_t>(p1, 1)); st->cd_part2.alloc(std::max<int64_t>(p2, 1));
     st->nw_cd1 = st->nw_cd2 = 0;
-    if (c->cd_nIp > 0) {
-      const int P1 = (int)std::max<int64_t>(1, std::min<int64_t>(c->P_c, ntl));
-      const int P2 = (int)std::max<int64_t>(1, std::min<int64_t>(c->P_c, ntl - tS));
-      st->cd_part1.alloc((int64_t)P1 * nl); st->cd_part2.alloc((int64_t)P2 * nl);
-      slice_work(c->d_Kloc.p, 0, st->cd_map1.p, c->w_rc.p, st->cd_part1.p, nl, 0, ntl, P1);
-      st->w_cd1.upload(wl, s); st->nw_cd1 = wl.size(); wl.clear();
-      slice_work(c->d_Kloc.p, 0, st->cd_map2.p, c->w_uc.p, st->cd_part2.p, nl, tS, ntl, P2);
-      st->w_cd2.upload(wl, s); st->nw_cd2 = wl.size(); wl.clear();
-    }
-    st->sm_cd = gemv_smem(nl, GV_WARPS_C);
+    for (int j = 0; j < no; ++j)
+      if (D[j].P1) slice_work(c->d_Kloc.p + D[j].koff, 0, st->cd_map1.p + D[j].moff, c->w_rc.p, st->cd_part1.p + D[j].p1off,
+                              D[j].nloc, 0, (D[j].nloc + 31) / 32, D[j].P1);
+    st->w_cd1.upload(wl, s); st->nw_cd1 = wl.size(); wl.clear();
+    for (int j = 0; j < no; ++j)
+      if (D[j].P2) slice_work(c->d_Kloc.p + D[j].koff, 0, st->cd_map2.p + D[j].moff, c->w_uc.p, st->cd_part2.p + D[j].p2off,
+                              D[j].nloc, D[j].nIp / 32, (D[j].nloc + 31) / 32, D[j].P2);
+    st->w_cd2.upload(wl, s); st->nw_cd2 = wl.size(); wl.clear();
+    st->cd_parts.upload(D, s);
+    st->cd_no = no; st->cd_maxloc = maxloc; st->cd_maxI = maxI;
+    c->cd_parts = D;
+    st->sm_cd = gemv_smem(maxloc, GV_WARPS_C);
     st->big_cd = st->sm_cd > 200 * 1024;
     if (!st->big_cd)
       raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS_C, false, true>, st->sm_cd);
@@ -1818,8 +1861,9 @@ void prepare_solve(vb_ctx *c) {
   }
   // (the deluxe blocks are folded into S_DD^-1 and Phi at factor time: no per-iteration D traffic)
   b += 8.0 * (c->nranks > 1 ? (double)c->d_Kcs.n : (double)packed_size(c->cdis ? c->Nroot : c->Nc));
-  if (c->cdis && c->cd_nIp > 0)   // dissection passes 1 (all of the local matrix) and 2 (its S tile rows)
-    b += 8.0 * (2.0 * packed_size(c->cd_nloc) - ptile_row_start(c->cd_nIp / 32));
+  if (c->cdis)   // dissection passes 1 (all of each part's matrix) and 2 (its S tile rows)
+    for (auto &d : c->cd_parts)
+      if (d.nIp > 0) b += 8.0 * (2.0 * packed_size((int)d.nloc) - ptile_row_start(d.nIp / 32));
   c->bytes_per_iter = b;
 }
 

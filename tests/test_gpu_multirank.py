@@ -229,7 +229,11 @@ def test_multirank_peer_stores_bitwise(name, kw, assign):
 
 
 @pytest.mark.parametrize("name,kw,grid", [
-    ("c1", dict(n=8), 1),                 # one rank: root = the p_0's only
+    ("c1", dict(n=8), 1),                 # one rank, one part: root = the p_0's only
+    ("c1", dict(n=8), "blocks8"),         # one rank, 8 blocks of 2^3 subdomains (RCB)
+    ("c2", {}, "blocks8"),                # 64 subdomains in 8 blocks
+    ("c4", dict(n=16, constraints=dict(adaptive_tau=2.0)), "blocks4"),   # adaptive rows, 4 blocks
+    ("c3", dict(n=8), "blocks2"),         # k = 3, 2 blocks
     ("c1", dict(n=8), (2, 2, 2)),         # 8 rank boxes of 2^3 subdomains (interior entities on every rank)
     ("c1", dict(n=8), "checkerboard"),    # every entity crosses ranks: no interior DOFs anywhere
     ("c1", dict(n=8), "stripes3"),        # ragged rank sizes
@@ -244,11 +248,13 @@ def test_coarse_dissection_matches_dense_coarse(name, kw, grid):
     import torch
     import paper_2304_09770_b200 as vb
     prob = make_problem(name, **kw)
-    if grid == 1:
+    if grid == 1 or str(grid).startswith("blocks"):
+        blocks = 1 if grid == 1 else int(grid[6:])
         runs = []
         for opt in (0, 1):
             ctx = vb.context_for(prob)
             ctx.set_option("coarse_dissection", opt)
+            ctx.set_option("coarse_blocks", blocks)
             ctx.factor()
             st = ctx.stats()
             rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
@@ -258,7 +264,10 @@ def test_coarse_dissection_matches_dense_coarse(name, kw, grid):
             runs.append([dict(rep=rep, x=x.cpu().numpy(), ids=ctx.dof_layout(), stats=st)])
             ctx.close()
         n_sub = int(np.prod(prob.sub_grid))
-        assert runs[1][0]["stats"]["n_coarse_root"] == n_sub          # only the p_0's
+        if blocks == 1:
+            assert runs[1][0]["stats"]["n_coarse_root"] == n_sub      # only the p_0's
+        else:
+            assert n_sub < runs[1][0]["stats"]["n_coarse_root"] < runs[1][0]["stats"]["n_coarse"]
         assert runs[0][0]["stats"]["n_coarse_root"] == 0
     else:
         if isinstance(grid, str):
