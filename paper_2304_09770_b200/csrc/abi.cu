@@ -680,11 +680,17 @@ vb_status vb_stats(const vb_ctx *c, int64_t *o) {
   int64_t pkG = 0, pkD = 0, ndsq = 0, ndpi = 0;
   for (auto &S : c->h_sub) { pkG += (int64_t)S.nG * (S.nG + 1) / 2; pkD += (int64_t)S.nd * (S.nd + 1) / 2; ndpi += (int64_t)S.nd * S.npi; }
   for (auto &sl : c->h_slot) ndsq += (int64_t)sl.nd * sl.nd;
-  int64_t cd_nloc = 0;
-  if (c->cdis) for (auto &d : c->cd_parts) cd_nloc += d.nloc;
+  // coarse doubles streamed in the timed coarse window (the B6 kernel-time category): the inverse's
+  // slice (or all of it), plus with the dissection the parts' packed matrices of pass 1
+  int64_t cd_nloc = 0, pk_coarse = c->nranks > 1 ? (int64_t)c->d_Kcs.n : (int64_t)packed_size((int)(c->cdis ? c->Nroot : c->Nc));
+  if (c->cdis)
+    for (auto &d : c->cd_parts) {
+      cd_nloc += d.nloc;
+      if (d.nIp > 0) pk_coarse += packed_size((int)d.nloc);
+    }
   int64_t v[28] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
                    c->NPi_g, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max,
-                   c->ncolors, pkG, pkD, ndsq, ndpi, (c->nranks > 1 ? (int64_t)c->d_Kcs.n : (c->cdis ? c->Nroot * (c->Nroot + 1) / 2 : c->Nc * (c->Nc + 1) / 2)), c->last_iterations, c->nK,
+                   c->ncolors, pkG, pkD, ndsq, ndpi, pk_coarse, c->last_iterations, c->nK,
                    (int64_t)c->factor_flops, (int64_t)(c->factor_alloc_s * 1e6), (int64_t)(c->factor_gemm_s * 1e6),
                    c->cdis ? c->Nroot : 0, cd_nloc};
   memcpy(o, v, sizeof(v));
