@@ -564,7 +564,13 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
       for (int b = 0; b < S3; ++b) v += Q(a * S3 + b) * PIN((int64_t)b * nv + i);
       QP((int64_t)a * nv + i) = v;
     }
-  if (stop == 8) return;   // VB_K9_STOP: stage-time experiment
+  // ================= (10) B^K = |K| DIVc (dual pressure basis, P:130-137)
+  double *Bout = elB + cell * (int64_t)D1 * nvmax;
+  for (int a = 0; a < D1; ++a)
+    for (int i = 0; i < nv; ++i) Bout[(int64_t)a * nv + i] = g.vol * DIV(a * nv + i);
+  // (9) here when stop == -1, else in vem_assemble_A_kernel (a thread per (cell, row)) or not at all
+  // (VB_K9_STOP stage-time experiment)
+  if (stop != -1) return;
   // ================= (9) A = A_cons + (I - Pihat)^T D (I - Pihat)  (Eq.(discreteA))
   double *Aout = elA + cell * (int64_t)nvmax * nvmax;
   for (int i = 0; i < nv; ++i)
@@ -581,10 +587,57 @@ __global__ void __launch_bounds__(128) vem_element_kernel(const int *__restrict_
       Aout[(int64_t)i * nv + j] = v;
       Aout[(int64_t)j * nv + i] = v;
     }
-  // ================= (10) B^K = |K| DIVc (dual pressure basis, P:130-137)
-  double *Bout = elB + cell * (int64_t)D1 * nvmax;
-  for (int a = 0; a < D1; ++a)
-    for (int i = 0; i < nv; ++i) Bout[(int64_t)a * nv + i] = g.vol * DIV(a * nv + i);
+
+}
+
+// K9 stage (9), A^K = A_cons + (I - Pihat)^T D (I - Pihat) (Eq.(discreteA)), one thread per (cell,
+// row i) instead of one per cell (a c3 cell has 252 rows: the single-thread loop was 40 % of K9):
+// row i for j >= i from the cell's scratch (PIN, DP, QP, E, GE, ACD of vem_element_kernel), written
+// to both triangles, the same arithmetic in the same order as the single-thread version.
+template <int K>
+__global__ void __launch_bounds__(128) vem_assemble_A_kernel(const int *__restrict__ cell_nv,
+                                                             const double *__restrict__ nu, int64_t K0, int64_t nE,
+                                                             int nvmax, int nfmax, const double *__restrict__ scratch,
+                                                             int64_t NE, double *elA) {
+  using Ar = Arena<K>;
+  constexpr int D1 = Ar::D1, S3 = Ar::S3;
+  // lanes = consecutive cells, same row: the cell-interleaved scratch stays coalesced
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t e = t % nE;
+  const int i = (int)(t / nE);
+  if (i >= nvmax) return;
+  const int64_t cell = K0 + e;
+  const int nv = cell_nv[cell];
+  if (i >= nv) return;
+  const double nuK = nu[cell];
+  const Ar ar(nvmax, nfmax);
+  auto S = [&](int64_t off) { return SM{const_cast<double *>(scratch) + off * NE + e, NE}; };
+  const SM PIN = S(ar.PIN), DP = S(ar.DP), QP = S(ar.QP), E = S(ar.E), GE = S(ar.GE), ACD = S(ar.ACD);
+  auto acons = [&](int a_, int b_) {
+    double v = 0.0;
+    for (int p = 0; p < 6; ++p) {
+      const double wgt = p < 3 ? 1.0 : 2.0;
+      double s = 0.0;
+      for (int a = 0; a < D1; ++a) s += E(((int64_t)p * D1 + a) * nv + a_) * GE(((int64_t)p * D1 + a) * nv + b_);
+      v += wgt * s;
+    }
+    return nuK * v;
+  };
+  double *Aout = elA + cell * (int64_t)nvmax * nvmax;
+  const double acd_i = ACD(i);
+  for (int j = i; j < nv; ++j) {
+    double pij = 0.0, pji = 0.0, quad = 0.0;
+    for (int a = 0; a < S3; ++a) {
+      const double pa_i = PIN((int64_t)a * nv + i), pa_j = PIN((int64_t)a * nv + j);
+      pij += DP((int64_t)i * S3 + a) * pa_j;
+      pji += DP((int64_t)j * S3 + a) * pa_i;
+      quad += pa_i * QP((int64_t)a * nv + j);
+    }
+    double v = acons(i, j) - acd_i * pij - ACD(j) * pji + quad;
+    if (i == j) v += acd_i;
+    Aout[(int64_t)i * nv + j] = v;
+    Aout[(int64_t)j * nv + i] = v;
+  }
 }
 
 void element_matrices_device(vb_ctx *c, bool wait) {
@@ -614,14 +667,27 @@ void element_matrices_device(vb_ctx *c, bool wait) {
   for (int64_t K0 = 0; K0 < c->nKl; K0 += NE) {
     const int64_t n = std::min<int64_t>(NE, c->nKl - K0);
     const int blocks = (int)((n + k9_block - 1) / k9_block);
+    // stage (9) in its own thread-per-(cell, row) kernel when a thread per cell under-fills the GPU
+    // (c3: 4,096 cells, K9 1.33 -> 0.96 s); with many cells (c5: 32,768) the one-thread-per-cell
+    // loop is faster (0.135 against 0.173 s)
+    const bool split9 = k9_stop == 0 && n < 16384;
+    const int stop_arg = k9_stop == 0 && !split9 ? -1 : k9_stop;
 #define VB_K9(KK)                                                                                           \
   vem_element_kernel<KK><<<blocks, k9_block, 0, s>>>(c->d_topo.p, c->d_xyz.p, c->d_nu.p, K0, n, nvm, nfm, scratch.p, NE, \
-                                                c->d_elA.p, c->d_elB.p, c->d_P0.p, k9_stop)
+                                                c->d_elA.p, c->d_elB.p, c->d_P0.p, stop_arg)
     if (c->k == 2) VB_K9(2);
     else if (c->k == 3) VB_K9(3);
     else VB_K9(4);
 #undef VB_K9
     VB_STAGE();
+    if (split9) {   // stage (9): a thread per (cell, row)
+      const int64_t nt = n * nvm;
+      const int ab = (int)((nt + 127) / 128);
+      if (c->k == 2) vem_assemble_A_kernel<2><<<ab, 128, 0, s>>>(c->d_cell_nv.p, c->d_nu.p, K0, n, nvm, nfm, scratch.p, NE, c->d_elA.p);
+      else if (c->k == 3) vem_assemble_A_kernel<3><<<ab, 128, 0, s>>>(c->d_cell_nv.p, c->d_nu.p, K0, n, nvm, nfm, scratch.p, NE, c->d_elA.p);
+      else vem_assemble_A_kernel<4><<<ab, 128, 0, s>>>(c->d_cell_nv.p, c->d_nu.p, K0, n, nvm, nfm, scratch.p, NE, c->d_elA.p);
+      VB_STAGE();
+    }
   }
   if (wait) {
     VB_CUDA(cudaStreamSynchronize(s));

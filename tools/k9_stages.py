@@ -17,7 +17,7 @@ for i in range(2):
     ctx = vb.context_for(prob); ctx.close()
 '''
 for cfg in sys.argv[1:] or ["c5"]:
-    for stop in [1, 2, 3, 5, 6, 8, 0]:
+    for stop in [1, 2, 3, 5, 6, 8, 0]:   # 8: everything but stage (9)
         env = dict(os.environ, VB_K9_STOP=str(stop), VB_SETUP_TIMES="1", VB_NO_SETUP_OVERLAP="1")
         r = subprocess.run([sys.executable, "-c", code, cfg], env=env, capture_output=True, text=True)
         lines = [l for l in r.stderr.splitlines() if "K9" in l]
