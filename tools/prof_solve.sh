@@ -8,6 +8,6 @@ python tools/profile_solve.py --with-k7 > gpurun_out/ps_plain.log 2>&1 &&
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches_solve.csv python tools/profile_solve.py --with-k7 > gpurun_out/ps_ncu1.log 2>&1
 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k regex:"sym_gemv_kernel|phit_kernel|coarse_ext_kernel|local2_entity_sum_kernel|chunk_gather_dot_kernel|elem_apply_bulk_kernel" -c 9 \
+    -k regex:"sym_gemv_kernel|phit_kernel|coarse_ext_kernel|local2_entity_sum_kernel|chunk_gather_dot_kernel|cd_sum_parts_kernel|cd_interior_kernel|elem_apply_bulk_kernel" -c 14 \
     -o gpurun_out/${TAG}_solve_full python tools/profile_solve.py --with-k7 > gpurun_out/ps_ncu2.log 2>&1
 ls -la gpurun_out/${TAG}_*
