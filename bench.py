@@ -385,10 +385,11 @@ def main():
                                 "*_warm: a second vb_factor on the same context"},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ctx.n_free,
                 "d2h_bytes_per_step": 8 * ctx.n_free, "ms_per_step": e2e_ms},
-        # kernels per solve (single rank): 24 + 17 it, counted in the ncu launch list of a host-driven
-        # solve (profiles/r02_launches_c5_solve_hostdriven_summary.txt); multi-rank adds the exchange
-        # pack/sum kernels
-        "gpu_launches": int(args.steps * (24 + 17 * it)),
+        # kernels per solve (single rank): 24 + 21 it with the coarse dissection, 24 + 15 it with the
+        # dense coarse inverse, counted in the ncu launch lists of host-driven c5 solves
+        # (profiles/r02t_, r02k_launches_c5_solve_hostdriven_summary.txt; the graph runs the same
+        # kernels); multi-rank runs add the exchange pack/sum kernels (not counted here)
+        "gpu_launches": int(args.steps * (24 + (21 if st["n_coarse_root"] else 15) * it)),
         "clocks": clk.summary(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
