@@ -102,3 +102,22 @@ def test_binding_rejects_bad_buffers():
             ctx.pcg_solve(bad, x)
     with pytest.raises(ValueError):
         ctx.pcg_solve_host(rhs.cpu().numpy().astype(np.float32), np.zeros(ctx.n_free))
+
+
+def test_coarse_options_state_machine():
+    """vb_set_option("coarse_dissection" / "coarse_blocks") are read by vb_factor: VB_ESTATE after
+    it; unknown option names are VB_EINVAL; the auto rule picks the dense inverse for a small coarse
+    problem (c1: N_c = 65) and the blocked dissection for N_c >= 4096 (include/vbddc.h)."""
+    import paper_2304_09770_b200 as vb
+    from synthetic import make_problem
+    ctx = vb.context_for(make_problem("c1"))
+    with pytest.raises(vb.VBError) as e:
+        ctx.set_option("coarse_nonsense", 1)
+    assert e.value.status == vb.VB_EINVAL
+    ctx.factor()
+    assert ctx.stats()["n_coarse_root"] == 0          # auto: dense inverse for N_c = 65
+    for name in ("coarse_dissection", "coarse_blocks"):
+        with pytest.raises(vb.VBError) as e:
+            ctx.set_option(name, 1)
+        assert e.value.status == vb.VB_ESTATE
+    ctx.close()
