@@ -193,8 +193,12 @@ vb_status vb_pcg_solve(vb_ctx *ctx, const double *rhs_dev, double *x_dev, double
  *                   rounding.  Read by vb_factor (collective: every rank the same value); VB_ESTATE
  *                   after it.
  *   "coarse_blocks" (>= 1, or -1 auto = the default: the largest power of two <= 8 with at least
- *                   16 subdomains per block): the parts of the dissection on ONE rank, by recursive
- *                   coordinate bisection of the subdomain centroids.  Read by vb_factor.
+ *                   16 of the rank's subdomains per block, e.g. 8 for 512): blocks of this
+ *                   rank's subdomains by recursive coordinate bisection of their centroids.  One
+ *                   rank: the blocks are the parts.  Several ranks, > 1: two levels -- the rank
+ *                   first eliminates its blocks' interiors, then the separator between its blocks
+ *                   from the sum of their Schur contributions; the root is unchanged.  Read by
+ *                   vb_factor.
  * VB_EINVAL on an unknown name. */
 vb_status vb_set_option(vb_ctx *ctx, const char *name, double value);
 

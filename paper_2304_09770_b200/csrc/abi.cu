@@ -683,11 +683,14 @@ vb_status vb_stats(const vb_ctx *c, int64_t *o) {
   // coarse doubles streamed in the timed coarse window (the B6 kernel-time category): the inverse's
   // slice (or all of it), plus with the dissection the parts' packed matrices of pass 1
   int64_t cd_nloc = 0, pk_coarse = c->nranks > 1 ? (int64_t)c->d_Kcs.n : (int64_t)packed_size((int)(c->cdis ? c->Nroot : c->Nc));
-  if (c->cdis)
-    for (auto &d : c->cd_parts) {
+  if (c->cdis) {
+    std::vector<CdPart> all = c->cd_parts;
+    if (c->cd_two) all.push_back(c->cd2_part);
+    for (auto &d : all) {
       cd_nloc += d.nloc;
       if (d.nIp > 0) pk_coarse += packed_size((int)d.nloc);
     }
+  }
   int64_t v[28] = {c->nvel + c->npres, c->n_free_vel, c->npres, c->N, (int64_t)c->ents.size(), c->nGamma,
                    c->NPi_g, c->Nc, c->n_delta_glob, maxn, maxnG, maxnd, c->nE, (int64_t)c->bytes_per_iter, c->nv_max,
                    c->ncolors, pkG, pkD, ndsq, ndpi, pk_coarse, c->last_iterations, c->nK,

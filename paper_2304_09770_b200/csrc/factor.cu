@@ -905,6 +905,115 @@ static std::vector<int> coarse_blocks_rcb(const vb_ctx *c, int B) {
   return part;
 }
 
+// One level of the coarse dissection: the parts j (index lists I_j, S_j of global coarse indices)
+// each get a dense matrix on [I_j | pad | S_j] from `assemble` (K, Koff, D), a partial LDL^T
+// eliminating I_j (A_II SPD), W = L_II^-1, E = W^T D^-1 W and F^T = L_SI W packed as
+// [[E, .], [F^T, 0]] into Kpk, and their Schur contributions on S_j into pieces (part j at
+// j maxS^2, full symmetric, leading dimension maxS).  All batched over the parts.
+template <class Assemble>
+static std::vector<CdPart> eliminate_level(vb_ctx *c, const std::vector<std::vector<int64_t>> &I,
+                                           const std::vector<std::vector<int64_t>> &S, const std::vector<int> &ids,
+                                           int64_t maxS, DBuf<double> &Kpk, DBuf<double> &pieces,
+                                           const Assemble &assemble) {
+  cudaStream_t s = c->stream;
+  const int no = I.size();
+  std::vector<CdPart> D(no);
+  std::vector<int64_t> Koff(no + 1, 0), Woff(no + 1, 0);
+  int64_t kpk = 0;
+  for (int j = 0; j < no; ++j) {
+    CdPart &d = D[j];
+    d.part = ids[j];
+    d.nI = I[j].size();
+    d.nIp = (d.nI + 31) / 32 * 32;
+    d.nS = S[j].size();
+    d.nloc = d.nIp + d.nS;
+    d.koff = kpk;
+    kpk += packed_size((int)d.nloc);
+    Koff[j + 1] = Koff[j] + (int64_t)ld4((int)d.nloc) * d.nloc;
+    Woff[j + 1] = Woff[j] + (int64_t)ld4((int)std::max<int64_t>(d.nIp, 1)) * d.nIp;
+  }
+  DBuf<double> K;
+  K.alloc(std::max<int64_t>(Koff[no], 1));
+  K.zero(s);
+  assemble(K.p, Koff, D);
+  for (int j = 0; j < no; ++j)
+    if (D[j].nIp > D[j].nI) {
+      unit_diag_kernel<<<1, 64, 0, s>>>(K.p + Koff[j], ld4((int)D[j].nloc), D[j].nI, D[j].nIp);
+      VB_STAGE();
+    }
+  Kpk.release();
+  Kpk.alloc(std::max<int64_t>(kpk, 1));
+  Kpk.zero(s);
+  std::vector<MatDesc> lm;
+  std::vector<int> who;
+  for (int j = 0; j < no; ++j) {
+    if (!D[j].nIp) continue;
+    MatDesc m{K.p + Koff[j], (int)D[j].nloc, ld4((int)D[j].nloc), (int)D[j].nIp};
+    m.npos = (int)D[j].nIp;   // A_II SPD
+    lm.push_back(m);
+    who.push_back(D[j].part);
+  }
+  if (!lm.empty()) {
+    c->d_info.zero(s);
+    ldl_partial_batched(lm, c->d_info.p, s);
+    check_info(c, (int)lm.size(), "coarse interior LDL^T (f1)", &who, "part");
+    DBuf<double> W, dI, M;
+    W.alloc(std::max<int64_t>(Woff[no], 1));
+    W.zero(s);
+    std::vector<TriDesc> td;
+    for (int j = 0; j < no; ++j)
+      if (D[j].nIp)
+        td.push_back(TriDesc{K.p + Koff[j], ld4((int)D[j].nloc), W.p + Woff[j], ld4((int)D[j].nIp), (int)D[j].nIp});
+    tri_inverse_batched(td, s);
+    std::vector<int64_t> doff(no + 1, 0);
+    for (int j = 0; j < no; ++j) doff[j + 1] = doff[j] + D[j].nIp;
+    dI.alloc(std::max<int64_t>(doff[no], 1));
+    for (int j = 0; j < no; ++j)
+      if (D[j].nIp) {
+        recip_diag_kernel<<<(int)((D[j].nIp + 255) / 256), 256, 0, s>>>(K.p + Koff[j], ld4((int)D[j].nloc),
+                                                                        (int)D[j].nIp, dI.p + doff[j]);
+        VB_STAGE();
+      }
+    M.alloc(std::max<int64_t>(Koff[no], 1));
+    M.zero(s);
+    GemmPlan plan;
+    int l0 = plan.begin_launch();
+    for (int j = 0; j < no; ++j) {
+      if (!D[j].nIp) continue;
+      const int ldk = ld4((int)D[j].nloc), ldw = ld4((int)D[j].nIp);
+      GemmProb p{};
+      p.A = W.p + Woff[j]; p.lda = ldw; p.transA = 1; p.d = dI.p + doff[j]; p.dstride = 1;   // E = W^T D^-1 W
+      p.B = W.p + Woff[j]; p.ldb = ldw; p.C = M.p + Koff[j]; p.ldc = ldk;
+      p.M = p.N = p.K = (int)D[j].nIp; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
+      p.kz_on = 8;   // W lower triangular (site bit 8)
+      plan.add(p);
+      GemmProb q{};
+      q.A = K.p + Koff[j] + D[j].nIp; q.lda = ldk;                                           // F^T = L_SI W
+      q.B = W.p + Woff[j]; q.ldb = ldw; q.C = M.p + Koff[j] + D[j].nIp; q.ldc = ldk;
+      q.M = (int)D[j].nS; q.N = (int)D[j].nIp; q.K = (int)D[j].nIp; q.alpha = 1.0; q.beta = 0.0;
+      plan.add(q);
+    }
+    plan.upload(s);
+    plan.run(l0, s);
+    sync(c);
+    std::vector<PackDesc> pk;
+    for (int j = 0; j < no; ++j)
+      if (D[j].nIp) pk.push_back(PackDesc{M.p + Koff[j], (int)D[j].nloc, ld4((int)D[j].nloc), Kpk.p + D[j].koff});
+    pack_tiles_batched(pk, s);
+  }
+  pieces.alloc((size_t)maxS * maxS * std::max(no, 1));
+  pieces.zero(s);
+  for (int j = 0; j < no; ++j) {
+    const int64_t n = D[j].nS, ldk = ld4((int)D[j].nloc);
+    if (!n) continue;
+    copy_sym_lower_kernel<<<(int)std::min<int64_t>((n * n + 255) / 256, 8192), 256, 0, s>>>(
+        K.p + Koff[j] + D[j].nIp * (ldk + 1), ldk, n, pieces.p + (size_t)j * maxS * maxS, maxS);
+    VB_STAGE();
+  }
+  sync(c);
+  return D;
+}
+
 // dissection of the coarse saddle problem (solved by block elimination; DESIGN.md
 // §9).  The primal DOFs of an entity whose sharers all lie in one part p are interior to p: only p's
 // subdomains contribute to their rows and columns, so p is eliminated alone.  The other primal DOFs
@@ -916,76 +1025,82 @@ static std::vector<int> coarse_blocks_rcb(const vb_ctx *c, int B) {
 // like the dense coarse matrix (coarse_inverse_pack, sliced over ranks).  Solve: y_I = E g_I,
 // t = F^T g_I (one GEMV pass per part); x_S = S^-1 (g_S - sum_p t_p); x_I = y_I - F x_S.  Velocity
 // DOFs first in the local and the root orderings (A_II SPD; the root's pressure Schur complement
-// negative definite: the pivot test of ldl_panel).  Parts: ranks (R > 1) or blocks of one rank's
-// subdomains (R = 1, coarse_blocks).
+// negative definite: the pivot test of ldl_panel).
+// Parts: one GPU -- blocks of its subdomains (coarse_blocks); several ranks -- the ranks, and with
+// blocks (two levels) each rank first eliminates its blocks' interiors, then the separator between
+// its blocks (the rank-interior DOFs no block owns) from the sum of the blocks' Schur contributions;
+// only the cut between rank boxes and the p_0's reach the replicated root.
 static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector<int64_t> &lpoff,
                               const std::vector<int> &gnpi, const std::vector<int64_t> &pimoff,
                               const std::vector<int64_t> &pimap, double gam_c, int blocks) {
   cudaStream_t s = c->stream;
   const int R = c->nranks, Ng = c->Ng, N = c->N;
   const int64_t NPi = c->NPi_g, Nc = c->Nc;
-  const int nparts = R > 1 ? R : blocks;
-  const CoarsePlan P = plan_coarse_dissection(c, R > 1 ? c->sub_rank : coarse_blocks_rcb(c, blocks), nparts);
-  const std::vector<int64_t> &root = P.root, &rptr = P.rptr, &ridx = P.ridx;
-  const int64_t nsep = P.nsep, nroot = root.size(), maxS = P.maxS;
-  std::vector<int64_t> rpos(Nc, -1);
-  for (int64_t j = 0; j < nroot; ++j) rpos[root[j]] = j;
-  const int no = P.owned.size();
-  // owned parts j: sizes, matrix offsets (dense K_j / M_j: ld_j x nloc_j; W_j: ldW_j x nIp_j;
-  // packed [[E, .], [F^T, 0]] at koff_j)
-  std::vector<CdPart> D(no);
-  std::vector<int64_t> Koff(no + 1, 0), Woff(no + 1, 0), lp(Nc, -1), lpart(Nc, -1);
-  int64_t kpk = 0;
-  for (int j = 0; j < no; ++j) {
-    const int p = P.owned[j];
-    CdPart &d = D[j];
-    d.part = p;
-    d.nI = P.I[p].size();
-    d.nIp = (d.nI + 31) / 32 * 32;
-    d.nS = P.S[p].size();
-    d.nloc = d.nIp + d.nS;
-    d.koff = kpk;
-    kpk += packed_size((int)d.nloc);
-    Koff[j + 1] = Koff[j] + (int64_t)ld4((int)d.nloc) * d.nloc;
-    Woff[j + 1] = Woff[j] + (int64_t)ld4((int)std::max<int64_t>(d.nIp, 1)) * d.nIp;
-    for (int64_t a = 0; a < d.nI; ++a) { lp[P.I[p][a]] = a; lpart[P.I[p][a]] = j; }
-  }
-  // ---- local matrices on [I | pad | S] from the owned parts' pieces (no communication)
-  std::vector<int64_t> lmap, mapoff(N + 1, 0), p0pos(N), kbase(N);
-  std::vector<int> lnpi(N), kld(N);
-  for (int i = 0; i < N; ++i) {
-    const int g = c->sub_gid[i];
-    int j = 0;
-    while (j < no && P.owned[j] != P.part[g]) ++j;
-    VB_REQUIRE(j < no, VB_EINVAL, "internal: coarse dissection part");
-    const CdPart &d = D[j];
-    // S positions of this part (a subdomain's S DOFs are in its part's root list)
-    auto spos = [&](int64_t v) {
-      const auto &S = P.S[d.part];
-      const auto it = std::lower_bound(S.begin(), S.end(), v);
-      // the p_0's follow the sorted separator DOFs, in subdomain order (also sorted)
-      VB_REQUIRE(it != S.end() && *it == v, VB_EINVAL, "internal: coarse dissection map");
-      return d.nIp + (int64_t)(it - S.begin());
-    };
-    for (int64_t q = pimoff[g]; q < pimoff[g + 1]; ++q) {
-      const int64_t v = pimap[q];
-      lmap.push_back(lpart[v] == j ? lp[v] : spos(v));
+  const bool two = R > 1 && blocks > 1;
+  // global plan (parts = ranks, or the one-GPU blocks): root, S lists, root-rhs sources
+  const CoarsePlan G = plan_coarse_dissection(c, R > 1 ? c->sub_rank : coarse_blocks_rcb(c, blocks), R > 1 ? R : blocks);
+  // level-0 parts: the owned parts of G, or (two levels) this rank's blocks, planned with every
+  // other rank's subdomains in one extra part (entities they touch are never block-interior)
+  CoarsePlan L;
+  std::vector<std::vector<int64_t>> I0, S0;
+  std::vector<int> ids0;
+  int64_t maxS0 = G.maxS;
+  if (two) {
+    std::vector<int> part = coarse_blocks_rcb(c, blocks);
+    for (int g = 0; g < Ng; ++g)
+      if (c->sub_rank[g] != c->rank) part[g] = blocks;
+    L = plan_coarse_dissection(c, part, blocks + 1);
+    maxS0 = 1;
+    for (int b = 0; b < blocks; ++b) {
+      I0.push_back(L.I[b]); S0.push_back(L.S[b]); ids0.push_back(b);
+      maxS0 = std::max<int64_t>(maxS0, L.S[b].size());
     }
-    mapoff[i + 1] = lmap.size();
-    p0pos[i] = spos(NPi + g);
-    lnpi[i] = gnpi[g];
-    kbase[i] = Koff[j];
-    kld[i] = ld4((int)d.nloc);
+  } else {
+    for (int p : G.owned) { I0.push_back(G.I[p]); S0.push_back(G.S[p]); ids0.push_back(p); }
   }
-  if (lmap.empty()) lmap.push_back(0);
-  DBuf<int64_t> dlpoff, dmapoff, dlmap, dp0, dkb;
-  DBuf<int> dlnpi, dkld;
-  dlpoff.upload(lpoff, s); dmapoff.upload(mapoff, s); dlmap.upload(lmap, s); dp0.upload(p0pos, s);
-  dlnpi.upload(lnpi, s); dkb.upload(kbase, s); dkld.upload(kld, s);
-  DBuf<double> K;
-  K.alloc(std::max<int64_t>(Koff[no], 1));
-  K.zero(s);
+  const int no = I0.size();
+  // part of every level-0 interior DOF, its position; S positions by search in the sorted S lists
+  std::vector<int> lpart(Nc, -1);
+  std::vector<int64_t> lp(Nc, -1);
+  for (int j = 0; j < no; ++j)
+    for (size_t a = 0; a < I0[j].size(); ++a) { lp[I0[j][a]] = a; lpart[I0[j][a]] = j; }
+  std::vector<int> sub_j(N, -1);
   {
+    const std::vector<int> &part = two ? L.part : G.part;
+    for (int i = 0; i < N; ++i) {
+      const int pg = part[c->sub_gid[i]];
+      for (int j = 0; j < no; ++j) if (ids0[j] == pg) sub_j[i] = j;
+      VB_REQUIRE(sub_j[i] >= 0, VB_EINVAL, "internal: coarse dissection part");
+    }
+  }
+  auto spos = [&](const std::vector<int64_t> &Sl, int64_t nIp, int64_t v) {
+    const auto it = std::lower_bound(Sl.begin(), Sl.end(), v);   // separator DOFs, then p_0's: sorted
+    VB_REQUIRE(it != Sl.end() && *it == v, VB_EINVAL, "internal: coarse dissection map");
+    return nIp + (int64_t)(it - Sl.begin());
+  };
+  // ---- level 0: matrices from the local subdomains' (S_c, b~0) pieces (no communication)
+  DBuf<double> P0;
+  auto asm0 = [&](double *K, const std::vector<int64_t> &Koff, const std::vector<CdPart> &D) {
+    std::vector<int64_t> lmap, mapoff(N + 1, 0), p0pos(N), kbase(N);
+    std::vector<int> lnpi(N), kld(N);
+    for (int i = 0; i < N; ++i) {
+      const int g = c->sub_gid[i], j = sub_j[i];
+      const CdPart &d = D[j];
+      for (int64_t q = pimoff[g]; q < pimoff[g + 1]; ++q) {
+        const int64_t v = pimap[q];
+        lmap.push_back(lpart[v] == j ? lp[v] : spos(S0[j], d.nIp, v));
+      }
+      mapoff[i + 1] = lmap.size();
+      p0pos[i] = spos(S0[j], d.nIp, NPi + g);
+      lnpi[i] = gnpi[g];
+      kbase[i] = Koff[j];
+      kld[i] = ld4((int)d.nloc);
+    }
+    if (lmap.empty()) lmap.push_back(0);
+    DBuf<int64_t> dlpoff, dmapoff, dlmap, dp0, dkb;
+    DBuf<int> dlnpi, dkld;
+    dlpoff.upload(lpoff, s); dmapoff.upload(mapoff, s); dlmap.upload(lmap, s); dp0.upload(p0pos, s);
+    dlnpi.upload(lnpi, s); dkb.upload(kbase, s); dkld.upload(kld, s);
     std::vector<std::vector<int>> colors(c->ncolors);
     for (int i = 0; i < N; ++i) colors[c->gsub_color[c->sub_gid[i]]].push_back(i);
     for (auto &col : colors) {
@@ -993,97 +1108,76 @@ static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector
       DBuf<int> dcol;
       dcol.upload(col, s);
       coarse_assemble_local_kernel<<<dim3(8, col.size()), 256, 0, s>>>(dcol.p, dlpoff.p, dlnpi.p, dmapoff.p, dlmap.p,
-                                                                       dp0.p, pieces.p, K.p, dkb.p, dkld.p);
+                                                                       dp0.p, pieces.p, K, dkb.p, dkld.p);
       VB_STAGE();
       sync(c);
     }
-  }
-  for (int j = 0; j < no; ++j)
-    if (D[j].nIp > D[j].nI) {
-      unit_diag_kernel<<<1, 64, 0, s>>>(K.p + Koff[j], ld4((int)D[j].nloc), D[j].nI, D[j].nIp);
-      VB_STAGE();
+  };
+  std::vector<CdPart> D0 = eliminate_level(c, I0, S0, ids0, maxS0, c->d_Kloc, P0, asm0);
+  STAGE_T("  coarse level-0 elimination (f1)");
+  // ---- level 1 (two levels): this rank's matrix on [RS | pad | S_r], RS = the rank-interior DOFs
+  // no block owns, from the sum of its blocks' Schur contributions (block order)
+  DBuf<double> Ptop;
+  std::vector<CdPart> D1;
+  std::vector<int64_t> RS, l2ptr, l2idx;
+  if (two) {
+    {
+      std::vector<char> inblk(Nc, 0);
+      for (auto &v : I0) for (int64_t x : v) inblk[x] = 1;
+      for (int64_t x : G.I[c->rank]) if (!inblk[x]) RS.push_back(x);
     }
-  STAGE_T("  coarse local assembly (f1)");
-  c->d_Kloc.release();
-  c->d_Kloc.alloc(std::max<int64_t>(kpk, 1));
-  c->d_Kloc.zero(s);
-  {
-    std::vector<MatDesc> lm;
-    std::vector<int> who;
-    std::vector<TriDesc> td;
-    for (int j = 0; j < no; ++j) {
-      if (!D[j].nIp) continue;
-      const int ldk = ld4((int)D[j].nloc);
-      MatDesc m{K.p + Koff[j], (int)D[j].nloc, ldk, (int)D[j].nIp};
-      m.npos = (int)D[j].nIp;   // A_II SPD
-      lm.push_back(m);
-      who.push_back(D[j].part);
+    const std::vector<int64_t> &Sr = G.S[c->rank];
+    const int64_t nRS = RS.size(), nRSp = (nRS + 31) / 32 * 32;
+    auto pos1 = [&](int64_t v) {
+      const auto it = std::lower_bound(RS.begin(), RS.end(), v);
+      if (it != RS.end() && *it == v) return (int64_t)(it - RS.begin());
+      return spos(Sr, nRSp, v);
+    };
+    // level-0 S entries -> level-1 positions (the scatter of the Schur pieces and, in the solve, of
+    // the blocks' t vectors: CSR over level-1 positions, sources b * maxS0 + q in block order)
+    std::vector<std::vector<int64_t>> pos0(no);
+    for (int j = 0; j < no; ++j)
+      for (int64_t v : S0[j]) pos0[j].push_back(pos1(v));
+    const int64_t nl1 = nRSp + Sr.size();
+    l2ptr.assign(nl1 + 1, 0);
+    for (int j = 0; j < no; ++j) for (int64_t t : pos0[j]) ++l2ptr[t + 1];
+    for (int64_t a = 0; a < nl1; ++a) l2ptr[a + 1] += l2ptr[a];
+    l2idx.resize(l2ptr[nl1]);
+    {
+      std::vector<int64_t> fill(l2ptr.begin(), l2ptr.end() - 1);
+      for (int j = 0; j < no; ++j)
+        for (size_t q = 0; q < pos0[j].size(); ++q) l2idx[fill[pos0[j][q]]++] = (int64_t)j * maxS0 + q;
     }
-    if (!lm.empty()) {
-      c->d_info.zero(s);
-      ldl_partial_batched(lm, c->d_info.p, s);
-      check_info(c, (int)lm.size(), "coarse interior LDL^T (f1)", &who, "part");
-      DBuf<double> W, dI, M;
-      W.alloc(std::max<int64_t>(Woff[no], 1));
-      W.zero(s);
-      for (int j = 0; j < no; ++j)
-        if (D[j].nIp)
-          td.push_back(TriDesc{K.p + Koff[j], ld4((int)D[j].nloc), W.p + Woff[j], ld4((int)D[j].nIp), (int)D[j].nIp});
-      tri_inverse_batched(td, s);
-      std::vector<int64_t> doff(no + 1, 0);
-      for (int j = 0; j < no; ++j) doff[j + 1] = doff[j] + D[j].nIp;
-      dI.alloc(std::max<int64_t>(doff[no], 1));
-      for (int j = 0; j < no; ++j)
-        if (D[j].nIp) {
-          recip_diag_kernel<<<(int)((D[j].nIp + 255) / 256), 256, 0, s>>>(K.p + Koff[j], ld4((int)D[j].nloc),
-                                                                          (int)D[j].nIp, dI.p + doff[j]);
-          VB_STAGE();
-        }
-      M.alloc(std::max<int64_t>(Koff[no], 1));
-      M.zero(s);
-      GemmPlan plan;
-      int l0 = plan.begin_launch();
+    auto asm1 = [&](double *K, const std::vector<int64_t> &Koff, const std::vector<CdPart> &D) {
+      const int64_t ld = ld4((int)D[0].nloc);
       for (int j = 0; j < no; ++j) {
-        if (!D[j].nIp) continue;
-        const int ldk = ld4((int)D[j].nloc), ldw = ld4((int)D[j].nIp);
-        GemmProb p{};
-        p.A = W.p + Woff[j]; p.lda = ldw; p.transA = 1; p.d = dI.p + doff[j]; p.dstride = 1;   // E = W^T D^-1 W
-        p.B = W.p + Woff[j]; p.ldb = ldw; p.C = M.p + Koff[j]; p.ldc = ldk;
-        p.M = p.N = p.K = (int)D[j].nIp; p.alpha = 1.0; p.beta = 0.0; p.lower = 1;
-        p.kz_on = 8;   // W lower triangular (site bit 8)
-        plan.add(p);
-        GemmProb q{};
-        q.A = K.p + Koff[j] + D[j].nIp; q.lda = ldk;                                           // F^T = L_SI W
-        q.B = W.p + Woff[j]; q.ldb = ldw; q.C = M.p + Koff[j] + D[j].nIp; q.ldc = ldk;
-        q.M = (int)D[j].nS; q.N = (int)D[j].nIp; q.K = (int)D[j].nIp; q.alpha = 1.0; q.beta = 0.0;
-        plan.add(q);
+        const int64_t n = S0[j].size();
+        if (!n) continue;
+        DBuf<int64_t> dp;
+        dp.upload(pos0[j], s);
+        root_scatter_add_kernel<<<(int)std::min<int64_t>((n * n + 255) / 256, 8192), 256, 0, s>>>(
+            P0.p + (size_t)j * maxS0 * maxS0, maxS0, n, dp.p, K + Koff[0], ld);
+        VB_STAGE();
+        sync(c);
       }
-      plan.upload(s);
-      plan.run(l0, s);
-      sync(c);
-      std::vector<PackDesc> pk;
-      for (int j = 0; j < no; ++j)
-        if (D[j].nIp) pk.push_back(PackDesc{M.p + Koff[j], (int)D[j].nloc, ld4((int)D[j].nloc), c->d_Kloc.p + D[j].koff});
-      pack_tiles_batched(pk, s);
-    }
+    };
+    D1 = eliminate_level(c, {RS}, {Sr}, {c->rank}, G.maxS, c->d_Kloc2, Ptop, asm1);
+    P0.release();
+    STAGE_T("  coarse level-1 elimination (f1)");
   }
-  STAGE_T("  coarse local elimination (f1)");
-  // ---- root: the parts' Schur contributions (allgathered across ranks), summed in part order,
-  // augmented, factored, inverted
-  DBuf<double> piece, gath;
-  piece.alloc((size_t)maxS * maxS * no);
-  piece.zero(s);
-  for (int j = 0; j < no; ++j) {
-    const int64_t n = D[j].nS, ldk = ld4((int)D[j].nloc);
-    copy_sym_lower_kernel<<<(int)std::min<int64_t>((n * n + 255) / 256, 8192), 256, 0, s>>>(
-        K.p + Koff[j] + D[j].nIp * (ldk + 1), ldk, n, piece.p + (size_t)j * maxS * maxS, maxS);
-    VB_STAGE();
-  }
-  K.release();
-  const double *all = piece.p;   // part p at p * maxS^2 (R = 1: the owned parts are all parts, in order)
+  DBuf<double> &top = two ? Ptop : P0;
+  // ---- root: the top level's Schur contributions (allgathered across ranks), summed in part
+  // order, augmented, factored, inverted
+  const std::vector<int64_t> &root = G.root;
+  const int64_t nsep = G.nsep, nroot = root.size(), maxS = G.maxS;
+  std::vector<int64_t> rpos(Nc, -1);
+  for (int64_t j = 0; j < nroot; ++j) rpos[root[j]] = j;
+  const int nparts = G.nparts;
+  DBuf<double> gath;
+  const double *all = top.p;   // part p at p * maxS^2 (one GPU: the owned parts are all parts, in order)
   if (R > 1) {
     gath.alloc((size_t)maxS * maxS * R);
-    c->comm->allgather(piece.p, gath.p, maxS * maxS, s);
+    c->comm->allgather(top.p, gath.p, maxS * maxS, s);
     all = gath.p;
   }
   const int64_t ldR = ld4((int)nroot);
@@ -1094,11 +1188,11 @@ static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector
   {
     std::vector<int64_t> rp((size_t)maxS * nparts, 0);
     for (int p = 0; p < nparts; ++p)
-      for (size_t q = 0; q < P.S[p].size(); ++q) rp[(size_t)p * maxS + q] = rpos[P.S[p][q]];
+      for (size_t q = 0; q < G.S[p].size(); ++q) rp[(size_t)p * maxS + q] = rpos[G.S[p][q]];
     drp.upload(rp, s);
   }
   for (int p = 0; p < nparts; ++p) {
-    const int64_t n = P.S[p].size();
+    const int64_t n = G.S[p].size();
     root_scatter_add_kernel<<<(int)std::min<int64_t>((n * n + 255) / 256, 8192), 256, 0, s>>>(
         all + (size_t)p * maxS * maxS, maxS, n, drp.p + (size_t)p * maxS, Kr.p, ldR);
     VB_STAGE();
@@ -1108,6 +1202,7 @@ static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector
       gvol.p, Ng, gam_c, Kr.p, ldR, nsep);
   VB_STAGE();
   gath.release();
+  top.release();
   STAGE_T("  coarse root assembly (f1)");
   cd_dump(c, "kroot", Kr.p, nroot, nroot, ldR);
   c->d_info.zero(s);
@@ -1117,12 +1212,18 @@ static void coarse_dissection(vb_ctx *c, DBuf<double> &pieces, const std::vector
   check_info(c, 1, "coarse root LDL^T (f1)");
   coarse_inverse_pack(c, Kr, ldR, nroot);
   STAGE_T("  coarse root inverse (f1)");
-  c->Nroot = nroot; c->cd_nsep = nsep; c->cd_maxS = maxS; c->cd_nparts = nparts;
-  c->cd_parts = D;
-  c->cd_I.clear(); c->cd_S.clear();
-  for (int j = 0; j < no; ++j) { c->cd_I.push_back(P.I[D[j].part]); c->cd_S.push_back(P.S[D[j].part]); }
+  c->Nroot = nroot; c->cd_nsep = nsep; c->cd_maxS = maxS; c->cd_maxS0 = maxS0; c->cd_nparts = nparts;
+  c->cd_parts = D0;
+  c->cd_I = I0; c->cd_S = S0;
+  c->cd_two = two;
+  if (two) {
+    c->cd2_part = D1[0];
+    c->cd2_RS = RS;
+    c->cd2_S = G.S[c->rank];
+    c->cd2_ptr = l2ptr; c->cd2_idx = l2idx;
+  }
   c->cd_root_glob = root;
-  c->cd_rptr = rptr; c->cd_ridx = ridx;
+  c->cd_rptr = G.rptr; c->cd_ridx = G.ridx;
 }
 
 // A3 (second half) .. A5: dual Schur inverse, Phi, S_c, b~0, deluxe D_G^(m), coarse inverse.
@@ -1350,14 +1451,12 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
   const int Ng = c->Ng;
   const int64_t Nc = c->NPi_g + Ng;
   c->Nc = Nc;
-  // parts of the dissection on one rank: blocks of its subdomains (auto: the largest power of two
-  // <= 8 with at least 16 subdomains per block)
+  // blocks of this rank's subdomains (auto: the largest power of two <= 8 with at least 16
+  // subdomains per block): the parts on one rank; the first level of two on several ranks
   int blocks = 1;
-  if (c->nranks == 1) {
-    if (c->opt_coarse_blocks > 0) blocks = c->opt_coarse_blocks;
-    else while (blocks < 8 && 2 * blocks * 16 <= N) blocks *= 2;
-    blocks = std::max(1, std::min(blocks, N));
-  }
+  if (c->opt_coarse_blocks > 0) blocks = c->opt_coarse_blocks;
+  else while (blocks < 8 && 2 * blocks * 16 <= N) blocks *= 2;
+  blocks = std::max(1, std::min(blocks, N));
   // auto: always for several ranks; on one rank for coarse problems of >= 4096 unknowns split into
   // >= 2 blocks (c5: 1,025 -> 1,055 M DOF*it/s; small coarse problems keep the dense inverse)
   c->cdis = c->opt_coarse_dis < 0 ? (c->nranks > 1 || (Nc >= 4096 && blocks >= 2)) : c->opt_coarse_dis != 0;

@@ -381,6 +381,14 @@ struct vb_ctx {
   std::vector<std::vector<int64_t>> cd_I, cd_S;   // per owned part: interior / root list -> global coarse index
   std::vector<int64_t> cd_root_glob;
   std::vector<int64_t> cd_rptr, cd_ridx;   // root entry <- t entries p * maxS + q, part order
+  // two levels (R > 1 with coarse_blocks > 1): level 0 = this rank's blocks (t stride cd_maxS0),
+  // level 1 = the rank's separator between its blocks (cd2_RS) against its root list (cd2_S)
+  bool cd_two = false;
+  int64_t cd_maxS0 = 0;
+  vb::CdPart cd2_part;
+  std::vector<int64_t> cd2_RS, cd2_S;
+  std::vector<int64_t> cd2_ptr, cd2_idx;   // level-1 position <- block t entries b * maxS0 + q
+  vb::DBuf<double> d_Kloc2;
   vb::DBuf<double> d_Kloc;           // per owned part, packed [[A_II^-1, sym], [A_SI A_II^-1, 0]] (n_loc = nIp + nS)
   double factor_flops = 0;     // DMMA GEMM flops of the last vb_factor
   double factor_gemm_s = 0;    // their kernel time (CUDA events; VB_KERNEL_TIMING=1 only, else 0)

@@ -1038,14 +1038,29 @@ __global__ void cd_root_finish_kernel(const double *__restrict__ vol, int Ng, in
 // dissection pass 1 per owned part j (blockIdx.y): the P1 chunk partials of [[E, .], [F^T, 0]] [g_I; 0]
 // summed in fixed order, y_I = E g_I to Y, t = F^T g_I to T[j maxS ...]
 __global__ void cd_sum_parts_kernel(const CdPart *__restrict__ parts, const double *__restrict__ part1, double *Y,
-                                    double *T, int64_t maxS) {
+                                    double *T, int64_t maxS, const double *__restrict__ addT) {
   pdl_prologue();
   const CdPart D = parts[blockIdx.y];
   for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < D.nloc; a += (int64_t)gridDim.x * blockDim.x) {
     double v = 0.0;
     for (int q = 0; q < D.P1; ++q) v += part1[D.p1off + q * D.nloc + a];
     if (a < D.nIp) Y[D.yoff + a] = v;
-    else T[blockIdx.y * maxS + (a - D.nIp)] = v;
+    else T[blockIdx.y * maxS + (a - D.nIp)] = addT ? v + addT[a - D.nIp] : v;   // two levels: + the blocks' part
+  }
+}
+
+// two levels: the rank-level input from the blocks' t vectors (CSR over level-1 positions, block
+// order): X[a] = rc[RS[a]] - sum (a < nRS; the GEMV input [g_RS; 0]); C[q] = sum at S position q
+__global__ void cd_l2_input_kernel(const int64_t *__restrict__ ptr, const int64_t *__restrict__ idx,
+                                   const double *__restrict__ T1, const double *__restrict__ rc,
+                                   const int64_t *__restrict__ RS, int64_t nRS, int64_t nRSp, int64_t nl,
+                                   double *X, double *C) {
+  pdl_prologue();
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nl; a += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int64_t k = ptr[a]; k < ptr[a + 1]; ++k) v += T1[idx[k]];
+    if (a < nRS) X[a] = rc[RS[a]] - v;
+    else if (a >= nRSp) C[a - nRSp] = v;
   }
 }
 
@@ -1108,6 +1123,13 @@ struct SolveState {
   DBuf<CdPart> cd_parts;
   int cd_no = 0;
   int64_t cd_maxloc = 1, cd_maxI = 1;
+  // two levels: the blocks' t (T1, stride maxS0), the rank-level GEMV input X2, the blocks' part
+  // of the rank's root contribution C, the level-1 passes
+  DBuf<double> cd_T1, cd_X2, cd_C, cd2_part1, cd2_part2, cd2_Y;
+  DBuf<int64_t> cd2_map2, cd2_RS, cd2_ptr, cd2_idx;
+  DBuf<CdPart> cd2_desc;
+  DBuf<GemvWork> w_cd21, w_cd22;
+  int nw_cd21 = 0, nw_cd22 = 0;
   DBuf<double> gam2, gbuf, hbuf;     // B0: entity-major b_e; [zG | received]; DOF halo receive
   int64_t cmax = 0;
   SlotExchange XS, XE, XB, XH, XR;   // apply_S copies, extension products, B0 zG, DOF halo, rank partials
@@ -1375,7 +1397,16 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
     if (st->nw_cd1) {
       coarse_gemv(st->w_cd1.p, st->nw_cd1, st->sm_cd, st->big_cd);
       launch_pdl(st, cd_sum_parts_kernel, dim3((unsigned)((st->cd_maxloc + 255) / 256), st->cd_no), dim3(256), 0, s2,
-                 st->cd_parts.p, st->cd_part1.p, st->cd_Y.p, st->cd_T.p, c->cd_maxS);
+                 st->cd_parts.p, st->cd_part1.p, st->cd_Y.p, c->cd_two ? st->cd_T1.p : st->cd_T.p,
+                 c->cd_two ? c->cd_maxS0 : c->cd_maxS, (const double *)nullptr);
+    }
+    if (c->cd_two) {   // the rank level: its input from the blocks, pass 1, its root contribution
+      const CdPart &d2 = c->cd2_part;
+      launch_pdl(st, cd_l2_input_kernel, dim3(grid_for(d2.nloc)), dim3(256), 0, s2, st->cd2_ptr.p, st->cd2_idx.p,
+                 st->cd_T1.p, c->w_rc.p, st->cd2_RS.p, d2.nI, d2.nIp, d2.nloc, st->cd_X2.p, st->cd_C.p);
+      if (st->nw_cd21) coarse_gemv(st->w_cd21.p, st->nw_cd21, st->sm_cd, st->big_cd);
+      launch_pdl(st, cd_sum_parts_kernel, dim3((unsigned)((d2.nloc + 255) / 256), 1), dim3(256), 0, s2,
+                 st->cd2_desc.p, st->cd2_part1.p, st->cd2_Y.p, st->cd_T.p, c->cd_maxS, (const double *)st->cd_C.p);
     }
     const double *tg = st->cd_T.p;
     if (c->nranks > 1) {
@@ -1401,6 +1432,11 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
     // x_S (gauge-projected) to its global positions; pass 2: x_I = y_I - F x_S
     launch_pdl(st, cd_root_finish_kernel, dim3(1), dim3(1024), 0, s2, st->gvol.p, c->Ng, c->cd_nsep, st->cd_xroot.p,
                st->cd_root.p, c->Nroot, c->w_uc.p);
+    if (c->cd_two && st->nw_cd22) {   // x_RS = y_RS - F2 x_S before the blocks' pass 2 reads it
+      coarse_gemv(st->w_cd22.p, st->nw_cd22, st->sm_cd, st->big_cd);
+      launch_pdl(st, cd_interior_kernel, dim3((unsigned)((c->cd2_part.nI + 255) / 256), 1), dim3(256), 0, s2,
+                 st->cd2_desc.p, st->cd2_part2.p, st->cd2_Y.p, st->cd2_RS.p, c->w_uc.p);
+    }
     if (st->nw_cd2) {
       coarse_gemv(st->w_cd2.p, st->nw_cd2, st->sm_cd, st->big_cd);
       launch_pdl(st, cd_interior_kernel, dim3((unsigned)((st->cd_maxI + 255) / 256), st->cd_no), dim3(256), 0, s2,
@@ -1590,7 +1626,8 @@ void prepare_solve(vb_ctx *c) {
     st->cd_rptr.upload(c->cd_rptr, s);
     st->cd_ridx.upload(c->cd_ridx.empty() ? std::vector<int64_t>{0} : c->cd_ridx, s);
     st->cd_Y.alloc(std::max<int64_t>(y, 1));
-    st->cd_T.alloc((int64_t)std::max(no, 1) * c->cd_maxS); st->cd_T.zero(s);
+    st->cd_T.alloc((int64_t)(c->cd_two ? 1 : std::max(no, 1)) * c->cd_maxS); st->cd_T.zero(s);
+    if (c->cd_two) { st->cd_T1.alloc((int64_t)std::max(no, 1) * c->cd_maxS0); st->cd_T1.zero(s); }
     if (c->nranks > 1) st->cd_tg.alloc(c->cd_maxS * c->nranks);
     st->cd_part1.alloc(std::max<int64_t>(p1, 1)); st->cd_part2.alloc(std::max<int64_t>(p2, 1));
     st->nw_cd1 = st->nw_cd2 = 0;
@@ -1605,6 +1642,31 @@ void prepare_solve(vb_ctx *c) {
     st->cd_parts.upload(D, s);
     st->cd_no = no; st->cd_maxloc = maxloc; st->cd_maxI = maxI;
     c->cd_parts = D;
+    if (c->cd_two) {
+      CdPart d2 = c->cd2_part;
+      const int64_t ntl = (d2.nloc + 31) / 32, tS = d2.nIp / 32;
+      d2.P1 = d2.nIp ? (int)std::min<int64_t>(ntl, c->P_c) : 0;
+      d2.P2 = d2.nIp ? (int)std::min<int64_t>(ntl - tS, c->P_c) : 0;
+      d2.p1off = d2.p2off = d2.yoff = d2.moff = d2.ioff = 0;
+      std::vector<int64_t> mp2(d2.nloc, c->Nc);
+      for (int64_t q = 0; q < d2.nS; ++q) mp2[d2.nIp + q] = c->cd2_S[q];
+      st->cd2_map2.upload(mp2, s);
+      st->cd2_RS.upload(c->cd2_RS.empty() ? std::vector<int64_t>{0} : c->cd2_RS, s);
+      st->cd2_ptr.upload(c->cd2_ptr, s);
+      st->cd2_idx.upload(c->cd2_idx.empty() ? std::vector<int64_t>{0} : c->cd2_idx, s);
+      st->cd_X2.alloc(std::max<int64_t>(d2.nloc, 1)); st->cd_X2.zero(s);
+      st->cd_C.alloc(std::max<int64_t>(d2.nS, 1)); st->cd_C.zero(s);
+      st->cd2_Y.alloc(std::max<int64_t>(d2.nIp, 1));
+      st->cd2_part1.alloc(std::max<int64_t>((int64_t)d2.P1 * d2.nloc, 1));
+      st->cd2_part2.alloc(std::max<int64_t>((int64_t)d2.P2 * d2.nloc, 1));
+      if (d2.P1) slice_work(c->d_Kloc2.p, 0, nullptr, st->cd_X2.p, st->cd2_part1.p, d2.nloc, 0, ntl, d2.P1);
+      st->w_cd21.upload(wl, s); st->nw_cd21 = wl.size(); wl.clear();
+      if (d2.P2) slice_work(c->d_Kloc2.p, 0, st->cd2_map2.p, c->w_uc.p, st->cd2_part2.p, d2.nloc, tS, ntl, d2.P2);
+      st->w_cd22.upload(wl, s); st->nw_cd22 = wl.size(); wl.clear();
+      st->cd2_desc.upload(std::vector<CdPart>{d2}, s);
+      c->cd2_part = d2;
+      maxloc = std::max(maxloc, d2.nloc);
+    }
     st->sm_cd = gemv_smem(maxloc, GV_WARPS_C);
     st->big_cd = st->sm_cd > 200 * 1024;
     if (!st->big_cd)
@@ -1861,9 +1923,12 @@ void prepare_solve(vb_ctx *c) {
   }
   // (the deluxe blocks are folded into S_DD^-1 and Phi at factor time: no per-iteration D traffic)
   b += 8.0 * (c->nranks > 1 ? (double)c->d_Kcs.n : (double)packed_size(c->cdis ? c->Nroot : c->Nc));
-  if (c->cdis)   // dissection passes 1 (all of each part's matrix) and 2 (its S tile rows)
-    for (auto &d : c->cd_parts)
+  if (c->cdis) {   // dissection passes 1 (all of each part's matrix) and 2 (its S tile rows)
+    std::vector<CdPart> all = c->cd_parts;
+    if (c->cd_two) all.push_back(c->cd2_part);
+    for (auto &d : all)
       if (d.nIp > 0) b += 8.0 * (2.0 * packed_size((int)d.nloc) - ptile_row_start(d.nIp / 32));
+  }
   c->bytes_per_iter = b;
 }
 

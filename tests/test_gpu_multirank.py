@@ -14,7 +14,8 @@ from synthetic import make_problem
 pytestmark = pytest.mark.gpu
 
 
-def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=None, p2p=False, coarse=None):
+def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=None, p2p=False, coarse=None,
+               blocks=None):
     import torch
     import paper_2304_09770_b200 as vb
     if srank is None:
@@ -29,6 +30,8 @@ def _run_ranks(prob, rank_grid, rtol=1e-10, check_operator=True, srank=None, R=N
             ctx.set_option("p2p", 1)
         if coarse is not None:
             ctx.set_option("coarse_dissection", coarse)
+        if blocks is not None:
+            ctx.set_option("coarse_blocks", blocks)
         ctx.factor()
         stats = ctx.stats()
         rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda")
@@ -238,6 +241,9 @@ def test_multirank_peer_stores_bitwise(name, kw, assign):
     ("c1", dict(n=8), "checkerboard"),    # every entity crosses ranks: no interior DOFs anywhere
     ("c1", dict(n=8), "stripes3"),        # ragged rank sizes
     ("c3", dict(n=8), (2, 1, 1)),         # k = 3, jittered triangulated cells
+    ("c1", dict(n=8), ((1, 1, 2), 2)),    # two levels: 2 ranks x 2 blocks of 16 subdomains
+    ("c2", {}, ((2, 2, 2), 2)),           # 8 ranks x 2 blocks
+    ("c4", dict(n=16, constraints=dict(adaptive_tau=2.0)), ((2, 1, 1), 4)),   # adaptive, 4 blocks per rank
     ("c4", dict(n=16, constraints=dict(adaptive_tau=2.0)), (2, 2, 1)),   # adaptive rows on the separator
 ])
 def test_coarse_dissection_matches_dense_coarse(name, kw, grid):
@@ -273,6 +279,9 @@ def test_coarse_dissection_matches_dense_coarse(name, kw, grid):
         if isinstance(grid, str):
             srank, R = _srank(prob, grid)
             runs = [_run_ranks(prob, None, srank=srank, R=R, coarse=opt, check_operator=False) for opt in (0, 1)]
+        elif isinstance(grid[0], tuple):   # two levels: (rank grid, blocks per rank)
+            runs = [_run_ranks(prob, grid[0], coarse=opt, blocks=grid[1] if opt else None, check_operator=False)
+                    for opt in (0, 1)]
         else:
             runs = [_run_ranks(prob, grid, coarse=opt, check_operator=False) for opt in (0, 1)]
     dense, dis = runs
@@ -290,8 +299,8 @@ def test_coarse_dissection_matches_dense_coarse(name, kw, grid):
     assert np.linalg.norm(xb - xa) <= 1e-10 * np.linalg.norm(xa)
 
 
-@pytest.mark.parametrize("name", ["c2", "c5"])
-def test_full_size_eight_ranks_vs_oracle_golden(name):
+@pytest.mark.parametrize("name,blocks", [("c2", None), ("c5", None), ("c5", 4)])
+def test_full_size_eight_ranks_vs_oracle_golden(name, blocks):
     """SURVEY f1 / §8(e) at full size: config 2 (64 subdomains) and config 5 (the bench workload,
     512 subdomains, 954,947 DOFs) split over 8 loopback ranks in 2x2x2 boxes, coarse problem by
     rank-level dissection (the default for R > 1), against the stored whole-vector oracle solve
@@ -308,7 +317,7 @@ def test_full_size_eight_ranks_vs_oracle_golden(name):
     ctx1.close()
     pos = np.full(int(ids1.max()) + 1, -1, np.int64)
     pos[ids1] = np.arange(ids1.size)
-    outs = _run_ranks(prob, (2, 2, 2), check_operator=False)
+    outs = _run_ranks(prob, (2, 2, 2), check_operator=False, blocks=blocks)
     x = np.full(ids1.size, np.nan)
     for o in outs:
         x[pos[o["ids"]]] = o["x"]
@@ -319,7 +328,7 @@ def test_full_size_eight_ranks_vs_oracle_golden(name):
     xo = z["x_full"]
     du = np.linalg.norm(x[:nv] - xo[:nv]) / np.linalg.norm(xo[:nv])
     dp = np.linalg.norm(x[nv:] - xo[nv:]) / np.linalg.norm(xo[nv:])
-    print("%s 8 ranks: du %.2e dp %.2e it %d (oracle %d), root %d of N_c %d, local %s"
-          % (name, du, dp, outs[0]["rep"]["iterations"], meta["iterations"], outs[0]["stats"]["n_coarse_root"],
+    print("%s 8 ranks (blocks %s): du %.2e dp %.2e it %d (oracle %d), root %d of N_c %d, local %s"
+          % (name, blocks, du, dp, outs[0]["rep"]["iterations"], meta["iterations"], outs[0]["stats"]["n_coarse_root"],
              outs[0]["stats"]["n_coarse"], [o["stats"]["n_coarse_local"] for o in outs]))
     assert du <= 1e-8 and dp <= 1e-8, (du, dp)
