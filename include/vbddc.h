@@ -114,7 +114,7 @@ vb_status vb_plan_exchange(const vb_mesh *mesh, const int32_t *cell_subdomain, i
                            const int32_t *subdomain_rank, int32_t rank, int32_t nranks, int32_t mode,
                            int64_t *send_counts, int64_t *recv_counts, int64_t *n_owned_free);
 
-/* Host-only planning, no GPU needed: the sizes of the rank-level coarse
+/* Host-only planning, no GPU needed: the sizes of the single-level coarse
  * dissection this rank would build if every interface entity of kind q (0 vertex, 1 edge, 2 face)
  * carried min(n_e, primal_per_kind[q]) primal DOFs (the factor computes the true counts by the
  * pivoted QR of the constraint rows; for the BASELINE constraints on hexahedral meshes they are
