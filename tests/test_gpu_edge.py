@@ -184,7 +184,8 @@ def test_refactor_then_solve():
 
 def test_no_uninitialised_reads_poisoned_memory():
     """Every device allocation filled with NaN bits (VB_POISON=1, in a fresh process): a 1-rank solve,
-    an adaptive solve and a 2-rank loopback solve must still converge to the same answers -- no kernel
+    an adaptive solve, a 2-rank loopback solve and the coarse dissection (4 blocks on one rank; two
+    levels on 2 ranks x 2 blocks) must still converge to the same answers -- no kernel
     may read memory it has not written (regression: the first CG direction once read p)."""
     import os
     import subprocess
@@ -195,8 +196,10 @@ import sys, concurrent.futures as cf, numpy as np, torch
 sys.path.insert(0, %r); sys.path.insert(0, %r)
 import paper_2304_09770_b200 as vb
 from synthetic import make_problem
-def solve(prob, **kw):
-    ctx = vb.context_for(prob, **kw); ctx.factor()
+def solve(prob, opts=(), **kw):
+    ctx = vb.context_for(prob, **kw)
+    for k, v in opts: ctx.set_option(k, v)
+    ctx.factor()
     rhs = torch.zeros(ctx.n_free, dtype=torch.float64, device="cuda"); x = torch.zeros_like(rhs)
     torch.cuda.synchronize(); ctx.build_rhs(vb.problem_args(prob), rhs)
     rep = ctx.pcg_solve(rhs, x, rtol=1e-10); ids = ctx.dof_layout(); xh = x.cpu().numpy(); ctx.close()
@@ -212,6 +215,20 @@ with cf.ThreadPoolExecutor(2) as ex:
     outs = list(ex.map(lambda r: solve(prob, stream=streams[r], rank=r, nranks=2, subdomain_rank=srank, world=world), range(2)))
 world.close()
 pos = {int(g): i for i, g in enumerate(ids1)}
+xr = np.full(x1.size, np.nan)
+for rep, ids, x in outs:
+    assert rep["status"] == "OK"
+    xr[[pos[int(g)] for g in ids]] = x
+assert np.linalg.norm(xr - x1) <= 1e-10 * np.linalg.norm(x1)
+# the coarse dissection over 4 blocks on one rank, and two levels (2 ranks x 2 blocks)
+cd = (("coarse_dissection", 1), ("coarse_blocks", 4))
+rep, ids, x = solve(prob, opts=cd)
+assert rep["status"] == "OK" and np.linalg.norm(x - x1) <= 1e-10 * np.linalg.norm(x1)
+world = vb.LoopbackWorld(2)
+with cf.ThreadPoolExecutor(2) as ex:
+    outs = list(ex.map(lambda r: solve(prob, opts=(("coarse_blocks", 2),), stream=streams[r], rank=r, nranks=2,
+                                        subdomain_rank=srank, world=world), range(2)))
+world.close()
 xr = np.full(x1.size, np.nan)
 for rep, ids, x in outs:
     assert rep["status"] == "OK"
