@@ -18,7 +18,10 @@ namespace vb {
 // on the factor's shapes (profiles/r02_gemm_proto.txt).
 using GCfg = g2::Cfg<64, 64, 16, 4, 1, 3, 4>;
 constexpr int GBM = GCfg::BM, GBN = GCfg::BN, GBK = GCfg::BK;
-constexpr int LDL_NB = 256;        // wide-panel width of the blocked LDL^T
+#ifndef LDL_NB_CFG
+#define LDL_NB_CFG 256
+#endif
+constexpr int LDL_NB = LDL_NB_CFG;   // wide-panel width of the blocked LDL^T (VB_NVCC_DEFINES knob)
 #ifndef TRI_NB_CFG
 #define TRI_NB_CFG 256
 #endif
