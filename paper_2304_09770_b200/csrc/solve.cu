@@ -1102,6 +1102,7 @@ struct SolveState {
   int phit_split = 4;                // CTAs per subdomain of phit_kernel
   bool big_c = false;                // coarse vectors exceed shared memory: BIG GEMV variant
   bool big_op = false, big_loc = false, big_kd = false;   // the same for the subdomain matrices
+  bool pair_sub = false;             // subdomain GEMVs with two tiles per warp step (sym_gemv PAIR)
   size_t sm_op = 0, sm_loc = 0, sm_c = 0, sm_ex = 0, sm_kd = 0;
   DBuf<int64_t> xptr, xidx;          // B2: x coordinate <- copies (local s or received), sharer order
   DBuf<int64_t> pptr, pidx;          // B6: global coarse index <- coarse pieces, fixed order
@@ -1217,6 +1218,8 @@ static void run_sub_gemv(const SolveState *st, const GemvWork *w, int nw, size_t
   if (nw <= 0) return;
   if (big)
     launch_pdl(st, sym_gemv_kernel<GV_WARPS, true>, dim3(nw), dim3(GV_WARPS * 32), GV_WARPS * 32 * sizeof(double), s, w);
+  else if (st->pair_sub)   // two tiles per warp step: twice the loads in flight when smem limits the CTAs per SM
+    launch_pdl(st, sym_gemv_kernel<GV_WARPS, false, true>, dim3(nw), dim3(GV_WARPS * 32), sm, s, w);
   else
     launch_pdl(st, sym_gemv_kernel<GV_WARPS>, dim3(nw), dim3(GV_WARPS * 32), sm, s, w);
 }
@@ -1676,6 +1679,11 @@ void prepare_solve(vb_ctx *c) {
   st->big_loc = st->sm_loc > 200 * 1024;
   size_t smmax = std::max(st->big_op ? 0 : st->sm_op, st->big_loc ? 0 : st->sm_loc);
   raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS>, smmax);
+  {
+    const char *ep = getenv("VB_GV_PAIR");   // experiment knob: 1 on, 0 off
+    st->pair_sub = ep ? atoi(ep) != 0 : false;
+  }
+  if (st->pair_sub) raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS, false, true>, smmax);
   if (!st->big_c)
     raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS_C, false, true>, st->sm_c);
   st->max_nd = nmaxD;
@@ -1869,6 +1877,7 @@ void prepare_solve(vb_ctx *c) {
     st->big_kd = st->sm_kd > 200 * 1024;
     size_t smg = std::max(std::max(st->big_op ? 0 : st->sm_op, st->big_loc ? 0 : st->sm_loc), st->big_kd ? 0 : st->sm_kd);
     raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS>, smg);
+    if (st->pair_sub) raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS, false, true>, smg);
   }
   // ---------------- B0 / B8 coupling gathers: output row <- (cell, element row) slots in cell order
   {
