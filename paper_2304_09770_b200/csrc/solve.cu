@@ -1675,8 +1675,11 @@ void prepare_solve(vb_ctx *c) {
     if (!st->big_cd)
       raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS_C, false, true>, st->sm_cd);
   }
-  st->big_op = st->sm_op > 200 * 1024;
-  st->big_loc = st->sm_loc > 200 * 1024;
+  // VB_GV_BIG=<bytes>: experiment knob, the BIG variant (x through the L2, partial output in global
+  // memory, shared memory only for the row reduction) from that many bytes of staged vectors on
+  static const int64_t gv_big = getenv("VB_GV_BIG") ? atoll(getenv("VB_GV_BIG")) : 200 * 1024;
+  st->big_op = (int64_t)st->sm_op > gv_big;
+  st->big_loc = (int64_t)st->sm_loc > gv_big;
   size_t smmax = std::max(st->big_op ? 0 : st->sm_op, st->big_loc ? 0 : st->sm_loc);
   raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS>, smmax);
   {
@@ -1874,7 +1877,7 @@ void prepare_solve(vb_ctx *c) {
     st->w_kd.upload(wk, s);
     st->nw_kd = wk.size();
     st->sm_kd = gemv_smem(nmaxDn);
-    st->big_kd = st->sm_kd > 200 * 1024;
+    st->big_kd = (int64_t)st->sm_kd > gv_big;
     size_t smg = std::max(std::max(st->big_op ? 0 : st->sm_op, st->big_loc ? 0 : st->sm_loc), st->big_kd ? 0 : st->sm_kd);
     raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS>, smg);
     if (st->pair_sub) raise_smem_limit((const void *)sym_gemv_kernel<GV_WARPS, false, true>, smg);
