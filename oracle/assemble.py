@@ -32,14 +32,25 @@ class GlobalDofs:
         self.oC = self.oF + 3 * self.nm * nF
         self.nvel = self.oC + nK * (self.n4 + self.n5)
         self.npres = nK * self.np_
-        # boundary entities
-        bf = np.nonzero(mesh.face_on_boundary)[0]
+        # boundary entities: face_on_boundary 1 = Dirichlet, 2 = Neumann (natural condition, the
+        # DOFs of the face closure stay free unless they also lie on a Dirichlet face; DESIGN A35)
+        bf = np.nonzero(mesh.face_on_boundary == 1)[0]
         bverts = set(); bedges = set()
         for f in bf:
             lp = mesh.face(f)
             for i in range(len(lp)):
                 bverts.add(int(lp[i]))
                 bedges.add(self.eidx(lp[i], lp[(i + 1) % len(lp)]))
+        nf = np.nonzero(mesh.face_on_boundary == 2)[0]
+        self.neumann = nf.size > 0
+        on_neu = np.zeros(self.nvel, dtype=bool)
+        for f in nf:
+            lp = mesh.face(f)
+            for i in range(len(lp)):
+                on_neu[3 * int(lp[i]) + np.arange(3)] = True
+                e = self.eidx(lp[i], lp[(i + 1) % len(lp)])
+                on_neu[self.oE + 3 * (k - 1) * e + np.arange(3 * (k - 1))] = True
+            on_neu[self.oF + 3 * self.nm * f + np.arange(3 * self.nm)] = True
         self.bverts = np.array(sorted(bverts), dtype=np.int64)
         self.bedges = np.array(sorted(bedges), dtype=np.int64)
         self.bfaces = bf
@@ -56,6 +67,7 @@ class GlobalDofs:
         self.n_free_vel = self.free_vel.size
         self.vel2free = -np.ones(self.nvel, dtype=np.int64)
         self.vel2free[self.free_vel] = np.arange(self.free_vel.size)
+        self.free_on_neumann = on_neu[self.free_vel]      # per free velocity DOF
 
     def n_dofs_paper(self):
         """nDofs as counted in T2-T4: all velocity DOFs incl. boundary + all pressure."""
@@ -236,9 +248,13 @@ class GlobalSystem:
 
     def direct_solve(self):
         """Sparse direct solve of Eq.(DiscProblem) with the zero-mean pressure gauge
-        (Q_{h,0}) imposed by a Lagrange multiplier."""
+        (Q_{h,0}) imposed by a Lagrange multiplier; with Neumann faces the
+        pressure is unique and the saddle matrix is solved as it stands."""
         import scipy.sparse.linalg as spla
         nvf, npr = self.dofs.n_free_vel, self.dofs.npres
+        if self.dofs.neumann:
+            x = spla.spsolve(self.saddle_matrix().tocsc(), np.concatenate([self.rhs_u, self.rhs_p]))
+            return x[:nvf], x[nvf:]
         m = sp.csr_matrix(self.pmass[None, :])
         M = sp.bmat([[self.Aff, self.Bf.T, None], [self.Bf, None, m.T], [None, m, None]]).tocsc()
         rhs = np.concatenate([self.rhs_u, self.rhs_p, [0.0]])

@@ -65,24 +65,33 @@ class BDDC:
         for i in range(N):
             for d in sub_vel[i]:
                 sharers.setdefault(d, []).append(i)
-        gam = sorted(d for d, s in sharers.items() if len(s) > 1)
+        # Gamma_i = the free DOFs on the subdomain boundary: shared DOFs, and with Neumann faces
+        # also the DOFs on the subdomain's part of the Neumann boundary (one sharer), so
+        # the flux row b_0^(i) keeps acting on Gamma only (DESIGN A35)
+        self.neumann = bool(dofs.neumann)
+        onN = dofs.free_on_neumann
+        gam = sorted(d for d, s in sharers.items() if len(s) > 1 or onN[d])
         self.gamma = np.array(gam, dtype=np.int64)        # interface DOFs (free-velocity ids)
         self.nG = len(gam)
         gpos = {d: j for j, d in enumerate(gam)}
         # ---------------- entities = classes of interface DOFs with equal sharer sets
+        # (with Neumann faces the class key also says whether the DOF lies on the Neumann boundary,
+        # so the lines and points where subdomains meet on it are entities of their own; DESIGN A35)
         classes = {}
         for d in gam:
-            classes.setdefault(tuple(sharers[d]), []).append(d)
+            classes.setdefault(tuple(sharers[d]) + ((-1,) if onN[d] else ()), []).append(d)
         ents = sorted(classes.items(), key=lambda kv: min(kv[1]))
         self.ents = []
         for key, dl in ents:
             E = Entity()
-            E.sharers = list(key)
+            E.sharers = [x for x in key if x >= 0]
             E.dofs = np.array(sorted(dl), dtype=np.int64)          # free-velocity ids
             E.gpos = np.array([gpos[d] for d in E.dofs])           # interface positions
             gv = dofs.free_vel[E.dofs]                             # global velocity ids
             if np.all(gv < dofs.oE) and len(np.unique(gv // 3)) == 1:
                 E.kind = "vertex"
+            elif key[-1] == -1:          # on the Neumann boundary: face iff it holds face moments
+                E.kind = "face" if np.any((gv >= dofs.oF) & (gv < dofs.oC)) else "edge"
             elif len(key) == 2:
                 E.kind = "face"
             else:
@@ -314,7 +323,8 @@ class BDDC:
             E.Sblocks = blocks
 
     def _coarse(self):
-        """Coarse saddle problem on (u_Pi, p_0) (SURVEY O-13) with gauge sum vol_i p0_i = 0."""
+        """Coarse saddle problem on (u_Pi, p_0) (SURVEY O-13) with gauge sum vol_i p0_i = 0
+        (no gauge with Neumann faces: the Neumann patches' flux constraints make it nonsingular)."""
         N, NPi = self.N, self.NPi
         nc = NPi + N
         Kc = np.zeros((nc, nc))
@@ -326,6 +336,10 @@ class BDDC:
             Kc[g, NPi + i] += b
         self.Kc = Kc
         vol = np.array([S.vol for S in self.sub])
+        self.vols = vol
+        if self.neumann:
+            self.Kc_lu = sla.lu_factor(Kc)
+            return
         Mb = np.zeros((nc + 1, nc + 1))
         Mb[:nc, :nc] = Kc
         Mb[nc, NPi:nc] = vol; Mb[NPi:nc, nc] = vol
@@ -333,6 +347,8 @@ class BDDC:
         self.vols = vol
 
     def coarse_solve(self, rc):
+        if self.neumann:
+            return sla.lu_solve(self.Kc_lu, rc)
         x = sla.lu_solve(self.Kc_lu, np.concatenate([rc, [0.0]]))
         return x[:-1]
 
@@ -406,6 +422,8 @@ class BDDC:
             y = S.KDD_lu.solve(self._bD[i] - S.KDG @ uG[S.Gpos])
             u[S.I] = y[:S.nI]
             p[S.P] = S.Z @ y[S.nI:] + p0[i] * S.c
+        if self.neumann:
+            return u, p
         mean = (gs.pmass @ p) / gs.pmass[::dofs.np_].sum()
         cglob = np.zeros(dofs.npres)
         for i, S in enumerate(self.sub):
@@ -424,7 +442,7 @@ class BDDC:
         self.adaptive_count = 0
         self.adaptive_pencils = {}
         for e, E in enumerate(self.ents):
-            if E.kind != "face" or E.nd == 0:
+            if E.kind != "face" or E.nd == 0 or len(E.sharers) != 2:
                 continue
             St, Sf = [], []
             for m in E.sharers:

@@ -16,7 +16,7 @@ Multi-sinker (config 4; BASELINE.json configs[3]):
 """
 from dataclasses import dataclass, field
 import numpy as np
-from .mesh import hex_mesh, box_partition, cvt_mesh, centroid_partition, octa_mesh
+from .mesh import hex_mesh, box_partition, cvt_mesh, centroid_partition, octa_mesh, mark_neumann
 
 
 @dataclass
@@ -83,8 +83,10 @@ C5_DIMS = {1: (32, 32, 32), 2: (32, 32, 64), 4: (32, 64, 64), 8: (64, 64, 64)}
 
 
 def make_problem(name, seed=20230419, n=None, sub=None, k=None, dims=None, nu=1.0, kind=None,
-                 constraints=None):
-    """Build the seeded inputs of config `name`; keyword overrides give small variants."""
+                 constraints=None, neumann=None):
+    """Build the seeded inputs of config `name`; keyword overrides give small variants.
+    neumann: sides of the cube posed with the natural (homogeneous traction) condition, e.g.
+    ("x1", "y1") for the paper's two Neumann faces (DESIGN A35)."""
     cfg = dict(CONFIGS[name])
     if n is not None:
         cfg["n"] = n
@@ -102,6 +104,8 @@ def make_problem(name, seed=20230419, n=None, sub=None, k=None, dims=None, nu=1.
     if constraints is not None:
         cons.update(constraints)
     mesh = hex_mesh(cfg["n"], dims=cfg["dims"], jitter=cfg["jitter"], seed=seed, triangulate=cfg["tri"])
+    if neumann:
+        mesh = mark_neumann(mesh, neumann)
     cell_sub, grid = box_partition(mesh, cfg["sub"])
     params = {}
     if cfg["kind"] == "sinker":

@@ -153,6 +153,22 @@ def hex_mesh(n, dims=None, jitter=0.0, seed=0, triangulate=False):
                     cell_ijk, (nx, ny, nz), h)
 
 
+def mark_neumann(mesh, sides=("x1", "y1"), tol=1e-9):
+    """Input recipe of the paper's numerical setting ("Neumann boundary conditions on two
+    faces of the cube and homogeneous Dirichlet on the other ones"): boundary faces lying on the
+    named sides of [0,1]^3 ("x0", "x1", "y0", ...) get face_on_boundary = 2 (Neumann), the other
+    boundary faces keep 1 (Dirichlet).  Returns a new mesh; nothing else changes."""
+    import dataclasses
+    fb = np.array(mesh.face_on_boundary, dtype=np.uint8).copy()
+    for f in np.nonzero(fb)[0]:
+        X = mesh.xyz[mesh.face(f)]
+        for sd in sides:
+            a, v = "xyz".index(sd[0]), float(sd[1])
+            if np.all(np.abs(X[:, a] - v) < tol):
+                fb[f] = 2
+    return dataclasses.replace(mesh, face_on_boundary=fb)
+
+
 def box_partition(mesh, sub):
     """Subdomain id per cell for a box partition with `sub`=(sx,sy,sz) cells per subdomain.
 
