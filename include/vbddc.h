@@ -36,7 +36,10 @@ typedef enum {
 /* General polyhedral mesh.  Host arrays, copied by vb_setup (borrowed only for the
  * duration of the call).  Face loops must be planar; cell_face_sign[j] = +1 iff the right-hand
  * normal of the loop of cell_face[j] points out of the cell.  face_on_dirichlet = 1 marks
- * boundary faces (homogeneous Dirichlet after lifting, Eq.(ContinuousProblem)). */
+ * boundary faces (homogeneous Dirichlet after lifting, Eq.(ContinuousProblem)); = 2 marks
+ * a Neumann face (homogeneous traction, the paper's two Neumann faces of P:1197, DESIGN A35): its
+ * velocity DOFs stay free, belong to the subdomain interface, and the pressure has no gauge (no
+ * zero-mean projection, no flux-compatibility check of the rhs).  Other values: VB_EINVAL. */
 typedef struct {
   int32_t k;                       /* VEM degree: 2 or 3                         */
   int64_t n_vertices; const double *xyz;              /* [n_vertices][3]                      */

@@ -1497,7 +1497,8 @@ static void stage_dual(vb_ctx *c, DBuf<double> &sidebuf, DBuf<double> &sumbuf) {
     for (int64_t K = 0; K < c->nK; ++K) nubar += c->nu[K];
     nubar /= c->nK;
     for (int g = 0; g < Ng; ++g) volO += c->gsub_vol[g];
-    const double gam_c = 1.0 / (nubar * volO);
+    // augmentation of the p_0 block for the gauge sum vol_i p0_i = 0; none with Neumann faces (A35)
+    const double gam_c = c->neumann ? 0.0 : 1.0 / (nubar * volO);
     if (c->cdis) {
       coarse_dissection(c, mine, lpoff, gnpi, pimoff, pimap, gam_c, blocks);
     } else {

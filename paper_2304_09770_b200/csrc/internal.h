@@ -251,7 +251,9 @@ struct vb_ctx {
   std::vector<double> xyz;
   std::vector<int64_t> face_ptr, face_vtx, cell_ptr, cell_face;
   std::vector<int8_t> cell_sign;
-  std::vector<uint8_t> face_bnd;
+  std::vector<uint8_t> face_bnd;                   // 0 interior, 1 Dirichlet, 2 Neumann
+  std::vector<char> vel_on_neu;                    // per velocity DOF: on a Neumann face's closure
+  bool neumann = false;                            // any Neumann face: no pressure gauge (DESIGN A35)
   std::vector<int64_t> edges;        // [nE][2] (a<b), lexicographic
   std::vector<double> nu;
   // ---------------- DOF numbering

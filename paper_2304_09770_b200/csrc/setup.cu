@@ -130,10 +130,27 @@ void build_topology(vb_ctx *c, const vb_mesh *m) {
   c->oC = c->oF + 3 * (int64_t)c->nm * c->nF;
   c->nvel = c->oC + c->nK * (c->n4 + c->n5);
   c->npres = c->nK * c->np;
-  // boundary DOFs
+  // boundary DOFs: face_bnd 1 = Dirichlet (removed, lifted); 2 = Neumann (natural
+  // condition): the DOFs of its closure stay free unless they also lie on a Dirichlet face, and are
+  // marked so the subdomain interface includes them (DESIGN A35)
   std::vector<char> isb(c->nvel, 0);
+  c->vel_on_neu.assign(c->nvel, 0);
+  c->neumann = false;
   for (int64_t f = 0; f < c->nF; ++f) {
-    if (!c->face_bnd[f]) continue;
+    if (c->face_bnd[f] != 2) continue;
+    c->neumann = true;
+    int64_t s = c->face_ptr[f], e = c->face_ptr[f + 1];
+    for (int64_t i = s; i < e; ++i) {
+      int64_t a = c->face_vtx[i], b = c->face_vtx[i + 1 < e ? i + 1 : s];
+      for (int q = 0; q < 3; ++q) c->vel_on_neu[3 * a + q] = 1;
+      int64_t ed = edge_id(a, b);
+      for (int q = 0; q < 3 * (k - 1); ++q) c->vel_on_neu[c->oE + 3 * (k - 1) * ed + q] = 1;
+    }
+    for (int q = 0; q < 3 * c->nm; ++q) c->vel_on_neu[c->oF + 3 * c->nm * f + q] = 1;
+  }
+  for (int64_t f = 0; f < c->nF; ++f) {
+    VB_REQUIRE(c->face_bnd[f] <= 2, VB_EINVAL, "face " + std::to_string(f) + ": face_on_dirichlet must be 0, 1 or 2");
+    if (c->face_bnd[f] != 1) continue;
     int64_t s = c->face_ptr[f], e = c->face_ptr[f + 1];
     for (int64_t i = s; i < e; ++i) {
       int64_t a = c->face_vtx[i], b = c->face_vtx[i + 1 < e ? i + 1 : s];
@@ -313,9 +330,11 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t 
     while (j < ds.size() && ds[j].first == ds[i].first) ++j;
     c->dof_owner_sub[ds[i].first] = ds[i].second;
     c->dof_nsh[ds[i].first] = j - i;
-    if (j - i > 1) {
+    const bool neu = c->neumann && c->vel_on_neu[c->free2vel[ds[i].first]];
+    if (j - i > 1 || neu) {
       sh.clear();
       for (size_t q = i; q < j; ++q) sh.push_back(ds[q].second);
+      if (neu) sh.push_back(-1);   // Neumann-boundary DOFs form classes of their own
       auto it = emap.find(sh);
       int e;
       if (it == emap.end()) { e = ekeys.size(); emap.emplace(sh, e); ekeys.push_back(sh); edofs.push_back({}); }
@@ -338,11 +357,19 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t 
   for (int q = 0; q < nge; ++q) {
     GEnt &G = c->gents[q];
     G.sharers = ekeys[order[q]];
+    const bool neu = G.sharers.back() < 0;
+    if (neu) G.sharers.pop_back();
     G.n = edofs[order[q]].size();
-    bool vert = true;
+    bool vert = true, has_face = false;
     int64_t v0 = c->free2vel[edofs[order[q]][0]] / 3;
-    for (auto d : edofs[order[q]]) { int64_t g = c->free2vel[d]; if (g >= c->oE || g / 3 != v0) vert = false; }
-    G.kind = vert ? 0 : (G.sharers.size() == 2 ? 2 : 1);
+    for (auto d : edofs[order[q]]) {
+      int64_t g = c->free2vel[d];
+      if (g >= c->oE || g / 3 != v0) vert = false;
+      has_face |= g >= c->oF && g < c->oC;
+    }
+    // on the Neumann boundary a class is a face iff it holds face moments (a subdomain's Neumann
+    // patch has one sharer), otherwise an edge (the lines where subdomains meet on it)
+    G.kind = vert ? 0 : (neu ? (has_face ? 2 : 1) : (G.sharers.size() == 2 ? 2 : 1));
     for (int s : G.sharers) c->gsub_ents[s].push_back(q);
     bool local = false;
     for (int s : G.sharers) local |= c->sub_lid[s] >= 0;
@@ -371,7 +398,8 @@ void build_subdomains(vb_ctx *c, const int32_t *cell_sub, int Ng, const int32_t 
       const int64_t K = c->cell_gid[l];
       for (int64_t j = c->cell_l2g_ptr[K]; j < c->cell_l2g_ptr[K + 1]; ++j) {
         int64_t f = c->vel2free[c->cell_l2g[j]];
-        if (f >= 0 && c->dof_nsh[f] == 1 && c->dof_owner_sub[f] == gi) fr.push_back(f);
+        if (f >= 0 && c->dof_nsh[f] == 1 && c->dof_owner_sub[f] == gi && !(c->neumann && c->vel_on_neu[c->cell_l2g[j]]))
+          fr.push_back(f);
       }
       for (int q = 0; q < c->np; ++q) S.P.push_back(K * c->np + q);
     }

@@ -1029,7 +1029,7 @@ __global__ void cd_root_finish_kernel(const double *__restrict__ vol, int Ng, in
   if (threadIdx.x == 0) {
     double A = 0, Wt = 0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { A += ra[q]; Wt += rw[q]; }
-    mean = A / Wt;
+    mean = Ng > 0 ? A / Wt : 0.0;   // Ng = 0: no gauge (Neumann faces)
   }
   __syncthreads();
   for (int64_t j = threadIdx.x; j < nroot; j += blockDim.x) uc[root[j]] = j >= nsep ? x[j] - mean : x[j];
@@ -1385,7 +1385,8 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
     pieces = st->cgath.p;
   }
   launch_pdl(st, gather_src_kernel, dim3(grid_for(c->Nc)), dim3(256), 0, s2, st->pptr.p, st->pidx.p, pieces, c->Nc, c->w_rc.p);
-  launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
+  if (!c->neumann)   // the gauge of the p_0 block (none with Neumann faces, DESIGN A35)
+    launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_rc.p + c->NPi_g, 0);
   tick(c, st, 2, true, s2);
   auto coarse_gemv = [&](const GemvWork *w, int nw, size_t sm, bool big) {
     if (big)
@@ -1418,7 +1419,8 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
     }
     launch_pdl(st, cd_root_rhs_kernel, dim3(grid_for(c->Nroot)), dim3(256), 0, s2, st->cd_rptr.p, st->cd_ridx.p, tg,
                c->w_rc.p, st->cd_root.p, c->Nroot, st->cd_groot.p);
-    launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, st->cd_groot.p + c->cd_nsep, 0);
+    if (!c->neumann)
+      launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, st->cd_groot.p + c->cd_nsep, 0);
   }
   // the packed inverse (all of it on one rank; this rank's tile rows otherwise)
   coarse_gemv(st->w_c.p, st->nw_c, st->sm_c, st->big_c);
@@ -1433,8 +1435,8 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
   }
   if (c->cdis) {
     // x_S (gauge-projected) to its global positions; pass 2: x_I = y_I - F x_S
-    launch_pdl(st, cd_root_finish_kernel, dim3(1), dim3(1024), 0, s2, st->gvol.p, c->Ng, c->cd_nsep, st->cd_xroot.p,
-               st->cd_root.p, c->Nroot, c->w_uc.p);
+    launch_pdl(st, cd_root_finish_kernel, dim3(1), dim3(1024), 0, s2, st->gvol.p, c->neumann ? 0 : c->Ng, c->cd_nsep,
+               st->cd_xroot.p, st->cd_root.p, c->Nroot, c->w_uc.p);
     if (c->cd_two && st->nw_cd22) {   // x_RS = y_RS - F2 x_S before the blocks' pass 2 reads it
       coarse_gemv(st->w_cd22.p, st->nw_cd22, st->sm_cd, st->big_cd);
       launch_pdl(st, cd_interior_kernel, dim3((unsigned)((c->cd2_part.nI + 255) / 256), 1), dim3(256), 0, s2,
@@ -1445,7 +1447,7 @@ static void apply_M(vb_ctx *c, SolveState *st, bool fill_tail = true) {
       launch_pdl(st, cd_interior_kernel, dim3((unsigned)((st->cd_maxI + 255) / 256), st->cd_no), dim3(256), 0, s2,
                  st->cd_parts.p, st->cd_part2.p, st->cd_Y.p, st->cd_Iall.p, c->w_uc.p);
     }
-  } else {
+  } else if (!c->neumann) {
     launch_pdl(st, coarse_p0_project_kernel, dim3(1), dim3(256), 0, s2, st->gvol.p, c->Ng, c->w_uc.p + c->NPi_g, 1);
   }
   launch_pdl(st, coarse_ext_kernel, dim3((st->max_nd + 127) / 128, c->N), dim3(128), c->max_npi * sizeof(double), s2,
@@ -2206,9 +2208,11 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   run_entity_sum(c, st->ESB, st->gbuf.p, c->w_gam.p, st->gam2.p);             // ghat = b + sum_m zG^(m)
   if (!c->h_ent.empty())
     gamma_rhs_kernel<<<c->h_ent.size(), 512, 0, s>>>(c->d_ent.p, c->d_T.p, c->w_gam.p, NDelta, c->w_r.p);
-  p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + W_P0, 0, c->Ng, st->g0abs.p);
-  allreduce_sum_fixed(c, c->w_dots.p + W_P0, 2);
-  p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + W_P0, 1, c->Ng, st->g0abs.p);
+  if (!c->neumann) {   // with Neumann faces the p_0 rows carry no compatibility condition (A35)
+    p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + W_P0, 0, c->Ng, st->g0abs.p);
+    allreduce_sum_fixed(c, c->w_dots.p + W_P0, 2);
+    p0_compat_kernel<<<1, 32, 0, s>>>(c->w_r.p + NDelta + c->NPi, N, c->w_dots.p + W_P0, 1, c->Ng, st->g0abs.p);
+  }
   VB_STAGE();
   // ---------------- PCG (SURVEY O-15), iterations driven on the device (scal[6] = it, scal[7] = status)
   c->w_x.zero(s);
@@ -2222,7 +2226,7 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   // flux compatibility of the rhs: sum_i g0_i = 0 up to rounding, else VB_EINVAL
   // scale: the terms g0 is summed from, plus ||r0|| (rounding-level pressure data, e.g. a lifted trace
   // with u.n = 0 on the boundary, makes both sides pure rounding)
-  VB_REQUIRE(fabs(compat[0]) <= kCompatRel * (compat[1] + h[4]), VB_EINVAL,
+  VB_REQUIRE(c->neumann || fabs(compat[0]) <= kCompatRel * (compat[1] + h[4]), VB_EINVAL,
              "flux-incompatible rhs: sum_i g0_i = " + std::to_string(compat[0]) + " (sum_i |g0_i| = " +
                  std::to_string(compat[1]) + "); the pressure rows must integrate to zero against constants");
   const double r0n = h[4];
@@ -2308,6 +2312,7 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
                                 c->w_x.p + NDelta + c->NPi, nvf, x);
   VB_STAGE();
   double *pm = c->w_dots.p + W_PM;
+  if (!c->neumann) {   // zero-mean pressure gauge; the pressure is unique with Neumann faces
   pressure_mean_kernel<<<PM_BLOCKS, 256, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np, c->nKl,
                                                  x + nvf, 0, pm, PM_BLOCKS);
   pressure_mean_kernel<<<1, 32, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np, c->nKl, x + nvf, 1,
@@ -2315,6 +2320,7 @@ void pcg_device(vb_ctx *c, const double *rhs_in, double *x_out, double rtol, int
   allreduce_sum_fixed(c, pm + 2 * PM_BLOCKS, 2);
   pressure_mean_kernel<<<grid_for(c->nKl), 256, 0, s>>>(c->d_cellgeo.p, c->d_cell_gid.p, c->geo_stride, c->np,
                                                         c->nKl, x + nvf, 2, pm, PM_BLOCKS);
+  }
   VB_STAGE();
   if (c->nranks > 1) dev_gather(x, c->d_owned_free.p, (int64_t)c->owned_free.size(), x_out, s);
   double true_rel = -1.0;

@@ -158,7 +158,7 @@ def mark_neumann(mesh, sides=("x1", "y1"), tol=1e-9):
     faces of the cube and homogeneous Dirichlet on the other ones"): boundary faces lying on the
     named sides of [0,1]^3 ("x0", "x1", "y0", ...) get face_on_boundary = 2 (Neumann), the other
     boundary faces keep 1 (Dirichlet).  Returns a new mesh; nothing else changes."""
-    import dataclasses
+    import copy
     fb = np.array(mesh.face_on_boundary, dtype=np.uint8).copy()
     for f in np.nonzero(fb)[0]:
         X = mesh.xyz[mesh.face(f)]
@@ -166,7 +166,9 @@ def mark_neumann(mesh, sides=("x1", "y1"), tol=1e-9):
             a, v = "xyz".index(sd[0]), float(sd[1])
             if np.all(np.abs(X[:, a] - v) < tol):
                 fb[f] = 2
-    return dataclasses.replace(mesh, face_on_boundary=fb)
+    out = copy.copy(mesh)          # keeps attributes set outside the dataclass fields (generators)
+    out.face_on_boundary = fb
+    return out
 
 
 def box_partition(mesh, sub):
