@@ -176,6 +176,8 @@ def main():
     ap.add_argument("--no-kernel-timing", action="store_true", help="skip the per-kernel CUDA events")
     ap.add_argument("--coarse-dissection", type=int, default=-1, choices=[-1, 0, 1],
                     help="coarse problem by dissection (1), dense replicated (0), auto (-1)")
+    ap.add_argument("--neumann", action="store_true",
+                    help="the paper's setting (P:1197): Neumann faces x = 1, y = 1 (DESIGN A35); not the default")
     ap.add_argument("--coarse-blocks", type=int, default=-1,
                     help="parts of the coarse dissection on one GPU (blocks of subdomains; -1 auto)")
     args = ap.parse_args()
@@ -204,7 +206,7 @@ def main():
     if ws > 1 and (args.config != "c5" or rank_grid is None):
         raise SystemExit("multi-GPU runs use config c5 on 1, 2, 4 or 8 GPUs")
     dims = C5_DIMS[ws] if args.config == "c5" else None
-    prob = make_problem(args.config, dims=dims)
+    prob = make_problem(args.config, dims=dims, neumann=("x1", "y1") if args.neumann else None)
     stream = torch.cuda.current_stream()
     dist_kw = {}
     if ws > 1:
@@ -346,7 +348,8 @@ def main():
         "data": "synthetic",
         "config": {"workload": "%s: %dx%dx%d hex cells, k=%d, %d subdomains%s"
                                % ((args.config,) + tuple(prob.mesh.dims) + (prob.k, int(prob.cell_subdomain.max()) + 1,
-                                  " of 4^3 cells (32^3 cells per GPU)" if args.config == "c5" else "")),
+                                  (" of 4^3 cells (32^3 cells per GPU)" if args.config == "c5" else "")
+                                  + (", Neumann faces x=1, y=1" if args.neumann else ""))),
                    "n_dofs": ndofs, "iterations": it, "kappa": rep["kappa"], "rel_residual": rep["rel_residual"],
                    "n_primal": st["n_primal"], "n_coarse": st["n_coarse"], "rtol": 1e-10,
                    "coarse": ("dissection: root %d, local %d" % (st["n_coarse_root"], st["n_coarse_local"])

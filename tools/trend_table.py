@@ -3,9 +3,11 @@ BASELINE-style CUBE meshes (homogeneous Dirichlet, box partitions): PCG iteratio
 kappa of the GPU solver for the minimal coarse space (vertex + face flux, nu_tol = inf in the
 paper's terms), the BASELINE space (vertex + edge + face averages + flux) and the adaptive space
 (tau = 2, the paper's nu_tol = 2), as H/h grows at a fixed subdomain count, and as k grows.
-Context only: the paper's meshes, partitions and Neumann faces differ.
+Context only: the paper's meshes and partitions differ.  With --neumann the faces
+x = 1 and y = 1 carry the natural condition, as in the paper's runs (DESIGN A35).
 
   python tools/trend_table.py > profiles/r01_trends.txt
+  python tools/trend_table.py --neumann > profiles/r02y_trends_neumann.txt
 """
 import os
 import sys
@@ -28,6 +30,10 @@ def run(prob, cons):
 
 def main():
     from synthetic import make_problem
+    neu = ("x1", "y1") if "--neumann" in sys.argv else None
+    ks = (2, 3, 4) if neu else (2, 3)
+    if neu:
+        print("Neumann faces x = 1, y = 1 (homogeneous traction), Dirichlet elsewhere")
     spaces = {
         "minimal (vertex+flux)": dict(vertex=1, edge_avg=0, face_avg=0, face_flux=1, adaptive_tau=0.0),
         "BASELINE (vertex+edge+face)": dict(vertex=1, edge_avg=1, face_avg=1, face_flux=1, adaptive_tau=0.0),
@@ -37,15 +43,19 @@ def main():
     print("%-30s %6s %10s %8s %10s %8s" % ("space", "H/h", "nDofs", "N_Pi", "iterations", "kappa"))
     for name, cons in spaces.items():
         for hh in (2, 3, 4, 6):
-            prob = make_problem("c2", n=4 * hh, sub=(hh, hh, hh))
+            prob = make_problem("c2", n=4 * hh, sub=(hh, hh, hh), neumann=neu)
             rep = run(prob, cons)
             print("%-30s %6d %10d %8d %10d %8.2f" % (name, hh, rep["n_dofs_paper"], rep["n_primal"],
                                                      rep["iterations"], rep["kappa"]), flush=True)
     print("\nk sweep: CUBE 8^3, 2^3 subdomains, nu = 1, rtol 1e-8")
     for name, cons in spaces.items():
-        for k in (2, 3):
-            prob = make_problem("c1", n=8, sub=(4, 4, 4), k=k)
-            rep = run(prob, cons)
+        for k in ks:
+            prob = make_problem("c1", n=8, sub=(4, 4, 4), k=k, neumann=neu)
+            try:
+                rep = run(prob, cons)
+            except Exception as e:   # e.g. adaptive k = 4 faces beyond the Jacobi GEVP kernel (EINVAL)
+                print("%-30s k=%d  not run: %s" % (name, k, e), flush=True)
+                continue
             print("%-30s k=%d %10d %8d %10d %8.2f" % (name, k, rep["n_dofs_paper"], rep["n_primal"],
                                                       rep["iterations"], rep["kappa"]), flush=True)
 
