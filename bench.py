@@ -333,13 +333,14 @@ def main():
     loc_ms, loc_bytes = kt[names[1]], 8.0 * st["sum_pk_D"]
     c_ms, c_bytes = kt[names[2]], 8.0 * st["pk_coarse"]
     achieved = op_bytes / (op_ms / 1e3) / 1e9
-    traffic, traffic_src = _ncu_traffic()
+    # the committed ncu capture is of the c5 one-GPU workload: no traffic figure for other configs
+    traffic, traffic_src = _ncu_traffic() if (args.config == "c5" and ws == 1 and not args.neumann) else (None, None)
     npr = {2: 4, 3: 10, 4: 20}[prob.k]
     k7_bytes = 8.0 * st["n_cells"] * (st["nv_max"] * (st["nv_max"] + 1) / 2 + npr * st["nv_max"])
     k7_entry = {"ms": k7_ms, "bytes_per_launch": k7_bytes,
                 "GBps": k7_bytes / (k7_ms / 1e3) / 1e9 if k7_ms else None,
                 "frac": k7_bytes / (k7_ms / 1e3) / 1e9 / peak if k7_ms else None,
-                "bytes_note": "hexahedral cells (c5): every cell has nv = nv_max"}
+                "bytes_note": "every cell counted with nv = nv_max (exact for hexahedral cells)"}
     iter_ms = ms / max(it, 1)
     per_iter_bytes = st["bytes_per_iter"]
     line = {

@@ -207,6 +207,7 @@ void layout_phase_a(vb_ctx *c, cudaStream_t s_upload) {
     c->d_el_ptr.upload(ptr, s);
     c->d_el_ent.upload(idx, s);
     c->w_elt.alloc((size_t)c->nKl * stride);
+    c->w_elx.alloc((size_t)c->nKl * ((stride + 1) & ~1));   // K7 per-cell inputs, 16-byte aligned cells
   }
   // greedy colouring of the GLOBAL subdomain adjacency (shared entities) for the coarse assembly
   {

@@ -341,7 +341,7 @@ struct vb_ctx {
   vb::DBuf<int> d_info;
   // solve workspaces
   vb::DBuf<double> w_x, w_r, w_z, w_p, w_q, w_part, w_locD, w_locY, w_locC, w_uc, w_rc, w_ucp,
-      w_scal, w_gam, w_bD, w_zG, w_dots, w_elt, w_yDp, w_xD;
+      w_scal, w_gam, w_bD, w_zG, w_dots, w_elt, w_elx, w_yDp, w_xD;   // w_elx: K7 per-cell inputs
   int P_kd = 4;
   vb::DBuf<int> d_op_work, d_loc_work, d_c_work;   // packed-GEMV chunk work lists
   int n_op_work = 0, n_loc_work = 0, n_c_work = 0, P_op = 4, P_loc = 4, P_c = 148;

@@ -886,13 +886,16 @@ __global__ void __launch_bounds__(K7_WARPS * 32) elem_apply_packed_kernel(
 // K7 with the element matrices staged by the bulk-copy engine: one cp.async.bulk of the cell's packed
 // lower triangle (~26 KB for k = 2 hexahedra) and one of B^K into shared memory per CTA, signalled
 // on an mbarrier, while the threads gather the cell's inputs; rows then come from shared memory
-// (the streaming kernel above waits on one global-memory row segment at a time), one thread per
-// row summing its row and its column of the lower triangle (no warp reductions).  Needs
+// (the streaming kernel above waits on one global-memory row segment at a time), a lane pair per
+// row summing its row and its column of the lower triangle over interleaved columns (round 1-2:
+// one thread per row, a serial 85-term FMA chain, 0.52 of HBM on c5).  Needs
 // (nv_max (nv_max+1)/2 + np nv_max) doubles of shared memory: used while that fits (k = 2
 // hexahedra and small polyhedra).
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-__global__ void __launch_bounds__(128) elem_apply_bulk_kernel(
+// K7B_TPR threads per row (default 2, CTA of 256; VB_K7_TPR / VB_K7_THREADS experiment knobs)
+template <int K7B_TPR>
+__global__ void __launch_bounds__(512) elem_apply_bulk_kernel(
     const double *__restrict__ elAp, int64_t slotA, const double *__restrict__ elB,
     const int64_t *__restrict__ l2g, const int64_t *__restrict__ vel2free, const int *__restrict__ cell_nv,
     const int64_t *__restrict__ gid, int nvmax, int np, int64_t nK, int64_t nvf, const double *__restrict__ x,
@@ -936,20 +939,199 @@ __global__ void __launch_bounds__(128) elem_apply_bulk_kernel(
           smem_u32(&bar))
       : "memory");
   __syncthreads();
-  // one thread per row, no reductions: y_i = sum_{j <= i} L_ij x_j + sum_{k > i} L_ki x_k + (B^T p)_i
-  for (int i = threadIdx.x; i < nv + np; i += blockDim.x) {
-    double v = 0.0;
+  // K7B_TPR threads per row (lane pairs, interleaved columns, two accumulators each -> four
+  // independent FMA chains per row), partials combined in a fixed order by shuffles:
+  // y_i = sum_{j <= i} L_ij x_j + sum_{k > i} L_ki x_k + (B^T p)_i
+  const int sub = threadIdx.x % K7B_TPR, rpp = blockDim.x / K7B_TPR, nrows = nv + np;
+  for (int base = 0; base < nrows; base += rpp) {       // uniform trip count (full-mask shuffles)
+    const int i = base + threadIdx.x / K7B_TPR;
+    double v0 = 0.0, v1 = 0.0;
     if (i < nv) {
       const double *row = As + (int64_t)i * (i + 1) / 2;
-      for (int j = 0; j <= i; ++j) v += row[j] * xs[j];
-      for (int k = i + 1; k < nv; ++k) v += As[(int64_t)k * (k + 1) / 2 + i] * xs[k];
-      for (int q = 0; q < np; ++q) v += Bs[q * nv + i] * xs[nv + q];
-      yel[K * stride + i] = v;
-    } else {
-      const int q = i - nv;
-      for (int j = 0; j < nv; ++j) v += Bs[q * nv + j] * xs[j];
-      yel[K * stride + nvmax + q] = v;
+      int j = sub;
+      for (; j + K7B_TPR <= i; j += 2 * K7B_TPR) {
+        v0 += row[j] * xs[j];
+        v1 += row[j + K7B_TPR] * xs[j + K7B_TPR];
+      }
+      if (j <= i) v0 += row[j] * xs[j];
+      int k = i + 1 + sub;
+      const double *col = As + (int64_t)k * (k + 1) / 2 + i;   // L_ki, k > i: next at + (k + 1), + (k + 2), ...
+      for (; k + K7B_TPR < nv; k += 2 * K7B_TPR) {
+        const double *col1 = col + (int64_t)K7B_TPR * k + K7B_TPR * (K7B_TPR + 1) / 2;
+        v0 += col[0] * xs[k];
+        v1 += col1[0] * xs[k + K7B_TPR];
+        col = col1 + (int64_t)K7B_TPR * (k + K7B_TPR) + K7B_TPR * (K7B_TPR + 1) / 2;
+      }
+      if (k < nv) v0 += col[0] * xs[k];
+      for (int q = sub; q < np; q += K7B_TPR) v1 += Bs[q * nv + i] * xs[nv + q];
+    } else if (i < nrows) {
+      const double *brow = Bs + (i - nv) * nv;
+      int j = sub;
+      for (; j + K7B_TPR < nv; j += 2 * K7B_TPR) {
+        v0 += brow[j] * xs[j];
+        v1 += brow[j + K7B_TPR] * xs[j + K7B_TPR];
+      }
+      if (j < nv) v0 += brow[j] * xs[j];
     }
+    double v = v0 + v1;
+#pragma unroll
+    for (int o = K7B_TPR / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (sub == 0 && i < nrows) yel[K * stride + (i < nv ? i : nvmax + (i - nv))] = v;
+  }
+}
+
+// K7, persistent and warp specialised (round 2, the default while two stages fit in shared
+// memory): the one-cell-per-CTA kernel above moves 3.1 TB/s on c5 whatever its compute shape
+// (profiles/r02z_k7_sweep.txt) -- every CTA pays launch, the l2g -> vel2free -> x gather chain, one
+// bulk-copy round trip and its compute back to back.  Here each CTA walks cells
+// blockIdx.x, + gridDim.x, ... through a ring of nst stages [A^K packed | B^K | inputs]: the
+// cells' inputs are gathered beforehand by elem_xgather_kernel into contiguous per-cell vectors (a
+// producer that walked the gather chain itself, one cell at a time, capped the first version at
+// 5 us per cell and CTA); one producer lane waits for a free stage and issues three cp.async.bulk
+// copies (complete_tx on the stage's full barrier); K7P_CONSUMERS threads wait on the full
+// barrier, compute the rows as above (lane pairs) and release the stage through its empty barrier.
+constexpr int K7P_MAXST = 8;   // consumers = blockDim.x - 32 (the last warp produces)
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+// one lane's share (columns sub, sub + TPR, ...) of row i of [A^K B^K^T; B^K 0] x from the staged cell:
+// four accumulators, loads of four terms issued ahead of their FMAs (shared-memory latency, not
+// FP64 throughput, bounds this loop: 8 consumer warps took 2 us per cell with a single chain)
+template <int TPR>
+__device__ __forceinline__ double k7_row_share(const double *As, const double *Bs, const double *xs, int i, int nv,
+                                               int np, int sub) {
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+  if (i < nv) {
+    const double *row = As + ((i * (i + 1)) >> 1);
+    int j = sub;
+    for (; j + 3 * TPR <= i; j += 4 * TPR) {
+      const double a0 = row[j], a1 = row[j + TPR], a2 = row[j + 2 * TPR], a3 = row[j + 3 * TPR];
+      const double x0 = xs[j], x1 = xs[j + TPR], x2 = xs[j + 2 * TPR], x3 = xs[j + 3 * TPR];
+      v0 += a0 * x0, v1 += a1 * x1, v2 += a2 * x2, v3 += a3 * x3;
+    }
+    for (; j <= i; j += TPR) v0 += row[j] * xs[j];
+    int k = i + 1 + sub;
+    const double *col = As + i;
+    for (; k + 3 * TPR < nv; k += 4 * TPR) {
+      const int k1 = k + TPR, k2 = k + 2 * TPR, k3 = k + 3 * TPR;
+      const double a0 = col[(k * (k + 1)) >> 1], a1 = col[(k1 * (k1 + 1)) >> 1], a2 = col[(k2 * (k2 + 1)) >> 1],
+                   a3 = col[(k3 * (k3 + 1)) >> 1];
+      const double x0 = xs[k], x1 = xs[k1], x2 = xs[k2], x3 = xs[k3];
+      v0 += a0 * x0, v1 += a1 * x1, v2 += a2 * x2, v3 += a3 * x3;
+    }
+    for (; k < nv; k += TPR) v1 += col[(k * (k + 1)) >> 1] * xs[k];
+    for (int a = sub; a < np; a += TPR) v2 += Bs[a * nv + i] * xs[nv + a];
+  } else if (i < nv + np) {
+    const double *brow = Bs + (i - nv) * nv;
+    int j = sub;
+    for (; j + 3 * TPR < nv; j += 4 * TPR) {
+      const double a0 = brow[j], a1 = brow[j + TPR], a2 = brow[j + 2 * TPR], a3 = brow[j + 3 * TPR];
+      const double x0 = xs[j], x1 = xs[j + TPR], x2 = xs[j + 2 * TPR], x3 = xs[j + 3 * TPR];
+      v0 += a0 * x0, v1 += a1 * x1, v2 += a2 * x2, v3 += a3 * x3;
+    }
+    for (; j < nv; j += TPR) v0 += brow[j] * xs[j];
+  }
+  return (v0 + v1) + (v2 + v3);
+}
+
+__global__ void elem_xgather_kernel(const int64_t *__restrict__ l2g, const int64_t *__restrict__ vel2free,
+                                    const int *__restrict__ cell_nv, const int64_t *__restrict__ gid, int nvmax,
+                                    int np, int64_t nK, int64_t nvf, int xstride, const double *__restrict__ x,
+                                    double *__restrict__ xel) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nK * xstride;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t K = e / xstride;
+    const int j = (int)(e - K * xstride), nv = cell_nv[K];
+    double v = 0.0;
+    if (j < nv) {
+      const int64_t f = vel2free[l2g[K * nvmax + j]];
+      if (f >= 0) v = x[f];
+    } else if (j < nv + np) {
+      v = x[nvf + gid[K] * np + (j - nv)];
+    }
+    xel[e] = v;
+  }
+}
+
+template <int K7P_TPR>
+__global__ void __launch_bounds__(544) elem_apply_pipe_kernel(
+    const double *__restrict__ elAp, int64_t slotA, const double *__restrict__ elB,
+    const double *__restrict__ xel, const int *__restrict__ cell_nv, int nvmax, int np, int64_t nK, double *yel,
+    int nst, int stage_dbl, int nocompute) {
+  extern __shared__ __align__(16) double k7b[];
+  __shared__ __align__(8) uint64_t full[K7P_MAXST], empty[K7P_MAXST];
+  const int offB = (int)((slotA + 1) & ~1LL), offX = offB + ((np * nvmax + 1) & ~1);
+  const int stride = nvmax + np, K7P_CONSUMERS = blockDim.x - 32;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < nst; ++q) {
+      mbar_init(&full[q], 1);                     // the producer lane's expect_tx arrival
+      mbar_init(&empty[q], K7P_CONSUMERS / 32);   // one arrival per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t first = blockIdx.x;
+  const int64_t cnt = first < nK ? (nK - first + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x >= K7P_CONSUMERS) {   // producer warp: one lane issues the bulk copies
+    if (threadIdx.x != K7P_CONSUMERS || cnt == 0) return;
+    const int xstride = (stride + 1) & ~1;
+    int nv_next = cell_nv[first];
+    for (int64_t n = 0; n < cnt; ++n) {
+      const int q = (int)(n % nst);
+      const unsigned round = (unsigned)(n / nst);
+      const int64_t K = first + n * gridDim.x;
+      double *As = k7b + (int64_t)q * stage_dbl, *Bs = As + offB, *xs = As + offX;
+      const int nv = nv_next;
+      if (n + 1 < cnt) nv_next = cell_nv[K + gridDim.x];   // in flight during the wait below
+      mbar_wait(&empty[q], (round & 1u) ^ 1u);             // passes at once in the first round
+      const int64_t lenA = (int64_t)nv * (nv + 1) / 2;
+      const unsigned bA = 8u * (unsigned)((lenA + 1) & ~1LL), bB = 8u * (unsigned)(np * nv), bX = 8u * xstride;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[q])),
+                   "r"(bA + bB + bX)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(As)),
+                   "l"(elAp + K * slotA), "r"(bA), "r"(smem_u32(&full[q]))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(Bs)),
+                   "l"(elB + K * np * nvmax), "r"(bB), "r"(smem_u32(&full[q]))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(xs)),
+                   "l"(xel + K * xstride), "r"(bX), "r"(smem_u32(&full[q]))
+                   : "memory");
+    }
+    return;
+  }
+  const int sub = threadIdx.x % K7P_TPR, rpp = K7P_CONSUMERS / K7P_TPR;
+  for (int64_t n = 0; n < cnt; ++n) {
+    const int q = (int)(n % nst);
+    const unsigned round = (unsigned)(n / nst);
+    const int64_t K = first + n * gridDim.x;
+    const double *As = k7b + (int64_t)q * stage_dbl, *Bs = As + offB, *xs = As + offX;
+    const int nv = cell_nv[K], nrows = nv + np;
+    mbar_wait(&full[q], round & 1u);
+    for (int base = 0; base < nrows; base += rpp) {
+      const int i = base + threadIdx.x / K7P_TPR;
+      double v = nocompute ? xs[0] : k7_row_share<K7P_TPR>(As, Bs, xs, i, nv, np, sub);   // nocompute: load-only probe
+#pragma unroll
+      for (int o = K7P_TPR / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (sub == 0 && i < nrows) yel[K * stride + (i < nv ? i : nvmax + (i - nv))] = v;
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[q]);
   }
 }
 
@@ -2018,9 +2200,36 @@ void apply_operator_device(vb_ctx *c, const double *x, double *y) {
   const size_t smem_bulk = (size_t)(((slot + 1) & ~1LL) + (int64_t)c->np * c->nv_max + stride) * sizeof(double);
   SolveState *st = get_state(c);
   tick(c, st, 5, true);
-  if (smem_bulk <= kK7BulkSmem && !(getenv("VB_K7_STREAM") && atoi(getenv("VB_K7_STREAM")))) {
-    raise_smem_limit((const void *)elem_apply_bulk_kernel, smem_bulk);
-    elem_apply_bulk_kernel<<<c->nKl, 128, smem_bulk, s>>>(
+  // pipelined persistent kernel: nst stages per CTA, ctas CTAs per SM (VB_K7_STAGES / VB_K7_CTAS /
+  // VB_K7_PIPE=0 experiment knobs; default 2 stages x 3 CTAs per SM, 6 consumer warps, when they
+  // fit, else fewer: profiles/r02z_k7_sweep.txt)
+  const int stage_dbl = (int)(((slot + 1) & ~1LL) + (((int64_t)c->np * c->nv_max + 1) & ~1LL) + ((stride + 1) & ~1));
+  const size_t stage_b = (size_t)stage_dbl * sizeof(double), smem_sm = 220 * 1024;
+  int ctas = getenv("VB_K7_CTAS") ? std::max(1, atoi(getenv("VB_K7_CTAS"))) : 3;
+  int nst = getenv("VB_K7_STAGES") ? std::max(1, atoi(getenv("VB_K7_STAGES"))) : 2;
+  while (ctas > 1 && (size_t)ctas * (2 * stage_b + 1024) > smem_sm) --ctas;
+  nst = (int)std::min<size_t>(std::min(nst, K7P_MAXST), (smem_sm / ctas - 1024) / stage_b);
+  const bool stream_only = getenv("VB_K7_STREAM") && atoi(getenv("VB_K7_STREAM"));
+  const bool pipe = !(getenv("VB_K7_PIPE") && !atoi(getenv("VB_K7_PIPE")));
+  if (!stream_only && pipe && nst >= 2) {
+    const int tpr = getenv("VB_K7_TPR") ? atoi(getenv("VB_K7_TPR")) : 2;
+    const int cons = getenv("VB_K7_CONS") ? std::min(512, std::max(32, atoi(getenv("VB_K7_CONS")) / 32 * 32)) : 192;
+    auto pk = tpr == 4 ? elem_apply_pipe_kernel<4> : tpr == 8 ? elem_apply_pipe_kernel<8> : elem_apply_pipe_kernel<2>;
+    raise_smem_limit((const void *)pk, nst * stage_b);
+    const int64_t grid = std::min<int64_t>(c->nKl, (int64_t)148 * ctas);   // B200: 148 SMs
+    const int xstride = (stride + 1) & ~1;
+    elem_xgather_kernel<<<grid_for(c->nKl * xstride), 256, 0, s>>>(c->d_cell_l2g.p, c->d_vel2free.p, c->d_cell_nv.p,
+                                                                   c->d_cell_gid.p, c->nv_max, c->np, c->nKl,
+                                                                   c->n_free_vel, xstride, xin, c->w_elx.p);
+    pk<<<(unsigned)grid, cons + 32, nst * stage_b, s>>>(
+        c->d_elAp.p, slot, c->d_elB.p, c->w_elx.p, c->d_cell_nv.p, c->nv_max, c->np, c->nKl, c->w_elt.p, nst,
+        stage_dbl, getenv("VB_K7_NOCOMPUTE") && atoi(getenv("VB_K7_NOCOMPUTE")));
+  } else if (smem_bulk <= kK7BulkSmem && !stream_only) {
+    const int tpr = getenv("VB_K7_TPR") ? atoi(getenv("VB_K7_TPR")) : 2;
+    const int thr = getenv("VB_K7_THREADS") ? std::min(512, std::max(32, atoi(getenv("VB_K7_THREADS")) / 32 * 32)) : 256;
+    auto kern = tpr == 1 ? elem_apply_bulk_kernel<1> : tpr == 4 ? elem_apply_bulk_kernel<4> : elem_apply_bulk_kernel<2>;
+    raise_smem_limit((const void *)kern, smem_bulk);
+    kern<<<c->nKl, thr, smem_bulk, s>>>(
         c->d_elAp.p, slot, c->d_elB.p, c->d_cell_l2g.p, c->d_vel2free.p, c->d_cell_nv.p, c->d_cell_gid.p, c->nv_max,
         c->np, c->nKl, c->n_free_vel, xin, c->w_elt.p);
   } else {

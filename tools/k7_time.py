@@ -18,13 +18,28 @@ def main():
     y = torch.empty_like(x)
     os.environ["VB_KERNEL_TIMING"] = "1"
     ctx.apply_operator(x, y)
-    ts = []
-    for _ in range(10):
-        ctx.apply_operator(x, y)
-        ts.append(ctx.kernel_times()["elem_apply K7 (packed element matrices)"])
-    ms = float(np.median(ts))
     b = 8.0 * st["n_cells"] * (st["nv_max"] * (st["nv_max"] + 1) / 2 + 4 * st["nv_max"])
-    print("K7 elem_apply: %.4f ms, %.3f GB algorithmic, %.0f GB/s" % (ms, b / 1e9, b / ms / 1e6))
+    # --sweep: the pipelined kernel's stages / CTAs per SM (default 3 x 2) and the one-cell-per-CTA
+    # bulk kernel (VB_K7_PIPE=0) with its threads-per-row / CTA-size knobs
+    combos = [{}]
+    if "--sweep" in sys.argv:
+        combos += [{"VB_K7_TPR": str(t), "VB_K7_CONS": str(n), "VB_K7_STAGES": str(a), "VB_K7_CTAS": str(b)}
+                   for t, n, a, b in ((2, 256, 2, 3), (2, 256, 3, 2), (2, 192, 2, 3), (4, 384, 2, 3), (4, 512, 2, 3),
+                                      (4, 384, 3, 2), (4, 512, 3, 2), (8, 512, 3, 2), (2, 256, 6, 1), (4, 512, 7, 1))]
+        combos += [{"VB_K7_CONS": "128"}, {"VB_K7_NOCOMPUTE": "1"}, {"VB_K7_NOCOMPUTE": "1", "VB_K7_STAGES": "6", "VB_K7_CTAS": "1"},
+                   {"VB_K7_NOCOMPUTE": "1", "VB_K7_STAGES": "3", "VB_K7_CTAS": "2"}]
+        combos += [{"VB_K7_PIPE": "0"}, {"VB_K7_PIPE": "0", "VB_K7_TPR": "1", "VB_K7_THREADS": "128"}]
+    for env in combos:
+        for k in ("VB_K7_STAGES", "VB_K7_CTAS", "VB_K7_PIPE", "VB_K7_TPR", "VB_K7_THREADS", "VB_K7_CONS", "VB_K7_NOCOMPUTE"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        tpr, thr = " ".join("%s=%s" % (k[6:], v) for k, v in env.items()) or "default", ""
+        ts = []
+        for _ in range(10):
+            ctx.apply_operator(x, y)
+            ts.append(ctx.kernel_times()["elem_apply K7 (packed element matrices)"])
+        ms = float(np.median(ts))
+        print("K7 elem_apply (%s%s): %.4f ms, %.3f GB algorithmic, %.0f GB/s" % (tpr, thr, ms, b / 1e9, b / ms / 1e6))
 
 
 if __name__ == "__main__":
