@@ -1116,12 +1116,14 @@ __global__ void __launch_bounds__(544) elem_apply_pipe_kernel(
     return;
   }
   const int sub = threadIdx.x % K7P_TPR, rpp = K7P_CONSUMERS / K7P_TPR;
+  int nv_next = cnt > 0 ? cell_nv[first] : 0;
   for (int64_t n = 0; n < cnt; ++n) {
     const int q = (int)(n % nst);
     const unsigned round = (unsigned)(n / nst);
     const int64_t K = first + n * gridDim.x;
     const double *As = k7b + (int64_t)q * stage_dbl, *Bs = As + offB, *xs = As + offX;
-    const int nv = cell_nv[K], nrows = nv + np;
+    const int nv = nv_next, nrows = nv + np;
+    if (n + 1 < cnt) nv_next = cell_nv[K + gridDim.x];   // a global load per cell: one cell ahead, off the critical path
     mbar_wait(&full[q], round & 1u);
     for (int base = 0; base < nrows; base += rpp) {
       const int i = base + threadIdx.x / K7P_TPR;
@@ -1132,6 +1134,149 @@ __global__ void __launch_bounds__(544) elem_apply_pipe_kernel(
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[q]);
+  }
+}
+
+// K7, warp-per-row consumers (VB_K7_PIPE=2; cells with nv <= 32 MX): the lane-pair kernel above is
+// bound by shared-memory wavefronts (every L_ij is read twice, rows with 2-way bank conflicts, x from
+// shared memory: ~1,900 cycles per cell and SM whatever the thread shape).  Here warp w owns rows
+// w, w + W, ...: lanes read a row contiguously (conflict free), x_j lives in registers, each L_ij is
+// read once and used for y_i (row sum, shuffle reduction, four rows interleaved) and y_j (per-lane
+// column partials, summed over the warps in fixed order after one named barrier).
+template <int MX, int W>
+__global__ void __launch_bounds__(W * 32 + 32, 3) elem_apply_pipe2_kernel(
+    const double *__restrict__ elAp, int64_t slotA, const double *__restrict__ elB,
+    const double *__restrict__ xel, const int *__restrict__ cell_nv, int nvmax, int np, int64_t nK, double *yel,
+    int nst, int stage_dbl) {
+  extern __shared__ __align__(16) double k7b[];
+  __shared__ __align__(8) uint64_t full[K7P_MAXST], empty[K7P_MAXST];
+  const int offB = (int)((slotA + 1) & ~1LL), offX = offB + ((np * nvmax + 1) & ~1);
+  constexpr int ncons = W * 32, RW = (32 * MX + W - 1) / W;   // rows per warp, all in registers
+  const int stride = nvmax + np;
+  double *red = k7b + (int64_t)nst * stage_dbl;   // 2 x [y rows (stride) | W column partial vectors (nvmax each)]
+  const int red_dbl = stride + W * nvmax;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < nst; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], W);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t first = blockIdx.x;
+  const int64_t cnt = first < nK ? (nK - first + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x >= ncons) {   // producer warp: one lane issues the bulk copies
+    if (threadIdx.x != ncons || cnt == 0) return;
+    const int xstride = (stride + 1) & ~1;
+    int nv_next = cell_nv[first];
+    for (int64_t n = 0; n < cnt; ++n) {
+      const int q = (int)(n % nst);
+      const unsigned round = (unsigned)(n / nst);
+      const int64_t K = first + n * gridDim.x;
+      double *As = k7b + (int64_t)q * stage_dbl, *Bs = As + offB, *xs = As + offX;
+      const int nv = nv_next;
+      if (n + 1 < cnt) nv_next = cell_nv[K + gridDim.x];
+      mbar_wait(&empty[q], (round & 1u) ^ 1u);
+      const int64_t lenA = (int64_t)nv * (nv + 1) / 2;
+      const unsigned bA = 8u * (unsigned)((lenA + 1) & ~1LL), bB = 8u * (unsigned)(np * nv), bX = 8u * xstride;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[q])),
+                   "r"(bA + bB + bX)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(As)),
+                   "l"(elAp + K * slotA), "r"(bA), "r"(smem_u32(&full[q]))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(Bs)),
+                   "l"(elB + K * np * nvmax), "r"(bB), "r"(smem_u32(&full[q]))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(xs)),
+                   "l"(xel + K * xstride), "r"(bX), "r"(smem_u32(&full[q]))
+                   : "memory");
+    }
+    return;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int nv_next = cnt > 0 ? cell_nv[first] : 0;
+  for (int64_t n = 0; n < cnt; ++n) {
+    const int q = (int)(n % nst);
+    const unsigned round = (unsigned)(n / nst);
+    const int64_t K = first + n * gridDim.x;
+    const double *As = k7b + (int64_t)q * stage_dbl, *Bs = As + offB, *xs = As + offX;
+    double *ysm = red + (n & 1) * red_dbl, *tw = ysm + stride;
+    const int nv = nv_next;
+    if (n + 1 < cnt) nv_next = cell_nv[K + gridDim.x];
+    mbar_wait(&full[q], round & 1u);
+    double xr[MX], yc[MX];
+#pragma unroll
+    for (int m = 0; m < MX; ++m) {
+      const int j = lane + 32 * m;
+      xr[m] = j < nv ? xs[j] : 0.0;
+      yc[m] = 0.0;
+    }
+    double p[RW];   // this warp's row sums (lane partials), reduced together: RW independent shuffle chains
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int i = w + r * W;
+      p[r] = 0.0;
+      if (i < nv) {
+        const double *row = As + ((i * (i + 1)) >> 1);
+        const double xi = xs[i];
+#pragma unroll
+        for (int m = 0; m < MX; ++m) {
+          const int j = lane + 32 * m;
+          if (32 * m <= i && j <= i) {
+            const double a = row[j];
+            p[r] += a * xr[m];
+            if (j < i) yc[m] += a * xi;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int r = 0; r < RW; ++r) p[r] += __shfl_xor_sync(0xffffffffu, p[r], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < RW; ++r)
+        if (w + r * W < nv) ysm[w + r * W] = p[r];
+    }
+    for (int a = w; a < np; a += W) {   // pressure rows: (B x_v)_a
+      double pb = 0.0;
+#pragma unroll
+      for (int m = 0; m < MX; ++m) {
+        const int j = lane + 32 * m;
+        if (j < nv) pb += Bs[a * nv + j] * xr[m];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) pb += __shfl_xor_sync(0xffffffffu, pb, o);
+      if (lane == 0) ysm[nv + a] = pb;
+    }
+#pragma unroll
+    for (int m = 0; m < MX; ++m) {
+      const int j = lane + 32 * m;
+      if (j < nv) tw[w * nvmax + j] = yc[m];
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(ncons) : "memory");
+    for (int t = threadIdx.x; t < nv + np; t += ncons) {
+      double v = ysm[t];
+      if (t < nv) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < W; ww += 2) c0 += tw[ww * nvmax + t], c1 += tw[(ww + 1) * nvmax + t];
+        double b0 = 0.0, b1 = 0.0;   // np is even (4, 10, 20)
+        for (int a = 0; a < np; a += 2) b0 += Bs[a * nv + t] * xs[nv + a], b1 += Bs[(a + 1) * nv + t] * xs[nv + a + 1];
+        v += (c0 + c1) + (b0 + b1);
+        yel[K * stride + t] = v;
+      } else {
+        yel[K * stride + nvmax + (t - nv)] = v;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[q]);
   }
 }
 
@@ -2211,7 +2356,27 @@ void apply_operator_device(vb_ctx *c, const double *x, double *y) {
   nst = (int)std::min<size_t>(std::min(nst, K7P_MAXST), (smem_sm / ctas - 1024) / stage_b);
   const bool stream_only = getenv("VB_K7_STREAM") && atoi(getenv("VB_K7_STREAM"));
   const bool pipe = !(getenv("VB_K7_PIPE") && !atoi(getenv("VB_K7_PIPE")));
-  if (!stream_only && pipe && nst >= 2) {
+  const int pipe_ver = getenv("VB_K7_PIPE") ? atoi(getenv("VB_K7_PIPE")) : 1;
+  if (!stream_only && pipe_ver == 2 && c->nv_max <= 128) {
+    const int mx = (c->nv_max + 31) / 32;
+    const int cons2 = (mx == 4 || (getenv("VB_K7_CONS") && atoi(getenv("VB_K7_CONS")) >= 256)) ? 256 : 192;
+    const size_t red_b = 2 * (size_t)(stride + (cons2 / 32) * c->nv_max) * sizeof(double);
+    int ctas2 = getenv("VB_K7_CTAS") ? std::max(1, atoi(getenv("VB_K7_CTAS"))) : 3;
+    while (ctas2 > 1 && (size_t)ctas2 * (2 * stage_b + red_b + 1024) > smem_sm) --ctas2;
+    int nst2 = getenv("VB_K7_STAGES") ? std::max(1, atoi(getenv("VB_K7_STAGES"))) : 2;
+    nst2 = (int)std::min<size_t>(std::min(nst2, K7P_MAXST), (smem_sm / ctas2 - 1024 - red_b) / stage_b);
+    VB_REQUIRE(nst2 >= 1, VB_EINVAL, "K7 pipe2: a stage does not fit in shared memory");
+    auto pk2 = mx == 4 ? elem_apply_pipe2_kernel<4, 8> : cons2 == 256 ? elem_apply_pipe2_kernel<3, 8> : elem_apply_pipe2_kernel<3, 6>;
+    raise_smem_limit((const void *)pk2, nst2 * stage_b + red_b);
+    const int64_t grid = std::min<int64_t>(c->nKl, (int64_t)148 * ctas2);
+    const int xstride = (stride + 1) & ~1;
+    elem_xgather_kernel<<<grid_for(c->nKl * xstride), 256, 0, s>>>(c->d_cell_l2g.p, c->d_vel2free.p, c->d_cell_nv.p,
+                                                                   c->d_cell_gid.p, c->nv_max, c->np, c->nKl,
+                                                                   c->n_free_vel, xstride, xin, c->w_elx.p);
+    pk2<<<(unsigned)grid, cons2 + 32, nst2 * stage_b + red_b, s>>>(c->d_elAp.p, slot, c->d_elB.p, c->w_elx.p,
+                                                                   c->d_cell_nv.p, c->nv_max, c->np, c->nKl,
+                                                                   c->w_elt.p, nst2, stage_dbl);
+  } else if (!stream_only && pipe && nst >= 2) {
     const int tpr = getenv("VB_K7_TPR") ? atoi(getenv("VB_K7_TPR")) : 2;
     const int cons = getenv("VB_K7_CONS") ? std::min(512, std::max(32, atoi(getenv("VB_K7_CONS")) / 32 * 32)) : 192;
     auto pk = tpr == 4 ? elem_apply_pipe_kernel<4> : tpr == 8 ? elem_apply_pipe_kernel<8> : elem_apply_pipe_kernel<2>;

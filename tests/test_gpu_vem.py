@@ -218,3 +218,37 @@ def test_k4_dof_count_table3():
     prob = make_problem("c1", n=8, k=4, sub=(4, 4, 4))
     ctx = vb.context_for(prob)
     assert ctx.stats()["n_dofs_paper"] == 76387
+
+
+@pytest.mark.parametrize("case", ["hex_k2", "hex_jitter_k2", "cvt_k2", "hex_k3"])
+def test_k7_kernel_variants_match_oracle(case, monkeypatch):
+    """Every K7 kernel (the persistent pipelined kernels with lane-pair and warp-per-row
+    consumers, ragged stage counts, the one-cell-per-CTA bulk kernel, the streaming kernel) against
+    the oracle's assembled saddle matrix; CVT cells have ragged nv (bulk sizes vary per cell), k = 3
+    hexahedra exceed the staged kernels' shared memory (fallback path)."""
+    import torch
+    import paper_2304_09770_b200 as vb
+    from oracle.assemble import GlobalSystem
+    from synthetic import make_cvt_problem
+    prob = {"hex_k2": lambda: make_problem("c1"), "hex_jitter_k2": lambda: make_problem("c3", n=4, sub=(2, 2, 2), k=2),
+            "cvt_k2": lambda: make_cvt_problem(4, grid=(2, 2, 1), k=2),
+            "hex_k3": lambda: make_problem("c1", n=4, k=3)}[case]()
+    gs = GlobalSystem(prob)
+    ctx = _ctx(prob)
+    x = np.random.default_rng(11).standard_normal(ctx.n_free)
+    yo = gs.saddle_matrix() @ x
+    xd = torch.tensor(x, device="cuda")
+    variants = [{}, {"VB_K7_PIPE": "1"}, {"VB_K7_PIPE": "2"}, {"VB_K7_PIPE": "0"}, {"VB_K7_STREAM": "1"},
+                {"VB_K7_PIPE": "1", "VB_K7_STAGES": "5", "VB_K7_CTAS": "1", "VB_K7_TPR": "4", "VB_K7_CONS": "128"},
+                {"VB_K7_PIPE": "2", "VB_K7_STAGES": "3", "VB_K7_CTAS": "2", "VB_K7_CONS": "64"},
+                {"VB_K7_PIPE": "2", "VB_K7_STAGES": "1", "VB_K7_CTAS": "1", "VB_K7_CONS": "256"}]
+    knobs = ("VB_K7_PIPE", "VB_K7_STREAM", "VB_K7_STAGES", "VB_K7_CTAS", "VB_K7_TPR", "VB_K7_CONS")
+    for env in variants:
+        for k in knobs:
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        y = torch.full_like(xd, float("nan"))
+        ctx.apply_operator(xd, y)
+        err = np.linalg.norm(y.cpu().numpy() - yo) / np.linalg.norm(yo)
+        assert err <= 1e-11, (env, err)

@@ -23,12 +23,11 @@ def main():
     # bulk kernel (VB_K7_PIPE=0) with its threads-per-row / CTA-size knobs
     combos = [{}]
     if "--sweep" in sys.argv:
-        combos += [{"VB_K7_TPR": str(t), "VB_K7_CONS": str(n), "VB_K7_STAGES": str(a), "VB_K7_CTAS": str(b)}
-                   for t, n, a, b in ((2, 256, 2, 3), (2, 256, 3, 2), (2, 192, 2, 3), (4, 384, 2, 3), (4, 512, 2, 3),
-                                      (4, 384, 3, 2), (4, 512, 3, 2), (8, 512, 3, 2), (2, 256, 6, 1), (4, 512, 7, 1))]
-        combos += [{"VB_K7_CONS": "128"}, {"VB_K7_NOCOMPUTE": "1"}, {"VB_K7_NOCOMPUTE": "1", "VB_K7_STAGES": "6", "VB_K7_CTAS": "1"},
-                   {"VB_K7_NOCOMPUTE": "1", "VB_K7_STAGES": "3", "VB_K7_CTAS": "2"}]
-        combos += [{"VB_K7_PIPE": "0"}, {"VB_K7_PIPE": "0", "VB_K7_TPR": "1", "VB_K7_THREADS": "128"}]
+        combos += [{"VB_K7_PIPE": "2", "VB_K7_CONS": str(n), "VB_K7_STAGES": str(a), "VB_K7_CTAS": str(b)}
+                   for n, a, b in ((192, 2, 3), (256, 2, 3), (192, 3, 2), (256, 3, 2), (256, 6, 1), (192, 6, 1))]
+        combos += [{"VB_K7_PIPE": "1"}, {"VB_K7_PIPE": "1", "VB_K7_NOCOMPUTE": "1"},
+                   {"VB_K7_PIPE": "1", "VB_K7_NOCOMPUTE": "1", "VB_K7_STAGES": "6", "VB_K7_CTAS": "1"},
+                   {"VB_K7_PIPE": "0"}]
     for env in combos:
         for k in ("VB_K7_STAGES", "VB_K7_CTAS", "VB_K7_PIPE", "VB_K7_TPR", "VB_K7_THREADS", "VB_K7_CONS", "VB_K7_NOCOMPUTE"):
             os.environ.pop(k, None)
